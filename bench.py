@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py — KV-migrate throughput of the B200-native chunked KV-cache push.
+
+One "step" = one dyna_kv_migrate of one split request's first-segment KV
+(§3.1, §4.3) on BASELINE.json configs[1]: Llama-2-7B
+shape (32 layers, 32 KV heads, d128, fp16, block 16), a 2048-token prompt
+split mid-prefill at s = 1024, chunk 256.  At N = 1 the destination pool is a
+second pool on the same B200 (intra-device reblocking, HBM roofline); at N > 1
+each rank r pushes into rank (r+1) % N's pool, mapped over CUDA IPC, with
+in-kernel NVLink stores (NVLink roofline).  Per-GPU work is fixed: weak
+scaling.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dyna|reference]
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the
+test-infrastructure program in oracle/) on a bounded sample of the same
+workload — the only other place this file runs oracle/ code besides the
+cpu_baseline leg.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KV-migrate GB/s & tokens/s per pair and aggregate at 1/2/4/8 B200; % of roofline"
+WORKLOAD = "configs[1]: Llama-2-7B shape (32L, 32 KV heads, d128, fp16, block 16), 2048-token prompt split at s=1024, chunk 256"
+N_TOKENS, S_SPLIT, CHUNK, N_SETS = 2048, 1024, 256, 4
+HBM_FALLBACK = 6650.0         # B200_PROFILING.md fallback (GB/s, read+write copy)
+NVLINK_MEASURED = 770.0       # B200_PROFILING.md measured peer copy per direction (GB/s)
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, read+write copy)"
+    return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampler running during warm-up + timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(", ") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- oracle (CPU) timing
+class OracleSample:
+    """oracle.migrate (single-threaded plain C, as it stands) on a bounded sample of the
+    workload: the configs[1] request shape (Llama-2-7B rows, s = 1024) on 1 of its 32 layers.
+    Pools are generated once; each run() repeats the migration to fill a time budget."""
+
+    def __init__(self):
+        import kvgen
+        import oracle
+        self.oracle = oracle
+        g = kvgen.LLAMA2_7B
+        self.row = g.row_bytes
+        self.gp = g.with_(num_layers=1, num_blocks=N_TOKENS // g.block_size)
+        self.ts, self.td = kvgen.table_pair(7, N_TOKENS, self.gp, self.gp)
+        self.hs, self.hd = kvgen.fill_bytes(1, self.gp.pool_bytes), kvgen.fill_bytes(2, self.gp.pool_bytes)
+        t = time.perf_counter()
+        self._once(S_SPLIT)
+        self.per_rep = time.perf_counter() - t
+
+    def _once(self, ntok):
+        self.oracle.migrate(self.hs, self.gp, self.ts, self.hd, self.gp, self.td, (0, ntok), (0, 1))
+
+    def run(self, budget_s: float):
+        reps = max(1, int(budget_s / self.per_rep))
+        ntok = S_SPLIT if budget_s >= self.per_rep else max(16, int(S_SPLIT * budget_s / self.per_rep))
+        t = time.perf_counter()
+        for _ in range(reps):
+            self._once(ntok)
+        dt = time.perf_counter() - t
+        payload = reps * ntok * 2 * self.row
+        sample = (f"oracle.migrate (plain C, 1 thread) of the configs[1] request (Llama-2-7B rows, "
+                  f"tokens [0,{ntok}) of s=1024) on 1 of 32 layers, x{reps} = {payload / 2**20:.1f} MiB")
+        return payload / dt / 1e9, sample, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    per_step_budget = max(0.02, 90.0 / max(1, args.steps + args.warmup))
+    o = OracleSample()
+    for _ in range(args.warmup):
+        o.run(per_step_budget)
+    vals, total, sample = [], 0.0, ""
+    for _ in range(args.steps):
+        v, sample, dt = o.run(per_step_budget)
+        vals.append(v)
+        total += dt
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "kv_dtype": "fp16"},
+            "tokens_per_s": v * 1e9 / (2 * 32 * o.row),
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_dyna(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import kvgen
+    import paper_2504_09285_b200 as dk
+
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+
+    g = kvgen.LLAMA2_7B
+    payload = S_SPLIT * 2 * g.num_layers * g.row_bytes  # bytes per step (one request's [0, s) KV)
+    stream = torch.cuda.Stream()
+    cs = stream.cuda_stream
+
+    src = dk.Pool(g, dev, instance=rank)
+    dk.dyna_kv_debug_fill(src.tensor.data_ptr(), src.tensor.numel(), 1000 + rank, 0, cs)
+    if world == 1:
+        dst = dk.Pool(g, dev, instance=rank)
+        dk.dyna_kv_debug_fill(dst.tensor.data_ptr(), dst.tensor.numel(), 2000, 0, cs)
+        peer = None
+    else:
+        mine = dk.Pool(g, dev, instance=rank)
+        dk.dyna_kv_debug_fill(mine.tensor.data_ptr(), mine.tensor.numel(), 2000 + rank, 0, cs)
+        torch.cuda.synchronize()
+        handles = [None] * world
+        dist.all_gather_object(handles, dk.dyna_kv_pool_export(mine.handle))
+        peer = (rank + 1) % world
+        dst = dk.Pool.imported(handles[peer], dev)
+    # N_SETS disjoint request placements per pool, rotated every step: each step
+    # reads 512 MiB and writes 512 MiB that the previous steps did not touch (> 126 MB L2).
+    tabs = kvgen.batch_tables(500 + rank, [N_TOKENS] * N_SETS, g, g)
+    dts = [(torch.from_numpy(ts).to(f"cuda:{dev}"), torch.from_numpy(td).to(f"cuda:{dev}")) for ts, td in tabs]
+    tables = [(dk.table(src, a, ts), dk.table(dst, b, td)) for (a, b), (ts, td) in zip(dts, tabs)]
+    mopts = dk.opts(variant=args.variant, engine=args.engine)
+    torch.cuda.synchronize()
+
+    def step(i, o=mopts):
+        st, dt_ = tables[i % N_SETS]
+        return dk.dyna_kv_migrate_ex(st, dt_, (0, S_SPLIT), (0, g.num_layers), CHUNK, cs, o)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    clocks = Clocks(dev)
+    # warm-up (untimed), then ~0.5 s of untimed load so the clock samples see the part under load
+    xs = [step(i) for i in range(args.warmup)]
+    for x in xs:
+        dk.dyna_kv_wait(x)
+    t_end = time.perf_counter() + 0.5
+    i = 0
+    while time.perf_counter() < t_end:
+        xs = [step(i + j) for j in range(50)]
+        for x in xs:
+            dk.dyna_kv_wait(x)
+        i += 50
+
+    # ---------------- timed region: exactly K steps, device-timed with CUDA events on the launch stream
+    ev_a = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev_b = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    n_launch0 = dk.dyna_kv_launch_count()
+    t0.record(stream)
+    xs = []
+    for k in range(args.steps):
+        ev_a[k].record(stream)
+        xs.append(step(k))
+        ev_b[k].record(stream)
+    t1.record(stream)
+    for x in xs:
+        dk.dyna_kv_wait(x)
+    barrier()
+    launches = dk.dyna_kv_launch_count() - n_launch0
+    clk = clocks.stop()
+    total_ms = max_over_ranks(t0.elapsed_time(t1))
+    kern_ms = statistics.fmean(a.elapsed_time(b) for a, b in zip(ev_a, ev_b))
+    kern_ms = max_over_ranks(kern_ms)
+
+    # ---------------- e2e through the public API with host buffers: every step copies the
+    # request's two block tables from pinned host memory, migrates with per-chunk flags, reads
+    # the chunk flags back to the host and blocks in dyna_kv_wait.
+    nchunks = -(-S_SPLIT // CHUNK)
+    host_tabs = [(torch.from_numpy(ts).pin_memory(), torch.from_numpy(td).pin_memory()) for ts, td in tabs]
+    dev_tabs = [(torch.empty_like(a, device=f"cuda:{dev}"), torch.empty_like(b, device=f"cuda:{dev}"))
+                for a, b in host_tabs]
+    e2e_tables = [(dk.table(src, a, ts), dk.table(dst, b, td)) for (a, b), (ts, td) in zip(dev_tabs, tabs)]
+    flags_host = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
+    sig_opts = dk.opts(variant=args.variant, engine=args.engine, flags=dk.DYNA_MIGRATE_SIGNAL)
+    sender = rank
+    flag_pool = dst.handle
+    h2d = sum(a.numel() * 4 + b.numel() * 4 for a, b in host_tabs) // N_SETS
+    d2h = nchunks * 8
+
+    def e2e_step(k):
+        (ha, hb), (da, db) = host_tabs[k % N_SETS], dev_tabs[k % N_SETS]
+        with torch.cuda.stream(stream):
+            da.copy_(ha, non_blocking=True)
+            db.copy_(hb, non_blocking=True)
+        st, dt_ = e2e_tables[k % N_SETS]
+        x = dk.dyna_kv_migrate_ex(st, dt_, (0, S_SPLIT), (0, g.num_layers), CHUNK, cs, sig_opts)
+        epoch = dk.dyna_kv_xfer_info(x)[0]
+        dk.dyna_kv_copy_flags(flag_pool, sender, 0, nchunks, flags_host.data_ptr(), cs)
+        dk.dyna_kv_wait(x)
+        return epoch
+
+    for k in range(args.warmup):
+        e2e_step(k)
+    barrier()
+    t = time.perf_counter()
+    for k in range(args.steps):
+        epoch = e2e_step(k)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t)
+    assert int(flags_host.min()) == epoch, "chunk flags did not reach the last epoch"
+    barrier()
+
+    if rank == 0:
+        hbm_peak, hbm_src = load_peaks()
+        gbps = world * args.steps * payload / (total_ms / 1e3) / 1e9
+        if world == 1:
+            achieved = 2 * payload / (kern_ms / 1e3) / 1e9  # HBM read + write bytes per launch / duration
+            roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                    "traffic": ncu_traffic(), "peak_source": hbm_src,
+                    "kernel": "dynakv::k_copy_vec (K4-local fused reblock)" if args.engine != dk.DYNA_ENGINE_BULK
+                    else "dynakv::k_copy_bulk (K4-local fused reblock)",
+                    "algorithmic_bytes_per_launch": 2 * payload, "kernel_ms": kern_ms}
+        else:
+            achieved = payload / (kern_ms / 1e3) / 1e9      # bytes crossing NVLink per launch / duration
+            roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_MEASURED, "unit": "GB/s",
+                    "frac": achieved / NVLINK_MEASURED, "traffic": None,
+                    "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900",
+                    "algorithmic_bytes_per_launch": payload, "kernel_ms": kern_ms}
+        line = {
+            "metric": METRIC, "value": gbps, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "kv_dtype": "fp16", "payload_bytes_per_step": payload,
+                       "pairs": "rank r -> rank (r+1) % N over CUDA IPC" if world > 1 else "intra-device reblock",
+                       "variant": args.variant, "engine": args.engine,
+                       "l2": f"{N_SETS} disjoint block-table sets rotated per step; 1 GiB of HBM traffic per step > 126 MB L2"},
+            "tokens_per_s": world * args.steps * S_SPLIT / (total_ms / 1e3),
+            "roofline": roof,
+            "e2e": {"value": world * args.steps * payload / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, sample, dt = OracleSample().run(12.0)
+            line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+                                    "seconds": dt, "host_cpus": os.cpu_count()}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="dyna", choices=["dyna", "reference"])
+    ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 VEC, 2 BULK")
+    ap.add_argument("--variant", type=int, default=0, help="0 auto, 1 FUSED, 2 STAGED")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local_rank = env_rank()
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_dyna(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,237 @@
+/*
+ * dyna_kv.h — C ABI of the B200-native chunked KV-cache migration library
+ * (libdyna_kv.so, sources in paper_2504_09285_b200/csrc/).
+ *
+ * The operation (PAPER.md = arXiv 2504.09285, DynaServe):
+ *   §3.1 P:306-308  a request of L = P + D tokens is split at s into the
+ *                   micro-requests r^alpha (tokens 1..s) and r^beta
+ *                   (tokens s+1..L); s = ceil(phi*L).
+ *   §3.1 P:352      "When the micro-requests of an LLM request span two
+ *                   execution instances, the instances exchange the required
+ *                   KV cache blocks."
+ *   §4.3 P:556      r^alpha is processed "in equal-sized chunks"; "once chunk
+ *                   k completes, its KV block is immediately DMA-pushed" to
+ *                   the other instance, and messages steer "placement on the
+ *                   receiver side".
+ * dyna_kv_migrate() is that push: for every layer l in layer_range, K and V,
+ * every token t in token_range, all KV heads, the row of the source pool
+ * reached through the source block table is copied, bit for bit, to the row
+ * of the destination pool reached through the destination block table
+ * (the receiver's placement).  Nothing else in either pool changes.  Token
+ * indices are 0-based and ranges half-open (reading R1: paper token
+ * i is index i-1, so r^alpha is [0, s)).
+ *
+ * Pool layout (reading R3; the paper does not fix one):
+ *   element (l, kv, block b, slot j, head h, i) of e bytes lives at byte
+ *   ((((l*2 + kv)*NB + b)*bs + j)*H + h)*d*e + i*e        kv: 0 = K, 1 = V
+ * i.e. [L][2][NB][bs][H][d].  One token's K (or V) in one layer is one
+ * contiguous "row" of H*d*e bytes; a block is bs consecutive rows.
+ *
+ * Errors: every call returns a dyna_status; negative values are errors and
+ * dyna_kv_last_error() returns a thread-local message.  No call throws.
+ * Synchronous errors leave nothing enqueued.
+ *
+ * Threading: calls are thread-safe; a pool handle may be used from several
+ * threads as long as it is not destroyed concurrently.
+ */
+#ifndef DYNA_KV_H
+#define DYNA_KV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define DYNA_API __attribute__((visibility("default")))
+#else
+#define DYNA_API
+#endif
+
+struct CUstream_st; /* cudaStream_t == struct CUstream_st* ; NULL = legacy default stream */
+
+typedef int32_t dyna_status;
+#define DYNA_OK         0
+#define DYNA_EINVAL    (-1)  /* NULL handle/pointer, bad option value, misaligned base */
+#define DYNA_EGEOM     (-2)  /* geometry mismatch (L, H, d, e differ) or row bytes % 16 != 0 */
+#define DYNA_ERANGE    (-3)  /* token/layer range outside the tables/pool, block id out of range,
+                                chunk_tokens <= 0, too many chunks for signalling */
+#define DYNA_EALIAS    (-4)  /* two destination rows coincide, or dst rows overlap src rows of the same pool */
+#define DYNA_EPEER     (-5)  /* destination memory not reachable from the source device (no P2P / IPC) */
+#define DYNA_ENOMEM    (-6)
+#define DYNA_ECUDA     (-7)  /* a CUDA runtime error (message in dyna_kv_last_error) */
+#define DYNA_ETIMEDOUT (-8)
+#define DYNA_EAGAIN    (-9)  /* dyna_kv_query: still in flight */
+#define DYNA_ENOTSUP   (-10)
+
+/* Pool geometry.  All fields > 0 except device (a CUDA ordinal >= 0) and
+ * instance (0 <= instance < DYNA_MAX_INSTANCES; the id this pool's owner uses
+ * as a sender when signalling peers, e.g. its rank). */
+typedef struct {
+    int32_t num_layers;    /* L */
+    int32_t num_kv_heads;  /* H */
+    int32_t head_dim;      /* d */
+    int32_t elem_bytes;    /* e: 2 for fp16/bf16.  The copy is bitwise, dtype-agnostic. */
+    int32_t block_size;    /* bs: tokens per block (source and destination may differ) */
+    int32_t num_blocks;    /* NB */
+    int32_t device;        /* CUDA ordinal owning the memory */
+    int32_t instance;      /* sender id for per-chunk flags */
+} dyna_kv_pool_desc;
+
+#define DYNA_MAX_INSTANCES 64
+#define DYNA_MAX_CHUNKS    4096   /* per migration when per-chunk flags are written */
+
+typedef struct dyna_kv_pool* dyna_kv_pool_t;
+typedef struct dyna_kv_xfer* dyna_kv_xfer_t;
+
+/* A request's block table on one pool: logical token t lives in block
+ * block_ids[t / bs] at slot t % bs.
+ *   block_ids       DEVICE pointer, int32[len], readable from the source
+ *                   device (device memory of the source GPU, or of a peer
+ *                   with P2P enabled).  Caller-owned; must stay valid and
+ *                   unmodified until dyna_kv_wait returns (like the source of
+ *                   cudaMemcpyAsync).
+ *   host_block_ids  optional HOST copy of the same ids.  When given for both
+ *                   tables, ids are range-checked and destination aliasing is
+ *                   rejected synchronously (DYNA_ERANGE / DYNA_EALIAS).  When
+ *                   NULL, ids are range-checked on the device: offending rows
+ *                   are skipped and dyna_kv_wait returns DYNA_ERANGE. */
+typedef struct {
+    dyna_kv_pool_t pool;
+    const int32_t* block_ids;
+    const int32_t* host_block_ids;
+    int64_t len;
+} dyna_block_table;
+
+typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
+
+/* Variant. */
+#define DYNA_VARIANT_AUTO   0  /* calibrated choice per (row bytes, chunk size) */
+#define DYNA_VARIANT_FUSED  1  /* one kernel: source rows -> destination rows (K4 / K4-local) */
+#define DYNA_VARIANT_STAGED 2  /* gather -> staging -> peer staging (+flag) -> scatter (K1, K2, K3) */
+/* Copy engine inside the kernels. */
+#define DYNA_ENGINE_AUTO 0
+#define DYNA_ENGINE_VEC  1     /* warp-per-segment 16-B vector loads/stores (LDG.128 / STG.128) */
+#define DYNA_ENGINE_BULK 2     /* TMA bulk copies through a shared-memory ring (UBLKCP) */
+/* flags */
+#define DYNA_MIGRATE_SIGNAL 1  /* write a per-chunk flag into the destination pool's inbox */
+
+typedef struct {
+    int32_t variant;    /* DYNA_VARIANT_*  (0 = auto) */
+    int32_t engine;     /* DYNA_ENGINE_*   (0 = auto) */
+    int32_t max_ctas;   /* cap on CTAs per kernel (SM budget for overlap with a producer); 0 = no cap */
+    int32_t flags;      /* DYNA_MIGRATE_* */
+    int32_t piece_bytes;/* bytes per work item; 0 = engine default.  Multiple of 16. */
+    int32_t stages;     /* BULK: shared-memory ring depth; 0 = default */
+} dyna_kv_opts;
+
+/* Bytes a pool of this geometry needs: L*2*NB*bs*H*d*e.  0 if desc invalid. */
+DYNA_API size_t dyna_kv_pool_bytes(const dyna_kv_pool_desc* desc);
+
+/* Wrap caller memory as a pool.  device_base: device pointer on desc->device,
+ * 256-B aligned, at least dyna_kv_pool_bytes(desc) bytes, BORROWED (the
+ * library never frees it; keep it alive until dyna_kv_pool_destroy).  The
+ * library allocates a small per-pool inbox of chunk flags on desc->device. */
+DYNA_API dyna_status dyna_kv_pool_create(const dyna_kv_pool_desc* desc, void* device_base, dyna_kv_pool_t* out);
+DYNA_API dyna_status dyna_kv_pool_destroy(dyna_kv_pool_t pool);
+
+/* Migrate src -> dst for token_range x layer_range in chunks of chunk_tokens
+ * (chunk k = [begin + k*c, min(begin + (k+1)*c, end)), reading R5).
+ * Work is enqueued on `stream`, which must belong to the SOURCE pool's
+ * device; it runs after prior work on that stream (so a caller orders each
+ * chunk's migrate after the prefill that produced it — P:556).  The source
+ * rows must not be written until completion (KV is append-only); the
+ * destination rows must not be read before completion (or their chunk flag).
+ * An empty token or layer range returns DYNA_OK with nothing enqueued.
+ * *out receives a handle that must be passed to dyna_kv_wait exactly once. */
+DYNA_API dyna_status dyna_kv_migrate(dyna_block_table src, dyna_block_table dst,
+                            dyna_range token_range, dyna_range layer_range,
+                            int32_t chunk_tokens, struct CUstream_st* stream,
+                            dyna_kv_xfer_t* out);
+
+/* Same, with explicit options (opts may be NULL = all defaults). */
+DYNA_API dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst,
+                               dyna_range token_range, dyna_range layer_range,
+                               int32_t chunk_tokens, struct CUstream_st* stream,
+                               const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
+
+/* Block the host until every chunk is resident in the destination, report
+ * deferred errors (DYNA_ECUDA, DYNA_ERANGE from device-side id checks), free
+ * the handle. */
+DYNA_API dyna_status dyna_kv_wait(dyna_kv_xfer_t xfer);
+
+/* Non-blocking: DYNA_OK if complete, DYNA_EAGAIN if in flight.  Does not free. */
+DYNA_API dyna_status dyna_kv_query(dyna_kv_xfer_t xfer);
+
+/* Enqueue on `stream` (work is ordered after it) a wait until the whole
+ * migration is complete — the device-side form of dyna_kv_wait, for a
+ * consumer (r^beta's compute) on another stream of the source device. */
+DYNA_API dyna_status dyna_kv_stream_wait(dyna_kv_xfer_t xfer, struct CUstream_st* stream);
+
+/* Per-chunk readiness (DYNA_MIGRATE_SIGNAL).  Each signalled migration gets
+ * an epoch, monotone per (sender instance, destination pool).  Chunk k of
+ * that migration is resident when the destination inbox slot [sender][k]
+ * holds a value >= epoch.  Migrations from one sender into one destination
+ * pool that request signalling must be ordered on one stream. */
+DYNA_API dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t xfer, uint64_t* epoch, int32_t* num_chunks, int32_t* sender);
+
+/* Enqueue on `stream` (a stream of the DESTINATION pool's device) a device
+ * wait (acquire, system scope) until chunk `chunk` from `sender` reaches
+ * `epoch`; work after it on `stream` sees the chunk's rows.  timeout_ns 0 =
+ * no timeout; on timeout the kernel records DYNA_ETIMEDOUT for the next
+ * dyna_kv_wait / dyna_kv_poll_error on that process. */
+DYNA_API dyna_status dyna_kv_stream_wait_chunk(dyna_kv_pool_t dst, int32_t sender, int32_t chunk,
+                                      uint64_t epoch, uint64_t timeout_ns,
+                                      struct CUstream_st* stream);
+
+/* Enqueue on `stream` a copy of inbox slots [sender][first, first+n) of
+ * `dst` into host memory `host_out` (n uint64 values; pinned memory makes it
+ * asynchronous).  Lets a host-side scheduler see which chunks have landed
+ * (r^beta may start once all chunks covering [0, s) are resident). */
+DYNA_API dyna_status dyna_kv_copy_flags(dyna_kv_pool_t dst, int32_t sender, int32_t first, int32_t n,
+                                        uint64_t* host_out, struct CUstream_st* stream);
+
+/* Thread-local description of the last error on this thread. */
+DYNA_API const char* dyna_kv_last_error(void);
+
+/* Deferred device-side error recorded since the last call (and clear it). */
+DYNA_API dyna_status dyna_kv_poll_error(void);
+
+/* Number of kernels this library has launched in this process. */
+DYNA_API uint64_t dyna_kv_launch_count(void);
+
+/* ---------------- peers ---------------- */
+
+/* Enable P2P from `device` to `peer` (both in this process).  DYNA_EPEER if
+ * the pair cannot access each other.  dyna_kv_migrate also does this lazily. */
+DYNA_API dyna_status dyna_kv_enable_peer(int32_t device, int32_t peer);
+
+/* Cross-process pools (one process per GPU): the owner exports its pool, a
+ * peer imports it and can then use it as a migration destination (or
+ * source).  The handle is plain bytes; send it with any channel (e.g.
+ * torch.distributed all_gather_object). */
+typedef struct {
+    uint8_t pool_mem[64];    /* cudaIpcMemHandle_t of the allocation holding the pool */
+    uint8_t inbox_mem[64];   /* cudaIpcMemHandle_t of the pool's flag inbox */
+    uint64_t pool_offset;    /* byte offset of device_base inside its allocation */
+    dyna_kv_pool_desc desc;  /* the owner's geometry */
+} dyna_kv_ipc_handle;
+
+DYNA_API dyna_status dyna_kv_pool_export(dyna_kv_pool_t pool, dyna_kv_ipc_handle* out);
+/* Map a peer's pool into `local_device`'s address space. */
+DYNA_API dyna_status dyna_kv_pool_import(const dyna_kv_ipc_handle* handle, int32_t local_device, dyna_kv_pool_t* out);
+
+/* ---------------- test-input generator (NOT part of the migration) -------------
+ * Fill `bytes` (multiple of 16) at device pointer `dst` with the kvgen stream
+ * for `seed`, starting at stream byte `byte_offset` (multiple of 8):
+ *   word(w) = splitmix64(splitmix64(seed) ^ (w * 0xD1B54A32D192ED03)).
+ * Same counter generator as kvgen/__init__.py (each side implements it). */
+DYNA_API dyna_status dyna_kv_debug_fill(void* dst, uint64_t bytes, uint64_t seed, uint64_t byte_offset,
+                               struct CUstream_st* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNA_KV_H */

@@ -1,0 +1,276 @@
+"""Python binding of libdyna_kv.so — the B200 chunked KV-cache migration path.
+
+Argument marshalling only (ctypes).  Every step of the migration runs in the
+CUDA kernels behind the C ABI declared in include/dyna_kv.h; PyTorch is used
+by callers for device memory, streams and process groups.  There is no CPU
+fallback: importing this package without the built library raises.
+
+The C functions are exposed under their own names (dyna_kv_pool_create,
+dyna_kv_migrate, dyna_kv_wait, ...).  `Pool` and `table` are small
+conveniences that keep the torch tensors backing a pool / block table alive.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdyna_kv.so")
+
+# ---------------------------------------------------------------- constants (include/dyna_kv.h)
+DYNA_OK, DYNA_EINVAL, DYNA_EGEOM, DYNA_ERANGE, DYNA_EALIAS = 0, -1, -2, -3, -4
+DYNA_EPEER, DYNA_ENOMEM, DYNA_ECUDA, DYNA_ETIMEDOUT, DYNA_EAGAIN, DYNA_ENOTSUP = -5, -6, -7, -8, -9, -10
+STATUS_NAMES = {0: "DYNA_OK", -1: "DYNA_EINVAL", -2: "DYNA_EGEOM", -3: "DYNA_ERANGE", -4: "DYNA_EALIAS",
+                -5: "DYNA_EPEER", -6: "DYNA_ENOMEM", -7: "DYNA_ECUDA", -8: "DYNA_ETIMEDOUT", -9: "DYNA_EAGAIN",
+                -10: "DYNA_ENOTSUP"}
+DYNA_MAX_INSTANCES, DYNA_MAX_CHUNKS = 64, 4096
+DYNA_VARIANT_AUTO, DYNA_VARIANT_FUSED, DYNA_VARIANT_STAGED = 0, 1, 2
+DYNA_ENGINE_AUTO, DYNA_ENGINE_VEC, DYNA_ENGINE_BULK = 0, 1, 2
+DYNA_MIGRATE_SIGNAL = 1
+
+# every symbol include/dyna_kv.h declares
+EXPORTS = (
+    "dyna_kv_pool_bytes", "dyna_kv_pool_create", "dyna_kv_pool_destroy", "dyna_kv_migrate",
+    "dyna_kv_migrate_ex", "dyna_kv_wait", "dyna_kv_query", "dyna_kv_stream_wait", "dyna_kv_xfer_info",
+    "dyna_kv_stream_wait_chunk", "dyna_kv_last_error", "dyna_kv_poll_error", "dyna_kv_launch_count",
+    "dyna_kv_enable_peer", "dyna_kv_pool_export", "dyna_kv_pool_import", "dyna_kv_debug_fill",
+    "dyna_kv_copy_flags",
+)
+
+
+class dyna_kv_pool_desc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("num_layers", "num_kv_heads", "head_dim", "elem_bytes",
+                                               "block_size", "num_blocks", "device", "instance")]
+
+
+class dyna_block_table(ctypes.Structure):
+    _fields_ = [("pool", ctypes.c_void_p), ("block_ids", ctypes.c_void_p),
+                ("host_block_ids", ctypes.c_void_p), ("len", ctypes.c_int64)]
+
+
+class dyna_range(ctypes.Structure):
+    _fields_ = [("begin", ctypes.c_int64), ("end", ctypes.c_int64)]
+
+
+class dyna_kv_opts(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("variant", "engine", "max_ctas", "flags", "piece_bytes", "stages")]
+
+
+class dyna_kv_ipc_handle(ctypes.Structure):
+    _fields_ = [("pool_mem", ctypes.c_uint8 * 64), ("inbox_mem", ctypes.c_uint8 * 64),
+                ("pool_offset", ctypes.c_uint64), ("desc", dyna_kv_pool_desc)]
+
+
+class DynaKVError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run `python paper_2504_09285_b200/build.py` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    st, vp, p = ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER
+    sig = {
+        "dyna_kv_pool_bytes": (ctypes.c_size_t, [p(dyna_kv_pool_desc)]),
+        "dyna_kv_pool_create": (st, [p(dyna_kv_pool_desc), vp, p(vp)]),
+        "dyna_kv_pool_destroy": (st, [vp]),
+        "dyna_kv_migrate": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32, vp,
+                                 p(vp)]),
+        "dyna_kv_migrate_ex": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
+                                    vp, p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_wait": (st, [vp]),
+        "dyna_kv_query": (st, [vp]),
+        "dyna_kv_stream_wait": (st, [vp, vp]),
+        "dyna_kv_xfer_info": (st, [vp, p(ctypes.c_uint64), p(ctypes.c_int32), p(ctypes.c_int32)]),
+        "dyna_kv_stream_wait_chunk": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64,
+                                           vp]),
+        "dyna_kv_copy_flags": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp]),
+        "dyna_kv_last_error": (ctypes.c_char_p, []),
+        "dyna_kv_poll_error": (st, []),
+        "dyna_kv_launch_count": (ctypes.c_uint64, []),
+        "dyna_kv_enable_peer": (st, [ctypes.c_int32, ctypes.c_int32]),
+        "dyna_kv_pool_export": (st, [vp, p(dyna_kv_ipc_handle)]),
+        "dyna_kv_pool_import": (st, [p(dyna_kv_ipc_handle), ctypes.c_int32, p(vp)]),
+        "dyna_kv_debug_fill": (st, [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype, f.argtypes = res, args
+    return L
+
+
+lib = _load()
+
+
+def _check(status: int) -> int:
+    if status < 0:
+        raise DynaKVError(status, lib.dyna_kv_last_error().decode(errors="replace"))
+    return status
+
+
+# ---------------------------------------------------------------- C functions, same names
+def dyna_kv_pool_bytes(desc: dyna_kv_pool_desc) -> int:
+    return lib.dyna_kv_pool_bytes(ctypes.byref(desc))
+
+
+def dyna_kv_pool_create(desc: dyna_kv_pool_desc, device_base: int) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_pool_create(ctypes.byref(desc), ctypes.c_void_p(device_base), ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_pool_destroy(pool: int) -> None:
+    _check(lib.dyna_kv_pool_destroy(ctypes.c_void_p(pool)))
+
+
+def dyna_kv_migrate(src: dyna_block_table, dst: dyna_block_table, token_range, layer_range, chunk_tokens: int,
+                    stream: int = 0) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_migrate(src, dst, dyna_range(*token_range), dyna_range(*layer_range), chunk_tokens,
+                               ctypes.c_void_p(stream), ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_migrate_ex(src: dyna_block_table, dst: dyna_block_table, token_range, layer_range, chunk_tokens: int,
+                       stream: int = 0, opts: dyna_kv_opts | None = None) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_migrate_ex(src, dst, dyna_range(*token_range), dyna_range(*layer_range), chunk_tokens,
+                                  ctypes.c_void_p(stream), ctypes.byref(opts) if opts is not None else None,
+                                  ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_wait(xfer: int) -> None:
+    _check(lib.dyna_kv_wait(ctypes.c_void_p(xfer)))
+
+
+def dyna_kv_query(xfer: int) -> bool:
+    s = lib.dyna_kv_query(ctypes.c_void_p(xfer))
+    if s == DYNA_EAGAIN:
+        return False
+    _check(s)
+    return True
+
+
+def dyna_kv_stream_wait(xfer: int, stream: int) -> None:
+    _check(lib.dyna_kv_stream_wait(ctypes.c_void_p(xfer), ctypes.c_void_p(stream)))
+
+
+def dyna_kv_xfer_info(xfer: int) -> tuple[int, int, int]:
+    e, n, s = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.dyna_kv_xfer_info(ctypes.c_void_p(xfer), ctypes.byref(e), ctypes.byref(n), ctypes.byref(s)))
+    return e.value, n.value, s.value
+
+
+def dyna_kv_stream_wait_chunk(dst_pool: int, sender: int, chunk: int, epoch: int, timeout_ns: int = 0,
+                              stream: int = 0) -> None:
+    _check(lib.dyna_kv_stream_wait_chunk(ctypes.c_void_p(dst_pool), sender, chunk, epoch, timeout_ns,
+                                         ctypes.c_void_p(stream)))
+
+
+def dyna_kv_copy_flags(dst_pool: int, sender: int, first: int, n: int, host_out_ptr: int, stream: int = 0) -> None:
+    """host_out_ptr: address of n uint64 (e.g. a pinned torch.int64 tensor's data_ptr())."""
+    _check(lib.dyna_kv_copy_flags(ctypes.c_void_p(dst_pool), sender, first, n, ctypes.c_void_p(host_out_ptr),
+                                  ctypes.c_void_p(stream)))
+
+
+def dyna_kv_last_error() -> str:
+    return lib.dyna_kv_last_error().decode(errors="replace")
+
+
+def dyna_kv_poll_error() -> None:
+    _check(lib.dyna_kv_poll_error())
+
+
+def dyna_kv_launch_count() -> int:
+    return lib.dyna_kv_launch_count()
+
+
+def dyna_kv_enable_peer(device: int, peer: int) -> None:
+    _check(lib.dyna_kv_enable_peer(device, peer))
+
+
+def dyna_kv_pool_export(pool: int) -> bytes:
+    h = dyna_kv_ipc_handle()
+    _check(lib.dyna_kv_pool_export(ctypes.c_void_p(pool), ctypes.byref(h)))
+    return bytes(h)
+
+
+def dyna_kv_pool_import(handle: bytes, local_device: int) -> int:
+    h = dyna_kv_ipc_handle.from_buffer_copy(handle)
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_pool_import(ctypes.byref(h), local_device, ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_debug_fill(dst: int, nbytes: int, seed: int, byte_offset: int = 0, stream: int = 0) -> None:
+    _check(lib.dyna_kv_debug_fill(ctypes.c_void_p(dst), nbytes, seed & ((1 << 64) - 1), byte_offset,
+                                  ctypes.c_void_p(stream)))
+
+
+# ---------------------------------------------------------------- conveniences (keep torch memory alive)
+class Pool:
+    """A paged KV pool in a torch uint8 tensor on `device`, wrapped by the library."""
+
+    def __init__(self, geom, device: int = 0, instance: int = 0, tensor=None):
+        import torch
+        self.geom = geom
+        self.desc = dyna_kv_pool_desc(geom.num_layers, geom.num_kv_heads, geom.head_dim, geom.elem_bytes,
+                                      geom.block_size, geom.num_blocks, device, instance)
+        nbytes = dyna_kv_pool_bytes(self.desc)
+        if nbytes == 0:
+            raise DynaKVError(DYNA_EINVAL, "invalid geometry")
+        self.tensor = tensor if tensor is not None else torch.empty(nbytes, dtype=torch.uint8,
+                                                                    device=f"cuda:{device}")
+        assert self.tensor.numel() >= nbytes and self.tensor.dtype == torch.uint8
+        self.device = device
+        self.handle = dyna_kv_pool_create(self.desc, self.tensor.data_ptr())
+
+    @classmethod
+    def imported(cls, handle: bytes, local_device: int):
+        self = cls.__new__(cls)
+        h = dyna_kv_ipc_handle.from_buffer_copy(handle)
+        self.desc, self.geom, self.tensor, self.device = h.desc, None, None, local_device
+        self.handle = dyna_kv_pool_import(handle, local_device)
+        return self
+
+    def close(self):
+        if getattr(self, "handle", None):
+            dyna_kv_pool_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def table(pool: Pool, ids, host_ids=None) -> dyna_block_table:
+    """Block table over `pool`.  ids: int32 CUDA tensor; host_ids: optional numpy int32 (validation)."""
+    import numpy as np
+    t = dyna_block_table(pool.handle, ids.data_ptr(), None, ids.numel())
+    t._keep = [ids]
+    if host_ids is not None:
+        h = np.ascontiguousarray(host_ids, dtype=np.int32)
+        t.host_block_ids = h.ctypes.data
+        t._keep.append(h)
+    return t
+
+
+def opts(variant=0, engine=0, max_ctas=0, flags=0, piece_bytes=0, stages=0) -> dyna_kv_opts:
+    return dyna_kv_opts(variant, engine, max_ctas, flags, piece_bytes, stages)
+
+
+def migrate(src: dyna_block_table, dst: dyna_block_table, token_range, layer_range, chunk_tokens, stream=None,
+            **kw) -> int:
+    """dyna_kv_migrate_ex on a torch stream (default: current stream of the source device)."""
+    import torch
+    if stream is None:
+        s = torch.cuda.current_stream().cuda_stream
+    else:
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return dyna_kv_migrate_ex(src, dst, token_range, layer_range, chunk_tokens, s, opts(**kw) if kw else None)

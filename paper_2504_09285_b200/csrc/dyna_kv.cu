@@ -1,0 +1,805 @@
+// dyna_kv.cu — host side of the C ABI declared in include/dyna_kv.h.
+//
+// Owns pool geometry and validation, peer mappings (P2P in-process, CUDA IPC
+// across processes), the per-(sender, destination) signalling channels, the
+// variant/engine choice, and the launch of the kernels in
+// dyna_kv_kernels.cuh.  Paper mapping: PAPER.md §3.1 P:352 (instances
+// exchange the required KV blocks) and §4.3 P:556 (chunk-granular push,
+// placement steered on the receiver = the destination block table).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "dyna_kv.h"
+#include "dyna_kv_kernels.cuh"
+
+using namespace dynakv;
+
+// ============================================================== errors
+namespace {
+thread_local std::string g_err;
+
+dyna_status fail(dyna_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+  do {                                                                                         \
+    cudaError_t e_ = (expr);                                                                   \
+    if (e_ != cudaSuccess) {                                                                   \
+      return fail(DYNA_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                   \
+    }                                                                                          \
+  } while (0)
+
+struct DeviceGuard {  // restores the caller's current device
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+std::atomic<uint64_t> g_launches{0};
+std::mutex g_mu;
+
+// Process-wide deferred error word in mapped pinned host memory: kernels
+// atomicOr ERR_* bits into it; dyna_kv_wait / dyna_kv_poll_error read it.
+unsigned int* g_err_word = nullptr;
+
+unsigned int* err_word() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_err_word) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    std::memset(p, 0, 64);
+    g_err_word = static_cast<unsigned int*>(p);
+  }
+  return g_err_word;
+}
+
+dyna_status take_device_error() {
+  unsigned int* w = err_word();
+  if (!w) return DYNA_OK;
+  const unsigned int bits = __atomic_exchange_n(w, 0u, __ATOMIC_ACQ_REL);
+  if (bits & ERR_BAD_BLOCK) return fail(DYNA_ERANGE, "device-side check: block id outside [0, num_blocks)");
+  if (bits & ERR_TIMEOUT) return fail(DYNA_ETIMEDOUT, "device-side chunk wait timed out");
+  return DYNA_OK;
+}
+
+struct DevInfo {
+  int sms = 0;
+  int vec_occ = 0;   // resident CTAs/SM of the VEC kernel
+  int bulk_occ = 0;  // for the default BULK smem size
+  int bulk_smem_set = 0;
+  cudaStream_t aux = nullptr;  // library stream for destination-side kernels (staged, cross-device)
+};
+std::map<int, DevInfo> g_dev;
+
+constexpr int kVecU = 8;
+constexpr int kVecThreads = 256;
+constexpr int kVecPiece = 8192;
+constexpr int kBulkPiece = 32768;
+constexpr int kBulkStages = 6;
+constexpr int64_t kStageSlotBytes = 64ll << 20;  // staged variant: bytes per staging slot
+
+DevInfo* dev_info(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevInfo& d = g_dev[dev];
+  if (d.sms == 0) {
+    DeviceGuard g(dev);
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.vec_occ, k_copy_vec<kVecU, false>, kVecThreads, 0);
+    if (d.vec_occ <= 0) d.vec_occ = 1;
+    if (d.sms <= 0) d.sms = 1;
+  }
+  return &d;
+}
+
+}  // namespace
+
+// ============================================================== objects
+struct Channel {  // sender pool -> destination pool
+  std::map<int, unsigned long long*> counters;  // per kernel device: [DYNA_MAX_CHUNKS], zero at rest
+  char* sstage = nullptr;                      // staged variant: 2 slots on the source device
+  char* dstage = nullptr;                      // staged variant: 2 slots on the destination device
+  int64_t slot_bytes = 0;
+  int sdev = -1, ddev = -1;
+};
+
+struct dyna_kv_pool {
+  dyna_kv_pool_desc desc{};
+  char* base = nullptr;
+  int dev = 0;               // device on which `base` can be dereferenced
+  bool imported = false;
+  void* ipc_pool_map = nullptr;
+  void* ipc_inbox_map = nullptr;
+  unsigned long long* inbox = nullptr;  // [DYNA_MAX_INSTANCES][DYNA_MAX_CHUNKS]
+  bool own_inbox = false;
+  int64_t row = 0;
+  std::mutex mu;
+  std::map<const dyna_kv_pool*, Channel> channels;  // keyed by destination pool
+};
+
+struct dyna_kv_xfer {
+  cudaEvent_t ev = nullptr;
+  int dev = 0;
+  bool empty = false;
+  uint64_t epoch = 0;
+  int32_t nchunks = 0;
+  int32_t sender = 0;
+};
+
+namespace {
+
+std::mutex g_ev_mu;
+std::map<int, std::vector<cudaEvent_t>> g_ev_free;
+
+cudaError_t get_event(int dev, cudaEvent_t* ev) {
+  {
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    auto& v = g_ev_free[dev];
+    if (!v.empty()) {
+      *ev = v.back();
+      v.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+}
+void put_event(int dev, cudaEvent_t ev) {
+  std::lock_guard<std::mutex> lk(g_ev_mu);
+  g_ev_free[dev].push_back(ev);
+}
+
+constexpr size_t kInboxBytes = sizeof(unsigned long long) * DYNA_MAX_INSTANCES * DYNA_MAX_CHUNKS;
+
+bool desc_valid(const dyna_kv_pool_desc* d) {
+  return d && d->num_layers > 0 && d->num_kv_heads > 0 && d->head_dim > 0 && d->elem_bytes > 0 &&
+         d->block_size > 0 && d->num_blocks > 0 && d->device >= 0 && d->instance >= 0 &&
+         d->instance < DYNA_MAX_INSTANCES;
+}
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// Build a launch plan for tokens [t0, t1) cut into chunks of c tokens.
+// g: run grid in tokens (absolute token index; divides the paged block sizes).
+Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1, int l0, int lm, int64_t c,
+               int64_t g, int piece) {
+  Plan p{};
+  p.src = s;
+  p.dst = d;
+  p.row = row;
+  p.t0 = t0;
+  p.t1 = t1;
+  p.l0 = l0;
+  p.lm = lm;
+  p.c = (int32_t)c;
+  p.g = (int32_t)g;
+  const bool aligned = (t0 % g == 0) && (c % g == 0);
+  p.R = aligned ? (int32_t)(c / g) : (int32_t)((c - 1) / g + 2);
+  const int64_t run_max = std::min(g, c) * row;
+  p.piece = piece;
+  p.P = (int32_t)((run_max + piece - 1) / piece);
+  p.nchunks = (int32_t)((t1 - t0 + c - 1) / c);
+  p.items_per_chunk = (int64_t)lm * 2 * p.R * p.P;
+  p.n_items = p.items_per_chunk * p.nchunks;
+  p.mig_t0 = t0;
+  p.mig_t1 = t1;
+  p.sig_c = (int32_t)c;
+  p.err = g_err_word;
+  return p;
+}
+
+// Launch one copy kernel.  engine: DYNA_ENGINE_VEC / BULK.
+dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int dev, cudaStream_t st) {
+  if (p.n_items == 0) return DYNA_OK;
+  DevInfo* di = dev_info(dev);
+  const bool sig = p.counters != nullptr;
+  if (engine == DYNA_ENGINE_BULK) {
+    const size_t smem = (size_t)stages * p.piece;
+    auto kern = sig ? k_copy_bulk<true> : k_copy_bulk<false>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem));
+    if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
+    int64_t grid = std::min<int64_t>(p.n_items, (int64_t)di->sms * occ);
+    if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+    kern<<<(unsigned)grid, 32, smem, st>>>(p, stages);
+  } else {
+    int64_t grid = std::min<int64_t>((p.n_items + kVecThreads / 32 - 1) / (kVecThreads / 32),
+                                     (int64_t)di->sms * di->vec_occ);
+    if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+    if (sig)
+      k_copy_vec<kVecU, true><<<(unsigned)grid, kVecThreads, 0, st>>>(p);
+    else
+      k_copy_vec<kVecU, false><<<(unsigned)grid, kVecThreads, 0, st>>>(p);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+Side paged(const dyna_kv_pool* pool, const int32_t* ids) {
+  Side s{};
+  s.base = pool->base;
+  s.table = ids;
+  s.nb = pool->desc.num_blocks;
+  s.bs = pool->desc.block_size;
+  s.linear = 0;
+  return s;
+}
+Side linear(char* base) {
+  Side s{};
+  s.base = base;
+  s.linear = 1;
+  return s;
+}
+
+// Synchronous checks that need the host copies of the tables.
+dyna_status check_host_tables(const dyna_block_table& src, const dyna_block_table& dst, int64_t t0, int64_t t1) {
+  struct Span {
+    int32_t id;
+    int64_t lo, hi;  // slot range [lo, hi) inside block id
+  };
+  auto spans = [&](const dyna_block_table& t, std::vector<Span>& out) -> dyna_status {
+    const int64_t bs = t.pool->desc.block_size, nb = t.pool->desc.num_blocks;
+    for (int64_t j = t0 / bs; j <= (t1 - 1) / bs; ++j) {
+      const int32_t id = t.host_block_ids[j];
+      if (id < 0 || id >= nb) return fail(DYNA_ERANGE, "block_ids[%lld] = %d outside [0, %lld)", (long long)j, id, (long long)nb);
+      const int64_t lo = std::max(t0, j * bs) - j * bs, hi = std::min(t1, (j + 1) * bs) - j * bs;
+      out.push_back({id, lo, hi});
+    }
+    return DYNA_OK;
+  };
+  std::vector<Span> s, d;
+  if (src.host_block_ids) {
+    dyna_status r = spans(src, s);
+    if (r) return r;
+  }
+  if (dst.host_block_ids) {
+    dyna_status r = spans(dst, d);
+    if (r) return r;
+    auto by_id = [](const Span& a, const Span& b) { return a.id != b.id ? a.id < b.id : a.lo < b.lo; };
+    std::vector<Span> ds = d;
+    std::sort(ds.begin(), ds.end(), by_id);
+    for (size_t i = 1; i < ds.size(); ++i)
+      if (ds[i].id == ds[i - 1].id && ds[i].lo < ds[i - 1].hi)
+        return fail(DYNA_EALIAS, "destination block %d is reached twice by the token range", ds[i].id);
+    if (src.host_block_ids && src.pool->base == dst.pool->base) {
+      std::vector<Span> ss = s;
+      std::sort(ss.begin(), ss.end(), by_id);
+      size_t i = 0;
+      for (const Span& x : ds) {
+        while (i < ss.size() && ss[i].id < x.id) ++i;
+        for (size_t k = i; k < ss.size() && ss[k].id == x.id; ++k)
+          if (ss[k].lo < x.hi && x.lo < ss[k].hi)
+            return fail(DYNA_EALIAS, "same pool: destination rows of block %d overlap source rows", x.id);
+      }
+    }
+  }
+  return DYNA_OK;
+}
+
+dyna_status ensure_peer(int dev, int peer) {
+  if (dev == peer) return DYNA_OK;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess || !can)
+    return fail(DYNA_EPEER, "device %d cannot access device %d (no P2P)", dev, peer);
+  DeviceGuard g(dev);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return DYNA_OK;
+  }
+  if (e != cudaSuccess) return fail(DYNA_EPEER, "cudaDeviceEnablePeerAccess(%d->%d): %s", dev, peer, cudaGetErrorString(e));
+  return DYNA_OK;
+}
+
+// Epochs are monotone per (sender instance, destination pool), whatever the
+// variant or the source pool object, so a flag never moves backwards.
+std::map<std::pair<int, const dyna_kv_pool*>, uint64_t> g_epochs;
+
+uint64_t next_epoch(int sender, const dyna_kv_pool* dst) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return ++g_epochs[{sender, dst}];
+}
+
+// Self-resetting per-chunk byte counters of channel src -> dst on device kdev.
+dyna_status channel_counters(dyna_kv_pool* src, const dyna_kv_pool* dst, int kdev, unsigned long long** out) {
+  std::lock_guard<std::mutex> lk(src->mu);
+  Channel& ch = src->channels[dst];
+  unsigned long long*& c = ch.counters[kdev];
+  if (!c) {
+    DeviceGuard g(kdev);
+    CUDA_TRY(cudaMalloc(&c, sizeof(unsigned long long) * DYNA_MAX_CHUNKS));
+    CUDA_TRY(cudaMemset(c, 0, sizeof(unsigned long long) * DYNA_MAX_CHUNKS));
+  }
+  *out = c;
+  return DYNA_OK;
+}
+
+// Staging slots of channel src -> dst (staged variant): 2 x slot on each side.
+dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t slot, char** sbuf, char** dbuf) {
+  std::lock_guard<std::mutex> lk(src->mu);
+  Channel& ch = src->channels[dst];
+  if (ch.slot_bytes < slot) {
+    if (ch.sstage) {  // grow: the previous migration on this channel must be done with them
+      DeviceGuard g(ch.sdev);
+      cudaDeviceSynchronize();
+      cudaFree(ch.sstage);
+      ch.sstage = nullptr;
+    }
+    if (ch.dstage) {
+      DeviceGuard g(ch.ddev);
+      cudaDeviceSynchronize();
+      cudaFree(ch.dstage);
+      ch.dstage = nullptr;
+    }
+    ch.slot_bytes = 0;
+    {
+      DeviceGuard g(src->dev);
+      if (cudaMalloc(&ch.sstage, 2 * slot) != cudaSuccess) return fail(DYNA_ENOMEM, "staging (source side)");
+      ch.sdev = src->dev;
+    }
+    {
+      DeviceGuard g(dst->dev);
+      if (cudaMalloc(&ch.dstage, 2 * slot) != cudaSuccess) return fail(DYNA_ENOMEM, "staging (destination side)");
+      ch.ddev = dst->dev;
+    }
+    ch.slot_bytes = slot;
+  }
+  *sbuf = ch.sstage;
+  *dbuf = ch.dstage;
+  return DYNA_OK;
+}
+
+}  // namespace
+
+// ============================================================== API
+extern "C" {
+
+const char* dyna_kv_last_error(void) { return g_err.c_str(); }
+uint64_t dyna_kv_launch_count(void) { return g_launches.load(); }
+dyna_status dyna_kv_poll_error(void) { return take_device_error(); }
+
+size_t dyna_kv_pool_bytes(const dyna_kv_pool_desc* d) {
+  if (!desc_valid(d)) return 0;
+  return (size_t)d->num_layers * 2 * (size_t)d->num_blocks * d->block_size * (size_t)d->num_kv_heads *
+         d->head_dim * d->elem_bytes;
+}
+
+dyna_status dyna_kv_pool_create(const dyna_kv_pool_desc* desc, void* device_base, dyna_kv_pool_t* out) {
+  if (!out || !desc || !device_base) return fail(DYNA_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (!desc_valid(desc)) return fail(DYNA_EINVAL, "invalid pool descriptor");
+  const int64_t row = (int64_t)desc->num_kv_heads * desc->head_dim * desc->elem_bytes;
+  if (row % 16) return fail(DYNA_EGEOM, "row bytes H*d*e = %lld is not a multiple of 16", (long long)row);
+  if (reinterpret_cast<uintptr_t>(device_base) % 256) return fail(DYNA_EINVAL, "device_base not 256-B aligned");
+  if (!err_word()) return fail(DYNA_ECUDA, "cannot allocate mapped error word");
+  cudaPointerAttributes attr{};
+  CUDA_TRY(cudaPointerGetAttributes(&attr, device_base));
+  if (attr.type != cudaMemoryTypeDevice || attr.device != desc->device)
+    return fail(DYNA_EINVAL, "device_base is not device memory of device %d", desc->device);
+  auto* p = new dyna_kv_pool();
+  p->desc = *desc;
+  p->base = static_cast<char*>(device_base);
+  p->dev = desc->device;
+  p->row = row;
+  {
+    DeviceGuard g(desc->device);
+    if (cudaMalloc(&p->inbox, kInboxBytes) != cudaSuccess || cudaMemset(p->inbox, 0, kInboxBytes) != cudaSuccess) {
+      delete p;
+      return fail(DYNA_ENOMEM, "cannot allocate the %zu B chunk-flag inbox", kInboxBytes);
+    }
+  }
+  p->own_inbox = true;
+  dev_info(desc->device);
+  *out = p;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_pool_destroy(dyna_kv_pool_t p) {
+  if (!p) return fail(DYNA_EINVAL, "NULL pool");
+  {
+    DeviceGuard g(p->dev);
+    for (auto& kv : p->channels) {
+      for (auto& c : kv.second.counters) {
+        DeviceGuard g2(c.first);
+        cudaFree(c.second);
+      }
+      if (kv.second.sstage) {
+        DeviceGuard g2(kv.second.sdev);
+        cudaFree(kv.second.sstage);
+      }
+      if (kv.second.dstage) {
+        DeviceGuard g2(kv.second.ddev);
+        cudaFree(kv.second.dstage);
+      }
+    }
+    if (p->own_inbox) cudaFree(p->inbox);
+    if (p->imported) {
+      if (p->ipc_pool_map) cudaIpcCloseMemHandle(p->ipc_pool_map);
+      if (p->ipc_inbox_map) cudaIpcCloseMemHandle(p->ipc_inbox_map);
+    }
+  }
+  delete p;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_enable_peer(int32_t device, int32_t peer) { return ensure_peer(device, peer); }
+
+dyna_status dyna_kv_migrate(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                            int32_t chunk_tokens, struct CUstream_st* stream, dyna_kv_xfer_t* out) {
+  return dyna_kv_migrate_ex(src, dst, tr, lr, chunk_tokens, stream, nullptr, out);
+}
+
+dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                               int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
+                               dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  if (!src.pool || !dst.pool) return fail(DYNA_EINVAL, "NULL pool in a block table");
+  dyna_kv_opts o{};
+  if (opts) o = *opts;
+  if (o.variant < 0 || o.variant > 2 || o.engine < 0 || o.engine > 2 || o.max_ctas < 0 || o.piece_bytes < 0 ||
+      o.piece_bytes % 16 || o.stages < 0 || o.stages > kMaxStages)
+    return fail(DYNA_EINVAL, "invalid dyna_kv_opts");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  dyna_kv_pool* S = src.pool;
+  dyna_kv_pool* D = dst.pool;
+  const dyna_kv_pool_desc &gs = S->desc, &gd = D->desc;
+  if (gs.num_layers != gd.num_layers || gs.num_kv_heads != gd.num_kv_heads || gs.head_dim != gd.head_dim ||
+      gs.elem_bytes != gd.elem_bytes)
+    return fail(DYNA_EGEOM, "source and destination geometry differ (L, H, d, e)");
+  if (lr.begin < 0 || lr.begin > lr.end || lr.end > gs.num_layers)
+    return fail(DYNA_ERANGE, "layer range [%lld, %lld) outside [0, %d)", (long long)lr.begin, (long long)lr.end,
+                gs.num_layers);
+  if (tr.begin < 0 || tr.begin > tr.end) return fail(DYNA_ERANGE, "bad token range");
+  const bool empty = tr.begin == tr.end || lr.begin == lr.end;
+  if (!empty) {
+    if (chunk_tokens <= 0) return fail(DYNA_ERANGE, "chunk_tokens must be > 0");
+    if (tr.end > src.len * gs.block_size || tr.end > dst.len * gd.block_size)
+      return fail(DYNA_ERANGE, "token range end %lld exceeds a block table (src %lld, dst %lld tokens)",
+                  (long long)tr.end, (long long)(src.len * gs.block_size), (long long)(dst.len * gd.block_size));
+    if (!src.block_ids || !dst.block_ids) return fail(DYNA_EINVAL, "NULL device block_ids");
+    dyna_status r = check_host_tables(src, dst, tr.begin, tr.end);
+    if (r) return r;
+  }
+  const int64_t ntok = tr.end - tr.begin;
+  const int64_t nchunks = empty ? 0 : (ntok + chunk_tokens - 1) / chunk_tokens;
+  const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
+  if (signal && nchunks > DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks, DYNA_MAX_CHUNKS);
+
+  auto* x = new dyna_kv_xfer();
+  x->dev = S->dev;
+  x->sender = gs.instance;
+  x->nchunks = (int32_t)nchunks;
+  if (empty) {  // s = 0 (or no layers) -> nothing to ship, nothing enqueued
+    x->empty = true;
+    *out = x;
+    return DYNA_OK;
+  }
+  // reachability of the destination from the source device
+  if (D->imported) {
+    if (D->dev != S->dev) {
+      delete x;
+      return fail(DYNA_EPEER, "imported destination is mapped on device %d, source is on %d", D->dev, S->dev);
+    }
+  } else if (D->dev != S->dev) {
+    dyna_status r = ensure_peer(S->dev, D->dev);
+    if (r) {
+      delete x;
+      return r;
+    }
+  }
+  if (!err_word()) {
+    delete x;
+    return fail(DYNA_ECUDA, "no error word");
+  }
+
+  const int64_t row = S->row;
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  const int64_t c = chunk_tokens;
+  const int variant = o.variant == DYNA_VARIANT_AUTO ? DYNA_VARIANT_FUSED : o.variant;
+  const int engine = o.engine == DYNA_ENGINE_AUTO ? DYNA_ENGINE_VEC : o.engine;
+  const int piece = o.piece_bytes ? o.piece_bytes : (engine == DYNA_ENGINE_BULK ? kBulkPiece : kVecPiece);
+  const int stages = o.stages ? o.stages : kBulkStages;
+
+  DeviceGuard guard(S->dev);
+  dyna_status r = DYNA_OK;
+  if (variant == DYNA_VARIANT_FUSED) {
+    // K4 / K4-local: source rows -> destination rows, one launch for all chunks.
+    const int64_t g = gcd64(gs.block_size, gd.block_size);
+    Plan p = make_plan(paged(S, src.block_ids), paged(D, dst.block_ids), row, tr.begin, tr.end, l0, lm, c, g, piece);
+    if (signal) {
+      if ((r = channel_counters(S, D, S->dev, &p.counters))) {
+        delete x;
+        return r;
+      }
+      p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
+      p.epoch = x->epoch = next_epoch(gs.instance, D);
+    }
+    r = launch_copy(p, engine, o.max_ctas, stages, S->dev, stream);
+  } else {
+    // Staged: K1 gather -> staging slot, K2 slot -> destination-side slot,
+    // K3 scatter slot -> destination rows.  Chunks are cut into sub-chunks
+    // that fit one staging slot; two slots per side alternate.
+    const bool cross = D->dev != S->dev;
+    if (D->imported) {
+      delete x;
+      return fail(DYNA_ENOTSUP, "STAGED variant into an imported (cross-process) pool is not supported; use FUSED");
+    }
+    DevInfo* ddi = dev_info(D->dev);
+    cudaStream_t dstream = stream;
+    if (cross) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      if (!ddi->aux) {
+        DeviceGuard g(D->dev);
+        CUDA_TRY(cudaStreamCreateWithFlags(&ddi->aux, cudaStreamNonBlocking));
+      }
+      dstream = ddi->aux;
+    }
+    const int64_t tok_bytes = row * lm * 2;
+    const int64_t sc = std::max<int64_t>(1, std::min<int64_t>(c, kStageSlotBytes / tok_bytes));
+    const int64_t slot = sc * tok_bytes;
+    char *sbuf = nullptr, *dbuf = nullptr;
+    if ((r = channel_staging(S, D, slot, &sbuf, &dbuf))) {
+      delete x;
+      return r;
+    }
+    unsigned long long* counters = nullptr;
+    if (signal) {
+      if ((r = channel_counters(S, D, D->dev, &counters))) {
+        delete x;
+        return r;
+      }
+      x->epoch = next_epoch(gs.instance, D);
+    }
+    cudaEvent_t done_src[2] = {nullptr, nullptr};  // K2 of slot i finished (cross-device)
+    cudaEvent_t done_dst[2] = {nullptr, nullptr};  // K3 of slot i finished (cross-device)
+    if (cross)
+      for (int i = 0; i < 2; ++i) {
+        CUDA_TRY(get_event(S->dev, &done_src[i]));
+        DeviceGuard g(D->dev);
+        CUDA_TRY(get_event(D->dev, &done_dst[i]));
+      }
+    int64_t sub = 0;
+    for (int64_t k = 0; k < nchunks && !r; ++k) {
+      const int64_t a = tr.begin + k * c, b = std::min(a + c, tr.end);
+      for (int64_t sa = a; sa < b && !r; sa += sc, ++sub) {
+        const int64_t sb = std::min(sa + sc, b);
+        const int si = (int)(sub & 1);
+        char* sslot = sbuf + si * slot;
+        char* dslot = dbuf + si * slot;
+        if (cross && sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[si], 0));
+        Plan k1 = make_plan(paged(S, src.block_ids), linear(sslot), row, sa, sb, l0, lm, sb - sa, gs.block_size, piece);
+        if ((r = launch_copy(k1, engine, o.max_ctas, stages, S->dev, stream))) break;
+        // K2: the sub-chunk slot is [lm][2][n][row] = two contiguous halves
+        // (K and V of all layers): a flat plan with one token of `half` bytes.
+        Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
+        if ((r = launch_copy(k2, engine, o.max_ctas, stages, S->dev, stream))) break;
+        Plan k3 = make_plan(linear(dslot), paged(D, dst.block_ids), row, sa, sb, l0, lm, sb - sa, gd.block_size, piece);
+        k3.mig_t0 = tr.begin;
+        k3.mig_t1 = tr.end;
+        k3.sig_c = (int32_t)c;
+        if (signal) {
+          k3.counters = counters;
+          k3.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
+          k3.epoch = x->epoch;
+        }
+        if (cross) {
+          CUDA_TRY(cudaEventRecord(done_src[si], stream));
+          DeviceGuard g(D->dev);
+          CUDA_TRY(cudaStreamWaitEvent(dstream, done_src[si], 0));
+          if ((r = launch_copy(k3, engine, o.max_ctas, stages, D->dev, dstream))) break;
+          CUDA_TRY(cudaEventRecord(done_dst[si], dstream));
+        } else {
+          if ((r = launch_copy(k3, engine, o.max_ctas, stages, S->dev, stream))) break;
+        }
+      }
+    }
+    if (cross) {  // the migration completes on `stream` once the last scatters are done
+      const int last = (int)((sub - 1) & 1);
+      CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[last], 0));
+      if (sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[last ^ 1], 0));
+      for (int i = 0; i < 2; ++i) {
+        put_event(S->dev, done_src[i]);
+        put_event(D->dev, done_dst[i]);
+      }
+    }
+  }
+  if (r) {
+    delete x;
+    return r;
+  }
+  cudaError_t e = get_event(S->dev, &x->ev);
+  if (e == cudaSuccess) e = cudaEventRecord(x->ev, stream);
+  if (e != cudaSuccess) {
+    delete x;
+    return fail(DYNA_ECUDA, "event record: %s", cudaGetErrorString(e));
+  }
+  *out = x;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_query(dyna_kv_xfer_t x) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (x->empty) return DYNA_OK;
+  cudaError_t e = cudaEventQuery(x->ev);
+  if (e == cudaSuccess) return DYNA_OK;
+  if (e == cudaErrorNotReady) return DYNA_EAGAIN;
+  return fail(DYNA_ECUDA, "%s", cudaGetErrorString(e));
+}
+
+dyna_status dyna_kv_wait(dyna_kv_xfer_t x) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  dyna_status r = DYNA_OK;
+  if (!x->empty) {
+    cudaError_t e = cudaEventSynchronize(x->ev);
+    if (e != cudaSuccess) r = fail(DYNA_ECUDA, "migration failed: %s", cudaGetErrorString(e));
+    put_event(x->dev, x->ev);
+    if (!r) r = take_device_error();
+  }
+  delete x;
+  return r;
+}
+
+dyna_status dyna_kv_stream_wait(dyna_kv_xfer_t x, struct CUstream_st* stream) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (x->empty) return DYNA_OK;
+  CUDA_TRY(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), x->ev, 0));
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t x, uint64_t* epoch, int32_t* num_chunks, int32_t* sender) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (epoch) *epoch = x->epoch;
+  if (num_chunks) *num_chunks = x->nchunks;
+  if (sender) *sender = x->sender;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_stream_wait_chunk(dyna_kv_pool_t dst, int32_t sender, int32_t chunk, uint64_t epoch,
+                                      uint64_t timeout_ns, struct CUstream_st* stream) {
+  if (!dst) return fail(DYNA_EINVAL, "NULL pool");
+  if (dst->imported) return fail(DYNA_EINVAL, "wait on the owner's side: this pool is an imported mapping");
+  if (sender < 0 || sender >= DYNA_MAX_INSTANCES || chunk < 0 || chunk >= DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "sender/chunk out of range");
+  if (!err_word()) return fail(DYNA_ECUDA, "no error word");
+  DeviceGuard g(dst->dev);
+  k_wait_flag<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      dst->inbox + (size_t)sender * DYNA_MAX_CHUNKS + chunk, epoch, timeout_ns, g_err_word);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_copy_flags(dyna_kv_pool_t dst, int32_t sender, int32_t first, int32_t n, uint64_t* host_out,
+                               struct CUstream_st* stream) {
+  if (!dst || !host_out) return fail(DYNA_EINVAL, "NULL argument");
+  if (sender < 0 || sender >= DYNA_MAX_INSTANCES || first < 0 || n < 0 || first + n > DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "sender/chunk range out of range");
+  if (n == 0) return DYNA_OK;
+  DeviceGuard g(dst->dev);
+  CUDA_TRY(cudaMemcpyAsync(host_out, dst->inbox + (size_t)sender * DYNA_MAX_CHUNKS + first,
+                           sizeof(uint64_t) * (size_t)n, cudaMemcpyDeviceToHost,
+                           reinterpret_cast<cudaStream_t>(stream)));
+  return DYNA_OK;
+}
+
+// ---------------------------------------------------------------- IPC
+typedef int (*PFN_cuMemGetAddressRange)(unsigned long long*, size_t*, unsigned long long);
+
+dyna_status dyna_kv_pool_export(dyna_kv_pool_t p, dyna_kv_ipc_handle* out) {
+  if (!p || !out) return fail(DYNA_EINVAL, "NULL argument");
+  if (p->imported) return fail(DYNA_EINVAL, "cannot re-export an imported pool");
+  std::memset(out, 0, sizeof *out);
+  DeviceGuard g(p->dev);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+  if (!fn) return fail(DYNA_ENOTSUP, "cuMemGetAddressRange unavailable");
+  unsigned long long alloc_base = 0;
+  size_t alloc_size = 0;
+  if (reinterpret_cast<PFN_cuMemGetAddressRange>(fn)(&alloc_base, &alloc_size,
+                                                    reinterpret_cast<unsigned long long>(p->base)) != 0)
+    return fail(DYNA_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h{};
+  CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(alloc_base)));
+  static_assert(sizeof(h) <= 64, "ipc handle size");
+  std::memcpy(out->pool_mem, &h, sizeof h);
+  out->pool_offset = reinterpret_cast<unsigned long long>(p->base) - alloc_base;
+  cudaIpcMemHandle_t hi{};
+  CUDA_TRY(cudaIpcGetMemHandle(&hi, p->inbox));
+  std::memcpy(out->inbox_mem, &hi, sizeof hi);
+  out->desc = p->desc;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_pool_import(const dyna_kv_ipc_handle* h, int32_t local_device, dyna_kv_pool_t* out) {
+  if (!h || !out) return fail(DYNA_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (!desc_valid(&h->desc)) return fail(DYNA_EINVAL, "invalid descriptor in handle");
+  DeviceGuard g(local_device);
+  cudaIpcMemHandle_t hp{}, hi{};
+  std::memcpy(&hp, h->pool_mem, sizeof hp);
+  std::memcpy(&hi, h->inbox_mem, sizeof hi);
+  void *mp = nullptr, *mi = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&mp, hp, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(DYNA_EPEER, "cudaIpcOpenMemHandle(pool): %s", cudaGetErrorString(e));
+  e = cudaIpcOpenMemHandle(&mi, hi, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaIpcCloseMemHandle(mp);
+    return fail(DYNA_EPEER, "cudaIpcOpenMemHandle(inbox): %s", cudaGetErrorString(e));
+  }
+  auto* p = new dyna_kv_pool();
+  p->desc = h->desc;
+  p->base = static_cast<char*>(mp) + h->pool_offset;
+  p->dev = local_device;
+  p->imported = true;
+  p->ipc_pool_map = mp;
+  p->ipc_inbox_map = mi;
+  p->inbox = static_cast<unsigned long long*>(mi);
+  p->row = (int64_t)h->desc.num_kv_heads * h->desc.head_dim * h->desc.elem_bytes;
+  if (!err_word()) {
+    dyna_kv_pool_destroy(p);
+    return fail(DYNA_ECUDA, "no error word");
+  }
+  dev_info(local_device);
+  *out = p;
+  return DYNA_OK;
+}
+
+// ---------------------------------------------------------------- test-input generator
+dyna_status dyna_kv_debug_fill(void* dst, uint64_t bytes, uint64_t seed, uint64_t byte_offset,
+                               struct CUstream_st* stream) {
+  if (!dst || bytes % 16 || byte_offset % 8 || reinterpret_cast<uintptr_t>(dst) % 16)
+    return fail(DYNA_EINVAL, "fill: dst 16-B aligned, bytes multiple of 16, offset multiple of 8");
+  if (bytes == 0) return DYNA_OK;
+  cudaPointerAttributes attr{};
+  CUDA_TRY(cudaPointerGetAttributes(&attr, dst));
+  const int dev = attr.device;
+  DevInfo* di = dev_info(dev);
+  DeviceGuard g(dev);
+  const unsigned long long key = [](unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }(seed);
+  const uint64_t n16 = bytes / 16;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n16 + 255) / 256, (uint64_t)di->sms * 8);
+  k_fill<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(static_cast<ulonglong2*>(dst), n16, key,
+                                                                   byte_offset / 8);
+  CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,354 @@
+// dyna_kv_kernels.cuh — sm_100a kernels of the chunked KV-cache migration.
+//
+// One templated copy-kernel family covers the paper's push (§4.3,
+// P:556) in all its shapes:
+//   K4 / K4-local  paged src  -> paged dst   (fused; dst local or NVLink peer)
+//   K1 gather      paged src  -> linear staging slot
+//   K2 transfer    linear     -> linear (peer staging)
+//   K3 scatter     linear     -> paged dst
+// Two copy engines share one work decomposition:
+//   VEC   one warp per work item; 16-B vector loads (ld.global.nc) issued in
+//         an unrolled batch, then 16-B stores.
+//   BULK  one elected thread per CTA drives TMA bulk copies
+//         (cp.async.bulk global->smem completing on an mbarrier, then
+//         smem->global as a bulk group) through a multi-stage smem ring.
+// The payload is never interpreted: every byte is copied untouched (DESIGN.md
+// reading R8), so there is no arithmetic and no tensor-core work.
+//
+// Work decomposition (step a1, computed on the device from the item index;
+// no host-side descriptor list):
+//   chunk k   = tokens [t0 + k*c, min(t0 + (k+1)*c, t1))               (R5)
+//   run j     = chunk ∩ [G*g, (G+1)*g), G = floor(a_k / g) + j.  g divides
+//               both block sizes, so a run is one contiguous byte range in
+//               the source AND in the destination.
+//   piece p   = bytes [p*piece, (p+1)*piece) of the run
+//   item      = (k, l, kv, j, p), chunk-major so chunk 0 completes first.
+#pragma once
+#include <cstdint>
+
+namespace dynakv {
+
+struct Side {
+  char* base;            // pool base, or staging base for a linear side
+  const int32_t* table;  // block table (paged side); nullptr for a linear side
+  int64_t nb;            // blocks in the pool (paged side)
+  int32_t bs;            // tokens per block (paged side)
+  int32_t linear;        // 1: staging layout [l-l0][kv][t-a][row] of one chunk
+};
+
+struct Plan {
+  Side src, dst;
+  int64_t row;              // bytes of one token's K or V in one layer (multiple of 16)
+  int64_t t0, t1;           // token range of this launch
+  int32_t l0, lm;           // first layer, number of layers
+  int32_t c;                // chunk tokens
+  int32_t g;                // run grid in tokens
+  int32_t R;                // max runs per chunk
+  int32_t P;                // pieces per run
+  int32_t piece;            // bytes per piece (multiple of 16)
+  int32_t nchunks;
+  int64_t items_per_chunk;  // lm * 2 * R * P
+  int64_t n_items;          // nchunks * items_per_chunk
+  // The migration's own chunking (a launch may cover a sub-range of it,
+  // e.g. one staging sub-chunk): flags and counters are per migration chunk.
+  int64_t mig_t0, mig_t1;   // the whole migration's token range
+  int32_t sig_c;            // the migration's chunk tokens
+  // per-chunk completion signal (counters == nullptr: none)
+  unsigned long long* counters;  // on the launching device, self-resetting
+  unsigned long long* flags;     // destination inbox row of this sender
+  unsigned long long epoch;
+  unsigned int* err;             // deferred error word (mapped host memory)
+};
+
+enum : unsigned { ERR_BAD_BLOCK = 1u, ERR_TIMEOUT = 2u };
+
+struct Item {
+  const char* src;
+  char* dst;
+  uint32_t n;    // bytes to copy (multiple of 16); 0 = nothing to copy
+  uint32_t acc;  // bytes this item accounts for in its chunk (== n unless skipped)
+  int32_t k;     // chunk index within the migration
+};
+
+__device__ __forceinline__ int64_t side_row(const Side& s, const Plan& p, int l, int kv, int64_t t,
+                                            int64_t a, int64_t clen, bool& bad) {
+  if (s.linear) return (((int64_t)(l - p.l0) * 2 + kv) * clen + (t - a)) * p.row;
+  const int64_t jb = t / s.bs;
+  const int32_t b = __ldg(s.table + jb);
+  if (b < 0 || (int64_t)b >= s.nb) { bad = true; return 0; }
+  return ((((int64_t)l * 2 + kv) * s.nb + b) * s.bs + (t - jb * s.bs)) * p.row;
+}
+
+__device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
+  Item it{nullptr, nullptr, 0u, 0u, 0};
+  const int64_t k = item / p.items_per_chunk;
+  int64_t i = item - k * p.items_per_chunk;
+  const int32_t pp = (int32_t)(i % p.P); i /= p.P;
+  const int32_t j = (int32_t)(i % p.R);  i /= p.R;
+  const int kv = (int)(i & 1);
+  const int l = p.l0 + (int)(i >> 1);
+  const int64_t a = p.t0 + k * p.c;
+  const int64_t b = min(a + (int64_t)p.c, p.t1);
+  const int64_t G = a / p.g + j;
+  const int64_t ta = max(a, G * p.g);
+  const int64_t tb = min(b, (G + 1) * p.g);
+  it.k = (int32_t)((a - p.mig_t0) / p.sig_c);
+  if (ta >= tb) return it;
+  const int64_t run = (tb - ta) * p.row;
+  const int64_t off = (int64_t)pp * p.piece;
+  if (off >= run) return it;
+  const uint32_t n = (uint32_t)min((int64_t)p.piece, run - off);
+  it.acc = n;
+  bool bad = false;
+  const int64_t so = side_row(p.src, p, l, kv, ta, a, b - a, bad);
+  const int64_t dO = side_row(p.dst, p, l, kv, ta, a, b - a, bad);
+  if (bad) {  // out-of-range block id: skip these rows, report at dyna_kv_wait
+    if (p.err) atomicOr(p.err, ERR_BAD_BLOCK);
+    return it;
+  }
+  it.src = p.src.base + so + off;
+  it.dst = p.dst.base + dO + off;
+  it.n = n;
+  return it;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* ptr, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ptr), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* ptr) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
+// Bytes of global chunk k of the whole migration.
+__device__ __forceinline__ unsigned long long chunk_bytes(const Plan& p, int32_t k) {
+  const int64_t a = p.mig_t0 + (int64_t)k * p.sig_c;
+  const int64_t b = min(a + (int64_t)p.sig_c, p.mig_t1);
+  return (unsigned long long)((b - a) * p.row * p.lm * 2);
+}
+
+// Called by ONE thread once an item's bytes are complete and visible at
+// system scope (the caller fenced).  The thread that closes chunk k resets
+// the counter (self-cleaning channel) and releases the flag.
+__device__ __forceinline__ void account_chunk(const Plan& p, int32_t k, uint32_t n) {
+  if (n == 0) return;
+  unsigned long long* ctr = p.counters + k;
+  const unsigned long long total = chunk_bytes(p, k);
+  const unsigned long long old = atomicAdd(ctr, (unsigned long long)n);
+  if (old + n == total) {
+    *ctr = 0ull;
+    __threadfence_system();
+    st_release_sys(p.flags + k, p.epoch);
+  }
+}
+
+// ------------------------------------------------------------------ VEC engine
+__device__ __forceinline__ int4 ld_nc_v4(const int4* ptr) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr));
+  return r;
+}
+__device__ __forceinline__ void st_v4(int4* ptr, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// A warp copies n bytes (multiple of 16): U 16-B loads per lane in flight.
+template <int U>
+__device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __restrict__ dst, uint32_t n,
+                                          int lane) {
+  const int4* s = reinterpret_cast<const int4*>(src);
+  int4* d = reinterpret_cast<int4*>(dst);
+  const uint32_t nv = n >> 4;
+  uint32_t base = 0;
+  for (; base + 32 * U <= nv; base += 32 * U) {
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ld_nc_v4(s + base + u * 32 + lane);
+#pragma unroll
+    for (int u = 0; u < U; ++u) st_v4(d + base + u * 32 + lane, v[u]);
+  }
+  if (base < nv) {
+    int4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t idx = base + u * 32 + lane;
+      if (idx < nv) v[u] = ld_nc_v4(s + idx);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t idx = base + u * 32 + lane;
+      if (idx < nv) st_v4(d + idx, v[u]);
+    }
+  }
+}
+
+template <int U, bool SIGNAL>
+__global__ void __launch_bounds__(256) k_copy_vec(const Plan p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t item = warp; item < p.n_items; item += nwarps) {
+    const Item it = decode_item(p, item);
+    if (it.n) warp_copy<U>(it.src, it.dst, it.n, lane);
+    if (SIGNAL && it.acc) {
+      __threadfence_system();  // every lane's stores visible system-wide ...
+      __syncwarp();            // ... before lane 0 counts them
+      if (lane == 0) account_chunk(p, it.k, it.acc);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ BULK engine
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(ptr));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int kMaxStages = 16;
+
+// One thread per CTA drives a ring of `stages` smem slots of p.piece bytes:
+// up to stages-1 loads in flight while the oldest slot drains to global.
+template <bool SIGNAL>
+__global__ void __launch_bounds__(32) k_copy_bulk(const Plan p, int stages) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ char* pend_dst[kMaxStages];
+  __shared__ uint32_t pend_n[kMaxStages];
+  __shared__ int32_t pend_k[kMaxStages];
+  if (threadIdx.x != 0) return;
+
+  for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+  int64_t next = blockIdx.x;
+  const int64_t stride = gridDim.x;
+
+  // Load the next non-empty item of this CTA into slot s (pend_n[s] = 0 if none).
+  auto refill = [&](int s) {
+    while (next < p.n_items) {
+      const Item it = decode_item(p, next);
+      next += stride;
+      if (it.n == 0) {
+        if (SIGNAL && it.acc) account_chunk(p, it.k, it.acc);  // skipped (bad id): still closes the chunk
+        continue;
+      }
+      mbar_expect_tx(&full[s], it.n);
+      bulk_load(ring + (size_t)s * p.piece, it.src, it.n, &full[s]);
+      pend_dst[s] = it.dst;
+      pend_n[s] = it.n;
+      pend_k[s] = it.k;
+      return;
+    }
+    pend_n[s] = 0;
+  };
+
+  for (int s = 0; s < stages; ++s) refill(s);
+
+  int prev = -1;
+  for (int64_t iter = 0;; ++iter) {
+    const int s = (int)(iter % stages);
+    if (pend_n[s] == 0) break;
+    mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
+    bulk_store(pend_dst[s], ring + (size_t)s * p.piece, pend_n[s]);
+    bulk_commit();
+    if (prev >= 0) {
+      if (SIGNAL) {
+        bulk_wait_all<1>();  // the previous store's writes are complete
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence_system();
+        account_chunk(p, pend_k[prev], pend_n[prev]);
+      } else {
+        bulk_wait_read<1>();  // the previous store finished reading its slot
+      }
+      refill(prev);
+    }
+    prev = s;
+  }
+  bulk_wait_all<0>();
+  if (SIGNAL && prev >= 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __threadfence_system();
+    account_chunk(p, pend_k[prev], pend_n[prev]);
+  }
+}
+
+// ------------------------------------------------------------------ consumer-side chunk wait
+__global__ void k_wait_flag(const unsigned long long* flag, unsigned long long epoch,
+                            unsigned long long timeout_ns, unsigned int* err) {
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  while (ld_acquire_sys(flag) < epoch) {
+    if (timeout_ns) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t_start > timeout_ns) {
+        if (err) atomicOr(err, ERR_TIMEOUT);
+        return;
+      }
+    }
+    __nanosleep(256);
+  }
+}
+
+// ------------------------------------------------------------------ test-input generator (not the method)
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void k_fill(ulonglong2* dst, uint64_t n16, unsigned long long key, uint64_t first_word) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
+    const uint64_t w = first_word + 2 * i;
+    ulonglong2 v;
+    v.x = splitmix64(key ^ (w * 0xD1B54A32D192ED03ull));
+    v.y = splitmix64(key ^ ((w + 1) * 0xD1B54A32D192ED03ull));
+    dst[i] = v;
+  }
+}
+
+}  // namespace dynakv

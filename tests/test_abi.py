@@ -1,0 +1,88 @@
+"""The C-ABI library loads and exports every symbol include/dyna_kv.h declares
+(CPU only; no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "dyna_kv.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^DYNA_API [^(]*?\b(dyna_kv_\w+)\(", src, re.M)))
+
+
+def test_header_declares_the_north_star_calls():
+    syms = declared_symbols()
+    for s in ("dyna_kv_pool_create", "dyna_kv_migrate", "dyna_kv_wait"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2504_09285_b200 as dk
+    out = subprocess.run(["nm", "-D", "--defined-only", dk.LIB_PATH], capture_output=True, text=True, check=True)
+    exported = set(re.findall(r" T (dyna_kv_\w+)$", out.stdout, re.M))
+    missing = set(declared_symbols()) - exported
+    assert not missing, missing
+    # and the Python binding binds the same names
+    assert set(dk.EXPORTS) == set(declared_symbols())
+    for s in dk.EXPORTS:
+        assert hasattr(dk, s) and hasattr(dk.lib, s)
+
+
+def test_library_is_sm100a_only():
+    import paper_2504_09285_b200 as dk
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", dk.LIB_PATH], capture_output=True,
+                         text=True)
+    assert "sm_100a" in out.stdout
+    assert not re.search(r"sm_(?!100a)\d+", out.stdout)
+
+
+def test_sass_has_bulk_copies_and_vector_moves():
+    import paper_2504_09285_b200 as dk
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", dk.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    assert "UBLKCP" in sass          # TMA bulk copies (cp.async.bulk)
+    assert re.search(r"LDG\.E[.A-Z0-9]*\.128", sass)   # 16-B vector loads
+    assert re.search(r"STG\.E[.A-Z0-9]*\.128", sass)   # 16-B vector stores
+    assert "HMMA" not in sass and "UTCHMMA" not in sass  # no contraction on this path
+
+
+def test_struct_layouts_match_header():
+    import paper_2504_09285_b200 as dk
+    assert ctypes.sizeof(dk.dyna_kv_pool_desc) == 32
+    assert ctypes.sizeof(dk.dyna_block_table) == 32
+    assert ctypes.sizeof(dk.dyna_range) == 16
+    assert ctypes.sizeof(dk.dyna_kv_opts) == 24
+    assert ctypes.sizeof(dk.dyna_kv_ipc_handle) == 64 + 64 + 8 + 32
+
+
+def test_status_constants_match_header():
+    import paper_2504_09285_b200 as dk
+    src = open(HEADER).read()
+    for name, val in re.findall(r"#define (DYNA_E\w+|DYNA_OK)\s+\(?(-?\d+)\)?", src):
+        assert getattr(dk, name) == int(val), name
+
+
+def test_host_validation_without_gpu():
+    import paper_2504_09285_b200 as dk
+    bad = dk.dyna_kv_pool_desc(2, 2, 64, 2, 16, 64, 0, 0)
+    assert dk.dyna_kv_pool_bytes(bad) == 2 * 2 * 64 * 16 * 2 * 64 * 2
+    assert dk.dyna_kv_pool_bytes(dk.dyna_kv_pool_desc(0, 2, 64, 2, 16, 64, 0, 0)) == 0
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_pool_create(bad, 0)
+    assert e.value.status == dk.DYNA_EINVAL
+    # row bytes not a multiple of 16 -> EGEOM before touching the device
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_pool_create(dk.dyna_kv_pool_desc(1, 1, 3, 2, 16, 4, 0, 0), 256)
+    assert e.value.status == dk.DYNA_EGEOM
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_migrate(dk.dyna_block_table(), dk.dyna_block_table(), (0, 1), (0, 1), 1)
+    assert e.value.status == dk.DYNA_EINVAL
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_wait(0)
+    assert e.value.status == dk.DYNA_EINVAL

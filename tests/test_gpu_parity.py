@@ -1,0 +1,266 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit for bit.
+
+Small and medium geometries are compared element by element (whole pools)
+against oracle.migrate on the same kvgen inputs.  Full BASELINE.json sizes
+(in the launch configuration bench.py times) are checked on sampled rows the
+oracle maps one by one, plus properties that hold at any size (every mapped
+row equal through both tables; every other row untouched).
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import kvgen
+import oracle
+import paper_2504_09285_b200 as dk
+from kvgen import Geom
+from tests.gpu_util import (dev_table, mapped_mask, migrate_and_wait, pool_filled, pool_from_host,
+                            sampled_rows_match, torch_rows_equal, untouched_equal)
+
+pytestmark = pytest.mark.gpu
+
+ENGINES = [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK]
+VARIANTS = [dk.DYNA_VARIANT_FUSED, dk.DYNA_VARIANT_STAGED]
+
+
+def _parity(gs, gd, n_tok, tr, lr, c, seed=1, table_kind="fragmented", **kw):
+    ts, td = kvgen.table_pair(seed + 100, n_tok, gs, gd, table_kind)
+    hs, hd = kvgen.fill_bytes(seed, gs.pool_bytes), kvgen.fill_bytes(seed + 1, gd.pool_bytes)
+    want = hd.copy()
+    oracle.migrate(hs, gs, ts, want, gd, td, tr, lr)
+    src, dst = pool_from_host(gs, hs), pool_from_host(gd, hd)
+    migrate_and_wait(src, ts, dst, td, tr, lr, c, **kw)
+    got = dst.tensor.cpu().numpy()
+    assert np.array_equal(src.tensor.cpu().numpy(), hs), "source pool modified"
+    if not np.array_equal(got, want):
+        diff = np.flatnonzero(got != want)
+        pytest.fail(f"{len(diff)} bytes differ; first at {diff[0]} (row {diff[0] // gs.row_bytes})")
+
+
+def test_device_fill_matches_kvgen():
+    g = kvgen.TOY
+    p = pool_filled(g, 1234)
+    torch.cuda.synchronize()
+    assert np.array_equal(p.tensor.cpu().numpy(), kvgen.fill_bytes(1234, g.pool_bytes))
+    buf = torch.empty(4096, dtype=torch.uint8, device="cuda")
+    dk.dyna_kv_debug_fill(buf.data_ptr(), 4096, 99, 8 * 1000, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(buf.cpu().numpy(), kvgen.bytes_at(99, 8 * 1000, 4096))
+
+
+# ------------------------------------------------ config 1 (toy), every variant / engine / chunk size
+@pytest.mark.parametrize("variant,engine", list(itertools.product(VARIANTS, ENGINES)))
+@pytest.mark.parametrize("c", [1, 15, 16, 17, 32, 64, 100, 1000])
+def test_toy_config(variant, engine, c):
+    _parity(kvgen.TOY, kvgen.TOY, 256, (0, 100), (0, 2), c, variant=variant, engine=engine)
+
+
+@pytest.mark.parametrize("variant,engine", list(itertools.product(VARIANTS, ENGINES)))
+@pytest.mark.parametrize("tr,lr", [((37, 100), (0, 2)), ((0, 100), (1, 2)), ((5, 6), (0, 1)), ((0, 256), (0, 2))])
+def test_toy_subranges(variant, engine, tr, lr):
+    _parity(kvgen.TOY, kvgen.TOY, 256, tr, lr, 32, variant=variant, engine=engine)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("bss,bsd", [(16, 32), (32, 16), (16, 24), (8, 16), (16, 16)])
+def test_reblocking(engine, bss, bsd):
+    gs = kvgen.TOY.with_(block_size=bss, num_blocks=64 * 16 // bss)
+    gd = kvgen.TOY.with_(block_size=bsd, num_blocks=64 * 16 // bsd + 8)
+    for variant in VARIANTS:
+        _parity(gs, gd, 256, (3, 201), (0, 2), 40, variant=variant, engine=engine)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_contiguous_tables(engine):
+    _parity(kvgen.TOY, kvgen.TOY, 256, (0, 256), (0, 2), 64, table_kind="contiguous", engine=engine)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("max_ctas", [1, 3, 150])
+def test_sm_budget(engine, max_ctas):
+    _parity(kvgen.TOY, kvgen.TOY, 256, (0, 100), (0, 2), 32, engine=engine, max_ctas=max_ctas)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("piece,stages", [(256, 2), (1024, 3), (4096, 16), (65536, 3)])
+def test_piece_and_stage_shapes(engine, piece, stages):
+    g = Geom(2, 8, 128, 2, 16, 64)  # row 2 KiB
+    _parity(g, g, 512, (0, 333), (0, 2), 128, engine=engine, piece_bytes=piece, stages=stages)
+
+
+# ------------------------------------------------ medium geometries: paper rows, several tiles, ragged tails
+LLAMA2_ROWS = Geom(3, 32, 128, 2, 16, 160)   # Llama-2-7B rows (8 KiB), 3 layers
+LLAMA3_ROWS = Geom(4, 8, 128, 2, 16, 400)    # Llama-3-8B GQA rows (2 KiB), 4 layers
+
+
+@pytest.mark.parametrize("s", [1, 15, 16, 17, 100, 1000, 2047, 2048])   # reading R12 edge sweep
+@pytest.mark.parametrize("variant,engine", list(itertools.product(VARIANTS, ENGINES)))
+def test_llama2_rows_split_sweep(s, variant, engine):
+    _parity(LLAMA2_ROWS, LLAMA2_ROWS, 2048, (0, s), (0, 3), 256, variant=variant, engine=engine)
+
+
+@pytest.mark.parametrize("variant,engine", list(itertools.product(VARIANTS, ENGINES)))
+@pytest.mark.parametrize("c", [512, 1000, 4096])
+def test_llama3_rows_ragged(variant, engine, c):
+    _parity(LLAMA3_ROWS, LLAMA3_ROWS.with_(num_blocks=420), 6000, (0, 5003), (0, 4), c,
+            variant=variant, engine=engine)
+
+
+# ------------------------------------------------ same pool, signalling, errors
+@pytest.mark.parametrize("engine", ENGINES)
+def test_same_pool_disjoint_blocks(engine):
+    g = kvgen.TOY
+    host = kvgen.fill_bytes(7, g.pool_bytes)
+    rng = np.random.default_rng(3)
+    perm = rng.permutation(g.num_blocks).astype(np.int32)
+    ts, td = perm[:7], perm[7:14]
+    want = host.copy()
+    oracle.migrate(host.copy(), g, ts, want, g, td, (0, 100))
+    p = pool_from_host(g, host)
+    migrate_and_wait(p, ts, p, td, (0, 100), (0, 2), 32, engine=engine)
+    assert np.array_equal(p.tensor.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("variant,engine", list(itertools.product(VARIANTS, ENGINES)))
+def test_signal_per_chunk_flags(variant, engine):
+    g = LLAMA3_ROWS
+    src, dst = pool_filled(g, 11, instance=5), pool_filled(g, 12)
+    ts, td = kvgen.table_pair(3, 3000, g, g)
+    s, c = 3000, 512
+    epochs = []
+    for rep in range(3):
+        x = dk.migrate(dev_table(src, ts), dev_table(dst, td), (0, s), (0, 4), c, variant=variant, engine=engine,
+                       flags=dk.DYNA_MIGRATE_SIGNAL)
+        epoch, nchunks, sender = dk.dyna_kv_xfer_info(x)
+        assert nchunks == -(-s // c) and sender == 5
+        epochs.append(epoch)
+        consumer = torch.cuda.Stream()
+        for k in range(nchunks):  # the destination waits chunk by chunk
+            dk.dyna_kv_stream_wait_chunk(dst.handle, sender, k, epoch, 5_000_000_000, consumer.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(consumer)
+        ev.synchronize()
+        dk.dyna_kv_poll_error()
+        assert torch_rows_equal(src, ts, dst, td, (0, s), (0, 4))
+        dk.dyna_kv_wait(x)
+    assert epochs == sorted(epochs) and len(set(epochs)) == 3
+
+
+def test_chunk_wait_times_out():
+    g = kvgen.TOY
+    dst = pool_filled(g, 1)
+    dk.dyna_kv_stream_wait_chunk(dst.handle, 3, 0, 1 << 40, 1_000_000, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_poll_error()
+    assert e.value.status == dk.DYNA_ETIMEDOUT
+
+
+def _expect(status, fn):
+    with pytest.raises(dk.DynaKVError) as e:
+        fn()
+    assert e.value.status == status, e.value
+
+
+def test_synchronous_errors():
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(1, 256, g, g)
+    T = lambda p, ids, h=True: dev_table(p, ids, h)  # noqa: E731
+    mig = lambda a, b, tr=(0, 100), lr=(0, 2), c=32: dk.migrate(a, b, tr, lr, c)  # noqa: E731
+    alias = td.copy()
+    alias[3] = alias[2]
+    _expect(dk.DYNA_EALIAS, lambda: mig(T(src, ts), T(dst, alias)))
+    _expect(dk.DYNA_ERANGE, lambda: mig(T(src, ts), T(dst, td), tr=(0, 257)))
+    _expect(dk.DYNA_ERANGE, lambda: mig(T(src, ts), T(dst, td), lr=(0, 3)))
+    _expect(dk.DYNA_ERANGE, lambda: mig(T(src, ts), T(dst, td), c=0))
+    bad = td.copy()
+    bad[1] = g.num_blocks
+    _expect(dk.DYNA_ERANGE, lambda: mig(T(src, ts), T(dst, bad)))
+    other = pool_filled(g.with_(num_kv_heads=1, head_dim=128), 3)
+    _expect(dk.DYNA_EGEOM, lambda: mig(T(src, ts), T(other, td)))
+    # same pool, overlapping rows
+    _expect(dk.DYNA_EALIAS, lambda: mig(T(src, ts), T(src, ts)))
+    # partially covered blocks may repeat if their rows do not overlap: token 16 of a 17-token range
+    # lands in entry 1 only; entry 0 and entry 1 are distinct rows even if... (here ids differ) -> OK
+    x = mig(T(src, ts), T(dst, td), tr=(0, 17))
+    dk.dyna_kv_wait(x)
+
+
+def test_device_side_bad_block_id():
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(1, 256, g, g)
+    bad = td.copy()
+    bad[2] = -5
+    for engine in ENGINES:
+        x = dk.migrate(dev_table(src, ts, False), dev_table(dst, bad, False), (0, 100), (0, 2), 32, engine=engine)
+        _expect(dk.DYNA_ERANGE, lambda: dk.dyna_kv_wait(x))
+
+
+def test_empty_ranges_enqueue_nothing():
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(1, 256, g, g)
+    torch.cuda.synchronize()
+    before = dst.tensor.clone()
+    n0 = dk.dyna_kv_launch_count()
+    for tr, lr in (((0, 0), (0, 2)), ((50, 50), (0, 2)), ((0, 100), (1, 1))):
+        x = dk.migrate(dev_table(src, ts), dev_table(dst, td), tr, lr, 32)
+        assert dk.dyna_kv_query(x)
+        dk.dyna_kv_wait(x)
+    assert dk.dyna_kv_launch_count() == n0
+    assert torch.equal(before, dst.tensor)
+
+
+# ------------------------------------------------ full BASELINE.json sizes
+def test_config2_llama2_7b_full_size():
+    """configs[1]: Llama-2-7B, 2k prompt split at 1024, chunk 256 — the bench.py workload (1-GPU reblock)."""
+    g = kvgen.LLAMA2_7B
+    src, dst = pool_filled(g, 21), pool_filled(g, 22)
+    ts, td = kvgen.table_pair(5, 2048, g, g)
+    migrate_and_wait(src, ts, dst, td, (0, 1024), (0, 32), 256)
+    assert torch_rows_equal(src, ts, dst, td, (0, 1024), (0, 32))
+    assert untouched_equal(dst, 22, mapped_mask(g, [(td, (0, 1024))]))
+    assert sampled_rows_match(21, g, ts, dst, g, td, (0, 1024), (0, 32), 300, np.random.default_rng(0)) == 0
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config3_llama3_skewed_batch_full_size(engine):
+    """configs[2]: Llama-3-8B, 64 requests with trace-like skew, 1-GPU reblock."""
+    g = kvgen.LLAMA3_8B
+    reqs = kvgen.migrating(kvgen.skewed_batch(1, 64))
+    tabs = kvgen.batch_tables(2, [r.s for r in reqs], g, g)
+    src, dst = pool_filled(g, 31), pool_filled(g, 32)
+    xs = [dk.migrate(dev_table(src, ts), dev_table(dst, td), (0, r.s), (0, 32), 256, engine=engine)
+          for r, (ts, td) in zip(reqs, tabs)]
+    for x in xs:
+        dk.dyna_kv_wait(x)
+    for r, (ts, td) in zip(reqs, tabs):
+        assert torch_rows_equal(src, ts, dst, td, (0, r.s), (0, 32))
+    assert untouched_equal(dst, 32, mapped_mask(g, [(td, (0, r.s)) for r, (ts, td) in zip(reqs, tabs)]))
+
+
+@pytest.mark.parametrize("c", [512, 1024, 2048, 4096])
+def test_config4_long_context_chunk_sweep(c):
+    """configs[3]: Llama-3-8B 32k-token prompt, chunk 512..4096 (1-GPU form)."""
+    g = kvgen.LLAMA3_8B.with_(num_blocks=4096)
+    src, dst = pool_filled(g, 41), pool_filled(g, 42)
+    ts, td = kvgen.table_pair(6, 32768, g, g)
+    migrate_and_wait(src, ts, dst, td, (0, 32768), (0, 32), c)
+    assert torch_rows_equal(src, ts, dst, td, (0, 32768), (0, 32))
+    assert untouched_equal(dst, 42, mapped_mask(g, [(td, (0, 32768))]))
+    assert sampled_rows_match(41, g, ts, dst, g, td, (0, 32768), (0, 32), 100, np.random.default_rng(c)) == 0
+
+
+def test_config5_qwen72b_shard_pair():
+    """configs[4] per-GPU shard shape (80 layers, 8 KV heads): one ordered pair, 1-GPU form."""
+    g = kvgen.QWEN2_72B.with_(num_blocks=1024)
+    src, dst = pool_filled(g, 51), pool_filled(g, 52)
+    reqs = kvgen.migrating(kvgen.skewed_batch(1000 + 1, 4))
+    tabs = kvgen.batch_tables(3, [r.s for r in reqs], g, g)
+    for r, (ts, td) in zip(reqs, tabs):
+        migrate_and_wait(src, ts, dst, td, (0, r.s), (0, 80), 1024)
+        assert torch_rows_equal(src, ts, dst, td, (0, r.s), (0, 80))
