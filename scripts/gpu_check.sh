@@ -1,0 +1,14 @@
+# GPU-box check: smoke, GPU tests, bench lines, ncu launch list + full capture.
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
+timeout 1500 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} 2>&1 | tail -30
+if [ -n "$NCU" ]; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv \
+      python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_bench.log 2>&1
+  for e in 1 2; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_copy -s 20 -c 2 -o gpurun_out/prof_e$e \
+        python bench.py --steps 20 --warmup 3 --no-cpu-baseline --engine $e > gpurun_out/ncu_full_e$e.log 2>&1
+  done
+fi
+timeout 300 python bench.py --steps 1000 --warmup 10 2>&1 | tail -2

@@ -16,7 +16,7 @@ import kvgen
 import oracle
 import paper_2504_09285_b200 as dk
 from kvgen import Geom
-from tests.gpu_util import (dev_table, mapped_mask, migrate_and_wait, pool_filled, pool_from_host,
+from gpu_util import (dev_table, mapped_mask, migrate_and_wait, pool_filled, pool_from_host,
                             sampled_rows_match, torch_rows_equal, untouched_equal)
 
 pytestmark = pytest.mark.gpu
