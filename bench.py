@@ -287,6 +287,21 @@ def run_dyna(args, rank, world, local_rank):
     assert int(flags_host.min()) == epoch, "chunk flags did not reach the last epoch"
     barrier()
 
+    # context for the roofline: torch's own copy_ of a contiguous buffer of the same payload size
+    a = torch.empty(payload, dtype=torch.uint8, device=f"cuda:{dev}")
+    b = torch.empty_like(a)
+    a.fill_(1)
+    ref_ms = []
+    for _ in range(20):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        e1.synchronize()
+        ref_ms.append(e0.elapsed_time(e1))
+    same_size_copy = 2 * payload / (statistics.median(ref_ms[5:]) / 1e3) / 1e9
+    del a, b
+
     if rank == 0:
         hbm_peak, hbm_src = load_peaks()
         gbps = world * args.steps * payload / (total_ms / 1e3) / 1e9
@@ -296,7 +311,8 @@ def run_dyna(args, rank, world, local_rank):
                     "traffic": ncu_traffic(), "peak_source": hbm_src,
                     "kernel": "dynakv::k_copy_vec (K4-local fused reblock)" if args.engine != dk.DYNA_ENGINE_BULK
                     else "dynakv::k_copy_bulk (K4-local fused reblock)",
-                    "algorithmic_bytes_per_launch": 2 * payload, "kernel_ms": kern_ms}
+                    "algorithmic_bytes_per_launch": 2 * payload, "kernel_ms": kern_ms,
+                    "same_size_torch_copy_gbs": same_size_copy}
         else:
             achieved = payload / (kern_ms / 1e3) / 1e9      # bytes crossing NVLink per launch / duration
             roof = {"bound": "nvlink", "achieved": achieved, "peak": NVLINK_MEASURED, "unit": "GB/s",

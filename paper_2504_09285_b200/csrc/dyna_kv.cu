@@ -545,6 +545,7 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
       }
       p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
       p.epoch = x->epoch = next_epoch(gs.instance, D);
+      p.sys_fence = (D->dev != S->dev || D->imported) ? 1 : 0;
     }
     r = launch_copy(p, engine, o.max_ctas, stages, S->dev, stream);
   } else {

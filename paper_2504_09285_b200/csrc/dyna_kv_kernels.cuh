@@ -57,6 +57,7 @@ struct Plan {
   unsigned long long* counters;  // on the launching device, self-resetting
   unsigned long long* flags;     // destination inbox row of this sender
   unsigned long long epoch;
+  int32_t sys_fence;             // 1: destination on another GPU (fence at system scope)
   unsigned int* err;             // deferred error word (mapped host memory)
 };
 
@@ -128,8 +129,12 @@ __device__ __forceinline__ unsigned long long chunk_bytes(const Plan& p, int32_t
   return (unsigned long long)((b - a) * p.row * p.lm * 2);
 }
 
+__device__ __forceinline__ void fence_for(const Plan& p) {
+  if (p.sys_fence) __threadfence_system(); else __threadfence();
+}
+
 // Called by ONE thread once an item's bytes are complete and visible at
-// system scope (the caller fenced).  The thread that closes chunk k resets
+// the destination's scope (the caller fenced).  The thread that closes chunk k resets
 // the counter (self-cleaning channel) and releases the flag.
 __device__ __forceinline__ void account_chunk(const Plan& p, int32_t k, uint32_t n) {
   if (n == 0) return;
@@ -192,14 +197,29 @@ __global__ void __launch_bounds__(256) k_copy_vec(const Plan p) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // Signalling: a warp's consecutive items mostly share a chunk (chunk-major
+  // order), so bytes are accumulated per chunk and fenced + counted once when
+  // the warp moves on to another chunk — one fence per (warp, chunk), not per item.
+  int32_t cur_k = -1;
+  uint32_t cur_acc = 0;
   for (int64_t item = warp; item < p.n_items; item += nwarps) {
     const Item it = decode_item(p, item);
-    if (it.n) warp_copy<U>(it.src, it.dst, it.n, lane);
-    if (SIGNAL && it.acc) {
-      __threadfence_system();  // every lane's stores visible system-wide ...
-      __syncwarp();            // ... before lane 0 counts them
-      if (lane == 0) account_chunk(p, it.k, it.acc);
+    if (SIGNAL && it.acc && it.k != cur_k) {
+      if (cur_acc) {
+        fence_for(p);   // every lane's stores of chunk cur_k are performed ...
+        __syncwarp();   // ... before lane 0 counts them
+        if (lane == 0) account_chunk(p, cur_k, cur_acc);
+      }
+      cur_k = it.k;
+      cur_acc = 0;
     }
+    if (it.n) warp_copy<U>(it.src, it.dst, it.n, lane);
+    if (SIGNAL) cur_acc += it.acc;
+  }
+  if (SIGNAL && cur_acc) {
+    fence_for(p);
+    __syncwarp();
+    if (lane == 0) account_chunk(p, cur_k, cur_acc);
   }
 }
 
@@ -287,31 +307,40 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Plan p, int stages) {
 
   for (int s = 0; s < stages; ++s) refill(s);
 
+  // Signalling: stores are counted per chunk; when the next store belongs to
+  // another chunk, wait for all outstanding stores of this CTA once, fence,
+  // and count the finished chunk's bytes.
+  int32_t cur_k = -1;
+  uint32_t cur_acc = 0;
   int prev = -1;
   for (int64_t iter = 0;; ++iter) {
     const int s = (int)(iter % stages);
     if (pend_n[s] == 0) break;
+    if (SIGNAL && pend_k[s] != cur_k) {
+      if (cur_acc) {
+        bulk_wait_all<0>();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        fence_for(p);
+        account_chunk(p, cur_k, cur_acc);
+      }
+      cur_k = pend_k[s];
+      cur_acc = 0;
+    }
     mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
     bulk_store(pend_dst[s], ring + (size_t)s * p.piece, pend_n[s]);
     bulk_commit();
+    if (SIGNAL) cur_acc += pend_n[s];
     if (prev >= 0) {
-      if (SIGNAL) {
-        bulk_wait_all<1>();  // the previous store's writes are complete
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence_system();
-        account_chunk(p, pend_k[prev], pend_n[prev]);
-      } else {
-        bulk_wait_read<1>();  // the previous store finished reading its slot
-      }
+      bulk_wait_read<1>();  // the previous store finished reading its slot
       refill(prev);
     }
     prev = s;
   }
   bulk_wait_all<0>();
-  if (SIGNAL && prev >= 0) {
+  if (SIGNAL && cur_acc) {
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    __threadfence_system();
-    account_chunk(p, pend_k[prev], pend_n[prev]);
+    fence_for(p);
+    account_chunk(p, cur_k, cur_acc);
   }
 }
 

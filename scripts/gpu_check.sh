@@ -1,4 +1,4 @@
-# GPU-box check: smoke, GPU tests, bench lines, ncu launch list + full capture.
+# GPU-box check: smoke, GPU tests, bench lines, optional ncu and overlap runs.
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
@@ -11,4 +11,6 @@ if [ -n "$NCU" ]; then
         python bench.py --steps 20 --warmup 3 --no-cpu-baseline --engine $e > gpurun_out/ncu_full_e$e.log 2>&1
   done
 fi
-timeout 300 python bench.py --steps 1000 --warmup 10 2>&1 | tail -2
+for e in 1 2; do timeout 300 python bench.py --steps 1000 --warmup 10 --engine $e --no-cpu-baseline 2>&1 | tail -1; done
+timeout 300 python bench.py --steps 1000 --warmup 10 2>&1 | tail -1 > gpurun_out/bench_default.json; cat gpurun_out/bench_default.json
+if [ -n "$OVERLAP" ]; then timeout 900 python scripts/overlap.py 2>&1 | tail -40; fi

@@ -1,0 +1,82 @@
+"""Cross-process path on one GPU: the destination instance exports its pool over
+CUDA IPC, the source instance (another process) imports it and pushes its
+request's KV into it with per-chunk flags (§3.1, §4.3).
+
+On the 8-GPU box the two processes sit on different GPUs and the same kernel
+stores over NVLink; here both map the same B200, which exercises the export /
+import / offset / inbox / system-scope-fence logic end to end.
+"""
+import multiprocessing as mp
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SRC_SEED, DST_SEED, SENDER = 71, 72, 3
+S, CHUNK = 3001, 512
+
+
+def _geom():
+    from kvgen import Geom
+    return Geom(4, 8, 128, 2, 16, 400)
+
+
+def _sender(handle: bytes, q, engine: int):
+    try:
+        import torch
+
+        import kvgen
+        import paper_2504_09285_b200 as dk
+        from gpu_util import dev_table, pool_filled
+        torch.cuda.set_device(0)
+        g = _geom()
+        src = pool_filled(g, SRC_SEED, instance=SENDER)
+        dst = dk.Pool.imported(handle, 0)
+        ts, td = kvgen.table_pair(9, 4000, g, g)
+        src_t = dev_table(src, ts)
+        dst_t = dk.table(dst, torch.from_numpy(td).cuda(), td)
+        x = dk.migrate(src_t, dst_t, (0, S), (0, 4), CHUNK, engine=engine, flags=dk.DYNA_MIGRATE_SIGNAL)
+        info = dk.dyna_kv_xfer_info(x)
+        dk.dyna_kv_wait(x)
+        dst.close()
+        q.put(("ok", info))
+    except Exception as e:  # surface the failure to the parent
+        q.put(("err", repr(e)))
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_ipc_push_with_chunk_flags(engine):
+    import torch
+
+    import kvgen
+    import paper_2504_09285_b200 as dk
+    from gpu_util import pool_filled, torch_rows_equal, untouched_equal, mapped_mask
+    torch.cuda.set_device(0)
+    g = _geom()
+    dst = pool_filled(g, DST_SEED)
+    torch.cuda.synchronize()
+    handle = dk.dyna_kv_pool_export(dst.handle)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_sender, args=(handle, q, engine))
+    p.start()
+    status, info = q.get(timeout=300)
+    p.join(timeout=60)
+    assert status == "ok", info
+    epoch, nchunks, sender = info
+    assert sender == SENDER and nchunks == -(-S // CHUNK) and epoch >= 1
+    # the owner waits on every chunk flag (already released) and reads them back
+    st = torch.cuda.current_stream()
+    for k in range(nchunks):
+        dk.dyna_kv_stream_wait_chunk(dst.handle, sender, k, epoch, 2_000_000_000, st.cuda_stream)
+    flags = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
+    dk.dyna_kv_copy_flags(dst.handle, sender, 0, nchunks, flags.data_ptr(), st.cuda_stream)
+    torch.cuda.synchronize()
+    dk.dyna_kv_poll_error()
+    assert (flags.numpy() == epoch).all()
+    # contents: the sender's source pool is the kvgen stream SRC_SEED; rebuild it here to compare
+    src = pool_filled(g, SRC_SEED)
+    ts, td = kvgen.table_pair(9, 4000, g, g)
+    assert torch_rows_equal(src, ts, dst, td, (0, S), (0, 4))
+    assert untouched_equal(dst, DST_SEED, mapped_mask(g, [(td, (0, S))]))
