@@ -124,8 +124,27 @@ typedef struct {
     int32_t max_ctas;   /* cap on CTAs per kernel (SM budget for overlap with a producer); 0 = no cap */
     int32_t flags;      /* DYNA_MIGRATE_* */
     int32_t piece_bytes;/* bytes per work item; 0 = engine default.  Multiple of 16. */
-    int32_t stages;     /* BULK: shared-memory ring depth; 0 = default */
+    int32_t stages;     /* BULK: shared-memory ring depth (2..16); 0 = default */
+    int32_t unroll;     /* VEC: 16-B loads in flight per lane (4, 8 or 16); 0 = default */
 } dyna_kv_opts;
+
+/* Calibration table used by DYNA_VARIANT_AUTO / DYNA_ENGINE_AUTO (SURVEY §8 a6:
+ * "chosen over the staged variant per chunk size by measured bandwidth").
+ * An entry applies to migrations whose row bytes (H*d*e) equal row_bytes
+ * (0 = any), whose destination locality matches peer (0 = same GPU, 1 = other
+ * GPU), and whose chunk_tokens <= max_chunk_tokens; among matching entries the
+ * one with the smallest max_chunk_tokens wins.  The library starts with the
+ * table measured on B200 (profiles/), replaceable at run time. */
+typedef struct {
+    int32_t row_bytes;
+    int32_t peer;
+    int32_t max_chunk_tokens;
+    int32_t variant;      /* DYNA_VARIANT_FUSED / STAGED */
+    int32_t engine;       /* DYNA_ENGINE_VEC / BULK */
+    int32_t piece_bytes;  /* 0 = engine default */
+    int32_t stages;
+    int32_t unroll;
+} dyna_kv_calib_entry;
 
 /* Bytes a pool of this geometry needs: L*2*NB*bs*H*d*e.  0 if desc invalid. */
 DYNA_API size_t dyna_kv_pool_bytes(const dyna_kv_pool_desc* desc);
@@ -192,6 +211,11 @@ DYNA_API dyna_status dyna_kv_stream_wait_chunk(dyna_kv_pool_t dst, int32_t sende
  * (r^beta may start once all chunks covering [0, s) are resident). */
 DYNA_API dyna_status dyna_kv_copy_flags(dyna_kv_pool_t dst, int32_t sender, int32_t first, int32_t n,
                                         uint64_t* host_out, struct CUstream_st* stream);
+
+/* Replace the calibration table (copied; n <= 256).  n = 0 restores the built-in table. */
+DYNA_API dyna_status dyna_kv_calib_set(const dyna_kv_calib_entry* entries, int32_t n);
+/* Copy up to cap entries of the current table into out; returns the entry count (>= 0). */
+DYNA_API int32_t dyna_kv_calib_get(dyna_kv_calib_entry* out, int32_t cap);
 
 /* Thread-local description of the last error on this thread. */
 DYNA_API const char* dyna_kv_last_error(void);

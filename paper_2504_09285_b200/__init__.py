@@ -34,7 +34,7 @@ EXPORTS = (
     "dyna_kv_migrate_ex", "dyna_kv_wait", "dyna_kv_query", "dyna_kv_stream_wait", "dyna_kv_xfer_info",
     "dyna_kv_stream_wait_chunk", "dyna_kv_last_error", "dyna_kv_poll_error", "dyna_kv_launch_count",
     "dyna_kv_enable_peer", "dyna_kv_pool_export", "dyna_kv_pool_import", "dyna_kv_debug_fill",
-    "dyna_kv_copy_flags",
+    "dyna_kv_copy_flags", "dyna_kv_calib_set", "dyna_kv_calib_get",
 )
 
 
@@ -53,7 +53,13 @@ class dyna_range(ctypes.Structure):
 
 
 class dyna_kv_opts(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_int32) for n in ("variant", "engine", "max_ctas", "flags", "piece_bytes", "stages")]
+    _fields_ = [(n, ctypes.c_int32) for n in ("variant", "engine", "max_ctas", "flags", "piece_bytes", "stages",
+                                               "unroll")]
+
+
+class dyna_kv_calib_entry(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("row_bytes", "peer", "max_chunk_tokens", "variant", "engine",
+                                               "piece_bytes", "stages", "unroll")]
 
 
 class dyna_kv_ipc_handle(ctypes.Structure):
@@ -88,6 +94,8 @@ def _load():
         "dyna_kv_stream_wait_chunk": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64,
                                            vp]),
         "dyna_kv_copy_flags": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp]),
+        "dyna_kv_calib_set": (st, [p(dyna_kv_calib_entry), ctypes.c_int32]),
+        "dyna_kv_calib_get": (ctypes.c_int32, [p(dyna_kv_calib_entry), ctypes.c_int32]),
         "dyna_kv_last_error": (ctypes.c_char_p, []),
         "dyna_kv_poll_error": (st, []),
         "dyna_kv_launch_count": (ctypes.c_uint64, []),
@@ -177,6 +185,20 @@ def dyna_kv_copy_flags(dst_pool: int, sender: int, first: int, n: int, host_out_
                                   ctypes.c_void_p(stream)))
 
 
+def dyna_kv_calib_set(entries) -> None:
+    """entries: list of dyna_kv_calib_entry (or tuples in field order); [] restores the built-in table."""
+    arr = (dyna_kv_calib_entry * max(1, len(entries)))(*[e if isinstance(e, dyna_kv_calib_entry)
+                                                          else dyna_kv_calib_entry(*e) for e in entries])
+    _check(lib.dyna_kv_calib_set(arr, len(entries)))
+
+
+def dyna_kv_calib_get() -> list:
+    n = lib.dyna_kv_calib_get(None, 0)
+    arr = (dyna_kv_calib_entry * max(1, n))()
+    lib.dyna_kv_calib_get(arr, n)
+    return [tuple(getattr(arr[i], f) for f, _ in dyna_kv_calib_entry._fields_) for i in range(n)]
+
+
 def dyna_kv_last_error() -> str:
     return lib.dyna_kv_last_error().decode(errors="replace")
 
@@ -261,8 +283,8 @@ def table(pool: Pool, ids, host_ids=None) -> dyna_block_table:
     return t
 
 
-def opts(variant=0, engine=0, max_ctas=0, flags=0, piece_bytes=0, stages=0) -> dyna_kv_opts:
-    return dyna_kv_opts(variant, engine, max_ctas, flags, piece_bytes, stages)
+def opts(variant=0, engine=0, max_ctas=0, flags=0, piece_bytes=0, stages=0, unroll=0) -> dyna_kv_opts:
+    return dyna_kv_opts(variant, engine, max_ctas, flags, piece_bytes, stages, unroll)
 
 
 def migrate(src: dyna_block_table, dst: dyna_block_table, token_range, layer_range, chunk_tokens, stream=None,

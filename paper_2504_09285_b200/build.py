@@ -13,7 +13,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdyna_kv.so")
 SOURCES = [os.path.join(CSRC, "dyna_kv.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "dyna_kv_kernels.cuh"), os.path.join(ROOT, "include", "dyna_kv.h")]
+DEPS = SOURCES + [os.path.join(CSRC, "dyna_kv_kernels.cuh"), os.path.join(CSRC, "calib_default.inc"),
+                  os.path.join(ROOT, "include", "dyna_kv.h")]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

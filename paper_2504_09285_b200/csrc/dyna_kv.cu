@@ -87,9 +87,6 @@ dyna_status take_device_error() {
 
 struct DevInfo {
   int sms = 0;
-  int vec_occ = 0;   // resident CTAs/SM of the VEC kernel
-  int bulk_occ = 0;  // for the default BULK smem size
-  int bulk_smem_set = 0;
   cudaStream_t aux = nullptr;  // library stream for destination-side kernels (staged, cross-device)
 };
 std::map<int, DevInfo> g_dev;
@@ -107,8 +104,6 @@ DevInfo* dev_info(int dev) {
   if (d.sms == 0) {
     DeviceGuard g(dev);
     cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.vec_occ, k_copy_vec<kVecU, false>, kVecThreads, 0);
-    if (d.vec_occ <= 0) d.vec_occ = 1;
     if (d.sms <= 0) d.sms = 1;
   }
   return &d;
@@ -172,6 +167,8 @@ void put_event(int dev, cudaEvent_t ev) {
 
 constexpr size_t kInboxBytes = sizeof(unsigned long long) * DYNA_MAX_INSTANCES * DYNA_MAX_CHUNKS;
 
+int64_t row_bytes_of(const dyna_kv_pool* p) { return p->row; }
+
 bool desc_valid(const dyna_kv_pool_desc* d) {
   return d && d->num_layers > 0 && d->num_kv_heads > 0 && d->head_dim > 0 && d->elem_bytes > 0 &&
          d->block_size > 0 && d->num_blocks > 0 && d->device >= 0 && d->instance >= 0 &&
@@ -216,8 +213,37 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   return p;
 }
 
+template <int U, bool SIG>
+int vec_occupancy() {
+  static std::map<int, int> cache;  // per device
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copy_vec<U, SIG>, kVecThreads, 0);
+  if (occ <= 0) occ = 1;
+  cache[dev] = occ;
+  return occ;
+}
+
+template <int U>
+void launch_vec(const Plan& p, int64_t max_grid, int sms, cudaStream_t st) {
+  const bool sig = p.counters != nullptr;
+  const int occ = sig ? vec_occupancy<U, true>() : vec_occupancy<U, false>();
+  int64_t grid = std::min<int64_t>((p.n_items + kVecThreads / 32 - 1) / (kVecThreads / 32), (int64_t)sms * occ);
+  if (max_grid > 0) grid = std::min<int64_t>(grid, max_grid);
+  if (sig)
+    k_copy_vec<U, true><<<(unsigned)grid, kVecThreads, 0, st>>>(p);
+  else
+    k_copy_vec<U, false><<<(unsigned)grid, kVecThreads, 0, st>>>(p);
+}
+
 // Launch one copy kernel.  engine: DYNA_ENGINE_VEC / BULK.
-dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int dev, cudaStream_t st) {
+dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev,
+                        cudaStream_t st) {
   if (p.n_items == 0) return DYNA_OK;
   DevInfo* di = dev_info(dev);
   const bool sig = p.counters != nullptr;
@@ -231,18 +257,39 @@ dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int
     int64_t grid = std::min<int64_t>(p.n_items, (int64_t)di->sms * occ);
     if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
     kern<<<(unsigned)grid, 32, smem, st>>>(p, stages);
+  } else if (unroll == 4) {
+    launch_vec<4>(p, max_ctas, di->sms, st);
+  } else if (unroll == 16) {
+    launch_vec<16>(p, max_ctas, di->sms, st);
   } else {
-    int64_t grid = std::min<int64_t>((p.n_items + kVecThreads / 32 - 1) / (kVecThreads / 32),
-                                     (int64_t)di->sms * di->vec_occ);
-    if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
-    if (sig)
-      k_copy_vec<kVecU, true><<<(unsigned)grid, kVecThreads, 0, st>>>(p);
-    else
-      k_copy_vec<kVecU, false><<<(unsigned)grid, kVecThreads, 0, st>>>(p);
+    launch_vec<8>(p, max_ctas, di->sms, st);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   CUDA_TRY(cudaGetLastError());
   return DYNA_OK;
+}
+
+// ------------------------------------------------------------------ calibration (a6)
+const dyna_kv_calib_entry kCalibDefault[] = {
+#include "calib_default.inc"
+    {0, -1, 0, 0, 0, 0, 0, 0}  // sentinel (never matches: peer = -1)
+};
+std::mutex g_calib_mu;
+std::vector<dyna_kv_calib_entry> g_calib(std::begin(kCalibDefault), std::end(kCalibDefault) - 1);
+
+// Best calibrated entry for (row bytes, locality, chunk tokens); returns false if none.
+bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out) {
+  std::lock_guard<std::mutex> lk(g_calib_mu);
+  const dyna_kv_calib_entry* best = nullptr;
+  for (const auto& e : g_calib) {
+    if ((e.row_bytes != 0 && e.row_bytes != row) || e.peer != peer || c > e.max_chunk_tokens) continue;
+    if (!best || e.max_chunk_tokens < best->max_chunk_tokens ||
+        (e.max_chunk_tokens == best->max_chunk_tokens && best->row_bytes == 0 && e.row_bytes != 0))
+      best = &e;
+  }
+  if (!best) return false;
+  *out = *best;
+  return true;
 }
 
 Side paged(const dyna_kv_pool* pool, const int32_t* ids) {
@@ -385,6 +432,29 @@ dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t 
 extern "C" {
 
 const char* dyna_kv_last_error(void) { return g_err.c_str(); }
+
+dyna_status dyna_kv_calib_set(const dyna_kv_calib_entry* entries, int32_t n) {
+  if (n < 0 || n > 256 || (n > 0 && !entries)) return fail(DYNA_EINVAL, "calibration: 0 <= n <= 256");
+  for (int32_t i = 0; i < n; ++i) {
+    const auto& e = entries[i];
+    if (e.row_bytes < 0 || e.peer < 0 || e.peer > 1 || e.max_chunk_tokens <= 0 || e.variant < 0 || e.variant > 2 ||
+        e.engine < 0 || e.engine > 2 || e.piece_bytes < 0 || e.piece_bytes % 16 || e.stages < 0 || e.stages == 1 ||
+        e.stages > kMaxStages || (e.unroll != 0 && e.unroll != 4 && e.unroll != 8 && e.unroll != 16))
+      return fail(DYNA_EINVAL, "calibration entry %d invalid", i);
+  }
+  std::lock_guard<std::mutex> lk(g_calib_mu);
+  if (n == 0)
+    g_calib.assign(std::begin(kCalibDefault), std::end(kCalibDefault) - 1);
+  else
+    g_calib.assign(entries, entries + n);
+  return DYNA_OK;
+}
+
+int32_t dyna_kv_calib_get(dyna_kv_calib_entry* out, int32_t cap) {
+  std::lock_guard<std::mutex> lk(g_calib_mu);
+  for (int32_t i = 0; i < cap && i < (int32_t)g_calib.size(); ++i) out[i] = g_calib[i];
+  return (int32_t)g_calib.size();
+}
 uint64_t dyna_kv_launch_count(void) { return g_launches.load(); }
 dyna_status dyna_kv_poll_error(void) { return take_device_error(); }
 
@@ -468,7 +538,8 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
   dyna_kv_opts o{};
   if (opts) o = *opts;
   if (o.variant < 0 || o.variant > 2 || o.engine < 0 || o.engine > 2 || o.max_ctas < 0 || o.piece_bytes < 0 ||
-      o.piece_bytes % 16 || o.stages < 0 || o.stages > kMaxStages)
+      o.piece_bytes % 16 || o.stages < 0 || o.stages == 1 || o.stages > kMaxStages ||
+      (o.unroll != 0 && o.unroll != 4 && o.unroll != 8 && o.unroll != 16))
     return fail(DYNA_EINVAL, "invalid dyna_kv_opts");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   dyna_kv_pool* S = src.pool;
@@ -527,10 +598,20 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
   const int64_t row = S->row;
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
   const int64_t c = chunk_tokens;
-  const int variant = o.variant == DYNA_VARIANT_AUTO ? DYNA_VARIANT_FUSED : o.variant;
-  const int engine = o.engine == DYNA_ENGINE_AUTO ? DYNA_ENGINE_VEC : o.engine;
-  const int piece = o.piece_bytes ? o.piece_bytes : (engine == DYNA_ENGINE_BULK ? kBulkPiece : kVecPiece);
-  const int stages = o.stages ? o.stages : kBulkStages;
+  // a6: unset choices come from the calibration table (measured GB/s per row bytes,
+  // locality and chunk size), else FUSED + VEC.
+  const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
+  dyna_kv_calib_entry ce{};
+  const bool calibrated = (o.variant == DYNA_VARIANT_AUTO || o.engine == DYNA_ENGINE_AUTO) &&
+                          calib_lookup(row_bytes_of(S), peer_dst, chunk_tokens, &ce);
+  const int variant = o.variant ? o.variant : (calibrated && ce.variant ? ce.variant : DYNA_VARIANT_FUSED);
+  const int engine = o.engine ? o.engine : (calibrated && ce.engine ? ce.engine : DYNA_ENGINE_VEC);
+  const bool use_ce = calibrated && (!o.engine || o.engine == ce.engine);
+  const int piece = o.piece_bytes ? o.piece_bytes
+                                  : (use_ce && ce.piece_bytes ? ce.piece_bytes
+                                                             : (engine == DYNA_ENGINE_BULK ? kBulkPiece : kVecPiece));
+  const int stages = o.stages ? o.stages : (use_ce && ce.stages ? ce.stages : kBulkStages);
+  const int unroll = o.unroll ? o.unroll : (use_ce && ce.unroll ? ce.unroll : kVecU);
 
   DeviceGuard guard(S->dev);
   dyna_status r = DYNA_OK;
@@ -547,7 +628,7 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
       p.epoch = x->epoch = next_epoch(gs.instance, D);
       p.sys_fence = (D->dev != S->dev || D->imported) ? 1 : 0;
     }
-    r = launch_copy(p, engine, o.max_ctas, stages, S->dev, stream);
+    r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream);
   } else {
     // Staged: K1 gather -> staging slot, K2 slot -> destination-side slot,
     // K3 scatter slot -> destination rows.  Chunks are cut into sub-chunks
@@ -601,11 +682,11 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
         char* dslot = dbuf + si * slot;
         if (cross && sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[si], 0));
         Plan k1 = make_plan(paged(S, src.block_ids), linear(sslot), row, sa, sb, l0, lm, sb - sa, gs.block_size, piece);
-        if ((r = launch_copy(k1, engine, o.max_ctas, stages, S->dev, stream))) break;
+        if ((r = launch_copy(k1, engine, o.max_ctas, stages, unroll, S->dev, stream))) break;
         // K2: the sub-chunk slot is [lm][2][n][row] = two contiguous halves
         // (K and V of all layers): a flat plan with one token of `half` bytes.
         Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
-        if ((r = launch_copy(k2, engine, o.max_ctas, stages, S->dev, stream))) break;
+        if ((r = launch_copy(k2, engine, o.max_ctas, stages, unroll, S->dev, stream))) break;
         Plan k3 = make_plan(linear(dslot), paged(D, dst.block_ids), row, sa, sb, l0, lm, sb - sa, gd.block_size, piece);
         k3.mig_t0 = tr.begin;
         k3.mig_t1 = tr.end;
@@ -619,10 +700,10 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
           CUDA_TRY(cudaEventRecord(done_src[si], stream));
           DeviceGuard g(D->dev);
           CUDA_TRY(cudaStreamWaitEvent(dstream, done_src[si], 0));
-          if ((r = launch_copy(k3, engine, o.max_ctas, stages, D->dev, dstream))) break;
+          if ((r = launch_copy(k3, engine, o.max_ctas, stages, unroll, D->dev, dstream))) break;
           CUDA_TRY(cudaEventRecord(done_dst[si], dstream));
         } else {
-          if ((r = launch_copy(k3, engine, o.max_ctas, stages, S->dev, stream))) break;
+          if ((r = launch_copy(k3, engine, o.max_ctas, stages, unroll, S->dev, stream))) break;
         }
       }
     }

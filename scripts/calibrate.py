@@ -1,0 +1,117 @@
+#!/usr/bin/env python
+"""Variant / engine calibration sweep ("chosen over the staged
+variant per chunk size by measured bandwidth").
+
+For each row geometry and chunk size c, migrate one c-token chunk per call
+(the paper's per-chunk push), cycling through the whole 4 GiB pool so
+the working set never sits in L2, and time every candidate
+(variant x engine x piece/stages/unroll) with CUDA events around each call.
+The best candidate per (row bytes, chunk bucket) becomes the built-in table
+(paper_2504_09285_b200/csrc/calib_default.inc); all measurements go to JSON.
+
+    python scripts/calibrate.py [--out gpurun_out/calibration.json] [--inc gpurun_out/calib_default.inc]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import kvgen  # noqa: E402
+import paper_2504_09285_b200 as dk  # noqa: E402
+
+F, S = dk.DYNA_VARIANT_FUSED, dk.DYNA_VARIANT_STAGED
+V, B = dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK
+CANDIDATES = [  # (variant, engine, piece, stages, unroll)
+    (F, V, 8192, 0, 4), (F, V, 8192, 0, 8), (F, V, 16384, 0, 16), (F, V, 4096, 0, 8),
+    (F, B, 16384, 8, 0), (F, B, 32768, 6, 0), (F, B, 65536, 3, 0),
+    (S, V, 8192, 0, 8), (S, B, 32768, 6, 0),
+]
+GEOMS = {8192: kvgen.LLAMA2_7B, 2048: kvgen.LLAMA3_8B.with_(num_blocks=2048)}
+CHUNKS = [16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "calibration.json"))
+    ap.add_argument("--inc", default=os.path.join(ROOT, "gpurun_out", "calib_default.inc"))
+    ap.add_argument("--min-ms", type=float, default=15.0)
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    cs = stream.cuda_stream
+    rows, chosen = [], []
+    for row, g in GEOMS.items():
+        ntok = g.num_blocks * g.block_size
+        src, dst = dk.Pool(g, 0), dk.Pool(g, 0)
+        for p, seed in ((src, 1), (dst, 2)):
+            dk.dyna_kv_debug_fill(p.tensor.data_ptr(), p.tensor.numel(), seed, 0, cs)
+        rng = np.random.default_rng(row)
+        ts, td = rng.permutation(g.num_blocks).astype(np.int32), rng.permutation(g.num_blocks).astype(np.int32)
+        st = dk.table(src, torch.from_numpy(ts).cuda(), ts)
+        dt = dk.table(dst, torch.from_numpy(td).cuda(), td)
+        tok_bytes = 2 * g.num_layers * g.row_bytes
+        for c in CHUNKS:
+            n_calls = min(2000, max(20, int(args.min_ms * 1e-3 * 3.0e12 / (c * tok_bytes))))
+            offs = [(i * c) % (ntok - c + 1) for i in range(n_calls)]
+            results = []
+            for (var, eng, piece, stages, unroll) in CANDIDATES:
+                o = dk.opts(variant=var, engine=eng, piece_bytes=piece, stages=stages, unroll=unroll)
+
+                def batch():
+                    evs, xs = [], []
+                    for off in offs:
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record(stream)
+                        xs.append(dk.dyna_kv_migrate_ex(st, dt, (off, off + c), (0, g.num_layers), c, cs, o))
+                        b.record(stream)
+                        evs.append((a, b))
+                    for x in xs:
+                        dk.dyna_kv_wait(x)
+                    return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+                batch()  # warm-up
+                ms = min(batch() for _ in range(2))
+                gbps = c * tok_bytes / (ms / 1e3) / 1e9
+                r = {"row_bytes": row, "chunk": c, "variant": var, "engine": eng, "piece": piece, "stages": stages,
+                     "unroll": unroll, "ms_per_call": ms, "GBps": gbps}
+                results.append(r)
+                rows.append(r)
+                print(json.dumps(r), flush=True)
+            best = max(results, key=lambda r: r["GBps"])
+            chosen.append(best)
+        src.close()
+        dst.close()
+    # compress consecutive buckets with the same choice into one entry (largest c of the run)
+    entries = []
+    for row in GEOMS:
+        seq = [b for b in chosen if b["row_bytes"] == row]
+        for i, b in enumerate(seq):
+            key = (b["variant"], b["engine"], b["piece"], b["stages"], b["unroll"])
+            nxt = seq[i + 1] if i + 1 < len(seq) else None
+            if nxt and (nxt["variant"], nxt["engine"], nxt["piece"], nxt["stages"], nxt["unroll"]) == key:
+                continue
+            maxc = b["chunk"] if nxt else (1 << 30)
+            entries.append((row, 0, maxc) + key)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    json.dump({"device": torch.cuda.get_device_name(0), "candidates": CANDIDATES, "measurements": rows,
+               "chosen": chosen, "entries": entries}, open(args.out, "w"), indent=1)
+    with open(args.inc, "w") as f:
+        f.write("// Built-in calibration table, generated by scripts/calibrate.py on "
+                f"{torch.cuda.get_device_name(0)} (see profiles/*calibration*).\n")
+        f.write("// row_bytes, peer, max_chunk_tokens, variant, engine, piece_bytes, stages, unroll\n")
+        for e in entries:
+            f.write("    {" + ", ".join(str(x) for x in e) + "},\n")
+    print(json.dumps({"entries": entries}))
+
+
+if __name__ == "__main__":
+    main()

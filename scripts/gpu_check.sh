@@ -14,3 +14,4 @@ fi
 for e in 1 2; do timeout 300 python bench.py --steps 1000 --warmup 10 --engine $e --no-cpu-baseline 2>&1 | tail -1; done
 timeout 300 python bench.py --steps 1000 --warmup 10 2>&1 | tail -1 > gpurun_out/bench_default.json; cat gpurun_out/bench_default.json
 if [ -n "$OVERLAP" ]; then timeout 900 python scripts/overlap.py 2>&1 | tail -40; fi
+if [ -n "$CALIB" ]; then timeout 1200 python scripts/calibrate.py 2>&1 | tail -3; fi

@@ -57,7 +57,8 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(dk.dyna_kv_pool_desc) == 32
     assert ctypes.sizeof(dk.dyna_block_table) == 32
     assert ctypes.sizeof(dk.dyna_range) == 16
-    assert ctypes.sizeof(dk.dyna_kv_opts) == 24
+    assert ctypes.sizeof(dk.dyna_kv_opts) == 28
+    assert ctypes.sizeof(dk.dyna_kv_calib_entry) == 32
     assert ctypes.sizeof(dk.dyna_kv_ipc_handle) == 64 + 64 + 8 + 32
 
 
@@ -86,3 +87,17 @@ def test_host_validation_without_gpu():
     with pytest.raises(dk.DynaKVError) as e:
         dk.dyna_kv_wait(0)
     assert e.value.status == dk.DYNA_EINVAL
+
+
+def test_calibration_table_roundtrip_without_gpu():
+    import paper_2504_09285_b200 as dk
+    base = dk.dyna_kv_calib_get()
+    entries = [(8192, 0, 64, 2, 2, 16384, 4, 0), (8192, 0, 4096, 1, 1, 0, 0, 8), (0, 1, 1 << 30, 1, 2, 0, 0, 0)]
+    dk.dyna_kv_calib_set(entries)
+    assert dk.dyna_kv_calib_get() == entries
+    with pytest.raises(dk.DynaKVError):
+        dk.dyna_kv_calib_set([(8192, 0, 64, 2, 2, 17, 4, 0)])   # piece not a multiple of 16
+    with pytest.raises(dk.DynaKVError):
+        dk.dyna_kv_calib_set([(8192, 2, 64, 2, 2, 0, 4, 0)])    # peer must be 0/1
+    dk.dyna_kv_calib_set([])
+    assert dk.dyna_kv_calib_get() == base
