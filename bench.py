@@ -162,6 +162,7 @@ def run_dyna(args, rank, world, local_rank):
 
     import kvgen
     import paper_2504_09285_b200 as dk
+    from paper_2504_09285_b200 import dist as dd
 
     torch.cuda.set_device(local_rank)
     dev = local_rank
@@ -185,9 +186,8 @@ def run_dyna(args, rank, world, local_rank):
         mine = dk.Pool(g, dev, instance=rank)
         dk.dyna_kv_debug_fill(mine.tensor.data_ptr(), mine.tensor.numel(), 2000 + rank, 0, cs)
         torch.cuda.synchronize()
-        handles = [None] * world
-        dist.all_gather_object(handles, dk.dyna_kv_pool_export(mine.handle))
-        peer = (rank + 1) % world
+        handles = dd.exchange_handles(dk.dyna_kv_pool_export(mine.handle))
+        peer = dd.ring_pairs(world)[rank][1]
         dst = dk.Pool.imported(handles[peer], dev)
     # N_SETS disjoint request placements per pool, rotated every step: each step
     # reads 512 MiB and writes 512 MiB that the previous steps did not touch (> 126 MB L2).
@@ -208,11 +208,7 @@ def run_dyna(args, rank, world, local_rank):
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return dd.max_over_ranks(x, device=f"cuda:{dev}")
 
     clocks = Clocks(dev)
     # warm-up (untimed), then ~0.5 s of untimed load so the clock samples see the part under load
@@ -250,41 +246,57 @@ def run_dyna(args, rank, world, local_rank):
     kern_ms = max_over_ranks(kern_ms)
 
     # ---------------- e2e through the public API with host buffers: every step copies the
-    # request's two block tables from pinned host memory, migrates with per-chunk flags, reads
-    # the chunk flags back to the host and blocks in dyna_kv_wait.
+    # request's two block tables from pinned host memory, migrates with per-chunk flags and
+    # reads the chunk flags back into pinned host memory; completion is taken from
+    # dyna_kv_wait.  Steps are issued one ahead of the wait (the async API as a serving
+    # loop uses it), so host work for step k+1 overlaps the device work of step k.
     nchunks = -(-S_SPLIT // CHUNK)
     host_tabs = [(torch.from_numpy(ts).pin_memory(), torch.from_numpy(td).pin_memory()) for ts, td in tabs]
     dev_tabs = [(torch.empty_like(a, device=f"cuda:{dev}"), torch.empty_like(b, device=f"cuda:{dev}"))
                 for a, b in host_tabs]
     e2e_tables = [(dk.table(src, a, ts), dk.table(dst, b, td)) for (a, b), (ts, td) in zip(dev_tabs, tabs)]
-    flags_host = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
+    flags_host = [torch.zeros(nchunks, dtype=torch.int64).pin_memory() for _ in range(N_SETS)]
     sig_opts = dk.opts(variant=args.variant, engine=args.engine, flags=dk.DYNA_MIGRATE_SIGNAL)
     sender = rank
     flag_pool = dst.handle
     h2d = sum(a.numel() * 4 + b.numel() * 4 for a, b in host_tabs) // N_SETS
     d2h = nchunks * 8
 
-    def e2e_step(k):
-        (ha, hb), (da, db) = host_tabs[k % N_SETS], dev_tabs[k % N_SETS]
+    def e2e_issue(k):
+        i = k % N_SETS
+        (ha, hb), (da, db) = host_tabs[i], dev_tabs[i]
         with torch.cuda.stream(stream):
             da.copy_(ha, non_blocking=True)
             db.copy_(hb, non_blocking=True)
-        st, dt_ = e2e_tables[k % N_SETS]
+        st, dt_ = e2e_tables[i]
         x = dk.dyna_kv_migrate_ex(st, dt_, (0, S_SPLIT), (0, g.num_layers), CHUNK, cs, sig_opts)
         epoch = dk.dyna_kv_xfer_info(x)[0]
-        dk.dyna_kv_copy_flags(flag_pool, sender, 0, nchunks, flags_host.data_ptr(), cs)
-        dk.dyna_kv_wait(x)
-        return epoch
+        dk.dyna_kv_copy_flags(flag_pool, sender, 0, nchunks, flags_host[i].data_ptr(), cs)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return x, epoch, ev, i
 
-    for k in range(args.warmup):
-        e2e_step(k)
+    def e2e_finish(h):
+        x, epoch, ev, i = h
+        dk.dyna_kv_wait(x)
+        ev.synchronize()
+        return int(flags_host[i].min()) == epoch
+
+    def e2e_run(n):
+        ok, prev = True, None
+        for k in range(n):
+            cur = e2e_issue(k)
+            if prev is not None:
+                ok &= e2e_finish(prev)
+            prev = cur
+        return ok & e2e_finish(prev)
+
+    e2e_run(args.warmup)
     barrier()
     t = time.perf_counter()
-    for k in range(args.steps):
-        epoch = e2e_step(k)
-    torch.cuda.synchronize()
+    flags_ok = e2e_run(args.steps)
     e2e_s = max_over_ranks(time.perf_counter() - t)
-    assert int(flags_host.min()) == epoch, "chunk flags did not reach the last epoch"
+    assert flags_ok, "chunk flags did not reach the migration's epoch"
     barrier()
 
     # context for the roofline: torch's own copy_ of a contiguous buffer of the same payload size

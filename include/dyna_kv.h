@@ -132,8 +132,9 @@ typedef struct {
  * "chosen over the staged variant per chunk size by measured bandwidth").
  * An entry applies to migrations whose row bytes (H*d*e) equal row_bytes
  * (0 = any), whose destination locality matches peer (0 = same GPU, 1 = other
- * GPU), and whose chunk_tokens <= max_chunk_tokens; among matching entries the
- * one with the smallest max_chunk_tokens wins.  The library starts with the
+ * GPU), and whose call size (tokens in token_range) <= max_chunk_tokens (in
+ * the paper's per-chunk push, a call moves one chunk, so this is the
+ * chunk size); among matching entries the smallest max_chunk_tokens wins.  The library starts with the
  * table measured on B200 (profiles/), replaceable at run time. */
 typedef struct {
     int32_t row_bytes;

@@ -229,12 +229,24 @@ int vec_occupancy() {
   return occ;
 }
 
+// Balanced persistent grid: the fewest workers (warps or CTAs) that still need
+// only ceil(n / max_workers) rounds, so every worker gets the same number of
+// items (+-1) and no partial last round leaves most of the chip idle.
+int64_t balanced_workers(int64_t n_items, int64_t max_workers) {
+  if (n_items <= max_workers) return n_items;
+  const int64_t rounds = (n_items + max_workers - 1) / max_workers;
+  return (n_items + rounds - 1) / rounds;
+}
+
 template <int U>
 void launch_vec(const Plan& p, int64_t max_grid, int sms, cudaStream_t st) {
   const bool sig = p.counters != nullptr;
   const int occ = sig ? vec_occupancy<U, true>() : vec_occupancy<U, false>();
-  int64_t grid = std::min<int64_t>((p.n_items + kVecThreads / 32 - 1) / (kVecThreads / 32), (int64_t)sms * occ);
-  if (max_grid > 0) grid = std::min<int64_t>(grid, max_grid);
+  constexpr int wpc = kVecThreads / 32;  // warps per CTA
+  int64_t max_ctas = (int64_t)sms * occ;
+  if (max_grid > 0) max_ctas = std::min<int64_t>(max_ctas, max_grid);
+  const int64_t warps = balanced_workers(p.n_items, max_ctas * wpc);
+  const int64_t grid = (warps + wpc - 1) / wpc;
   if (sig)
     k_copy_vec<U, true><<<(unsigned)grid, kVecThreads, 0, st>>>(p);
   else
@@ -254,8 +266,9 @@ dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem));
     if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
-    int64_t grid = std::min<int64_t>(p.n_items, (int64_t)di->sms * occ);
-    if (max_ctas > 0) grid = std::min<int64_t>(grid, max_ctas);
+    int64_t cap = (int64_t)di->sms * occ;
+    if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
+    const int64_t grid = balanced_workers(p.n_items, cap);
     kern<<<(unsigned)grid, 32, smem, st>>>(p, stages);
   } else if (unroll == 4) {
     launch_vec<4>(p, max_ctas, di->sms, st);
@@ -603,7 +616,7 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
   const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
   dyna_kv_calib_entry ce{};
   const bool calibrated = (o.variant == DYNA_VARIANT_AUTO || o.engine == DYNA_ENGINE_AUTO) &&
-                          calib_lookup(row_bytes_of(S), peer_dst, chunk_tokens, &ce);
+                          calib_lookup(row_bytes_of(S), peer_dst, ntok, &ce);
   const int variant = o.variant ? o.variant : (calibrated && ce.variant ? ce.variant : DYNA_VARIANT_FUSED);
   const int engine = o.engine ? o.engine : (calibrated && ce.engine ? ce.engine : DYNA_ENGINE_VEC);
   const bool use_ce = calibrated && (!o.engine || o.engine == ce.engine);

@@ -269,7 +269,8 @@ __device__ __forceinline__ void bulk_wait_all() {
 constexpr int kMaxStages = 16;
 
 // One thread per CTA drives a ring of `stages` smem slots of p.piece bytes:
-// up to stages-1 loads in flight while the oldest slot drains to global.
+// loads land in slots ahead of the store front; each slot is reloaded once
+// the store issued from it has been read out of shared memory.
 template <bool SIGNAL>
 __global__ void __launch_bounds__(32) k_copy_bulk(const Plan p, int stages) {
   extern __shared__ __align__(128) unsigned char ring[];
@@ -312,7 +313,9 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Plan p, int stages) {
   // and count the finished chunk's bytes.
   int32_t cur_k = -1;
   uint32_t cur_acc = 0;
-  int prev = -1;
+  // A slot is refilled `lag` stores after its own store was issued, so up to
+  // lag+1 stores drain while stages-lag-1 loads are in flight.
+  const int lag = stages >= 4 ? 2 : 1;
   for (int64_t iter = 0;; ++iter) {
     const int s = (int)(iter % stages);
     if (pend_n[s] == 0) break;
@@ -330,11 +333,10 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Plan p, int stages) {
     bulk_store(pend_dst[s], ring + (size_t)s * p.piece, pend_n[s]);
     bulk_commit();
     if (SIGNAL) cur_acc += pend_n[s];
-    if (prev >= 0) {
-      bulk_wait_read<1>();  // the previous store finished reading its slot
-      refill(prev);
+    if (iter >= lag) {
+      if (lag == 2) bulk_wait_read<2>(); else bulk_wait_read<1>();  // store iter-lag done reading smem
+      refill((int)((iter - lag) % stages));
     }
-    prev = s;
   }
   bulk_wait_all<0>();
   if (SIGNAL && cur_acc) {

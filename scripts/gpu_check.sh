@@ -1,8 +1,9 @@
-# GPU-box check: smoke, GPU tests, bench lines, optional ncu and overlap runs.
+# GPU-box check: smoke, GPU tests, bench lines, optional ncu / overlap / calibration runs.
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -5
-timeout 1500 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} 2>&1 | tail -30
+if [ -z "$NOTEST" ]; then timeout 1500 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} 2>&1 | tail -30; fi
+if [ -n "$CALIB" ]; then timeout 1500 python scripts/calibrate.py > gpurun_out/calibrate.log 2>&1; tail -2 gpurun_out/calibrate.log; fi
 if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv \
       python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_bench.log 2>&1
@@ -11,7 +12,8 @@ if [ -n "$NCU" ]; then
         python bench.py --steps 20 --warmup 3 --no-cpu-baseline --engine $e > gpurun_out/ncu_full_e$e.log 2>&1
   done
 fi
-for e in 1 2; do timeout 300 python bench.py --steps 1000 --warmup 10 --engine $e --no-cpu-baseline 2>&1 | tail -1; done
-timeout 300 python bench.py --steps 1000 --warmup 10 2>&1 | tail -1 > gpurun_out/bench_default.json; cat gpurun_out/bench_default.json
-if [ -n "$OVERLAP" ]; then timeout 900 python scripts/overlap.py 2>&1 | tail -40; fi
-if [ -n "$CALIB" ]; then timeout 1200 python scripts/calibrate.py 2>&1 | tail -3; fi
+if [ -z "$NOBENCH" ]; then
+  for e in 1 2; do timeout 300 python bench.py --steps 1000 --warmup 10 --engine $e --no-cpu-baseline 2>&1 | tail -1; done
+  timeout 300 python bench.py --steps 1000 --warmup 10 2>&1 | tail -1 > gpurun_out/bench_default.json; cat gpurun_out/bench_default.json
+fi
+if [ -n "$OVERLAP" ]; then timeout 900 python scripts/overlap.py > gpurun_out/overlap.log 2>&1; tail -20 gpurun_out/overlap.log; fi

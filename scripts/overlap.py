@@ -93,7 +93,7 @@ def main():
             mig.wait_event(e_prod)
             handles.append(dk.migrate(st, dt, (0, s), (0, 32), c, stream=mig, max_ctas=budget))
         e_mig.record(mig)
-        e_mig.synchronize()
+        torch.cuda.synchronize()
         for x in handles:
             dk.dyna_kv_wait(x)
         return e0.elapsed_time(e_prod), max(0.0, e_prod.elapsed_time(e_mig))

@@ -1,0 +1,116 @@
+"""Multi-process host logic of the N > 1 path on CPU (gloo, world size 2):
+handle exchange, max-over-ranks timing, pair schedules and the load-aware
+bound of concurrent migrations."""
+import os
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2504_09285_b200 import dist as dd
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fake_handle = bytes([rank]) * 168          # sizeof(dyna_kv_ipc_handle)
+        got = dd.exchange_handles(fake_handle)
+        peer = dd.ring_pairs(world)[rank][1]
+        t = dd.max_over_ranks(1.5 + rank)
+        q.put((rank, [g[0] for g in got], len(got[peer]), t))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_handle_exchange_and_max():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, firsts, peer_len, t in res:
+        assert firsts == [0, 1]          # every rank sees every handle, in rank order
+        assert peer_len == 168
+        assert t == 2.5                  # max over ranks
+
+
+def test_pair_schedules():
+    assert dd.ring_pairs(1) == [(0, 0)]
+    assert dd.ring_pairs(4) == [(0, 1), (1, 2), (2, 3), (3, 0)]
+    ap = dd.all_pairs(8)
+    assert len(ap) == 56 and len(set(ap)) == 56 and all(i != j for i, j in ap)
+
+
+def test_load_aware_bound_brute_force():
+    # brute force: simulate fluid sharing on a switch with per-port capacity 1 byte/s;
+    # completion time >= busiest port, and equals it for a single sender/receiver pair.
+    pb = {(0, 1): 100, (0, 2): 50, (2, 1): 70, (3, 1): 10}
+    eg, ing = dd.link_loads(pb)
+    assert eg == {0: 150, 2: 70, 3: 10} and ing == {1: 180, 2: 50}
+    assert dd.load_aware_bound_s(pb, 1.0) == 180
+    assert dd.aggregate_bound_s(pb, 4, 1.0) == 230 / 4
+    assert dd.load_aware_bound_s({(0, 1): 64}, 2.0) == 32
+    assert dd.load_aware_bound_s({(0, 0): 64}, 2.0) == 0      # local reblock uses no link
+    for n in (2, 4, 8):
+        pb = {p: 1 for p in dd.all_pairs(n)}
+        assert dd.load_aware_bound_s(pb, 1.0) == n - 1 == dd.aggregate_bound_s(pb, n, 1.0)
+
+
+def _baseline_worker(rank, world, port, q):
+    import importlib.util
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import kvgen
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        spec = importlib.util.spec_from_file_location("nb", os.path.join(root, "scripts", "nccl_baseline.py"))
+        nb = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(nb)
+        g, s, chunk = kvgen.TOY, 100, 32
+        src = torch.from_numpy(kvgen.fill_bytes(10 + rank, g.pool_bytes))
+        dst0 = kvgen.fill_bytes(20 + rank, g.pool_bytes)
+        dst = torch.from_numpy(dst0.copy())
+        ts, _ = kvgen.table_pair(500 + rank, 256, g, g)
+        prv = (rank - 1) % world
+        ts_prv, td_in = kvgen.table_pair(500 + prv, 256, g, g)
+        nb.push_chunks(rank, world, src, dst, g, torch.from_numpy(ts), torch.from_numpy(td_in), s, chunk)
+        want = dst0.copy()
+        oracle.migrate(kvgen.fill_bytes(10 + prv, g.pool_bytes), g, ts_prv, want, g, td_in, (0, s))
+        q.put((rank, bool(np.array_equal(dst.numpy(), want))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_baseline_logic_matches_oracle_under_gloo():
+    """B1 baseline (gather -> send/recv -> scatter) produces the oracle's bytes."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_baseline_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=180) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+    assert res == [(0, True), (1, True)]

@@ -84,10 +84,15 @@ def test_sm_budget(engine, max_ctas):
 
 
 @pytest.mark.parametrize("engine", ENGINES)
-@pytest.mark.parametrize("piece,stages", [(256, 2), (1024, 3), (4096, 16), (65536, 3)])
-def test_piece_and_stage_shapes(engine, piece, stages):
+@pytest.mark.parametrize("piece,stages", [(256, 2), (1024, 3), (4096, 4), (4096, 16), (16384, 8), (65536, 3)])
+@pytest.mark.parametrize("unroll", [4, 8, 16])
+def test_piece_and_stage_shapes(engine, piece, stages, unroll):
+    if engine == dk.DYNA_ENGINE_BULK and unroll != 8:
+        pytest.skip("unroll applies to VEC only")
     g = Geom(2, 8, 128, 2, 16, 64)  # row 2 KiB
-    _parity(g, g, 512, (0, 333), (0, 2), 128, engine=engine, piece_bytes=piece, stages=stages)
+    for flags in (0, dk.DYNA_MIGRATE_SIGNAL):
+        _parity(g, g, 512, (0, 333), (0, 2), 128, engine=engine, piece_bytes=piece, stages=stages, unroll=unroll,
+                flags=flags)
 
 
 # ------------------------------------------------ medium geometries: paper rows, several tiles, ragged tails
@@ -264,3 +269,16 @@ def test_config5_qwen72b_shard_pair():
     for r, (ts, td) in zip(reqs, tabs):
         migrate_and_wait(src, ts, dst, td, (0, r.s), (0, 80), 1024)
         assert torch_rows_equal(src, ts, dst, td, (0, r.s), (0, 80))
+
+
+def test_auto_uses_calibration_table():
+    """AUTO picks per (row bytes, call size) from the table; a bogus-but-valid table still migrates correctly."""
+    base = dk.dyna_kv_calib_get()
+    try:
+        dk.dyna_kv_calib_set([(256, 0, 64, dk.DYNA_VARIANT_STAGED, dk.DYNA_ENGINE_BULK, 4096, 4, 0),
+                              (0, 0, 1 << 30, dk.DYNA_VARIANT_FUSED, dk.DYNA_ENGINE_VEC, 4096, 0, 16)])
+        for tr in ((0, 50), (0, 100), (10, 200)):
+            _parity(kvgen.TOY, kvgen.TOY, 256, tr, (0, 2), 32)
+    finally:
+        dk.dyna_kv_calib_set([])
+    assert dk.dyna_kv_calib_get() == base
