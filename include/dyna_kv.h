@@ -134,7 +134,8 @@ typedef struct {
  * (0 = any), whose destination locality matches peer (0 = same GPU, 1 = other
  * GPU), and whose call size (tokens in token_range) <= max_chunk_tokens (in
  * the paper's per-chunk push, a call moves one chunk, so this is the
- * chunk size); among matching entries the smallest max_chunk_tokens wins.  The library starts with the
+ * chunk size).  Entries for the exact row size are preferred over generic
+ * ones; within each class the smallest covering max_chunk_tokens wins.  The library starts with the
  * table measured on B200 (profiles/), replaceable at run time. */
 typedef struct {
     int32_t row_bytes;

@@ -290,19 +290,24 @@ const dyna_kv_calib_entry kCalibDefault[] = {
 std::mutex g_calib_mu;
 std::vector<dyna_kv_calib_entry> g_calib(std::begin(kCalibDefault), std::end(kCalibDefault) - 1);
 
-// Best calibrated entry for (row bytes, locality, chunk tokens); returns false if none.
+// Best calibrated entry for (row bytes, locality, call tokens): entries for this
+// exact row size first, generic (row_bytes == 0) ones only if none matches;
+// within a class the smallest max_chunk_tokens that covers the call wins.
 bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out) {
   std::lock_guard<std::mutex> lk(g_calib_mu);
-  const dyna_kv_calib_entry* best = nullptr;
-  for (const auto& e : g_calib) {
-    if ((e.row_bytes != 0 && e.row_bytes != row) || e.peer != peer || c > e.max_chunk_tokens) continue;
-    if (!best || e.max_chunk_tokens < best->max_chunk_tokens ||
-        (e.max_chunk_tokens == best->max_chunk_tokens && best->row_bytes == 0 && e.row_bytes != 0))
-      best = &e;
+  for (int pass = 0; pass < 2; ++pass) {
+    const dyna_kv_calib_entry* best = nullptr;
+    for (const auto& e : g_calib) {
+      const bool row_ok = pass == 0 ? e.row_bytes == row : e.row_bytes == 0;
+      if (!row_ok || e.peer != peer || c > e.max_chunk_tokens) continue;
+      if (!best || e.max_chunk_tokens < best->max_chunk_tokens) best = &e;
+    }
+    if (best) {
+      *out = *best;
+      return true;
+    }
   }
-  if (!best) return false;
-  *out = *best;
-  return true;
+  return false;
 }
 
 Side paged(const dyna_kv_pool* pool, const int32_t* ids) {

@@ -45,7 +45,12 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "calibration.json"))
     ap.add_argument("--inc", default=os.path.join(ROOT, "gpurun_out", "calib_default.inc"))
     ap.add_argument("--min-ms", type=float, default=15.0)
+    ap.add_argument("--select", help="re-run only the selection on a saved calibration.json")
     args = ap.parse_args()
+    if args.select:
+        d = json.load(open(args.select))
+        write_outputs(args, d["measurements"], d["device"])
+        return
     torch.cuda.set_device(0)
     stream = torch.cuda.Stream()
     cs = stream.cuda_stream
@@ -91,26 +96,56 @@ def main():
             chosen.append(best)
         src.close()
         dst.close()
-    # compress consecutive buckets with the same choice into one entry (largest c of the run)
-    entries = []
-    for row in GEOMS:
-        seq = [b for b in chosen if b["row_bytes"] == row]
-        for i, b in enumerate(seq):
-            key = (b["variant"], b["engine"], b["piece"], b["stages"], b["unroll"])
+    write_outputs(args, rows, torch.cuda.get_device_name(0))
+
+
+def select(rows):
+    """Per (row bytes, chunk bucket) pick the candidate with the best geometric-mean GB/s over the
+    bucket and its two neighbours — event timing of one call is quantised (~0.5 us), so a plain
+    per-bucket argmax flips between candidates that are within noise of each other."""
+    import math
+    chosen, entries = [], []
+    for row in sorted({r["row_bytes"] for r in rows}, reverse=True):
+        chunks = sorted({r["chunk"] for r in rows if r["row_bytes"] == row})
+        key = lambda r: (r["variant"], r["engine"], r["piece"], r["stages"], r["unroll"])  # noqa: E731
+        perf = {}
+        for r in rows:
+            if r["row_bytes"] == row:
+                perf[(r["chunk"], key(r))] = r["GBps"]
+        cands = sorted({key(r) for r in rows if r["row_bytes"] == row})
+        seq = []
+        for i, c in enumerate(chunks):
+            win = chunks[max(0, i - 1): i + 2]
+            score = {k: sum(math.log(perf[(w, k)]) for w in win) / len(win) for k in cands}
+            best = max(cands, key=lambda k: (score[k], perf[(c, k)]))
+            seq.append((c, best, perf[(c, best)]))
+            chosen.append({"row_bytes": row, "chunk": c, "choice": best, "GBps": perf[(c, best)],
+                           "best_single": max(perf[(c, k)] for k in cands)})
+        for i, (c, best, _) in enumerate(seq):
             nxt = seq[i + 1] if i + 1 < len(seq) else None
-            if nxt and (nxt["variant"], nxt["engine"], nxt["piece"], nxt["stages"], nxt["unroll"]) == key:
+            if nxt and nxt[1] == best:
                 continue
-            maxc = b["chunk"] if nxt else (1 << 30)
-            entries.append((row, 0, maxc) + key)
+            entries.append((row, 0, c if nxt else (1 << 30)) + tuple(best))
+    return chosen, entries
+
+
+def write_outputs(args, rows, device):
+    chosen, entries = select(rows)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
-    json.dump({"device": torch.cuda.get_device_name(0), "candidates": CANDIDATES, "measurements": rows,
+    json.dump({"device": device, "candidates": CANDIDATES, "measurements": rows,
                "chosen": chosen, "entries": entries}, open(args.out, "w"), indent=1)
     with open(args.inc, "w") as f:
-        f.write("// Built-in calibration table, generated by scripts/calibrate.py on "
-                f"{torch.cuda.get_device_name(0)} (see profiles/*calibration*).\n")
+        f.write(f"// Built-in calibration table, generated by scripts/calibrate.py on {device}\n")
+        f.write("// (measurements and choices: profiles/*calibration*.json).  Same-GPU entries only;\n")
+        f.write("// peer (NVLink) migrations fall back to FUSED + VEC until measured on a multi-GPU box.\n")
         f.write("// row_bytes, peer, max_chunk_tokens, variant, engine, piece_bytes, stages, unroll\n")
         for e in entries:
             f.write("    {" + ", ".join(str(x) for x in e) + "},\n")
+        # generic fallback for other row sizes: the table of the most common (GQA, 2 KiB) row
+        gen = [e for e in entries if e[0] == 2048] or entries
+        f.write("    // generic fallback (row_bytes 0) = the 2 KiB-row choices\n")
+        for e in gen:
+            f.write("    {" + ", ".join(str(x) for x in (0,) + tuple(e[1:])) + "},\n")
     print(json.dumps({"entries": entries}))
 
 
