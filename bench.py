@@ -210,6 +210,9 @@ def run_dyna(args, rank, world, local_rank):
     def max_over_ranks(x: float) -> float:
         return dd.max_over_ranks(x, device=f"cuda:{dev}")
 
+    probe = step(0)
+    plan = dk.dyna_kv_xfer_plan(probe)
+    dk.dyna_kv_wait(probe)
     clocks = Clocks(dev)
     # warm-up (untimed), then ~0.5 s of untimed load so the clock samples see the part under load
     xs = [step(i) for i in range(args.warmup)]
@@ -245,29 +248,24 @@ def run_dyna(args, rank, world, local_rank):
     kern_ms = statistics.fmean(a.elapsed_time(b) for a, b in zip(ev_a, ev_b))
     kern_ms = max_over_ranks(kern_ms)
 
-    # ---------------- e2e through the public API with host buffers: every step copies the
-    # request's two block tables from pinned host memory, migrates with per-chunk flags and
-    # reads the chunk flags back into pinned host memory; completion is taken from
-    # dyna_kv_wait.  Steps are issued one ahead of the wait (the async API as a serving
-    # loop uses it), so host work for step k+1 overlaps the device work of step k.
+    # ---------------- e2e through the public API with host buffers: every step passes the
+    # request's two block tables as HOST arrays (the library copies the entries it needs to
+    # the device on the stream), migrates with per-chunk flags, and reads the chunk flags
+    # back into pinned host memory; completion is taken from dyna_kv_wait.  Steps are
+    # issued one ahead of the wait (the async API as a serving loop uses it), so host work
+    # for step k+1 overlaps the device work of step k.
     nchunks = -(-S_SPLIT // CHUNK)
-    host_tabs = [(torch.from_numpy(ts).pin_memory(), torch.from_numpy(td).pin_memory()) for ts, td in tabs]
-    dev_tabs = [(torch.empty_like(a, device=f"cuda:{dev}"), torch.empty_like(b, device=f"cuda:{dev}"))
-                for a, b in host_tabs]
-    e2e_tables = [(dk.table(src, a, ts), dk.table(dst, b, td)) for (a, b), (ts, td) in zip(dev_tabs, tabs)]
+    e2e_tables = [(dk.table(src, None, ts), dk.table(dst, None, td)) for ts, td in tabs]
     flags_host = [torch.zeros(nchunks, dtype=torch.int64).pin_memory() for _ in range(N_SETS)]
     sig_opts = dk.opts(variant=args.variant, engine=args.engine, flags=dk.DYNA_MIGRATE_SIGNAL)
     sender = rank
     flag_pool = dst.handle
-    h2d = sum(a.numel() * 4 + b.numel() * 4 for a, b in host_tabs) // N_SETS
+    blocks = -(-S_SPLIT // g.block_size)
+    h2d = 2 * blocks * 4            # the table entries [0, s) reaches, both tables
     d2h = nchunks * 8
 
     def e2e_issue(k):
         i = k % N_SETS
-        (ha, hb), (da, db) = host_tabs[i], dev_tabs[i]
-        with torch.cuda.stream(stream):
-            da.copy_(ha, non_blocking=True)
-            db.copy_(hb, non_blocking=True)
         st, dt_ = e2e_tables[i]
         x = dk.dyna_kv_migrate_ex(st, dt_, (0, S_SPLIT), (0, g.num_layers), CHUNK, cs, sig_opts)
         epoch = dk.dyna_kv_xfer_info(x)[0]
@@ -321,8 +319,8 @@ def run_dyna(args, rank, world, local_rank):
             achieved = 2 * payload / (kern_ms / 1e3) / 1e9  # HBM read + write bytes per launch / duration
             roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                     "traffic": ncu_traffic(), "peak_source": hbm_src,
-                    "kernel": "dynakv::k_copy_vec (K4-local fused reblock)" if args.engine != dk.DYNA_ENGINE_BULK
-                    else "dynakv::k_copy_bulk (K4-local fused reblock)",
+                    "kernel": ("dynakv::k_copy_bulk" if plan["engine"] == dk.DYNA_ENGINE_BULK
+                               else "dynakv::k_copy_vec") + " (K4-local fused reblock)",
                     "algorithmic_bytes_per_launch": 2 * payload, "kernel_ms": kern_ms,
                     "same_size_torch_copy_gbs": same_size_copy}
         else:
@@ -337,7 +335,7 @@ def run_dyna(args, rank, world, local_rank):
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": WORKLOAD, "kv_dtype": "fp16", "payload_bytes_per_step": payload,
                        "pairs": "rank r -> rank (r+1) % N over CUDA IPC" if world > 1 else "intra-device reblock",
-                       "variant": args.variant, "engine": args.engine,
+                       "variant": args.variant, "engine": args.engine, "resolved_plan": plan,
                        "l2": f"{N_SETS} disjoint block-table sets rotated per step; 1 GiB of HBM traffic per step > 126 MB L2"},
             "tokens_per_s": world * args.steps * S_SPLIT / (total_ms / 1e3),
             "roofline": roof,

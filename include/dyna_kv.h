@@ -92,12 +92,16 @@ typedef struct dyna_kv_xfer* dyna_kv_xfer_t;
  *                   device (device memory of the source GPU, or of a peer
  *                   with P2P enabled).  Caller-owned; must stay valid and
  *                   unmodified until dyna_kv_wait returns (like the source of
- *                   cudaMemcpyAsync).
- *   host_block_ids  optional HOST copy of the same ids.  When given for both
- *                   tables, ids are range-checked and destination aliasing is
- *                   rejected synchronously (DYNA_ERANGE / DYNA_EALIAS).  When
- *                   NULL, ids are range-checked on the device: offending rows
- *                   are skipped and dyna_kv_wait returns DYNA_ERANGE. */
+ *                   cudaMemcpyAsync).  May be NULL when host_block_ids is
+ *                   given: the library then copies the entries the call needs
+ *                   ([0, last touched block]) to the device itself, ordered on
+ *                   `stream` (a scheduler's tables usually live on the host).
+ *   host_block_ids  HOST copy of the same ids.  When given for both tables,
+ *                   ids are range-checked and destination aliasing is
+ *                   rejected synchronously (DYNA_ERANGE / DYNA_EALIAS); the
+ *                   host array may be reused as soon as the call returns.
+ *                   When NULL, ids are range-checked on the device: offending
+ *                   rows are skipped and dyna_kv_wait returns DYNA_ERANGE. */
 typedef struct {
     dyna_kv_pool_t pool;
     const int32_t* block_ids;
@@ -178,6 +182,22 @@ DYNA_API dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table d
                                int32_t chunk_tokens, struct CUstream_st* stream,
                                const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
 
+/* Many migrations in ONE kernel launch (a batch of short
+ * requests, e.g. configs[2]'s 64-request skewed batch).  Every non-empty entry
+ * is validated like dyna_kv_migrate; all sources must live on one device (the
+ * launching device, `stream`'s) and share one row size; destinations may be
+ * any reachable pools.  FUSED variant only, no per-chunk signalling
+ * (DYNA_ENOTSUP otherwise).  n <= DYNA_MAX_BATCH.  The descriptors are copied
+ * before the call returns; block tables follow dyna_block_table's rules. */
+#define DYNA_MAX_BATCH 16384
+typedef struct {
+    dyna_block_table src, dst;
+    dyna_range token_range;
+} dyna_kv_migration;
+DYNA_API dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna_range layer_range,
+                                           int32_t chunk_tokens, struct CUstream_st* stream,
+                                           const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
+
 /* Block the host until every chunk is resident in the destination, report
  * deferred errors (DYNA_ECUDA, DYNA_ERANGE from device-side id checks), free
  * the handle. */
@@ -197,6 +217,11 @@ DYNA_API dyna_status dyna_kv_stream_wait(dyna_kv_xfer_t xfer, struct CUstream_st
  * holds a value >= epoch.  Migrations from one sender into one destination
  * pool that request signalling must be ordered on one stream. */
 DYNA_API dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t xfer, uint64_t* epoch, int32_t* num_chunks, int32_t* sender);
+
+/* What a migration resolved to (AUTO choices included) and how many kernels
+ * it launched — for logs and benchmarks.  Any pointer may be NULL. */
+DYNA_API dyna_status dyna_kv_xfer_plan(dyna_kv_xfer_t xfer, int32_t* variant, int32_t* engine, int32_t* piece_bytes,
+                                       int32_t* stages, int32_t* unroll, int32_t* launches);
 
 /* Enqueue on `stream` (a stream of the DESTINATION pool's device) a device
  * wait (acquire, system scope) until chunk `chunk` from `sender` reaches

@@ -34,8 +34,10 @@ EXPORTS = (
     "dyna_kv_migrate_ex", "dyna_kv_wait", "dyna_kv_query", "dyna_kv_stream_wait", "dyna_kv_xfer_info",
     "dyna_kv_stream_wait_chunk", "dyna_kv_last_error", "dyna_kv_poll_error", "dyna_kv_launch_count",
     "dyna_kv_enable_peer", "dyna_kv_pool_export", "dyna_kv_pool_import", "dyna_kv_debug_fill",
-    "dyna_kv_copy_flags", "dyna_kv_calib_set", "dyna_kv_calib_get",
+    "dyna_kv_copy_flags", "dyna_kv_calib_set", "dyna_kv_calib_get", "dyna_kv_migrate_batch",
+    "dyna_kv_xfer_plan",
 )
+DYNA_MAX_BATCH = 16384
 
 
 class dyna_kv_pool_desc(ctypes.Structure):
@@ -50,6 +52,10 @@ class dyna_block_table(ctypes.Structure):
 
 class dyna_range(ctypes.Structure):
     _fields_ = [("begin", ctypes.c_int64), ("end", ctypes.c_int64)]
+
+
+class dyna_kv_migration(ctypes.Structure):
+    _fields_ = [("src", dyna_block_table), ("dst", dyna_block_table), ("token_range", dyna_range)]
 
 
 class dyna_kv_opts(ctypes.Structure):
@@ -87,10 +93,13 @@ def _load():
                                  p(vp)]),
         "dyna_kv_migrate_ex": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
                                     vp, p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_migrate_batch": (st, [p(dyna_kv_migration), ctypes.c_int32, dyna_range, ctypes.c_int32, vp,
+                                       p(dyna_kv_opts), p(vp)]),
         "dyna_kv_wait": (st, [vp]),
         "dyna_kv_query": (st, [vp]),
         "dyna_kv_stream_wait": (st, [vp, vp]),
         "dyna_kv_xfer_info": (st, [vp, p(ctypes.c_uint64), p(ctypes.c_int32), p(ctypes.c_int32)]),
+        "dyna_kv_xfer_plan": (st, [vp] + [p(ctypes.c_int32)] * 6),
         "dyna_kv_stream_wait_chunk": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64,
                                            vp]),
         "dyna_kv_copy_flags": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp]),
@@ -151,6 +160,16 @@ def dyna_kv_migrate_ex(src: dyna_block_table, dst: dyna_block_table, token_range
     return out.value
 
 
+def dyna_kv_migrate_batch(migs, layer_range, chunk_tokens: int, stream: int = 0,
+                          opts: dyna_kv_opts | None = None) -> int:
+    """migs: list of (src dyna_block_table, dst dyna_block_table, (t0, t1))."""
+    arr = (dyna_kv_migration * max(1, len(migs)))(*[dyna_kv_migration(a, b, dyna_range(*tr)) for a, b, tr in migs])
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_migrate_batch(arr, len(migs), dyna_range(*layer_range), chunk_tokens, ctypes.c_void_p(stream),
+                                     ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
+    return out.value
+
+
 def dyna_kv_wait(xfer: int) -> None:
     _check(lib.dyna_kv_wait(ctypes.c_void_p(xfer)))
 
@@ -171,6 +190,12 @@ def dyna_kv_xfer_info(xfer: int) -> tuple[int, int, int]:
     e, n, s = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_int32()
     _check(lib.dyna_kv_xfer_info(ctypes.c_void_p(xfer), ctypes.byref(e), ctypes.byref(n), ctypes.byref(s)))
     return e.value, n.value, s.value
+
+
+def dyna_kv_xfer_plan(xfer: int) -> dict:
+    v = [ctypes.c_int32() for _ in range(6)]
+    _check(lib.dyna_kv_xfer_plan(ctypes.c_void_p(xfer), *[ctypes.byref(a) for a in v]))
+    return dict(zip(("variant", "engine", "piece_bytes", "stages", "unroll", "launches"), (a.value for a in v)))
 
 
 def dyna_kv_stream_wait_chunk(dst_pool: int, sender: int, chunk: int, epoch: int, timeout_ns: int = 0,
@@ -272,9 +297,13 @@ class Pool:
 
 
 def table(pool: Pool, ids, host_ids=None) -> dyna_block_table:
-    """Block table over `pool`.  ids: int32 CUDA tensor; host_ids: optional numpy int32 (validation)."""
+    """Block table over `pool`.  ids: int32 CUDA tensor, or None for a host-resident table
+    (host_ids required; the library uploads it); host_ids: numpy int32 (also enables validation)."""
     import numpy as np
-    t = dyna_block_table(pool.handle, ids.data_ptr(), None, ids.numel())
+    if ids is None and host_ids is None:
+        raise DynaKVError(DYNA_EINVAL, "a table needs device ids or host ids")
+    n = ids.numel() if ids is not None else len(host_ids)
+    t = dyna_block_table(pool.handle, ids.data_ptr() if ids is not None else None, None, n)
     t._keep = [ids]
     if host_ids is not None:
         h = np.ascontiguousarray(host_ids, dtype=np.int32)
@@ -296,3 +325,13 @@ def migrate(src: dyna_block_table, dst: dyna_block_table, token_range, layer_ran
     else:
         s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     return dyna_kv_migrate_ex(src, dst, token_range, layer_range, chunk_tokens, s, opts(**kw) if kw else None)
+
+
+def migrate_batch(migs, layer_range, chunk_tokens, stream=None, **kw) -> int:
+    """dyna_kv_migrate_batch on a torch stream; migs: list of (src_table, dst_table, (t0, t1))."""
+    import torch
+    if stream is None:
+        s = torch.cuda.current_stream().cuda_stream
+    else:
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return dyna_kv_migrate_batch(migs, layer_range, chunk_tokens, s, opts(**kw) if kw else None)

@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <string>
@@ -136,6 +137,7 @@ struct dyna_kv_pool {
 
 struct dyna_kv_xfer {
   cudaEvent_t ev = nullptr;
+  int32_t variant = 0, engine = 0, piece = 0, stages = 0, unroll = 0, launches = 0;
   int dev = 0;
   bool empty = false;
   uint64_t epoch = 0;
@@ -213,7 +215,7 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   return p;
 }
 
-template <int U, bool SIG>
+template <int U, bool SIG, class Src>
 int vec_occupancy() {
   static std::map<int, int> cache;  // per device
   static std::mutex mu;
@@ -223,7 +225,7 @@ int vec_occupancy() {
   auto it = cache.find(dev);
   if (it != cache.end()) return it->second;
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copy_vec<U, SIG>, kVecThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copy_vec<U, SIG, Src>, kVecThreads, 0);
   if (occ <= 0) occ = 1;
   cache[dev] = occ;
   return occ;
@@ -238,48 +240,62 @@ int64_t balanced_workers(int64_t n_items, int64_t max_workers) {
   return (n_items + rounds - 1) / rounds;
 }
 
-template <int U>
-void launch_vec(const Plan& p, int64_t max_grid, int sms, cudaStream_t st) {
-  const bool sig = p.counters != nullptr;
-  const int occ = sig ? vec_occupancy<U, true>() : vec_occupancy<U, false>();
+template <int U, bool SIG, class Src>
+void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cudaStream_t st) {
+  const int occ = vec_occupancy<U, SIG, Src>();
   constexpr int wpc = kVecThreads / 32;  // warps per CTA
   int64_t max_ctas = (int64_t)sms * occ;
   if (max_grid > 0) max_ctas = std::min<int64_t>(max_ctas, max_grid);
-  const int64_t warps = balanced_workers(p.n_items, max_ctas * wpc);
+  const int64_t warps = balanced_workers(n_items, max_ctas * wpc);
   const int64_t grid = (warps + wpc - 1) / wpc;
-  if (sig)
-    k_copy_vec<U, true><<<(unsigned)grid, kVecThreads, 0, st>>>(p);
-  else
-    k_copy_vec<U, false><<<(unsigned)grid, kVecThreads, 0, st>>>(p);
+  k_copy_vec<U, SIG, Src><<<(unsigned)grid, kVecThreads, 0, st>>>(src);
 }
 
-// Launch one copy kernel.  engine: DYNA_ENGINE_VEC / BULK.
-dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev,
+template <bool SIG, class Src>
+dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, int64_t max_grid, int sms,
                         cudaStream_t st) {
-  if (p.n_items == 0) return DYNA_OK;
+  const size_t smem = (size_t)stages * piece;
+  auto kern = k_copy_bulk<SIG, Src>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem));
+  if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
+  int64_t cap = (int64_t)sms * occ;
+  if (max_grid > 0) cap = std::min<int64_t>(cap, max_grid);
+  kern<<<(unsigned)balanced_workers(n_items, cap), 32, smem, st>>>(src, stages);
+  return DYNA_OK;
+}
+
+// Launch one copy kernel over `src` (n_items items; piece bytes per item).
+// engine: DYNA_ENGINE_VEC / BULK.  SIG: per-chunk signalling (single plan only).
+template <class Src>
+dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int engine, int max_ctas, int stages,
+                       int unroll, int dev, cudaStream_t st) {
+  if (n_items == 0) return DYNA_OK;
   DevInfo* di = dev_info(dev);
-  const bool sig = p.counters != nullptr;
   if (engine == DYNA_ENGINE_BULK) {
-    const size_t smem = (size_t)stages * p.piece;
-    auto kern = sig ? k_copy_bulk<true> : k_copy_bulk<false>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem));
-    if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
-    int64_t cap = (int64_t)di->sms * occ;
-    if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
-    const int64_t grid = balanced_workers(p.n_items, cap);
-    kern<<<(unsigned)grid, 32, smem, st>>>(p, stages);
+    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st)
+                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st);
+    if (r) return r;
   } else if (unroll == 4) {
-    launch_vec<4>(p, max_ctas, di->sms, st);
+    sig ? launch_vec<4, true>(src, n_items, max_ctas, di->sms, st)
+        : launch_vec<4, false>(src, n_items, max_ctas, di->sms, st);
   } else if (unroll == 16) {
-    launch_vec<16>(p, max_ctas, di->sms, st);
+    sig ? launch_vec<16, true>(src, n_items, max_ctas, di->sms, st)
+        : launch_vec<16, false>(src, n_items, max_ctas, di->sms, st);
   } else {
-    launch_vec<8>(p, max_ctas, di->sms, st);
+    sig ? launch_vec<8, true>(src, n_items, max_ctas, di->sms, st)
+        : launch_vec<8, false>(src, n_items, max_ctas, di->sms, st);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   CUDA_TRY(cudaGetLastError());
   return DYNA_OK;
+}
+
+dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev,
+                        cudaStream_t st) {
+  SingleSource src{p};
+  return launch_src(src, p.n_items, p.counters != nullptr, p.piece, engine, max_ctas, stages, unroll, dev, st);
 }
 
 // ------------------------------------------------------------------ calibration (a6)
@@ -444,6 +460,264 @@ dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t 
   return DYNA_OK;
 }
 
+// ------------------------------------------------------------------ staged variant (a2, a3, a4)
+// K1 gather -> source staging slot, K2 slot -> destination-side slot, K3 scatter
+// slot -> destination rows (+ per-chunk flag).  Chunks are cut into sub-chunks
+// that fit one staging slot; two slots per side alternate.  Same device:
+// everything in stream order.  Two devices of one process: K3 runs on a
+// library stream of the destination device, ordered with events.
+dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, const int32_t* dids, dyna_range tr,
+                       int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
+                       int max_ctas, cudaStream_t stream, dyna_kv_xfer* x) {
+  if (D->imported)
+    return fail(DYNA_ENOTSUP, "STAGED variant into an imported (cross-process) pool is not supported; use FUSED");
+  const int64_t row = S->row;
+  const bool cross = D->dev != S->dev;
+  const int64_t nchunks = (tr.end - tr.begin + c - 1) / c;
+  DevInfo* ddi = dev_info(D->dev);
+  cudaStream_t dstream = stream;
+  if (cross) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!ddi->aux) {
+      DeviceGuard g(D->dev);
+      CUDA_TRY(cudaStreamCreateWithFlags(&ddi->aux, cudaStreamNonBlocking));
+    }
+    dstream = ddi->aux;
+  }
+  const int64_t tok_bytes = row * lm * 2;
+  const int64_t sc = std::max<int64_t>(1, std::min<int64_t>(c, kStageSlotBytes / tok_bytes));
+  const int64_t slot = sc * tok_bytes;
+  char *sbuf = nullptr, *dbuf = nullptr;
+  dyna_status r = channel_staging(S, D, slot, &sbuf, &dbuf);
+  if (r) return r;
+  unsigned long long* counters = nullptr;
+  if (signal) {
+    if ((r = channel_counters(S, D, D->dev, &counters))) return r;
+    x->epoch = next_epoch(S->desc.instance, D);
+  }
+  cudaEvent_t done_src[2] = {nullptr, nullptr};  // K2 of slot i finished (cross-device)
+  cudaEvent_t done_dst[2] = {nullptr, nullptr};  // K3 of slot i finished (cross-device)
+  if (cross)
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(get_event(S->dev, &done_src[i]));
+      DeviceGuard g(D->dev);
+      CUDA_TRY(get_event(D->dev, &done_dst[i]));
+    }
+  int64_t sub = 0;
+  for (int64_t k = 0; k < nchunks && !r; ++k) {
+    const int64_t a = tr.begin + k * c, b = std::min(a + c, tr.end);
+    for (int64_t sa = a; sa < b && !r; sa += sc, ++sub) {
+      const int64_t sb = std::min(sa + sc, b);
+      const int si = (int)(sub & 1);
+      char* sslot = sbuf + si * slot;
+      char* dslot = dbuf + si * slot;
+      if (cross && sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[si], 0));
+      Plan k1 = make_plan(paged(S, sids), linear(sslot), row, sa, sb, l0, lm, sb - sa, S->desc.block_size, piece);
+      if ((r = launch_copy(k1, engine, max_ctas, stages, unroll, S->dev, stream))) break;
+      // K2: the sub-chunk slot is [lm][2][n][row] = two contiguous halves
+      // (K and V of all layers): a flat plan with one token of `half` bytes.
+      Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
+      if ((r = launch_copy(k2, engine, max_ctas, stages, unroll, S->dev, stream))) break;
+      Plan k3 = make_plan(linear(dslot), paged(D, dids), row, sa, sb, l0, lm, sb - sa, D->desc.block_size, piece);
+      k3.mig_t0 = tr.begin;
+      k3.mig_t1 = tr.end;
+      k3.sig_c = (int32_t)c;
+      if (signal) {
+        k3.counters = counters;
+        k3.flags = D->inbox + (size_t)S->desc.instance * DYNA_MAX_CHUNKS;
+        k3.epoch = x->epoch;
+      }
+      if (cross) {
+        CUDA_TRY(cudaEventRecord(done_src[si], stream));
+        DeviceGuard g(D->dev);
+        CUDA_TRY(cudaStreamWaitEvent(dstream, done_src[si], 0));
+        if ((r = launch_copy(k3, engine, max_ctas, stages, unroll, D->dev, dstream))) break;
+        CUDA_TRY(cudaEventRecord(done_dst[si], dstream));
+      } else {
+        if ((r = launch_copy(k3, engine, max_ctas, stages, unroll, S->dev, stream))) break;
+      }
+    }
+  }
+  if (cross) {  // the migration completes on `stream` once the last scatters are done
+    const int last = (int)((sub - 1) & 1);
+    CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[last], 0));
+    if (sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[last ^ 1], 0));
+    for (int i = 0; i < 2; ++i) {
+      put_event(S->dev, done_src[i]);
+      put_event(D->dev, done_dst[i]);
+    }
+  }
+  return r;
+}
+
+// ------------------------------------------------------------------ upload ring
+// Host-resident inputs (block tables passed only as host_block_ids, batch
+// descriptors) travel to the device through a per-device ring: pinned host
+// staging -> one cudaMemcpyAsync on the caller's stream -> device buffer read
+// by the kernel that follows on the same stream.  A span is reused only after
+// the event recorded behind its consumer kernel has completed.
+constexpr size_t kRingBytes = 8u << 20;
+
+struct UploadRing {
+  char* host = nullptr;
+  char* dev = nullptr;
+  size_t head = 0;
+  struct Span {
+    size_t b, e;
+    cudaEvent_t ev;
+  };
+  std::deque<Span> live;
+  std::vector<cudaEvent_t> free_ev;
+  std::mutex mu;
+};
+std::mutex g_rings_mu;
+std::map<int, UploadRing*> g_rings;
+
+// Holds the ring's lock from upload() until finish() records the release event.
+class RingLease {
+ public:
+  explicit RingLease(int dev) : dev_(dev) {}
+  ~RingLease() {
+    if (ring_) ring_->mu.unlock();
+  }
+
+  // Reserve `bytes` of the ring: *hptr (pinned host) is filled by the caller,
+  // then copy() moves it to *dptr on the stream.  At most once per lease.
+  dyna_status reserve(size_t bytes, char** dptr, char** hptr) {
+    {
+      std::lock_guard<std::mutex> lk(g_rings_mu);
+      UploadRing*& r = g_rings[dev_];
+      if (!r) r = new UploadRing();
+      ring_ = r;
+    }
+    ring_->mu.lock();  // held until the lease is destroyed (after finish())
+    UploadRing& R = *ring_;
+    if (!R.host) {
+      DeviceGuard g(dev_);
+      if (cudaHostAlloc(&R.host, kRingBytes, cudaHostAllocPortable) != cudaSuccess ||
+          cudaMalloc(&R.dev, kRingBytes) != cudaSuccess)
+        return fail(DYNA_ENOMEM, "upload ring (%zu B pinned + device)", kRingBytes);
+    }
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes > kRingBytes) return fail(DYNA_ENOMEM, "host-resident inputs of %zu B exceed the upload ring", bytes);
+    size_t b = R.head;
+    if (b + bytes > kRingBytes) b = 0;
+    const size_t e = b + bytes;
+    // free every live span that overlaps [b, e) (spans sit in allocation order)
+    while (!R.live.empty() && R.live.front().b < e && b < R.live.front().e) {
+      cudaEventSynchronize(R.live.front().ev);
+      R.free_ev.push_back(R.live.front().ev);
+      R.live.pop_front();
+    }
+    R.head = e;
+    span_b_ = b;
+    span_e_ = e;
+    *dptr = R.dev + b;
+    *hptr = R.host + b;
+    return DYNA_OK;
+  }
+
+  dyna_status copy(cudaStream_t st) {
+    UploadRing& R = *ring_;
+    CUDA_TRY(cudaMemcpyAsync(R.dev + span_b_, R.host + span_b_, span_e_ - span_b_, cudaMemcpyHostToDevice, st));
+    return DYNA_OK;
+  }
+
+  // After the consumer kernel(s) are enqueued on `st`.
+  dyna_status finish(cudaStream_t st) {
+    if (!ring_ || span_e_ == 0) return DYNA_OK;
+    UploadRing& R = *ring_;
+    cudaEvent_t ev = nullptr;
+    if (!R.free_ev.empty()) {
+      ev = R.free_ev.back();
+      R.free_ev.pop_back();
+    } else {
+      DeviceGuard g(dev_);
+      CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(ev, st));
+    R.live.push_back({span_b_, span_e_, ev});
+    span_e_ = 0;
+    return DYNA_OK;
+  }
+
+ private:
+  int dev_;
+  UploadRing* ring_ = nullptr;
+  size_t span_b_ = 0, span_e_ = 0;
+};
+
+// ------------------------------------------------------------------ shared validation
+dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
+  *o = dyna_kv_opts{};
+  if (opts) *o = *opts;
+  if (o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > 2 || o->max_ctas < 0 || o->piece_bytes < 0 ||
+      o->piece_bytes % 16 || o->stages < 0 || o->stages == 1 || o->stages > kMaxStages ||
+      (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16))
+    return fail(DYNA_EINVAL, "invalid dyna_kv_opts");
+  return DYNA_OK;
+}
+
+// Geometry, ranges, table presence and (with host ids) ids / aliasing.  *empty: nothing to move.
+dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
+                          int32_t chunk_tokens, bool* empty) {
+  if (!src.pool || !dst.pool) return fail(DYNA_EINVAL, "NULL pool in a block table");
+  const dyna_kv_pool_desc &gs = src.pool->desc, &gd = dst.pool->desc;
+  if (gs.num_layers != gd.num_layers || gs.num_kv_heads != gd.num_kv_heads || gs.head_dim != gd.head_dim ||
+      gs.elem_bytes != gd.elem_bytes)
+    return fail(DYNA_EGEOM, "source and destination geometry differ (L, H, d, e)");
+  if (lr.begin < 0 || lr.begin > lr.end || lr.end > gs.num_layers)
+    return fail(DYNA_ERANGE, "layer range [%lld, %lld) outside [0, %d)", (long long)lr.begin, (long long)lr.end,
+                gs.num_layers);
+  if (tr.begin < 0 || tr.begin > tr.end) return fail(DYNA_ERANGE, "bad token range");
+  *empty = tr.begin == tr.end || lr.begin == lr.end;
+  if (*empty) return DYNA_OK;
+  if (chunk_tokens <= 0) return fail(DYNA_ERANGE, "chunk_tokens must be > 0");
+  if (src.len < 0 || dst.len < 0 || tr.end > src.len * gs.block_size || tr.end > dst.len * gd.block_size)
+    return fail(DYNA_ERANGE, "token range end %lld exceeds a block table (src %lld, dst %lld tokens)",
+                (long long)tr.end, (long long)(src.len * gs.block_size), (long long)(dst.len * gd.block_size));
+  if ((!src.block_ids && !src.host_block_ids) || (!dst.block_ids && !dst.host_block_ids))
+    return fail(DYNA_EINVAL, "a block table has neither device nor host block ids");
+  return check_host_tables(src, dst, tr.begin, tr.end);
+}
+
+// The destination must be addressable from the source (launching) device.
+dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D) {
+  if (D->imported) {
+    if (D->dev != S->dev)
+      return fail(DYNA_EPEER, "imported destination is mapped on device %d, source is on %d", D->dev, S->dev);
+    return DYNA_OK;
+  }
+  return D->dev == S->dev ? DYNA_OK : ensure_peer(S->dev, D->dev);
+}
+
+struct Choice {
+  int variant, engine, piece, stages, unroll;
+};
+
+// a6: unset choices come from the calibration table (measured GB/s per row
+// bytes, locality and call size), else FUSED + VEC.
+Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok) {
+  dyna_kv_calib_entry ce{};
+  const bool calibrated =
+      (o.variant == DYNA_VARIANT_AUTO || o.engine == DYNA_ENGINE_AUTO) && calib_lookup(row, peer, ntok, &ce);
+  Choice c{};
+  c.variant = o.variant ? o.variant : (calibrated && ce.variant ? ce.variant : DYNA_VARIANT_FUSED);
+  c.engine = o.engine ? o.engine : (calibrated && ce.engine ? ce.engine : DYNA_ENGINE_VEC);
+  const bool use_ce = calibrated && (!o.engine || o.engine == ce.engine);
+  c.piece = o.piece_bytes ? o.piece_bytes
+                          : (use_ce && ce.piece_bytes ? ce.piece_bytes
+                                                     : (c.engine == DYNA_ENGINE_BULK ? kBulkPiece : kVecPiece));
+  c.stages = o.stages ? o.stages : (use_ce && ce.stages ? ce.stages : kBulkStages);
+  c.unroll = o.unroll ? o.unroll : (use_ce && ce.unroll ? ce.unroll : kVecU);
+  return c;
+}
+
+// Entries [0, last touched] of a table's host ids (what the kernel may read).
+size_t table_upload_bytes(const dyna_block_table& t, int64_t t1) {
+  return (size_t)((t1 - 1) / t.pool->desc.block_size + 1) * sizeof(int32_t);
+}
+
 }  // namespace
 
 // ============================================================== API
@@ -552,91 +826,71 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
                                dyna_kv_xfer_t* out) {
   if (!out) return fail(DYNA_EINVAL, "NULL out");
   *out = nullptr;
-  if (!src.pool || !dst.pool) return fail(DYNA_EINVAL, "NULL pool in a block table");
   dyna_kv_opts o{};
-  if (opts) o = *opts;
-  if (o.variant < 0 || o.variant > 2 || o.engine < 0 || o.engine > 2 || o.max_ctas < 0 || o.piece_bytes < 0 ||
-      o.piece_bytes % 16 || o.stages < 0 || o.stages == 1 || o.stages > kMaxStages ||
-      (o.unroll != 0 && o.unroll != 4 && o.unroll != 8 && o.unroll != 16))
-    return fail(DYNA_EINVAL, "invalid dyna_kv_opts");
+  dyna_status r = check_opts(opts, &o);
+  if (r) return r;
+  bool empty = false;
+  if ((r = validate_pair(src, dst, tr, lr, chunk_tokens, &empty))) return r;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   dyna_kv_pool* S = src.pool;
   dyna_kv_pool* D = dst.pool;
   const dyna_kv_pool_desc &gs = S->desc, &gd = D->desc;
-  if (gs.num_layers != gd.num_layers || gs.num_kv_heads != gd.num_kv_heads || gs.head_dim != gd.head_dim ||
-      gs.elem_bytes != gd.elem_bytes)
-    return fail(DYNA_EGEOM, "source and destination geometry differ (L, H, d, e)");
-  if (lr.begin < 0 || lr.begin > lr.end || lr.end > gs.num_layers)
-    return fail(DYNA_ERANGE, "layer range [%lld, %lld) outside [0, %d)", (long long)lr.begin, (long long)lr.end,
-                gs.num_layers);
-  if (tr.begin < 0 || tr.begin > tr.end) return fail(DYNA_ERANGE, "bad token range");
-  const bool empty = tr.begin == tr.end || lr.begin == lr.end;
-  if (!empty) {
-    if (chunk_tokens <= 0) return fail(DYNA_ERANGE, "chunk_tokens must be > 0");
-    if (tr.end > src.len * gs.block_size || tr.end > dst.len * gd.block_size)
-      return fail(DYNA_ERANGE, "token range end %lld exceeds a block table (src %lld, dst %lld tokens)",
-                  (long long)tr.end, (long long)(src.len * gs.block_size), (long long)(dst.len * gd.block_size));
-    if (!src.block_ids || !dst.block_ids) return fail(DYNA_EINVAL, "NULL device block_ids");
-    dyna_status r = check_host_tables(src, dst, tr.begin, tr.end);
-    if (r) return r;
-  }
   const int64_t ntok = tr.end - tr.begin;
   const int64_t nchunks = empty ? 0 : (ntok + chunk_tokens - 1) / chunk_tokens;
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
   if (signal && nchunks > DYNA_MAX_CHUNKS)
     return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks, DYNA_MAX_CHUNKS);
+  if (empty) {  // P:309: s = 0 (or no layers) -> nothing to ship, nothing enqueued
+    auto* x = new dyna_kv_xfer();
+    x->dev = S->dev;
+    x->sender = gs.instance;
+    x->empty = true;
+    *out = x;
+    return DYNA_OK;
+  }
+  if ((r = check_reach(S, D))) return r;
+  if (!err_word()) return fail(DYNA_ECUDA, "no error word");
+
+  const int64_t row = S->row;
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  const int64_t c = chunk_tokens;
+  const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
+  const Choice ch = choose(o, row, peer_dst, ntok);
+  const int variant = ch.variant, engine = ch.engine, piece = ch.piece, stages = ch.stages, unroll = ch.unroll;
+
+  DeviceGuard guard(S->dev);
+  // Host-resident tables (block_ids == NULL): upload the entries the kernels may read.
+  RingLease lease(S->dev);
+  const int32_t* sids = src.block_ids;
+  const int32_t* dids = dst.block_ids;
+  if (!sids || !dids) {
+    if (variant == DYNA_VARIANT_STAGED && D->dev != S->dev)
+      return fail(DYNA_ENOTSUP, "cross-device STAGED needs device block_ids for the destination");
+    const size_t sb = sids ? 0 : (table_upload_bytes(src, tr.end) + 15) & ~size_t(15);
+    const size_t db = dids ? 0 : table_upload_bytes(dst, tr.end);
+    char *base = nullptr, *h = nullptr;
+    if ((r = lease.reserve(sb + db, &base, &h))) return r;
+    if (!sids) std::memcpy(h, src.host_block_ids, table_upload_bytes(src, tr.end));
+    if (!dids) std::memcpy(h + sb, dst.host_block_ids, db);
+    if ((r = lease.copy(stream))) return r;
+    if (!sids) sids = reinterpret_cast<const int32_t*>(base);
+    if (!dids) dids = reinterpret_cast<const int32_t*>(base + sb);
+  }
 
   auto* x = new dyna_kv_xfer();
   x->dev = S->dev;
   x->sender = gs.instance;
   x->nchunks = (int32_t)nchunks;
-  if (empty) {  // P:309: s = 0 (or no layers) -> nothing to ship, nothing enqueued
-    x->empty = true;
-    *out = x;
-    return DYNA_OK;
-  }
-  // reachability of the destination from the source device
-  if (D->imported) {
-    if (D->dev != S->dev) {
-      delete x;
-      return fail(DYNA_EPEER, "imported destination is mapped on device %d, source is on %d", D->dev, S->dev);
-    }
-  } else if (D->dev != S->dev) {
-    dyna_status r = ensure_peer(S->dev, D->dev);
-    if (r) {
-      delete x;
-      return r;
-    }
-  }
-  if (!err_word()) {
-    delete x;
-    return fail(DYNA_ECUDA, "no error word");
-  }
-
-  const int64_t row = S->row;
-  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
-  const int64_t c = chunk_tokens;
-  // a6: unset choices come from the calibration table (measured GB/s per row bytes,
-  // locality and chunk size), else FUSED + VEC.
-  const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
-  dyna_kv_calib_entry ce{};
-  const bool calibrated = (o.variant == DYNA_VARIANT_AUTO || o.engine == DYNA_ENGINE_AUTO) &&
-                          calib_lookup(row_bytes_of(S), peer_dst, ntok, &ce);
-  const int variant = o.variant ? o.variant : (calibrated && ce.variant ? ce.variant : DYNA_VARIANT_FUSED);
-  const int engine = o.engine ? o.engine : (calibrated && ce.engine ? ce.engine : DYNA_ENGINE_VEC);
-  const bool use_ce = calibrated && (!o.engine || o.engine == ce.engine);
-  const int piece = o.piece_bytes ? o.piece_bytes
-                                  : (use_ce && ce.piece_bytes ? ce.piece_bytes
-                                                             : (engine == DYNA_ENGINE_BULK ? kBulkPiece : kVecPiece));
-  const int stages = o.stages ? o.stages : (use_ce && ce.stages ? ce.stages : kBulkStages);
-  const int unroll = o.unroll ? o.unroll : (use_ce && ce.unroll ? ce.unroll : kVecU);
-
-  DeviceGuard guard(S->dev);
-  dyna_status r = DYNA_OK;
+  x->variant = variant;
+  x->engine = engine;
+  x->piece = piece;
+  x->stages = engine == DYNA_ENGINE_BULK ? stages : 0;
+  x->unroll = engine == DYNA_ENGINE_VEC ? unroll : 0;
+  const uint64_t launches0 = g_launches.load();
   if (variant == DYNA_VARIANT_FUSED) {
     // K4 / K4-local: source rows -> destination rows, one launch for all chunks.
     const int64_t g = gcd64(gs.block_size, gd.block_size);
-    Plan p = make_plan(paged(S, src.block_ids), paged(D, dst.block_ids), row, tr.begin, tr.end, l0, lm, c, g, piece);
+    Plan p = make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
     if (signal) {
       if ((r = channel_counters(S, D, S->dev, &p.counters))) {
         delete x;
@@ -644,102 +898,140 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
       }
       p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
       p.epoch = x->epoch = next_epoch(gs.instance, D);
-      p.sys_fence = (D->dev != S->dev || D->imported) ? 1 : 0;
+      p.sys_fence = peer_dst;
     }
     r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream);
   } else {
-    // Staged: K1 gather -> staging slot, K2 slot -> destination-side slot,
-    // K3 scatter slot -> destination rows.  Chunks are cut into sub-chunks
-    // that fit one staging slot; two slots per side alternate.
-    const bool cross = D->dev != S->dev;
-    if (D->imported) {
-      delete x;
-      return fail(DYNA_ENOTSUP, "STAGED variant into an imported (cross-process) pool is not supported; use FUSED");
-    }
-    DevInfo* ddi = dev_info(D->dev);
-    cudaStream_t dstream = stream;
-    if (cross) {
-      std::lock_guard<std::mutex> lk(g_mu);
-      if (!ddi->aux) {
-        DeviceGuard g(D->dev);
-        CUDA_TRY(cudaStreamCreateWithFlags(&ddi->aux, cudaStreamNonBlocking));
-      }
-      dstream = ddi->aux;
-    }
-    const int64_t tok_bytes = row * lm * 2;
-    const int64_t sc = std::max<int64_t>(1, std::min<int64_t>(c, kStageSlotBytes / tok_bytes));
-    const int64_t slot = sc * tok_bytes;
-    char *sbuf = nullptr, *dbuf = nullptr;
-    if ((r = channel_staging(S, D, slot, &sbuf, &dbuf))) {
-      delete x;
-      return r;
-    }
-    unsigned long long* counters = nullptr;
-    if (signal) {
-      if ((r = channel_counters(S, D, D->dev, &counters))) {
-        delete x;
-        return r;
-      }
-      x->epoch = next_epoch(gs.instance, D);
-    }
-    cudaEvent_t done_src[2] = {nullptr, nullptr};  // K2 of slot i finished (cross-device)
-    cudaEvent_t done_dst[2] = {nullptr, nullptr};  // K3 of slot i finished (cross-device)
-    if (cross)
-      for (int i = 0; i < 2; ++i) {
-        CUDA_TRY(get_event(S->dev, &done_src[i]));
-        DeviceGuard g(D->dev);
-        CUDA_TRY(get_event(D->dev, &done_dst[i]));
-      }
-    int64_t sub = 0;
-    for (int64_t k = 0; k < nchunks && !r; ++k) {
-      const int64_t a = tr.begin + k * c, b = std::min(a + c, tr.end);
-      for (int64_t sa = a; sa < b && !r; sa += sc, ++sub) {
-        const int64_t sb = std::min(sa + sc, b);
-        const int si = (int)(sub & 1);
-        char* sslot = sbuf + si * slot;
-        char* dslot = dbuf + si * slot;
-        if (cross && sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[si], 0));
-        Plan k1 = make_plan(paged(S, src.block_ids), linear(sslot), row, sa, sb, l0, lm, sb - sa, gs.block_size, piece);
-        if ((r = launch_copy(k1, engine, o.max_ctas, stages, unroll, S->dev, stream))) break;
-        // K2: the sub-chunk slot is [lm][2][n][row] = two contiguous halves
-        // (K and V of all layers): a flat plan with one token of `half` bytes.
-        Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
-        if ((r = launch_copy(k2, engine, o.max_ctas, stages, unroll, S->dev, stream))) break;
-        Plan k3 = make_plan(linear(dslot), paged(D, dst.block_ids), row, sa, sb, l0, lm, sb - sa, gd.block_size, piece);
-        k3.mig_t0 = tr.begin;
-        k3.mig_t1 = tr.end;
-        k3.sig_c = (int32_t)c;
-        if (signal) {
-          k3.counters = counters;
-          k3.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
-          k3.epoch = x->epoch;
-        }
-        if (cross) {
-          CUDA_TRY(cudaEventRecord(done_src[si], stream));
-          DeviceGuard g(D->dev);
-          CUDA_TRY(cudaStreamWaitEvent(dstream, done_src[si], 0));
-          if ((r = launch_copy(k3, engine, o.max_ctas, stages, unroll, D->dev, dstream))) break;
-          CUDA_TRY(cudaEventRecord(done_dst[si], dstream));
-        } else {
-          if ((r = launch_copy(k3, engine, o.max_ctas, stages, unroll, S->dev, stream))) break;
-        }
-      }
-    }
-    if (cross) {  // the migration completes on `stream` once the last scatters are done
-      const int last = (int)((sub - 1) & 1);
-      CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[last], 0));
-      if (sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[last ^ 1], 0));
-      for (int i = 0; i < 2; ++i) {
-        put_event(S->dev, done_src[i]);
-        put_event(D->dev, done_dst[i]);
-      }
-    }
+    r = run_staged(S, D, sids, dids, tr, l0, lm, c, signal, engine, piece, stages, unroll, o.max_ctas, stream, x);
   }
+  if (!r) r = lease.finish(stream);
   if (r) {
     delete x;
     return r;
   }
+  x->launches = (int32_t)(g_launches.load() - launches0);
   cudaError_t e = get_event(S->dev, &x->ev);
+  if (e == cudaSuccess) e = cudaEventRecord(x->ev, stream);
+  if (e != cudaSuccess) {
+    delete x;
+    return fail(DYNA_ECUDA, "event record: %s", cudaGetErrorString(e));
+  }
+  *out = x;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna_range lr, int32_t chunk_tokens,
+                                  struct CUstream_st* stream_, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  if (n < 0 || (n > 0 && !migs) || n > DYNA_MAX_BATCH) return fail(DYNA_EINVAL, "0 <= n <= DYNA_MAX_BATCH");
+  dyna_kv_opts o{};
+  dyna_status r = check_opts(opts, &o);
+  if (r) return r;
+  if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "batch: FUSED variant only");
+  if (o.flags & DYNA_MIGRATE_SIGNAL) return fail(DYNA_ENOTSUP, "batch: no per-chunk signalling (use dyna_kv_migrate_ex)");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  std::vector<int32_t> live;
+  int64_t total_tok = 0;
+  dyna_kv_pool* S0 = nullptr;
+  int peer = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    bool empty = false;
+    if ((r = validate_pair(migs[i].src, migs[i].dst, migs[i].token_range, lr, chunk_tokens, &empty))) {
+      g_err = "migration " + std::to_string(i) + ": " + g_err;
+      return r;
+    }
+    if (empty) continue;
+    dyna_kv_pool *S = migs[i].src.pool, *D = migs[i].dst.pool;
+    if (!S0) S0 = S;
+    if (S->dev != S0->dev || S->row != S0->row)
+      return fail(DYNA_EINVAL, "batch: all sources on one device with one row size");
+    if ((r = check_reach(S, D))) return r;
+    peer |= (D->dev != S->dev || D->imported) ? 1 : 0;
+    total_tok += migs[i].token_range.end - migs[i].token_range.begin;
+    live.push_back(i);
+  }
+  auto* x = new dyna_kv_xfer();
+  if (live.empty()) {
+    x->empty = true;
+    *out = x;
+    return DYNA_OK;
+  }
+  if (!err_word()) {
+    delete x;
+    return fail(DYNA_ECUDA, "no error word");
+  }
+  x->dev = S0->dev;
+  x->sender = S0->desc.instance;
+  const Choice ch = choose(o, S0->row, peer, total_tok);
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  DeviceGuard guard(S0->dev);
+  // One upload: [plans][item bases][host-resident tables].
+  const size_t m = live.size();
+  const size_t plans_b = ((m * sizeof(Plan)) + 15) & ~size_t(15);
+  const size_t bases_b = ((m * sizeof(int64_t)) + 15) & ~size_t(15);
+  std::vector<size_t> soff(m, 0), doff(m, 0);
+  size_t tab_b = 0;
+  for (size_t k = 0; k < m; ++k) {
+    const dyna_kv_migration& mg = migs[live[k]];
+    if (!mg.src.block_ids) {
+      soff[k] = plans_b + bases_b + tab_b;
+      tab_b += (table_upload_bytes(mg.src, mg.token_range.end) + 15) & ~size_t(15);
+    }
+    if (!mg.dst.block_ids) {
+      doff[k] = plans_b + bases_b + tab_b;
+      tab_b += (table_upload_bytes(mg.dst, mg.token_range.end) + 15) & ~size_t(15);
+    }
+  }
+  RingLease lease(S0->dev);
+  int64_t total_items = 0;
+  char *dbase = nullptr, *h = nullptr;
+  if ((r = lease.reserve(plans_b + bases_b + tab_b, &dbase, &h))) {
+    delete x;
+    return r;
+  }
+  std::vector<Plan> plans(m);
+  std::vector<int64_t> bases(m);
+  for (size_t k = 0; k < m; ++k) {
+    const dyna_kv_migration& mg = migs[live[k]];
+    dyna_kv_pool *S = mg.src.pool, *D = mg.dst.pool;
+    const int32_t* sids = mg.src.block_ids ? mg.src.block_ids : reinterpret_cast<const int32_t*>(dbase + soff[k]);
+    const int32_t* dids = mg.dst.block_ids ? mg.dst.block_ids : reinterpret_cast<const int32_t*>(dbase + doff[k]);
+    const int64_t g = gcd64(S->desc.block_size, D->desc.block_size);
+    plans[k] = make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end, l0, lm,
+                         chunk_tokens, g, ch.piece);
+    bases[k] = total_items;
+    total_items += plans[k].n_items;
+  }
+  // fill the pinned staging now that the device pointers are known, then one copy
+  std::memcpy(h, plans.data(), m * sizeof(Plan));
+  std::memcpy(h + plans_b, bases.data(), m * sizeof(int64_t));
+  for (size_t k = 0; k < m; ++k) {
+    const dyna_kv_migration& mg = migs[live[k]];
+    if (!mg.src.block_ids)
+      std::memcpy(h + soff[k], mg.src.host_block_ids, table_upload_bytes(mg.src, mg.token_range.end));
+    if (!mg.dst.block_ids)
+      std::memcpy(h + doff[k], mg.dst.host_block_ids, table_upload_bytes(mg.dst, mg.token_range.end));
+  }
+  if ((r = lease.copy(stream))) {
+    delete x;
+    return r;
+  }
+  BatchSource bsrc{reinterpret_cast<const Plan*>(dbase), reinterpret_cast<const int64_t*>(dbase + plans_b),
+                   (int32_t)m, total_items};
+  x->variant = DYNA_VARIANT_FUSED;
+  x->engine = ch.engine;
+  x->piece = ch.piece;
+  x->stages = ch.engine == DYNA_ENGINE_BULK ? ch.stages : 0;
+  x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
+  x->launches = 1;
+  r = launch_src(bsrc, total_items, false, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev, stream);
+  if (!r) r = lease.finish(stream);
+  if (r) {
+    delete x;
+    return r;
+  }
+  cudaError_t e = get_event(S0->dev, &x->ev);
   if (e == cudaSuccess) e = cudaEventRecord(x->ev, stream);
   if (e != cudaSuccess) {
     delete x;
@@ -783,6 +1075,18 @@ dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t x, uint64_t* epoch, int32_t* num_ch
   if (epoch) *epoch = x->epoch;
   if (num_chunks) *num_chunks = x->nchunks;
   if (sender) *sender = x->sender;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_xfer_plan(dyna_kv_xfer_t x, int32_t* variant, int32_t* engine, int32_t* piece, int32_t* stages,
+                              int32_t* unroll, int32_t* launches) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (variant) *variant = x->variant;
+  if (engine) *engine = x->engine;
+  if (piece) *piece = x->piece;
+  if (stages) *stages = x->stages;
+  if (unroll) *unroll = x->unroll;
+  if (launches) *launches = x->launches;
   return DYNA_OK;
 }
 

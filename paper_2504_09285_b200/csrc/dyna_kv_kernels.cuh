@@ -113,6 +113,33 @@ __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   return it;
 }
 
+// Where a kernel's items come from: one plan (by value, in the constant bank),
+// or a batch of plans in global memory with an exclusive prefix of item counts
+// (dyna_kv_migrate_batch: many requests, one launch).
+struct SingleSource {
+  Plan p;
+  __device__ __forceinline__ int64_t total() const { return p.n_items; }
+  __device__ __forceinline__ const Plan& locate(int64_t& item) const { return p; }
+  __device__ __forceinline__ const Plan& locate_signal() const { return p; }
+};
+struct BatchSource {
+  const Plan* plans;
+  const int64_t* base;  // base[r] = first global item of plan r; nondecreasing
+  int32_t n;
+  int64_t total_items;
+  __device__ __forceinline__ int64_t total() const { return total_items; }
+  __device__ __forceinline__ const Plan& locate(int64_t& item) const {
+    int lo = 0, hi = n - 1;  // the last r with base[r] <= item
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (__ldg(base + mid) <= item) lo = mid; else hi = mid - 1;
+    }
+    item -= __ldg(base + lo);
+    return plans[lo];
+  }
+  __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }
+};
+
 __device__ __forceinline__ void st_release_sys(unsigned long long* ptr, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ptr), "l"(v) : "memory");
 }
@@ -192,8 +219,8 @@ __device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __
   }
 }
 
-template <int U, bool SIGNAL>
-__global__ void __launch_bounds__(256) k_copy_vec(const Plan p) {
+template <int U, bool SIGNAL, class Src>
+__global__ void __launch_bounds__(256) k_copy_vec(const Src src) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -202,13 +229,16 @@ __global__ void __launch_bounds__(256) k_copy_vec(const Plan p) {
   // the warp moves on to another chunk — one fence per (warp, chunk), not per item.
   int32_t cur_k = -1;
   uint32_t cur_acc = 0;
-  for (int64_t item = warp; item < p.n_items; item += nwarps) {
+  const int64_t n_items = src.total();
+  for (int64_t gitem = warp; gitem < n_items; gitem += nwarps) {
+    int64_t item = gitem;
+    const Plan& p = src.locate(item);
     const Item it = decode_item(p, item);
     if (SIGNAL && it.acc && it.k != cur_k) {
       if (cur_acc) {
         fence_for(p);   // every lane's stores of chunk cur_k are performed ...
         __syncwarp();   // ... before lane 0 counts them
-        if (lane == 0) account_chunk(p, cur_k, cur_acc);
+        if (lane == 0) account_chunk(p, cur_k, cur_acc);   // (SIGNAL => single plan: same p)
       }
       cur_k = it.k;
       cur_acc = 0;
@@ -216,10 +246,10 @@ __global__ void __launch_bounds__(256) k_copy_vec(const Plan p) {
     if (it.n) warp_copy<U>(it.src, it.dst, it.n, lane);
     if (SIGNAL) cur_acc += it.acc;
   }
-  if (SIGNAL && cur_acc) {
-    fence_for(p);
+  if (SIGNAL && cur_acc) {  // signalling is single-plan only
+    fence_for(src.locate_signal());
     __syncwarp();
-    if (lane == 0) account_chunk(p, cur_k, cur_acc);
+    if (lane == 0) account_chunk(src.locate_signal(), cur_k, cur_acc);
   }
 }
 
@@ -271,8 +301,8 @@ constexpr int kMaxStages = 16;
 // One thread per CTA drives a ring of `stages` smem slots of p.piece bytes:
 // loads land in slots ahead of the store front; each slot is reloaded once
 // the store issued from it has been read out of shared memory.
-template <bool SIGNAL>
-__global__ void __launch_bounds__(32) k_copy_bulk(const Plan p, int stages) {
+template <bool SIGNAL, class Src>
+__global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ char* pend_dst[kMaxStages];
@@ -286,11 +316,15 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Plan p, int stages) {
 
   int64_t next = blockIdx.x;
   const int64_t stride = gridDim.x;
+  const int64_t n_items = src.total();
+  const Plan& p = src.locate_signal();  // used only for per-launch fields (piece, signalling)
 
   // Load the next non-empty item of this CTA into slot s (pend_n[s] = 0 if none).
   auto refill = [&](int s) {
-    while (next < p.n_items) {
-      const Item it = decode_item(p, next);
+    while (next < n_items) {
+      int64_t item = next;
+      const Plan& ip = src.locate(item);
+      const Item it = decode_item(ip, item);
       next += stride;
       if (it.n == 0) {
         if (SIGNAL && it.acc) account_chunk(p, it.k, it.acc);  // skipped (bad id): still closes the chunk

@@ -59,6 +59,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(dk.dyna_range) == 16
     assert ctypes.sizeof(dk.dyna_kv_opts) == 28
     assert ctypes.sizeof(dk.dyna_kv_calib_entry) == 32
+    assert ctypes.sizeof(dk.dyna_kv_migration) == 32 + 32 + 16
     assert ctypes.sizeof(dk.dyna_kv_ipc_handle) == 64 + 64 + 8 + 32
 
 
@@ -101,3 +102,15 @@ def test_calibration_table_roundtrip_without_gpu():
         dk.dyna_kv_calib_set([(8192, 2, 64, 2, 2, 0, 4, 0)])    # peer must be 0/1
     dk.dyna_kv_calib_set([])
     assert dk.dyna_kv_calib_get() == base
+
+
+def test_batch_host_validation_without_gpu():
+    import paper_2504_09285_b200 as dk
+    assert dk.lib.dyna_kv_migrate_batch(None, -1, dk.dyna_range(0, 1), 1, None, None,
+                                        ctypes.byref(ctypes.c_void_p())) == dk.DYNA_EINVAL
+    x = dk.dyna_kv_migrate_batch([], (0, 1), 16)          # nothing to move: nothing enqueued
+    assert dk.dyna_kv_query(x)
+    dk.dyna_kv_wait(x)
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_migrate_batch([], (0, 1), 16, opts=dk.opts(variant=dk.DYNA_VARIANT_STAGED))
+    assert e.value.status == dk.DYNA_ENOTSUP

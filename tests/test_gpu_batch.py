@@ -1,0 +1,127 @@
+"""GPU parity of dyna_kv_migrate_batch (many requests, one launch) and of
+host-resident block tables (uploaded by the library), against the oracle."""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import kvgen
+import oracle
+import paper_2504_09285_b200 as dk
+from kvgen import Geom
+from gpu_util import dev_table, mapped_mask, pool_filled, pool_from_host, torch_rows_equal, untouched_equal
+
+pytestmark = pytest.mark.gpu
+ENGINES = [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK]
+
+
+def host_table(pool, ids):
+    return dk.table(pool, None, np.ascontiguousarray(ids, dtype=np.int32))
+
+
+@pytest.mark.parametrize("variant,engine", list(itertools.product([1, 2], ENGINES)))
+@pytest.mark.parametrize("which", ["src", "dst", "both"])
+def test_host_resident_tables(variant, engine, which):
+    g = Geom(3, 8, 128, 2, 16, 200)
+    ts, td = kvgen.table_pair(4, 2000, g, g)
+    hs, hd = kvgen.fill_bytes(1, g.pool_bytes), kvgen.fill_bytes(2, g.pool_bytes)
+    want = hd.copy()
+    oracle.migrate(hs, g, ts, want, g, td, (37, 1801))
+    src, dst = pool_from_host(g, hs), pool_from_host(g, hd)
+    st = host_table(src, ts) if which in ("src", "both") else dev_table(src, ts)
+    dt = host_table(dst, td) if which in ("dst", "both") else dev_table(dst, td)
+    x = dk.migrate(st, dt, (37, 1801), (0, 3), 300, variant=variant, engine=engine)
+    dk.dyna_kv_wait(x)
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
+
+
+def test_upload_ring_wraps_many_calls():
+    """Thousands of host-table calls cycle the 8 MiB upload ring several times."""
+    g = Geom(1, 1, 8, 2, 16, 8192)          # row 16 B; tables of up to 8192 ids = 32 KiB each
+    src, dst = pool_filled(g, 5), pool_filled(g, 6)
+    rng = np.random.default_rng(0)
+    ts, td = rng.permutation(8192).astype(np.int32), rng.permutation(8192).astype(np.int32)
+    st, dt = host_table(src, ts), host_table(dst, td)
+    xs = []
+    for i in range(700):                    # 700 x 64 KiB of tables = 5.5 ring turns
+        a = (i * 97) % (8192 * 16 - 200)
+        xs.append(dk.migrate(st, dt, (a, 8192 * 16), (0, 1), 4096))
+        if len(xs) > 64:
+            dk.dyna_kv_wait(xs.pop(0))
+    for x in xs:
+        dk.dyna_kv_wait(x)
+    assert torch_rows_equal(src, ts, dst, td, (0, 8192 * 16), (0, 1))
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("host_tables", [False, True])
+def test_batch_matches_oracle(engine, host_tables):
+    g = Geom(2, 8, 128, 2, 16, 700)
+    reqs = kvgen.migrating(kvgen.skewed_batch(7, 24))
+    lens = [min(r.s, 1000) for r in reqs]
+    tabs = kvgen.batch_tables(8, [max(n, 1) + 40 for n in lens], g, g)
+    hs, hd = kvgen.fill_bytes(11, g.pool_bytes), kvgen.fill_bytes(12, g.pool_bytes)
+    want = hd.copy()
+    rng = np.random.default_rng(1)
+    ranges = []
+    for n, (ts, td) in zip(lens, tabs):
+        t0 = int(rng.integers(0, 30))
+        ranges.append((t0, t0 + n))
+        oracle.migrate(hs, g, ts, want, g, td, (t0, t0 + n))
+    src, dst = pool_from_host(g, hs), pool_from_host(g, hd)
+    T = host_table if host_tables else dev_table
+    migs = [(T(src, ts), T(dst, td), tr) for (ts, td), tr in zip(tabs, ranges)]
+    migs.append((T(src, tabs[0][0]), T(dst, tabs[0][1]), (5, 5)))   # empty entry
+    x = dk.migrate_batch(migs, (0, 2), 256, engine=engine)
+    dk.dyna_kv_wait(x)
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
+    assert np.array_equal(src.tensor.cpu().numpy(), hs)
+
+
+def test_batch_mixed_destinations_and_reblocking():
+    gs = Geom(2, 2, 64, 2, 16, 64)
+    gd1, gd2 = gs.with_(block_size=32, num_blocks=40), gs.with_(block_size=8, num_blocks=140)
+    hs = kvgen.fill_bytes(1, gs.pool_bytes)
+    h1, h2 = kvgen.fill_bytes(2, gd1.pool_bytes), kvgen.fill_bytes(3, gd2.pool_bytes)
+    ta, t1 = kvgen.table_pair(3, 300, gs, gd1)
+    tb, t2 = kvgen.table_pair(4, 300, gs, gd2)
+    tb = (tb + 20) % 64  # keep both sources valid; aliasing of sources is allowed
+    w1, w2 = h1.copy(), h2.copy()
+    oracle.migrate(hs, gs, ta, w1, gd1, t1, (0, 257))
+    oracle.migrate(hs, gs, tb, w2, gd2, t2, (11, 300))
+    src = pool_from_host(gs, hs)
+    d1, d2 = pool_from_host(gd1, h1), pool_from_host(gd2, h2)
+    x = dk.migrate_batch([(dev_table(src, ta), dev_table(d1, t1), (0, 257)),
+                          (dev_table(src, tb), dev_table(d2, t2), (11, 300))], (0, 2), 64)
+    dk.dyna_kv_wait(x)
+    assert np.array_equal(d1.tensor.cpu().numpy(), w1)
+    assert np.array_equal(d2.tensor.cpu().numpy(), w2)
+
+
+def test_batch_errors_name_the_entry():
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(1, 256, g, g)
+    bad = td.copy()
+    bad[1] = bad[0]
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, 10)),
+                          (dev_table(src, ts), dev_table(dst, bad), (0, 100))], (0, 2), 32)
+    assert e.value.status == dk.DYNA_EALIAS and "migration 1" in str(e.value)
+
+
+def test_config3_batch_full_size():
+    """configs[2] (Llama-3-8B, 64 skewed requests) in ONE launch, full size, checked at any size."""
+    g = kvgen.LLAMA3_8B
+    reqs = kvgen.migrating(kvgen.skewed_batch(1, 64))
+    tabs = kvgen.batch_tables(2, [r.s for r in reqs], g, g)
+    src, dst = pool_filled(g, 31), pool_filled(g, 32)
+    n0 = dk.dyna_kv_launch_count()
+    x = dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, r.s)) for r, (ts, td) in zip(reqs, tabs)],
+                         (0, 32), 256)
+    dk.dyna_kv_wait(x)
+    assert dk.dyna_kv_launch_count() - n0 == 1
+    for r, (ts, td) in zip(reqs, tabs):
+        assert torch_rows_equal(src, ts, dst, td, (0, r.s), (0, 32))
+    assert untouched_equal(dst, 32, mapped_mask(g, [(td, (0, r.s)) for r, (ts, td) in zip(reqs, tabs)]))
