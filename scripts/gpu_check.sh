@@ -7,7 +7,7 @@ if [ -n "$CALIB" ]; then timeout 1500 python scripts/calibrate.py > gpurun_out/c
 if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv \
       python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_bench.log 2>&1
-  for e in 1 2; do
+  for e in 0 1; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_copy -s 20 -c 2 -o gpurun_out/prof_e$e \
         python bench.py --steps 20 --warmup 3 --no-cpu-baseline --engine $e > gpurun_out/ncu_full_e$e.log 2>&1
   done
@@ -17,3 +17,4 @@ if [ -z "$NOBENCH" ]; then
   timeout 300 python bench.py --steps 1000 --warmup 10 2>&1 | tail -1 > gpurun_out/bench_default.json; cat gpurun_out/bench_default.json
 fi
 if [ -n "$OVERLAP" ]; then timeout 900 python scripts/overlap.py > gpurun_out/overlap.log 2>&1; tail -20 gpurun_out/overlap.log; fi
+if [ -n "$CONFIGS" ]; then timeout 900 python scripts/configs_sweep.py > gpurun_out/configs.log 2>&1; tail -20 gpurun_out/configs.log; fi
