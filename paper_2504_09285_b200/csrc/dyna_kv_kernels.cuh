@@ -342,11 +342,23 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages) {
 
   for (int s = 0; s < stages; ++s) refill(s);
 
-  // Signalling: stores are counted per chunk; when the next store belongs to
-  // another chunk, wait for all outstanding stores of this CTA once, fence,
-  // and count the finished chunk's bytes.
-  int32_t cur_k = -1;
-  uint32_t cur_acc = 0;
+  // Signalling: stores are counted per chunk.  When the next store belongs to
+  // another chunk, the finished chunk's bytes are parked; they are counted
+  // once kDefer more stores have been committed after it, behind a
+  // `cp.async.bulk.wait_group kDefer` (all older groups complete) — by then
+  // they have normally landed, so the pipeline does not drain.
+  constexpr int kDefer = 4;
+  int32_t cur_k = -1, park_k = -1;
+  uint32_t cur_acc = 0, park_acc = 0;
+  int since_park = 0;
+  auto flush_park = [&](bool all) {
+    if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    fence_for(p);
+    account_chunk(p, park_k, park_acc);
+    park_k = -1;
+    park_acc = 0;
+  };
   // A slot is refilled `lag` stores after its own store was issued, so up to
   // lag+1 stores drain while stages-lag-1 loads are in flight.
   const int lag = stages >= 4 ? 2 : 1;
@@ -354,29 +366,33 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages) {
     const int s = (int)(iter % stages);
     if (pend_n[s] == 0) break;
     if (SIGNAL && pend_k[s] != cur_k) {
-      if (cur_acc) {
-        bulk_wait_all<0>();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        fence_for(p);
-        account_chunk(p, cur_k, cur_acc);
-      }
+      if (park_acc) flush_park(true);  // chunks shorter than kDefer stores per CTA
+      park_k = cur_k;
+      park_acc = cur_acc;
+      since_park = 0;
       cur_k = pend_k[s];
       cur_acc = 0;
     }
     mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
     bulk_store(pend_dst[s], ring + (size_t)s * p.piece, pend_n[s]);
     bulk_commit();
-    if (SIGNAL) cur_acc += pend_n[s];
+    if (SIGNAL) {
+      cur_acc += pend_n[s];
+      if (park_acc && ++since_park == kDefer) flush_park(false);
+    }
     if (iter >= lag) {
       if (lag == 2) bulk_wait_read<2>(); else bulk_wait_read<1>();  // store iter-lag done reading smem
       refill((int)((iter - lag) % stages));
     }
   }
   bulk_wait_all<0>();
-  if (SIGNAL && cur_acc) {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-    fence_for(p);
-    account_chunk(p, cur_k, cur_acc);
+  if (SIGNAL) {
+    if (park_acc) flush_park(true);
+    if (cur_acc) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      fence_for(p);
+      account_chunk(p, cur_k, cur_acc);
+    }
   }
 }
 

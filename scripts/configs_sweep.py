@@ -48,6 +48,7 @@ def run_set(stream, calls, reps=10, warm=3):
         b.record(stream)
         for x in xs:
             dk.dyna_kv_wait(x)
+        b.synchronize()
         ts.append(a.elapsed_time(b))
     return statistics.median(ts)
 
