@@ -198,6 +198,32 @@ DYNA_API dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_
                                            int32_t chunk_tokens, struct CUstream_st* stream,
                                            const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
 
+/* Producer-coupled push (§4.3: "once chunk
+ * k completes, its KV block is immediately DMA-pushed ... while Server1
+ * continues with chunk k+1").  A ready board is an array of u64 slots on the
+ * source device.  The producer (the prefill) marks chunk k on ITS stream after
+ * the kernels that wrote chunk k's KV; one dyna_kv_migrate_on_ready launch on
+ * another stream covers the whole range and copies chunk k as soon as its
+ * mark (>= epoch) is visible — no host round trip per chunk.
+ * Chunk k = tokens [begin + k*c, min(begin + (k+1)*c, end)) of that call.
+ * The migration kernel stays resident while it waits, so its grid is capped
+ * (opts->max_ctas, default and maximum: half the SMs) to leave the producer
+ * room to run; FUSED variant with the VEC engine only.  A board is reused
+ * across requests with increasing epochs (dyna_kv_ready_begin). */
+typedef struct dyna_kv_ready* dyna_kv_ready_t;
+DYNA_API dyna_status dyna_kv_ready_create(int32_t device, int32_t max_chunks, dyna_kv_ready_t* out);
+DYNA_API dyna_status dyna_kv_ready_destroy(dyna_kv_ready_t board);
+/* A fresh epoch for the next request on this board (host counter; no device work). */
+DYNA_API dyna_status dyna_kv_ready_begin(dyna_kv_ready_t board, uint64_t* epoch);
+/* Enqueue on the producer's stream: slot[chunk] = epoch (release, GPU scope). */
+DYNA_API dyna_status dyna_kv_ready_mark(dyna_kv_ready_t board, int32_t chunk, uint64_t epoch,
+                                        struct CUstream_st* producer_stream);
+DYNA_API dyna_status dyna_kv_migrate_on_ready(dyna_block_table src, dyna_block_table dst,
+                                              dyna_range token_range, dyna_range layer_range,
+                                              int32_t chunk_tokens, dyna_kv_ready_t board, uint64_t epoch,
+                                              struct CUstream_st* stream, const dyna_kv_opts* opts,
+                                              dyna_kv_xfer_t* out);
+
 /* Block the host until every chunk is resident in the destination, report
  * deferred errors (DYNA_ECUDA, DYNA_ERANGE from device-side id checks), free
  * the handle. */

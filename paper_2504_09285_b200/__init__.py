@@ -35,7 +35,8 @@ EXPORTS = (
     "dyna_kv_stream_wait_chunk", "dyna_kv_last_error", "dyna_kv_poll_error", "dyna_kv_launch_count",
     "dyna_kv_enable_peer", "dyna_kv_pool_export", "dyna_kv_pool_import", "dyna_kv_debug_fill",
     "dyna_kv_copy_flags", "dyna_kv_calib_set", "dyna_kv_calib_get", "dyna_kv_migrate_batch",
-    "dyna_kv_xfer_plan",
+    "dyna_kv_xfer_plan", "dyna_kv_ready_create", "dyna_kv_ready_destroy", "dyna_kv_ready_begin",
+    "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -95,6 +96,12 @@ def _load():
                                     vp, p(dyna_kv_opts), p(vp)]),
         "dyna_kv_migrate_batch": (st, [p(dyna_kv_migration), ctypes.c_int32, dyna_range, ctypes.c_int32, vp,
                                        p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_ready_create": (st, [ctypes.c_int32, ctypes.c_int32, p(vp)]),
+        "dyna_kv_ready_destroy": (st, [vp]),
+        "dyna_kv_ready_begin": (st, [vp, p(ctypes.c_uint64)]),
+        "dyna_kv_ready_mark": (st, [vp, ctypes.c_int32, ctypes.c_uint64, vp]),
+        "dyna_kv_migrate_on_ready": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
+                                          vp, ctypes.c_uint64, vp, p(dyna_kv_opts), p(vp)]),
         "dyna_kv_wait": (st, [vp]),
         "dyna_kv_query": (st, [vp]),
         "dyna_kv_stream_wait": (st, [vp, vp]),
@@ -167,6 +174,36 @@ def dyna_kv_migrate_batch(migs, layer_range, chunk_tokens: int, stream: int = 0,
     out = ctypes.c_void_p()
     _check(lib.dyna_kv_migrate_batch(arr, len(migs), dyna_range(*layer_range), chunk_tokens, ctypes.c_void_p(stream),
                                      ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_ready_create(device: int, max_chunks: int) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_ready_create(device, max_chunks, ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_ready_destroy(board: int) -> None:
+    _check(lib.dyna_kv_ready_destroy(ctypes.c_void_p(board)))
+
+
+def dyna_kv_ready_begin(board: int) -> int:
+    e = ctypes.c_uint64()
+    _check(lib.dyna_kv_ready_begin(ctypes.c_void_p(board), ctypes.byref(e)))
+    return e.value
+
+
+def dyna_kv_ready_mark(board: int, chunk: int, epoch: int, stream: int = 0) -> None:
+    _check(lib.dyna_kv_ready_mark(ctypes.c_void_p(board), chunk, epoch, ctypes.c_void_p(stream)))
+
+
+def dyna_kv_migrate_on_ready(src: dyna_block_table, dst: dyna_block_table, token_range, layer_range,
+                             chunk_tokens: int, board: int, epoch: int, stream: int = 0,
+                             opts: dyna_kv_opts | None = None) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_migrate_on_ready(src, dst, dyna_range(*token_range), dyna_range(*layer_range), chunk_tokens,
+                                        ctypes.c_void_p(board), epoch, ctypes.c_void_p(stream),
+                                        ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
     return out.value
 
 

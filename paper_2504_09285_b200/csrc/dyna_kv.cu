@@ -135,6 +135,13 @@ struct dyna_kv_pool {
   std::map<const dyna_kv_pool*, Channel> channels;  // keyed by destination pool
 };
 
+struct dyna_kv_ready {
+  int dev = 0;
+  int32_t max_chunks = 0;
+  unsigned long long* slots = nullptr;  // device, zero-initialised
+  std::atomic<uint64_t> epoch{0};
+};
+
 struct dyna_kv_xfer {
   cudaEvent_t ev = nullptr;
   int32_t variant = 0, engine = 0, piece = 0, stages = 0, unroll = 0, launches = 0;
@@ -287,6 +294,32 @@ dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int
     sig ? launch_vec<8, true>(src, n_items, max_ctas, di->sms, st)
         : launch_vec<8, false>(src, n_items, max_ctas, di->sms, st);
   }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+// Producer-coupled launch: VEC engine, coherent loads, per-warp ready waits.
+dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st) {
+  DevInfo* di = dev_info(dev);
+  SingleSource src{p};
+  const bool sig = p.counters != nullptr;
+  int occ = 0;
+  if (sig)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copy_vec<8, true, SingleSource, true>, kVecThreads, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copy_vec<8, false, SingleSource, true>, kVecThreads, 0);
+  // never more than half the SMs' worth of CTAs: the producer must be able to run beside us
+  int64_t cap = std::max(1, di->sms / 2);
+  if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
+  cap = std::min<int64_t>(cap, (int64_t)di->sms * std::max(occ, 1));
+  constexpr int wpc = kVecThreads / 32;
+  const int64_t warps = balanced_workers(p.n_items, cap * wpc);
+  const unsigned grid = (unsigned)((warps + wpc - 1) / wpc);
+  if (sig)
+    k_copy_vec<8, true, SingleSource, true><<<grid, kVecThreads, 0, st>>>(src);
+  else
+    k_copy_vec<8, false, SingleSource, true><<<grid, kVecThreads, 0, st>>>(src);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   CUDA_TRY(cudaGetLastError());
   return DYNA_OK;
@@ -821,9 +854,26 @@ dyna_status dyna_kv_migrate(dyna_block_table src, dyna_block_table dst, dyna_ran
   return dyna_kv_migrate_ex(src, dst, tr, lr, chunk_tokens, stream, nullptr, out);
 }
 
+static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                                int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
+                                dyna_kv_ready* board, uint64_t ready_epoch, dyna_kv_xfer_t* out);
+
 dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
                                int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
                                dyna_kv_xfer_t* out) {
+  return migrate_impl(src, dst, tr, lr, chunk_tokens, stream_, opts, nullptr, 0, out);
+}
+
+dyna_status dyna_kv_migrate_on_ready(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                                     int32_t chunk_tokens, dyna_kv_ready_t board, uint64_t epoch,
+                                     struct CUstream_st* stream_, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
+  if (!board) return fail(DYNA_EINVAL, "NULL ready board");
+  return migrate_impl(src, dst, tr, lr, chunk_tokens, stream_, opts, board, epoch, out);
+}
+
+static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                                int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
+                                dyna_kv_ready* board, uint64_t ready_epoch, dyna_kv_xfer_t* out) {
   if (!out) return fail(DYNA_EINVAL, "NULL out");
   *out = nullptr;
   dyna_kv_opts o{};
@@ -840,6 +890,13 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
   if (signal && nchunks > DYNA_MAX_CHUNKS)
     return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks, DYNA_MAX_CHUNKS);
+  if (board) {
+    if (board->dev != src.pool->dev) return fail(DYNA_EINVAL, "ready board must live on the source device");
+    if (nchunks > board->max_chunks)
+      return fail(DYNA_ERANGE, "%lld chunks > the ready board's %d slots", (long long)nchunks, board->max_chunks);
+    if (o.variant == DYNA_VARIANT_STAGED || o.engine == DYNA_ENGINE_BULK)
+      return fail(DYNA_ENOTSUP, "producer-coupled migration: FUSED variant, VEC engine only");
+  }
   if (empty) {  // s = 0 (or no layers) -> nothing to ship, nothing enqueued
     auto* x = new dyna_kv_xfer();
     x->dev = S->dev;
@@ -855,7 +912,13 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
   const int64_t c = chunk_tokens;
   const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
-  const Choice ch = choose(o, row, peer_dst, ntok);
+  Choice ch = choose(o, row, peer_dst, ntok);
+  if (board) {  // producer-coupled: the VEC engine (each warp waits on its own chunk's mark)
+    ch.variant = DYNA_VARIANT_FUSED;
+    ch.engine = DYNA_ENGINE_VEC;
+    ch.unroll = 8;
+    if (!o.piece_bytes) ch.piece = kVecPiece;
+  }
   const int variant = ch.variant, engine = ch.engine, piece = ch.piece, stages = ch.stages, unroll = ch.unroll;
 
   DeviceGuard guard(S->dev);
@@ -900,7 +963,13 @@ dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_
       p.epoch = x->epoch = next_epoch(gs.instance, D);
       p.sys_fence = peer_dst;
     }
-    r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream);
+    if (board) {
+      p.ready = board->slots;
+      p.ready_epoch = ready_epoch;
+      r = launch_ready(p, o.max_ctas, S->dev, stream);
+    } else {
+      r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream);
+    }
   } else {
     r = run_staged(S, D, sids, dids, tr, l0, lm, c, signal, engine, piece, stages, unroll, o.max_ctas, stream, x);
   }
@@ -1038,6 +1107,49 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     return fail(DYNA_ECUDA, "event record: %s", cudaGetErrorString(e));
   }
   *out = x;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_ready_create(int32_t device, int32_t max_chunks, dyna_kv_ready_t* out) {
+  if (!out || device < 0 || max_chunks <= 0 || max_chunks > (1 << 24)) return fail(DYNA_EINVAL, "bad argument");
+  *out = nullptr;
+  auto* b = new dyna_kv_ready();
+  b->dev = device;
+  b->max_chunks = max_chunks;
+  DeviceGuard g(device);
+  if (cudaMalloc(&b->slots, sizeof(unsigned long long) * max_chunks) != cudaSuccess ||
+      cudaMemset(b->slots, 0, sizeof(unsigned long long) * max_chunks) != cudaSuccess) {
+    delete b;
+    return fail(DYNA_ENOMEM, "ready board of %d slots", max_chunks);
+  }
+  dev_info(device);
+  *out = b;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_ready_destroy(dyna_kv_ready_t b) {
+  if (!b) return fail(DYNA_EINVAL, "NULL board");
+  {
+    DeviceGuard g(b->dev);
+    cudaFree(b->slots);
+  }
+  delete b;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_ready_begin(dyna_kv_ready_t b, uint64_t* epoch) {
+  if (!b || !epoch) return fail(DYNA_EINVAL, "NULL argument");
+  *epoch = ++b->epoch;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_ready_mark(dyna_kv_ready_t b, int32_t chunk, uint64_t epoch, struct CUstream_st* stream) {
+  if (!b) return fail(DYNA_EINVAL, "NULL board");
+  if (chunk < 0 || chunk >= b->max_chunks) return fail(DYNA_ERANGE, "chunk %d outside the board", chunk);
+  DeviceGuard g(b->dev);
+  k_mark_ready<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(b->slots + chunk, epoch);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CUDA_TRY(cudaGetLastError());
   return DYNA_OK;
 }
 

@@ -59,6 +59,9 @@ struct Plan {
   unsigned long long epoch;
   int32_t sys_fence;             // 1: destination on another GPU (fence at system scope)
   unsigned int* err;             // deferred error word (mapped host memory)
+  // producer coupling (nullptr: none): chunk k may be read only once ready[k] >= ready_epoch
+  const unsigned long long* ready;
+  unsigned long long ready_epoch;
 };
 
 enum : unsigned { ERR_BAD_BLOCK = 1u, ERR_TIMEOUT = 2u };
@@ -149,6 +152,18 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* ptr) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
+// Producer coupling (§4.3, "once chunk k completes, its KV block
+// is immediately DMA-pushed"): block until the producer marked chunk k.
+__device__ __forceinline__ void wait_ready(const Plan& p, int32_t k) {
+  while (ld_acquire_gpu(p.ready + k) < p.ready_epoch) __nanosleep(200);
+}
+
 // Bytes of global chunk k of the whole migration.
 __device__ __forceinline__ unsigned long long chunk_bytes(const Plan& p, int32_t k) {
   const int64_t a = p.mig_t0 + (int64_t)k * p.sig_c;
@@ -183,6 +198,14 @@ __device__ __forceinline__ int4 ld_nc_v4(const int4* ptr) {
                : "l"(ptr));
   return r;
 }
+__device__ __forceinline__ int4 ld_v4(const int4* ptr) {  // coherent: source may be written during the kernel
+  int4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr)
+               : "memory");
+  return r;
+}
 __device__ __forceinline__ void st_v4(int4* ptr, const int4& v) {
   asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(ptr), "r"(v.x), "r"(v.y),
                "r"(v.z), "r"(v.w)
@@ -190,7 +213,7 @@ __device__ __forceinline__ void st_v4(int4* ptr, const int4& v) {
 }
 
 // A warp copies n bytes (multiple of 16): U 16-B loads per lane in flight.
-template <int U>
+template <int U, bool NC = true>
 __device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __restrict__ dst, uint32_t n,
                                           int lane) {
   const int4* s = reinterpret_cast<const int4*>(src);
@@ -200,7 +223,7 @@ __device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __
   for (; base + 32 * U <= nv; base += 32 * U) {
     int4 v[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ld_nc_v4(s + base + u * 32 + lane);
+    for (int u = 0; u < U; ++u) v[u] = NC ? ld_nc_v4(s + base + u * 32 + lane) : ld_v4(s + base + u * 32 + lane);
 #pragma unroll
     for (int u = 0; u < U; ++u) st_v4(d + base + u * 32 + lane, v[u]);
   }
@@ -209,7 +232,7 @@ __device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t idx = base + u * 32 + lane;
-      if (idx < nv) v[u] = ld_nc_v4(s + idx);
+      if (idx < nv) v[u] = NC ? ld_nc_v4(s + idx) : ld_v4(s + idx);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -219,7 +242,7 @@ __device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __
   }
 }
 
-template <int U, bool SIGNAL, class Src>
+template <int U, bool SIGNAL, class Src, bool READY = false>
 __global__ void __launch_bounds__(256) k_copy_vec(const Src src) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -229,6 +252,7 @@ __global__ void __launch_bounds__(256) k_copy_vec(const Src src) {
   // the warp moves on to another chunk — one fence per (warp, chunk), not per item.
   int32_t cur_k = -1;
   uint32_t cur_acc = 0;
+  int32_t ready_k = -1;
   const int64_t n_items = src.total();
   for (int64_t gitem = warp; gitem < n_items; gitem += nwarps) {
     int64_t item = gitem;
@@ -243,7 +267,12 @@ __global__ void __launch_bounds__(256) k_copy_vec(const Src src) {
       cur_k = it.k;
       cur_acc = 0;
     }
-    if (it.n) warp_copy<U>(it.src, it.dst, it.n, lane);
+    if (READY && it.acc && it.k != ready_k) {  // warp-uniform
+      if (lane == 0) wait_ready(p, it.k);
+      __syncwarp();
+      ready_k = it.k;
+    }
+    if (it.n) warp_copy<U, !READY>(it.src, it.dst, it.n, lane);
     if (SIGNAL) cur_acc += it.acc;
   }
   if (SIGNAL && cur_acc) {  // signalling is single-plan only
@@ -412,6 +441,11 @@ __global__ void k_wait_flag(const unsigned long long* flag, unsigned long long e
     }
     __nanosleep(256);
   }
+}
+
+// ------------------------------------------------------------------ producer side of the ready board
+__global__ void k_mark_ready(unsigned long long* slot, unsigned long long epoch) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(slot), "l"(epoch) : "memory");
 }
 
 // ------------------------------------------------------------------ test-input generator (not the method)

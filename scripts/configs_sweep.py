@@ -110,7 +110,11 @@ def main():
     tot = sum(r.s for r in reqs)
     ms = run_set(stream, calls, reps=5)
     report(f"configs[2] Llama-3-8B skewed batch ({len(reqs)} migrating of 64, sum s={tot}) c=256",
-           tot * 2 * 32 * g.row_bytes, ms, tot, len(calls))
+           tot * 2 * 32 * g.row_bytes, ms, tot, len(calls), "one dyna_kv_migrate per request")
+    migs = [(t[0], t[1], (0, t[2])) for t in T]
+    ms = run_set(stream, [lambda: dk.dyna_kv_migrate_batch(migs, (0, 32), 256, cs, None)], reps=5)
+    report(f"configs[2] Llama-3-8B skewed batch ({len(reqs)} migrating of 64, sum s={tot}) c=256, batched",
+           tot * 2 * 32 * g.row_bytes, ms, tot, 1, "one dyna_kv_migrate_batch launch")
     del src, dst, T
 
     # configs[3] Llama-3-8B 32k prompt, chunk sweep: one call per chunk (the per-chunk push) and one call per range

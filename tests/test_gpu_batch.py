@@ -57,9 +57,9 @@ def test_upload_ring_wraps_many_calls():
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("host_tables", [False, True])
 def test_batch_matches_oracle(engine, host_tables):
-    g = Geom(2, 8, 128, 2, 16, 700)
+    g = Geom(2, 8, 128, 2, 16, 1200)
     reqs = kvgen.migrating(kvgen.skewed_batch(7, 24))
-    lens = [min(r.s, 1000) for r in reqs]
+    lens = [min(r.s, 600) for r in reqs]
     tabs = kvgen.batch_tables(8, [max(n, 1) + 40 for n in lens], g, g)
     hs, hd = kvgen.fill_bytes(11, g.pool_bytes), kvgen.fill_bytes(12, g.pool_bytes)
     want = hd.copy()
