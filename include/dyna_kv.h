@@ -209,10 +209,18 @@ DYNA_API dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_
  * The migration kernel stays resident while it waits, so its grid is capped
  * (opts->max_ctas, default and maximum: half the SMs) to leave the producer
  * room to run; FUSED variant with the VEC engine only.  A board is reused
- * across requests with increasing epochs (dyna_kv_ready_begin). */
+ * across requests with increasing epochs (dyna_kv_ready_begin).
+ * HAZARD: while such a migration waits, anything that synchronises the whole
+ * device (cudaDeviceSynchronize, cudaMalloc/cudaFree that sync, synchronous
+ * copies on the legacy stream) before the last chunk is marked deadlocks: the
+ * device waits for the migration, the migration for a mark that is never
+ * issued.  Each chunk wait therefore gives up after the board's timeout
+ * (default 10 s; dyna_kv_ready_set_timeout) and dyna_kv_wait then returns
+ * DYNA_ETIMEDOUT (the rows of late chunks are then unspecified). */
 typedef struct dyna_kv_ready* dyna_kv_ready_t;
 DYNA_API dyna_status dyna_kv_ready_create(int32_t device, int32_t max_chunks, dyna_kv_ready_t* out);
 DYNA_API dyna_status dyna_kv_ready_destroy(dyna_kv_ready_t board);
+DYNA_API dyna_status dyna_kv_ready_set_timeout(dyna_kv_ready_t board, uint64_t timeout_ns);
 /* A fresh epoch for the next request on this board (host counter; no device work). */
 DYNA_API dyna_status dyna_kv_ready_begin(dyna_kv_ready_t board, uint64_t* epoch);
 /* Enqueue on the producer's stream: slot[chunk] = epoch (release, GPU scope). */

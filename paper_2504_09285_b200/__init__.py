@@ -36,7 +36,7 @@ EXPORTS = (
     "dyna_kv_enable_peer", "dyna_kv_pool_export", "dyna_kv_pool_import", "dyna_kv_debug_fill",
     "dyna_kv_copy_flags", "dyna_kv_calib_set", "dyna_kv_calib_get", "dyna_kv_migrate_batch",
     "dyna_kv_xfer_plan", "dyna_kv_ready_create", "dyna_kv_ready_destroy", "dyna_kv_ready_begin",
-    "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready",
+    "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready", "dyna_kv_ready_set_timeout",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -99,6 +99,7 @@ def _load():
         "dyna_kv_ready_create": (st, [ctypes.c_int32, ctypes.c_int32, p(vp)]),
         "dyna_kv_ready_destroy": (st, [vp]),
         "dyna_kv_ready_begin": (st, [vp, p(ctypes.c_uint64)]),
+        "dyna_kv_ready_set_timeout": (st, [vp, ctypes.c_uint64]),
         "dyna_kv_ready_mark": (st, [vp, ctypes.c_int32, ctypes.c_uint64, vp]),
         "dyna_kv_migrate_on_ready": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
                                           vp, ctypes.c_uint64, vp, p(dyna_kv_opts), p(vp)]),
@@ -185,6 +186,10 @@ def dyna_kv_ready_create(device: int, max_chunks: int) -> int:
 
 def dyna_kv_ready_destroy(board: int) -> None:
     _check(lib.dyna_kv_ready_destroy(ctypes.c_void_p(board)))
+
+
+def dyna_kv_ready_set_timeout(board: int, timeout_ns: int) -> None:
+    _check(lib.dyna_kv_ready_set_timeout(ctypes.c_void_p(board), timeout_ns))
 
 
 def dyna_kv_ready_begin(board: int) -> int:

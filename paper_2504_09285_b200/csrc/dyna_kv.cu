@@ -138,6 +138,7 @@ struct dyna_kv_pool {
 struct dyna_kv_ready {
   int dev = 0;
   int32_t max_chunks = 0;
+  unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;  // per chunk wait
   unsigned long long* slots = nullptr;  // device, zero-initialised
   std::atomic<uint64_t> epoch{0};
 };
@@ -966,6 +967,7 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     if (board) {
       p.ready = board->slots;
       p.ready_epoch = ready_epoch;
+      p.ready_timeout_ns = board->timeout_ns;
       r = launch_ready(p, o.max_ctas, S->dev, stream);
     } else {
       r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream);
@@ -1134,6 +1136,12 @@ dyna_status dyna_kv_ready_destroy(dyna_kv_ready_t b) {
     cudaFree(b->slots);
   }
   delete b;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_ready_set_timeout(dyna_kv_ready_t b, uint64_t timeout_ns) {
+  if (!b || timeout_ns == 0) return fail(DYNA_EINVAL, "bad argument");
+  b->timeout_ns = timeout_ns;
   return DYNA_OK;
 }
 

@@ -62,6 +62,7 @@ struct Plan {
   // producer coupling (nullptr: none): chunk k may be read only once ready[k] >= ready_epoch
   const unsigned long long* ready;
   unsigned long long ready_epoch;
+  unsigned long long ready_timeout_ns;  // give up (ERR_TIMEOUT) after this long without the mark
 };
 
 enum : unsigned { ERR_BAD_BLOCK = 1u, ERR_TIMEOUT = 2u };
@@ -161,7 +162,17 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
 // Producer coupling (§4.3, "once chunk k completes, its KV block
 // is immediately DMA-pushed"): block until the producer marked chunk k.
 __device__ __forceinline__ void wait_ready(const Plan& p, int32_t k) {
-  while (ld_acquire_gpu(p.ready + k) < p.ready_epoch) __nanosleep(200);
+  if (ld_acquire_gpu(p.ready + k) >= p.ready_epoch) return;
+  unsigned long long t0, now;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (ld_acquire_gpu(p.ready + k) < p.ready_epoch) {
+    __nanosleep(500);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > p.ready_timeout_ns) {  // never hang the device: report at dyna_kv_wait
+      if (p.err) atomicOr(p.err, ERR_TIMEOUT);
+      return;
+    }
+  }
 }
 
 // Bytes of global chunk k of the whole migration.

@@ -20,6 +20,8 @@ Reported per (c, SM budget), all from CUDA events inside the same run:
                    issued after the prefill (no chunking)
   reduction = 1 - exposed_chunked / exposed_whole     (the P:738 analogue)
   producer_slowdown  producer time with concurrent chunked migrations vs alone
+  ready_coupled    the same with ONE dyna_kv_migrate_on_ready launch that waits
+                   on the device for the producer's per-chunk marks
 On one GPU the migration is an intra-device reblock (HBM); on the 8-GPU box
 the same script with a peer destination measures the NVLink form.
 """
@@ -79,9 +81,15 @@ def main():
         e0.record(prod)
         mig.wait_event(e0)
         handles = []
+        if mode == "ready":   # one launch for the whole range; waits on the device for each chunk's mark
+            epoch = dk.dyna_kv_ready_begin(board)
+            handles.append(dk.dyna_kv_migrate_on_ready(st, dt, (0, s), (0, 32), c, board, epoch, mig.cuda_stream,
+                                                       dk.opts(max_ctas=budget or 32)))
         for k in range(nck):
             with torch.cuda.stream(prod):
                 producer_chunk(X)
+            if mode == "ready":
+                dk.dyna_kv_ready_mark(board, k, epoch, prod.cuda_stream)
             if mode == "chunked":                     # chunk k complete -> push it now
                 ev = torch.cuda.Event()
                 ev.record(prod)
@@ -98,6 +106,7 @@ def main():
             dk.dyna_kv_wait(x)
         return e0.elapsed_time(e_prod), max(0.0, e_prod.elapsed_time(e_mig))
 
+    board = dk.dyna_kv_ready_create(0, 1024)
     xs_in = {}
     for c in [int(x) for x in args.chunks.split(",")]:
         xs_in[c] = torch.randn(c, 4096, dtype=torch.bfloat16, device="cuda")
@@ -111,21 +120,28 @@ def main():
         t_mig = a0.elapsed_time(a1)
         prod_alone = statistics.median(run(c, "none", 0)[0] for _ in range(args.reps))
         for budget in [int(x) for x in args.budgets.split(",")]:
-            W_, C_ = [], []
+            W_, C_, R_ = [], [], []
             run(c, "whole", budget)
             run(c, "chunked", budget)   # warm
-            for _ in range(args.reps):  # interleaved so drift hits both modes alike
+            run(c, "ready", budget)
+            for _ in range(args.reps):  # interleaved so drift hits all modes alike
                 W_.append(run(c, "whole", budget))
                 C_.append(run(c, "chunked", budget))
+                R_.append(run(c, "ready", budget))
             exp_w = statistics.median(e for _, e in W_)
             exp_c = statistics.median(e for _, e in C_)
+            exp_r = statistics.median(e for _, e in R_)
             prod_c = statistics.median(p for p, _ in C_)
+            prod_r = statistics.median(p for p, _ in R_)
             r = {"chunk": c, "sm_budget_ctas": budget, "T_migrate_alone_ms": t_mig,
                  "migrate_alone_GBps": payload / (t_mig / 1e3) / 1e9,
                  "T_prod_alone_ms": prod_alone, "T_prod_with_chunked_ms": prod_c,
                  "producer_slowdown": prod_c / prod_alone - 1,
                  "exposed_whole_ms": exp_w, "exposed_chunked_ms": exp_c,
-                 "reduction": 1 - exp_c / exp_w if exp_w > 0 else None}
+                 "reduction": 1 - exp_c / exp_w if exp_w > 0 else None,
+                 "ready_coupled": {"ctas": budget or 32, "exposed_ms": exp_r, "T_prod_ms": prod_r,
+                                   "producer_slowdown": prod_r / prod_alone - 1,
+                                   "reduction": 1 - exp_r / exp_w if exp_w > 0 else None}}
             print(json.dumps(r), flush=True)
             results.append(r)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)

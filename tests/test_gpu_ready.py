@@ -14,16 +14,15 @@ from gpu_util import dev_table, mapped_mask, pool_filled, torch_rows_equal, unto
 pytestmark = pytest.mark.gpu
 
 
-def _produce_chunk(src, g, ts, a, b, fresh, stream):
-    """Stand-in producer: write tokens [a, b) of the request (all layers, K and V) from `fresh`."""
+def _produce_chunk(fresh_t, src_t, g, a, b, stream):
+    """Stand-in producer for chunk [a, b): ~1 ms of "prefill compute", then the chunk's KV
+    lands in the source pool (copied from `fresh` with the library's own fused kernel).
+    Nothing here allocates device memory: a cudaMalloc that synchronises the device while
+    the coupled migration waits would deadlock (see dyna_kv.h, producer-coupled push)."""
     with torch.cuda.stream(stream):
-        torch.cuda._sleep(2_000_000)  # ~1 ms of "prefill compute" before the KV lands
-        S = src.tensor.view(g.num_layers, 2, g.num_blocks, g.block_size, g.row_bytes)
-        F = fresh.view_as(S)
-        t = torch.arange(a, b, device="cuda")
-        T = torch.as_tensor(ts, device="cuda").long()
-        idx = (slice(None), slice(None), T[t // g.block_size], t % g.block_size)
-        S[idx] = F[idx]
+        torch.cuda._sleep(2_000_000)
+    x = dk.dyna_kv_migrate_ex(fresh_t, src_t, (a, b), (0, g.num_layers), b - a, stream.cuda_stream, None)
+    return x
 
 
 @pytest.mark.parametrize("c", [64, 100, 256])
@@ -32,21 +31,36 @@ def test_migration_waits_for_each_chunk(c, signal):
     g = Geom(4, 8, 128, 2, 16, 300)
     s = 1000
     src, dst = pool_filled(g, 1), pool_filled(g, 2)
-    fresh = pool_filled(g, 3).tensor               # the values the producer will write
+    fresh = pool_filled(g, 3)                      # the values the producer will write
     ts, td = kvgen.table_pair(5, 1200, g, g)
-    torch.cuda.synchronize()
+    src_t, dst_t, fresh_t = dev_table(src, ts), dev_table(dst, td), dev_table(fresh, ts)
+    prod, mig = torch.cuda.Stream(), torch.cuda.Stream()
     board = dk.dyna_kv_ready_create(0, 64)
+    dk.dyna_kv_ready_set_timeout(board, 20_000_000_000)
+    # warm every library path used below so nothing allocates while the migration waits
+    flags = dk.DYNA_MIGRATE_SIGNAL if signal else 0
+    e0 = dk.dyna_kv_ready_begin(board)
+    for k in range(-(-s // c)):
+        dk.dyna_kv_ready_mark(board, k, e0, prod.cuda_stream)
+    prod.synchronize()
+    dk.dyna_kv_wait(dk.dyna_kv_migrate_on_ready(src_t, dst_t, (0, s), (0, 4), c, board, e0, mig.cuda_stream,
+                                                dk.opts(max_ctas=8, flags=flags)))
+    dk.dyna_kv_wait(_produce_chunk(fresh_t, src_t, g, 0, 1, prod))
+    src = pool_filled(g, 1)                        # back to the stale values
+    src_t = dev_table(src, ts)
+    torch.cuda.synchronize()
     try:
-        prod, mig = torch.cuda.Stream(), torch.cuda.Stream()
         epoch = dk.dyna_kv_ready_begin(board)
-        flags = dk.DYNA_MIGRATE_SIGNAL if signal else 0
-        x = dk.dyna_kv_migrate_on_ready(dev_table(src, ts), dev_table(dst, td), (0, s), (0, 4), c, board, epoch,
+        x = dk.dyna_kv_migrate_on_ready(src_t, dst_t, (0, s), (0, 4), c, board, epoch,
                                         mig.cuda_stream, dk.opts(max_ctas=8, flags=flags))
         nck = -(-s // c)
+        px = []
         for k in range(nck):                         # prefill chunk k, then mark it ready
-            _produce_chunk(src, g, ts, k * c, min((k + 1) * c, s), fresh, prod)
+            px.append(_produce_chunk(fresh_t, src_t, g, k * c, min((k + 1) * c, s), prod))
             dk.dyna_kv_ready_mark(board, k, epoch, prod.cuda_stream)
         dk.dyna_kv_wait(x)
+        for y in px:
+            dk.dyna_kv_wait(y)
         torch.cuda.synchronize()
         assert torch_rows_equal(src, ts, dst, td, (0, s), (0, 4))        # fresh values arrived
         assert untouched_equal(dst, 2, mapped_mask(g, [(td, (0, s))]))
@@ -73,5 +87,22 @@ def test_ready_errors():
         with pytest.raises(dk.DynaKVError) as e:
             dk.dyna_kv_ready_mark(board, 2, 1)
         assert e.value.status == dk.DYNA_ERANGE
+    finally:
+        dk.dyna_kv_ready_destroy(board)
+
+
+def test_missing_mark_times_out_instead_of_hanging():
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(1, 256, g, g)
+    board = dk.dyna_kv_ready_create(0, 8)
+    try:
+        dk.dyna_kv_ready_set_timeout(board, 2_000_000)          # 2 ms
+        epoch = dk.dyna_kv_ready_begin(board)
+        dk.dyna_kv_ready_mark(board, 0, epoch)                  # chunk 1..3 never marked
+        x = dk.dyna_kv_migrate_on_ready(dev_table(src, ts), dev_table(dst, td), (0, 100), (0, 2), 32, board, epoch)
+        with pytest.raises(dk.DynaKVError) as e:
+            dk.dyna_kv_wait(x)
+        assert e.value.status == dk.DYNA_ETIMEDOUT
     finally:
         dk.dyna_kv_ready_destroy(board)
