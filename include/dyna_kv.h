@@ -232,6 +232,14 @@ DYNA_API dyna_status dyna_kv_migrate_on_ready(dyna_block_table src, dyna_block_t
                                               struct CUstream_st* stream, const dyna_kv_opts* opts,
                                               dyna_kv_xfer_t* out);
 
+/* CUDA graphs: dyna_kv_migrate / _ex with DEVICE block tables may be captured
+ * into a CUDA graph (stream capture) and replayed; release each handle with
+ * dyna_kv_wait after the capture ends (it returns at once — the captured work
+ * runs at replay).  Host-resident tables and dyna_kv_migrate_batch (whose
+ * descriptors travel through the upload ring) are refused during capture
+ * (DYNA_ENOTSUP).  Per-chunk signalling inside a replayed graph reuses the
+ * epoch assigned at capture time. */
+
 /* Block the host until every chunk is resident in the destination, report
  * deferred errors (DYNA_ECUDA, DYNA_ERANGE from device-side id checks), free
  * the handle. */

@@ -178,3 +178,43 @@ def batch_tables(seed: int, lengths: list[int], gs: Geom, gd: Geom):
         td, free_d = fragmented_table(rng, free_d, blocks_needed(n, gd.block_size))
         out.append((ts, td))
     return out
+
+
+# --------------------------------------------------------------------------
+# configs[4]: all ordered instance pairs migrate concurrently.
+# Every rank computes the same plan from seeds alone.
+# --------------------------------------------------------------------------
+@dataclass(frozen=True)
+class PairMigration:
+    src_rank: int
+    dst_rank: int
+    req: Request
+    src_table: np.ndarray   # blocks of the source rank's pool
+    dst_table: np.ndarray   # freshly allocated blocks of the destination rank's pool
+
+
+def allpairs_plan(world: int, g: Geom, n_req: int = 4, seed_base: int = 1000) -> list[PairMigration]:
+    """Pair (i, j), i != j, ships the migrating requests of skewed_batch(seed_base + 8i + j, n_req).
+    Source blocks come from rank i's free list, destination blocks from rank j's free list
+    (both drawn in a fixed order, so the plan is identical on every rank)."""
+    reqs = {(i, j): migrating(skewed_batch(seed_base + 8 * i + j, n_req))
+            for i in range(world) for j in range(world) if i != j}
+    free_s = {i: np.arange(g.num_blocks) for i in range(world)}
+    free_d = {j: np.arange(g.num_blocks) for j in range(world)}
+    rng_s = {i: np.random.default_rng(seed_base * 7 + i) for i in range(world)}
+    rng_d = {j: np.random.default_rng(seed_base * 11 + j) for j in range(world)}
+    out = []
+    for i in range(world):
+        for j in range(world):
+            if i == j:
+                continue
+            for r in reqs[(i, j)]:
+                ts, free_s[i] = fragmented_table(rng_s[i], free_s[i], blocks_needed(r.s, g.block_size))
+                out.append(PairMigration(i, j, r, ts, None))
+    # destination blocks, receiver by receiver in sender order
+    res = []
+    for m in out:
+        td, free_d[m.dst_rank] = fragmented_table(rng_d[m.dst_rank], free_d[m.dst_rank],
+                                                  blocks_needed(m.req.s, g.block_size))
+        res.append(replace(m, dst_table=td))
+    return res

@@ -617,7 +617,11 @@ class RingLease {
 
   // Reserve `bytes` of the ring: *hptr (pinned host) is filled by the caller,
   // then copy() moves it to *dptr on the stream.  At most once per lease.
-  dyna_status reserve(size_t bytes, char** dptr, char** hptr) {
+  dyna_status reserve(size_t bytes, char** dptr, char** hptr, cudaStream_t st) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+      return fail(DYNA_ENOTSUP, "host-resident inputs cannot be captured in a CUDA graph "
+                                "(a replay would read recycled staging); pass device block_ids");
     {
       std::lock_guard<std::mutex> lk(g_rings_mu);
       UploadRing*& r = g_rings[dev_];
@@ -933,7 +937,7 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     const size_t sb = sids ? 0 : (table_upload_bytes(src, tr.end) + 15) & ~size_t(15);
     const size_t db = dids ? 0 : table_upload_bytes(dst, tr.end);
     char *base = nullptr, *h = nullptr;
-    if ((r = lease.reserve(sb + db, &base, &h))) return r;
+    if ((r = lease.reserve(sb + db, &base, &h, stream))) return r;
     if (!sids) std::memcpy(h, src.host_block_ids, table_upload_bytes(src, tr.end));
     if (!dids) std::memcpy(h + sb, dst.host_block_ids, db);
     if ((r = lease.copy(stream))) return r;
@@ -1057,7 +1061,7 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   RingLease lease(S0->dev);
   int64_t total_items = 0;
   char *dbase = nullptr, *h = nullptr;
-  if ((r = lease.reserve(plans_b + bases_b + tab_b, &dbase, &h))) {
+  if ((r = lease.reserve(plans_b + bases_b + tab_b, &dbase, &h, stream))) {
     delete x;
     return r;
   }

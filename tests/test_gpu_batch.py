@@ -125,3 +125,34 @@ def test_config3_batch_full_size():
     for r, (ts, td) in zip(reqs, tabs):
         assert torch_rows_equal(src, ts, dst, td, (0, r.s), (0, 32))
     assert untouched_equal(dst, 32, mapped_mask(g, [(td, (0, r.s)) for r, (ts, td) in zip(reqs, tabs)]))
+
+
+def test_cuda_graph_capture_and_replay():
+    """Many small migrations captured once in a CUDA graph, replayed: same bytes as the oracle."""
+    g = kvgen.TOY
+    hs, hd = kvgen.fill_bytes(1, g.pool_bytes), kvgen.fill_bytes(2, g.pool_bytes)
+    tabs = kvgen.batch_tables(1, [256] * 4, g, g)
+    want = hd.copy()
+    for ts, td in tabs:
+        oracle.migrate(hs, g, ts, want, g, td, (0, 100))
+    src, dst = pool_from_host(g, hs), pool_from_host(g, hd)
+    T = [(dev_table(src, a), dev_table(dst, b)) for a, b in tabs]
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        xs = [dk.dyna_kv_migrate_ex(a, b, (0, 100), (0, 2), 32, stream.cuda_stream, None) for a, b in T]
+        with pytest.raises(dk.DynaKVError) as e:   # host tables are refused under capture
+            dk.dyna_kv_migrate_ex(dk.table(src, None, tabs[0][0]), T[0][1], (0, 100), (0, 2), 32,
+                                  stream.cuda_stream, None)
+        assert e.value.status == dk.DYNA_ENOTSUP
+    for x in xs:
+        dk.dyna_kv_wait(x)
+    assert np.array_equal(dst.tensor.cpu().numpy(), hd)   # nothing ran yet
+    graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
+    dst.tensor.copy_(torch.from_numpy(hd).cuda())
+    graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
