@@ -27,6 +27,7 @@ DYNA_MAX_INSTANCES, DYNA_MAX_CHUNKS = 64, 4096
 DYNA_VARIANT_AUTO, DYNA_VARIANT_FUSED, DYNA_VARIANT_STAGED = 0, 1, 2
 DYNA_ENGINE_AUTO, DYNA_ENGINE_VEC, DYNA_ENGINE_BULK = 0, 1, 2
 DYNA_MIGRATE_SIGNAL = 1
+DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC = 1, 2
 
 # every symbol include/dyna_kv.h declares
 EXPORTS = (
@@ -61,7 +62,7 @@ class dyna_kv_migration(ctypes.Structure):
 
 class dyna_kv_opts(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("variant", "engine", "max_ctas", "flags", "piece_bytes", "stages",
-                                               "unroll")]
+                                               "unroll", "schedule")]
 
 
 class dyna_kv_calib_entry(ctypes.Structure):
@@ -354,8 +355,8 @@ def table(pool: Pool, ids, host_ids=None) -> dyna_block_table:
     return t
 
 
-def opts(variant=0, engine=0, max_ctas=0, flags=0, piece_bytes=0, stages=0, unroll=0) -> dyna_kv_opts:
-    return dyna_kv_opts(variant, engine, max_ctas, flags, piece_bytes, stages, unroll)
+def opts(variant=0, engine=0, max_ctas=0, flags=0, piece_bytes=0, stages=0, unroll=0, schedule=0) -> dyna_kv_opts:
+    return dyna_kv_opts(variant, engine, max_ctas, flags, piece_bytes, stages, unroll, schedule)
 
 
 def migrate(src: dyna_block_table, dst: dyna_block_table, token_range, layer_range, chunk_tokens, stream=None,

@@ -89,6 +89,8 @@ dyna_status take_device_error() {
 struct DevInfo {
   int sms = 0;
   cudaStream_t aux = nullptr;  // library stream for destination-side kernels (staged, cross-device)
+  unsigned long long* sched = nullptr;  // [kSchedSlots][2] dynamic-scheduling counters, zero at rest
+  std::atomic<uint32_t> sched_seq{0};
 };
 std::map<int, DevInfo> g_dev;
 
@@ -98,6 +100,7 @@ constexpr int kVecPiece = 8192;
 constexpr int kBulkPiece = 32768;
 constexpr int kBulkStages = 6;
 constexpr int64_t kStageSlotBytes = 64ll << 20;  // staged variant: bytes per staging slot
+constexpr uint32_t kSchedSlots = 1u << 15;       // dynamic-scheduling counter slots per device
 
 DevInfo* dev_info(int dev) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -106,6 +109,9 @@ DevInfo* dev_info(int dev) {
     DeviceGuard g(dev);
     cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
     if (d.sms <= 0) d.sms = 1;
+    if (cudaMalloc(&d.sched, sizeof(unsigned long long) * 2 * kSchedSlots) != cudaSuccess ||
+        cudaMemset(d.sched, 0, sizeof(unsigned long long) * 2 * kSchedSlots) != cudaSuccess)
+      d.sched = nullptr;  // dynamic scheduling unavailable: static round-robin
   }
   return &d;
 }
@@ -248,20 +254,28 @@ int64_t balanced_workers(int64_t n_items, int64_t max_workers) {
   return (n_items + rounds - 1) / rounds;
 }
 
+// Counter slot for one dynamically scheduled launch (nullptr: static round-robin).
+unsigned long long* sched_slot(DevInfo* di, int schedule) {
+  if (schedule == DYNA_SCHED_STATIC || !di->sched) return nullptr;
+  const uint32_t k = di->sched_seq.fetch_add(1, std::memory_order_relaxed) % kSchedSlots;
+  return di->sched + 2 * (size_t)k;
+}
+
 template <int U, bool SIG, class Src>
-void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cudaStream_t st) {
+void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cudaStream_t st,
+                unsigned long long* sched) {
   const int occ = vec_occupancy<U, SIG, Src>();
   constexpr int wpc = kVecThreads / 32;  // warps per CTA
   int64_t max_ctas = (int64_t)sms * occ;
   if (max_grid > 0) max_ctas = std::min<int64_t>(max_ctas, max_grid);
   const int64_t warps = balanced_workers(n_items, max_ctas * wpc);
   const int64_t grid = (warps + wpc - 1) / wpc;
-  k_copy_vec<U, SIG, Src><<<(unsigned)grid, kVecThreads, 0, st>>>(src);
+  k_copy_vec<U, SIG, Src><<<(unsigned)grid, kVecThreads, 0, st>>>(src, sched);
 }
 
 template <bool SIG, class Src>
 dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, int64_t max_grid, int sms,
-                        cudaStream_t st) {
+                        cudaStream_t st, unsigned long long* sched) {
   const size_t smem = (size_t)stages * piece;
   auto kern = k_copy_bulk<SIG, Src>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -270,7 +284,7 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
   if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
   int64_t cap = (int64_t)sms * occ;
   if (max_grid > 0) cap = std::min<int64_t>(cap, max_grid);
-  kern<<<(unsigned)balanced_workers(n_items, cap), 32, smem, st>>>(src, stages);
+  kern<<<(unsigned)balanced_workers(n_items, cap), 32, smem, st>>>(src, stages, sched);
   return DYNA_OK;
 }
 
@@ -278,22 +292,23 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
 // engine: DYNA_ENGINE_VEC / BULK.  SIG: per-chunk signalling (single plan only).
 template <class Src>
 dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int engine, int max_ctas, int stages,
-                       int unroll, int dev, cudaStream_t st) {
+                       int unroll, int dev, cudaStream_t st, int schedule) {
   if (n_items == 0) return DYNA_OK;
   DevInfo* di = dev_info(dev);
+  unsigned long long* sc = sched_slot(di, schedule);
   if (engine == DYNA_ENGINE_BULK) {
-    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st)
-                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st);
+    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st, sc)
+                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st, sc);
     if (r) return r;
   } else if (unroll == 4) {
-    sig ? launch_vec<4, true>(src, n_items, max_ctas, di->sms, st)
-        : launch_vec<4, false>(src, n_items, max_ctas, di->sms, st);
+    sig ? launch_vec<4, true>(src, n_items, max_ctas, di->sms, st, sc)
+        : launch_vec<4, false>(src, n_items, max_ctas, di->sms, st, sc);
   } else if (unroll == 16) {
-    sig ? launch_vec<16, true>(src, n_items, max_ctas, di->sms, st)
-        : launch_vec<16, false>(src, n_items, max_ctas, di->sms, st);
+    sig ? launch_vec<16, true>(src, n_items, max_ctas, di->sms, st, sc)
+        : launch_vec<16, false>(src, n_items, max_ctas, di->sms, st, sc);
   } else {
-    sig ? launch_vec<8, true>(src, n_items, max_ctas, di->sms, st)
-        : launch_vec<8, false>(src, n_items, max_ctas, di->sms, st);
+    sig ? launch_vec<8, true>(src, n_items, max_ctas, di->sms, st, sc)
+        : launch_vec<8, false>(src, n_items, max_ctas, di->sms, st, sc);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   CUDA_TRY(cudaGetLastError());
@@ -301,7 +316,7 @@ dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int
 }
 
 // Producer-coupled launch: VEC engine, coherent loads, per-warp ready waits.
-dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st) {
+dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st, int schedule) {
   DevInfo* di = dev_info(dev);
   SingleSource src{p};
   const bool sig = p.counters != nullptr;
@@ -317,19 +332,21 @@ dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st) 
   constexpr int wpc = kVecThreads / 32;
   const int64_t warps = balanced_workers(p.n_items, cap * wpc);
   const unsigned grid = (unsigned)((warps + wpc - 1) / wpc);
+  unsigned long long* sc = sched_slot(di, schedule);
   if (sig)
-    k_copy_vec<8, true, SingleSource, true><<<grid, kVecThreads, 0, st>>>(src);
+    k_copy_vec<8, true, SingleSource, true><<<grid, kVecThreads, 0, st>>>(src, sc);
   else
-    k_copy_vec<8, false, SingleSource, true><<<grid, kVecThreads, 0, st>>>(src);
+    k_copy_vec<8, false, SingleSource, true><<<grid, kVecThreads, 0, st>>>(src, sc);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   CUDA_TRY(cudaGetLastError());
   return DYNA_OK;
 }
 
 dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev,
-                        cudaStream_t st) {
+                        cudaStream_t st, int schedule) {
   SingleSource src{p};
-  return launch_src(src, p.n_items, p.counters != nullptr, p.piece, engine, max_ctas, stages, unroll, dev, st);
+  return launch_src(src, p.n_items, p.counters != nullptr, p.piece, engine, max_ctas, stages, unroll, dev, st,
+                    schedule);
 }
 
 // ------------------------------------------------------------------ calibration (a6)
@@ -502,7 +519,7 @@ dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t 
 // library stream of the destination device, ordered with events.
 dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, const int32_t* dids, dyna_range tr,
                        int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
-                       int max_ctas, cudaStream_t stream, dyna_kv_xfer* x) {
+                       int max_ctas, cudaStream_t stream, dyna_kv_xfer* x, int schedule) {
   if (D->imported)
     return fail(DYNA_ENOTSUP, "STAGED variant into an imported (cross-process) pool is not supported; use FUSED");
   const int64_t row = S->row;
@@ -547,11 +564,11 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
       char* dslot = dbuf + si * slot;
       if (cross && sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[si], 0));
       Plan k1 = make_plan(paged(S, sids), linear(sslot), row, sa, sb, l0, lm, sb - sa, S->desc.block_size, piece);
-      if ((r = launch_copy(k1, engine, max_ctas, stages, unroll, S->dev, stream))) break;
+      if ((r = launch_copy(k1, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
       // K2: the sub-chunk slot is [lm][2][n][row] = two contiguous halves
       // (K and V of all layers): a flat plan with one token of `half` bytes.
       Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
-      if ((r = launch_copy(k2, engine, max_ctas, stages, unroll, S->dev, stream))) break;
+      if ((r = launch_copy(k2, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
       Plan k3 = make_plan(linear(dslot), paged(D, dids), row, sa, sb, l0, lm, sb - sa, D->desc.block_size, piece);
       k3.mig_t0 = tr.begin;
       k3.mig_t1 = tr.end;
@@ -565,10 +582,10 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
         CUDA_TRY(cudaEventRecord(done_src[si], stream));
         DeviceGuard g(D->dev);
         CUDA_TRY(cudaStreamWaitEvent(dstream, done_src[si], 0));
-        if ((r = launch_copy(k3, engine, max_ctas, stages, unroll, D->dev, dstream))) break;
+        if ((r = launch_copy(k3, engine, max_ctas, stages, unroll, D->dev, dstream, schedule))) break;
         CUDA_TRY(cudaEventRecord(done_dst[si], dstream));
       } else {
-        if ((r = launch_copy(k3, engine, max_ctas, stages, unroll, S->dev, stream))) break;
+        if ((r = launch_copy(k3, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
       }
     }
   }
@@ -691,7 +708,8 @@ dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
   if (opts) *o = *opts;
   if (o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > 2 || o->max_ctas < 0 || o->piece_bytes < 0 ||
       o->piece_bytes % 16 || o->stages < 0 || o->stages == 1 || o->stages > kMaxStages ||
-      (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16))
+      (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16) || o->schedule < 0 ||
+      o->schedule > DYNA_SCHED_DYNAMIC)
     return fail(DYNA_EINVAL, "invalid dyna_kv_opts");
   return DYNA_OK;
 }
@@ -972,12 +990,13 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
       p.ready = board->slots;
       p.ready_epoch = ready_epoch;
       p.ready_timeout_ns = board->timeout_ns;
-      r = launch_ready(p, o.max_ctas, S->dev, stream);
+      r = launch_ready(p, o.max_ctas, S->dev, stream, o.schedule);
     } else {
-      r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream);
+      r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream, o.schedule);
     }
   } else {
-    r = run_staged(S, D, sids, dids, tr, l0, lm, c, signal, engine, piece, stages, unroll, o.max_ctas, stream, x);
+    r = run_staged(S, D, sids, dids, tr, l0, lm, c, signal, engine, piece, stages, unroll, o.max_ctas, stream, x,
+                   o.schedule);
   }
   if (!r) r = lease.finish(stream);
   if (r) {
@@ -1100,7 +1119,8 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   x->stages = ch.engine == DYNA_ENGINE_BULK ? ch.stages : 0;
   x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
   x->launches = 1;
-  r = launch_src(bsrc, total_items, false, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev, stream);
+  r = launch_src(bsrc, total_items, false, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev, stream,
+                 o.schedule);
   if (!r) r = lease.finish(stream);
   if (r) {
     delete x;

@@ -201,6 +201,42 @@ __device__ __forceinline__ void account_chunk(const Plan& p, int32_t k, uint32_t
   }
 }
 
+// ------------------------------------------------------------------ work distribution
+// Static round-robin (ctr == nullptr) or dynamic: workers grab the next item
+// index from a per-launch counter ctr[0], prefetched one grab ahead so the
+// atomic's latency overlaps the current item.  ctr[1] counts finished
+// workers; the last one resets the slot for the launch that reuses it.
+struct Sched {
+  unsigned long long* ctr;
+  int64_t next, stride;
+  unsigned long long pre;
+  __device__ __forceinline__ void init(unsigned long long* c, int64_t first, int64_t stride_) {
+    ctr = c;
+    next = first;
+    stride = stride_;
+    if (ctr) pre = atomicAdd(ctr, 1ull);
+  }
+  __device__ __forceinline__ int64_t get() {
+    if (!ctr) {
+      const int64_t r = next;
+      next += stride;
+      return r;
+    }
+    const int64_t r = (int64_t)pre;
+    pre = atomicAdd(ctr, 1ull);
+    return r;
+  }
+  __device__ __forceinline__ void finish(unsigned long long n_workers) {
+    if (!ctr) return;
+    __threadfence();  // this worker's grabs are performed before it counts itself done
+    if (atomicAdd(ctr + 1, 1ull) == n_workers - 1) {
+      __threadfence();
+      ctr[0] = 0ull;
+      ctr[1] = 0ull;
+    }
+  }
+};
+
 // ------------------------------------------------------------------ VEC engine
 __device__ __forceinline__ int4 ld_nc_v4(const int4* ptr) {
   int4 r;
@@ -254,10 +290,12 @@ __device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __
 }
 
 template <int U, bool SIGNAL, class Src, bool READY = false>
-__global__ void __launch_bounds__(256) k_copy_vec(const Src src) {
+__global__ void __launch_bounds__(256) k_copy_vec(const Src src, unsigned long long* sched_ctr) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  Sched sched;  // lane 0 grabs, the warp follows
+  if (lane == 0) sched.init(sched_ctr, warp, nwarps);
   // Signalling: a warp's consecutive items mostly share a chunk (chunk-major
   // order), so bytes are accumulated per chunk and fenced + counted once when
   // the warp moves on to another chunk — one fence per (warp, chunk), not per item.
@@ -265,7 +303,11 @@ __global__ void __launch_bounds__(256) k_copy_vec(const Src src) {
   uint32_t cur_acc = 0;
   int32_t ready_k = -1;
   const int64_t n_items = src.total();
-  for (int64_t gitem = warp; gitem < n_items; gitem += nwarps) {
+  for (;;) {
+    long long gi = 0;
+    if (lane == 0) gi = sched.get();
+    const int64_t gitem = __shfl_sync(0xffffffffu, gi, 0);
+    if (gitem >= n_items) break;
     int64_t item = gitem;
     const Plan& p = src.locate(item);
     const Item it = decode_item(p, item);
@@ -291,6 +333,7 @@ __global__ void __launch_bounds__(256) k_copy_vec(const Src src) {
     __syncwarp();
     if (lane == 0) account_chunk(src.locate_signal(), cur_k, cur_acc);
   }
+  if (lane == 0) sched.finish((unsigned long long)nwarps);
 }
 
 // ------------------------------------------------------------------ BULK engine
@@ -342,7 +385,7 @@ constexpr int kMaxStages = 16;
 // loads land in slots ahead of the store front; each slot is reloaded once
 // the store issued from it has been read out of shared memory.
 template <bool SIGNAL, class Src>
-__global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages) {
+__global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, unsigned long long* sched_ctr) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ char* pend_dst[kMaxStages];
@@ -354,18 +397,22 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
-  int64_t next = blockIdx.x;
-  const int64_t stride = gridDim.x;
+  Sched sched;
+  sched.init(sched_ctr, blockIdx.x, gridDim.x);
+  bool drained = false;
   const int64_t n_items = src.total();
   const Plan& p = src.locate_signal();  // used only for per-launch fields (piece, signalling)
 
   // Load the next non-empty item of this CTA into slot s (pend_n[s] = 0 if none).
   auto refill = [&](int s) {
-    while (next < n_items) {
-      int64_t item = next;
+    while (!drained) {
+      int64_t item = sched.get();
+      if (item >= n_items) {
+        drained = true;
+        break;
+      }
       const Plan& ip = src.locate(item);
       const Item it = decode_item(ip, item);
-      next += stride;
       if (it.n == 0) {
         if (SIGNAL && it.acc) account_chunk(p, it.k, it.acc);  // skipped (bad id): still closes the chunk
         continue;
@@ -434,6 +481,7 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages) {
       account_chunk(p, cur_k, cur_acc);
     }
   }
+  sched.finish(gridDim.x);
 }
 
 // ------------------------------------------------------------------ consumer-side chunk wait

@@ -18,3 +18,8 @@ if [ -z "$NOBENCH" ]; then
 fi
 if [ -n "$OVERLAP" ]; then timeout 900 python scripts/overlap.py > gpurun_out/overlap.log 2>&1; tail -20 gpurun_out/overlap.log; fi
 if [ -n "$CONFIGS" ]; then timeout 900 python scripts/configs_sweep.py > gpurun_out/configs.log 2>&1; tail -20 gpurun_out/configs.log; fi
+if [ -n "$PROBE" ]; then
+  timeout 300 python scripts/batch_probe.py 2>&1 | tail -8
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_copy -s 3 -c 1 -o gpurun_out/prof_batch_bulk \
+      env ONLY=batch-bulk-2 python scripts/batch_probe.py > gpurun_out/ncu_batch.log 2>&1
+fi

@@ -79,8 +79,24 @@ def test_contiguous_tables(engine):
 
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("max_ctas", [1, 3, 150])
-def test_sm_budget(engine, max_ctas):
-    _parity(kvgen.TOY, kvgen.TOY, 256, (0, 100), (0, 2), 32, engine=engine, max_ctas=max_ctas)
+@pytest.mark.parametrize("schedule", [dk.DYNA_SCHED_STATIC, dk.DYNA_SCHED_DYNAMIC])
+def test_sm_budget_and_schedule(engine, max_ctas, schedule):
+    _parity(kvgen.TOY, kvgen.TOY, 256, (0, 100), (0, 2), 32, engine=engine, max_ctas=max_ctas, schedule=schedule)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_dynamic_schedule_slots_are_reusable(engine):
+    """Hundreds of back-to-back dynamically scheduled launches: every counter slot must come back
+    clean (a stale counter would skip items and leave rows uncopied)."""
+    g = LLAMA3_ROWS
+    src, dst = pool_filled(g, 61), pool_filled(g, 62)
+    ts, td = kvgen.table_pair(8, 6000, g, g)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    xs = [dk.migrate(st, dt, (a, a + 64), (0, 4), 64, engine=engine, schedule=dk.DYNA_SCHED_DYNAMIC)
+          for a in range(0, 5952, 16)]
+    for x in xs:
+        dk.dyna_kv_wait(x)
+    assert torch_rows_equal(src, ts, dst, td, (0, 6000), (0, 4))
 
 
 @pytest.mark.parametrize("engine", ENGINES)
