@@ -130,7 +130,7 @@ typedef struct {
     int32_t piece_bytes;/* bytes per work item; 0 = engine default.  Multiple of 16. */
     int32_t stages;     /* BULK: shared-memory ring depth (2..16); 0 = default */
     int32_t unroll;     /* VEC: 16-B loads in flight per lane (4, 8 or 16); 0 = default */
-    int32_t schedule;   /* work distribution: 0 = default (dynamic), DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC */
+    int32_t schedule;   /* work distribution: 0 = default (static), DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC */
 } dyna_kv_opts;
 #define DYNA_SCHED_STATIC  1   /* round-robin items over a balanced persistent grid */
 #define DYNA_SCHED_DYNAMIC 2   /* workers grab items from a per-launch atomic counter (no static tail) */

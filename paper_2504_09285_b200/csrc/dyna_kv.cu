@@ -151,6 +151,7 @@ struct dyna_kv_ready {
 
 struct dyna_kv_xfer {
   cudaEvent_t ev = nullptr;
+  bool captured = false;  // enqueued during CUDA-graph capture: the work runs at replay
   int32_t variant = 0, engine = 0, piece = 0, stages = 0, unroll = 0, launches = 0;
   int dev = 0;
   bool empty = false;
@@ -256,7 +257,7 @@ int64_t balanced_workers(int64_t n_items, int64_t max_workers) {
 
 // Counter slot for one dynamically scheduled launch (nullptr: static round-robin).
 unsigned long long* sched_slot(DevInfo* di, int schedule) {
-  if (schedule == DYNA_SCHED_STATIC || !di->sched) return nullptr;
+  if (schedule != DYNA_SCHED_DYNAMIC || !di->sched) return nullptr;  // default: static
   const uint32_t k = di->sched_seq.fetch_add(1, std::memory_order_relaxed) % kSchedSlots;
   return di->sched + 2 * (size_t)k;
 }
@@ -599,6 +600,20 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
     }
   }
   return r;
+}
+
+// Completion event of a migration (none while the stream is being captured
+// into a CUDA graph: the captured work only runs at replay).
+dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone) {
+    x->captured = true;
+    return DYNA_OK;
+  }
+  cudaError_t e = get_event(dev, &x->ev);
+  if (e == cudaSuccess) e = cudaEventRecord(x->ev, stream);
+  if (e != cudaSuccess) return fail(DYNA_ECUDA, "event record: %s", cudaGetErrorString(e));
+  return DYNA_OK;
 }
 
 // ------------------------------------------------------------------ upload ring
@@ -1004,11 +1019,9 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     return r;
   }
   x->launches = (int32_t)(g_launches.load() - launches0);
-  cudaError_t e = get_event(S->dev, &x->ev);
-  if (e == cudaSuccess) e = cudaEventRecord(x->ev, stream);
-  if (e != cudaSuccess) {
+  if ((r = record_completion(x, S->dev, stream))) {
     delete x;
-    return fail(DYNA_ECUDA, "event record: %s", cudaGetErrorString(e));
+    return r;
   }
   *out = x;
   return DYNA_OK;
@@ -1057,7 +1070,14 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   }
   x->dev = S0->dev;
   x->sender = S0->desc.instance;
-  const Choice ch = choose(o, S0->row, peer, total_tok);
+  Choice ch = choose(o, S0->row, peer, total_tok);
+  if (!o.engine && ch.engine == DYNA_ENGINE_BULK) {
+    // measured (scripts/batch_probe.py): with many plans the BULK engine's single issuing
+    // thread is latency-bound on per-item plan lookups; the warp-parallel VEC engine is not
+    ch.engine = DYNA_ENGINE_VEC;
+    ch.unroll = kVecU;
+    if (!o.piece_bytes) ch.piece = kVecPiece;
+  }
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
   DeviceGuard guard(S0->dev);
   // One upload: [plans][item bases][host-resident tables].
@@ -1126,11 +1146,9 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     delete x;
     return r;
   }
-  cudaError_t e = get_event(S0->dev, &x->ev);
-  if (e == cudaSuccess) e = cudaEventRecord(x->ev, stream);
-  if (e != cudaSuccess) {
+  if ((r = record_completion(x, S0->dev, stream))) {
     delete x;
-    return fail(DYNA_ECUDA, "event record: %s", cudaGetErrorString(e));
+    return r;
   }
   *out = x;
   return DYNA_OK;
@@ -1187,7 +1205,7 @@ dyna_status dyna_kv_ready_mark(dyna_kv_ready_t b, int32_t chunk, uint64_t epoch,
 
 dyna_status dyna_kv_query(dyna_kv_xfer_t x) {
   if (!x) return fail(DYNA_EINVAL, "NULL xfer");
-  if (x->empty) return DYNA_OK;
+  if (x->empty || x->captured) return DYNA_OK;
   cudaError_t e = cudaEventQuery(x->ev);
   if (e == cudaSuccess) return DYNA_OK;
   if (e == cudaErrorNotReady) return DYNA_EAGAIN;
@@ -1197,7 +1215,7 @@ dyna_status dyna_kv_query(dyna_kv_xfer_t x) {
 dyna_status dyna_kv_wait(dyna_kv_xfer_t x) {
   if (!x) return fail(DYNA_EINVAL, "NULL xfer");
   dyna_status r = DYNA_OK;
-  if (!x->empty) {
+  if (!x->empty && !x->captured) {
     cudaError_t e = cudaEventSynchronize(x->ev);
     if (e != cudaSuccess) r = fail(DYNA_ECUDA, "migration failed: %s", cudaGetErrorString(e));
     put_event(x->dev, x->ev);
@@ -1210,6 +1228,7 @@ dyna_status dyna_kv_wait(dyna_kv_xfer_t x) {
 dyna_status dyna_kv_stream_wait(dyna_kv_xfer_t x, struct CUstream_st* stream) {
   if (!x) return fail(DYNA_EINVAL, "NULL xfer");
   if (x->empty) return DYNA_OK;
+  if (x->captured) return fail(DYNA_ENOTSUP, "captured migration: order on the graph instead");
   CUDA_TRY(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), x->ev, 0));
   return DYNA_OK;
 }
