@@ -15,7 +15,8 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdyna_kv.so")
+# DYNA_KV_LIB: load another build of the same library (A/B experiments on one box)
+LIB_PATH = os.environ.get("DYNA_KV_LIB") or os.path.join(_PKG, "libdyna_kv.so")
 
 # ---------------------------------------------------------------- constants (include/dyna_kv.h)
 DYNA_OK, DYNA_EINVAL, DYNA_EGEOM, DYNA_ERANGE, DYNA_EALIAS = 0, -1, -2, -3, -4
@@ -123,6 +124,8 @@ def _load():
         "dyna_kv_debug_fill": (st, [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, vp]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("DYNA_KV_LIB") and not hasattr(L, name):
+            continue  # an older build under A/B test may lack newer entry points
         f = getattr(L, name)
         f.restype, f.argtypes = res, args
     return L

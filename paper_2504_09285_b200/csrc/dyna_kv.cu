@@ -227,6 +227,12 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   p.mig_t1 = t1;
   p.sig_c = (int32_t)c;
   p.err = g_err_word;
+  p.f_ipc = FastDiv::make((uint32_t)p.items_per_chunk);
+  p.f_P = FastDiv::make((uint32_t)p.P);
+  p.f_R = FastDiv::make((uint32_t)p.R);
+  p.f_g = FastDiv::make((uint32_t)p.g);
+  if (!p.src.linear) p.src.fbs = FastDiv::make((uint32_t)p.src.bs);
+  if (!p.dst.linear) p.dst.fbs = FastDiv::make((uint32_t)p.dst.bs);
   return p;
 }
 
@@ -295,6 +301,9 @@ template <class Src>
 dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int engine, int max_ctas, int stages,
                        int unroll, int dev, cudaStream_t st, int schedule) {
   if (n_items == 0) return DYNA_OK;
+  if (n_items >= (int64_t(1) << 31))
+    return fail(DYNA_ERANGE, "%lld work items in one launch (item math is 32-bit); use a larger piece or split the range",
+                (long long)n_items);
   DevInfo* di = dev_info(dev);
   unsigned long long* sc = sched_slot(di, schedule);
   if (engine == DYNA_ENGINE_BULK) {
@@ -741,6 +750,7 @@ dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& d
     return fail(DYNA_ERANGE, "layer range [%lld, %lld) outside [0, %d)", (long long)lr.begin, (long long)lr.end,
                 gs.num_layers);
   if (tr.begin < 0 || tr.begin > tr.end) return fail(DYNA_ERANGE, "bad token range");
+  if (tr.end >= (int64_t(1) << 31)) return fail(DYNA_ERANGE, "token indices must be < 2^31");
   *empty = tr.begin == tr.end || lr.begin == lr.end;
   if (*empty) return DYNA_OK;
   if (chunk_tokens <= 0) return fail(DYNA_ERANGE, "chunk_tokens must be > 0");
