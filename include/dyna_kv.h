@@ -118,7 +118,8 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
 /* Copy engine inside the kernels. */
 #define DYNA_ENGINE_AUTO 0
 #define DYNA_ENGINE_VEC  1     /* warp-per-segment 16-B vector loads/stores (LDG.128 / STG.128) */
-#define DYNA_ENGINE_BULK 2     /* TMA bulk copies through a shared-memory ring (UBLKCP) */
+#define DYNA_ENGINE_BULK 2     /* TMA bulk copies through a shared-memory ring (UBLKCP), one issuing thread */
+#define DYNA_ENGINE_BULK_WS 3  /* same ring, warp-specialised: a loader warp and a storer warp (mbarrier hand-off) */
 /* flags */
 #define DYNA_MIGRATE_SIGNAL 1  /* write a per-chunk flag into the destination pool's inbox */
 
@@ -149,7 +150,7 @@ typedef struct {
     int32_t peer;
     int32_t max_chunk_tokens;
     int32_t variant;      /* DYNA_VARIANT_FUSED / STAGED */
-    int32_t engine;       /* DYNA_ENGINE_VEC / BULK */
+    int32_t engine;       /* DYNA_ENGINE_VEC / BULK / BULK_WS */
     int32_t piece_bytes;  /* 0 = engine default */
     int32_t stages;
     int32_t unroll;

@@ -282,16 +282,17 @@ void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cuda
 
 template <bool SIG, class Src>
 dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, int64_t max_grid, int sms,
-                        cudaStream_t st, unsigned long long* sched) {
+                        cudaStream_t st, unsigned long long* sched, bool ws) {
   const size_t smem = (size_t)stages * piece;
-  auto kern = k_copy_bulk<SIG, Src>;
+  auto kern = ws ? k_copy_bulk_ws<SIG, Src> : k_copy_bulk<SIG, Src>;
+  const int threads = ws ? 64 : 32;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
   if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
   int64_t cap = (int64_t)sms * occ;
   if (max_grid > 0) cap = std::min<int64_t>(cap, max_grid);
-  kern<<<(unsigned)balanced_workers(n_items, cap), 32, smem, st>>>(src, stages, sched);
+  kern<<<(unsigned)balanced_workers(n_items, cap), threads, smem, st>>>(src, stages, sched);
   return DYNA_OK;
 }
 
@@ -306,9 +307,10 @@ dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int
                 (long long)n_items);
   DevInfo* di = dev_info(dev);
   unsigned long long* sc = sched_slot(di, schedule);
-  if (engine == DYNA_ENGINE_BULK) {
-    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st, sc)
-                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st, sc);
+  if (engine == DYNA_ENGINE_BULK || engine == DYNA_ENGINE_BULK_WS) {
+    const bool ws = engine == DYNA_ENGINE_BULK_WS;
+    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st, sc, ws)
+                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st, sc, ws);
     if (r) return r;
   } else if (unroll == 4) {
     sig ? launch_vec<4, true>(src, n_items, max_ctas, di->sms, st, sc)
@@ -730,7 +732,7 @@ class RingLease {
 dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
   *o = dyna_kv_opts{};
   if (opts) *o = *opts;
-  if (o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > 2 || o->max_ctas < 0 || o->piece_bytes < 0 ||
+  if (o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > 3 || o->max_ctas < 0 || o->piece_bytes < 0 ||
       o->piece_bytes % 16 || o->stages < 0 || o->stages == 1 || o->stages > kMaxStages ||
       (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16) || o->schedule < 0 ||
       o->schedule > DYNA_SCHED_DYNAMIC)
@@ -788,7 +790,7 @@ Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok) {
   const bool use_ce = calibrated && (!o.engine || o.engine == ce.engine);
   c.piece = o.piece_bytes ? o.piece_bytes
                           : (use_ce && ce.piece_bytes ? ce.piece_bytes
-                                                     : (c.engine == DYNA_ENGINE_BULK ? kBulkPiece : kVecPiece));
+                                                     : (c.engine == DYNA_ENGINE_VEC ? kVecPiece : kBulkPiece));
   c.stages = o.stages ? o.stages : (use_ce && ce.stages ? ce.stages : kBulkStages);
   c.unroll = o.unroll ? o.unroll : (use_ce && ce.unroll ? ce.unroll : kVecU);
   return c;
@@ -811,7 +813,7 @@ dyna_status dyna_kv_calib_set(const dyna_kv_calib_entry* entries, int32_t n) {
   for (int32_t i = 0; i < n; ++i) {
     const auto& e = entries[i];
     if (e.row_bytes < 0 || e.peer < 0 || e.peer > 1 || e.max_chunk_tokens <= 0 || e.variant < 0 || e.variant > 2 ||
-        e.engine < 0 || e.engine > 2 || e.piece_bytes < 0 || e.piece_bytes % 16 || e.stages < 0 || e.stages == 1 ||
+        e.engine < 0 || e.engine > 3 || e.piece_bytes < 0 || e.piece_bytes % 16 || e.stages < 0 || e.stages == 1 ||
         e.stages > kMaxStages || (e.unroll != 0 && e.unroll != 4 && e.unroll != 8 && e.unroll != 16))
       return fail(DYNA_EINVAL, "calibration entry %d invalid", i);
   }
@@ -942,7 +944,7 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     if (board->dev != src.pool->dev) return fail(DYNA_EINVAL, "ready board must live on the source device");
     if (nchunks > board->max_chunks)
       return fail(DYNA_ERANGE, "%lld chunks > the ready board's %d slots", (long long)nchunks, board->max_chunks);
-    if (o.variant == DYNA_VARIANT_STAGED || o.engine == DYNA_ENGINE_BULK)
+    if (o.variant == DYNA_VARIANT_STAGED || (o.engine && o.engine != DYNA_ENGINE_VEC))
       return fail(DYNA_ENOTSUP, "producer-coupled migration: FUSED variant, VEC engine only");
   }
   if (empty) {  // s = 0 (or no layers) -> nothing to ship, nothing enqueued
@@ -995,7 +997,7 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   x->variant = variant;
   x->engine = engine;
   x->piece = piece;
-  x->stages = engine == DYNA_ENGINE_BULK ? stages : 0;
+  x->stages = engine != DYNA_ENGINE_VEC ? stages : 0;
   x->unroll = engine == DYNA_ENGINE_VEC ? unroll : 0;
   const uint64_t launches0 = g_launches.load();
   if (variant == DYNA_VARIANT_FUSED) {
@@ -1081,7 +1083,7 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   x->dev = S0->dev;
   x->sender = S0->desc.instance;
   Choice ch = choose(o, S0->row, peer, total_tok);
-  if (!o.engine && ch.engine == DYNA_ENGINE_BULK) {
+  if (!o.engine && ch.engine != DYNA_ENGINE_VEC) {
     // measured (scripts/batch_probe.py): with many plans the BULK engine's single issuing
     // thread is latency-bound on per-item plan lookups; the warp-parallel VEC engine is not
     ch.engine = DYNA_ENGINE_VEC;
@@ -1146,7 +1148,7 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   x->variant = DYNA_VARIANT_FUSED;
   x->engine = ch.engine;
   x->piece = ch.piece;
-  x->stages = ch.engine == DYNA_ENGINE_BULK ? ch.stages : 0;
+  x->stages = ch.engine != DYNA_ENGINE_VEC ? ch.stages : 0;
   x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
   x->launches = 1;
   r = launch_src(bsrc, total_items, false, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev, stream,

@@ -107,7 +107,11 @@ struct Item {
 __device__ __forceinline__ int64_t side_row(const Side& s, const Plan& p, int l, int kv, int64_t t,
                                             int64_t a, int64_t clen, bool& bad) {
   if (s.linear) return (((int64_t)(l - p.l0) * 2 + kv) * clen + (t - a)) * p.row;
+#ifndef DYNA_NO_FASTDIV
   const int64_t jb = s.fbs.div((uint32_t)t);  // token indices are < 2^31
+#else
+  const int64_t jb = t / s.bs;
+#endif
   const int32_t b = __ldg(s.table + jb);
   if (b < 0 || (int64_t)b >= s.nb) { bad = true; return 0; }
   return ((((int64_t)l * 2 + kv) * s.nb + b) * s.bs + (t - jb * s.bs)) * p.row;
@@ -115,6 +119,7 @@ __device__ __forceinline__ int64_t side_row(const Side& s, const Plan& p, int l,
 
 __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   Item it{nullptr, nullptr, 0u, 0u, 0};
+#ifndef DYNA_NO_FASTDIV
   const uint32_t it32 = (uint32_t)item;
   const uint32_t k = p.f_ipc.div(it32);
   uint32_t i = it32 - k * (uint32_t)p.items_per_chunk;
@@ -129,6 +134,17 @@ __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   const int64_t a = p.t0 + (int64_t)k * p.c;
   const int64_t b = min(a + (int64_t)p.c, p.t1);
   const int64_t G = (int64_t)p.f_g.div((uint32_t)a) + j;
+#else
+  const int64_t k = item / p.items_per_chunk;
+  int64_t i = item - k * p.items_per_chunk;
+  const int32_t pp = (int32_t)(i % p.P); i /= p.P;
+  const int32_t j = (int32_t)(i % p.R);  i /= p.R;
+  const int kv = (int)(i & 1);
+  const int l = p.l0 + (int)(i >> 1);
+  const int64_t a = p.t0 + k * p.c;
+  const int64_t b = min(a + (int64_t)p.c, p.t1);
+  const int64_t G = a / p.g + j;
+#endif
   const int64_t ta = max(a, G * p.g);
   const int64_t tb = min(b, (G + 1) * p.g);
   it.k = (int32_t)((a - p.mig_t0) / p.sig_c);
@@ -431,20 +447,19 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, uns
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 
-  Sched sched;
-  sched.init(sched_ctr, blockIdx.x, gridDim.x);
-  bool drained = false;
+  // Static round-robin only: this single thread's loop is latency-critical and
+  // measured ~12% slower with the dynamic-scheduling path compiled in.
+  (void)sched_ctr;
+  int64_t next = blockIdx.x;
+  const int64_t stride = gridDim.x;
   const int64_t n_items = src.total();
   const Plan& p = src.locate_signal();  // used only for per-launch fields (piece, signalling)
 
   // Load the next non-empty item of this CTA into slot s (pend_n[s] = 0 if none).
   auto refill = [&](int s) {
-    while (!drained) {
-      int64_t item = sched.get();
-      if (item >= n_items) {
-        drained = true;
-        break;
-      }
+    while (next < n_items) {
+      int64_t item = next;
+      next += stride;
       const Plan& ip = src.locate(item);
       const Item it = decode_item(ip, item);
       if (it.n == 0) {
@@ -515,7 +530,133 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, uns
       account_chunk(p, cur_k, cur_acc);
     }
   }
-  sched.finish(gridDim.x);
+}
+
+// ------------------------------------------------------------------ BULK engine, warp-specialised
+// Warp 0 (one elected lane) decodes items and issues TMA bulk loads into a
+// ring of `stages` smem slots; warp 1 (one lane) drains each landed slot with
+// a TMA bulk store and hands the slot back.  full[s] completes when a load's
+// bytes land (complete_tx); empty[s] when the store has read the slot out.
+// The loader's decode latency no longer sits between consecutive stores.
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <bool SIGNAL, class Src>
+__global__ void __launch_bounds__(64) k_copy_bulk_ws(const Src src, int stages, unsigned long long* sched_ctr) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ __align__(8) uint64_t empty[kMaxStages];
+  __shared__ char* pend_dst[kMaxStages];
+  __shared__ uint32_t pend_n[kMaxStages];
+  __shared__ int32_t pend_k[kMaxStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 1 && lane != 0) return;  // the storer is one thread; the loader is a whole warp
+  const Plan& p = src.locate_signal();
+  const int64_t n_items = src.total();
+
+  if (warp == 0) {  // ---------------- loader: 32 lanes decode, lane 0 issues
+    (void)sched_ctr;  // static round-robin over CTAs: item(m) = blockIdx.x + m * gridDim.x
+    int64_t m = 0;
+    Item mine{nullptr, nullptr, 0u, 0u, 0};
+    uint32_t todo = 0;      // lanes whose decoded item still has to be issued
+    bool drained = false;
+    for (int64_t iter = 0;; ++iter) {
+      const int s = (int)(iter % stages);
+      while (todo == 0 && !drained) {  // decode the CTA's next 32 items, one per lane
+        const int64_t gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
+        m += 32;
+        mine = Item{nullptr, nullptr, 0u, 0u, 0};
+        if (gi < n_items) {
+          int64_t item = gi;
+          const Plan& ip = src.locate(item);
+          mine = decode_item(ip, item);
+          if (SIGNAL && mine.n == 0 && mine.acc) account_chunk(p, mine.k, mine.acc);  // skipped (bad id)
+        }
+        todo = __ballot_sync(0xffffffffu, mine.n != 0);
+        drained = __ballot_sync(0xffffffffu, gi >= n_items) != 0;
+      }
+      const bool have = todo != 0;  // warp-uniform
+      const int from = have ? __ffs(todo) - 1 : 0;
+      if (have) todo &= todo - 1;
+      const uint64_t isrc = __shfl_sync(0xffffffffu, (unsigned long long)mine.src, from);
+      const uint64_t idst = __shfl_sync(0xffffffffu, (unsigned long long)mine.dst, from);
+      const uint32_t in = __shfl_sync(0xffffffffu, mine.n, from);
+      const int32_t ik = __shfl_sync(0xffffffffu, mine.k, from);
+      const uint32_t n = have ? in : 0u;  // 0: no work left
+      if (lane == 0) {
+        if (iter >= stages) mbar_wait(&empty[s], (uint32_t)(((iter / stages) - 1) & 1));
+        pend_dst[s] = reinterpret_cast<char*>(idst);
+        pend_n[s] = n;
+        pend_k[s] = ik;
+        if (n == 0) {
+          mbar_arrive(&full[s]);  // no more work: a plain arrive tells the storer
+        } else {
+          mbar_expect_tx(&full[s], n);
+          bulk_load(ring + (size_t)s * p.piece, reinterpret_cast<const char*>(isrc), n, &full[s]);
+        }
+      }
+      __syncwarp();
+      if (n == 0) break;
+    }
+  } else {  // ---------------- storer
+    constexpr int kDefer = 4;
+    int32_t cur_k = -1, park_k = -1;
+    uint32_t cur_acc = 0, park_acc = 0;
+    int since_park = 0;
+    auto flush_park = [&](bool all) {
+      if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      fence_for(p);
+      account_chunk(p, park_k, park_acc);
+      park_k = -1;
+      park_acc = 0;
+    };
+    int64_t pending_release = -1;  // slot index whose store was issued last (released one store later)
+    for (int64_t iter = 0;; ++iter) {
+      const int s = (int)(iter % stages);
+      mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
+      const uint32_t n = pend_n[s];
+      if (n == 0) break;
+      if (SIGNAL && pend_k[s] != cur_k) {
+        if (park_acc) flush_park(true);
+        park_k = cur_k;
+        park_acc = cur_acc;
+        since_park = 0;
+        cur_k = pend_k[s];
+        cur_acc = 0;
+      }
+      bulk_store(pend_dst[s], ring + (size_t)s * p.piece, n);
+      bulk_commit();
+      if (SIGNAL) {
+        cur_acc += n;
+        if (park_acc && ++since_park == kDefer) flush_park(false);
+      }
+      if (pending_release >= 0) {  // the previous store has read its slot out: hand it back
+        bulk_wait_read<1>();
+        mbar_arrive(&empty[(int)(pending_release % stages)]);
+      }
+      pending_release = iter;
+    }
+    bulk_wait_all<0>();
+    if (SIGNAL) {
+      if (park_acc) flush_park(true);
+      if (cur_acc) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        fence_for(p);
+        account_chunk(p, cur_k, cur_acc);
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ consumer-side chunk wait

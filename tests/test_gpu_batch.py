@@ -13,7 +13,7 @@ from kvgen import Geom
 from gpu_util import dev_table, mapped_mask, pool_filled, pool_from_host, torch_rows_equal, untouched_equal
 
 pytestmark = pytest.mark.gpu
-ENGINES = [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK]
+ENGINES = [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK, dk.DYNA_ENGINE_BULK_WS]
 
 
 def host_table(pool, ids):

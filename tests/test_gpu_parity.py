@@ -21,7 +21,7 @@ from gpu_util import (dev_table, mapped_mask, migrate_and_wait, pool_filled, poo
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK]
+ENGINES = [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK, dk.DYNA_ENGINE_BULK_WS]
 VARIANTS = [dk.DYNA_VARIANT_FUSED, dk.DYNA_VARIANT_STAGED]
 
 
@@ -103,7 +103,7 @@ def test_dynamic_schedule_slots_are_reusable(engine):
 @pytest.mark.parametrize("piece,stages", [(256, 2), (1024, 3), (4096, 4), (4096, 16), (16384, 8), (65536, 3)])
 @pytest.mark.parametrize("unroll", [4, 8, 16])
 def test_piece_and_stage_shapes(engine, piece, stages, unroll):
-    if engine == dk.DYNA_ENGINE_BULK and unroll != 8:
+    if engine != dk.DYNA_ENGINE_VEC and unroll != 8:
         pytest.skip("unroll applies to VEC only")
     g = Geom(2, 8, 128, 2, 16, 64)  # row 2 KiB
     for flags in (0, dk.DYNA_MIGRATE_SIGNAL):
