@@ -227,12 +227,6 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   p.mig_t1 = t1;
   p.sig_c = (int32_t)c;
   p.err = g_err_word;
-  p.f_ipc = FastDiv::make((uint32_t)p.items_per_chunk);
-  p.f_P = FastDiv::make((uint32_t)p.P);
-  p.f_R = FastDiv::make((uint32_t)p.R);
-  p.f_g = FastDiv::make((uint32_t)p.g);
-  if (!p.src.linear) p.src.fbs = FastDiv::make((uint32_t)p.src.bs);
-  if (!p.dst.linear) p.dst.fbs = FastDiv::make((uint32_t)p.dst.bs);
   return p;
 }
 

@@ -28,40 +28,12 @@
 
 namespace dynakv {
 
-// Unsigned 32-bit division by a divisor fixed per launch, as a multiply-high and
-// two shifts (Granlund & Montgomery, "Division by invariant integers using
-// multiplication", 1994): exact for every n < 2^32 and 1 <= d < 2^31.  The
-// single issuing thread of the BULK engine decodes every item, so software
-// 64-bit divisions there would cost more than the item's copy time.
-struct FastDiv {
-  uint32_t d, m, s1, s2;
-  static FastDiv make(uint32_t d) {
-    FastDiv f{};
-    f.d = d;
-    uint32_t l = 0;
-    while ((1ull << l) < d) ++l;  // ceil(log2 d)
-    f.m = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
-    f.s1 = l > 0 ? 1u : 0u;
-    f.s2 = l > 0 ? l - 1 : 0u;
-    return f;
-  }
-  __host__ __device__ __forceinline__ uint32_t div(uint32_t n) const {
-#ifdef __CUDA_ARCH__
-    const uint32_t t1 = __umulhi(m, n);
-#else
-    const uint32_t t1 = (uint32_t)(((uint64_t)m * n) >> 32);
-#endif
-    return (t1 + ((n - t1) >> s1)) >> s2;
-  }
-};
-
 struct Side {
   char* base;            // pool base, or staging base for a linear side
   const int32_t* table;  // block table (paged side); nullptr for a linear side
   int64_t nb;            // blocks in the pool (paged side)
   int32_t bs;            // tokens per block (paged side)
   int32_t linear;        // 1: staging layout [l-l0][kv][t-a][row] of one chunk
-  FastDiv fbs;           // division by bs
 };
 
 struct Plan {
@@ -76,8 +48,7 @@ struct Plan {
   int32_t piece;            // bytes per piece (multiple of 16)
   int32_t nchunks;
   int64_t items_per_chunk;  // lm * 2 * R * P
-  int64_t n_items;          // nchunks * items_per_chunk  (< 2^31: item math is 32-bit)
-  FastDiv f_ipc, f_P, f_R, f_g;  // division by items_per_chunk, P, R, g
+  int64_t n_items;          // nchunks * items_per_chunk
   // The migration's own chunking (a launch may cover a sub-range of it,
   // e.g. one staging sub-chunk): flags and counters are per migration chunk.
   int64_t mig_t0, mig_t1;   // the whole migration's token range
@@ -107,11 +78,7 @@ struct Item {
 __device__ __forceinline__ int64_t side_row(const Side& s, const Plan& p, int l, int kv, int64_t t,
                                             int64_t a, int64_t clen, bool& bad) {
   if (s.linear) return (((int64_t)(l - p.l0) * 2 + kv) * clen + (t - a)) * p.row;
-#ifndef DYNA_NO_FASTDIV
-  const int64_t jb = s.fbs.div((uint32_t)t);  // token indices are < 2^31
-#else
   const int64_t jb = t / s.bs;
-#endif
   const int32_t b = __ldg(s.table + jb);
   if (b < 0 || (int64_t)b >= s.nb) { bad = true; return 0; }
   return ((((int64_t)l * 2 + kv) * s.nb + b) * s.bs + (t - jb * s.bs)) * p.row;
@@ -119,22 +86,6 @@ __device__ __forceinline__ int64_t side_row(const Side& s, const Plan& p, int l,
 
 __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   Item it{nullptr, nullptr, 0u, 0u, 0};
-#ifndef DYNA_NO_FASTDIV
-  const uint32_t it32 = (uint32_t)item;
-  const uint32_t k = p.f_ipc.div(it32);
-  uint32_t i = it32 - k * (uint32_t)p.items_per_chunk;
-  uint32_t q = p.f_P.div(i);
-  const int32_t pp = (int32_t)(i - q * (uint32_t)p.P);
-  i = q;
-  q = p.f_R.div(i);
-  const int32_t j = (int32_t)(i - q * (uint32_t)p.R);
-  i = q;
-  const int kv = (int)(i & 1);
-  const int l = p.l0 + (int)(i >> 1);
-  const int64_t a = p.t0 + (int64_t)k * p.c;
-  const int64_t b = min(a + (int64_t)p.c, p.t1);
-  const int64_t G = (int64_t)p.f_g.div((uint32_t)a) + j;
-#else
   const int64_t k = item / p.items_per_chunk;
   int64_t i = item - k * p.items_per_chunk;
   const int32_t pp = (int32_t)(i % p.P); i /= p.P;
@@ -144,7 +95,6 @@ __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   const int64_t a = p.t0 + k * p.c;
   const int64_t b = min(a + (int64_t)p.c, p.t1);
   const int64_t G = a / p.g + j;
-#endif
   const int64_t ta = max(a, G * p.g);
   const int64_t tb = min(b, (G + 1) * p.g);
   it.k = (int32_t)((a - p.mig_t0) / p.sig_c);
@@ -621,7 +571,9 @@ __global__ void __launch_bounds__(64) k_copy_bulk_ws(const Src src, int stages, 
       park_k = -1;
       park_acc = 0;
     };
-    int64_t pending_release = -1;  // slot index whose store was issued last (released one store later)
+    // a slot goes back to the loader `lag` stores after its own store was issued, so up
+    // to lag+1 stores drain at once (measured on the single-thread engine: lag 2 >> lag 1)
+    const int lag = stages >= 4 ? 2 : 1;
     for (int64_t iter = 0;; ++iter) {
       const int s = (int)(iter % stages);
       mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
@@ -641,11 +593,10 @@ __global__ void __launch_bounds__(64) k_copy_bulk_ws(const Src src, int stages, 
         cur_acc += n;
         if (park_acc && ++since_park == kDefer) flush_park(false);
       }
-      if (pending_release >= 0) {  // the previous store has read its slot out: hand it back
-        bulk_wait_read<1>();
-        mbar_arrive(&empty[(int)(pending_release % stages)]);
+      if (iter >= lag) {  // store iter-lag has read its slot out: hand it back
+        if (lag == 2) bulk_wait_read<2>(); else bulk_wait_read<1>();
+        mbar_arrive(&empty[(int)((iter - lag) % stages)]);
       }
-      pending_release = iter;
     }
     bulk_wait_all<0>();
     if (SIGNAL) {
