@@ -957,6 +957,13 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int64_t c = chunk_tokens;
   const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
   Choice ch = choose(o, row, peer_dst, ntok);
+  if (signal && !o.engine && ch.engine != DYNA_ENGINE_VEC) {
+    // measured (bench.py e2e, per-chunk flags on): the VEC engine's per-warp fences beat
+    // draining bulk-store groups before each chunk's count (2720 vs 2540 GB/s)
+    ch.engine = DYNA_ENGINE_VEC;
+    ch.unroll = kVecU;
+    if (!o.piece_bytes) ch.piece = kVecPiece;
+  }
   if (board) {  // producer-coupled: the VEC engine (each warp waits on its own chunk's mark)
     ch.variant = DYNA_VARIANT_FUSED;
     ch.engine = DYNA_ENGINE_VEC;
