@@ -164,12 +164,18 @@ def run_dyna(args, rank, world, local_rank):
     import paper_2504_09285_b200 as dk
     from paper_2504_09285_b200 import dist as dd
 
-    torch.cuda.set_device(local_rank)
-    dev = local_rank
+    # DYNA_BENCH_SAME_DEVICE=1 + DYNA_BENCH_BACKEND=gloo: every rank on cuda:0 (functional
+    # check of the N > 1 path — IPC pools, pairing, timing — on a one-GPU box; not a measurement)
+    dev = 0 if os.environ.get("DYNA_BENCH_SAME_DEVICE") == "1" else local_rank
+    torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        backend = os.environ.get("DYNA_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
+        else:
+            dist.init_process_group(backend)
 
     g = kvgen.LLAMA2_7B
     payload = S_SPLIT * 2 * g.num_layers * g.row_bytes  # bytes per step (one request's [0, s) KV)
@@ -208,7 +214,8 @@ def run_dyna(args, rank, world, local_rank):
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        return dd.max_over_ranks(x, device=f"cuda:{dev}")
+        on_cpu = dist is not None and dist.get_backend() == "gloo"
+        return dd.max_over_ranks(x, device="cpu" if on_cpu else f"cuda:{dev}")
 
     probe = step(0)
     plan = dk.dyna_kv_xfer_plan(probe)

@@ -12,6 +12,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -184,8 +185,6 @@ void put_event(int dev, cudaEvent_t ev) {
 
 constexpr size_t kInboxBytes = sizeof(unsigned long long) * DYNA_MAX_INSTANCES * DYNA_MAX_CHUNKS;
 
-int64_t row_bytes_of(const dyna_kv_pool* p) { return p->row; }
-
 bool desc_valid(const dyna_kv_pool_desc* d) {
   return d && d->num_layers > 0 && d->num_kv_heads > 0 && d->head_dim > 0 && d->elem_bytes > 0 &&
          d->block_size > 0 && d->num_blocks > 0 && d->device >= 0 && d->instance >= 0 &&
@@ -230,6 +229,33 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   return p;
 }
 
+// Programmatic dependent launch for the copy kernels (DYNA_KV_PDL=1 in the
+// environment): consecutive migrations on a stream overlap launch + prologue
+// with the previous kernel's drain.  Correct either way (see pdl_enter()).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYNA_KV_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kernel(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                          Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 template <int U, bool SIG, class Src>
 int vec_occupancy() {
   static std::map<int, int> cache;  // per device
@@ -271,7 +297,7 @@ void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cuda
   if (max_grid > 0) max_ctas = std::min<int64_t>(max_ctas, max_grid);
   const int64_t warps = balanced_workers(n_items, max_ctas * wpc);
   const int64_t grid = (warps + wpc - 1) / wpc;
-  k_copy_vec<U, SIG, Src><<<(unsigned)grid, kVecThreads, 0, st>>>(src, sched);
+  launch_kernel(k_copy_vec<U, SIG, Src, false>, (unsigned)grid, kVecThreads, 0, st, src, sched);
 }
 
 template <bool SIG, class Src>
@@ -286,7 +312,7 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
   if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
   int64_t cap = (int64_t)sms * occ;
   if (max_grid > 0) cap = std::min<int64_t>(cap, max_grid);
-  kern<<<(unsigned)balanced_workers(n_items, cap), threads, smem, st>>>(src, stages, sched);
+  CUDA_TRY(launch_kernel(kern, (unsigned)balanced_workers(n_items, cap), threads, smem, st, src, stages, sched));
   return DYNA_OK;
 }
 

@@ -201,6 +201,17 @@ __device__ __forceinline__ void account_chunk(const Plan& p, int32_t k, uint32_t
   }
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Launched with programmatic stream serialization, a copy kernel may start
+// while the previous kernel on the stream drains.  It lets its own dependents
+// start launching at once, then waits for the previous grid to complete (and
+// its memory to be visible) before touching any global memory.  Without the
+// launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ work distribution
 // Static round-robin (ctr == nullptr) or dynamic: workers grab the next item
 // index from a per-launch counter ctr[0], prefetched one grab ahead so the
@@ -291,6 +302,7 @@ __device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __
 
 template <int U, bool SIGNAL, class Src, bool READY = false>
 __global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : 3) k_copy_vec(const Src src, unsigned long long* sched_ctr) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -396,6 +408,7 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, uns
   for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  pdl_enter();
 
   // Static round-robin only: this single thread's loop is latency-critical and
   // measured ~12% slower with the dynamic-scheduling path compiled in.
@@ -510,6 +523,7 @@ __global__ void __launch_bounds__(64) k_copy_bulk_ws(const Src src, int stages, 
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  pdl_enter();
   if (warp == 1 && lane != 0) return;  // the storer is one thread; the loader is a whole warp
   const Plan& p = src.locate_signal();
   const int64_t n_items = src.total();

@@ -44,8 +44,15 @@ def main():
     ap.add_argument("--num-blocks", type=int, default=6144)
     a = ap.parse_args()
     rank, world, lr = (int(os.environ.get(k, d)) for k, d in (("RANK", 0), ("WORLD_SIZE", 1), ("LOCAL_RANK", 0)))
+    # DYNA_BENCH_SAME_DEVICE=1 + DYNA_BENCH_BACKEND=gloo: functional check with every rank on cuda:0
+    if os.environ.get("DYNA_BENCH_SAME_DEVICE") == "1":
+        lr = 0
     torch.cuda.set_device(lr)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{lr}"))
+    if os.environ.get("DYNA_BENCH_BACKEND", "nccl") == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{lr}"))
+    else:
+        dist.init_process_group(os.environ["DYNA_BENCH_BACKEND"])
+    red_dev = "cpu" if dist.get_backend() == "gloo" else f"cuda:{lr}"
     g = kvgen.QWEN2_72B.with_(num_blocks=a.num_blocks)
     stream = torch.cuda.Stream()
     cs = stream.cuda_stream
@@ -83,8 +90,8 @@ def main():
         dk.dyna_kv_wait(x)
     torch.cuda.synchronize()
     dist.barrier()
-    ms = dd.max_over_ranks(e0.elapsed_time(e1) / a.steps, device=f"cuda:{lr}")
-    total = torch.tensor([my_bytes], dtype=torch.float64, device=f"cuda:{lr}")
+    ms = dd.max_over_ranks(e0.elapsed_time(e1) / a.steps, device=red_dev)
+    total = torch.tensor([my_bytes], dtype=torch.float64, device=red_dev)
     dist.all_reduce(total)
     bad = 0
     if a.check:
@@ -98,7 +105,7 @@ def main():
                 want = kvgen.bytes_at(3000 + m.src_rank, off, g.row_bytes)
                 got = S[l, kv, db, t % g.block_size].cpu().numpy()
                 bad += int(not np.array_equal(want, got))
-        b = torch.tensor([bad], device=f"cuda:{lr}")
+        b = torch.tensor([bad], device=red_dev)
         dist.all_reduce(b)
         bad = int(b.item())
     if rank == 0:
