@@ -119,6 +119,9 @@ def select(rows):
             win = chunks[max(0, i - 1): i + 2]
             score = {k: sum(math.log(perf[(w, k)]) for w in win) / len(win) for k in cands}
             best = max(cands, key=lambda k: (score[k], perf[(c, k)]))
+            # sticky: keep the previous bucket's choice while it is within 1% (fewer, stabler entries)
+            if seq and score[seq[-1][1]] >= score[best] + math.log(0.99):
+                best = seq[-1][1]
             seq.append((c, best, perf[(c, best)]))
             chosen.append({"row_bytes": row, "chunk": c, "choice": best, "GBps": perf[(c, best)],
                            "best_single": max(perf[(c, k)] for k in cands)})
