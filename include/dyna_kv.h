@@ -218,7 +218,11 @@ DYNA_API dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_
  * device (cudaDeviceSynchronize, cudaMalloc/cudaFree that sync, synchronous
  * copies on the legacy stream) before the last chunk is marked deadlocks: the
  * device waits for the migration, the migration for a mark that is never
- * issued.  Each chunk wait therefore gives up after the board's timeout
+ * issued.  The same holds for the FIRST launch of any kernel in the process
+ * while the migration waits: CUDA loads kernels lazily and a module load
+ * synchronises the context.  This library preloads all of its own kernels;
+ * run the producer's kernels once before the first coupled migration (or set
+ * CUDA_MODULE_LOADING=EAGER).  Each chunk wait therefore gives up after the board's timeout
  * (default 10 s; dyna_kv_ready_set_timeout) and dyna_kv_wait then returns
  * DYNA_ETIMEDOUT (the rows of late chunks are then unspecified). */
 typedef struct dyna_kv_ready* dyna_kv_ready_t;

@@ -103,11 +103,35 @@ constexpr int kBulkStages = 6;
 constexpr int64_t kStageSlotBytes = 64ll << 20;  // staged variant: bytes per staging slot
 constexpr uint32_t kSchedSlots = 1u << 15;       // dynamic-scheduling counter slots per device
 
+// CUDA loads kernels lazily by default, and loading one synchronises the
+// context.  A producer-coupled migration is resident and waiting while the
+// producer marks chunks; a first-ever launch of any kernel during that window
+// would deadlock against it.  So every kernel of this library is loaded when a
+// device is first used.
+void preload_kernels() {
+  cudaFuncAttributes a{};
+  const void* ks[] = {
+      (const void*)k_mark_ready, (const void*)k_wait_flag, (const void*)k_fill,
+      (const void*)k_copy_vec<4, false, SingleSource, false>, (const void*)k_copy_vec<4, true, SingleSource, false>,
+      (const void*)k_copy_vec<8, false, SingleSource, false>, (const void*)k_copy_vec<8, true, SingleSource, false>,
+      (const void*)k_copy_vec<16, false, SingleSource, false>, (const void*)k_copy_vec<16, true, SingleSource, false>,
+      (const void*)k_copy_vec<8, false, SingleSource, true>, (const void*)k_copy_vec<8, true, SingleSource, true>,
+      (const void*)k_copy_vec<4, false, BatchSource, false>, (const void*)k_copy_vec<8, false, BatchSource, false>,
+      (const void*)k_copy_vec<16, false, BatchSource, false>,
+      (const void*)k_copy_bulk<false, SingleSource>, (const void*)k_copy_bulk<true, SingleSource>,
+      (const void*)k_copy_bulk<false, BatchSource>,
+      (const void*)k_copy_bulk_ws<false, SingleSource>, (const void*)k_copy_bulk_ws<true, SingleSource>,
+      (const void*)k_copy_bulk_ws<false, BatchSource>,
+  };
+  for (const void* k : ks) cudaFuncGetAttributes(&a, k);
+}
+
 DevInfo* dev_info(int dev) {
   std::lock_guard<std::mutex> lk(g_mu);
   DevInfo& d = g_dev[dev];
   if (d.sms == 0) {
     DeviceGuard g(dev);
+    preload_kernels();
     cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
     if (d.sms <= 0) d.sms = 1;
     if (cudaMalloc(&d.sched, sizeof(unsigned long long) * 2 * kSchedSlots) != cudaSuccess ||
@@ -229,13 +253,13 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   return p;
 }
 
-// Programmatic dependent launch for the copy kernels (DYNA_KV_PDL=1 in the
-// environment): consecutive migrations on a stream overlap launch + prologue
-// with the previous kernel's drain.  Correct either way (see pdl_enter()).
-bool pdl_enabled() {
+// Programmatic dependent launch for the copy kernels (DYNA_KV_PDL=0 in the
+// environment turns it off): consecutive migrations on a stream overlap launch
+// + prologue with the previous kernel's drain.  Correct either way (see pdl_enter()).
+bool pdl_enabled() {  // default on (measured: +5-16% on small calls, +0.3% on 512 MiB calls)
   static const bool on = [] {
     const char* e = std::getenv("DYNA_KV_PDL");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }

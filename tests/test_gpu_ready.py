@@ -106,3 +106,41 @@ def test_missing_mark_times_out_instead_of_hanging():
         assert e.value.status == dk.DYNA_ETIMEDOUT
     finally:
         dk.dyna_kv_ready_destroy(board)
+
+
+_FRESH = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import kvgen, paper_2504_09285_b200 as dk
+torch.cuda.set_device(0)
+g = kvgen.TOY.with_(num_blocks=256)
+src, dst = dk.Pool(g, 0), dk.Pool(g, 0)          # first device use: the library preloads its kernels
+ts, td = kvgen.table_pair(1, 1024, g, g)
+st = dk.table(src, torch.from_numpy(ts).cuda(), ts)
+dt = dk.table(dst, torch.from_numpy(td).cuda(), td)
+board = dk.dyna_kv_ready_create(0, 16)
+dk.dyna_kv_ready_set_timeout(board, 5_000_000_000)
+prod, mig = torch.cuda.Stream(), torch.cuda.Stream()
+with torch.cuda.stream(prod):
+    torch.cuda._sleep(1000)                        # warm the producer's own kernel only
+torch.cuda.synchronize()
+epoch = dk.dyna_kv_ready_begin(board)
+x = dk.dyna_kv_migrate_on_ready(st, dt, (0, 1000), (0, 2), 100, board, epoch, mig.cuda_stream, dk.opts(max_ctas=4))
+for k in range(10):                                # first-ever k_mark_ready launches happen now
+    with torch.cuda.stream(prod):
+        torch.cuda._sleep(100000)
+    dk.dyna_kv_ready_mark(board, k, epoch, prod.cuda_stream)
+dk.dyna_kv_wait(x)
+print("ok")
+"""
+
+
+def test_first_mark_during_wait_does_not_deadlock():
+    """Regression: CUDA's lazy module loading synchronises the context; a first-ever launch of the
+    mark kernel while the coupled migration waits used to deadlock (until the device timeout)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _FRESH.format(root=root)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
