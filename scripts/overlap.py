@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--budgets", default="0,74,32,16")
     ap.add_argument("--n-gemm", type=int, default=N_GEMM)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--ready-ctas", type=int, default=8, help="CTA budget of the coupled launch when budget is 0")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "overlap.json"))
     args = ap.parse_args()
     torch.cuda.set_device(0)
@@ -84,7 +85,7 @@ def main():
         if mode == "ready":   # one launch for the whole range; waits on the device for each chunk's mark
             epoch = dk.dyna_kv_ready_begin(board)
             handles.append(dk.dyna_kv_migrate_on_ready(st, dt, (0, s), (0, 32), c, board, epoch, mig.cuda_stream,
-                                                       dk.opts(max_ctas=budget or 32)))
+                                                       dk.opts(max_ctas=budget or args.ready_ctas)))
         for k in range(nck):
             with torch.cuda.stream(prod):
                 producer_chunk(X)
@@ -139,7 +140,7 @@ def main():
                  "producer_slowdown": prod_c / prod_alone - 1,
                  "exposed_whole_ms": exp_w, "exposed_chunked_ms": exp_c,
                  "reduction": 1 - exp_c / exp_w if exp_w > 0 else None,
-                 "ready_coupled": {"ctas": budget or 32, "exposed_ms": exp_r, "T_prod_ms": prod_r,
+                 "ready_coupled": {"ctas": budget or args.ready_ctas, "exposed_ms": exp_r, "T_prod_ms": prod_r,
                                    "producer_slowdown": prod_r / prod_alone - 1,
                                    "reduction": 1 - exp_r / exp_w if exp_w > 0 else None}}
             print(json.dumps(r), flush=True)

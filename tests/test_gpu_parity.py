@@ -298,3 +298,19 @@ def test_auto_uses_calibration_table():
     finally:
         dk.dyna_kv_calib_set([])
     assert dk.dyna_kv_calib_get() == base
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_round_trip_identity_on_gpu(engine):
+    """north_star invariant: migrate A->B then B->A is the identity (A's range rows poisoned in between);
+    reblocking 16 -> 32 -> 16 on the way."""
+    gA, gB = LLAMA3_ROWS, LLAMA3_ROWS.with_(block_size=32, num_blocks=250)
+    hA = kvgen.fill_bytes(81, gA.pool_bytes)
+    A, B = pool_from_host(gA, hA), pool_filled(gB, 82)
+    ta, tb = kvgen.table_pair(83, 5000, gA, gB)
+    s = 4321
+    migrate_and_wait(A, ta, B, tb, (0, s), (0, 4), 512, engine=engine)
+    m = mapped_mask(gA, [(ta, (0, s))])
+    A.tensor.view(gA.num_layers, 2, gA.num_blocks, gA.block_size, gA.row_bytes)[m] = 0xA5   # poison
+    migrate_and_wait(B, tb, A, ta, (0, s), (0, 4), 512, engine=engine)
+    assert np.array_equal(A.tensor.cpu().numpy(), hA)
