@@ -248,6 +248,25 @@ struct Sched {
   }
 };
 
+// Same as account_chunk, for a thread whose counted writes are already complete
+// and proxy-fenced: the count itself is a release RMW at the destination's scope,
+// instead of a full fence followed by a relaxed add.
+__device__ __forceinline__ void account_chunk_release(const Plan& p, int32_t k, uint32_t n) {
+  if (n == 0) return;
+  unsigned long long* ctr = p.counters + k;
+  const unsigned long long total = chunk_bytes(p, k);
+  unsigned long long old;
+  if (p.sys_fence)
+    asm volatile("atom.add.release.sys.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(ctr), "l"((unsigned long long)n) : "memory");
+  else
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(ctr), "l"((unsigned long long)n) : "memory");
+  if (old + n == total) {
+    __threadfence_system();  // acquire the other contributors' releases before publishing
+    *ctr = 0ull;
+    st_release_sys(p.flags + k, p.epoch);
+  }
+}
+
 // ------------------------------------------------------------------ VEC engine
 __device__ __forceinline__ int4 ld_nc_v4(const int4* ptr) {
   int4 r;
@@ -453,8 +472,12 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, uns
   auto flush_park = [&](bool all) {
     if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
     asm volatile("fence.proxy.async.global;" ::: "memory");
+#ifdef DYNA_BULK_FENCED_COUNT
     fence_for(p);
     account_chunk(p, park_k, park_acc);
+#else
+    account_chunk_release(p, park_k, park_acc);
+#endif
     park_k = -1;
     park_acc = 0;
   };
