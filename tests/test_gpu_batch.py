@@ -156,3 +156,40 @@ def test_cuda_graph_capture_and_replay():
     graph.replay()
     torch.cuda.synchronize()
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
+
+
+def test_chunk_stream_prefill_then_decode():
+    """ChunkStream: prefill chunks + decoded tokens (s > P) pushed chunk by chunk; bytes match the oracle."""
+    from paper_2504_09285_b200.stream import ChunkStream
+    g = Geom(3, 8, 128, 2, 16, 200)
+    hs, hd = kvgen.fill_bytes(91, g.pool_bytes), kvgen.fill_bytes(92, g.pool_bytes)
+    ts, td = kvgen.table_pair(93, 1500, g, g)
+    P, decoded = 1100, 37
+    want = hd.copy()
+    oracle.migrate(hs, g, ts, want, g, td, (0, P + decoded))
+    src, dst = pool_from_host(g, hs), pool_from_host(g, hd)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    stream = torch.cuda.current_stream().cuda_stream
+    cs = ChunkStream(256, lambda tr: dk.dyna_kv_migrate_ex(st, dt, tr, (0, 3), tr[1] - tr[0], stream, None))
+    for n in (256, 256, 256, 256, 76):        # prefill of P = 1100 in scheduler-sized steps
+        cs.produced(n)
+    for _ in range(decoded):                  # alpha decodes past the prompt
+        cs.produced(1)
+    cs.close()
+    for x in cs.handles:
+        dk.dyna_kv_wait(x)
+    assert cs.chunks[-1] == (1024, P + decoded)
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_tp_sharded_rows(engine):
+    """TP-8 shard of Qwen2-72B (1 KV head per rank: 256-B rows, 4-KiB segments) — SURVEY §8f NEXT-3."""
+    g = Geom(8, 1, 128, 2, 16, 300)
+    hs, hd = kvgen.fill_bytes(95, g.pool_bytes), kvgen.fill_bytes(96, g.pool_bytes)
+    ts, td = kvgen.table_pair(97, 4000, g, g)
+    want = hd.copy()
+    oracle.migrate(hs, g, ts, want, g, td, (5, 3999))
+    src, dst = pool_from_host(g, hs), pool_from_host(g, hd)
+    dk.dyna_kv_wait(dk.migrate(dev_table(src, ts), dev_table(dst, td), (5, 3999), (0, 8), 1024, engine=engine))
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
