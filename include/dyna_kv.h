@@ -240,6 +240,47 @@ DYNA_API dyna_status dyna_kv_migrate_on_ready(dyna_block_table src, dyna_block_t
                                               struct CUstream_st* stream, const dyna_kv_opts* opts,
                                               dyna_kv_xfer_t* out);
 
+/* Receiver-steered placement across processes (the STAGED shape, SURVEY §8a
+ * a2-a4; §4.3: "messages steering placement on the receiver
+ * side").  The RECEIVER owns a channel: a ring of staging slots plus one
+ * "full" and one "credit" sequence word per slot, in its own device memory.
+ * It exports the channel; the SENDER imports it and pushes: for every
+ * sub-chunk (chunks cut to fit one slot) a kernel gathers the source rows
+ * straight into the receiver's slot over NVLink and releases the slot's full
+ * word (system scope), after waiting for the slot's credit.  The receiver
+ * places: it waits for the full word, scatters the slot through ITS OWN block
+ * table, optionally raises its per-chunk inbox flags, and returns the credit.
+ * The sender never sees the destination table.  Both sides must describe the
+ * same migration (token range, layer range, chunk_tokens) in the same order;
+ * each channel carries one sender's pushes to one destination pool. */
+typedef struct dyna_kv_channel* dyna_kv_channel_t;
+typedef struct {
+    uint8_t mem[64];         /* cudaIpcMemHandle_t of the channel allocation */
+    uint64_t slot_bytes;
+    int32_t slots;
+    int32_t sender;          /* sender instance id (inbox row for the chunk flags) */
+    dyna_kv_pool_desc desc;  /* the receiver pool's geometry */
+} dyna_kv_channel_handle;
+
+/* Receiver: a channel into `dst` for sender `sender` (slots >= 2, slot_bytes a
+ * multiple of 16 holding at least one token of the migrations to come). */
+DYNA_API dyna_status dyna_kv_channel_create(dyna_kv_pool_t dst, int32_t sender, int32_t slots, uint64_t slot_bytes,
+                                            dyna_kv_channel_t* out);
+DYNA_API dyna_status dyna_kv_channel_export(dyna_kv_channel_t ch, dyna_kv_channel_handle* out);
+/* Sender: map a receiver's channel into `local_device`. */
+DYNA_API dyna_status dyna_kv_channel_import(const dyna_kv_channel_handle* h, int32_t local_device,
+                                            dyna_kv_channel_t* out);
+DYNA_API dyna_status dyna_kv_channel_destroy(dyna_kv_channel_t ch);
+/* Sender: push tokens x layers of `src` into the channel, chunk by chunk, on `stream` (source device). */
+DYNA_API dyna_status dyna_kv_push(dyna_block_table src, dyna_range token_range, dyna_range layer_range,
+                                  int32_t chunk_tokens, dyna_kv_channel_t ch, struct CUstream_st* stream,
+                                  dyna_kv_xfer_t* out);
+/* Receiver: place the pushed rows through `dst` (a table of the channel's pool) on `stream`
+ * (receiver device).  opts->flags may request per-chunk inbox flags (sender = the channel's). */
+DYNA_API dyna_status dyna_kv_place(dyna_kv_channel_t ch, dyna_block_table dst, dyna_range token_range,
+                                   dyna_range layer_range, int32_t chunk_tokens, struct CUstream_st* stream,
+                                   const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
+
 /* CUDA graphs: dyna_kv_migrate / _ex with DEVICE block tables may be captured
  * into a CUDA graph (stream capture) and replayed; release each handle with
  * dyna_kv_wait after the capture ends (it returns at once — the captured work

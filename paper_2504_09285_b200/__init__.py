@@ -39,6 +39,8 @@ EXPORTS = (
     "dyna_kv_copy_flags", "dyna_kv_calib_set", "dyna_kv_calib_get", "dyna_kv_migrate_batch",
     "dyna_kv_xfer_plan", "dyna_kv_ready_create", "dyna_kv_ready_destroy", "dyna_kv_ready_begin",
     "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready", "dyna_kv_ready_set_timeout",
+    "dyna_kv_channel_create", "dyna_kv_channel_export", "dyna_kv_channel_import", "dyna_kv_channel_destroy",
+    "dyna_kv_push", "dyna_kv_place",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -76,6 +78,11 @@ class dyna_kv_ipc_handle(ctypes.Structure):
                 ("pool_offset", ctypes.c_uint64), ("desc", dyna_kv_pool_desc)]
 
 
+class dyna_kv_channel_handle(ctypes.Structure):
+    _fields_ = [("mem", ctypes.c_uint8 * 64), ("slot_bytes", ctypes.c_uint64), ("slots", ctypes.c_int32),
+                ("sender", ctypes.c_int32), ("desc", dyna_kv_pool_desc)]
+
+
 class DynaKVError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
@@ -105,6 +112,13 @@ def _load():
         "dyna_kv_ready_mark": (st, [vp, ctypes.c_int32, ctypes.c_uint64, vp]),
         "dyna_kv_migrate_on_ready": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
                                           vp, ctypes.c_uint64, vp, p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_channel_create": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, p(vp)]),
+        "dyna_kv_channel_export": (st, [vp, p(dyna_kv_channel_handle)]),
+        "dyna_kv_channel_import": (st, [p(dyna_kv_channel_handle), ctypes.c_int32, p(vp)]),
+        "dyna_kv_channel_destroy": (st, [vp]),
+        "dyna_kv_push": (st, [dyna_block_table, dyna_range, dyna_range, ctypes.c_int32, vp, vp, p(vp)]),
+        "dyna_kv_place": (st, [vp, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32, vp, p(dyna_kv_opts),
+                               p(vp)]),
         "dyna_kv_wait": (st, [vp]),
         "dyna_kv_query": (st, [vp]),
         "dyna_kv_stream_wait": (st, [vp, vp]),
@@ -213,6 +227,45 @@ def dyna_kv_migrate_on_ready(src: dyna_block_table, dst: dyna_block_table, token
     _check(lib.dyna_kv_migrate_on_ready(src, dst, dyna_range(*token_range), dyna_range(*layer_range), chunk_tokens,
                                         ctypes.c_void_p(board), epoch, ctypes.c_void_p(stream),
                                         ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_channel_create(dst_pool: int, sender: int, slots: int, slot_bytes: int) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_channel_create(ctypes.c_void_p(dst_pool), sender, slots, slot_bytes, ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_channel_export(ch: int) -> bytes:
+    h = dyna_kv_channel_handle()
+    _check(lib.dyna_kv_channel_export(ctypes.c_void_p(ch), ctypes.byref(h)))
+    return bytes(h)
+
+
+def dyna_kv_channel_import(handle: bytes, local_device: int) -> int:
+    h = dyna_kv_channel_handle.from_buffer_copy(handle)
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_channel_import(ctypes.byref(h), local_device, ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_channel_destroy(ch: int) -> None:
+    _check(lib.dyna_kv_channel_destroy(ctypes.c_void_p(ch)))
+
+
+def dyna_kv_push(src: dyna_block_table, token_range, layer_range, chunk_tokens: int, ch: int, stream: int = 0) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_push(src, dyna_range(*token_range), dyna_range(*layer_range), chunk_tokens,
+                            ctypes.c_void_p(ch), ctypes.c_void_p(stream), ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_place(ch: int, dst: dyna_block_table, token_range, layer_range, chunk_tokens: int, stream: int = 0,
+                  opts: dyna_kv_opts | None = None) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_place(ctypes.c_void_p(ch), dst, dyna_range(*token_range), dyna_range(*layer_range),
+                             chunk_tokens, ctypes.c_void_p(stream), ctypes.byref(opts) if opts is not None else None,
+                             ctypes.byref(out)))
     return out.value
 
 

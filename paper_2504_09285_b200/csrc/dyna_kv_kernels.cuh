@@ -670,6 +670,13 @@ __global__ void k_mark_ready(unsigned long long* slot, unsigned long long epoch)
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(slot), "l"(epoch) : "memory");
 }
 
+// Credit return of a placement channel: the slot may be overwritten once this
+// runs (stream-ordered after the scatter that read it); system scope, the
+// sender polls it from another GPU.
+__global__ void k_release_sys(unsigned long long* slot, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(v) : "memory");
+}
+
 // ------------------------------------------------------------------ test-input generator (not the method)
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long z) {
   z += 0x9E3779B97F4A7C15ull;

@@ -60,6 +60,7 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(dk.dyna_kv_opts) == 32
     assert ctypes.sizeof(dk.dyna_kv_calib_entry) == 32
     assert ctypes.sizeof(dk.dyna_kv_migration) == 32 + 32 + 16
+    assert ctypes.sizeof(dk.dyna_kv_channel_handle) == 64 + 8 + 4 + 4 + 32
     assert ctypes.sizeof(dk.dyna_kv_ipc_handle) == 64 + 64 + 8 + 32
 
 

@@ -1,0 +1,104 @@
+"""Receiver-steered placement through a channel (push on the sender, place on the
+receiver with its own block table) — bit-exact vs the oracle, in one process
+(two streams, loopback) and across two processes (CUDA IPC)."""
+import multiprocessing as mp
+
+import numpy as np
+import pytest
+import torch
+
+import kvgen
+import oracle
+import paper_2504_09285_b200 as dk
+from kvgen import Geom
+from gpu_util import dev_table, pool_from_host
+
+pytestmark = pytest.mark.gpu
+G = Geom(4, 8, 128, 2, 16, 400)     # 2 KiB rows
+
+
+@pytest.mark.parametrize("slots,slot_bytes,c", [(2, 4 * 2 * 4 * 2048 * 16, 100), (3, 1 << 20, 256), (4, 1 << 22, 1000)])
+@pytest.mark.parametrize("signal", [False, True])
+def test_push_place_loopback(slots, slot_bytes, c, signal):
+    ts, td = kvgen.table_pair(7, 5000, G, G)
+    hs, hd = kvgen.fill_bytes(1, G.pool_bytes), kvgen.fill_bytes(2, G.pool_bytes)
+    tr = (13, 4321)
+    want = hd.copy()
+    oracle.migrate(hs, G, ts, want, G, td, tr)
+    src, dst = pool_from_host(G, hs), pool_from_host(G, hd)
+    ch = dk.dyna_kv_channel_create(dst.handle, 9, slots, slot_bytes)
+    try:
+        s_push, s_place = torch.cuda.Stream(), torch.cuda.Stream()
+        for rep in range(2):   # the channel's sequence numbers carry over between migrations
+            xp = dk.dyna_kv_push(dev_table(src, ts), tr, (0, 4), c, ch, s_push.cuda_stream)
+            xq = dk.dyna_kv_place(ch, dev_table(dst, td), tr, (0, 4), c, s_place.cuda_stream,
+                                  dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0))
+            epoch, nchunks, sender = dk.dyna_kv_xfer_info(xq)
+            dk.dyna_kv_wait(xp)
+            dk.dyna_kv_wait(xq)
+            assert np.array_equal(dst.tensor.cpu().numpy(), want)
+            if signal:
+                flags = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
+                dk.dyna_kv_copy_flags(dst.handle, sender, 0, nchunks, flags.data_ptr(), 0)
+                torch.cuda.synchronize()
+                assert sender == 9 and (flags.numpy() == epoch).all()
+            dst.tensor.copy_(torch.from_numpy(hd).cuda())
+    finally:
+        dk.dyna_kv_channel_destroy(ch)
+
+
+def test_channel_errors():
+    src, dst = pool_from_host(G, kvgen.fill_bytes(1, G.pool_bytes)), pool_from_host(G, kvgen.fill_bytes(2, G.pool_bytes))
+    ts, td = kvgen.table_pair(7, 5000, G, G)
+    with pytest.raises(dk.DynaKVError):
+        dk.dyna_kv_channel_create(dst.handle, 0, 1, 1 << 20)          # slots >= 2
+    ch = dk.dyna_kv_channel_create(dst.handle, 0, 2, 4096)          # 4 KiB slots: < one token of 4 layers
+    try:
+        with pytest.raises(dk.DynaKVError) as e:
+            dk.dyna_kv_push(dev_table(src, ts), (0, 10), (0, 4), 4, ch)
+        assert e.value.status == dk.DYNA_EINVAL
+        other = pool_from_host(G, kvgen.fill_bytes(3, G.pool_bytes))
+        with pytest.raises(dk.DynaKVError):
+            dk.dyna_kv_place(ch, dev_table(other, td), (0, 10), (0, 1), 4)   # not the channel's pool
+    finally:
+        dk.dyna_kv_channel_destroy(ch)
+
+
+def _sender(handle, q):
+    try:
+        import torch
+        import kvgen
+        import paper_2504_09285_b200 as dk
+        from gpu_util import dev_table, pool_from_host
+        torch.cuda.set_device(0)
+        src = pool_from_host(G, kvgen.fill_bytes(1, G.pool_bytes), instance=3)
+        ts, _ = kvgen.table_pair(7, 5000, G, G)
+        ch = dk.dyna_kv_channel_import(handle, 0)
+        q.put("ready")
+        x = dk.dyna_kv_push(dev_table(src, ts), (0, 3000), (0, 4), 512, ch, torch.cuda.current_stream().cuda_stream)
+        dk.dyna_kv_wait(x)
+        dk.dyna_kv_channel_destroy(ch)
+        q.put("ok")
+    except Exception as e:  # surface to the parent
+        q.put(repr(e))
+
+
+def test_push_place_across_processes():
+    ts, td = kvgen.table_pair(7, 5000, G, G)
+    hs, hd = kvgen.fill_bytes(1, G.pool_bytes), kvgen.fill_bytes(2, G.pool_bytes)
+    want = hd.copy()
+    oracle.migrate(hs, G, ts, want, G, td, (0, 3000))
+    dst = pool_from_host(G, hd)
+    ch = dk.dyna_kv_channel_create(dst.handle, 3, 8, 1 << 23)   # 8 x 8 MiB: the sender never waits for credit
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_sender, args=(dk.dyna_kv_channel_export(ch), q))
+    p.start()
+    assert q.get(timeout=300) == "ready"
+    # place concurrently: the receiver's kernels wait on the device for each slot's full word
+    x = dk.dyna_kv_place(ch, dev_table(dst, td), (0, 3000), (0, 4), 512)
+    assert q.get(timeout=300) == "ok"
+    p.join(timeout=60)
+    dk.dyna_kv_wait(x)
+    dk.dyna_kv_channel_destroy(ch)
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
