@@ -200,7 +200,7 @@ def run_dyna(args, rank, world, local_rank):
     tabs = kvgen.batch_tables(500 + rank, [N_TOKENS] * N_SETS, g, g)
     dts = [(torch.from_numpy(ts).to(f"cuda:{dev}"), torch.from_numpy(td).to(f"cuda:{dev}")) for ts, td in tabs]
     tables = [(dk.table(src, a, ts), dk.table(dst, b, td)) for (a, b), (ts, td) in zip(dts, tabs)]
-    mopts = dk.opts(variant=args.variant, engine=args.engine)
+    mopts = dk.opts(variant=args.variant, engine=args.engine, piece_bytes=args.piece, unroll=args.unroll)
     torch.cuda.synchronize()
 
     def step(i, o=mopts):
@@ -264,7 +264,8 @@ def run_dyna(args, rank, world, local_rank):
     nchunks = -(-S_SPLIT // CHUNK)
     e2e_tables = [(dk.table(src, None, ts), dk.table(dst, None, td)) for ts, td in tabs]
     flags_host = [torch.zeros(nchunks, dtype=torch.int64).pin_memory() for _ in range(N_SETS)]
-    sig_opts = dk.opts(variant=args.variant, engine=args.engine, flags=dk.DYNA_MIGRATE_SIGNAL)
+    sig_opts = dk.opts(variant=args.variant, engine=args.engine, flags=dk.DYNA_MIGRATE_SIGNAL,
+                       piece_bytes=args.piece, unroll=args.unroll)
     sender = rank
     flag_pool = dst.handle
     blocks = -(-S_SPLIT // g.block_size)
@@ -370,6 +371,8 @@ def main():
     ap.add_argument("--impl", default="dyna", choices=["dyna", "reference"])
     ap.add_argument("--engine", type=int, default=0, help="0 auto, 1 VEC, 2 BULK")
     ap.add_argument("--variant", type=int, default=0, help="0 auto, 1 FUSED, 2 STAGED")
+    ap.add_argument("--piece", type=int, default=0, help="bytes per work item (0 = calibrated)")
+    ap.add_argument("--unroll", type=int, default=0, help="VEC loads in flight per lane (0 = calibrated)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -27,7 +27,8 @@ def dev_table(pool: dk.Pool, ids, with_host: bool = True):
 
 
 def migrate_and_wait(src: dk.Pool, ts, dst: dk.Pool, td, tr, lr, c, with_host=True, **kw):
-    x = dk.migrate(dev_table(src, ts, with_host), dev_table(dst, td, with_host), tr, lr, c, **kw)
+    st, dt = dev_table(src, ts, with_host), dev_table(dst, td, with_host)  # alive until the wait
+    x = dk.migrate(st, dt, tr, lr, c, **kw)
     dk.dyna_kv_wait(x)
 
 

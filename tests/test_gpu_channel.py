@@ -29,9 +29,11 @@ def test_push_place_loopback(slots, slot_bytes, c, signal):
     ch = dk.dyna_kv_channel_create(dst.handle, 9, slots, slot_bytes)
     try:
         s_push, s_place = torch.cuda.Stream(), torch.cuda.Stream()
+        # tables must outlive the enqueued work (dyna_block_table contract): keep them in variables
+        st, dt = dev_table(src, ts), dev_table(dst, td)
         for rep in range(2):   # the channel's sequence numbers carry over between migrations
-            xp = dk.dyna_kv_push(dev_table(src, ts), tr, (0, 4), c, ch, s_push.cuda_stream)
-            xq = dk.dyna_kv_place(ch, dev_table(dst, td), tr, (0, 4), c, s_place.cuda_stream,
+            xp = dk.dyna_kv_push(st, tr, (0, 4), c, ch, s_push.cuda_stream)
+            xq = dk.dyna_kv_place(ch, dt, tr, (0, 4), c, s_place.cuda_stream,
                                   dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0))
             epoch, nchunks, sender = dk.dyna_kv_xfer_info(xq)
             dk.dyna_kv_wait(xp)
@@ -75,7 +77,8 @@ def _sender(handle, q):
         ts, _ = kvgen.table_pair(7, 5000, G, G)
         ch = dk.dyna_kv_channel_import(handle, 0)
         q.put("ready")
-        x = dk.dyna_kv_push(dev_table(src, ts), (0, 3000), (0, 4), 512, ch, torch.cuda.current_stream().cuda_stream)
+        st = dev_table(src, ts)
+        x = dk.dyna_kv_push(st, (0, 3000), (0, 4), 512, ch, torch.cuda.current_stream().cuda_stream)
         dk.dyna_kv_wait(x)
         dk.dyna_kv_channel_destroy(ch)
         q.put("ok")
@@ -96,7 +99,8 @@ def test_push_place_across_processes():
     p.start()
     assert q.get(timeout=300) == "ready"
     # place concurrently: the receiver's kernels wait on the device for each slot's full word
-    x = dk.dyna_kv_place(ch, dev_table(dst, td), (0, 3000), (0, 4), 512)
+    dt = dev_table(dst, td)
+    x = dk.dyna_kv_place(ch, dt, (0, 3000), (0, 4), 512)
     assert q.get(timeout=300) == "ok"
     p.join(timeout=60)
     dk.dyna_kv_wait(x)
