@@ -12,9 +12,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdyna_kv.so")
-SOURCES = [os.path.join(CSRC, "dyna_kv.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "dyna_kv_kernels.cuh"), os.path.join(CSRC, "calib_default.inc"),
-                  os.path.join(ROOT, "include", "dyna_kv.h")]
+SOURCES = [os.path.join(CSRC, f) for f in ("runtime.cu", "launch.cu", "migrate.cu", "coupling.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("runtime.cuh", "plan.cuh", "dyna_kv_kernels.cuh", "calib_default.inc")] \
+    + [os.path.join(ROOT, "include", "dyna_kv.h")]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

@@ -26,46 +26,9 @@
 #pragma once
 #include <cstdint>
 
+#include "plan.cuh"
+
 namespace dynakv {
-
-struct Side {
-  char* base;            // pool base, or staging base for a linear side
-  const int32_t* table;  // block table (paged side); nullptr for a linear side
-  int64_t nb;            // blocks in the pool (paged side)
-  int32_t bs;            // tokens per block (paged side)
-  int32_t linear;        // 1: staging layout [l-l0][kv][t-a][row] of one chunk
-};
-
-struct Plan {
-  Side src, dst;
-  int64_t row;              // bytes of one token's K or V in one layer (multiple of 16)
-  int64_t t0, t1;           // token range of this launch
-  int32_t l0, lm;           // first layer, number of layers
-  int32_t c;                // chunk tokens
-  int32_t g;                // run grid in tokens
-  int32_t R;                // max runs per chunk
-  int32_t P;                // pieces per run
-  int32_t piece;            // bytes per piece (multiple of 16)
-  int32_t nchunks;
-  int64_t items_per_chunk;  // lm * 2 * R * P
-  int64_t n_items;          // nchunks * items_per_chunk
-  // The migration's own chunking (a launch may cover a sub-range of it,
-  // e.g. one staging sub-chunk): flags and counters are per migration chunk.
-  int64_t mig_t0, mig_t1;   // the whole migration's token range
-  int32_t sig_c;            // the migration's chunk tokens
-  // per-chunk completion signal (counters == nullptr: none)
-  unsigned long long* counters;  // on the launching device, self-resetting
-  unsigned long long* flags;     // destination inbox row of this sender
-  unsigned long long epoch;
-  int32_t sys_fence;             // 1: destination on another GPU (fence at system scope)
-  unsigned int* err;             // deferred error word (mapped host memory)
-  // producer coupling (nullptr: none): chunk k may be read only once ready[k] >= ready_epoch
-  const unsigned long long* ready;
-  unsigned long long ready_epoch;
-  unsigned long long ready_timeout_ns;  // give up (ERR_TIMEOUT) after this long without the mark
-};
-
-enum : unsigned { ERR_BAD_BLOCK = 1u, ERR_TIMEOUT = 2u };
 
 struct Item {
   const char* src;
@@ -116,33 +79,6 @@ __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   it.n = n;
   return it;
 }
-
-// Where a kernel's items come from: one plan (by value, in the constant bank),
-// or a batch of plans in global memory with an exclusive prefix of item counts
-// (dyna_kv_migrate_batch: many requests, one launch).
-struct SingleSource {
-  Plan p;
-  __device__ __forceinline__ int64_t total() const { return p.n_items; }
-  __device__ __forceinline__ const Plan& locate(int64_t& item) const { return p; }
-  __device__ __forceinline__ const Plan& locate_signal() const { return p; }
-};
-struct BatchSource {
-  const Plan* plans;
-  const int64_t* base;  // base[r] = first global item of plan r; nondecreasing
-  int32_t n;
-  int64_t total_items;
-  __device__ __forceinline__ int64_t total() const { return total_items; }
-  __device__ __forceinline__ const Plan& locate(int64_t& item) const {
-    int lo = 0, hi = n - 1;  // the last r with base[r] <= item
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (__ldg(base + mid) <= item) lo = mid; else hi = mid - 1;
-    }
-    item -= __ldg(base + lo);
-    return plans[lo];
-  }
-  __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }
-};
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* ptr, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ptr), "l"(v) : "memory");
@@ -410,7 +346,6 @@ __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
-constexpr int kMaxStages = 16;
 
 // One thread per CTA drives a ring of `stages` smem slots of p.piece bytes:
 // loads land in slots ahead of the store front; each slot is reloaded once

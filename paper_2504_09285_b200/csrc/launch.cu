@@ -1,0 +1,342 @@
+// launch.cu — launch plans and every kernel launch of the library: the copy
+// engines (VEC, BULK, BULK_WS; balanced persistent grids, programmatic dependent
+// launch), the staged variant (K1 gather, K2 transfer, K3 scatter; SURVEY §8
+// a2-a4), producer-coupled launches, and the small flag / fill kernels.  The only
+// translation unit that includes the kernels.
+#include "dyna_kv_kernels.cuh"
+#include "runtime.cuh"
+
+using namespace dynakv;
+using namespace dynakv::rt;
+
+namespace dynakv {
+namespace rt {
+
+// CUDA loads kernels lazily by default, and loading one synchronises the
+// context.  A producer-coupled migration is resident and waiting while the
+// producer marks chunks; a first-ever launch of any kernel during that window
+// would deadlock against it.  So every kernel of this library is loaded when a
+// device is first used.
+void preload_kernels() {
+  cudaFuncAttributes a{};
+  const void* ks[] = {
+      (const void*)k_mark_ready, (const void*)k_wait_flag, (const void*)k_fill, (const void*)k_release_sys,
+      (const void*)k_copy_vec<4, false, SingleSource, false>, (const void*)k_copy_vec<4, true, SingleSource, false>,
+      (const void*)k_copy_vec<8, false, SingleSource, false>, (const void*)k_copy_vec<8, true, SingleSource, false>,
+      (const void*)k_copy_vec<16, false, SingleSource, false>, (const void*)k_copy_vec<16, true, SingleSource, false>,
+      (const void*)k_copy_vec<8, false, SingleSource, true>, (const void*)k_copy_vec<8, true, SingleSource, true>,
+      (const void*)k_copy_vec<4, false, BatchSource, false>, (const void*)k_copy_vec<8, false, BatchSource, false>,
+      (const void*)k_copy_vec<16, false, BatchSource, false>,
+      (const void*)k_copy_bulk<false, SingleSource>, (const void*)k_copy_bulk<true, SingleSource>,
+      (const void*)k_copy_bulk<false, BatchSource>,
+      (const void*)k_copy_bulk_ws<false, SingleSource>, (const void*)k_copy_bulk_ws<true, SingleSource>,
+      (const void*)k_copy_bulk_ws<false, BatchSource>,
+  };
+  for (const void* k : ks) cudaFuncGetAttributes(&a, k);
+}
+
+// Build a launch plan for tokens [t0, t1) cut into chunks of c tokens.
+// g: run grid in tokens (absolute token index; divides the paged block sizes).
+Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1, int l0, int lm, int64_t c,
+               int64_t g, int piece) {
+  Plan p{};
+  p.src = s;
+  p.dst = d;
+  p.row = row;
+  p.t0 = t0;
+  p.t1 = t1;
+  p.l0 = l0;
+  p.lm = lm;
+  p.c = (int32_t)c;
+  p.g = (int32_t)g;
+  const bool aligned = (t0 % g == 0) && (c % g == 0);
+  p.R = aligned ? (int32_t)(c / g) : (int32_t)((c - 1) / g + 2);
+  const int64_t run_max = std::min(g, c) * row;
+  p.piece = piece;
+  p.P = (int32_t)((run_max + piece - 1) / piece);
+  p.nchunks = (int32_t)((t1 - t0 + c - 1) / c);
+  p.items_per_chunk = (int64_t)lm * 2 * p.R * p.P;
+  p.n_items = p.items_per_chunk * p.nchunks;
+  p.mig_t0 = t0;
+  p.mig_t1 = t1;
+  p.sig_c = (int32_t)c;
+  p.err = g_err_word;
+  return p;
+}
+
+// Programmatic dependent launch for the copy kernels (DYNA_KV_PDL=0 in the
+// environment turns it off): consecutive migrations on a stream overlap launch
+// + prologue with the previous kernel's drain.  Correct either way (see pdl_enter()).
+bool pdl_enabled() {  // default on (measured: +5-16% on small calls, +0.3% on 512 MiB calls)
+  static const bool on = [] {
+    const char* e = std::getenv("DYNA_KV_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kernel(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                          Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <int U, bool SIG, class Src>
+int vec_occupancy() {
+  static std::map<int, int> cache;  // per device
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copy_vec<U, SIG, Src>, kVecThreads, 0);
+  if (occ <= 0) occ = 1;
+  cache[dev] = occ;
+  return occ;
+}
+
+// Balanced persistent grid: the fewest workers (warps or CTAs) that still need
+// only ceil(n / max_workers) rounds, so every worker gets the same number of
+// items (+-1) and no partial last round leaves most of the chip idle.
+int64_t balanced_workers(int64_t n_items, int64_t max_workers) {
+  if (n_items <= max_workers) return n_items;
+  const int64_t rounds = (n_items + max_workers - 1) / max_workers;
+  return (n_items + rounds - 1) / rounds;
+}
+
+// Counter slot for one dynamically scheduled launch (nullptr: static round-robin).
+unsigned long long* sched_slot(DevInfo* di, int schedule) {
+  if (schedule != DYNA_SCHED_DYNAMIC || !di->sched) return nullptr;  // default: static
+  const uint32_t k = di->sched_seq.fetch_add(1, std::memory_order_relaxed) % kSchedSlots;
+  return di->sched + 2 * (size_t)k;
+}
+
+template <int U, bool SIG, class Src>
+void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cudaStream_t st,
+                unsigned long long* sched) {
+  const int occ = vec_occupancy<U, SIG, Src>();
+  constexpr int wpc = kVecThreads / 32;  // warps per CTA
+  int64_t max_ctas = (int64_t)sms * occ;
+  if (max_grid > 0) max_ctas = std::min<int64_t>(max_ctas, max_grid);
+  const int64_t warps = balanced_workers(n_items, max_ctas * wpc);
+  const int64_t grid = (warps + wpc - 1) / wpc;
+  launch_kernel(k_copy_vec<U, SIG, Src, false>, (unsigned)grid, kVecThreads, 0, st, src, sched);
+}
+
+template <bool SIG, class Src>
+dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, int64_t max_grid, int sms,
+                        cudaStream_t st, unsigned long long* sched, bool ws) {
+  const size_t smem = (size_t)stages * piece;
+  auto kern = ws ? k_copy_bulk_ws<SIG, Src> : k_copy_bulk<SIG, Src>;
+  const int threads = ws ? 64 : 32;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
+  int64_t cap = (int64_t)sms * occ;
+  if (max_grid > 0) cap = std::min<int64_t>(cap, max_grid);
+  CUDA_TRY(launch_kernel(kern, (unsigned)balanced_workers(n_items, cap), threads, smem, st, src, stages, sched));
+  return DYNA_OK;
+}
+
+// Launch one copy kernel over `src` (n_items items; piece bytes per item).
+// engine: DYNA_ENGINE_VEC / BULK.  SIG: per-chunk signalling (single plan only).
+template <class Src>
+dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int engine, int max_ctas, int stages,
+                       int unroll, int dev, cudaStream_t st, int schedule) {
+  if (n_items == 0) return DYNA_OK;
+  if (n_items >= (int64_t(1) << 31))
+    return fail(DYNA_ERANGE, "%lld work items in one launch (item math is 32-bit); use a larger piece or split the range",
+                (long long)n_items);
+  DevInfo* di = dev_info(dev);
+  unsigned long long* sc = sched_slot(di, schedule);
+  if (engine == DYNA_ENGINE_BULK || engine == DYNA_ENGINE_BULK_WS) {
+    const bool ws = engine == DYNA_ENGINE_BULK_WS;
+    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st, sc, ws)
+                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st, sc, ws);
+    if (r) return r;
+  } else if (unroll == 4) {
+    sig ? launch_vec<4, true>(src, n_items, max_ctas, di->sms, st, sc)
+        : launch_vec<4, false>(src, n_items, max_ctas, di->sms, st, sc);
+  } else if (unroll == 16) {
+    sig ? launch_vec<16, true>(src, n_items, max_ctas, di->sms, st, sc)
+        : launch_vec<16, false>(src, n_items, max_ctas, di->sms, st, sc);
+  } else {
+    sig ? launch_vec<8, true>(src, n_items, max_ctas, di->sms, st, sc)
+        : launch_vec<8, false>(src, n_items, max_ctas, di->sms, st, sc);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+// Producer-coupled launch: VEC engine, coherent loads, per-warp ready waits.
+dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st, int schedule) {
+  DevInfo* di = dev_info(dev);
+  SingleSource src{p};
+  const bool sig = p.counters != nullptr;
+  int occ = 0;
+  if (sig)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copy_vec<8, true, SingleSource, true>, kVecThreads, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copy_vec<8, false, SingleSource, true>, kVecThreads, 0);
+  // never more than half the SMs' worth of CTAs: the producer must be able to run beside us
+  int64_t cap = std::max(1, di->sms / 2);
+  if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
+  cap = std::min<int64_t>(cap, (int64_t)di->sms * std::max(occ, 1));
+  constexpr int wpc = kVecThreads / 32;
+  const int64_t warps = balanced_workers(p.n_items, cap * wpc);
+  const unsigned grid = (unsigned)((warps + wpc - 1) / wpc);
+  unsigned long long* sc = sched_slot(di, schedule);
+  if (sig)
+    k_copy_vec<8, true, SingleSource, true><<<grid, kVecThreads, 0, st>>>(src, sc);
+  else
+    k_copy_vec<8, false, SingleSource, true><<<grid, kVecThreads, 0, st>>>(src, sc);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev,
+                        cudaStream_t st, int schedule) {
+  SingleSource src{p};
+  return launch_src(src, p.n_items, p.counters != nullptr, p.piece, engine, max_ctas, stages, unroll, dev, st,
+                    schedule);
+}
+
+// ------------------------------------------------------------------ staged variant (a2, a3, a4)
+// K1 gather -> source staging slot, K2 slot -> destination-side slot, K3 scatter
+// slot -> destination rows (+ per-chunk flag).  Chunks are cut into sub-chunks
+// that fit one staging slot; two slots per side alternate.  Same device:
+// everything in stream order.  Two devices of one process: K3 runs on a
+// library stream of the destination device, ordered with events.
+dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, const int32_t* dids, dyna_range tr,
+                       int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
+                       int max_ctas, cudaStream_t stream, dyna_kv_xfer* x, int schedule) {
+  if (D->imported)
+    return fail(DYNA_ENOTSUP, "STAGED variant into an imported (cross-process) pool is not supported; use FUSED");
+  const int64_t row = S->row;
+  const bool cross = D->dev != S->dev;
+  const int64_t nchunks = (tr.end - tr.begin + c - 1) / c;
+  DevInfo* ddi = dev_info(D->dev);
+  cudaStream_t dstream = stream;
+  if (cross) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!ddi->aux) {
+      DeviceGuard g(D->dev);
+      CUDA_TRY(cudaStreamCreateWithFlags(&ddi->aux, cudaStreamNonBlocking));
+    }
+    dstream = ddi->aux;
+  }
+  const int64_t tok_bytes = row * lm * 2;
+  const int64_t sc = std::max<int64_t>(1, std::min<int64_t>(c, kStageSlotBytes / tok_bytes));
+  const int64_t slot = sc * tok_bytes;
+  char *sbuf = nullptr, *dbuf = nullptr;
+  dyna_status r = channel_staging(S, D, slot, &sbuf, &dbuf);
+  if (r) return r;
+  unsigned long long* counters = nullptr;
+  if (signal) {
+    if ((r = channel_counters(S, D, D->dev, &counters))) return r;
+    x->epoch = next_epoch(S->desc.instance, D);
+  }
+  cudaEvent_t done_src[2] = {nullptr, nullptr};  // K2 of slot i finished (cross-device)
+  cudaEvent_t done_dst[2] = {nullptr, nullptr};  // K3 of slot i finished (cross-device)
+  if (cross)
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(get_event(S->dev, &done_src[i]));
+      DeviceGuard g(D->dev);
+      CUDA_TRY(get_event(D->dev, &done_dst[i]));
+    }
+  int64_t sub = 0;
+  for (int64_t k = 0; k < nchunks && !r; ++k) {
+    const int64_t a = tr.begin + k * c, b = std::min(a + c, tr.end);
+    for (int64_t sa = a; sa < b && !r; sa += sc, ++sub) {
+      const int64_t sb = std::min(sa + sc, b);
+      const int si = (int)(sub & 1);
+      char* sslot = sbuf + si * slot;
+      char* dslot = dbuf + si * slot;
+      if (cross && sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[si], 0));
+      Plan k1 = make_plan(paged(S, sids), linear(sslot), row, sa, sb, l0, lm, sb - sa, S->desc.block_size, piece);
+      if ((r = launch_copy(k1, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
+      // K2: the sub-chunk slot is [lm][2][n][row] = two contiguous halves
+      // (K and V of all layers): a flat plan with one token of `half` bytes.
+      Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
+      if ((r = launch_copy(k2, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
+      Plan k3 = make_plan(linear(dslot), paged(D, dids), row, sa, sb, l0, lm, sb - sa, D->desc.block_size, piece);
+      k3.mig_t0 = tr.begin;
+      k3.mig_t1 = tr.end;
+      k3.sig_c = (int32_t)c;
+      if (signal) {
+        k3.counters = counters;
+        k3.flags = D->inbox + (size_t)S->desc.instance * DYNA_MAX_CHUNKS;
+        k3.epoch = x->epoch;
+      }
+      if (cross) {
+        CUDA_TRY(cudaEventRecord(done_src[si], stream));
+        DeviceGuard g(D->dev);
+        CUDA_TRY(cudaStreamWaitEvent(dstream, done_src[si], 0));
+        if ((r = launch_copy(k3, engine, max_ctas, stages, unroll, D->dev, dstream, schedule))) break;
+        CUDA_TRY(cudaEventRecord(done_dst[si], dstream));
+      } else {
+        if ((r = launch_copy(k3, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
+      }
+    }
+  }
+  if (cross) {  // the migration completes on `stream` once the last scatters are done
+    const int last = (int)((sub - 1) & 1);
+    CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[last], 0));
+    if (sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[last ^ 1], 0));
+    for (int i = 0; i < 2; ++i) {
+      put_event(S->dev, done_src[i]);
+      put_event(D->dev, done_dst[i]);
+    }
+  }
+  return r;
+}
+
+dyna_status launch_batch(const BatchSource& src, int64_t n_items, int piece, int engine, int max_ctas, int stages,
+                         int unroll, int dev, cudaStream_t st, int schedule) {
+  return launch_src(src, n_items, false, piece, engine, max_ctas, stages, unroll, dev, st, schedule);
+}
+
+void launch_wait_flag(const unsigned long long* flag, unsigned long long epoch, unsigned long long timeout_ns,
+                      cudaStream_t st) {
+  k_wait_flag<<<1, 1, 0, st>>>(flag, epoch, timeout_ns, g_err_word);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_release_sys(unsigned long long* slot, unsigned long long v, cudaStream_t st) {
+  k_release_sys<<<1, 1, 0, st>>>(slot, v);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void launch_mark_ready(unsigned long long* slot, unsigned long long v, cudaStream_t st) {
+  k_mark_ready<<<1, 1, 0, st>>>(slot, v);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+dyna_status launch_fill(void* dst, uint64_t bytes, unsigned long long key, uint64_t first_word, int dev,
+                        cudaStream_t st) {
+  DevInfo* di = dev_info(dev);
+  const uint64_t n16 = bytes / 16;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n16 + 255) / 256, (uint64_t)di->sms * 8);
+  k_fill<<<grid, 256, 0, st>>>(static_cast<ulonglong2*>(dst), n16, key, first_word);
+  CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+}  // namespace rt
+}  // namespace dynakv
+

@@ -1,0 +1,452 @@
+// migrate.cu — the push itself (§4.3): validation, variant /
+// engine choice from the calibration table, host-resident tables through the
+// upload ring, dyna_kv_migrate(_ex/_batch/_on_ready), and completion (wait, query,
+// per-chunk flags on the receiver).
+#include "runtime.cuh"
+
+using namespace dynakv;
+using namespace dynakv::rt;
+
+namespace dynakv {
+namespace rt {
+
+// Completion event of a migration (none while the stream is being captured
+// into a CUDA graph: the captured work only runs at replay).
+dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone) {
+    x->captured = true;
+    return DYNA_OK;
+  }
+  cudaError_t e = get_event(dev, &x->ev);
+  if (e == cudaSuccess) e = cudaEventRecord(x->ev, stream);
+  if (e != cudaSuccess) return fail(DYNA_ECUDA, "event record: %s", cudaGetErrorString(e));
+  return DYNA_OK;
+}
+
+// ------------------------------------------------------------------ shared validation
+dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
+  *o = dyna_kv_opts{};
+  if (opts) *o = *opts;
+  if (o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > 3 || o->max_ctas < 0 || o->piece_bytes < 0 ||
+      o->piece_bytes % 16 || o->stages < 0 || o->stages == 1 || o->stages > kMaxStages ||
+      (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16) || o->schedule < 0 ||
+      o->schedule > DYNA_SCHED_DYNAMIC)
+    return fail(DYNA_EINVAL, "invalid dyna_kv_opts");
+  return DYNA_OK;
+}
+
+// Geometry, ranges, table presence and (with host ids) ids / aliasing.  *empty: nothing to move.
+dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
+                          int32_t chunk_tokens, bool* empty) {
+  if (!src.pool || !dst.pool) return fail(DYNA_EINVAL, "NULL pool in a block table");
+  const dyna_kv_pool_desc &gs = src.pool->desc, &gd = dst.pool->desc;
+  if (gs.num_layers != gd.num_layers || gs.num_kv_heads != gd.num_kv_heads || gs.head_dim != gd.head_dim ||
+      gs.elem_bytes != gd.elem_bytes)
+    return fail(DYNA_EGEOM, "source and destination geometry differ (L, H, d, e)");
+  if (lr.begin < 0 || lr.begin > lr.end || lr.end > gs.num_layers)
+    return fail(DYNA_ERANGE, "layer range [%lld, %lld) outside [0, %d)", (long long)lr.begin, (long long)lr.end,
+                gs.num_layers);
+  if (tr.begin < 0 || tr.begin > tr.end) return fail(DYNA_ERANGE, "bad token range");
+  if (tr.end >= (int64_t(1) << 31)) return fail(DYNA_ERANGE, "token indices must be < 2^31");
+  *empty = tr.begin == tr.end || lr.begin == lr.end;
+  if (*empty) return DYNA_OK;
+  if (chunk_tokens <= 0) return fail(DYNA_ERANGE, "chunk_tokens must be > 0");
+  if (src.len < 0 || dst.len < 0 || tr.end > src.len * gs.block_size || tr.end > dst.len * gd.block_size)
+    return fail(DYNA_ERANGE, "token range end %lld exceeds a block table (src %lld, dst %lld tokens)",
+                (long long)tr.end, (long long)(src.len * gs.block_size), (long long)(dst.len * gd.block_size));
+  if ((!src.block_ids && !src.host_block_ids) || (!dst.block_ids && !dst.host_block_ids))
+    return fail(DYNA_EINVAL, "a block table has neither device nor host block ids");
+  return check_host_tables(src, dst, tr.begin, tr.end);
+}
+
+// The destination must be addressable from the source (launching) device.
+dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D) {
+  if (D->imported) {
+    if (D->dev != S->dev)
+      return fail(DYNA_EPEER, "imported destination is mapped on device %d, source is on %d", D->dev, S->dev);
+    return DYNA_OK;
+  }
+  return D->dev == S->dev ? DYNA_OK : ensure_peer(S->dev, D->dev);
+}
+
+// a6: unset choices come from the calibration table (measured GB/s per row
+// bytes, locality and call size), else FUSED + VEC.
+Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok) {
+  dyna_kv_calib_entry ce{};
+  const bool calibrated =
+      (o.variant == DYNA_VARIANT_AUTO || o.engine == DYNA_ENGINE_AUTO) && calib_lookup(row, peer, ntok, &ce);
+  Choice c{};
+  c.variant = o.variant ? o.variant : (calibrated && ce.variant ? ce.variant : DYNA_VARIANT_FUSED);
+  c.engine = o.engine ? o.engine : (calibrated && ce.engine ? ce.engine : DYNA_ENGINE_VEC);
+  const bool use_ce = calibrated && (!o.engine || o.engine == ce.engine);
+  c.piece = o.piece_bytes ? o.piece_bytes
+                          : (use_ce && ce.piece_bytes ? ce.piece_bytes
+                                                     : (c.engine == DYNA_ENGINE_VEC ? kVecPiece : kBulkPiece));
+  c.stages = o.stages ? o.stages : (use_ce && ce.stages ? ce.stages : kBulkStages);
+  c.unroll = o.unroll ? o.unroll : (use_ce && ce.unroll ? ce.unroll : kVecU);
+  return c;
+}
+
+// Entries [0, last touched] of a table's host ids (what the kernel may read).
+size_t table_upload_bytes(const dyna_block_table& t, int64_t t1) {
+  return (size_t)((t1 - 1) / t.pool->desc.block_size + 1) * sizeof(int32_t);
+}
+
+}  // namespace rt
+}  // namespace dynakv
+
+extern "C" {
+
+dyna_status dyna_kv_migrate(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                            int32_t chunk_tokens, struct CUstream_st* stream, dyna_kv_xfer_t* out) {
+  return dyna_kv_migrate_ex(src, dst, tr, lr, chunk_tokens, stream, nullptr, out);
+}
+
+static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                                int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
+                                dyna_kv_ready* board, uint64_t ready_epoch, dyna_kv_xfer_t* out);
+
+dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                               int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
+                               dyna_kv_xfer_t* out) {
+  return migrate_impl(src, dst, tr, lr, chunk_tokens, stream_, opts, nullptr, 0, out);
+}
+
+dyna_status dyna_kv_migrate_on_ready(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                                     int32_t chunk_tokens, dyna_kv_ready_t board, uint64_t epoch,
+                                     struct CUstream_st* stream_, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
+  if (!board) return fail(DYNA_EINVAL, "NULL ready board");
+  return migrate_impl(src, dst, tr, lr, chunk_tokens, stream_, opts, board, epoch, out);
+}
+
+static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                                int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
+                                dyna_kv_ready* board, uint64_t ready_epoch, dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  dyna_kv_opts o{};
+  dyna_status r = check_opts(opts, &o);
+  if (r) return r;
+  bool empty = false;
+  if ((r = validate_pair(src, dst, tr, lr, chunk_tokens, &empty))) return r;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  dyna_kv_pool* S = src.pool;
+  dyna_kv_pool* D = dst.pool;
+  const dyna_kv_pool_desc &gs = S->desc, &gd = D->desc;
+  const int64_t ntok = tr.end - tr.begin;
+  const int64_t nchunks = empty ? 0 : (ntok + chunk_tokens - 1) / chunk_tokens;
+  const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
+  if (signal && nchunks > DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks, DYNA_MAX_CHUNKS);
+  if (board) {
+    if (board->dev != src.pool->dev) return fail(DYNA_EINVAL, "ready board must live on the source device");
+    if (nchunks > board->max_chunks)
+      return fail(DYNA_ERANGE, "%lld chunks > the ready board's %d slots", (long long)nchunks, board->max_chunks);
+    if (o.variant == DYNA_VARIANT_STAGED || (o.engine && o.engine != DYNA_ENGINE_VEC))
+      return fail(DYNA_ENOTSUP, "producer-coupled migration: FUSED variant, VEC engine only");
+  }
+  if (empty) {  // s = 0 (or no layers) -> nothing to ship, nothing enqueued
+    auto* x = new dyna_kv_xfer();
+    x->dev = S->dev;
+    x->sender = gs.instance;
+    x->empty = true;
+    *out = x;
+    return DYNA_OK;
+  }
+  if ((r = check_reach(S, D))) return r;
+  if (!err_word()) return fail(DYNA_ECUDA, "no error word");
+
+  const int64_t row = S->row;
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  const int64_t c = chunk_tokens;
+  const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
+  Choice ch = choose(o, row, peer_dst, ntok);
+  if (signal && !o.engine && ch.engine != DYNA_ENGINE_VEC) {
+    // measured (bench.py e2e, per-chunk flags on): the VEC engine's per-warp fences beat
+    // draining bulk-store groups before each chunk's count (2720 vs 2540 GB/s)
+    ch.engine = DYNA_ENGINE_VEC;
+    ch.unroll = kVecU;
+    if (!o.piece_bytes) ch.piece = kVecPiece;
+  }
+  if (board) {  // producer-coupled: the VEC engine (each warp waits on its own chunk's mark)
+    ch.variant = DYNA_VARIANT_FUSED;
+    ch.engine = DYNA_ENGINE_VEC;
+    ch.unroll = 8;
+    if (!o.piece_bytes) ch.piece = kVecPiece;
+  }
+  const int variant = ch.variant, engine = ch.engine, piece = ch.piece, stages = ch.stages, unroll = ch.unroll;
+
+  DeviceGuard guard(S->dev);
+  // Host-resident tables (block_ids == NULL): upload the entries the kernels may read.
+  RingLease lease(S->dev);
+  const int32_t* sids = src.block_ids;
+  const int32_t* dids = dst.block_ids;
+  if (!sids || !dids) {
+    if (variant == DYNA_VARIANT_STAGED && D->dev != S->dev)
+      return fail(DYNA_ENOTSUP, "cross-device STAGED needs device block_ids for the destination");
+    const size_t sb = sids ? 0 : (table_upload_bytes(src, tr.end) + 15) & ~size_t(15);
+    const size_t db = dids ? 0 : table_upload_bytes(dst, tr.end);
+    char *base = nullptr, *h = nullptr;
+    if ((r = lease.reserve(sb + db, &base, &h, stream))) return r;
+    if (!sids) std::memcpy(h, src.host_block_ids, table_upload_bytes(src, tr.end));
+    if (!dids) std::memcpy(h + sb, dst.host_block_ids, db);
+    if ((r = lease.copy(stream))) return r;
+    if (!sids) sids = reinterpret_cast<const int32_t*>(base);
+    if (!dids) dids = reinterpret_cast<const int32_t*>(base + sb);
+  }
+
+  auto* x = new dyna_kv_xfer();
+  x->dev = S->dev;
+  x->sender = gs.instance;
+  x->nchunks = (int32_t)nchunks;
+  x->variant = variant;
+  x->engine = engine;
+  x->piece = piece;
+  x->stages = engine != DYNA_ENGINE_VEC ? stages : 0;
+  x->unroll = engine == DYNA_ENGINE_VEC ? unroll : 0;
+  const uint64_t launches0 = g_launches.load();
+  if (variant == DYNA_VARIANT_FUSED) {
+    // K4 / K4-local: source rows -> destination rows, one launch for all chunks.
+    const int64_t g = gcd64(gs.block_size, gd.block_size);
+    Plan p = make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
+    if (signal) {
+      if ((r = channel_counters(S, D, S->dev, &p.counters))) {
+        delete x;
+        return r;
+      }
+      p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
+      p.epoch = x->epoch = next_epoch(gs.instance, D);
+      p.sys_fence = peer_dst;
+    }
+    if (board) {
+      p.ready = board->slots;
+      p.ready_epoch = ready_epoch;
+      p.ready_timeout_ns = board->timeout_ns;
+      r = launch_ready(p, o.max_ctas, S->dev, stream, o.schedule);
+    } else {
+      r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream, o.schedule);
+    }
+  } else {
+    r = run_staged(S, D, sids, dids, tr, l0, lm, c, signal, engine, piece, stages, unroll, o.max_ctas, stream, x,
+                   o.schedule);
+  }
+  if (!r) r = lease.finish(stream);
+  if (r) {
+    delete x;
+    return r;
+  }
+  x->launches = (int32_t)(g_launches.load() - launches0);
+  if ((r = record_completion(x, S->dev, stream))) {
+    delete x;
+    return r;
+  }
+  *out = x;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna_range lr, int32_t chunk_tokens,
+                                  struct CUstream_st* stream_, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  if (n < 0 || (n > 0 && !migs) || n > DYNA_MAX_BATCH) return fail(DYNA_EINVAL, "0 <= n <= DYNA_MAX_BATCH");
+  dyna_kv_opts o{};
+  dyna_status r = check_opts(opts, &o);
+  if (r) return r;
+  if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "batch: FUSED variant only");
+  if (o.flags & DYNA_MIGRATE_SIGNAL) return fail(DYNA_ENOTSUP, "batch: no per-chunk signalling (use dyna_kv_migrate_ex)");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  std::vector<int32_t> live;
+  int64_t total_tok = 0;
+  dyna_kv_pool* S0 = nullptr;
+  int peer = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    bool empty = false;
+    if ((r = validate_pair(migs[i].src, migs[i].dst, migs[i].token_range, lr, chunk_tokens, &empty))) {
+      g_err = "migration " + std::to_string(i) + ": " + g_err;
+      return r;
+    }
+    if (empty) continue;
+    dyna_kv_pool *S = migs[i].src.pool, *D = migs[i].dst.pool;
+    if (!S0) S0 = S;
+    if (S->dev != S0->dev || S->row != S0->row)
+      return fail(DYNA_EINVAL, "batch: all sources on one device with one row size");
+    if ((r = check_reach(S, D))) return r;
+    peer |= (D->dev != S->dev || D->imported) ? 1 : 0;
+    total_tok += migs[i].token_range.end - migs[i].token_range.begin;
+    live.push_back(i);
+  }
+  auto* x = new dyna_kv_xfer();
+  if (live.empty()) {
+    x->empty = true;
+    *out = x;
+    return DYNA_OK;
+  }
+  if (!err_word()) {
+    delete x;
+    return fail(DYNA_ECUDA, "no error word");
+  }
+  x->dev = S0->dev;
+  x->sender = S0->desc.instance;
+  Choice ch = choose(o, S0->row, peer, total_tok);
+  if (!o.engine && ch.engine != DYNA_ENGINE_VEC) {
+    // measured (scripts/batch_probe.py): with many plans the BULK engine's single issuing
+    // thread is latency-bound on per-item plan lookups; the warp-parallel VEC engine is not
+    ch.engine = DYNA_ENGINE_VEC;
+    ch.unroll = kVecU;
+    if (!o.piece_bytes) ch.piece = kVecPiece;
+  }
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  DeviceGuard guard(S0->dev);
+  // One upload: [plans][item bases][host-resident tables].
+  const size_t m = live.size();
+  const size_t plans_b = ((m * sizeof(Plan)) + 15) & ~size_t(15);
+  const size_t bases_b = ((m * sizeof(int64_t)) + 15) & ~size_t(15);
+  std::vector<size_t> soff(m, 0), doff(m, 0);
+  size_t tab_b = 0;
+  for (size_t k = 0; k < m; ++k) {
+    const dyna_kv_migration& mg = migs[live[k]];
+    if (!mg.src.block_ids) {
+      soff[k] = plans_b + bases_b + tab_b;
+      tab_b += (table_upload_bytes(mg.src, mg.token_range.end) + 15) & ~size_t(15);
+    }
+    if (!mg.dst.block_ids) {
+      doff[k] = plans_b + bases_b + tab_b;
+      tab_b += (table_upload_bytes(mg.dst, mg.token_range.end) + 15) & ~size_t(15);
+    }
+  }
+  RingLease lease(S0->dev);
+  int64_t total_items = 0;
+  char *dbase = nullptr, *h = nullptr;
+  if ((r = lease.reserve(plans_b + bases_b + tab_b, &dbase, &h, stream))) {
+    delete x;
+    return r;
+  }
+  std::vector<Plan> plans(m);
+  std::vector<int64_t> bases(m);
+  for (size_t k = 0; k < m; ++k) {
+    const dyna_kv_migration& mg = migs[live[k]];
+    dyna_kv_pool *S = mg.src.pool, *D = mg.dst.pool;
+    const int32_t* sids = mg.src.block_ids ? mg.src.block_ids : reinterpret_cast<const int32_t*>(dbase + soff[k]);
+    const int32_t* dids = mg.dst.block_ids ? mg.dst.block_ids : reinterpret_cast<const int32_t*>(dbase + doff[k]);
+    const int64_t g = gcd64(S->desc.block_size, D->desc.block_size);
+    plans[k] = make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end, l0, lm,
+                         chunk_tokens, g, ch.piece);
+    bases[k] = total_items;
+    total_items += plans[k].n_items;
+  }
+  // fill the pinned staging now that the device pointers are known, then one copy
+  std::memcpy(h, plans.data(), m * sizeof(Plan));
+  std::memcpy(h + plans_b, bases.data(), m * sizeof(int64_t));
+  for (size_t k = 0; k < m; ++k) {
+    const dyna_kv_migration& mg = migs[live[k]];
+    if (!mg.src.block_ids)
+      std::memcpy(h + soff[k], mg.src.host_block_ids, table_upload_bytes(mg.src, mg.token_range.end));
+    if (!mg.dst.block_ids)
+      std::memcpy(h + doff[k], mg.dst.host_block_ids, table_upload_bytes(mg.dst, mg.token_range.end));
+  }
+  if ((r = lease.copy(stream))) {
+    delete x;
+    return r;
+  }
+  BatchSource bsrc{reinterpret_cast<const Plan*>(dbase), reinterpret_cast<const int64_t*>(dbase + plans_b),
+                   (int32_t)m, total_items};
+  x->variant = DYNA_VARIANT_FUSED;
+  x->engine = ch.engine;
+  x->piece = ch.piece;
+  x->stages = ch.engine != DYNA_ENGINE_VEC ? ch.stages : 0;
+  x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
+  x->launches = 1;
+  r = launch_batch(bsrc, total_items, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev, stream,
+                   o.schedule);
+  if (!r) r = lease.finish(stream);
+  if (r) {
+    delete x;
+    return r;
+  }
+  if ((r = record_completion(x, S0->dev, stream))) {
+    delete x;
+    return r;
+  }
+  *out = x;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_query(dyna_kv_xfer_t x) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (x->empty || x->captured) return DYNA_OK;
+  cudaError_t e = cudaEventQuery(x->ev);
+  if (e == cudaSuccess) return DYNA_OK;
+  if (e == cudaErrorNotReady) return DYNA_EAGAIN;
+  return fail(DYNA_ECUDA, "%s", cudaGetErrorString(e));
+}
+
+dyna_status dyna_kv_wait(dyna_kv_xfer_t x) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  dyna_status r = DYNA_OK;
+  if (!x->empty && !x->captured) {
+    cudaError_t e = cudaEventSynchronize(x->ev);
+    if (e != cudaSuccess) r = fail(DYNA_ECUDA, "migration failed: %s", cudaGetErrorString(e));
+    put_event(x->dev, x->ev);
+    if (!r) r = take_device_error();
+  }
+  delete x;
+  return r;
+}
+
+dyna_status dyna_kv_stream_wait(dyna_kv_xfer_t x, struct CUstream_st* stream) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (x->empty) return DYNA_OK;
+  if (x->captured) return fail(DYNA_ENOTSUP, "captured migration: order on the graph instead");
+  CUDA_TRY(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), x->ev, 0));
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t x, uint64_t* epoch, int32_t* num_chunks, int32_t* sender) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (epoch) *epoch = x->epoch;
+  if (num_chunks) *num_chunks = x->nchunks;
+  if (sender) *sender = x->sender;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_xfer_plan(dyna_kv_xfer_t x, int32_t* variant, int32_t* engine, int32_t* piece, int32_t* stages,
+                              int32_t* unroll, int32_t* launches) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (variant) *variant = x->variant;
+  if (engine) *engine = x->engine;
+  if (piece) *piece = x->piece;
+  if (stages) *stages = x->stages;
+  if (unroll) *unroll = x->unroll;
+  if (launches) *launches = x->launches;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_stream_wait_chunk(dyna_kv_pool_t dst, int32_t sender, int32_t chunk, uint64_t epoch,
+                                      uint64_t timeout_ns, struct CUstream_st* stream) {
+  if (!dst) return fail(DYNA_EINVAL, "NULL pool");
+  if (dst->imported) return fail(DYNA_EINVAL, "wait on the owner's side: this pool is an imported mapping");
+  if (sender < 0 || sender >= DYNA_MAX_INSTANCES || chunk < 0 || chunk >= DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "sender/chunk out of range");
+  if (!err_word()) return fail(DYNA_ECUDA, "no error word");
+  DeviceGuard g(dst->dev);
+  launch_wait_flag(dst->inbox + (size_t)sender * DYNA_MAX_CHUNKS + chunk, epoch, timeout_ns,
+                   reinterpret_cast<cudaStream_t>(stream));
+  CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_copy_flags(dyna_kv_pool_t dst, int32_t sender, int32_t first, int32_t n, uint64_t* host_out,
+                               struct CUstream_st* stream) {
+  if (!dst || !host_out) return fail(DYNA_EINVAL, "NULL argument");
+  if (sender < 0 || sender >= DYNA_MAX_INSTANCES || first < 0 || n < 0 || first + n > DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "sender/chunk range out of range");
+  if (n == 0) return DYNA_OK;
+  DeviceGuard g(dst->dev);
+  CUDA_TRY(cudaMemcpyAsync(host_out, dst->inbox + (size_t)sender * DYNA_MAX_CHUNKS + first,
+                           sizeof(uint64_t) * (size_t)n, cudaMemcpyDeviceToHost,
+                           reinterpret_cast<cudaStream_t>(stream)));
+  return DYNA_OK;
+}
+
+}  // extern "C"

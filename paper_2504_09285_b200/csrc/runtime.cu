@@ -1,0 +1,453 @@
+// runtime.cu — devices, errors, events, pools and their IPC export/import, peer
+// access, the calibration table, signalling channels' counters and
+// staging, and the test-input fill.  Paper mapping: PAPER.md §3.1 P:352 (instances
+// exchange the required KV blocks).
+#include "runtime.cuh"
+
+using namespace dynakv;
+using namespace dynakv::rt;
+
+namespace dynakv {
+namespace rt {
+
+thread_local std::string g_err;
+
+dyna_status fail(dyna_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+std::atomic<uint64_t> g_launches{0};
+std::mutex g_mu;
+
+// Process-wide deferred error word in mapped pinned host memory: kernels
+// atomicOr ERR_* bits into it; dyna_kv_wait / dyna_kv_poll_error read it.
+unsigned int* g_err_word = nullptr;
+unsigned int* err_word() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_err_word) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    std::memset(p, 0, 64);
+    g_err_word = static_cast<unsigned int*>(p);
+  }
+  return g_err_word;
+}
+
+dyna_status take_device_error() {
+  unsigned int* w = err_word();
+  if (!w) return DYNA_OK;
+  const unsigned int bits = __atomic_exchange_n(w, 0u, __ATOMIC_ACQ_REL);
+  if (bits & ERR_BAD_BLOCK) return fail(DYNA_ERANGE, "device-side check: block id outside [0, num_blocks)");
+  if (bits & ERR_TIMEOUT) return fail(DYNA_ETIMEDOUT, "device-side chunk wait timed out");
+  return DYNA_OK;
+}
+
+std::map<int, DevInfo> g_dev;
+
+DevInfo* dev_info(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevInfo& d = g_dev[dev];
+  if (d.sms == 0) {
+    DeviceGuard g(dev);
+    preload_kernels();
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (d.sms <= 0) d.sms = 1;
+    if (cudaMalloc(&d.sched, sizeof(unsigned long long) * 2 * kSchedSlots) != cudaSuccess ||
+        cudaMemset(d.sched, 0, sizeof(unsigned long long) * 2 * kSchedSlots) != cudaSuccess)
+      d.sched = nullptr;  // dynamic scheduling unavailable: static round-robin
+  }
+  return &d;
+}
+
+std::mutex g_ev_mu;
+std::map<int, std::vector<cudaEvent_t>> g_ev_free;
+
+cudaError_t get_event(int dev, cudaEvent_t* ev) {
+  {
+    std::lock_guard<std::mutex> lk(g_ev_mu);
+    auto& v = g_ev_free[dev];
+    if (!v.empty()) {
+      *ev = v.back();
+      v.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+}
+
+void put_event(int dev, cudaEvent_t ev) {
+  std::lock_guard<std::mutex> lk(g_ev_mu);
+  g_ev_free[dev].push_back(ev);
+}
+
+bool desc_valid(const dyna_kv_pool_desc* d) {
+  return d && d->num_layers > 0 && d->num_kv_heads > 0 && d->head_dim > 0 && d->elem_bytes > 0 &&
+         d->block_size > 0 && d->num_blocks > 0 && d->device >= 0 && d->instance >= 0 &&
+         d->instance < DYNA_MAX_INSTANCES;
+}
+
+int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    int64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+// ------------------------------------------------------------------ calibration (a6)
+const dyna_kv_calib_entry kCalibDefault[] = {
+#include "calib_default.inc"
+    {0, -1, 0, 0, 0, 0, 0, 0}  // sentinel (never matches: peer = -1)
+};
+
+std::mutex g_calib_mu;
+std::vector<dyna_kv_calib_entry> g_calib(std::begin(kCalibDefault), std::end(kCalibDefault) - 1);
+
+// Best calibrated entry for (row bytes, locality, call tokens): entries for this
+// exact row size first, generic (row_bytes == 0) ones only if none matches;
+// within a class the smallest max_chunk_tokens that covers the call wins.
+bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out) {
+  std::lock_guard<std::mutex> lk(g_calib_mu);
+  for (int pass = 0; pass < 2; ++pass) {
+    const dyna_kv_calib_entry* best = nullptr;
+    for (const auto& e : g_calib) {
+      const bool row_ok = pass == 0 ? e.row_bytes == row : e.row_bytes == 0;
+      if (!row_ok || e.peer != peer || c > e.max_chunk_tokens) continue;
+      if (!best || e.max_chunk_tokens < best->max_chunk_tokens) best = &e;
+    }
+    if (best) {
+      *out = *best;
+      return true;
+    }
+  }
+  return false;
+}
+
+Side paged(const dyna_kv_pool* pool, const int32_t* ids) {
+  Side s{};
+  s.base = pool->base;
+  s.table = ids;
+  s.nb = pool->desc.num_blocks;
+  s.bs = pool->desc.block_size;
+  s.linear = 0;
+  return s;
+}
+
+Side linear(char* base) {
+  Side s{};
+  s.base = base;
+  s.linear = 1;
+  return s;
+}
+
+// Synchronous checks that need the host copies of the tables.
+dyna_status check_host_tables(const dyna_block_table& src, const dyna_block_table& dst, int64_t t0, int64_t t1) {
+  struct Span {
+    int32_t id;
+    int64_t lo, hi;  // slot range [lo, hi) inside block id
+  };
+  auto spans = [&](const dyna_block_table& t, std::vector<Span>& out) -> dyna_status {
+    const int64_t bs = t.pool->desc.block_size, nb = t.pool->desc.num_blocks;
+    for (int64_t j = t0 / bs; j <= (t1 - 1) / bs; ++j) {
+      const int32_t id = t.host_block_ids[j];
+      if (id < 0 || id >= nb) return fail(DYNA_ERANGE, "block_ids[%lld] = %d outside [0, %lld)", (long long)j, id, (long long)nb);
+      const int64_t lo = std::max(t0, j * bs) - j * bs, hi = std::min(t1, (j + 1) * bs) - j * bs;
+      out.push_back({id, lo, hi});
+    }
+    return DYNA_OK;
+  };
+  std::vector<Span> s, d;
+  if (src.host_block_ids) {
+    dyna_status r = spans(src, s);
+    if (r) return r;
+  }
+  if (dst.host_block_ids) {
+    dyna_status r = spans(dst, d);
+    if (r) return r;
+    auto by_id = [](const Span& a, const Span& b) { return a.id != b.id ? a.id < b.id : a.lo < b.lo; };
+    std::vector<Span> ds = d;
+    std::sort(ds.begin(), ds.end(), by_id);
+    for (size_t i = 1; i < ds.size(); ++i)
+      if (ds[i].id == ds[i - 1].id && ds[i].lo < ds[i - 1].hi)
+        return fail(DYNA_EALIAS, "destination block %d is reached twice by the token range", ds[i].id);
+    if (src.host_block_ids && src.pool->base == dst.pool->base) {
+      std::vector<Span> ss = s;
+      std::sort(ss.begin(), ss.end(), by_id);
+      size_t i = 0;
+      for (const Span& x : ds) {
+        while (i < ss.size() && ss[i].id < x.id) ++i;
+        for (size_t k = i; k < ss.size() && ss[k].id == x.id; ++k)
+          if (ss[k].lo < x.hi && x.lo < ss[k].hi)
+            return fail(DYNA_EALIAS, "same pool: destination rows of block %d overlap source rows", x.id);
+      }
+    }
+  }
+  return DYNA_OK;
+}
+
+dyna_status ensure_peer(int dev, int peer) {
+  if (dev == peer) return DYNA_OK;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, dev, peer) != cudaSuccess || !can)
+    return fail(DYNA_EPEER, "device %d cannot access device %d (no P2P)", dev, peer);
+  DeviceGuard g(dev);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return DYNA_OK;
+  }
+  if (e != cudaSuccess) return fail(DYNA_EPEER, "cudaDeviceEnablePeerAccess(%d->%d): %s", dev, peer, cudaGetErrorString(e));
+  return DYNA_OK;
+}
+
+// Epochs are monotone per (sender instance, destination pool), whatever the
+// variant or the source pool object, so a flag never moves backwards.
+std::map<std::pair<int, const dyna_kv_pool*>, uint64_t> g_epochs;
+
+uint64_t next_epoch(int sender, const dyna_kv_pool* dst) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return ++g_epochs[{sender, dst}];
+}
+
+// Self-resetting per-chunk byte counters of channel src -> dst on device kdev.
+dyna_status channel_counters(dyna_kv_pool* src, const dyna_kv_pool* dst, int kdev, unsigned long long** out) {
+  std::lock_guard<std::mutex> lk(src->mu);
+  Channel& ch = src->channels[dst];
+  unsigned long long*& c = ch.counters[kdev];
+  if (!c) {
+    DeviceGuard g(kdev);
+    CUDA_TRY(cudaMalloc(&c, sizeof(unsigned long long) * DYNA_MAX_CHUNKS));
+    CUDA_TRY(cudaMemset(c, 0, sizeof(unsigned long long) * DYNA_MAX_CHUNKS));
+  }
+  *out = c;
+  return DYNA_OK;
+}
+
+// Staging slots of channel src -> dst (staged variant): 2 x slot on each side.
+dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t slot, char** sbuf, char** dbuf) {
+  std::lock_guard<std::mutex> lk(src->mu);
+  Channel& ch = src->channels[dst];
+  if (ch.slot_bytes < slot) {
+    if (ch.sstage) {  // grow: the previous migration on this channel must be done with them
+      DeviceGuard g(ch.sdev);
+      cudaDeviceSynchronize();
+      cudaFree(ch.sstage);
+      ch.sstage = nullptr;
+    }
+    if (ch.dstage) {
+      DeviceGuard g(ch.ddev);
+      cudaDeviceSynchronize();
+      cudaFree(ch.dstage);
+      ch.dstage = nullptr;
+    }
+    ch.slot_bytes = 0;
+    {
+      DeviceGuard g(src->dev);
+      if (cudaMalloc(&ch.sstage, 2 * slot) != cudaSuccess) return fail(DYNA_ENOMEM, "staging (source side)");
+      ch.sdev = src->dev;
+    }
+    {
+      DeviceGuard g(dst->dev);
+      if (cudaMalloc(&ch.dstage, 2 * slot) != cudaSuccess) return fail(DYNA_ENOMEM, "staging (destination side)");
+      ch.ddev = dst->dev;
+    }
+    ch.slot_bytes = slot;
+  }
+  *sbuf = ch.sstage;
+  *dbuf = ch.dstage;
+  return DYNA_OK;
+}
+
+std::mutex g_rings_mu;
+std::map<int, UploadRing*> g_rings;
+
+}  // namespace rt
+}  // namespace dynakv
+
+extern "C" {
+
+const char* dyna_kv_last_error(void) { return g_err.c_str(); }
+
+dyna_status dyna_kv_calib_set(const dyna_kv_calib_entry* entries, int32_t n) {
+  if (n < 0 || n > 256 || (n > 0 && !entries)) return fail(DYNA_EINVAL, "calibration: 0 <= n <= 256");
+  for (int32_t i = 0; i < n; ++i) {
+    const auto& e = entries[i];
+    if (e.row_bytes < 0 || e.peer < 0 || e.peer > 1 || e.max_chunk_tokens <= 0 || e.variant < 0 || e.variant > 2 ||
+        e.engine < 0 || e.engine > 3 || e.piece_bytes < 0 || e.piece_bytes % 16 || e.stages < 0 || e.stages == 1 ||
+        e.stages > kMaxStages || (e.unroll != 0 && e.unroll != 4 && e.unroll != 8 && e.unroll != 16))
+      return fail(DYNA_EINVAL, "calibration entry %d invalid", i);
+  }
+  std::lock_guard<std::mutex> lk(g_calib_mu);
+  if (n == 0)
+    g_calib.assign(std::begin(kCalibDefault), std::end(kCalibDefault) - 1);
+  else
+    g_calib.assign(entries, entries + n);
+  return DYNA_OK;
+}
+
+int32_t dyna_kv_calib_get(dyna_kv_calib_entry* out, int32_t cap) {
+  std::lock_guard<std::mutex> lk(g_calib_mu);
+  for (int32_t i = 0; i < cap && i < (int32_t)g_calib.size(); ++i) out[i] = g_calib[i];
+  return (int32_t)g_calib.size();
+}
+
+uint64_t dyna_kv_launch_count(void) { return g_launches.load(); }
+
+dyna_status dyna_kv_poll_error(void) { return take_device_error(); }
+
+size_t dyna_kv_pool_bytes(const dyna_kv_pool_desc* d) {
+  if (!desc_valid(d)) return 0;
+  return (size_t)d->num_layers * 2 * (size_t)d->num_blocks * d->block_size * (size_t)d->num_kv_heads *
+         d->head_dim * d->elem_bytes;
+}
+
+dyna_status dyna_kv_pool_create(const dyna_kv_pool_desc* desc, void* device_base, dyna_kv_pool_t* out) {
+  if (!out || !desc || !device_base) return fail(DYNA_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (!desc_valid(desc)) return fail(DYNA_EINVAL, "invalid pool descriptor");
+  const int64_t row = (int64_t)desc->num_kv_heads * desc->head_dim * desc->elem_bytes;
+  if (row % 16) return fail(DYNA_EGEOM, "row bytes H*d*e = %lld is not a multiple of 16", (long long)row);
+  if (reinterpret_cast<uintptr_t>(device_base) % 256) return fail(DYNA_EINVAL, "device_base not 256-B aligned");
+  if (!err_word()) return fail(DYNA_ECUDA, "cannot allocate mapped error word");
+  cudaPointerAttributes attr{};
+  CUDA_TRY(cudaPointerGetAttributes(&attr, device_base));
+  if (attr.type != cudaMemoryTypeDevice || attr.device != desc->device)
+    return fail(DYNA_EINVAL, "device_base is not device memory of device %d", desc->device);
+  auto* p = new dyna_kv_pool();
+  p->desc = *desc;
+  p->base = static_cast<char*>(device_base);
+  p->dev = desc->device;
+  p->row = row;
+  {
+    DeviceGuard g(desc->device);
+    if (cudaMalloc(&p->inbox, kInboxBytes) != cudaSuccess || cudaMemset(p->inbox, 0, kInboxBytes) != cudaSuccess) {
+      delete p;
+      return fail(DYNA_ENOMEM, "cannot allocate the %zu B chunk-flag inbox", kInboxBytes);
+    }
+  }
+  p->own_inbox = true;
+  dev_info(desc->device);
+  *out = p;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_pool_destroy(dyna_kv_pool_t p) {
+  if (!p) return fail(DYNA_EINVAL, "NULL pool");
+  {
+    DeviceGuard g(p->dev);
+    for (auto& kv : p->channels) {
+      for (auto& c : kv.second.counters) {
+        DeviceGuard g2(c.first);
+        cudaFree(c.second);
+      }
+      if (kv.second.sstage) {
+        DeviceGuard g2(kv.second.sdev);
+        cudaFree(kv.second.sstage);
+      }
+      if (kv.second.dstage) {
+        DeviceGuard g2(kv.second.ddev);
+        cudaFree(kv.second.dstage);
+      }
+    }
+    if (p->own_inbox) cudaFree(p->inbox);
+    if (p->imported) {
+      if (p->ipc_pool_map) cudaIpcCloseMemHandle(p->ipc_pool_map);
+      if (p->ipc_inbox_map) cudaIpcCloseMemHandle(p->ipc_inbox_map);
+    }
+  }
+  delete p;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_enable_peer(int32_t device, int32_t peer) { return ensure_peer(device, peer); }
+
+// ---------------------------------------------------------------- IPC
+typedef int (*PFN_cuMemGetAddressRange)(unsigned long long*, size_t*, unsigned long long);
+
+dyna_status dyna_kv_pool_export(dyna_kv_pool_t p, dyna_kv_ipc_handle* out) {
+  if (!p || !out) return fail(DYNA_EINVAL, "NULL argument");
+  if (p->imported) return fail(DYNA_EINVAL, "cannot re-export an imported pool");
+  std::memset(out, 0, sizeof *out);
+  DeviceGuard g(p->dev);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  CUDA_TRY(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+  if (!fn) return fail(DYNA_ENOTSUP, "cuMemGetAddressRange unavailable");
+  unsigned long long alloc_base = 0;
+  size_t alloc_size = 0;
+  if (reinterpret_cast<PFN_cuMemGetAddressRange>(fn)(&alloc_base, &alloc_size,
+                                                    reinterpret_cast<unsigned long long>(p->base)) != 0)
+    return fail(DYNA_ECUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h{};
+  CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(alloc_base)));
+  static_assert(sizeof(h) <= 64, "ipc handle size");
+  std::memcpy(out->pool_mem, &h, sizeof h);
+  out->pool_offset = reinterpret_cast<unsigned long long>(p->base) - alloc_base;
+  cudaIpcMemHandle_t hi{};
+  CUDA_TRY(cudaIpcGetMemHandle(&hi, p->inbox));
+  std::memcpy(out->inbox_mem, &hi, sizeof hi);
+  out->desc = p->desc;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_pool_import(const dyna_kv_ipc_handle* h, int32_t local_device, dyna_kv_pool_t* out) {
+  if (!h || !out) return fail(DYNA_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (!desc_valid(&h->desc)) return fail(DYNA_EINVAL, "invalid descriptor in handle");
+  DeviceGuard g(local_device);
+  cudaIpcMemHandle_t hp{}, hi{};
+  std::memcpy(&hp, h->pool_mem, sizeof hp);
+  std::memcpy(&hi, h->inbox_mem, sizeof hi);
+  void *mp = nullptr, *mi = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&mp, hp, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(DYNA_EPEER, "cudaIpcOpenMemHandle(pool): %s", cudaGetErrorString(e));
+  e = cudaIpcOpenMemHandle(&mi, hi, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaIpcCloseMemHandle(mp);
+    return fail(DYNA_EPEER, "cudaIpcOpenMemHandle(inbox): %s", cudaGetErrorString(e));
+  }
+  auto* p = new dyna_kv_pool();
+  p->desc = h->desc;
+  p->base = static_cast<char*>(mp) + h->pool_offset;
+  p->dev = local_device;
+  p->imported = true;
+  p->ipc_pool_map = mp;
+  p->ipc_inbox_map = mi;
+  p->inbox = static_cast<unsigned long long*>(mi);
+  p->row = (int64_t)h->desc.num_kv_heads * h->desc.head_dim * h->desc.elem_bytes;
+  if (!err_word()) {
+    dyna_kv_pool_destroy(p);
+    return fail(DYNA_ECUDA, "no error word");
+  }
+  dev_info(local_device);
+  *out = p;
+  return DYNA_OK;
+}
+
+// ---------------------------------------------------------------- test-input generator
+dyna_status dyna_kv_debug_fill(void* dst, uint64_t bytes, uint64_t seed, uint64_t byte_offset,
+                               struct CUstream_st* stream) {
+  if (!dst || bytes % 16 || byte_offset % 8 || reinterpret_cast<uintptr_t>(dst) % 16)
+    return fail(DYNA_EINVAL, "fill: dst 16-B aligned, bytes multiple of 16, offset multiple of 8");
+  if (bytes == 0) return DYNA_OK;
+  cudaPointerAttributes attr{};
+  CUDA_TRY(cudaPointerGetAttributes(&attr, dst));
+  const int dev = attr.device;
+  DeviceGuard g(dev);
+  const unsigned long long key = [](unsigned long long z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+  }(seed);
+  return launch_fill(dst, bytes, key, byte_offset / 8, dev, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,294 @@
+// runtime.cuh — internals of the host runtime behind include/dyna_kv.h, shared by
+// runtime.cu (devices, pools, IPC, calibration, upload ring), launch.cu (plans and
+// every kernel launch), migrate.cu (migrations, batches, completion) and
+// coupling.cu (producer-coupled ready boards, receiver-steered channels).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "dyna_kv.h"
+#include "plan.cuh"
+
+#define CUDA_TRY(expr)                                                                         \
+  do {                                                                                         \
+    cudaError_t e_ = (expr);                                                                   \
+    if (e_ != cudaSuccess) {                                                                   \
+      return fail(DYNA_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                                   \
+    }                                                                                          \
+  } while (0)
+
+namespace dynakv {
+namespace rt {
+
+// ---------------------------------------------------------------- errors, globals
+extern thread_local std::string g_err;
+dyna_status fail(dyna_status s, const char* fmt, ...);
+extern std::atomic<uint64_t> g_launches;
+extern std::mutex g_mu;
+extern unsigned int* g_err_word;
+unsigned int* err_word();
+dyna_status take_device_error();
+
+// copy-engine defaults (the calibration table overrides them per call size)
+constexpr int kVecU = 8;
+constexpr int kVecThreads = 256;
+constexpr int kVecPiece = 8192;
+constexpr int kBulkPiece = 32768;
+constexpr int kBulkStages = 6;
+constexpr int64_t kStageSlotBytes = 64ll << 20;  // staged variant: bytes per staging slot
+constexpr uint32_t kSchedSlots = 1u << 15;       // dynamic-scheduling counter slots per device
+constexpr size_t kInboxBytes = sizeof(unsigned long long) * DYNA_MAX_INSTANCES * DYNA_MAX_CHUNKS;
+
+// ------------------------------------------------------------------ upload ring
+// Host-resident inputs (block tables passed only as host_block_ids, batch
+// descriptors) travel to the device through a per-device ring: pinned host
+// staging -> one cudaMemcpyAsync on the caller's stream -> device buffer read
+// by the kernel that follows on the same stream.  A span is reused only after
+// the event recorded behind its consumer kernel has completed.
+constexpr size_t kRingBytes = 8u << 20;
+
+struct DeviceGuard {  // restores the caller's current device
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+struct DevInfo {
+  int sms = 0;
+  cudaStream_t aux = nullptr;  // library stream for destination-side kernels (staged, cross-device)
+  unsigned long long* sched = nullptr;  // [kSchedSlots][2] dynamic-scheduling counters, zero at rest
+  std::atomic<uint32_t> sched_seq{0};
+};
+
+// ============================================================== objects
+
+DevInfo* dev_info(int dev);
+cudaError_t get_event(int dev, cudaEvent_t* ev);
+void put_event(int dev, cudaEvent_t ev);
+bool desc_valid(const dyna_kv_pool_desc* d);
+int64_t gcd64(int64_t a, int64_t b);
+bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out);
+dyna_status ensure_peer(int dev, int peer);
+uint64_t next_epoch(int sender, const dyna_kv_pool* dst);
+dyna_status check_host_tables(const dyna_block_table& src, const dyna_block_table& dst, int64_t t0, int64_t t1);
+
+}  // namespace rt
+}  // namespace dynakv
+
+// ---------------------------------------------------------------- objects behind the opaque handles
+struct Channel {  // sender pool -> destination pool
+  std::map<int, unsigned long long*> counters;  // per kernel device: [DYNA_MAX_CHUNKS], zero at rest
+  char* sstage = nullptr;                      // staged variant: 2 slots on the source device
+  char* dstage = nullptr;                      // staged variant: 2 slots on the destination device
+  int64_t slot_bytes = 0;
+  int sdev = -1, ddev = -1;
+};
+
+struct dyna_kv_pool {
+  dyna_kv_pool_desc desc{};
+  char* base = nullptr;
+  int dev = 0;               // device on which `base` can be dereferenced
+  bool imported = false;
+  void* ipc_pool_map = nullptr;
+  void* ipc_inbox_map = nullptr;
+  unsigned long long* inbox = nullptr;  // [DYNA_MAX_INSTANCES][DYNA_MAX_CHUNKS]
+  bool own_inbox = false;
+  int64_t row = 0;
+  std::mutex mu;
+  std::map<const dyna_kv_pool*, Channel> channels;  // keyed by destination pool
+};
+
+struct dyna_kv_ready {
+  int dev = 0;
+  int32_t max_chunks = 0;
+  unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;  // per chunk wait
+  unsigned long long* slots = nullptr;  // device, zero-initialised
+  std::atomic<uint64_t> epoch{0};
+};
+
+struct dyna_kv_channel {
+  int dev = 0;                 // device on which `base` can be dereferenced
+  bool imported = false;
+  char* base = nullptr;        // [slots][slot_bytes] | full[slots] | credit[slots]
+  int32_t slots = 0;
+  uint64_t slot_bytes = 0;
+  int32_t sender = 0;
+  dyna_kv_pool_desc desc{};    // the receiver pool's geometry
+  dyna_kv_pool* dst = nullptr; // receiver side
+  unsigned long long* full = nullptr;
+  unsigned long long* credit = nullptr;
+  uint64_t push_seq = 0, place_seq = 0;  // next sub-chunk number on each side
+  unsigned long long* push_counters = nullptr;  // sender-device counters for the full-word release
+  int push_counters_dev = -1;
+  unsigned long long* place_counters = nullptr; // receiver-device counters for inbox chunk flags
+  std::mutex mu;
+};
+
+struct dyna_kv_xfer {
+  cudaEvent_t ev = nullptr;
+  bool captured = false;  // enqueued during CUDA-graph capture: the work runs at replay
+  int32_t variant = 0, engine = 0, piece = 0, stages = 0, unroll = 0, launches = 0;
+  int dev = 0;
+  bool empty = false;
+  uint64_t epoch = 0;
+  int32_t nchunks = 0;
+  int32_t sender = 0;
+};
+
+
+namespace dynakv {
+namespace rt {
+
+struct UploadRing {
+  char* host = nullptr;
+  char* dev = nullptr;
+  size_t head = 0;
+  struct Span {
+    size_t b, e;
+    cudaEvent_t ev;
+  };
+  std::deque<Span> live;
+  std::vector<cudaEvent_t> free_ev;
+  std::mutex mu;
+};
+
+
+extern std::mutex g_rings_mu;
+extern std::map<int, UploadRing*> g_rings;
+
+// Holds the ring's lock from upload() until finish() records the release event.
+class RingLease {
+ public:
+  explicit RingLease(int dev) : dev_(dev) {}
+  ~RingLease() {
+    if (ring_) ring_->mu.unlock();
+  }
+
+  // Reserve `bytes` of the ring: *hptr (pinned host) is filled by the caller,
+  // then copy() moves it to *dptr on the stream.  At most once per lease.
+  dyna_status reserve(size_t bytes, char** dptr, char** hptr, cudaStream_t st) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+      return fail(DYNA_ENOTSUP, "host-resident inputs cannot be captured in a CUDA graph "
+                                "(a replay would read recycled staging); pass device block_ids");
+    {
+      std::lock_guard<std::mutex> lk(g_rings_mu);
+      UploadRing*& r = g_rings[dev_];
+      if (!r) r = new UploadRing();
+      ring_ = r;
+    }
+    ring_->mu.lock();  // held until the lease is destroyed (after finish())
+    UploadRing& R = *ring_;
+    if (!R.host) {
+      DeviceGuard g(dev_);
+      if (cudaHostAlloc(&R.host, kRingBytes, cudaHostAllocPortable) != cudaSuccess ||
+          cudaMalloc(&R.dev, kRingBytes) != cudaSuccess)
+        return fail(DYNA_ENOMEM, "upload ring (%zu B pinned + device)", kRingBytes);
+    }
+    bytes = (bytes + 255) & ~size_t(255);
+    if (bytes > kRingBytes) return fail(DYNA_ENOMEM, "host-resident inputs of %zu B exceed the upload ring", bytes);
+    size_t b = R.head;
+    if (b + bytes > kRingBytes) b = 0;
+    const size_t e = b + bytes;
+    // free every live span that overlaps [b, e) (spans sit in allocation order)
+    while (!R.live.empty() && R.live.front().b < e && b < R.live.front().e) {
+      cudaEventSynchronize(R.live.front().ev);
+      R.free_ev.push_back(R.live.front().ev);
+      R.live.pop_front();
+    }
+    R.head = e;
+    span_b_ = b;
+    span_e_ = e;
+    *dptr = R.dev + b;
+    *hptr = R.host + b;
+    return DYNA_OK;
+  }
+
+  dyna_status copy(cudaStream_t st) {
+    UploadRing& R = *ring_;
+    CUDA_TRY(cudaMemcpyAsync(R.dev + span_b_, R.host + span_b_, span_e_ - span_b_, cudaMemcpyHostToDevice, st));
+    return DYNA_OK;
+  }
+
+  // After the consumer kernel(s) are enqueued on `st`.
+  dyna_status finish(cudaStream_t st) {
+    if (!ring_ || span_e_ == 0) return DYNA_OK;
+    UploadRing& R = *ring_;
+    cudaEvent_t ev = nullptr;
+    if (!R.free_ev.empty()) {
+      ev = R.free_ev.back();
+      R.free_ev.pop_back();
+    } else {
+      DeviceGuard g(dev_);
+      CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(ev, st));
+    R.live.push_back({span_b_, span_e_, ev});
+    span_e_ = 0;
+    return DYNA_OK;
+  }
+
+ private:
+  int dev_;
+  UploadRing* ring_ = nullptr;
+  size_t span_b_ = 0, span_e_ = 0;
+};
+
+struct Choice {
+  int variant, engine, piece, stages, unroll;
+};
+
+Side paged(const dyna_kv_pool* pool, const int32_t* ids);
+Side linear(char* base);
+dyna_status channel_counters(dyna_kv_pool* src, const dyna_kv_pool* dst, int kdev, unsigned long long** out);
+dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t slot, char** sbuf, char** dbuf);
+
+// launch.cu — the only translation unit that instantiates and launches kernels
+void preload_kernels();
+Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1, int l0, int lm, int64_t c,
+               int64_t g, int piece);
+dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev, cudaStream_t st,
+                        int schedule);
+dyna_status launch_batch(const BatchSource& src, int64_t n_items, int piece, int engine, int max_ctas, int stages,
+                         int unroll, int dev, cudaStream_t st, int schedule);
+dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st, int schedule);
+dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, const int32_t* dids, dyna_range tr,
+                       int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
+                       int max_ctas, cudaStream_t stream, dyna_kv_xfer* x, int schedule);
+void launch_wait_flag(const unsigned long long* flag, unsigned long long epoch, unsigned long long timeout_ns,
+                      cudaStream_t st);
+void launch_release_sys(unsigned long long* slot, unsigned long long v, cudaStream_t st);
+void launch_mark_ready(unsigned long long* slot, unsigned long long v, cudaStream_t st);
+dyna_status launch_fill(void* dst, uint64_t bytes, unsigned long long key, uint64_t first_word, int dev,
+                        cudaStream_t st);
+
+// migrate.cu
+dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream);
+dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o);
+dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
+                          int32_t chunk_tokens, bool* empty);
+dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D);
+Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok);
+size_t table_upload_bytes(const dyna_block_table& t, int64_t t1);
+
+}  // namespace rt
+}  // namespace dynakv
