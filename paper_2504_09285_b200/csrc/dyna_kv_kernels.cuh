@@ -28,6 +28,10 @@
 
 #include "plan.cuh"
 
+#ifndef DYNA_BULK_DEFER
+#define DYNA_BULK_DEFER 4  // stores committed after a chunk switch before its bytes are counted
+#endif
+
 namespace dynakv {
 
 struct Item {
@@ -400,7 +404,7 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, uns
   // once kDefer more stores have been committed after it, behind a
   // `cp.async.bulk.wait_group kDefer` (all older groups complete) — by then
   // they have normally landed, so the pipeline does not drain.
-  constexpr int kDefer = 4;
+  constexpr int kDefer = DYNA_BULK_DEFER;
   int32_t cur_k = -1, park_k = -1;
   uint32_t cur_acc = 0, park_acc = 0;
   int since_park = 0;

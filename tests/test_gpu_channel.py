@@ -45,6 +45,7 @@ def test_push_place_loopback(slots, slot_bytes, c, signal):
                 torch.cuda.synchronize()
                 assert sender == 9 and (flags.numpy() == epoch).all()
             dst.tensor.copy_(torch.from_numpy(hd).cuda())
+            torch.cuda.synchronize()   # torch side streams are non-blocking: finish the reset first
     finally:
         dk.dyna_kv_channel_destroy(ch)
 
