@@ -72,7 +72,7 @@ dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D) {
 
 // a6: unset choices come from the calibration table (measured GB/s per row
 // bytes, locality and call size), else FUSED + VEC.
-Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok) {
+Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok, int64_t run_bytes) {
   dyna_kv_calib_entry ce{};
   const bool calibrated =
       (o.variant == DYNA_VARIANT_AUTO || o.engine == DYNA_ENGINE_AUTO) && calib_lookup(row, peer, ntok, &ce);
@@ -85,6 +85,14 @@ Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok) {
                                                      : (c.engine == DYNA_ENGINE_VEC ? kVecPiece : kBulkPiece));
   c.stages = o.stages ? o.stages : (use_ce && ce.stages ? ce.stages : kBulkStages);
   c.unroll = o.unroll ? o.unroll : (use_ce && ce.unroll ? ce.unroll : kVecU);
+  if (!o.engine && c.engine != DYNA_ENGINE_VEC && run_bytes < kMinBulkRun) {
+    // a BULK item never spans two blocks; with short contiguous runs (e.g. one KV
+    // head per TP rank: 256-B rows, 4-KiB blocks) its single issuing thread is
+    // bound by items, not bytes (measured: 341 GB/s) — many warps do better
+    c.engine = DYNA_ENGINE_VEC;
+    c.unroll = kVecU;
+    if (!o.piece_bytes) c.piece = kVecPiece;
+  }
   return c;
 }
 
@@ -161,7 +169,7 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
   const int64_t c = chunk_tokens;
   const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
-  Choice ch = choose(o, row, peer_dst, ntok);
+  Choice ch = choose(o, row, peer_dst, ntok, std::min<int64_t>(gcd64(gs.block_size, gd.block_size), c) * row);
   if (signal && !o.engine && ch.engine != DYNA_ENGINE_VEC) {
     // measured (bench.py e2e, per-chunk flags on): the VEC engine's per-warp fences beat
     // draining bulk-store groups before each chunk's count (2720 vs 2540 GB/s)
@@ -288,7 +296,12 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   }
   x->dev = S0->dev;
   x->sender = S0->desc.instance;
-  Choice ch = choose(o, S0->row, peer, total_tok);
+  int64_t run_min = std::numeric_limits<int64_t>::max();  // shortest contiguous run in the batch
+  for (int32_t i : live)
+    run_min = std::min<int64_t>(run_min, std::min<int64_t>(gcd64(migs[i].src.pool->desc.block_size,
+                                                                  migs[i].dst.pool->desc.block_size),
+                                                            chunk_tokens) * S0->row);
+  Choice ch = choose(o, S0->row, peer, total_tok, run_min);
   if (!o.engine && ch.engine != DYNA_ENGINE_VEC) {
     // measured (scripts/batch_probe.py): with many plans the BULK engine's single issuing
     // thread is latency-bound on per-item plan lookups; the warp-parallel VEC engine is not

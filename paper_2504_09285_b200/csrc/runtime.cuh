@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <limits>
 #include <map>
 #include <mutex>
 #include <string>
@@ -49,6 +50,7 @@ constexpr int kVecThreads = 256;
 constexpr int kVecPiece = 8192;
 constexpr int kBulkPiece = 32768;
 constexpr int kBulkStages = 6;
+constexpr int64_t kMinBulkRun = 16384;  // AUTO never picks BULK below this contiguous run length
 constexpr int64_t kStageSlotBytes = 64ll << 20;  // staged variant: bytes per staging slot
 constexpr uint32_t kSchedSlots = 1u << 15;       // dynamic-scheduling counter slots per device
 constexpr size_t kInboxBytes = sizeof(unsigned long long) * DYNA_MAX_INSTANCES * DYNA_MAX_CHUNKS;
@@ -287,7 +289,7 @@ dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o);
 dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
                           int32_t chunk_tokens, bool* empty);
 dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D);
-Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok);
+Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok, int64_t run_bytes);
 size_t table_upload_bytes(const dyna_block_table& t, int64_t t1);
 
 }  // namespace rt

@@ -37,7 +37,8 @@ CANDIDATES = [  # (variant, engine, piece, stages, unroll)
     (F, W, 16384, 12, 0), (F, W, 32768, 6, 0), (F, W, 49152, 4, 0),
     (S, V, 8192, 0, 8), (S, B, 32768, 6, 0),
 ]
-GEOMS = {8192: kvgen.LLAMA2_7B, 2048: kvgen.LLAMA3_8B.with_(num_blocks=2048)}
+GEOMS = {8192: kvgen.LLAMA2_7B, 2048: kvgen.LLAMA3_8B.with_(num_blocks=2048),
+         256: kvgen.QWEN2_72B.with_(num_kv_heads=1, num_blocks=6144)}   # TP-8 shard: 1 KV head per rank
 CHUNKS = [16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
 
 
