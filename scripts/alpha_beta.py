@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2504_09285_b200.model import fit_alpha_beta  # noqa: E402
 
-LAYERS = {8192: 32, 2048: 32}
+LAYERS = {8192: 32, 2048: 32, 256: 80}
 
 
 def main():

@@ -193,3 +193,47 @@ def test_tp_sharded_rows(engine):
     src, dst = pool_from_host(g, hs), pool_from_host(g, hd)
     dk.dyna_kv_wait(dk.migrate(dev_table(src, ts), dev_table(dst, td), (5, 3999), (0, 8), 1024, engine=engine))
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
+
+
+def test_concurrent_host_threads():
+    """Eight host threads migrate different requests at once, each on its own stream, mixing device
+    tables, host-resident tables (upload ring), batches and signalling — bit-exact vs the oracle."""
+    import threading
+    g = Geom(2, 8, 128, 2, 16, 1600)
+    hs, hd = kvgen.fill_bytes(201, g.pool_bytes), kvgen.fill_bytes(202, g.pool_bytes)
+    lens = [700, 333, 1000, 64, 517, 1200, 90, 800]
+    tabs = kvgen.batch_tables(203, lens, g, g)
+    want = hd.copy()
+    for n, (ts, td) in zip(lens, tabs):
+        oracle.migrate(hs, g, ts, want, g, td, (0, n))
+    src, dst = pool_from_host(g, hs), pool_from_host(g, hd)
+    torch.cuda.synchronize()
+    errors = []
+
+    def worker(i):
+        try:
+            n, (ts, td) = lens[i], tabs[i]
+            stream = torch.cuda.Stream()
+            kind = i % 4
+            if kind == 1:
+                st, dt = host_table(src, ts), host_table(dst, td)
+            else:
+                st, dt = dev_table(src, ts), dev_table(dst, td)
+            torch.cuda.synchronize()
+            for rep in range(5):
+                if kind == 2:
+                    x = dk.dyna_kv_migrate_batch([(st, dt, (0, n))], (0, 2), 128, stream.cuda_stream, None)
+                else:
+                    x = dk.dyna_kv_migrate_ex(st, dt, (0, n), (0, 2), 100 + 7 * i, stream.cuda_stream,
+                                              dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if kind == 3 else 0))
+                dk.dyna_kv_wait(x)
+        except Exception as e:  # noqa: BLE001 — reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
