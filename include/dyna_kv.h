@@ -271,6 +271,9 @@ DYNA_API dyna_status dyna_kv_channel_export(dyna_kv_channel_t ch, dyna_kv_channe
 DYNA_API dyna_status dyna_kv_channel_import(const dyna_kv_channel_handle* h, int32_t local_device,
                                             dyna_kv_channel_t* out);
 DYNA_API dyna_status dyna_kv_channel_destroy(dyna_kv_channel_t ch);
+/* Device-side waits of push (credits) and place (full words) give up after this
+ * long (default 10 s) and report DYNA_ETIMEDOUT at dyna_kv_wait. */
+DYNA_API dyna_status dyna_kv_channel_set_timeout(dyna_kv_channel_t ch, uint64_t timeout_ns);
 /* Sender: push tokens x layers of `src` into the channel, chunk by chunk, on `stream` (source device). */
 DYNA_API dyna_status dyna_kv_push(dyna_block_table src, dyna_range token_range, dyna_range layer_range,
                                   int32_t chunk_tokens, dyna_kv_channel_t ch, struct CUstream_st* stream,

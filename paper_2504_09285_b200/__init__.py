@@ -40,7 +40,7 @@ EXPORTS = (
     "dyna_kv_xfer_plan", "dyna_kv_ready_create", "dyna_kv_ready_destroy", "dyna_kv_ready_begin",
     "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready", "dyna_kv_ready_set_timeout",
     "dyna_kv_channel_create", "dyna_kv_channel_export", "dyna_kv_channel_import", "dyna_kv_channel_destroy",
-    "dyna_kv_push", "dyna_kv_place",
+    "dyna_kv_push", "dyna_kv_place", "dyna_kv_channel_set_timeout",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -116,6 +116,7 @@ def _load():
         "dyna_kv_channel_export": (st, [vp, p(dyna_kv_channel_handle)]),
         "dyna_kv_channel_import": (st, [p(dyna_kv_channel_handle), ctypes.c_int32, p(vp)]),
         "dyna_kv_channel_destroy": (st, [vp]),
+        "dyna_kv_channel_set_timeout": (st, [vp, ctypes.c_uint64]),
         "dyna_kv_push": (st, [dyna_block_table, dyna_range, dyna_range, ctypes.c_int32, vp, vp, p(vp)]),
         "dyna_kv_place": (st, [vp, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32, vp, p(dyna_kv_opts),
                                p(vp)]),
@@ -251,6 +252,10 @@ def dyna_kv_channel_import(handle: bytes, local_device: int) -> int:
 
 def dyna_kv_channel_destroy(ch: int) -> None:
     _check(lib.dyna_kv_channel_destroy(ctypes.c_void_p(ch)))
+
+
+def dyna_kv_channel_set_timeout(ch: int, timeout_ns: int) -> None:
+    _check(lib.dyna_kv_channel_set_timeout(ctypes.c_void_p(ch), timeout_ns))
 
 
 def dyna_kv_push(src: dyna_block_table, token_range, layer_range, chunk_tokens: int, ch: int, stream: int = 0) -> int:

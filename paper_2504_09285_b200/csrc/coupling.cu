@@ -59,7 +59,6 @@ dyna_status dyna_kv_ready_mark(dyna_kv_ready_t b, int32_t chunk, uint64_t epoch,
 }
 
 // ---------------------------------------------------------------- receiver-steered placement channel
-static constexpr unsigned long long kChanWaitNs = 10ull * 1000 * 1000 * 1000;
 
 static int64_t chan_subchunk(const dyna_kv_channel* ch, int64_t row, int lm, int64_t c) {
   const int64_t tok = row * lm * 2;
@@ -96,6 +95,12 @@ dyna_status dyna_kv_channel_create(dyna_kv_pool_t dst, int32_t sender, int32_t s
   }
   dev_info(dst->dev);
   *out = ch;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_channel_set_timeout(dyna_kv_channel_t ch, uint64_t timeout_ns) {
+  if (!ch || timeout_ns == 0) return fail(DYNA_EINVAL, "bad argument");
+  ch->timeout_ns = timeout_ns;
   return DYNA_OK;
 }
 
@@ -237,7 +242,7 @@ dyna_status dyna_kv_push(dyna_block_table src, dyna_range tr, dyna_range lr, int
       const uint64_t q = ch->push_seq++;
       const int slot = (int)(q % ch->slots);
       if (q >= (uint64_t)ch->slots) {  // wait for the receiver's credit on this slot
-        launch_wait_flag(ch->credit + slot, q - ch->slots + 1, kChanWaitNs, stream);
+        launch_wait_flag(ch->credit + slot, q - ch->slots + 1, ch->timeout_ns, stream);
       }
       // gather straight into the receiver's slot; the last writer releases full[slot] = q + 1
       Plan p = make_plan(paged(S, src.block_ids), linear(ch->base + (size_t)slot * ch->slot_bytes), S->row, sa,
@@ -307,7 +312,7 @@ dyna_status dyna_kv_place(dyna_kv_channel_t ch, dyna_block_table dst, dyna_range
       const int64_t sb = std::min(sa + sc, b);
       const uint64_t q = ch->place_seq++;
       const int slot = (int)(q % ch->slots);
-      launch_wait_flag(ch->full + slot, q + 1, kChanWaitNs, stream);
+      launch_wait_flag(ch->full + slot, q + 1, ch->timeout_ns, stream);
       Plan p = make_plan(linear(ch->base + (size_t)slot * ch->slot_bytes), paged(D, dst.block_ids), D->row, sa, sb,
                          l0, lm, sb - sa, D->desc.block_size, kVecPiece);
       p.mig_t0 = tr.begin;

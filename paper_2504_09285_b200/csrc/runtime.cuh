@@ -139,6 +139,7 @@ struct dyna_kv_channel {
   unsigned long long* full = nullptr;
   unsigned long long* credit = nullptr;
   uint64_t push_seq = 0, place_seq = 0;  // next sub-chunk number on each side
+  unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;  // device-side waits
   unsigned long long* push_counters = nullptr;  // sender-device counters for the full-word release
   int push_counters_dev = -1;
   unsigned long long* place_counters = nullptr; // receiver-device counters for inbox chunk flags

@@ -27,6 +27,7 @@ def test_push_place_loopback(slots, slot_bytes, c, signal):
     oracle.migrate(hs, G, ts, want, G, td, tr)
     src, dst = pool_from_host(G, hs), pool_from_host(G, hd)
     ch = dk.dyna_kv_channel_create(dst.handle, 9, slots, slot_bytes)
+    dk.dyna_kv_channel_set_timeout(ch, 120_000_000_000)   # a slow shared box must not turn into ETIMEDOUT
     try:
         s_push, s_place = torch.cuda.Stream(), torch.cuda.Stream()
         # tables must outlive the enqueued work (dyna_block_table contract): keep them in variables
@@ -77,6 +78,7 @@ def _sender(handle, q):
         src = pool_from_host(G, kvgen.fill_bytes(1, G.pool_bytes), instance=3)
         ts, _ = kvgen.table_pair(7, 5000, G, G)
         ch = dk.dyna_kv_channel_import(handle, 0)
+        dk.dyna_kv_channel_set_timeout(ch, 120_000_000_000)
         q.put("ready")
         st = dev_table(src, ts)
         x = dk.dyna_kv_push(st, (0, 3000), (0, 4), 512, ch, torch.cuda.current_stream().cuda_stream)
@@ -94,6 +96,7 @@ def test_push_place_across_processes():
     oracle.migrate(hs, G, ts, want, G, td, (0, 3000))
     dst = pool_from_host(G, hd)
     ch = dk.dyna_kv_channel_create(dst.handle, 3, 8, 1 << 23)   # 8 x 8 MiB: the sender never waits for credit
+    dk.dyna_kv_channel_set_timeout(ch, 120_000_000_000)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     p = ctx.Process(target=_sender, args=(dk.dyna_kv_channel_export(ch), q))
