@@ -38,6 +38,16 @@ HBM_FALLBACK = 6650.0         # B200_PROFILING.md fallback (GB/s, read+write cop
 NVLINK_MEASURED = 770.0       # B200_PROFILING.md measured peer copy per direction (GB/s)
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def env_rank():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
             int(os.environ.get("LOCAL_RANK", 0)))
@@ -149,7 +159,8 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": WORKLOAD, "kv_dtype": "fp16"},
             "tokens_per_s": v * 1e9 / (2 * 32 * o.row),
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "host_cpus": os.cpu_count(), "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -355,7 +366,7 @@ def run_dyna(args, rank, world, local_rank):
         if world == 1 and not args.no_cpu_baseline:
             v, sample, dt = OracleSample().run(12.0)
             line["cpu_baseline"] = {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
-                                    "seconds": dt, "host_cpus": os.cpu_count()}
+                                    "seconds": dt, "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

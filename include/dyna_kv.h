@@ -112,7 +112,7 @@ typedef struct {
 typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
 
 /* Variant. */
-#define DYNA_VARIANT_AUTO   0  /* calibrated choice per (row bytes, chunk size) */
+#define DYNA_VARIANT_AUTO   0  /* calibrated choice per (row bytes, locality, call size) */
 #define DYNA_VARIANT_FUSED  1  /* one kernel: source rows -> destination rows (K4 / K4-local) */
 #define DYNA_VARIANT_STAGED 2  /* gather -> staging -> peer staging (+flag) -> scatter (K1, K2, K3) */
 /* Copy engine inside the kernels. */
@@ -134,7 +134,8 @@ typedef struct {
     int32_t schedule;   /* work distribution: 0 = default (static), DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC */
 } dyna_kv_opts;
 #define DYNA_SCHED_STATIC  1   /* round-robin items over a balanced persistent grid */
-#define DYNA_SCHED_DYNAMIC 2   /* workers grab items from a per-launch atomic counter (no static tail) */
+#define DYNA_SCHED_DYNAMIC 2   /* workers grab items from a per-launch atomic counter (measured slower than
+                                  static on B200; VEC only, kept as an option) */
 
 /* Calibration table used by DYNA_VARIANT_AUTO / DYNA_ENGINE_AUTO (SURVEY §8 a6:
  * "chosen over the staged variant per chunk size by measured bandwidth").
@@ -143,8 +144,12 @@ typedef struct {
  * GPU), and whose call size (tokens in token_range) <= max_chunk_tokens (in
  * the paper's per-chunk push, a call moves one chunk, so this is the
  * chunk size).  Entries for the exact row size are preferred over generic
- * ones; within each class the smallest covering max_chunk_tokens wins.  The library starts with the
- * table measured on B200 (profiles/), replaceable at run time. */
+ * ones; within each class the smallest covering max_chunk_tokens wins.  The
+ * library starts with the table measured on B200 (profiles/), replaceable at
+ * run time.  Two measured rules apply on top of the table when the engine is
+ * AUTO: no BULK engine when a contiguous run (min(gcd(bs_src, bs_dst),
+ * chunk_tokens) * row bytes) is shorter than 16 KiB, and the VEC engine when
+ * per-chunk flags are requested. */
 typedef struct {
     int32_t row_bytes;
     int32_t peer;
