@@ -65,6 +65,7 @@ typedef int32_t dyna_status;
 #define DYNA_ETIMEDOUT (-8)
 #define DYNA_EAGAIN    (-9)  /* dyna_kv_query: still in flight */
 #define DYNA_ENOTSUP   (-10)
+#define DYNA_ECANCELED (-11) /* dyna_kv_wait: the producer-coupled migration was cancelled (dyna_kv_ready_cancel) */
 
 /* Pool geometry.  All fields > 0 except device (a CUDA ordinal >= 0) and
  * instance (0 <= instance < DYNA_MAX_INSTANCES; the id this pool's owner uses
@@ -122,6 +123,7 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
 #define DYNA_ENGINE_BULK_WS 3  /* same ring, warp-specialised: a loader warp and a storer warp (mbarrier hand-off) */
 /* flags */
 #define DYNA_MIGRATE_SIGNAL 1  /* write a per-chunk flag into the destination pool's inbox */
+#define DYNA_READY_PER_LAYER 2 /* dyna_kv_migrate_on_ready: one ready mark per (chunk, layer), see below */
 
 typedef struct {
     int32_t variant;    /* DYNA_VARIANT_*  (0 = auto) */
@@ -239,11 +241,31 @@ DYNA_API dyna_status dyna_kv_ready_begin(dyna_kv_ready_t board, uint64_t* epoch)
 /* Enqueue on the producer's stream: slot[chunk] = epoch (release, GPU scope). */
 DYNA_API dyna_status dyna_kv_ready_mark(dyna_kv_ready_t board, int32_t chunk, uint64_t epoch,
                                         struct CUstream_st* producer_stream);
+/* Layer-granular marks (opts->flags & DYNA_READY_PER_LAYER; §4.3
+ * chunk-level transfer "can be composed with" layer-level transfer):
+ * the producer marks slot k*(l1-l0) + (l-l0) once layer l of chunk k has
+ * written its KV, and those rows move as soon as that mark is visible, while
+ * the prefill still computes the chunk's later layers.  The board then needs
+ * num_chunks*(l1-l0) slots.
+ * Cancellation (when r^alpha ends before s, "its
+ * transfer is aborted"): see dyna_kv_ready_cancel.  The board must outlive
+ * every migration launched on it (until dyna_kv_wait returns). */
 DYNA_API dyna_status dyna_kv_migrate_on_ready(dyna_block_table src, dyna_block_table dst,
                                               dyna_range token_range, dyna_range layer_range,
                                               int32_t chunk_tokens, dyna_kv_ready_t board, uint64_t epoch,
                                               struct CUstream_st* stream, const dyna_kv_opts* opts,
                                               dyna_kv_xfer_t* out);
+/* Cancel, from the host and with immediate effect, every migration on this
+ * board whose epoch is <= `epoch`.  A running migration stops waiting: a slot
+ * whose mark is visible when a warp reaches it is still copied (so every
+ * MARKED chunk is delivered whole, and its per-chunk flag is raised when
+ * signalling); the items of a slot whose mark is not visible are skipped, and
+ * a chunk with any skipped item never gets its flag.  dyna_kv_wait of a
+ * cancelled migration returns DYNA_ECANCELED; destination rows of chunks
+ * without a flag are unspecified (partially written), rows outside the
+ * token range are untouched as always.  Cancelling is monotone (an epoch
+ * below the board's current cancel epoch is a no-op). */
+DYNA_API dyna_status dyna_kv_ready_cancel(dyna_kv_ready_t board, uint64_t epoch);
 
 /* Receiver-steered placement across processes (the STAGED shape, SURVEY §8a
  * a2-a4; §4.3: "messages steering placement on the receiver

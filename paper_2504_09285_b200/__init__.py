@@ -21,13 +21,15 @@ LIB_PATH = os.environ.get("DYNA_KV_LIB") or os.path.join(_PKG, "libdyna_kv.so")
 # ---------------------------------------------------------------- constants (include/dyna_kv.h)
 DYNA_OK, DYNA_EINVAL, DYNA_EGEOM, DYNA_ERANGE, DYNA_EALIAS = 0, -1, -2, -3, -4
 DYNA_EPEER, DYNA_ENOMEM, DYNA_ECUDA, DYNA_ETIMEDOUT, DYNA_EAGAIN, DYNA_ENOTSUP = -5, -6, -7, -8, -9, -10
+DYNA_ECANCELED = -11
 STATUS_NAMES = {0: "DYNA_OK", -1: "DYNA_EINVAL", -2: "DYNA_EGEOM", -3: "DYNA_ERANGE", -4: "DYNA_EALIAS",
                 -5: "DYNA_EPEER", -6: "DYNA_ENOMEM", -7: "DYNA_ECUDA", -8: "DYNA_ETIMEDOUT", -9: "DYNA_EAGAIN",
-                -10: "DYNA_ENOTSUP"}
+                -10: "DYNA_ENOTSUP", -11: "DYNA_ECANCELED"}
 DYNA_MAX_INSTANCES, DYNA_MAX_CHUNKS = 64, 4096
 DYNA_VARIANT_AUTO, DYNA_VARIANT_FUSED, DYNA_VARIANT_STAGED = 0, 1, 2
 DYNA_ENGINE_AUTO, DYNA_ENGINE_VEC, DYNA_ENGINE_BULK, DYNA_ENGINE_BULK_WS = 0, 1, 2, 3
 DYNA_MIGRATE_SIGNAL = 1
+DYNA_READY_PER_LAYER = 2
 DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC = 1, 2
 
 # every symbol include/dyna_kv.h declares
@@ -40,7 +42,7 @@ EXPORTS = (
     "dyna_kv_xfer_plan", "dyna_kv_ready_create", "dyna_kv_ready_destroy", "dyna_kv_ready_begin",
     "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready", "dyna_kv_ready_set_timeout",
     "dyna_kv_channel_create", "dyna_kv_channel_export", "dyna_kv_channel_import", "dyna_kv_channel_destroy",
-    "dyna_kv_push", "dyna_kv_place", "dyna_kv_channel_set_timeout",
+    "dyna_kv_push", "dyna_kv_place", "dyna_kv_channel_set_timeout", "dyna_kv_ready_cancel",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -110,6 +112,7 @@ def _load():
         "dyna_kv_ready_begin": (st, [vp, p(ctypes.c_uint64)]),
         "dyna_kv_ready_set_timeout": (st, [vp, ctypes.c_uint64]),
         "dyna_kv_ready_mark": (st, [vp, ctypes.c_int32, ctypes.c_uint64, vp]),
+        "dyna_kv_ready_cancel": (st, [vp, ctypes.c_uint64]),
         "dyna_kv_migrate_on_ready": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
                                           vp, ctypes.c_uint64, vp, p(dyna_kv_opts), p(vp)]),
         "dyna_kv_channel_create": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, p(vp)]),
@@ -219,6 +222,16 @@ def dyna_kv_ready_begin(board: int) -> int:
 
 def dyna_kv_ready_mark(board: int, chunk: int, epoch: int, stream: int = 0) -> None:
     _check(lib.dyna_kv_ready_mark(ctypes.c_void_p(board), chunk, epoch, ctypes.c_void_p(stream)))
+
+
+def dyna_kv_ready_cancel(board: int, epoch: int) -> None:
+    _check(lib.dyna_kv_ready_cancel(ctypes.c_void_p(board), epoch))
+
+
+def ready_slot(chunk: int, layer: int, layer_range) -> int:
+    """Board slot of (chunk, layer) for DYNA_READY_PER_LAYER migrations (include/dyna_kv.h)."""
+    l0, l1 = layer_range
+    return chunk * (l1 - l0) + (layer - l0)
 
 
 def dyna_kv_migrate_on_ready(src: dyna_block_table, dst: dyna_block_table, token_range, layer_range,

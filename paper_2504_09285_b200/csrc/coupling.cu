@@ -19,9 +19,19 @@ dyna_status dyna_kv_ready_create(int32_t device, int32_t max_chunks, dyna_kv_rea
   DeviceGuard g(device);
   if (cudaMalloc(&b->slots, sizeof(unsigned long long) * max_chunks) != cudaSuccess ||
       cudaMemset(b->slots, 0, sizeof(unsigned long long) * max_chunks) != cudaSuccess) {
+    cudaFree(b->slots);
     delete b;
     return fail(DYNA_ENOMEM, "ready board of %d slots", max_chunks);
   }
+  if (cudaHostAlloc(&b->cancel_host, sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) !=
+          cudaSuccess ||
+      cudaHostGetDevicePointer(&b->cancel_dev, b->cancel_host, 0) != cudaSuccess) {
+    cudaFree(b->slots);
+    if (b->cancel_host) cudaFreeHost(b->cancel_host);
+    delete b;
+    return fail(DYNA_ENOMEM, "ready board cancel word");
+  }
+  __atomic_store_n(b->cancel_host, 0ull, __ATOMIC_RELEASE);
   dev_info(device);
   *out = b;
   return DYNA_OK;
@@ -32,6 +42,7 @@ dyna_status dyna_kv_ready_destroy(dyna_kv_ready_t b) {
   {
     DeviceGuard g(b->dev);
     cudaFree(b->slots);
+    cudaFreeHost(b->cancel_host);
   }
   delete b;
   return DYNA_OK;
@@ -46,6 +57,16 @@ dyna_status dyna_kv_ready_set_timeout(dyna_kv_ready_t b, uint64_t timeout_ns) {
 dyna_status dyna_kv_ready_begin(dyna_kv_ready_t b, uint64_t* epoch) {
   if (!b || !epoch) return fail(DYNA_EINVAL, "NULL argument");
   *epoch = ++b->epoch;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_ready_cancel(dyna_kv_ready_t b, uint64_t epoch) {
+  if (!b) return fail(DYNA_EINVAL, "NULL board");
+  unsigned long long cur = __atomic_load_n(b->cancel_host, __ATOMIC_ACQUIRE);
+  while (cur < epoch &&
+         !__atomic_compare_exchange_n(b->cancel_host, &cur, (unsigned long long)epoch, false, __ATOMIC_ACQ_REL,
+                                      __ATOMIC_ACQUIRE)) {
+  }
   return DYNA_OK;
 }
 

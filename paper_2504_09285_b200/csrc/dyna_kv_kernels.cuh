@@ -40,6 +40,7 @@ struct Item {
   uint32_t n;    // bytes to copy (multiple of 16); 0 = nothing to copy
   uint32_t acc;  // bytes this item accounts for in its chunk (== n unless skipped)
   int32_t k;     // chunk index within the migration
+  int32_t l;     // layer
 };
 
 __device__ __forceinline__ int64_t side_row(const Side& s, const Plan& p, int l, int kv, int64_t t,
@@ -52,7 +53,7 @@ __device__ __forceinline__ int64_t side_row(const Side& s, const Plan& p, int l,
 }
 
 __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
-  Item it{nullptr, nullptr, 0u, 0u, 0};
+  Item it{nullptr, nullptr, 0u, 0u, 0, 0};
   const int64_t k = item / p.items_per_chunk;
   int64_t i = item - k * p.items_per_chunk;
   const int32_t pp = (int32_t)(i % p.P); i /= p.P;
@@ -65,6 +66,7 @@ __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   const int64_t ta = max(a, G * p.g);
   const int64_t tb = min(b, (G + 1) * p.g);
   it.k = (int32_t)((a - p.mig_t0) / p.sig_c);
+  it.l = l;
   if (ta >= tb) return it;
   const int64_t run = (tb - ta) * p.row;
   const int64_t off = (int64_t)pp * p.piece;
@@ -84,6 +86,60 @@ __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   return it;
 }
 
+// Head-sliced decode (dyna_kv_migrate_heads): the same chunk / run grid as
+// decode_item, but a token's bytes are a slice of `p.row` bytes at byte col of a
+// row of pitch bytes, so a run is `rows` slices at a stride, not one contiguous
+// range.  piece p = tokens [ta + p*tpp, ...) of the run.
+struct SItem {
+  const char* src;
+  char* dst;
+  uint32_t rows;  // slices to copy; 0 = nothing
+  uint32_t acc;   // bytes this item accounts for in its chunk
+  int32_t k;
+  int32_t l;
+};
+
+__device__ __forceinline__ int64_t side_slice(const Side& s, const Plan& p, int l, int kv, int64_t t, int64_t a,
+                                              int64_t clen, int64_t pitch, int32_t col, bool& bad) {
+  if (s.linear) return (((int64_t)(l - p.l0) * 2 + kv) * clen + (t - a)) * p.row;  // packed slices
+  const int64_t jb = t / s.bs;
+  const int32_t b = __ldg(s.table + jb);
+  if (b < 0 || (int64_t)b >= s.nb) { bad = true; return 0; }
+  return ((((int64_t)l * 2 + kv) * s.nb + b) * s.bs + (t - jb * s.bs)) * pitch + col;
+}
+
+__device__ __forceinline__ SItem decode_item_sliced(const Plan& p, int64_t item) {
+  SItem it{nullptr, nullptr, 0u, 0u, 0, 0};
+  const int64_t k = item / p.items_per_chunk;
+  int64_t i = item - k * p.items_per_chunk;
+  const int32_t pp = (int32_t)(i % p.P); i /= p.P;
+  const int32_t j = (int32_t)(i % p.R);  i /= p.R;
+  const int kv = (int)(i & 1);
+  const int l = p.l0 + (int)(i >> 1);
+  const int64_t a = p.t0 + k * p.c;
+  const int64_t b = min(a + (int64_t)p.c, p.t1);
+  const int64_t G = a / p.g + j;
+  const int64_t ta = max(a, G * p.g);
+  const int64_t tb = min(b, (G + 1) * p.g);
+  it.k = (int32_t)((a - p.mig_t0) / p.sig_c);
+  it.l = l;
+  const int64_t ra = ta + (int64_t)pp * p.tpp;
+  if (ra >= tb) return it;
+  const uint32_t rows = (uint32_t)min((int64_t)p.tpp, tb - ra);
+  it.acc = rows * (uint32_t)p.row;
+  bool bad = false;
+  const int64_t so = side_slice(p.src, p, l, kv, ra, a, b - a, p.spitch, p.scol, bad);
+  const int64_t dO = side_slice(p.dst, p, l, kv, ra, a, b - a, p.dpitch, p.dcol, bad);
+  if (bad) {
+    if (p.err) atomicOr(p.err, ERR_BAD_BLOCK);
+    return it;
+  }
+  it.src = p.src.base + so;
+  it.dst = p.dst.base + dO;
+  it.rows = rows;
+  return it;
+}
+
 __device__ __forceinline__ void st_release_sys(unsigned long long* ptr, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ptr), "l"(v) : "memory");
 }
@@ -100,19 +156,25 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
 }
 
 // Producer coupling (§4.3, "once chunk k completes, its KV block
-// is immediately DMA-pushed"): block until the producer marked chunk k.
-__device__ __forceinline__ void wait_ready(const Plan& p, int32_t k) {
-  if (ld_acquire_gpu(p.ready + k) >= p.ready_epoch) return;
+// is immediately DMA-pushed"): block until the producer marked ready slot `slot`
+// (chunk k, or (chunk k, layer l) when marks are per layer).  Returns false when
+// the migration was cancelled before the mark became visible: the caller skips
+// the slot's items.  A visible mark always wins, so a marked slot is copied by
+// every warp that owns part of it.
+__device__ __forceinline__ bool wait_ready(const Plan& p, int32_t slot) {
+  if (ld_acquire_gpu(p.ready + slot) >= p.ready_epoch) return true;
   unsigned long long t0, now;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (ld_acquire_gpu(p.ready + k) < p.ready_epoch) {
+  while (ld_acquire_gpu(p.ready + slot) < p.ready_epoch) {
+    if (p.cancel && *p.cancel >= p.ready_epoch) return false;
     __nanosleep(500);
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     if (now - t0 > p.ready_timeout_ns) {  // never hang the device: report at dyna_kv_wait
       if (p.err) atomicOr(p.err, ERR_TIMEOUT);
-      return;
+      return true;
     }
   }
+  return true;
 }
 
 // Bytes of global chunk k of the whole migration.
@@ -129,13 +191,14 @@ __device__ __forceinline__ void fence_for(const Plan& p) {
 // Called by ONE thread once an item's bytes are complete and visible at
 // the destination's scope (the caller fenced).  The thread that closes chunk k resets
 // the counter (self-cleaning channel) and releases the flag.
-__device__ __forceinline__ void account_chunk(const Plan& p, int32_t k, uint32_t n) {
+__device__ __forceinline__ void account_chunk(const Plan& p, int32_t k, unsigned long long n) {
   if (n == 0) return;
   unsigned long long* ctr = p.counters + k;
   const unsigned long long total = chunk_bytes(p, k);
-  const unsigned long long old = atomicAdd(ctr, (unsigned long long)n);
-  if (old + n == total) {
+  const unsigned long long now = atomicAdd(ctr, n) + n;
+  if ((now & kCountMask) == total) {
     *ctr = 0ull;
+    if (now >= kPoison) return;  // a part of the chunk was skipped (cancelled): no flag
     __threadfence_system();
     st_release_sys(p.flags + k, p.epoch);
   }
@@ -259,6 +322,66 @@ __device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __
   }
 }
 
+// A warp copies `rows` slices of p.row bytes (16-B vectors), source rows p.spitch
+// apart, destination rows p.dpitch apart: lane-major over the flattened vector
+// index, U loads in flight per lane.
+template <int U>
+__device__ __forceinline__ void warp_copy_rows(const char* __restrict__ src, char* __restrict__ dst, uint32_t rows,
+                                               const Plan& p, int lane) {
+  const uint32_t vps = (uint32_t)p.vps;
+  const uint32_t nv = rows * vps;
+  const int sh = p.vps_shift;
+  for (uint32_t base = 0; base < nv; base += 32 * U) {
+    int4 v[U];
+    uint32_t r[U], c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t idx = base + u * 32 + lane;
+      r[u] = sh >= 0 ? (idx >> sh) : idx / vps;
+      c[u] = idx - r[u] * vps;
+      if (idx < nv)
+        v[u] = ld_nc_v4(reinterpret_cast<const int4*>(src + (int64_t)r[u] * p.spitch + (int64_t)c[u] * 16));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t idx = base + u * 32 + lane;
+      if (idx < nv) st_v4(reinterpret_cast<int4*>(dst + (int64_t)r[u] * p.dpitch + (int64_t)c[u] * 16), v[u]);
+    }
+  }
+}
+
+// Head-sliced fused copy (dyna_kv_migrate_heads): one warp per item, static
+// round-robin over a balanced persistent grid, per-(warp, chunk) signalling as
+// in k_copy_vec.
+template <int U, bool SIGNAL>
+__global__ void __launch_bounds__(256, 3) k_copy_rows(const Plan p) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int32_t cur_k = -1;
+  uint32_t cur_acc = 0;
+  for (int64_t item = warp; item < p.n_items; item += nwarps) {
+    const SItem it = decode_item_sliced(p, item);
+    if (SIGNAL && it.acc && it.k != cur_k) {
+      if (cur_acc) {
+        fence_for(p);
+        __syncwarp();
+        if (lane == 0) account_chunk(p, cur_k, cur_acc);
+      }
+      cur_k = it.k;
+      cur_acc = 0;
+    }
+    if (it.rows) warp_copy_rows<U>(it.src, it.dst, it.rows, p, lane);
+    if (SIGNAL) cur_acc += it.acc;
+  }
+  if (SIGNAL && cur_acc) {
+    fence_for(p);
+    __syncwarp();
+    if (lane == 0) account_chunk(p, cur_k, cur_acc);
+  }
+}
+
 template <int U, bool SIGNAL, class Src, bool READY = false>
 __global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : 3) k_copy_vec(const Src src, unsigned long long* sched_ctr) {
   pdl_enter();
@@ -271,8 +394,9 @@ __global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : 3) k_copy_vec(co
   // order), so bytes are accumulated per chunk and fenced + counted once when
   // the warp moves on to another chunk — one fence per (warp, chunk), not per item.
   int32_t cur_k = -1;
-  uint32_t cur_acc = 0;
-  int32_t ready_k = -1;
+  unsigned long long cur_acc = 0;  // bytes of chunk cur_k, plus kPoison once if any of them was skipped
+  int32_t ready_slot = -1;
+  bool skip = false;      // READY: the current ready slot was cancelled
   const int64_t n_items = src.total();
   for (;;) {
     long long gi = 0;
@@ -291,10 +415,18 @@ __global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : 3) k_copy_vec(co
       cur_k = it.k;
       cur_acc = 0;
     }
-    if (READY && it.acc && it.k != ready_k) {  // warp-uniform
-      if (lane == 0) wait_ready(p, it.k);
-      __syncwarp();
-      ready_k = it.k;
+    if (READY && it.acc) {
+      const int32_t slot = p.ready_layers ? it.k * p.lm + (it.l - p.l0) : it.k;
+      if (slot != ready_slot) {  // warp-uniform
+        int go = 1;
+        if (lane == 0) go = wait_ready(p, slot) ? 1 : 0;
+        skip = __shfl_sync(0xffffffffu, go, 0) == 0;
+        ready_slot = slot;
+      }
+    }
+    if (READY && skip) {  // cancelled before this slot was marked: count it poisoned, copy nothing
+      if (SIGNAL) cur_acc = (cur_acc | kPoison) + it.acc;  // poison at most once per (warp, chunk)
+      continue;
     }
     if (it.n) warp_copy<U, !READY>(it.src, it.dst, it.n, lane);
     if (SIGNAL) cur_acc += it.acc;

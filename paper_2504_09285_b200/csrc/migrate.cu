@@ -28,7 +28,7 @@ dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream) {
 dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
   *o = dyna_kv_opts{};
   if (opts) *o = *opts;
-  if (o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > 3 || o->max_ctas < 0 || o->piece_bytes < 0 ||
+  if ((o->flags & ~(DYNA_MIGRATE_SIGNAL | DYNA_READY_PER_LAYER)) != 0 || o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > 3 || o->max_ctas < 0 || o->piece_bytes < 0 ||
       o->piece_bytes % 16 || o->stages < 0 || o->stages == 1 || o->stages > kMaxStages ||
       (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16) || o->schedule < 0 ||
       o->schedule > DYNA_SCHED_DYNAMIC)
@@ -149,10 +149,14 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks, DYNA_MAX_CHUNKS);
   if (board) {
     if (board->dev != src.pool->dev) return fail(DYNA_EINVAL, "ready board must live on the source device");
-    if (nchunks > board->max_chunks)
-      return fail(DYNA_ERANGE, "%lld chunks > the ready board's %d slots", (long long)nchunks, board->max_chunks);
+    const int64_t nslots = nchunks * ((o.flags & DYNA_READY_PER_LAYER) ? (lr.end - lr.begin) : 1);
+    if (nslots > board->max_chunks)
+      return fail(DYNA_ERANGE, "%lld ready slots (chunks%s) > the ready board's %d", (long long)nslots,
+                  (o.flags & DYNA_READY_PER_LAYER) ? " x layers" : "", board->max_chunks);
     if (o.variant == DYNA_VARIANT_STAGED || (o.engine && o.engine != DYNA_ENGINE_VEC))
       return fail(DYNA_ENOTSUP, "producer-coupled migration: FUSED variant, VEC engine only");
+  } else if (o.flags & DYNA_READY_PER_LAYER) {
+    return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board (dyna_kv_migrate_on_ready)");
   }
   if (empty) {  // s = 0 (or no layers) -> nothing to ship, nothing enqueued
     auto* x = new dyna_kv_xfer();
@@ -231,6 +235,10 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
       p.ready = board->slots;
       p.ready_epoch = ready_epoch;
       p.ready_timeout_ns = board->timeout_ns;
+      p.ready_layers = (o.flags & DYNA_READY_PER_LAYER) ? 1 : 0;
+      p.cancel = board->cancel_dev;
+      x->board = board;
+      x->ready_epoch = ready_epoch;
       r = launch_ready(p, o.max_ctas, S->dev, stream, o.schedule);
     } else {
       r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream, o.schedule);
@@ -402,6 +410,8 @@ dyna_status dyna_kv_wait(dyna_kv_xfer_t x) {
     if (e != cudaSuccess) r = fail(DYNA_ECUDA, "migration failed: %s", cudaGetErrorString(e));
     put_event(x->dev, x->ev);
     if (!r) r = take_device_error();
+    if (!r && x->board && __atomic_load_n(x->board->cancel_host, __ATOMIC_ACQUIRE) >= x->ready_epoch)
+      r = fail(DYNA_ECANCELED, "migration cancelled (dyna_kv_ready_cancel)");
   }
   delete x;
   return r;

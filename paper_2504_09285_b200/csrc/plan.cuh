@@ -42,9 +42,24 @@ struct Plan {
   const unsigned long long* ready;
   unsigned long long ready_epoch;
   unsigned long long ready_timeout_ns;  // give up (ERR_TIMEOUT) after this long without the mark
+  int32_t ready_layers;     // 0: one mark per chunk (slot k); 1: one per (chunk, layer) (slot k*lm + l-l0)
+  // cancellation of a producer-coupled migration (nullptr: none): once *cancel >= ready_epoch,
+  // chunks whose mark is not visible are skipped (mapped host word, written by dyna_kv_ready_cancel)
+  const volatile unsigned long long* cancel;
+  // head-sliced rows (dyna_kv_migrate_heads; k_copy_vec<..., SLICED>): `row` is then the
+  // slice of n_heads*d*e bytes moved per token, found at byte `col` of a pitch-byte row
+  int64_t spitch, dpitch;   // bytes between consecutive tokens' rows (paged side: H*d*e of that pool)
+  int32_t scol, dcol;       // byte offset of the slice inside a row
+  int32_t tpp;              // tokens per work item
+  int32_t vps, vps_shift;   // 16-B vectors per slice; log2(vps) or -1
 };
 
 enum : unsigned { ERR_BAD_BLOCK = 1u, ERR_TIMEOUT = 2u };
+
+// A skipped (cancelled) item adds its bytes plus this poison to its chunk's
+// counter: the counter still completes and self-resets, but no flag is raised.
+constexpr unsigned long long kPoison = 1ull << 48;
+constexpr unsigned long long kCountMask = kPoison - 1;
 
 constexpr int kMaxStages = 16;  // BULK ring depth limit
 

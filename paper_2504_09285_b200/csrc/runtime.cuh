@@ -125,6 +125,8 @@ struct dyna_kv_ready {
   unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;  // per chunk wait
   unsigned long long* slots = nullptr;  // device, zero-initialised
   std::atomic<uint64_t> epoch{0};
+  unsigned long long* cancel_host = nullptr;  // mapped pinned word: migrations with epoch <= *cancel stop
+  unsigned long long* cancel_dev = nullptr;   // its device alias
 };
 
 struct dyna_kv_channel {
@@ -155,6 +157,8 @@ struct dyna_kv_xfer {
   uint64_t epoch = 0;
   int32_t nchunks = 0;
   int32_t sender = 0;
+  dyna_kv_ready* board = nullptr;  // producer-coupled: the board (for cancellation at dyna_kv_wait)
+  uint64_t ready_epoch = 0;
 };
 
 

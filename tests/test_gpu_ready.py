@@ -144,3 +144,174 @@ def test_first_mark_during_wait_does_not_deadlock():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", _FRESH.format(root=root)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------- layer-granular marks
+
+def _oracle_expect(fresh_seed, g, ts, dst_seed, td, tr, lr=None, rows=None):
+    """Destination bytes the oracle computes from the fresh source values (host numpy)."""
+    import oracle
+    hs = kvgen.fill_bytes(fresh_seed, g.pool_bytes)
+    want = kvgen.fill_bytes(dst_seed, g.pool_bytes)
+    oracle.migrate(hs, g, ts, want, g, td, tr, lr)
+    return want
+
+
+@pytest.mark.parametrize("c", [64, 100])
+def test_per_layer_marks_copy_each_layer_after_its_mark(c):
+    """The producer rewrites layer l of chunk k, then marks slot k*lm + l; every row must
+    arrive with the rewritten (fresh) bytes, bit-exact against the oracle."""
+    g = Geom(4, 8, 128, 2, 16, 200)
+    s, lm = 700, 4
+    src, dst, fresh = pool_filled(g, 1), pool_filled(g, 2), pool_filled(g, 3)
+    ts, td = kvgen.table_pair(6, 800, g, g)
+    src_t, dst_t, fresh_t = dev_table(src, ts), dev_table(dst, td), dev_table(fresh, ts)
+    prod, mig = torch.cuda.Stream(), torch.cuda.Stream()
+    nck = -(-s // c)
+    board = dk.dyna_kv_ready_create(0, nck * lm)
+    dk.dyna_kv_ready_set_timeout(board, 20_000_000_000)
+    try:
+        o = dk.opts(max_ctas=8, flags=dk.DYNA_MIGRATE_SIGNAL | dk.DYNA_READY_PER_LAYER)
+        e0 = dk.dyna_kv_ready_begin(board)           # warm-up pass: every path runs once
+        for k in range(nck * lm):
+            dk.dyna_kv_ready_mark(board, k, e0, prod.cuda_stream)
+        prod.synchronize()
+        dk.dyna_kv_wait(dk.dyna_kv_migrate_on_ready(src_t, dst_t, (0, s), (0, lm), c, board, e0, mig.cuda_stream, o))
+        dk.dyna_kv_wait(dk.dyna_kv_migrate_ex(fresh_t, src_t, (0, 1), (0, 1), 1, prod.cuda_stream, None))
+        src = pool_filled(g, 1)
+        dst = pool_filled(g, 2)
+        src_t, dst_t = dev_table(src, ts), dev_table(dst, td)
+        torch.cuda.synchronize()
+
+        epoch = dk.dyna_kv_ready_begin(board)
+        x = dk.dyna_kv_migrate_on_ready(src_t, dst_t, (0, s), (0, lm), c, board, epoch, mig.cuda_stream, o)
+        info = dk.dyna_kv_xfer_info(x)
+        px = []
+        for k in range(nck):
+            a, b = k * c, min((k + 1) * c, s)
+            for l in range(lm):                       # layer l of chunk k: compute, write KV, mark
+                with torch.cuda.stream(prod):
+                    torch.cuda._sleep(200_000)
+                px.append(dk.dyna_kv_migrate_ex(fresh_t, src_t, (a, b), (l, l + 1), b - a, prod.cuda_stream, None))
+                dk.dyna_kv_ready_mark(board, dk.ready_slot(k, l, (0, lm)), epoch, prod.cuda_stream)
+        dk.dyna_kv_wait(x)
+        for y in px:
+            dk.dyna_kv_wait(y)
+        torch.cuda.synchronize()
+        want = _oracle_expect(3, g, ts, 2, td, (0, s))
+        assert np.array_equal(dst.tensor.cpu().numpy(), want)
+        flags = torch.zeros(nck, dtype=torch.int64).pin_memory()
+        dk.dyna_kv_copy_flags(dst.handle, info[2], 0, nck, flags.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert int(flags.min()) == info[0]
+    finally:
+        dk.dyna_kv_ready_destroy(board)
+
+
+def test_per_layer_errors():
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(1, 256, g, g)
+    board = dk.dyna_kv_ready_create(0, 7)
+    try:
+        with pytest.raises(dk.DynaKVError) as e:       # 4 chunks x 2 layers > 7 slots
+            dk.dyna_kv_migrate_on_ready(dev_table(src, ts), dev_table(dst, td), (0, 100), (0, 2), 32, board, 1,
+                                        opts=dk.opts(flags=dk.DYNA_READY_PER_LAYER))
+        assert e.value.status == dk.DYNA_ERANGE
+        with pytest.raises(dk.DynaKVError) as e:       # per-layer marks need a board
+            dk.dyna_kv_migrate_ex(dev_table(src, ts), dev_table(dst, td), (0, 100), (0, 2), 32, 0,
+                                  dk.opts(flags=dk.DYNA_READY_PER_LAYER))
+        assert e.value.status == dk.DYNA_EINVAL
+        with pytest.raises(dk.DynaKVError) as e:       # unknown flag bits
+            dk.dyna_kv_migrate_ex(dev_table(src, ts), dev_table(dst, td), (0, 100), (0, 2), 32, 0, dk.opts(flags=8))
+        assert e.value.status == dk.DYNA_EINVAL
+    finally:
+        dk.dyna_kv_ready_destroy(board)
+
+
+# ---------------------------------------------------------------- cancellation (SPEC S:61, S:439)
+
+@pytest.mark.parametrize("per_layer", [False, True])
+def test_cancel_delivers_marked_chunks_and_stops(per_layer):
+    """alpha ends early: chunks 0..m-1 were marked, the rest never will be.  After the cancel the
+    migration returns at once with DYNA_ECANCELED; marked chunks are delivered whole with their
+    flags, unmarked chunks have no flag, rows outside the range are untouched, and the channel's
+    per-chunk counters are clean for the next signalled migration."""
+    import time
+    g = Geom(2, 8, 128, 2, 16, 160)
+    s, c, m = 900, 128, 3
+    lm = g.num_layers
+    nck = -(-s // c)
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(7, 1000, g, g)
+    src_t, dst_t = dev_table(src, ts), dev_table(dst, td)
+    prod, mig = torch.cuda.Stream(), torch.cuda.Stream()
+    board = dk.dyna_kv_ready_create(0, nck * lm)
+    dk.dyna_kv_ready_set_timeout(board, 30_000_000_000)   # a cancel must not wait for this
+    flags = dk.DYNA_MIGRATE_SIGNAL | (dk.DYNA_READY_PER_LAYER if per_layer else 0)
+    try:
+        epoch = dk.dyna_kv_ready_begin(board)
+        x = dk.dyna_kv_migrate_on_ready(src_t, dst_t, (0, s), (0, lm), c, board, epoch, mig.cuda_stream,
+                                        dk.opts(max_ctas=8, flags=flags))
+        ep, nchunks, sender = dk.dyna_kv_xfer_info(x)
+        for k in range(m):
+            for l in (range(lm) if per_layer else [0]):
+                dk.dyna_kv_ready_mark(board, dk.ready_slot(k, l, (0, lm)) if per_layer else k, epoch,
+                                      prod.cuda_stream)
+        prod.synchronize()
+        time.sleep(0.05)
+        t = time.perf_counter()
+        dk.dyna_kv_ready_cancel(board, epoch)
+        with pytest.raises(dk.DynaKVError) as e:
+            dk.dyna_kv_wait(x)
+        assert e.value.status == dk.DYNA_ECANCELED
+        assert time.perf_counter() - t < 5.0
+        torch.cuda.synchronize()
+        fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
+        dk.dyna_kv_copy_flags(dst.handle, sender, 0, nck, fl.data_ptr(), 0)
+        torch.cuda.synchronize()
+        got = fl.numpy()
+        assert (got[:m] == ep).all() and (got[m:] < ep).all(), got
+        want = _oracle_expect(1, g, ts, 2, td, (0, m * c))
+        D = dst.tensor.cpu().numpy()
+        marked = mapped_mask(g, [(td, (0, m * c))]).cpu().numpy()
+        rows = D.reshape(marked.shape + (-1,))
+        assert np.array_equal(rows[marked], want.reshape(rows.shape)[marked])        # delivered chunks
+        assert untouched_equal(dst, 2, mapped_mask(g, [(td, (0, s))]))                 # outside the range
+        # the next signalled migration over the same (src, dst) channel gets every flag
+        dst2_seed = 2
+        y = dk.dyna_kv_migrate_ex(src_t, dst_t, (0, s), (0, lm), c, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL))
+        ep2 = dk.dyna_kv_xfer_info(y)[0]
+        dk.dyna_kv_wait(y)
+        dk.dyna_kv_copy_flags(dst.handle, sender, 0, nck, fl.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert (fl.numpy() == ep2).all()
+        assert np.array_equal(dst.tensor.cpu().numpy(), _oracle_expect(1, g, ts, dst2_seed, td, (0, s)))
+    finally:
+        dk.dyna_kv_ready_destroy(board)
+
+
+def test_cancel_before_launch_and_later_epochs_unaffected():
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(1, 256, g, g)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    board = dk.dyna_kv_ready_create(0, 8)
+    try:
+        dk.dyna_kv_ready_set_timeout(board, 30_000_000_000)
+        e1 = dk.dyna_kv_ready_begin(board)
+        dk.dyna_kv_ready_cancel(board, e1)
+        x = dk.dyna_kv_migrate_on_ready(st, dt, (0, 100), (0, 2), 32, board, e1)   # nothing marked
+        with pytest.raises(dk.DynaKVError) as e:
+            dk.dyna_kv_wait(x)
+        assert e.value.status == dk.DYNA_ECANCELED
+        torch.cuda.synchronize()
+        assert np.array_equal(dst.tensor.cpu().numpy(), kvgen.fill_bytes(2, g.pool_bytes))   # untouched
+        dk.dyna_kv_ready_cancel(board, 0)                                           # monotone: no-op
+        e2 = dk.dyna_kv_ready_begin(board)
+        for k in range(4):
+            dk.dyna_kv_ready_mark(board, k, e2)
+        dk.dyna_kv_wait(dk.dyna_kv_migrate_on_ready(st, dt, (0, 100), (0, 2), 32, board, e2))
+        assert np.array_equal(dst.tensor.cpu().numpy(), _oracle_expect(1, g, ts, 2, td, (0, 100)))
+    finally:
+        dk.dyna_kv_ready_destroy(board)
