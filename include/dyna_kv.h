@@ -193,6 +193,29 @@ DYNA_API dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table d
                                int32_t chunk_tokens, struct CUstream_st* stream,
                                const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
 
+/* Head resharding between tensor-parallel instances of different degree
+ * (§5 P:595-596 deploys r^alpha and r^beta as TP
+ * groups).  A TP-sharded instance keeps, per rank, a pool of its own heads;
+ * when the sender's and receiver's TP degrees differ, a rank pair exchanges
+ * only some heads of every row.  This call moves, for every layer in
+ * layer_range, K and V, token in token_range, the KV heads
+ * [src_heads.begin, src_heads.end) of the source row (reached through the
+ * source table) into heads [dst_head_begin, dst_head_begin + n) of the
+ * destination row (reached through the destination table); every other head
+ * of the destination row, and every other row, is untouched.  Pools must agree
+ * on L, d and e; H may differ.  The head slice (n*d*e bytes) and d*e must be
+ * multiples of 16.  When both slices are whole rows (n == H_src == H_dst) this
+ * is dyna_kv_migrate_ex.  Otherwise: FUSED variant, VEC engine (DYNA_ENOTSUP
+ * for others); per-chunk signalling (DYNA_MIGRATE_SIGNAL) as for
+ * dyna_kv_migrate_ex, with a chunk's bytes counted as its slices.  An empty
+ * head range is an empty migration.  Errors as dyna_kv_migrate_ex, plus
+ * DYNA_ERANGE for head ranges outside either pool. */
+DYNA_API dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst,
+                                           dyna_range token_range, dyna_range layer_range,
+                                           dyna_range src_heads, int32_t dst_head_begin,
+                                           int32_t chunk_tokens, struct CUstream_st* stream,
+                                           const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
+
 /* Many migrations in ONE kernel launch (a batch of short
  * requests, e.g. configs[2]'s 64-request skewed batch).  Every non-empty entry
  * is validated like dyna_kv_migrate; all sources must live on one device (the

@@ -54,6 +54,8 @@ def lib():
         L.oracle_migrate_chunked.argtypes = [u8p, gp, i32p, u8p, gp, i32p, i64, i64, i64, i64,
                                              i64, i64p, i64, u8p]
         L.oracle_migrate_chunked.restype = None
+        L.oracle_migrate_heads.argtypes = [u8p, gp, i32p, u8p, gp, i32p, i64, i64, i64, i64, i64, i64, i64]
+        L.oracle_migrate_heads.restype = None
         _lib = L
     return _lib
 
@@ -118,3 +120,20 @@ def migrate_chunked(Ps, gs, Ts, Pd, gd, Td, token_range, layer_range, chunk_toke
                                  token_range[0], token_range[1], layer_range[0], layer_range[1],
                                  chunk_tokens, order.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                  len(order), _u8(staging))
+
+
+def migrate_heads(Ps: np.ndarray, gs, Ts, Pd: np.ndarray, gd, Td, token_range, layer_range, src_heads,
+                  dst_head_begin: int) -> None:
+    """In-place: Pd <- the head-restricted definition (dyna_kv_oracle.c oracle_migrate_heads)."""
+    layer_range = layer_range or (0, gs.num_layers)
+    assert Ps.nbytes == pool_bytes(gs) and Pd.nbytes == pool_bytes(gd)
+    for a in ("num_layers", "head_dim", "elem_bytes"):
+        assert getattr(gs, a) == getattr(gd, a), a
+    h0, h1 = src_heads
+    assert 0 <= h0 <= h1 <= gs.num_kv_heads and 0 <= dst_head_begin and dst_head_begin + h1 - h0 <= gd.num_kv_heads
+    if token_range[1] > token_range[0]:
+        assert len(Ts) * gs.block_size >= token_range[1] and len(Td) * gd.block_size >= token_range[1]
+    ts, tsp = _i32(Ts)
+    td, tdp = _i32(Td)
+    lib().oracle_migrate_heads(_u8(Ps), ctypes.byref(geom(gs)), tsp, _u8(Pd), ctypes.byref(geom(gd)), tdp,
+                               token_range[0], token_range[1], layer_range[0], layer_range[1], h0, h1, dst_head_begin)

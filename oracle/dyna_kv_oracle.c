@@ -29,6 +29,11 @@
  * source into a contiguous buffer, then place it through the destination
  * table) for any chunk size and any chunk order; it exists so the tests can
  * pin that chunking does not change the result.
+ * oracle_migrate_heads() is the same definition restricted to a run of KV
+ * heads, for instances of different tensor-parallel degree (§5
+ * P:595-596 deploys r^alpha / r^beta as TP groups): the
+ * source heads [h0,h1) land in destination heads [hd0, hd0 + h1 - h0), every
+ * other head untouched (reading R14).
  *
  * No blocking, fusion or reordering: loops run in the order of the
  * definition.  Copies are bitwise (reading R8), so NaN payloads, -0 and
@@ -121,4 +126,24 @@ void oracle_migrate_chunked(const uint8_t* Ps, const oracle_geom* gs, const int3
                                    staging + (((((l - l0) * 2 + kv) * n + (t - a)) * H + h) * d + i) * e,
                                    (size_t)e);
     }
+}
+
+/* Head-restricted definition (reading R14).  Pools may differ in H (the
+ * head count of each TP shard); L, d, e agree.  For every l in [l0,l1), kv,
+ * t in [t0,t1), head h in [h0,h1), i < d:
+ *   the e bytes at off_d(l,kv,Td[t/bs_d], t mod bs_d, hd0 + (h - h0), i)
+ *   := the e bytes at off_s(l,kv,Ts[t/bs_s], t mod bs_s, h, i). */
+void oracle_migrate_heads(const uint8_t* Ps, const oracle_geom* gs, const int32_t* Ts,
+                          uint8_t* Pd, const oracle_geom* gd, const int32_t* Td,
+                          int64_t t0, int64_t t1, int64_t l0, int64_t l1,
+                          int64_t h0, int64_t h1, int64_t hd0)
+{
+    for (int64_t l = l0; l < l1; ++l)
+        for (int64_t kv = 0; kv < 2; ++kv)
+            for (int64_t t = t0; t < t1; ++t)
+                for (int64_t h = h0; h < h1; ++h)
+                    for (int64_t i = 0; i < gs->d; ++i)
+                        memcpy(Pd + oracle_logical_off(gd, Td, l, kv, t, hd0 + (h - h0), i),
+                               Ps + oracle_logical_off(gs, Ts, l, kv, t, h, i),
+                               (size_t)gs->e);
 }

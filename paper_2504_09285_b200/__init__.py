@@ -43,6 +43,7 @@ EXPORTS = (
     "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready", "dyna_kv_ready_set_timeout",
     "dyna_kv_channel_create", "dyna_kv_channel_export", "dyna_kv_channel_import", "dyna_kv_channel_destroy",
     "dyna_kv_push", "dyna_kv_place", "dyna_kv_channel_set_timeout", "dyna_kv_ready_cancel",
+    "dyna_kv_migrate_heads",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -105,6 +106,8 @@ def _load():
                                  p(vp)]),
         "dyna_kv_migrate_ex": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
                                     vp, p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_migrate_heads": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, dyna_range,
+                                       ctypes.c_int32, ctypes.c_int32, vp, p(dyna_kv_opts), p(vp)]),
         "dyna_kv_migrate_batch": (st, [p(dyna_kv_migration), ctypes.c_int32, dyna_range, ctypes.c_int32, vp,
                                        p(dyna_kv_opts), p(vp)]),
         "dyna_kv_ready_create": (st, [ctypes.c_int32, ctypes.c_int32, p(vp)]),
@@ -187,6 +190,16 @@ def dyna_kv_migrate_ex(src: dyna_block_table, dst: dyna_block_table, token_range
     _check(lib.dyna_kv_migrate_ex(src, dst, dyna_range(*token_range), dyna_range(*layer_range), chunk_tokens,
                                   ctypes.c_void_p(stream), ctypes.byref(opts) if opts is not None else None,
                                   ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_migrate_heads(src: dyna_block_table, dst: dyna_block_table, token_range, layer_range, src_heads,
+                          dst_head_begin: int, chunk_tokens: int, stream: int = 0,
+                          opts: dyna_kv_opts | None = None) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_migrate_heads(src, dst, dyna_range(*token_range), dyna_range(*layer_range),
+                                     dyna_range(*src_heads), dst_head_begin, chunk_tokens, ctypes.c_void_p(stream),
+                                     ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
     return out.value
 
 

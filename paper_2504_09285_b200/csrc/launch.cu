@@ -31,6 +31,7 @@ void preload_kernels() {
       (const void*)k_copy_bulk<false, BatchSource>,
       (const void*)k_copy_bulk_ws<false, SingleSource>, (const void*)k_copy_bulk_ws<true, SingleSource>,
       (const void*)k_copy_bulk_ws<false, BatchSource>,
+      (const void*)k_copy_rows<8, false>, (const void*)k_copy_rows<8, true>,
   };
   for (const void* k : ks) cudaFuncGetAttributes(&a, k);
 }
@@ -61,6 +62,25 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   p.mig_t1 = t1;
   p.sig_c = (int32_t)c;
   p.err = g_err_word;
+  return p;
+}
+
+// Plan of a head-sliced migration: `slice` bytes per token at byte scol of a
+// spitch-byte source row -> byte dcol of a dpitch-byte destination row.  Runs
+// follow the same token grid g as make_plan; an item is up to `tpp` tokens of a run.
+Plan make_plan_sliced(const Side& s, const Side& d, int64_t slice, int64_t spitch, int64_t scol, int64_t dpitch,
+                      int64_t dcol, int64_t t0, int64_t t1, int l0, int lm, int64_t c, int64_t g, int piece) {
+  Plan p = make_plan(s, d, slice, t0, t1, l0, lm, c, g, piece);
+  p.spitch = spitch;
+  p.dpitch = dpitch;
+  p.scol = (int32_t)scol;
+  p.dcol = (int32_t)dcol;
+  p.tpp = (int32_t)std::max<int64_t>(1, piece / slice);
+  p.P = (int32_t)((std::min(g, c) + p.tpp - 1) / p.tpp);
+  p.items_per_chunk = (int64_t)lm * 2 * p.R * p.P;
+  p.n_items = p.items_per_chunk * p.nchunks;
+  p.vps = (int32_t)(slice / 16);
+  p.vps_shift = (p.vps & (p.vps - 1)) == 0 ? __builtin_ctz((unsigned)p.vps) : -1;
   return p;
 }
 
@@ -206,6 +226,30 @@ dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st, 
     k_copy_vec<8, false, SingleSource, true><<<grid, kVecThreads, 0, st>>>(src, sc);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+// Head-sliced fused copy: warp-per-item VEC engine over a balanced persistent grid.
+dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st) {
+  if (p.n_items == 0) return DYNA_OK;
+  if (p.n_items >= (int64_t(1) << 31)) return fail(DYNA_ERANGE, "too many work items in one launch");
+  DevInfo* di = dev_info(dev);
+  const bool sig = p.counters != nullptr;
+  static int occ[2] = {0, 0};
+  int& o = occ[sig ? 1 : 0];
+  if (!o) {
+    if (sig) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_copy_rows<8, true>, kVecThreads, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_copy_rows<8, false>, kVecThreads, 0);
+    if (o <= 0) o = 1;
+  }
+  int64_t cap = (int64_t)di->sms * o;
+  if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
+  constexpr int wpc = kVecThreads / 32;
+  const int64_t warps = balanced_workers(p.n_items, cap * wpc);
+  const unsigned grid = (unsigned)((warps + wpc - 1) / wpc);
+  if (sig) CUDA_TRY(launch_kernel(k_copy_rows<8, true>, grid, kVecThreads, 0, st, p));
+  else CUDA_TRY(launch_kernel(k_copy_rows<8, false>, grid, kVecThreads, 0, st, p));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return DYNA_OK;
 }
 

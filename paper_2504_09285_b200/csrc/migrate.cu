@@ -38,12 +38,13 @@ dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
 
 // Geometry, ranges, table presence and (with host ids) ids / aliasing.  *empty: nothing to move.
 dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
-                          int32_t chunk_tokens, bool* empty) {
+                          int32_t chunk_tokens, bool* empty, bool heads_may_differ) {
   if (!src.pool || !dst.pool) return fail(DYNA_EINVAL, "NULL pool in a block table");
   const dyna_kv_pool_desc &gs = src.pool->desc, &gd = dst.pool->desc;
-  if (gs.num_layers != gd.num_layers || gs.num_kv_heads != gd.num_kv_heads || gs.head_dim != gd.head_dim ||
-      gs.elem_bytes != gd.elem_bytes)
-    return fail(DYNA_EGEOM, "source and destination geometry differ (L, H, d, e)");
+  if (gs.num_layers != gd.num_layers || (!heads_may_differ && gs.num_kv_heads != gd.num_kv_heads) ||
+      gs.head_dim != gd.head_dim || gs.elem_bytes != gd.elem_bytes)
+    return fail(DYNA_EGEOM, heads_may_differ ? "source and destination geometry differ (L, d, e)"
+                                             : "source and destination geometry differ (L, H, d, e)");
   if (lr.begin < 0 || lr.begin > lr.end || lr.end > gs.num_layers)
     return fail(DYNA_ERANGE, "layer range [%lld, %lld) outside [0, %d)", (long long)lr.begin, (long long)lr.end,
                 gs.num_layers);
@@ -247,6 +248,104 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     r = run_staged(S, D, sids, dids, tr, l0, lm, c, signal, engine, piece, stages, unroll, o.max_ctas, stream, x,
                    o.schedule);
   }
+  if (!r) r = lease.finish(stream);
+  if (r) {
+    delete x;
+    return r;
+  }
+  x->launches = (int32_t)(g_launches.load() - launches0);
+  if ((r = record_completion(x, S->dev, stream))) {
+    delete x;
+    return r;
+  }
+  *out = x;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                                  dyna_range src_heads, int32_t dst_head_begin, int32_t chunk_tokens,
+                                  struct CUstream_st* stream_, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  dyna_kv_opts o{};
+  dyna_status r = check_opts(opts, &o);
+  if (r) return r;
+  if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
+  bool empty = false;
+  if ((r = validate_pair(src, dst, tr, lr, chunk_tokens, &empty, true))) return r;
+  dyna_kv_pool* S = src.pool;
+  dyna_kv_pool* D = dst.pool;
+  const dyna_kv_pool_desc &gs = S->desc, &gd = D->desc;
+  const int64_t nh = src_heads.end - src_heads.begin;
+  if (src_heads.begin < 0 || nh < 0 || src_heads.end > gs.num_kv_heads || dst_head_begin < 0 ||
+      dst_head_begin + nh > gd.num_kv_heads)
+    return fail(DYNA_ERANGE, "heads [%lld, %lld) of %d -> [%d, %lld) of %d", (long long)src_heads.begin,
+                (long long)src_heads.end, gs.num_kv_heads, dst_head_begin, (long long)(dst_head_begin + nh),
+                gd.num_kv_heads);
+  const int64_t head_bytes = (int64_t)gs.head_dim * gs.elem_bytes;
+  if ((nh * head_bytes) % 16 || head_bytes % 16)
+    return fail(DYNA_EGEOM, "head slices must be multiples of 16 bytes (d*e = %lld)", (long long)head_bytes);
+  if (nh == gs.num_kv_heads && nh == gd.num_kv_heads)  // whole rows on both sides: the plain migration
+    return migrate_impl(src, dst, tr, lr, chunk_tokens, stream_, opts, nullptr, 0, out);
+  if (o.variant == DYNA_VARIANT_STAGED || (o.engine && o.engine != DYNA_ENGINE_VEC))
+    return fail(DYNA_ENOTSUP, "head-sliced migration: FUSED variant, VEC engine only");
+  const int64_t ntok = tr.end - tr.begin;
+  const int64_t nchunks = (empty || nh == 0) ? 0 : (ntok + chunk_tokens - 1) / chunk_tokens;
+  const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
+  if (signal && nchunks > DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks, DYNA_MAX_CHUNKS);
+  if (nchunks == 0) {
+    auto* x = new dyna_kv_xfer();
+    x->dev = S->dev;
+    x->sender = gs.instance;
+    x->empty = true;
+    *out = x;
+    return DYNA_OK;
+  }
+  if ((r = check_reach(S, D))) return r;
+  if (!err_word()) return fail(DYNA_ECUDA, "no error word");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
+  const int piece = o.piece_bytes ? o.piece_bytes : kVecPiece;
+
+  DeviceGuard guard(S->dev);
+  RingLease lease(S->dev);
+  const int32_t* sids = src.block_ids;
+  const int32_t* dids = dst.block_ids;
+  if (!sids || !dids) {
+    const size_t sb = sids ? 0 : (table_upload_bytes(src, tr.end) + 15) & ~size_t(15);
+    const size_t db = dids ? 0 : table_upload_bytes(dst, tr.end);
+    char *base = nullptr, *h = nullptr;
+    if ((r = lease.reserve(sb + db, &base, &h, stream))) return r;
+    if (!sids) std::memcpy(h, src.host_block_ids, table_upload_bytes(src, tr.end));
+    if (!dids) std::memcpy(h + sb, dst.host_block_ids, db);
+    if ((r = lease.copy(stream))) return r;
+    if (!sids) sids = reinterpret_cast<const int32_t*>(base);
+    if (!dids) dids = reinterpret_cast<const int32_t*>(base + sb);
+  }
+  auto* x = new dyna_kv_xfer();
+  x->dev = S->dev;
+  x->sender = gs.instance;
+  x->nchunks = (int32_t)nchunks;
+  x->variant = DYNA_VARIANT_FUSED;
+  x->engine = DYNA_ENGINE_VEC;
+  x->piece = piece;
+  x->unroll = 8;
+  const uint64_t launches0 = g_launches.load();
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  Plan p = make_plan_sliced(paged(S, sids), paged(D, dids), nh * head_bytes, S->row, src_heads.begin * head_bytes,
+                            D->row, (int64_t)dst_head_begin * head_bytes, tr.begin, tr.end, l0, lm, chunk_tokens,
+                            gcd64(gs.block_size, gd.block_size), piece);
+  if (signal) {
+    if ((r = channel_counters(S, D, S->dev, &p.counters))) {
+      delete x;
+      return r;
+    }
+    p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
+    p.epoch = x->epoch = next_epoch(gs.instance, D);
+    p.sys_fence = peer_dst;
+  }
+  r = launch_rows(p, o.max_ctas, S->dev, stream);
   if (!r) r = lease.finish(stream);
   if (r) {
     delete x;

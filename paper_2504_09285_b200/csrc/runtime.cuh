@@ -278,6 +278,9 @@ dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int
 dyna_status launch_batch(const BatchSource& src, int64_t n_items, int piece, int engine, int max_ctas, int stages,
                          int unroll, int dev, cudaStream_t st, int schedule);
 dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st, int schedule);
+Plan make_plan_sliced(const Side& s, const Side& d, int64_t slice, int64_t spitch, int64_t scol, int64_t dpitch,
+                      int64_t dcol, int64_t t0, int64_t t1, int l0, int lm, int64_t c, int64_t g, int piece);
+dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st);
 dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, const int32_t* dids, dyna_range tr,
                        int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
                        int max_ctas, cudaStream_t stream, dyna_kv_xfer* x, int schedule);
@@ -292,7 +295,7 @@ dyna_status launch_fill(void* dst, uint64_t bytes, unsigned long long key, uint6
 dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream);
 dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o);
 dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
-                          int32_t chunk_tokens, bool* empty);
+                          int32_t chunk_tokens, bool* empty, bool heads_may_differ = false);
 dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D);
 Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok, int64_t run_bytes);
 size_t table_upload_bytes(const dyna_block_table& t, int64_t t1);

@@ -51,6 +51,32 @@ def aggregate_bound_s(pair_bytes: dict[tuple[int, int], int], world: int, link_b
     return total / (world * link_bytes_per_s)
 
 
+def tp_heads(num_heads: int, tp: int, rank: int) -> tuple[int, int]:
+    """KV heads a rank of a TP-`tp` instance holds: the contiguous partition
+    [rank*H/tp, (rank+1)*H/tp) (tp must divide H; §5 P:595-596 runs
+    r^alpha and r^beta as TP groups)."""
+    if tp <= 0 or num_heads % tp:
+        raise ValueError(f"TP degree {tp} must divide the {num_heads} KV heads")
+    return rank * num_heads // tp, (rank + 1) * num_heads // tp
+
+
+def tp_reshard_plan(num_heads: int, tp_src: int, tp_dst: int) -> list[tuple[int, int, tuple[int, int], int]]:
+    """Head resharding between a TP-tp_src sender and a TP-tp_dst receiver
+    (SURVEY §8f NEXT-3): one entry (src_rank, dst_rank, src_heads, dst_head_begin)
+    per rank pair whose head sets overlap, in the local head numbering of each
+    rank's pool — the arguments of dyna_kv_migrate_heads.  Equal degrees give
+    the rank-i -> rank-i pairs with whole rows."""
+    out = []
+    for a in range(tp_src):
+        sa, sb = tp_heads(num_heads, tp_src, a)
+        for b in range(tp_dst):
+            da, db = tp_heads(num_heads, tp_dst, b)
+            lo, hi = max(sa, da), min(sb, db)
+            if lo < hi:
+                out.append((a, b, (lo - sa, hi - sa), lo - da))
+    return out
+
+
 def exchange_handles(handle: bytes, group=None) -> list[bytes]:
     """All-gather every rank's exported pool handle (dyna_kv_pool_export bytes)."""
     import torch.distributed as dist

@@ -114,3 +114,27 @@ def test_nccl_baseline_logic_matches_oracle_under_gloo():
     for p in ps:
         p.join(timeout=60)
     assert res == [(0, True), (1, True)]
+
+
+# ---------------------------------------------------------------- TP head resharding plan (host logic)
+@pytest.mark.parametrize("H", [8, 32])
+@pytest.mark.parametrize("ts", [1, 2, 4, 8])
+@pytest.mark.parametrize("td", [1, 2, 4, 8])
+def test_tp_reshard_plan_covers_every_head_once(H, ts, td):
+    plan = dd.tp_reshard_plan(H, ts, td)
+    seen = []
+    for a, b, (h0, h1), hd0 in plan:
+        sa, sb = dd.tp_heads(H, ts, a)
+        da, db = dd.tp_heads(H, td, b)
+        assert 0 <= h0 < h1 <= sb - sa and 0 <= hd0 and hd0 + (h1 - h0) <= db - da
+        assert sa + h0 == da + hd0                      # the same global heads on both sides
+        seen += list(range(sa + h0, sa + h1))
+    assert sorted(seen) == list(range(H))               # every global head moved exactly once
+    if ts == td:
+        assert plan == [(r, r, (0, H // ts), 0) for r in range(ts)]
+    assert len(plan) == max(ts, td)                     # nested partitions: one pair per finer rank
+
+
+def test_tp_heads_rejects_uneven():
+    with pytest.raises(ValueError):
+        dd.tp_heads(8, 3, 0)

@@ -1,0 +1,150 @@
+"""GPU parity of head-sliced migration (dyna_kv_migrate_heads; TP resharding,
+SURVEY §8f NEXT-3, reading R14) against oracle.migrate_heads, bit for
+bit on whole pools, plus a full-size TP-1 -> TP-4 Llama-3-8B reshard checked on
+sampled rows and by the scatter/gather round trip."""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import kvgen
+import oracle
+import paper_2504_09285_b200 as dk
+from kvgen import Geom
+from paper_2504_09285_b200 import dist as dd
+from gpu_util import dev_table, pool_filled, pool_from_host
+
+pytestmark = pytest.mark.gpu
+
+
+def _heads_parity(gs, gd, n_tok, tr, lr, c, heads, hd0, seed=1, flags=0, piece=0, with_host=True):
+    ts, td = kvgen.table_pair(seed + 100, n_tok, gs, gd)
+    hs, hd = kvgen.fill_bytes(seed, gs.pool_bytes), kvgen.fill_bytes(seed + 1, gd.pool_bytes)
+    want = hd.copy()
+    oracle.migrate_heads(hs, gs, ts, want, gd, td, tr, lr, heads, hd0)
+    src, dst = pool_from_host(gs, hs), pool_from_host(gd, hd)
+    st, dt = dev_table(src, ts, with_host), dev_table(dst, td, with_host)
+    x = dk.dyna_kv_migrate_heads(st, dt, tr, lr, heads, hd0, c, 0, dk.opts(flags=flags, piece_bytes=piece))
+    info = dk.dyna_kv_xfer_info(x)
+    dk.dyna_kv_wait(x)
+    got = dst.tensor.cpu().numpy()
+    assert np.array_equal(src.tensor.cpu().numpy(), hs), "source pool modified"
+    if not np.array_equal(got, want):
+        diff = np.flatnonzero(got != want)
+        pytest.fail(f"{len(diff)} bytes differ; first at {diff[0]}")
+    return src, dst, info
+
+
+G8 = Geom(3, 8, 64, 2, 16, 40)      # 8 heads of 128 B: a TP-1 shard
+G4 = Geom(3, 4, 64, 2, 16, 48)      # TP-2 shard
+G2 = Geom(3, 2, 64, 2, 8, 96)       # TP-4 shard, other block size
+G1 = Geom(3, 1, 64, 2, 32, 24)      # TP-8 shard
+
+
+@pytest.mark.parametrize("gs,gd,heads,hd0", [
+    (G8, G4, (0, 4), 0), (G8, G4, (4, 8), 0), (G8, G2, (2, 4), 0), (G8, G1, (7, 8), 0),
+    (G4, G8, (0, 4), 4), (G2, G8, (0, 2), 6), (G1, G8, (0, 1), 3), (G4, G2, (1, 3), 0),
+    (G2, G4, (0, 2), 1), (G8, G8, (3, 6), 1), (G8, G8, (0, 8), 0), (G4, G4, (2, 3), 2),
+])
+@pytest.mark.parametrize("c", [7, 16, 64, 500])
+def test_heads_parity(gs, gd, heads, hd0, c):
+    _heads_parity(gs, gd, 500, (0, 451), (0, 3), c, heads, hd0)
+
+
+@pytest.mark.parametrize("tr,lr", [((13, 400), (0, 3)), ((0, 1), (1, 2)), ((31, 33), (2, 3)), ((0, 500), (0, 3))])
+@pytest.mark.parametrize("piece", [0, 256, 1024, 65536])
+def test_heads_subranges_and_pieces(tr, lr, piece):
+    _heads_parity(G8, G2, 500, tr, lr, 48, (5, 7), 0, piece=piece)
+
+
+@pytest.mark.parametrize("bss,bsd", [(16, 32), (32, 16), (16, 24), (8, 16)])
+def test_heads_reblocking(bss, bsd):
+    gs = G8.with_(block_size=bss, num_blocks=40 * 16 // bss)
+    gd = G2.with_(block_size=bsd, num_blocks=96 * 8 // bsd + 8)
+    _heads_parity(gs, gd, 500, (3, 467), (0, 3), 40, (4, 6), 0)
+
+
+def test_heads_signal_flags_and_host_tables():
+    src, dst, (epoch, nck, sender) = _heads_parity(G8, G4, 500, (0, 451), (0, 3), 64, (4, 8), 0,
+                                                   flags=dk.DYNA_MIGRATE_SIGNAL, with_host=False)
+    assert nck == 8 and epoch > 0
+    fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
+    dk.dyna_kv_copy_flags(dst.handle, sender, 0, nck, fl.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert (fl.numpy() == epoch).all()
+    ts, td = kvgen.table_pair(101, 500, G8, G4)
+    st = dk.table(src, None, ts)              # host-resident tables (the library uploads them)
+    dt = dk.table(dst, None, td)
+    hd = dst.tensor.cpu().numpy()
+    want = hd.copy()
+    oracle.migrate_heads(src.tensor.cpu().numpy(), G8, ts, want, G4, td, (100, 300), (1, 3), (0, 2), 2)
+    dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(st, dt, (100, 300), (1, 3), (0, 2), 2, 32, 0, None))
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
+
+
+def test_heads_empty_and_errors():
+    src, dst = pool_filled(G8, 1), pool_filled(G4, 2)
+    ts, td = kvgen.table_pair(1, 200, G8, G4)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    for args in [((0, 0), (0, 3), (0, 4), 0), ((0, 100), (0, 3), (2, 2), 0), ((0, 100), (1, 1), (0, 4), 0)]:
+        dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(st, dt, args[0], args[1], args[2], args[3], 32, 0))
+    torch.cuda.synchronize()
+    before = dst.tensor.clone()
+    for heads, hd0 in [((0, 5), 0), ((3, 9), 0), ((0, 2), 3), ((0, 1), -1), ((2, 1), 0)]:
+        with pytest.raises(dk.DynaKVError) as e:
+            dk.dyna_kv_migrate_heads(st, dt, (0, 100), (0, 3), heads, hd0, 32, 0)
+        assert e.value.status == dk.DYNA_ERANGE, (heads, hd0)
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_migrate_heads(st, dt, (0, 100), (0, 3), (0, 2), 0, 32, 0, dk.opts(variant=dk.DYNA_VARIANT_STAGED))
+    assert e.value.status == dk.DYNA_ENOTSUP
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_migrate_heads(st, dt, (0, 100), (0, 3), (0, 2), 0, 32, 0, dk.opts(engine=dk.DYNA_ENGINE_BULK))
+    assert e.value.status == dk.DYNA_ENOTSUP
+    other = pool_filled(Geom(2, 4, 64, 2, 16, 48), 3)
+    with pytest.raises(dk.DynaKVError) as e:               # L differs
+        dk.dyna_kv_migrate_heads(st, dev_table(other, td), (0, 100), (0, 2), (0, 2), 0, 32, 0)
+    assert e.value.status == dk.DYNA_EGEOM
+    torch.cuda.synchronize()
+    assert torch.equal(dst.tensor, before)
+
+
+@pytest.mark.parametrize("tp_s,tp_d", [(1, 4), (4, 1), (2, 4), (4, 2), (2, 8)])
+def test_tp_reshard_round_trip_full_llama3_rows(tp_s, tp_d):
+    """Llama-3-8B rows (8 KV heads, d128, bf16): a request's KV sharded over tp_s source ranks is
+    resharded onto tp_d destination ranks with dd.tp_reshard_plan (one dyna_kv_migrate_heads per
+    overlapping rank pair, all on one GPU here), then gathered back into a TP-1 pool: the result
+    equals one plain migration (oracle), byte for byte."""
+    H, L, s = 8, 32, 1000
+    g1 = kvgen.LLAMA3_8B.with_(num_blocks=80)
+    gs = g1.with_(num_kv_heads=H // tp_s)
+    gd = g1.with_(num_kv_heads=H // tp_d, block_size=32, num_blocks=40)
+    full_s = pool_filled(g1, 11)
+    t1s, _ = kvgen.table_pair(12, s, g1, g1)
+    src_pools = [pool_filled(gs, 20 + r) for r in range(tp_s)]
+    src_tabs = [kvgen.table_pair(30 + r, s, gs, gs)[1] for r in range(tp_s)]
+    dst_pools = [pool_filled(gd, 40 + r) for r in range(tp_d)]
+    dst_tabs = [kvgen.table_pair(50 + r, s, gd, gd)[1] for r in range(tp_d)]
+    keep = []
+    for r in range(tp_s):                    # build the TP-tp_s source shards from the TP-1 pool
+        a = (dev_table(full_s, t1s), dev_table(src_pools[r], src_tabs[r]))
+        keep.append(a)
+        dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(*a, (0, s), (0, L), dd.tp_heads(H, tp_s, r), 0, 256, 0))
+    xs = []
+    for a, b, heads, hd0 in dd.tp_reshard_plan(H, tp_s, tp_d):     # the reshard under test
+        t = (dev_table(src_pools[a], src_tabs[a]), dev_table(dst_pools[b], dst_tabs[b]))
+        keep.append(t)
+        xs.append(dk.dyna_kv_migrate_heads(*t, (0, s), (0, L), heads, hd0, 256, 0))
+    for x in xs:
+        dk.dyna_kv_wait(x)
+    back = pool_filled(g1, 60)
+    _, t1d = kvgen.table_pair(61, s, g1, g1)
+    for b in range(tp_d):
+        t = (dev_table(dst_pools[b], dst_tabs[b]), dev_table(back, t1d))
+        keep.append(t)
+        h0, h1 = dd.tp_heads(H, tp_d, b)
+        dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(*t, (0, s), (0, L), (0, h1 - h0), h0, 256, 0))
+    torch.cuda.synchronize()
+    want = kvgen.fill_bytes(60, g1.pool_bytes)
+    oracle.migrate(full_s.tensor.cpu().numpy(), g1, t1s, want, g1, t1d, (0, s))
+    assert np.array_equal(back.tensor.cpu().numpy(), want)

@@ -294,3 +294,107 @@ def test_pins_detect_mutants():
     ]
     for m in mutants:
         assert not np.array_equal(mut(m), good)
+
+
+# ---------------------------------------------------------------- head-restricted definition (reading R14)
+def np_reference_heads(Ps, gs, Ts, Pd, gd, Td, t0, t1, l0, l1, h0, h1, hd0):
+    """Independent formulation: 6-D views [L][2][NB][bs][H][d*e], head slices assigned with fancy indexing."""
+    he = gs.head_dim * gs.elem_bytes
+    S = Ps.reshape(gs.num_layers, 2, gs.num_blocks, gs.block_size, gs.num_kv_heads, he)
+    D = Pd.reshape(gd.num_layers, 2, gd.num_blocks, gd.block_size, gd.num_kv_heads, he)
+    t = np.arange(t0, t1)
+    Ts, Td = np.asarray(Ts), np.asarray(Td)
+    if len(t) and l1 > l0 and h1 > h0:
+        D[l0:l1, :, Td[t // gd.block_size], t % gd.block_size, hd0:hd0 + (h1 - h0)] = \
+            S[l0:l1, :, Ts[t // gs.block_size], t % gs.block_size, h0:h1]
+
+
+def test_heads_full_range_is_the_plain_definition():
+    g = Geom(2, 4, 8, 2, 4, 12)
+    Ps, Pd0 = pools(g, g, seed=51)
+    ts, td = kvgen.table_pair(3, 37, g, g)
+    a, b = Pd0.copy(), Pd0.copy()
+    oracle.migrate(Ps, g, ts, a, g, td, (5, 37))
+    oracle.migrate_heads(Ps, g, ts, b, g, td, (5, 37), None, (0, 4), 0)
+    assert np.array_equal(a, b) and not np.array_equal(a, Pd0)
+
+
+def test_heads_brute_force_tiny_pools():
+    rng = np.random.default_rng(kvgen.MASTER_SEED + 14)
+    n = 0
+    for Hs, Hd, bss, bsd in itertools.product((1, 2, 3, 4), (1, 2, 4), (1, 2, 4), (2, 4)):
+        gs, gd = Geom(2, Hs, 8, 2, bss, 6), Geom(2, Hd, 8, 2, bsd, 6)
+        Ps, Pd0 = pools(gs, gd, seed=n)
+        for h0 in range(Hs):
+            for h1 in range(h0, Hs + 1):
+                for hd0 in range(0, Hd - (h1 - h0) + 1):
+                    s = int(rng.integers(0, 9))
+                    ts = rng.choice(6, kvgen.blocks_needed(s, bss), replace=True).astype(np.int32)
+                    td = rng.choice(6, kvgen.blocks_needed(s, bsd), replace=False).astype(np.int32)
+                    t0 = int(rng.integers(0, s + 1))
+                    lr = ((0, 2), (1, 2))[int(rng.integers(0, 2))]
+                    a, b = Pd0.copy(), Pd0.copy()
+                    oracle.migrate_heads(Ps, gs, ts, a, gd, td, (t0, s), lr, (h0, h1), hd0)
+                    np_reference_heads(Ps, gs, ts, b, gd, td, t0, s, *lr, h0, h1, hd0)
+                    assert np.array_equal(a, b), (gs, gd, s, t0, lr, h0, h1, hd0)
+                    n += 1
+    assert n > 500
+
+
+def _tp_heads(H, T, r):
+    """Contiguous head partition of a TP-T instance: rank r holds heads [r*H/T, (r+1)*H/T)."""
+    return r * H // T, (r + 1) * H // T
+
+
+@pytest.mark.parametrize("T", [2, 4, 8])
+def test_heads_tp_scatter_gather_round_trip(T):
+    """A TP-1 pool scattered head-wise into T shard pools (each its own H/T-head geometry and
+    fresh table), then gathered back into a TP-1 pool, equals one plain migration."""
+    H, s = 8, 45
+    g1 = Geom(2, H, 8, 2, 4, 20)
+    gT = Geom(2, H // T, 8, 2, 8, 10)
+    Ps, Pd0 = pools(g1, g1, seed=60 + T)
+    ts, td = kvgen.table_pair(61, s, g1, g1)
+    shards = [kvgen.fill_bytes(70 + r, gT.pool_bytes) for r in range(T)]
+    tsh = [kvgen.table_pair(80 + r, s, gT, gT)[1] for r in range(T)]
+    for r in range(T):
+        oracle.migrate_heads(Ps, g1, ts, shards[r], gT, tsh[r], (0, s), None, _tp_heads(H, T, r), 0)
+    got = Pd0.copy()
+    for r in range(T):
+        h0, h1 = _tp_heads(H, T, r)
+        oracle.migrate_heads(shards[r], gT, tsh[r], got, g1, td, (0, s), None, (0, h1 - h0), h0)
+    want = Pd0.copy()
+    oracle.migrate(Ps, g1, ts, want, g1, td, (0, s))
+    assert np.array_equal(got, want)
+
+
+def test_heads_untouched_outside_the_slice():
+    gs, gd = Geom(1, 2, 8, 2, 4, 4), Geom(1, 4, 8, 2, 4, 4)
+    Ps, Pd0 = pools(gs, gd, seed=90)
+    ts, td = np.array([2, 0], np.int32), np.array([3, 1], np.int32)
+    got = Pd0.copy()
+    oracle.migrate_heads(Ps, gs, ts, got, gd, td, (1, 7), None, (0, 2), 1)
+    D, D0 = got.reshape(1, 2, 4, 4, 4, 16), Pd0.reshape(1, 2, 4, 4, 4, 16)
+    S = Ps.reshape(1, 2, 4, 4, 2, 16)
+    changed = np.zeros(D.shape[:-1], bool)
+    for t in range(1, 7):
+        changed[0, :, td[t // 4], t % 4, 1:3] = True
+        assert np.array_equal(D[0, :, td[t // 4], t % 4, 1:3], S[0, :, ts[t // 4], t % 4, 0:2])
+    assert np.array_equal(D[~changed], D0[~changed])
+
+
+def test_heads_pins_detect_mutants():
+    """The brute force rejects a dropped head offset on either side and swapped head order."""
+    gs, gd = Geom(1, 4, 8, 2, 2, 4), Geom(1, 4, 8, 2, 2, 4)
+    Ps, Pd0 = pools(gs, gd, seed=91)
+    ts, td = np.array([1, 3], np.int32), np.array([2, 0], np.int32)
+    good = Pd0.copy()
+    oracle.migrate_heads(Ps, gs, ts, good, gd, td, (0, 4), None, (1, 3), 2)
+    S = Ps.reshape(1, 2, 4, 2, 4, 16)
+    variants = [((1, 3), (0, 2)), ((0, 2), (2, 4)), ((2, 0), (2, 4))]  # (src heads, dst heads) slips
+    for (a, b), (c, d_) in variants:
+        D = Pd0.copy().reshape(1, 2, 4, 2, 4, 16)
+        for t in range(4):
+            src = S[0, :, ts[t // 2], t % 2, a:b] if a < b else S[0, :, ts[t // 2], t % 2, [2, 1]]
+            D[0, :, td[t // 2], t % 2, c:d_] = src
+        assert not np.array_equal(D.reshape(-1), good)
