@@ -283,14 +283,17 @@ def run_dyna(args, rank, world, local_rank):
     h2d = 2 * blocks * 4            # the table entries [0, s) reaches, both tables
     d2h = nchunks * 8
 
+    flag_stream = torch.cuda.Stream()       # the read-back runs beside the next step's migration
+
     def e2e_issue(k):
         i = k % N_SETS
         st, dt_ = e2e_tables[i]
         x = dk.dyna_kv_migrate_ex(st, dt_, (0, S_SPLIT), (0, g.num_layers), CHUNK, cs, sig_opts)
         epoch = dk.dyna_kv_xfer_info(x)[0]
-        dk.dyna_kv_copy_flags(flag_pool, sender, 0, nchunks, flags_host[i].data_ptr(), cs)
+        dk.dyna_kv_stream_wait(x, flag_stream.cuda_stream)
+        dk.dyna_kv_copy_flags(flag_pool, sender, 0, nchunks, flags_host[i].data_ptr(), flag_stream.cuda_stream)
         ev = torch.cuda.Event()
-        ev.record(stream)
+        ev.record(flag_stream)
         return x, epoch, ev, i
 
     def e2e_finish(h):

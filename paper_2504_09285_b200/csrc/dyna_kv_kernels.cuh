@@ -165,8 +165,9 @@ __device__ __forceinline__ bool wait_ready(const Plan& p, int32_t slot) {
   if (ld_acquire_gpu(p.ready + slot) >= p.ready_epoch) return true;
   unsigned long long t0, now;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  while (ld_acquire_gpu(p.ready + slot) < p.ready_epoch) {
-    if (p.cancel && *p.cancel >= p.ready_epoch) return false;
+  for (uint32_t polls = 0; ld_acquire_gpu(p.ready + slot) < p.ready_epoch; ++polls) {
+    // the cancel word is host memory: read it on the first poll and then every 32nd (~16 us)
+    if (p.cancel && (polls & 31) == 0 && *p.cancel >= p.ready_epoch) return false;
     __nanosleep(500);
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     if (now - t0 > p.ready_timeout_ns) {  // never hang the device: report at dyna_kv_wait

@@ -77,6 +77,7 @@ struct DeviceGuard {  // restores the caller's current device
 struct DevInfo {
   int sms = 0;
   cudaStream_t aux = nullptr;  // library stream for destination-side kernels (staged, cross-device)
+  cudaStream_t upload = nullptr;  // library stream for host-resident table uploads (overlap the previous kernel)
   unsigned long long* sched = nullptr;  // [kSchedSlots][2] dynamic-scheduling counters, zero at rest
   std::atomic<uint32_t> sched_seq{0};
 };
@@ -230,9 +231,23 @@ class RingLease {
     return DYNA_OK;
   }
 
+  // The copy runs on the device's upload stream and `st` waits for it: the upload
+  // of call k+1 overlaps call k's kernel instead of sitting between the two on
+  // `st` (DYNA_KV_UPLOAD_STREAM=0: copy on `st` itself).  The span cannot still be
+  // read by an older kernel: reserve() waited for its release event.
   dyna_status copy(cudaStream_t st) {
     UploadRing& R = *ring_;
-    CUDA_TRY(cudaMemcpyAsync(R.dev + span_b_, R.host + span_b_, span_e_ - span_b_, cudaMemcpyHostToDevice, st));
+    cudaStream_t up = upload_stream();
+    if (!up) {
+      CUDA_TRY(cudaMemcpyAsync(R.dev + span_b_, R.host + span_b_, span_e_ - span_b_, cudaMemcpyHostToDevice, st));
+      return DYNA_OK;
+    }
+    cudaEvent_t ev = nullptr;
+    CUDA_TRY(get_event(dev_, &ev));
+    CUDA_TRY(cudaMemcpyAsync(R.dev + span_b_, R.host + span_b_, span_e_ - span_b_, cudaMemcpyHostToDevice, up));
+    CUDA_TRY(cudaEventRecord(ev, up));
+    CUDA_TRY(cudaStreamWaitEvent(st, ev, 0));
+    put_event(dev_, ev);  // the wait above already captured this record
     return DYNA_OK;
   }
 
@@ -258,6 +273,21 @@ class RingLease {
   int dev_;
   UploadRing* ring_ = nullptr;
   size_t span_b_ = 0, span_e_ = 0;
+
+  cudaStream_t upload_stream() {
+    static const bool on = [] {
+      const char* e = std::getenv("DYNA_KV_UPLOAD_STREAM");
+      return !(e && e[0] == '0');
+    }();
+    if (!on) return nullptr;
+    DevInfo* di = dev_info(dev_);
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!di->upload) {
+      DeviceGuard g(dev_);
+      if (cudaStreamCreateWithFlags(&di->upload, cudaStreamNonBlocking) != cudaSuccess) di->upload = nullptr;
+    }
+    return di->upload;
+  }
 };
 
 struct Choice {

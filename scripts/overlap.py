@@ -9,7 +9,7 @@ chunk size not stated) — context, not a target.
 Workload (BASELINE.json configs[3]): Llama-3-8B GQA pools (32 L, 8 KV heads,
 d128, bf16, block 16), a 32k-token prompt, chunk c in {512, 1024, 2048, 4096}.
 Stand-in producer (NOT part of the path; torch.matmul = cuBLAS): per chunk,
-N_GEMM bf16 GEMMs of [c, 4096] x [4096, 14336] — 120 of them ~= the dense
+N_GEMM bf16 GEMMs of [c, 4096] x [4096, 14336] — 128 of them ~= the dense
 prefill FLOPs of Llama-3-8B (2 * ~7e9 * c).  After chunk k's GEMMs an event is
 recorded; the migration stream waits on it and pushes chunk k.
 
@@ -22,6 +22,12 @@ Reported per (c, SM budget), all from CUDA events inside the same run:
   producer_slowdown  producer time with concurrent chunked migrations vs alone
   ready_coupled    the same with ONE dyna_kv_migrate_on_ready launch that waits
                    on the device for the producer's per-chunk marks
+  --layers adds the layer-granular forms ("can be composed with" layer-
+  level transfer): the producer runs a chunk layer by layer (n_gemm/32 GEMMs per
+  layer) and
+  layered          pushes (chunk k, layer l) as soon as layer l of chunk k is done
+                   (one dyna_kv_migrate per chunk x layer, host-enqueued)
+  ready_layers     one coupled launch with DYNA_READY_PER_LAYER marks
 On one GPU the migration is an intra-device reblock (HBM); on the 8-GPU box
 the same script with a peer destination measures the NVLink form.
 """
@@ -41,7 +47,7 @@ import torch  # noqa: E402
 import kvgen  # noqa: E402
 import paper_2504_09285_b200 as dk  # noqa: E402
 
-N_GEMM = 120
+N_GEMM = 128   # 4 per layer: ~= the dense prefill FLOPs of Llama-3-8B per chunk (2 * ~7e9 * c)
 
 
 def main():
@@ -52,6 +58,7 @@ def main():
     ap.add_argument("--n-gemm", type=int, default=N_GEMM)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--ready-ctas", type=int, default=8, help="CTA budget of the coupled launch when budget is 0")
+    ap.add_argument("--layers", action="store_true", help="add the layer-granular modes")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "overlap.json"))
     args = ap.parse_args()
     torch.cuda.set_device(0)
@@ -72,6 +79,10 @@ def main():
         for _ in range(args.n_gemm):
             torch.matmul(X, W)
 
+    def producer_layer(X):
+        for _ in range(max(1, args.n_gemm // g.num_layers)):
+            torch.matmul(X, W)
+
     def run(c, mode, budget):
         """One run.  Returns (T_prod_ms, exposed_ms): exposed = time from the end of the
         producer's last chunk to the end of the last migration (the non-overlapped transfer)."""
@@ -82,11 +93,25 @@ def main():
         e0.record(prod)
         mig.wait_event(e0)
         handles = []
-        if mode == "ready":   # one launch for the whole range; waits on the device for each chunk's mark
+        if mode in ("ready", "ready_layers"):   # one launch for the whole range; waits on the device for marks
             epoch = dk.dyna_kv_ready_begin(board)
+            fl = dk.DYNA_READY_PER_LAYER if mode == "ready_layers" else 0
             handles.append(dk.dyna_kv_migrate_on_ready(st, dt, (0, s), (0, 32), c, board, epoch, mig.cuda_stream,
-                                                       dk.opts(max_ctas=budget or args.ready_ctas)))
+                                                       dk.opts(max_ctas=budget or args.ready_ctas, flags=fl)))
         for k in range(nck):
+            if mode in ("layered", "ready_layers"):
+                for l in range(g.num_layers):
+                    with torch.cuda.stream(prod):
+                        producer_layer(X)
+                    if mode == "ready_layers":
+                        dk.dyna_kv_ready_mark(board, dk.ready_slot(k, l, (0, 32)), epoch, prod.cuda_stream)
+                    else:                             # layer l of chunk k complete -> push it now
+                        ev = torch.cuda.Event()
+                        ev.record(prod)
+                        mig.wait_event(ev)
+                        handles.append(dk.migrate(st, dt, (k * c, min((k + 1) * c, s)), (l, l + 1), c, stream=mig,
+                                                  max_ctas=budget))
+                continue
             with torch.cuda.stream(prod):
                 producer_chunk(X)
             if mode == "ready":
@@ -107,7 +132,7 @@ def main():
             dk.dyna_kv_wait(x)
         return e0.elapsed_time(e_prod), max(0.0, e_prod.elapsed_time(e_mig))
 
-    board = dk.dyna_kv_ready_create(0, 1024)
+    board = dk.dyna_kv_ready_create(0, 1 << 16)
     xs_in = {}
     for c in [int(x) for x in args.chunks.split(",")]:
         xs_in[c] = torch.randn(c, 4096, dtype=torch.bfloat16, device="cuda")
@@ -121,14 +146,20 @@ def main():
         t_mig = a0.elapsed_time(a1)
         prod_alone = statistics.median(run(c, "none", 0)[0] for _ in range(args.reps))
         for budget in [int(x) for x in args.budgets.split(",")]:
-            W_, C_, R_ = [], [], []
+            W_, C_, R_, LY, RL = [], [], [], [], []
             run(c, "whole", budget)
             run(c, "chunked", budget)   # warm
             run(c, "ready", budget)
+            if args.layers:
+                run(c, "layered", budget)
+                run(c, "ready_layers", budget)
             for _ in range(args.reps):  # interleaved so drift hits all modes alike
                 W_.append(run(c, "whole", budget))
                 C_.append(run(c, "chunked", budget))
                 R_.append(run(c, "ready", budget))
+                if args.layers:
+                    LY.append(run(c, "layered", budget))
+                    RL.append(run(c, "ready_layers", budget))
             exp_w = statistics.median(e for _, e in W_)
             exp_c = statistics.median(e for _, e in C_)
             exp_r = statistics.median(e for _, e in R_)
@@ -143,6 +174,14 @@ def main():
                  "ready_coupled": {"ctas": budget or args.ready_ctas, "exposed_ms": exp_r, "T_prod_ms": prod_r,
                                    "producer_slowdown": prod_r / prod_alone - 1,
                                    "reduction": 1 - exp_r / exp_w if exp_w > 0 else None}}
+            if args.layers:
+                for name, runs in (("layered", LY), ("ready_layers", RL)):
+                    exp_l = statistics.median(e for _, e in runs)
+                    prod_l = statistics.median(p for p, _ in runs)
+                    r[name] = {"exposed_ms": exp_l, "T_prod_ms": prod_l, "producer_slowdown": prod_l / prod_alone - 1,
+                               "reduction": 1 - exp_l / exp_w if exp_w > 0 else None}
+                    if name == "ready_layers":
+                        r[name]["ctas"] = budget or args.ready_ctas
             print(json.dumps(r), flush=True)
             results.append(r)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
