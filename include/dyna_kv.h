@@ -279,7 +279,9 @@ DYNA_API dyna_status dyna_kv_migrate_on_ready(dyna_block_table src, dyna_block_t
                                               struct CUstream_st* stream, const dyna_kv_opts* opts,
                                               dyna_kv_xfer_t* out);
 /* Cancel, from the host and with immediate effect, every migration on this
- * board whose epoch is <= `epoch`.  A running migration stops waiting: a slot
+ * board whose epoch is <= `epoch` (the cancel epoch reaches the device word
+ * the waiting warps poll by an 8-byte DMA on the board's own non-blocking
+ * stream; the call returns once it has landed and needs no free SM).  A running migration stops waiting: a slot
  * whose mark is visible when a warp reaches it is still copied (so every
  * MARKED chunk is delivered whole, and its per-chunk flag is raised when
  * signalling); the items of a slot whose mark is not visible are skipped, and

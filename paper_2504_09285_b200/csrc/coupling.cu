@@ -17,21 +17,25 @@ dyna_status dyna_kv_ready_create(int32_t device, int32_t max_chunks, dyna_kv_rea
   b->dev = device;
   b->max_chunks = max_chunks;
   DeviceGuard g(device);
-  if (cudaMalloc(&b->slots, sizeof(unsigned long long) * max_chunks) != cudaSuccess ||
-      cudaMemset(b->slots, 0, sizeof(unsigned long long) * max_chunks) != cudaSuccess) {
+  // cudaMalloc of a board (like any allocation) may synchronise the device: create boards
+  // before starting coupled migrations (dyna_kv.h).  The initialisation itself runs on the
+  // board's own non-blocking control stream.
+  const size_t sb = sizeof(unsigned long long) * max_chunks;
+  bool ok = cudaStreamCreateWithFlags(&b->ctrl, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMalloc(&b->slots, sb) == cudaSuccess &&
+            cudaMalloc(&b->cancel_dev, sizeof(unsigned long long)) == cudaSuccess &&
+            cudaHostAlloc(&b->cancel_stage, sizeof(unsigned long long), cudaHostAllocPortable) == cudaSuccess;
+  ok = ok && cudaMemsetAsync(b->slots, 0, sb, b->ctrl) == cudaSuccess &&
+       cudaMemsetAsync(b->cancel_dev, 0, sizeof(unsigned long long), b->ctrl) == cudaSuccess &&
+       cudaStreamSynchronize(b->ctrl) == cudaSuccess;
+  if (!ok) {
     cudaFree(b->slots);
+    cudaFree(b->cancel_dev);
+    if (b->cancel_stage) cudaFreeHost(b->cancel_stage);
+    if (b->ctrl) cudaStreamDestroy(b->ctrl);
     delete b;
     return fail(DYNA_ENOMEM, "ready board of %d slots", max_chunks);
   }
-  if (cudaHostAlloc(&b->cancel_host, sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable) !=
-          cudaSuccess ||
-      cudaHostGetDevicePointer(&b->cancel_dev, b->cancel_host, 0) != cudaSuccess) {
-    cudaFree(b->slots);
-    if (b->cancel_host) cudaFreeHost(b->cancel_host);
-    delete b;
-    return fail(DYNA_ENOMEM, "ready board cancel word");
-  }
-  __atomic_store_n(b->cancel_host, 0ull, __ATOMIC_RELEASE);
   dev_info(device);
   *out = b;
   return DYNA_OK;
@@ -42,7 +46,9 @@ dyna_status dyna_kv_ready_destroy(dyna_kv_ready_t b) {
   {
     DeviceGuard g(b->dev);
     cudaFree(b->slots);
-    cudaFreeHost(b->cancel_host);
+    cudaFree(b->cancel_dev);
+    cudaFreeHost(b->cancel_stage);
+    cudaStreamDestroy(b->ctrl);
   }
   delete b;
   return DYNA_OK;
@@ -62,11 +68,16 @@ dyna_status dyna_kv_ready_begin(dyna_kv_ready_t b, uint64_t* epoch) {
 
 dyna_status dyna_kv_ready_cancel(dyna_kv_ready_t b, uint64_t epoch) {
   if (!b) return fail(DYNA_EINVAL, "NULL board");
-  unsigned long long cur = __atomic_load_n(b->cancel_host, __ATOMIC_ACQUIRE);
-  while (cur < epoch &&
-         !__atomic_compare_exchange_n(b->cancel_host, &cur, (unsigned long long)epoch, false, __ATOMIC_ACQ_REL,
-                                      __ATOMIC_ACQUIRE)) {
-  }
+  std::lock_guard<std::mutex> lk(b->cancel_mu);
+  if (epoch <= b->cancel_epoch.load()) return DYNA_OK;  // monotone
+  b->cancel_epoch.store(epoch);
+  // one 8-byte DMA on the board's own non-blocking stream: it does not wait for the
+  // (possibly still waiting) migration kernels, and no SM is needed to deliver it
+  DeviceGuard g(b->dev);
+  *b->cancel_stage = epoch;
+  CUDA_TRY(cudaMemcpyAsync(b->cancel_dev, b->cancel_stage, sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                           b->ctrl));
+  CUDA_TRY(cudaStreamSynchronize(b->ctrl));
   return DYNA_OK;
 }
 

@@ -166,7 +166,7 @@ __device__ __forceinline__ bool wait_ready(const Plan& p, int32_t slot) {
   unsigned long long t0, now;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (uint32_t polls = 0; ld_acquire_gpu(p.ready + slot) < p.ready_epoch; ++polls) {
-    // the cancel word is host memory: read it on the first poll and then every 32nd (~16 us)
+    // the cancel word: read on the first poll and then every 32nd (~16 us)
     if (p.cancel && (polls & 31) == 0 && *p.cancel >= p.ready_epoch) return false;
     __nanosleep(500);
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));

@@ -509,7 +509,7 @@ dyna_status dyna_kv_wait(dyna_kv_xfer_t x) {
     if (e != cudaSuccess) r = fail(DYNA_ECUDA, "migration failed: %s", cudaGetErrorString(e));
     put_event(x->dev, x->ev);
     if (!r) r = take_device_error();
-    if (!r && x->board && __atomic_load_n(x->board->cancel_host, __ATOMIC_ACQUIRE) >= x->ready_epoch)
+    if (!r && x->board && x->board->cancel_epoch.load() >= x->ready_epoch)
       r = fail(DYNA_ECANCELED, "migration cancelled (dyna_kv_ready_cancel)");
   }
   delete x;

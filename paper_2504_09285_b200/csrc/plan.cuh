@@ -44,7 +44,7 @@ struct Plan {
   unsigned long long ready_timeout_ns;  // give up (ERR_TIMEOUT) after this long without the mark
   int32_t ready_layers;     // 0: one mark per chunk (slot k); 1: one per (chunk, layer) (slot k*lm + l-l0)
   // cancellation of a producer-coupled migration (nullptr: none): once *cancel >= ready_epoch,
-  // chunks whose mark is not visible are skipped (mapped host word, written by dyna_kv_ready_cancel)
+  // chunks whose mark is not visible are skipped (device word, DMA-written by dyna_kv_ready_cancel)
   const volatile unsigned long long* cancel;
   // head-sliced rows (dyna_kv_migrate_heads; k_copy_vec<..., SLICED>): `row` is then the
   // slice of n_heads*d*e bytes moved per token, found at byte `col` of a pitch-byte row

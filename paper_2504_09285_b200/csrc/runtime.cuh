@@ -126,8 +126,14 @@ struct dyna_kv_ready {
   unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;  // per chunk wait
   unsigned long long* slots = nullptr;  // device, zero-initialised
   std::atomic<uint64_t> epoch{0};
-  unsigned long long* cancel_host = nullptr;  // mapped pinned word: migrations with epoch <= *cancel stop
-  unsigned long long* cancel_dev = nullptr;   // its device alias
+  // Cancellation: migrations with epoch <= the cancel epoch stop waiting.  The kernels poll a
+  // DEVICE word (written by a DMA on the board's control stream): polling mapped host memory
+  // from the waiting warps was measured to slow a concurrent cuBLAS producer by 20-100%.
+  std::atomic<uint64_t> cancel_epoch{0};      // host copy (dyna_kv_wait reads it)
+  unsigned long long* cancel_dev = nullptr;   // device word the kernels poll
+  unsigned long long* cancel_stage = nullptr; // pinned staging of the DMA
+  cudaStream_t ctrl = nullptr;                // non-blocking control stream of the board
+  std::mutex cancel_mu;
 };
 
 struct dyna_kv_channel {
