@@ -80,3 +80,60 @@ def test_ipc_push_with_chunk_flags(engine):
     ts, td = kvgen.table_pair(9, 4000, g, g)
     assert torch_rows_equal(src, ts, dst, td, (0, S), (0, 4))
     assert untouched_equal(dst, DST_SEED, mapped_mask(g, [(td, (0, S))]))
+
+
+def _heads_sender(handle: bytes, q):
+    """TP-1 sender (8 heads) pushes heads [4, 8) into the importer's TP-2 rank-1 pool (4 heads)."""
+    try:
+        import torch
+
+        import kvgen
+        import paper_2504_09285_b200 as dk
+        from gpu_util import dev_table, pool_filled
+        torch.cuda.set_device(0)
+        g = _geom()
+        src = pool_filled(g, SRC_SEED, instance=SENDER)
+        dst = dk.Pool.imported(handle, 0)
+        ts, _ = kvgen.table_pair(9, 4000, g, g)
+        _, td = kvgen.table_pair(10, 4000, g.with_(num_kv_heads=4), g.with_(num_kv_heads=4))
+        x = dk.dyna_kv_migrate_heads(dev_table(src, ts), dk.table(dst, torch.from_numpy(td).cuda(), td), (0, S),
+                                     (0, 4), (4, 8), 0, CHUNK, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL))
+        info = dk.dyna_kv_xfer_info(x)
+        dk.dyna_kv_wait(x)
+        dst.close()
+        q.put(("ok", info))
+    except Exception as e:
+        q.put(("err", repr(e)))
+
+
+def test_ipc_head_reshard_with_chunk_flags():
+    """TP resharding across processes (reading R14): bit-exact against oracle.migrate_heads."""
+    import torch
+
+    import kvgen
+    import oracle
+    import paper_2504_09285_b200 as dk
+    from gpu_util import pool_filled
+    torch.cuda.set_device(0)
+    g = _geom()
+    gd = g.with_(num_kv_heads=4)
+    dst = pool_filled(gd, DST_SEED)
+    torch.cuda.synchronize()
+    handle = dk.dyna_kv_pool_export(dst.handle)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_heads_sender, args=(handle, q))
+    p.start()
+    status, info = q.get(timeout=300)
+    p.join(timeout=60)
+    assert status == "ok", info
+    epoch, nchunks, sender = info
+    flags = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
+    dk.dyna_kv_copy_flags(dst.handle, sender, 0, nchunks, flags.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert (flags.numpy() == epoch).all()
+    ts, _ = kvgen.table_pair(9, 4000, g, g)
+    _, td = kvgen.table_pair(10, 4000, gd, gd)
+    want = kvgen.fill_bytes(DST_SEED, gd.pool_bytes)
+    oracle.migrate_heads(kvgen.fill_bytes(SRC_SEED, g.pool_bytes), g, ts, want, gd, td, (0, S), None, (4, 8), 0)
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
