@@ -245,8 +245,10 @@ DYNA_API dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_
  * room to run; FUSED variant with the VEC engine only.  A board is reused
  * across requests with increasing epochs (dyna_kv_ready_begin).
  * HAZARD: while such a migration waits, anything that synchronises the whole
- * device (cudaDeviceSynchronize, cudaMalloc/cudaFree that sync, synchronous
- * copies on the legacy stream) before the last chunk is marked deadlocks: the
+ * device (cudaDeviceSynchronize, cudaMalloc/cudaFree that sync — including
+ * dyna_kv_pool_destroy, which frees the pool's flag inbox, e.g. from a
+ * binding object's garbage collection — synchronous copies on the legacy
+ * stream) before the last chunk is marked deadlocks: the
  * device waits for the migration, the migration for a mark that is never
  * issued.  The same holds for the FIRST launch of any kernel in the process
  * while the migration waits: CUDA loads kernels lazily and a module load

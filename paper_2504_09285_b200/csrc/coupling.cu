@@ -347,9 +347,7 @@ dyna_status dyna_kv_place(dyna_kv_channel_t ch, dyna_block_table dst, dyna_range
       launch_wait_flag(ch->full + slot, q + 1, ch->timeout_ns, stream);
       Plan p = make_plan(linear(ch->base + (size_t)slot * ch->slot_bytes), paged(D, dst.block_ids), D->row, sa, sb,
                          l0, lm, sb - sa, D->desc.block_size, kVecPiece);
-      p.mig_t0 = tr.begin;
-      p.mig_t1 = tr.end;
-      p.sig_c = c;
+      set_chunking(p, tr.begin, tr.end, c);
       if (signal) {
         p.counters = ch->place_counters;
         p.flags = D->inbox + (size_t)ch->sender * DYNA_MAX_CHUNKS;

@@ -65,7 +65,7 @@ __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   const int64_t G = a / p.g + j;
   const int64_t ta = max(a, G * p.g);
   const int64_t tb = min(b, (G + 1) * p.g);
-  it.k = (int32_t)((a - p.mig_t0) / p.sig_c);
+  it.k = p.k_direct ? (int32_t)k + p.k_base : (int32_t)((a - p.mig_t0) / p.sig_c);
   it.l = l;
   if (ta >= tb) return it;
   const int64_t run = (tb - ta) * p.row;
@@ -121,7 +121,7 @@ __device__ __forceinline__ SItem decode_item_sliced(const Plan& p, int64_t item)
   const int64_t G = a / p.g + j;
   const int64_t ta = max(a, G * p.g);
   const int64_t tb = min(b, (G + 1) * p.g);
-  it.k = (int32_t)((a - p.mig_t0) / p.sig_c);
+  it.k = p.k_direct ? (int32_t)k + p.k_base : (int32_t)((a - p.mig_t0) / p.sig_c);
   it.l = l;
   const int64_t ra = ta + (int64_t)pp * p.tpp;
   if (ra >= tb) return it;

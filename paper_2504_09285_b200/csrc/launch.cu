@@ -34,6 +34,21 @@ void preload_kernels() {
       (const void*)k_copy_rows<8, false>, (const void*)k_copy_rows<8, true>,
   };
   for (const void* k : ks) cudaFuncGetAttributes(&a, k);
+  // Allow the BULK rings any dynamic shared memory the device offers, once, here: a
+  // cudaFuncSetAttribute per launch is one more driver call that may synchronise while a
+  // producer-coupled migration waits.
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const void* bulk[] = {
+      (const void*)k_copy_bulk<false, SingleSource>, (const void*)k_copy_bulk<true, SingleSource>,
+      (const void*)k_copy_bulk<false, BatchSource>,  (const void*)k_copy_bulk_ws<false, SingleSource>,
+      (const void*)k_copy_bulk_ws<true, SingleSource>, (const void*)k_copy_bulk_ws<false, BatchSource>,
+  };
+  for (const void* k : bulk) {
+    cudaFuncGetAttributes(&a, k);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)a.sharedSizeBytes);
+  }
 }
 
 // Build a launch plan for tokens [t0, t1) cut into chunks of c tokens.
@@ -58,11 +73,20 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   p.nchunks = (int32_t)((t1 - t0 + c - 1) / c);
   p.items_per_chunk = (int64_t)lm * 2 * p.R * p.P;
   p.n_items = p.items_per_chunk * p.nchunks;
-  p.mig_t0 = t0;
-  p.mig_t1 = t1;
-  p.sig_c = (int32_t)c;
+  set_chunking(p, t0, t1, c);
   p.err = g_err_word;
   return p;
+}
+
+// The migration's own chunking for a launch that may cover a sub-range of it.
+// When the launch's chunks coincide with the migration's (same size, aligned
+// start), the kernels take the chunk index without a 64-bit division.
+void set_chunking(Plan& p, int64_t mig_t0, int64_t mig_t1, int64_t sig_c) {
+  p.mig_t0 = mig_t0;
+  p.mig_t1 = mig_t1;
+  p.sig_c = (int32_t)sig_c;
+  p.k_direct = (p.c == sig_c && (p.t0 - mig_t0) % sig_c == 0) ? 1 : 0;
+  p.k_base = p.k_direct ? (int32_t)((p.t0 - mig_t0) / sig_c) : 0;
 }
 
 // Plan of a head-sliced migration: `slice` bytes per token at byte scol of a
@@ -161,8 +185,7 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
   const size_t smem = (size_t)stages * piece;
   auto kern = ws ? k_copy_bulk_ws<SIG, Src> : k_copy_bulk<SIG, Src>;
   const int threads = ws ? 64 : 32;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
+  int occ = 0;  // (the dynamic shared memory limit was raised once in preload_kernels)
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
   if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
   int64_t cap = (int64_t)sms * occ;
@@ -319,9 +342,7 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
       Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
       if ((r = launch_copy(k2, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
       Plan k3 = make_plan(linear(dslot), paged(D, dids), row, sa, sb, l0, lm, sb - sa, D->desc.block_size, piece);
-      k3.mig_t0 = tr.begin;
-      k3.mig_t1 = tr.end;
-      k3.sig_c = (int32_t)c;
+      set_chunking(k3, tr.begin, tr.end, c);
       if (signal) {
         k3.counters = counters;
         k3.flags = D->inbox + (size_t)S->desc.instance * DYNA_MAX_CHUNKS;

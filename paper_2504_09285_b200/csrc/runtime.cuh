@@ -309,6 +309,7 @@ dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t 
 void preload_kernels();
 Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1, int l0, int lm, int64_t c,
                int64_t g, int piece);
+void set_chunking(Plan& p, int64_t mig_t0, int64_t mig_t1, int64_t sig_c);
 dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev, cudaStream_t st,
                         int schedule);
 dyna_status launch_batch(const BatchSource& src, int64_t n_items, int piece, int engine, int max_ctas, int stages,

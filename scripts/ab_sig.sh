@@ -1,4 +1,7 @@
-timeout 900 python -m pytest tests -m gpu -q -x -k "signal or ipc or ready" 2>&1 | tail -2
-ENGINE=2 bash scripts/ab_bench.sh paper_2504_09285_b200/libdyna_kv.so paper_2504_09285_b200/libdyna_kv_prev.so
-ENGINE=3 bash scripts/ab_bench.sh paper_2504_09285_b200/libdyna_kv.so
-ENGINE=1 bash scripts/ab_bench.sh paper_2504_09285_b200/libdyna_kv.so
+# A/B of per-chunk signalling cost per engine (scripts/sig_probe.py) across builds, interleaved.
+for i in 1 2; do
+  for lib in "$@"; do
+    echo "== $lib"
+    DYNA_KV_LIB=$PWD/$lib timeout 300 python scripts/sig_probe.py 2>&1 | grep engine
+  done
+done

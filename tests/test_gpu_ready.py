@@ -14,6 +14,21 @@ from gpu_util import dev_table, mapped_mask, pool_filled, torch_rows_equal, unto
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _no_gc_during_coupled_waits():
+    """A garbage-collected Pool left over from an earlier test destroys itself, and its inbox
+    cudaFree synchronises the device: inside a coupled migration's wait window that deadlocks
+    until the board's timeout (dyna_kv.h HAZARD).  Collect before each test, keep the collector
+    off while it runs."""
+    import gc
+    gc.collect()
+    gc.disable()
+    try:
+        yield
+    finally:
+        gc.enable()
+
+
 def _produce_chunk(fresh_t, src_t, g, a, b, stream):
     """Stand-in producer for chunk [a, b): ~1 ms of "prefill compute", then the chunk's KV
     lands in the source pool (copied from `fresh` with the library's own fused kernel).
@@ -177,7 +192,12 @@ def test_per_layer_marks_copy_each_layer_after_its_mark(c):
             dk.dyna_kv_ready_mark(board, k, e0, prod.cuda_stream)
         prod.synchronize()
         dk.dyna_kv_wait(dk.dyna_kv_migrate_on_ready(src_t, dst_t, (0, s), (0, lm), c, board, e0, mig.cuda_stream, o))
-        dk.dyna_kv_wait(dk.dyna_kv_migrate_ex(fresh_t, src_t, (0, 1), (0, 1), 1, prod.cuda_stream, None))
+        # warm every kernel the producer will launch while the coupled migration waits (a first
+        # launch loads its module lazily, which synchronises the context: dyna_kv.h HAZARD)
+        with torch.cuda.stream(prod):
+            torch.cuda._sleep(1000)
+        for n in sorted({c, s - (nck - 1) * c}):
+            dk.dyna_kv_wait(dk.dyna_kv_migrate_ex(fresh_t, src_t, (0, n), (0, 1), n, prod.cuda_stream, None))
         src = pool_filled(g, 1)
         dst = pool_filled(g, 2)
         src_t, dst_t = dev_table(src, ts), dev_table(dst, td)
