@@ -171,6 +171,12 @@ DYNA_API size_t dyna_kv_pool_bytes(const dyna_kv_pool_desc* desc);
  * library never frees it; keep it alive until dyna_kv_pool_destroy).  The
  * library allocates a small per-pool inbox of chunk flags on desc->device. */
 DYNA_API dyna_status dyna_kv_pool_create(const dyna_kv_pool_desc* desc, void* device_base, dyna_kv_pool_t* out);
+/* Destroy calls (pool, ready board, channel) never synchronise the device:
+ * the library's allocations are retired and released by the next call that
+ * allocates anyway (pool / board / channel create or import), so a destroy —
+ * e.g. from a binding object's garbage collection — cannot deadlock against a
+ * waiting producer-coupled migration.  Every migration using the object must
+ * have completed (dyna_kv_wait) before it is destroyed. */
 DYNA_API dyna_status dyna_kv_pool_destroy(dyna_kv_pool_t pool);
 
 /* Migrate src -> dst for token_range x layer_range in chunks of chunk_tokens
@@ -246,9 +252,8 @@ DYNA_API dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_
  * across requests with increasing epochs (dyna_kv_ready_begin).
  * HAZARD: while such a migration waits, anything that synchronises the whole
  * device (cudaDeviceSynchronize, cudaMalloc/cudaFree that sync — including
- * dyna_kv_pool_destroy, which frees the pool's flag inbox, e.g. from a
- * binding object's garbage collection — synchronous copies on the legacy
- * stream) before the last chunk is marked deadlocks: the
+ * this library's create / import calls, which allocate — synchronous copies
+ * on the legacy stream) before the last chunk is marked deadlocks: the
  * device waits for the migration, the migration for a mark that is never
  * issued.  The same holds for the FIRST launch of any kernel in the process
  * while the migration waits: CUDA loads kernels lazily and a module load

@@ -13,6 +13,7 @@ extern "C" {
 dyna_status dyna_kv_ready_create(int32_t device, int32_t max_chunks, dyna_kv_ready_t* out) {
   if (!out || device < 0 || max_chunks <= 0 || max_chunks > (1 << 24)) return fail(DYNA_EINVAL, "bad argument");
   *out = nullptr;
+  flush_retired();
   auto* b = new dyna_kv_ready();
   b->dev = device;
   b->max_chunks = max_chunks;
@@ -43,11 +44,11 @@ dyna_status dyna_kv_ready_create(int32_t device, int32_t max_chunks, dyna_kv_rea
 
 dyna_status dyna_kv_ready_destroy(dyna_kv_ready_t b) {
   if (!b) return fail(DYNA_EINVAL, "NULL board");
+  retire(b->dev, b->slots, Mem::Device);  // released by the next allocating call (no device sync here)
+  retire(b->dev, b->cancel_dev, Mem::Device);
+  retire(b->dev, b->cancel_stage, Mem::Host);
   {
     DeviceGuard g(b->dev);
-    cudaFree(b->slots);
-    cudaFree(b->cancel_dev);
-    cudaFreeHost(b->cancel_stage);
     cudaStreamDestroy(b->ctrl);
   }
   delete b;
@@ -102,6 +103,7 @@ dyna_status dyna_kv_channel_create(dyna_kv_pool_t dst, int32_t sender, int32_t s
   if (!out || !dst) return fail(DYNA_EINVAL, "NULL argument");
   *out = nullptr;
   if (dst->imported) return fail(DYNA_EINVAL, "create the channel on the destination pool's owner");
+  flush_retired();
   if (slots < 2 || slots > 1024 || slot_bytes == 0 || slot_bytes % 16 || sender < 0 || sender >= DYNA_MAX_INSTANCES)
     return fail(DYNA_EINVAL, "channel: 2 <= slots <= 1024, slot_bytes a positive multiple of 16, valid sender");
   auto* ch = new dyna_kv_channel();
@@ -155,6 +157,7 @@ dyna_status dyna_kv_channel_import(const dyna_kv_channel_handle* h, int32_t loca
   if (!h || !out) return fail(DYNA_EINVAL, "NULL argument");
   *out = nullptr;
   if (h->slots < 2 || h->slot_bytes == 0 || !desc_valid(&h->desc)) return fail(DYNA_EINVAL, "invalid channel handle");
+  flush_retired();
   DeviceGuard g(local_device);
   cudaIpcMemHandle_t mh{};
   std::memcpy(&mh, h->mem, sizeof mh);
@@ -183,18 +186,9 @@ dyna_status dyna_kv_channel_import(const dyna_kv_channel_handle* h, int32_t loca
 
 dyna_status dyna_kv_channel_destroy(dyna_kv_channel_t ch) {
   if (!ch) return fail(DYNA_EINVAL, "NULL channel");
-  if (ch->push_counters) {
-    DeviceGuard g(ch->push_counters_dev);
-    cudaFree(ch->push_counters);
-  }
-  {
-    DeviceGuard g(ch->dev);
-    if (ch->place_counters) cudaFree(ch->place_counters);
-    if (ch->imported)
-      cudaIpcCloseMemHandle(ch->base);
-    else
-      cudaFree(ch->base);
-  }
+  retire(ch->push_counters_dev, ch->push_counters, Mem::Device);  // no device sync in a destroy
+  retire(ch->dev, ch->place_counters, Mem::Device);
+  retire(ch->dev, ch->base, ch->imported ? Mem::Ipc : Mem::Device);
   delete ch;
   return DYNA_OK;
 }

@@ -271,7 +271,40 @@ std::map<int, UploadRing*> g_rings;
 }  // namespace rt
 }  // namespace dynakv
 
+namespace dynakv {
+namespace rt {
+struct Retired {
+  int dev;
+  void* ptr;
+  Mem kind;
+};
+static std::mutex g_retired_mu;
+static std::vector<Retired> g_retired;
+
+void retire(int dev, void* ptr, Mem kind) {
+  if (!ptr) return;
+  std::lock_guard<std::mutex> lk(g_retired_mu);
+  g_retired.push_back({dev, ptr, kind});
+}
+
+void flush_retired() {
+  std::vector<Retired> v;
+  {
+    std::lock_guard<std::mutex> lk(g_retired_mu);
+    v.swap(g_retired);
+  }
+  for (const Retired& r : v) {
+    DeviceGuard g(r.dev);
+    if (r.kind == Mem::Device) cudaFree(r.ptr);
+    else if (r.kind == Mem::Host) cudaFreeHost(r.ptr);
+    else cudaIpcCloseMemHandle(r.ptr);
+  }
+}
+}  // namespace rt
+}  // namespace dynakv
+
 extern "C" {
+
 
 const char* dyna_kv_last_error(void) { return g_err.c_str(); }
 
@@ -312,6 +345,7 @@ dyna_status dyna_kv_pool_create(const dyna_kv_pool_desc* desc, void* device_base
   if (!out || !desc || !device_base) return fail(DYNA_EINVAL, "NULL argument");
   *out = nullptr;
   if (!desc_valid(desc)) return fail(DYNA_EINVAL, "invalid pool descriptor");
+  flush_retired();
   const int64_t row = (int64_t)desc->num_kv_heads * desc->head_dim * desc->elem_bytes;
   if (row % 16) return fail(DYNA_EGEOM, "row bytes H*d*e = %lld is not a multiple of 16", (long long)row);
   if (reinterpret_cast<uintptr_t>(device_base) % 256) return fail(DYNA_EINVAL, "device_base not 256-B aligned");
@@ -340,27 +374,15 @@ dyna_status dyna_kv_pool_create(const dyna_kv_pool_desc* desc, void* device_base
 
 dyna_status dyna_kv_pool_destroy(dyna_kv_pool_t p) {
   if (!p) return fail(DYNA_EINVAL, "NULL pool");
-  {
-    DeviceGuard g(p->dev);
-    for (auto& kv : p->channels) {
-      for (auto& c : kv.second.counters) {
-        DeviceGuard g2(c.first);
-        cudaFree(c.second);
-      }
-      if (kv.second.sstage) {
-        DeviceGuard g2(kv.second.sdev);
-        cudaFree(kv.second.sstage);
-      }
-      if (kv.second.dstage) {
-        DeviceGuard g2(kv.second.ddev);
-        cudaFree(kv.second.dstage);
-      }
-    }
-    if (p->own_inbox) cudaFree(p->inbox);
-    if (p->imported) {
-      if (p->ipc_pool_map) cudaIpcCloseMemHandle(p->ipc_pool_map);
-      if (p->ipc_inbox_map) cudaIpcCloseMemHandle(p->ipc_inbox_map);
-    }
+  for (auto& kv : p->channels) {  // retired, not freed: a destroy never synchronises the device
+    for (auto& c : kv.second.counters) retire(c.first, c.second, Mem::Device);
+    retire(kv.second.sdev, kv.second.sstage, Mem::Device);
+    retire(kv.second.ddev, kv.second.dstage, Mem::Device);
+  }
+  if (p->own_inbox) retire(p->dev, p->inbox, Mem::Device);
+  if (p->imported) {
+    retire(p->dev, p->ipc_pool_map, Mem::Ipc);
+    retire(p->dev, p->ipc_inbox_map, Mem::Ipc);
   }
   delete p;
   return DYNA_OK;
@@ -401,6 +423,7 @@ dyna_status dyna_kv_pool_import(const dyna_kv_ipc_handle* h, int32_t local_devic
   if (!h || !out) return fail(DYNA_EINVAL, "NULL argument");
   *out = nullptr;
   if (!desc_valid(&h->desc)) return fail(DYNA_EINVAL, "invalid descriptor in handle");
+  flush_retired();
   DeviceGuard g(local_device);
   cudaIpcMemHandle_t hp{}, hi{};
   std::memcpy(&hp, h->pool_mem, sizeof hp);

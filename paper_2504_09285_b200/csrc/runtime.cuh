@@ -94,6 +94,15 @@ dyna_status ensure_peer(int dev, int peer);
 uint64_t next_epoch(int sender, const dyna_kv_pool* dst);
 dyna_status check_host_tables(const dyna_block_table& src, const dyna_block_table& dst, int64_t t0, int64_t t1);
 
+// Deferred release.  cudaFree / cudaFreeHost / cudaIpcCloseMemHandle may synchronise the
+// device, which deadlocks against a producer-coupled migration that is waiting for marks
+// (and a binding object's garbage collection can destroy a pool at any moment).  So the
+// destroy calls only retire their allocations; they are released by the next call that
+// allocates anyway (pool / board / channel create or import), or at process exit.
+enum class Mem { Device, Host, Ipc };
+void retire(int dev, void* ptr, Mem kind);
+void flush_retired();
+
 }  // namespace rt
 }  // namespace dynakv
 

@@ -335,3 +335,44 @@ def test_cancel_before_launch_and_later_epochs_unaffected():
         assert np.array_equal(dst.tensor.cpu().numpy(), _oracle_expect(1, g, ts, 2, td, (0, 100)))
     finally:
         dk.dyna_kv_ready_destroy(board)
+
+
+def test_destroy_during_coupled_wait_does_not_deadlock():
+    """Destroying a pool, a ready board and a channel while a coupled migration waits for marks
+    must not synchronise the device (their memory is retired, released by a later allocating call)."""
+    import time
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    victim, victim_dst = pool_filled(g, 3), pool_filled(g, 4)
+    ts, td = kvgen.table_pair(1, 256, g, g)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    vt, vdt = dev_table(victim, ts), dev_table(victim_dst, td)
+    dk.dyna_kv_wait(dk.migrate(vt, vdt, (0, 100), (0, 2), 32, flags=dk.DYNA_MIGRATE_SIGNAL))  # channel counters
+    ch = dk.dyna_kv_channel_create(victim_dst.handle, 5, 2, 1 << 16)
+    other = dk.dyna_kv_ready_create(0, 4)
+    board = dk.dyna_kv_ready_create(0, 8)
+    dk.dyna_kv_ready_set_timeout(board, 30_000_000_000)
+    prod, mig = torch.cuda.Stream(), torch.cuda.Stream()
+    try:
+        torch.cuda.synchronize()
+        epoch = dk.dyna_kv_ready_begin(board)
+        x = dk.dyna_kv_migrate_on_ready(st, dt, (0, 100), (0, 2), 32, board, epoch, mig.cuda_stream,
+                                        dk.opts(max_ctas=2))
+        t = time.perf_counter()
+        victim.close()                        # inbox + channel counters retired, not freed
+        victim_dst.close()
+        dk.dyna_kv_channel_destroy(ch)
+        dk.dyna_kv_ready_destroy(other)
+        for k in range(4):
+            dk.dyna_kv_ready_mark(board, k, epoch, prod.cuda_stream)
+        dk.dyna_kv_wait(x)
+        assert time.perf_counter() - t < 10.0
+        torch.cuda.synchronize()
+        want = kvgen.fill_bytes(2, g.pool_bytes)
+        import oracle
+        oracle.migrate(kvgen.fill_bytes(1, g.pool_bytes), g, ts, want, g, td, (0, 100))
+        assert np.array_equal(dst.tensor.cpu().numpy(), want)
+        extra = pool_filled(g, 9)             # an allocating call releases the retired memory
+        extra.close()
+    finally:
+        dk.dyna_kv_ready_destroy(board)
