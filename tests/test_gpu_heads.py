@@ -148,3 +148,51 @@ def test_tp_reshard_round_trip_full_llama3_rows(tp_s, tp_d):
     want = kvgen.fill_bytes(60, g1.pool_bytes)
     oracle.migrate(full_s.tensor.cpu().numpy(), g1, t1s, want, g1, t1d, (0, s))
     assert np.array_equal(back.tensor.cpu().numpy(), want)
+
+
+def test_full_size_qwen72b_tp4_to_tp8_sampled():
+    """BASELINE.json configs[4] geometry (Qwen2-72B: 80 layers, 8 KV heads, d128, bf16, block 16,
+    NB 6144 per pool) resharded from a TP-4 rank (2 heads) onto two TP-8 ranks (1 head each):
+    sampled rows against the oracle's offsets (kvgen bytes), every row by a property check
+    (destination head slice == source head slice through both tables), heads of other rows
+    untouched."""
+    H = 8
+    gs = kvgen.QWEN2_72B.with_(num_kv_heads=2)
+    gd = kvgen.QWEN2_72B.with_(num_kv_heads=1)
+    s = 4096                                        # one 4096-token prompt (the 4' target shape)
+    src = pool_filled(gs, 300)
+    ts = kvgen.table_pair(301, s, gs, gs)[0]
+    plan = [e for e in dd.tp_reshard_plan(H, 4, 8) if e[0] == 1]
+    assert [(b, heads, hd0) for _, b, heads, hd0 in plan] == [(2, (0, 1), 0), (3, (1, 2), 0)]
+    rng = np.random.default_rng(7)
+    st = dev_table(src, ts)
+    for _, b, heads, hd0 in plan:
+        dst = pool_filled(gd, 310 + b)
+        td = kvgen.table_pair(320 + b, s, gd, gd)[1]
+        dt = dev_table(dst, td)
+        dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(st, dt, (0, s), (0, 80), heads, hd0, 1024, 0))
+        torch.cuda.synchronize()
+        he = gs.head_dim * gs.elem_bytes
+        bad = 0
+        for _ in range(1500):                       # sampled: the oracle's offsets, kvgen's bytes
+            l, kv, t = int(rng.integers(0, 80)), int(rng.integers(0, 2)), int(rng.integers(0, s))
+            so = oracle.logical_off(gs, ts, l, kv, t, heads[0], 0)
+            do = oracle.logical_off(gd, td, l, kv, t, hd0, 0)
+            want = kvgen.bytes_at(300, so, (heads[1] - heads[0]) * he)
+            bad += int(not np.array_equal(dst.tensor[do:do + len(want)].cpu().numpy(), want))
+        assert bad == 0
+        S = src.tensor.view(80, 2, gs.num_blocks, 16, 2, he)     # every row, property form
+        D = dst.tensor.view(80, 2, gd.num_blocks, 16, 1, he)
+        Ts = torch.as_tensor(ts.astype(np.int64), device="cuda")
+        Td = torch.as_tensor(td.astype(np.int64), device="cuda")
+        for a in range(0, s, 2048):
+            t = torch.arange(a, min(a + 2048, s), device="cuda")
+            assert torch.equal(D[:, :, Td[t // 16], t % 16, hd0:hd0 + 1], S[:, :, Ts[t // 16], t % 16, heads[0]:heads[1]])
+        mask = torch.zeros(80, 2, gd.num_blocks, 16, dtype=torch.bool, device="cuda")
+        t = torch.arange(0, s, device="cuda")
+        mask[:, :, Td[t // 16], t % 16] = True
+        ref = torch.empty_like(dst.tensor)
+        dk.dyna_kv_debug_fill(ref.data_ptr(), ref.numel(), 310 + b, 0, torch.cuda.current_stream().cuda_stream)
+        assert torch.equal(D[~mask], ref.view_as(D)[~mask])
+        del dst, ref, D
+        torch.cuda.empty_cache()
