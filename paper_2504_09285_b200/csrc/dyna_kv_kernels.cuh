@@ -57,9 +57,19 @@ __device__ __forceinline__ Item decode_item(const Plan& p, int64_t item) {
   const int64_t k = item / p.items_per_chunk;
   int64_t i = item - k * p.items_per_chunk;
   const int32_t pp = (int32_t)(i % p.P); i /= p.P;
-  const int32_t j = (int32_t)(i % p.R);  i /= p.R;
-  const int kv = (int)(i & 1);
-  const int l = p.l0 + (int)(i >> 1);
+  int32_t j;
+  int kv, l;
+  if (p.J == p.R) {  // (layer, K|V) slowest: concurrent items walk the runs of one slab
+    j = (int32_t)(i % p.R);  i /= p.R;
+    kv = (int)(i & 1);
+    l = p.l0 + (int)(i >> 1);
+  } else {           // groups of J runs, each group over every (layer, K|V) slab
+    const int32_t jj = (int32_t)(i % p.J);  i /= p.J;
+    const int32_t lk = (int32_t)(i % (2 * p.lm));
+    j = (int32_t)(i / (2 * p.lm)) * p.J + jj;  // j >= runs of the chunk: an empty item
+    kv = lk & 1;
+    l = p.l0 + (lk >> 1);
+  }
   const int64_t a = p.t0 + k * p.c;
   const int64_t b = min(a + (int64_t)p.c, p.t1);
   const int64_t G = a / p.g + j;

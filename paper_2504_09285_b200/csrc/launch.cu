@@ -74,8 +74,24 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   p.items_per_chunk = (int64_t)lm * 2 * p.R * p.P;
   p.n_items = p.items_per_chunk * p.nchunks;
   set_chunking(p, t0, t1, c);
+  static const int jgroup = [] {  // experiment switch
+    const char* e = std::getenv("DYNA_KV_JGROUP");
+    return e ? std::atoi(e) : 0;
+  }();
+  set_run_groups(p, jgroup);
   p.err = g_err_word;
   return p;
+}
+
+// Item order inside a chunk: groups of J runs, each group visiting every (layer, K|V)
+// slab before the next group (J <= 0 or J >= R: the plain layer-major order).  The run
+// count is padded to a multiple of J; padding items are empty.
+void set_run_groups(Plan& p, int J) {
+  const int32_t R = p.R;
+  p.J = (J <= 0 || J >= R) ? R : J;
+  const int64_t rpad = (R + p.J - 1) / p.J * p.J;
+  p.items_per_chunk = (int64_t)p.lm * 2 * rpad * p.P;
+  p.n_items = p.items_per_chunk * p.nchunks;
 }
 
 // The migration's own chunking for a launch that may cover a sub-range of it.
@@ -101,6 +117,7 @@ Plan make_plan_sliced(const Side& s, const Side& d, int64_t slice, int64_t spitc
   p.dcol = (int32_t)dcol;
   p.tpp = (int32_t)std::max<int64_t>(1, piece / slice);
   p.P = (int32_t)((std::min(g, c) + p.tpp - 1) / p.tpp);
+  p.J = p.R;  // the sliced decode uses the layer-major order
   p.items_per_chunk = (int64_t)lm * 2 * p.R * p.P;
   p.n_items = p.items_per_chunk * p.nchunks;
   p.vps = (int32_t)(slice / 16);

@@ -32,6 +32,7 @@ struct Plan {
   // e.g. one staging sub-chunk): flags and counters are per migration chunk.
   int64_t mig_t0, mig_t1;   // the whole migration's token range
   int32_t sig_c;            // the migration's chunk tokens
+  int32_t J;                // runs per group: item order inside a chunk is (run group, l, kv, run, piece); J == R: (l, kv, run, piece)
   int32_t k_direct;         // 1: launch chunk k is migration chunk k + k_base (no division in the decode)
   int32_t k_base;
   // per-chunk completion signal (counters == nullptr: none)

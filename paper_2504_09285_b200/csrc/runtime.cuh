@@ -319,6 +319,7 @@ void preload_kernels();
 Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1, int l0, int lm, int64_t c,
                int64_t g, int piece);
 void set_chunking(Plan& p, int64_t mig_t0, int64_t mig_t1, int64_t sig_c);
+void set_run_groups(Plan& p, int J);
 dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev, cudaStream_t st,
                         int schedule);
 dyna_status launch_batch(const BatchSource& src, int64_t n_items, int piece, int engine, int max_ctas, int stages,
