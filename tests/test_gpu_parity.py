@@ -314,3 +314,43 @@ def test_round_trip_identity_on_gpu(engine):
     A.tensor.view(gA.num_layers, 2, gA.num_blocks, gA.block_size, gA.row_bytes)[m] = 0xA5   # poison
     migrate_and_wait(B, tb, A, ta, (0, s), (0, 4), 512, engine=engine)
     assert np.array_equal(A.tensor.cpu().numpy(), hA)
+
+
+@pytest.mark.parametrize("variant,engine", list(itertools.product(VARIANTS, ENGINES)))
+def test_flag_litmus_chunk_visible_when_flagged(variant, engine):
+    """Flag-protocol litmus: a consumer stream waits for chunk k's flag and at once
+    snapshots chunk k's destination rows, while the (deliberately slow: 2 CTAs) migration is
+    still writing later chunks.  Every snapshot must already hold the source rows — a flag
+    released before its chunk's stores were visible would show stale bytes.  Many epochs,
+    random chunk sizes, random consumer wait order."""
+    g = LLAMA3_ROWS
+    rng = np.random.default_rng(123)
+    src, dst = pool_filled(g, 31, instance=6), pool_filled(g, 32)
+    ts, td = kvgen.table_pair(33, 3000, g, g)
+    s = 3000
+    row = g.row_bytes
+    S = src.tensor.view(g.num_layers, 2, g.num_blocks, g.block_size, row)
+    D = dst.tensor.view_as(S)
+    Ts = torch.as_tensor(ts.astype(np.int64), device="cuda")
+    Td = torch.as_tensor(td.astype(np.int64), device="cuda")
+    consumer = torch.cuda.Stream()
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    for rep in range(8):
+        c = int(rng.choice([64, 128, 200, 512]))
+        dst.tensor.zero_()                                   # stale contents: zeros
+        torch.cuda.synchronize()
+        x = dk.migrate(st, dt, (0, s), (0, g.num_layers), c, variant=variant, engine=engine, max_ctas=2,
+                       flags=dk.DYNA_MIGRATE_SIGNAL)
+        epoch, nchunks, sender = dk.dyna_kv_xfer_info(x)
+        snaps = {}
+        with torch.cuda.stream(consumer):
+            for k in rng.permutation(nchunks):
+                dk.dyna_kv_stream_wait_chunk(dst.handle, sender, int(k), epoch, 10_000_000_000, consumer.cuda_stream)
+                t = torch.arange(int(k) * c, min((int(k) + 1) * c, s), device="cuda")
+                snaps[int(k)] = D[:, :, Td[t // g.block_size], t % g.block_size].clone()
+        consumer.synchronize()
+        dk.dyna_kv_wait(x)
+        dk.dyna_kv_poll_error()
+        for k, snap in snaps.items():
+            t = torch.arange(k * c, min((k + 1) * c, s), device="cuda")
+            assert torch.equal(snap, S[:, :, Ts[t // g.block_size], t % g.block_size]), (rep, c, k)
