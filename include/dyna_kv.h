@@ -121,6 +121,10 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
 #define DYNA_ENGINE_VEC  1     /* warp-per-segment 16-B vector loads/stores (LDG.128 / STG.128) */
 #define DYNA_ENGINE_BULK 2     /* TMA bulk copies through a shared-memory ring (UBLKCP), one issuing thread */
 #define DYNA_ENGINE_BULK_WS 3  /* same ring, warp-specialised: a loader warp and a storer warp (mbarrier hand-off) */
+#define DYNA_ENGINE_DMA  4     /* copy engines, no SM: one cudaMemcpyBatchAsync per chunk over the contiguous
+                                  runs ("DMA-pushed"); FUSED variant only, needs host_block_ids on both
+                                  tables, not for producer-coupled migrations (DYNA_ENOTSUP otherwise); with
+                                  DYNA_MIGRATE_SIGNAL a one-thread kernel releases each chunk's flag after its batch */
 /* flags */
 #define DYNA_MIGRATE_SIGNAL 1  /* write a per-chunk flag into the destination pool's inbox */
 #define DYNA_READY_PER_LAYER 2 /* dyna_kv_migrate_on_ready: one ready mark per (chunk, layer), see below */

@@ -28,7 +28,7 @@ dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream) {
 dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
   *o = dyna_kv_opts{};
   if (opts) *o = *opts;
-  if ((o->flags & ~(DYNA_MIGRATE_SIGNAL | DYNA_READY_PER_LAYER)) != 0 || o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > 3 || o->max_ctas < 0 || o->piece_bytes < 0 ||
+  if ((o->flags & ~(DYNA_MIGRATE_SIGNAL | DYNA_READY_PER_LAYER)) != 0 || o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > DYNA_ENGINE_DMA || o->max_ctas < 0 || o->piece_bytes < 0 ||
       o->piece_bytes % 16 || o->stages < 0 || o->stages == 1 || o->stages > kMaxStages ||
       (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16) || o->schedule < 0 ||
       o->schedule > DYNA_SCHED_DYNAMIC)
@@ -105,6 +105,73 @@ size_t table_upload_bytes(const dyna_block_table& t, int64_t t1) {
 }  // namespace rt
 }  // namespace dynakv
 
+namespace dynakv {
+namespace rt {
+
+// DMA engine: the copy engines move the contiguous runs (one run = the rows of one
+// (layer, K|V) of a token-grid cell, contiguous on both sides; adjacent runs that stay
+// contiguous on both sides are merged), one cudaMemcpyBatchAsync per chunk in chunk
+// order, marked to overlap with compute.  No SM does any copying; with per-chunk flags a
+// one-thread kernel releases chunk k's flag after chunk k's batch (stream order: the
+// batch's copies are complete before it runs).
+dyna_status run_dma(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* hs, const int32_t* hd, dyna_range tr, int l0,
+                    int lm, int64_t c, unsigned long long* flags, uint64_t epoch, cudaStream_t stream) {
+  const int64_t row = S->row;
+  const int64_t bss = S->desc.block_size, bsd = D->desc.block_size;
+  const int64_t nbs = S->desc.num_blocks, nbd = D->desc.num_blocks;
+  const int64_t g = gcd64(bss, bsd);
+  std::vector<void*> dsts, srcs;
+  std::vector<size_t> sizes;
+  cudaMemcpyAttributes attr{};
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  static const int mode = [] {  // experiment switch: 0 batch + overlap hint, 1 batch, 2 one cudaMemcpyAsync per run
+    const char* e = std::getenv("DYNA_KV_DMA_MODE");
+    return e ? std::atoi(e) : 0;
+  }();
+  attr.flags = mode == 0 ? cudaMemcpyFlagPreferOverlapWithCompute : 0;
+  size_t attr_idx = 0;
+  int32_t k = 0;
+  for (int64_t a = tr.begin; a < tr.end; a += c, ++k) {
+    const int64_t b = std::min<int64_t>(a + c, tr.end);
+    dsts.clear();
+    srcs.clear();
+    sizes.clear();
+    for (int l = l0; l < l0 + lm; ++l)
+      for (int kv = 0; kv < 2; ++kv)
+        for (int64_t t = a; t < b;) {
+          const int64_t te = std::min<int64_t>(b, (t / g + 1) * g);
+          char* sp = S->base + ((((int64_t)l * 2 + kv) * nbs + hs[t / bss]) * bss + t % bss) * row;
+          char* dp = D->base + ((((int64_t)l * 2 + kv) * nbd + hd[t / bsd]) * bsd + t % bsd) * row;
+          const size_t n = (size_t)((te - t) * row);
+          if (!sizes.empty() && (char*)srcs.back() + sizes.back() == sp && (char*)dsts.back() + sizes.back() == dp)
+            sizes.back() += n;  // still contiguous on both sides
+          else {
+            srcs.push_back(sp);
+            dsts.push_back(dp);
+            sizes.push_back(n);
+          }
+          t = te;
+        }
+    if (mode == 2 || stream == nullptr) {  // (the batch API refuses the legacy stream)
+      for (size_t i = 0; i < sizes.size(); ++i)
+        CUDA_TRY(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDeviceToDevice, stream));
+    } else {
+      size_t fail_idx = 0;
+      cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx,
+                                           1, &fail_idx, stream);
+      if (e != cudaSuccess)
+        return fail(DYNA_ECUDA, "cudaMemcpyBatchAsync (%zu copies, failed at %zu): %s", sizes.size(), fail_idx,
+                    cudaGetErrorString(e));
+    }
+    if (flags) launch_release_sys(flags + k, epoch, stream);
+  }
+  if (flags) CUDA_TRY(cudaGetLastError());
+  return DYNA_OK;
+}
+
+}  // namespace rt
+}  // namespace dynakv
+
 extern "C" {
 
 dyna_status dyna_kv_migrate(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
@@ -159,6 +226,11 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   } else if (o.flags & DYNA_READY_PER_LAYER) {
     return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board (dyna_kv_migrate_on_ready)");
   }
+  if (o.engine == DYNA_ENGINE_DMA) {
+    if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "DMA engine: FUSED variant only");
+    if (!src.host_block_ids || !dst.host_block_ids)
+      return fail(DYNA_ENOTSUP, "DMA engine: the copy list is built on the host from host_block_ids (both tables)");
+  }
   if (empty) {  // s = 0 (or no layers) -> nothing to ship, nothing enqueued
     auto* x = new dyna_kv_xfer();
     x->dev = S->dev;
@@ -195,7 +267,7 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   RingLease lease(S->dev);
   const int32_t* sids = src.block_ids;
   const int32_t* dids = dst.block_ids;
-  if (!sids || !dids) {
+  if ((!sids || !dids) && engine != DYNA_ENGINE_DMA) {  // (DMA reads the host ids itself)
     if (variant == DYNA_VARIANT_STAGED && D->dev != S->dev)
       return fail(DYNA_ENOTSUP, "cross-device STAGED needs device block_ids for the destination");
     const size_t sb = sids ? 0 : (table_upload_bytes(src, tr.end) + 15) & ~size_t(15);
@@ -219,7 +291,15 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   x->stages = engine != DYNA_ENGINE_VEC ? stages : 0;
   x->unroll = engine == DYNA_ENGINE_VEC ? unroll : 0;
   const uint64_t launches0 = g_launches.load();
-  if (variant == DYNA_VARIANT_FUSED) {
+  if (engine == DYNA_ENGINE_DMA) {
+    unsigned long long* flags = nullptr;
+    uint64_t epoch = 0;
+    if (signal) {
+      flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
+      epoch = x->epoch = next_epoch(gs.instance, D);
+    }
+    r = run_dma(S, D, src.host_block_ids, dst.host_block_ids, tr, l0, lm, c, flags, epoch, stream);
+  } else if (variant == DYNA_VARIANT_FUSED) {
     // K4 / K4-local: source rows -> destination rows, one launch for all chunks.
     const int64_t g = gcd64(gs.block_size, gd.block_size);
     Plan p = make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);

@@ -346,6 +346,8 @@ dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& d
 dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D);
 Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok, int64_t run_bytes);
 size_t table_upload_bytes(const dyna_block_table& t, int64_t t1);
+dyna_status run_dma(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* hs, const int32_t* hd, dyna_range tr, int l0,
+                    int lm, int64_t c, unsigned long long* flags, uint64_t epoch, cudaStream_t stream);
 
 }  // namespace rt
 }  // namespace dynakv

@@ -26,13 +26,13 @@ def main():
     dk.dyna_kv_debug_fill(src.tensor.data_ptr(), src.tensor.numel(), 1, 0, cs)
     dk.dyna_kv_debug_fill(dst.tensor.data_ptr(), dst.tensor.numel(), 2, 0, cs)
     s, c = int(os.environ.get("S", 1024)), int(os.environ.get("C", 256))
-    engines = [int(e) for e in os.environ.get("ENGINES", "1,2,3").split(",")]
+    engines = [int(e) for e in os.environ.get("ENGINES", "1,2,3,4").split(",")]
     tabs = kvgen.batch_tables(500, [max(s, 2048)] * 4, g, g) if s <= 2048 else kvgen.batch_tables(500, [s] * 2, g, g) * 2
     T = [(dk.table(src, torch.from_numpy(a).cuda(), a), dk.table(dst, torch.from_numpy(b).cuda(), b)) for a, b in tabs]
     payload = s * 2 * g.num_layers * g.row_bytes
     out = []
-    for engine, piece, stages, unroll in [e for e in ((1, 8192, 0, 8), (2, 32768, 6, 0), (3, 32768, 6, 0))
-                                          if e[0] in engines]:
+    for engine, piece, stages, unroll in [e for e in ((1, 8192, 0, 8), (2, 32768, 6, 0), (3, 32768, 6, 0),
+                                                      (4, 0, 0, 0)) if e[0] in engines]:
         for sig in (0, 1):
             o = dk.opts(variant=1, engine=engine, piece_bytes=piece, stages=stages, unroll=unroll,
                         flags=dk.DYNA_MIGRATE_SIGNAL if sig else 0)
