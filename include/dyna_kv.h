@@ -230,9 +230,15 @@ DYNA_API dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_tabl
  * requests, e.g. configs[2]'s 64-request skewed batch).  Every non-empty entry
  * is validated like dyna_kv_migrate; all sources must live on one device (the
  * launching device, `stream`'s) and share one row size; destinations may be
- * any reachable pools.  FUSED variant only, no per-chunk signalling
- * (DYNA_ENOTSUP otherwise).  n <= DYNA_MAX_BATCH.  The descriptors are copied
- * before the call returns; block tables follow dyna_block_table's rules. */
+ * any reachable pools.  FUSED variant only (DYNA_ENOTSUP otherwise; no DMA
+ * engine).  n <= DYNA_MAX_BATCH.  The descriptors are copied before the call
+ * returns; block tables follow dyna_block_table's rules.
+ * Per-chunk signalling (opts->flags & DYNA_MIGRATE_SIGNAL; VEC engine): every
+ * entry gets its own epoch and a disjoint range of inbox slots of its
+ * (sender, destination pool) — see dyna_kv_batch_info — so each request's
+ * r^beta can start as soon as its own chunks landed.  The signalled chunks of
+ * one batch into one destination pool from one sender must fit in
+ * DYNA_MAX_CHUNKS (DYNA_ERANGE otherwise). */
 #define DYNA_MAX_BATCH 16384
 typedef struct {
     dyna_block_table src, dst;
@@ -241,6 +247,13 @@ typedef struct {
 DYNA_API dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna_range layer_range,
                                            int32_t chunk_tokens, struct CUstream_st* stream,
                                            const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
+/* Signalled batch: chunk j (0-based, of that entry's token range) of entry
+ * `index` is resident when the destination inbox slot [sender][first_slot + j]
+ * holds a value >= epoch (dyna_kv_stream_wait_chunk / dyna_kv_copy_flags with
+ * chunk = first_slot + j).  Empty entries report num_chunks = 0.  DYNA_EINVAL
+ * for a handle that is not a signalled batch. */
+DYNA_API dyna_status dyna_kv_batch_info(dyna_kv_xfer_t xfer, int32_t index, uint64_t* epoch, int32_t* first_slot,
+                                        int32_t* num_chunks, int32_t* sender);
 
 /* Producer-coupled push (§4.3: "once chunk
  * k completes, its KV block is immediately DMA-pushed ... while Server1

@@ -43,7 +43,7 @@ EXPORTS = (
     "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready", "dyna_kv_ready_set_timeout",
     "dyna_kv_channel_create", "dyna_kv_channel_export", "dyna_kv_channel_import", "dyna_kv_channel_destroy",
     "dyna_kv_push", "dyna_kv_place", "dyna_kv_channel_set_timeout", "dyna_kv_ready_cancel",
-    "dyna_kv_migrate_heads",
+    "dyna_kv_migrate_heads", "dyna_kv_batch_info",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -106,6 +106,8 @@ def _load():
                                  p(vp)]),
         "dyna_kv_migrate_ex": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
                                     vp, p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_batch_info": (st, [vp, ctypes.c_int32, p(ctypes.c_uint64), p(ctypes.c_int32), p(ctypes.c_int32),
+                                    p(ctypes.c_int32)]),
         "dyna_kv_migrate_heads": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, dyna_range,
                                        ctypes.c_int32, ctypes.c_int32, vp, p(dyna_kv_opts), p(vp)]),
         "dyna_kv_migrate_batch": (st, [p(dyna_kv_migration), ctypes.c_int32, dyna_range, ctypes.c_int32, vp,
@@ -191,6 +193,14 @@ def dyna_kv_migrate_ex(src: dyna_block_table, dst: dyna_block_table, token_range
                                   ctypes.c_void_p(stream), ctypes.byref(opts) if opts is not None else None,
                                   ctypes.byref(out)))
     return out.value
+
+
+def dyna_kv_batch_info(xfer: int, index: int) -> tuple[int, int, int, int]:
+    """(epoch, first_slot, num_chunks, sender) of entry `index` of a signalled batch."""
+    e, f, n, snd = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.dyna_kv_batch_info(ctypes.c_void_p(xfer), index, ctypes.byref(e), ctypes.byref(f), ctypes.byref(n),
+                                  ctypes.byref(snd)))
+    return e.value, f.value, n.value, snd.value
 
 
 def dyna_kv_migrate_heads(src: dyna_block_table, dst: dyna_block_table, token_range, layer_range, src_heads,

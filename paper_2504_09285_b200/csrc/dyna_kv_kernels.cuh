@@ -25,6 +25,7 @@
 //   item      = (k, l, kv, j, p), chunk-major so chunk 0 completes first.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "plan.cuh"
 
@@ -404,7 +405,9 @@ __global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : 3) k_copy_vec(co
   // Signalling: a warp's consecutive items mostly share a chunk (chunk-major
   // order), so bytes are accumulated per chunk and fenced + counted once when
   // the warp moves on to another chunk — one fence per (warp, chunk), not per item.
+  constexpr bool kBatch = std::is_same<Src, BatchSource>::value;
   int32_t cur_k = -1;
+  const Plan* cur_p = nullptr;     // batches: the plan (request) chunk cur_k belongs to (flags are per request)
   unsigned long long cur_acc = 0;  // bytes of chunk cur_k, plus kPoison once if any of them was skipped
   int32_t ready_slot = -1;
   bool skip = false;      // READY: the current ready slot was cancelled
@@ -417,13 +420,15 @@ __global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : 3) k_copy_vec(co
     int64_t item = gitem;
     const Plan& p = src.locate(item);
     const Item it = decode_item(p, item);
-    if (SIGNAL && it.acc && it.k != cur_k) {
+    if (SIGNAL && it.acc && (it.k != cur_k || (kBatch && &p != cur_p))) {
       if (cur_acc) {
-        fence_for(p);   // every lane's stores of chunk cur_k are performed ...
+        const Plan& cp = kBatch ? *cur_p : p;  // (single plan: always the same)
+        fence_for(cp);  // every lane's stores of chunk cur_k are performed ...
         __syncwarp();   // ... before lane 0 counts them
-        if (lane == 0) account_chunk(p, cur_k, cur_acc);   // (SIGNAL => single plan: same p)
+        if (lane == 0) account_chunk(cp, cur_k, cur_acc);
       }
       cur_k = it.k;
+      if (kBatch) cur_p = &p;
       cur_acc = 0;
     }
     if (READY && it.acc) {
@@ -442,10 +447,11 @@ __global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : 3) k_copy_vec(co
     if (it.n) warp_copy<U, !READY>(it.src, it.dst, it.n, lane);
     if (SIGNAL) cur_acc += it.acc;
   }
-  if (SIGNAL && cur_acc) {  // signalling is single-plan only
-    fence_for(src.locate_signal());
+  if (SIGNAL && cur_acc) {
+    const Plan& cp = kBatch ? *cur_p : src.locate_signal();
+    fence_for(cp);
     __syncwarp();
-    if (lane == 0) account_chunk(src.locate_signal(), cur_k, cur_acc);
+    if (lane == 0) account_chunk(cp, cur_k, cur_acc);
   }
   if (lane == 0) sched.finish((unsigned long long)nwarps);
 }

@@ -26,6 +26,8 @@ void preload_kernels() {
       (const void*)k_copy_vec<16, false, SingleSource, false>, (const void*)k_copy_vec<16, true, SingleSource, false>,
       (const void*)k_copy_vec<8, false, SingleSource, true>, (const void*)k_copy_vec<8, true, SingleSource, true>,
       (const void*)k_copy_vec<4, false, BatchSource, false>, (const void*)k_copy_vec<8, false, BatchSource, false>,
+      (const void*)k_copy_vec<4, true, BatchSource, false>, (const void*)k_copy_vec<8, true, BatchSource, false>,
+      (const void*)k_copy_vec<16, true, BatchSource, false>,
       (const void*)k_copy_vec<16, false, BatchSource, false>,
       (const void*)k_copy_bulk<false, SingleSource>, (const void*)k_copy_bulk<true, SingleSource>,
       (const void*)k_copy_bulk<false, BatchSource>,
@@ -388,9 +390,9 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
   return r;
 }
 
-dyna_status launch_batch(const BatchSource& src, int64_t n_items, int piece, int engine, int max_ctas, int stages,
-                         int unroll, int dev, cudaStream_t st, int schedule) {
-  return launch_src(src, n_items, false, piece, engine, max_ctas, stages, unroll, dev, st, schedule);
+dyna_status launch_batch(const BatchSource& src, int64_t n_items, bool sig, int piece, int engine, int max_ctas,
+                         int stages, int unroll, int dev, cudaStream_t st, int schedule) {
+  return launch_src(src, n_items, sig, piece, engine, max_ctas, stages, unroll, dev, st, schedule);
 }
 
 void launch_wait_flag(const unsigned long long* flag, unsigned long long epoch, unsigned long long timeout_ns,

@@ -449,7 +449,10 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   dyna_status r = check_opts(opts, &o);
   if (r) return r;
   if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "batch: FUSED variant only");
-  if (o.flags & DYNA_MIGRATE_SIGNAL) return fail(DYNA_ENOTSUP, "batch: no per-chunk signalling (use dyna_kv_migrate_ex)");
+  if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
+  const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
+  if (signal && o.engine && o.engine != DYNA_ENGINE_VEC)
+    return fail(DYNA_ENOTSUP, "batch with per-chunk flags: VEC engine only");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   std::vector<int32_t> live;
   int64_t total_tok = 0;
@@ -489,6 +492,10 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
                                                                   migs[i].dst.pool->desc.block_size),
                                                             chunk_tokens) * S0->row);
   Choice ch = choose(o, S0->row, peer, total_tok, run_min);
+  if (ch.engine == DYNA_ENGINE_DMA) {
+    delete x;
+    return fail(DYNA_ENOTSUP, "batch: no DMA engine");
+  }
   if (!o.engine && ch.engine != DYNA_ENGINE_VEC) {
     // measured (scripts/batch_probe.py): with many plans the BULK engine's single issuing
     // thread is latency-bound on per-item plan lookups; the warp-parallel VEC engine is not
@@ -497,6 +504,26 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     if (!o.piece_bytes) ch.piece = kVecPiece;
   }
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  if (signal) {  // slot ranges: disjoint per (sender instance, destination pool) inside the batch
+    x->batch.assign(n, dyna_kv_xfer::BatchEntry{});
+    std::map<std::pair<int, const dyna_kv_pool*>, int64_t> next_slot;
+    for (int32_t i : live) {
+      dyna_kv_pool *S = migs[i].src.pool, *D = migs[i].dst.pool;
+      const int64_t nck = (migs[i].token_range.end - migs[i].token_range.begin + chunk_tokens - 1) / chunk_tokens;
+      int64_t& slot = next_slot[{S->desc.instance, D}];
+      if (slot + nck > DYNA_MAX_CHUNKS) {
+        delete x;
+        return fail(DYNA_ERANGE, "batch: more than DYNA_MAX_CHUNKS (%d) signalled chunks from sender %d into one "
+                                 "destination pool", DYNA_MAX_CHUNKS, S->desc.instance);
+      }
+      dyna_kv_xfer::BatchEntry& be = x->batch[i];
+      be.first_slot = (int32_t)slot;
+      be.nchunks = (int32_t)nck;
+      be.sender = S->desc.instance;
+      be.epoch = next_epoch(S->desc.instance, D);
+      slot += nck;
+    }
+  }
   DeviceGuard guard(S0->dev);
   // One upload: [plans][item bases][host-resident tables].
   const size_t m = live.size();
@@ -532,6 +559,18 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     const int64_t g = gcd64(S->desc.block_size, D->desc.block_size);
     plans[k] = make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end, l0, lm,
                          chunk_tokens, g, ch.piece);
+    if (signal) {  // entry k's chunk j: counter / inbox slot first_slot + j of its (sender, destination)
+      dyna_kv_xfer::BatchEntry& be = x->batch[live[k]];
+      unsigned long long* ctr = nullptr;
+      if ((r = channel_counters(S, D, S0->dev, &ctr))) {
+        delete x;
+        return r;
+      }
+      plans[k].counters = ctr + be.first_slot;
+      plans[k].flags = D->inbox + (size_t)S->desc.instance * DYNA_MAX_CHUNKS + be.first_slot;
+      plans[k].epoch = be.epoch;
+      plans[k].sys_fence = (D->dev != S->dev || D->imported) ? 1 : 0;
+    }
     bases[k] = total_items;
     total_items += plans[k].n_items;
   }
@@ -557,7 +596,14 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   x->stages = ch.engine != DYNA_ENGINE_VEC ? ch.stages : 0;
   x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
   x->launches = 1;
-  r = launch_batch(bsrc, total_items, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev, stream,
+  if (signal) {  // per-chunk accounting is per plan: the VEC engine only
+    ch.engine = DYNA_ENGINE_VEC;
+    x->engine = ch.engine;
+    x->stages = 0;
+    if (!ch.unroll) ch.unroll = kVecU;
+    x->unroll = ch.unroll;
+  }
+  r = launch_batch(bsrc, total_items, signal, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev, stream,
                    o.schedule);
   if (!r) r = lease.finish(stream);
   if (r) {
@@ -609,6 +655,19 @@ dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t x, uint64_t* epoch, int32_t* num_ch
   if (epoch) *epoch = x->epoch;
   if (num_chunks) *num_chunks = x->nchunks;
   if (sender) *sender = x->sender;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_batch_info(dyna_kv_xfer_t x, int32_t index, uint64_t* epoch, int32_t* first_slot,
+                               int32_t* num_chunks, int32_t* sender) {
+  if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (x->batch.empty()) return fail(DYNA_EINVAL, "not a signalled dyna_kv_migrate_batch");
+  if (index < 0 || (size_t)index >= x->batch.size()) return fail(DYNA_ERANGE, "batch index %d", index);
+  const dyna_kv_xfer::BatchEntry& be = x->batch[index];
+  if (epoch) *epoch = be.epoch;
+  if (first_slot) *first_slot = be.first_slot;
+  if (num_chunks) *num_chunks = be.nchunks;
+  if (sender) *sender = be.sender;
   return DYNA_OK;
 }
 

@@ -175,6 +175,11 @@ struct dyna_kv_xfer {
   int32_t sender = 0;
   dyna_kv_ready* board = nullptr;  // producer-coupled: the board (for cancellation at dyna_kv_wait)
   uint64_t ready_epoch = 0;
+  struct BatchEntry {              // signalled batches: where each entry's chunk flags live
+    uint64_t epoch = 0;
+    int32_t first_slot = 0, nchunks = 0, sender = 0;
+  };
+  std::vector<BatchEntry> batch;
 };
 
 
@@ -322,8 +327,8 @@ void set_chunking(Plan& p, int64_t mig_t0, int64_t mig_t1, int64_t sig_c);
 void set_run_groups(Plan& p, int J);
 dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev, cudaStream_t st,
                         int schedule);
-dyna_status launch_batch(const BatchSource& src, int64_t n_items, int piece, int engine, int max_ctas, int stages,
-                         int unroll, int dev, cudaStream_t st, int schedule);
+dyna_status launch_batch(const BatchSource& src, int64_t n_items, bool sig, int piece, int engine, int max_ctas,
+                         int stages, int unroll, int dev, cudaStream_t st, int schedule);
 dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st, int schedule);
 Plan make_plan_sliced(const Side& s, const Side& d, int64_t slice, int64_t spitch, int64_t scol, int64_t dpitch,
                       int64_t dcol, int64_t t0, int64_t t1, int l0, int lm, int64_t c, int64_t g, int piece);

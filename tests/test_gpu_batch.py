@@ -237,3 +237,83 @@ def test_concurrent_host_threads():
         t.join()
     assert not errors, errors
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
+
+
+# ---------------------------------------------------------------- signalled batches (per-request chunk flags)
+def _flags(pool, sender, first, n):
+    fl = torch.zeros(max(n, 1), dtype=torch.int64).pin_memory()
+    dk.dyna_kv_copy_flags(pool.handle, sender, first, n, fl.data_ptr(), 0)
+    torch.cuda.synchronize()
+    return fl.numpy()[:n]
+
+
+@pytest.mark.parametrize("host_tables", [False, True])
+def test_signalled_batch_per_request_flags(host_tables):
+    """Each entry of a signalled batch gets its own epoch and slot range; every chunk flag of every
+    request reaches its epoch, slot ranges of one (sender, destination) are disjoint, and the rows
+    match the oracle.  Two destination pools, an empty entry, ragged starts."""
+    gs = Geom(2, 8, 128, 2, 16, 1200)
+    gd1, gd2 = gs.with_(num_blocks=700), gs.with_(block_size=32, num_blocks=400)
+    reqs = kvgen.migrating(kvgen.skewed_batch(9, 20))
+    lens = [min(r.s, 500) for r in reqs]
+    hs = kvgen.fill_bytes(21, gs.pool_bytes)
+    h1, h2 = kvgen.fill_bytes(22, gd1.pool_bytes), kvgen.fill_bytes(23, gd2.pool_bytes)
+    w1, w2 = h1.copy(), h2.copy()
+    rng = np.random.default_rng(3)
+    free_s, free1, free2 = np.arange(gs.num_blocks), np.arange(gd1.num_blocks), np.arange(gd2.num_blocks)
+    entries = []
+    for i, n in enumerate(lens):
+        t0 = int(rng.integers(0, 20))
+        gd, free_d, want = (gd1, free1, w1) if i % 2 == 0 else (gd2, free2, w2)
+        ts, free_s = kvgen.fragmented_table(rng, free_s, kvgen.blocks_needed(t0 + n, gs.block_size))
+        td, free_d = kvgen.fragmented_table(rng, free_d, kvgen.blocks_needed(t0 + n, gd.block_size))
+        if i % 2 == 0:
+            free1 = free_d
+        else:
+            free2 = free_d
+        oracle.migrate(hs, gs, ts, want, gd, td, (t0, t0 + n))
+        entries.append((ts, td, (t0, t0 + n), i % 2))
+    src = pool_from_host(gs, hs, instance=4)
+    d1, d2 = pool_from_host(gd1, h1), pool_from_host(gd2, h2)
+    T = host_table if host_tables else dev_table
+    migs = [(T(src, ts), T(d1 if w == 0 else d2, td), tr) for ts, td, tr, w in entries]
+    migs.insert(3, (T(src, entries[0][0]), T(d1, entries[0][1]), (7, 7)))     # empty entry
+    c = 96
+    x = dk.migrate_batch(migs, (0, 2), c, flags=dk.DYNA_MIGRATE_SIGNAL)
+    infos = [dk.dyna_kv_batch_info(x, i) for i in range(len(migs))]
+    dk.dyna_kv_wait(x)
+    assert infos[3][2] == 0
+    used = {0: [], 1: []}
+    epochs = {0: set(), 1: set()}
+    for (ts, td, tr, w), info in zip(entries, infos[:3] + infos[4:]):
+        epoch, first, nck, sender = info
+        assert sender == 4 and nck == -(-(tr[1] - tr[0]) // c)
+        fl = _flags(d1 if w == 0 else d2, sender, first, nck)
+        assert (fl == epoch).all(), (info, fl)
+        used[w] += list(range(first, first + nck))
+        epochs[w].add(epoch)
+    for w in (0, 1):
+        assert len(used[w]) == len(set(used[w]))          # disjoint slot ranges per destination
+        assert len(epochs[w]) == sum(1 for e in entries if e[3] == w)   # one epoch per request (per destination)
+    assert np.array_equal(d1.tensor.cpu().numpy(), w1)
+    assert np.array_equal(d2.tensor.cpu().numpy(), w2)
+
+
+def test_signalled_batch_limits_and_errors():
+    g = Geom(1, 2, 64, 2, 16, 4200)
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(1, 65536, g, g)
+    with pytest.raises(dk.DynaKVError) as e:        # 2 x 4096 chunks into one destination > DYNA_MAX_CHUNKS
+        dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, 4096)),
+                          (dev_table(src, ts), dev_table(dst, td), (4096, 8192))], (0, 1), 1,
+                         flags=dk.DYNA_MIGRATE_SIGNAL)
+    assert e.value.status == dk.DYNA_ERANGE
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, 10))], (0, 1), 4,
+                         flags=dk.DYNA_MIGRATE_SIGNAL, engine=dk.DYNA_ENGINE_BULK)
+    assert e.value.status == dk.DYNA_ENOTSUP
+    x = dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, 10))], (0, 1), 4)
+    with pytest.raises(dk.DynaKVError) as e:         # not a signalled batch
+        dk.dyna_kv_batch_info(x, 0)
+    assert e.value.status == dk.DYNA_EINVAL
+    dk.dyna_kv_wait(x)
