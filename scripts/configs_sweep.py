@@ -149,6 +149,10 @@ def main():
     ms = run_set(stream, calls, reps=5)
     report(f"configs[4] Qwen2-72B shard, one pair's {len(reqs)} requests (sum s={tot}) c=1024",
            tot * 2 * 80 * g.row_bytes, ms, tot, len(calls), "all-pairs 8-GPU form needs 8 GPUs")
+    migs = [(t[0], t[1], (0, t[2])) for t in T]
+    ms = run_set(stream, [lambda: dk.dyna_kv_migrate_batch(migs, (0, 80), 1024, cs, None)], reps=5)
+    report(f"configs[4] Qwen2-72B shard, one pair's {len(reqs)} requests (sum s={tot}) c=1024, batched",
+           tot * 2 * 80 * g.row_bytes, ms, tot, 1, "one dyna_kv_migrate_batch launch")
     del src, dst, T
     # NEXT-3 shape: TP-8 Qwen2-72B shard (1 KV head per rank: 256-B rows, 4-KiB segments)
     g = kvgen.QWEN2_72B.with_(num_kv_heads=1, num_blocks=6144)
@@ -159,6 +163,10 @@ def main():
     ms = run_set(stream, calls, reps=5)
     report(f"TP-8 Qwen2-72B shard (1 KV head, 256-B rows), {len(reqs)} requests (sum s={tot}) c=1024",
            tot * 2 * 80 * g.row_bytes, ms, tot, len(calls))
+    migs = [(t[0], t[1], (0, t[2])) for t in T]
+    ms = run_set(stream, [lambda: dk.dyna_kv_migrate_batch(migs, (0, 80), 1024, cs, None)], reps=5)
+    report(f"TP-8 Qwen2-72B shard (1 KV head, 256-B rows), {len(reqs)} requests (sum s={tot}) c=1024, batched",
+           tot * 2 * 80 * g.row_bytes, ms, tot, 1, "one dyna_kv_migrate_batch launch")
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump({"device": torch.cuda.get_device_name(0), "hbm_peak_gbs": pk, "results": out},
               open(args.out, "w"), indent=1)
