@@ -351,6 +351,7 @@ def run_dyna(args, rank, world, local_rank):
         if world == 1:
             achieved = 2 * payload / (kern_ms / 1e3) / 1e9  # HBM read + write bytes per launch / duration
             roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                    "frac_of_nominal_8000": achieved / 8000.0,
                     "traffic": ncu_traffic(), "peak_source": hbm_src,
                     "kernel": ("dynakv::k_copy_bulk" if plan["engine"] == dk.DYNA_ENGINE_BULK
                                else "dynakv::k_copy_vec") + " (K4-local fused reblock)",
