@@ -31,8 +31,11 @@ def main():
     T = [(dk.table(src, torch.from_numpy(a).cuda(), a), dk.table(dst, torch.from_numpy(b).cuda(), b)) for a, b in tabs]
     payload = s * 2 * g.num_layers * g.row_bytes
     out = []
-    for engine, piece, stages, unroll in [e for e in ((1, 8192, 0, 8), (2, 32768, 6, 0), (3, 32768, 6, 0),
-                                                      (4, 0, 0, 0)) if e[0] in engines]:
+    cands = ((1, 8192, 0, 8), (2, 32768, 6, 0), (3, 32768, 6, 0), (4, 0, 0, 0))
+    if os.environ.get("VEC_SWEEP"):  # VEC shapes only
+        cands = ((1, 8192, 0, 8), (1, 4096, 0, 8), (1, 16384, 0, 8), (1, 8192, 0, 16), (1, 16384, 0, 16),
+                 (1, 32768, 0, 16), (1, 8192, 0, 4), (1, 4096, 0, 4))
+    for engine, piece, stages, unroll in [e for e in cands if e[0] in engines]:
         for sig in (0, 1):
             o = dk.opts(variant=1, engine=engine, piece_bytes=piece, stages=stages, unroll=unroll,
                         flags=dk.DYNA_MIGRATE_SIGNAL if sig else 0)
@@ -49,7 +52,8 @@ def main():
                 dk.dyna_kv_wait(x)
             torch.cuda.synchronize()
             ms = statistics.median(a.elapsed_time(b) for a, b in ev)
-            r = {"engine": engine, "signal": sig, "us": ms * 1e3, "GBps": payload / ms / 1e6}
+            r = {"engine": engine, "piece": piece, "unroll": unroll, "signal": sig, "us": ms * 1e3,
+                 "GBps": payload / ms / 1e6}
             print(json.dumps(r), flush=True)
             out.append(r)
     json.dump(out, open(os.path.join(ROOT, "gpurun_out", "sig_probe.json"), "w"), indent=1)
