@@ -558,9 +558,15 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, uns
   uint32_t cur_acc = 0, park_acc = 0;
   int since_park = 0;
   auto flush_park = [&](bool all) {
+#ifndef DYNA_DIAG_NO_WAIT  // (DYNA_DIAG_*: unsafe diagnostic builds that drop one step each)
     if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
+#endif
+#ifndef DYNA_DIAG_NO_PROXY
     asm volatile("fence.proxy.async.global;" ::: "memory");
-#ifdef DYNA_BULK_FENCED_COUNT
+#endif
+#if defined(DYNA_DIAG_NO_COUNT)
+    (void)park_k;
+#elif defined(DYNA_BULK_FENCED_COUNT)
     fence_for(p);
     account_chunk(p, park_k, park_acc);
 #else
