@@ -360,6 +360,21 @@ DYNA_API dyna_status dyna_kv_place(dyna_kv_channel_t ch, dyna_block_table dst, d
                                    dyna_range layer_range, int32_t chunk_tokens, struct CUstream_st* stream,
                                    const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
 
+/* Head-sliced channel traffic (TP resharding in the receiver-steered form;
+ * reading R14): the sender pushes its heads [src_heads) of every row, packed
+ * as [layer][K|V][token][n_heads*d*e] into the receiver's slots; the receiver
+ * places them into its heads [dst_head_begin, dst_head_begin + num_heads).
+ * Both sides must describe the same token range, layer range, chunk_tokens
+ * and head count, in the same order; the pools may differ in H (L, d, e
+ * agree with the channel's pool).  Everything else as dyna_kv_push / _place. */
+DYNA_API dyna_status dyna_kv_push_heads(dyna_block_table src, dyna_range token_range, dyna_range layer_range,
+                                        dyna_range src_heads, int32_t chunk_tokens, dyna_kv_channel_t ch,
+                                        struct CUstream_st* stream, dyna_kv_xfer_t* out);
+DYNA_API dyna_status dyna_kv_place_heads(dyna_kv_channel_t ch, dyna_block_table dst, dyna_range token_range,
+                                         dyna_range layer_range, int32_t dst_head_begin, int32_t num_heads,
+                                         int32_t chunk_tokens, struct CUstream_st* stream,
+                                         const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
+
 /* CUDA graphs: dyna_kv_migrate / _ex with DEVICE block tables may be captured
  * into a CUDA graph (stream capture) and replayed; release each handle with
  * dyna_kv_wait after the capture ends (it returns at once — the captured work

@@ -43,7 +43,7 @@ EXPORTS = (
     "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready", "dyna_kv_ready_set_timeout",
     "dyna_kv_channel_create", "dyna_kv_channel_export", "dyna_kv_channel_import", "dyna_kv_channel_destroy",
     "dyna_kv_push", "dyna_kv_place", "dyna_kv_channel_set_timeout", "dyna_kv_ready_cancel",
-    "dyna_kv_migrate_heads", "dyna_kv_batch_info",
+    "dyna_kv_migrate_heads", "dyna_kv_batch_info", "dyna_kv_push_heads", "dyna_kv_place_heads",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -106,6 +106,10 @@ def _load():
                                  p(vp)]),
         "dyna_kv_migrate_ex": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
                                     vp, p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_push_heads": (st, [dyna_block_table, dyna_range, dyna_range, dyna_range, ctypes.c_int32, vp, vp,
+                                    p(vp)]),
+        "dyna_kv_place_heads": (st, [vp, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32, ctypes.c_int32,
+                                     ctypes.c_int32, vp, p(dyna_kv_opts), p(vp)]),
         "dyna_kv_batch_info": (st, [vp, ctypes.c_int32, p(ctypes.c_uint64), p(ctypes.c_int32), p(ctypes.c_int32),
                                     p(ctypes.c_int32)]),
         "dyna_kv_migrate_heads": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, dyna_range,
@@ -307,6 +311,23 @@ def dyna_kv_place(ch: int, dst: dyna_block_table, token_range, layer_range, chun
     _check(lib.dyna_kv_place(ctypes.c_void_p(ch), dst, dyna_range(*token_range), dyna_range(*layer_range),
                              chunk_tokens, ctypes.c_void_p(stream), ctypes.byref(opts) if opts is not None else None,
                              ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_push_heads(src: dyna_block_table, token_range, layer_range, src_heads, chunk_tokens: int, ch: int,
+                       stream: int = 0) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_push_heads(src, dyna_range(*token_range), dyna_range(*layer_range), dyna_range(*src_heads),
+                                  chunk_tokens, ctypes.c_void_p(ch), ctypes.c_void_p(stream), ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_place_heads(ch: int, dst: dyna_block_table, token_range, layer_range, dst_head_begin: int,
+                        num_heads: int, chunk_tokens: int, stream: int = 0, opts: dyna_kv_opts | None = None) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_place_heads(ctypes.c_void_p(ch), dst, dyna_range(*token_range), dyna_range(*layer_range),
+                                   dst_head_begin, num_heads, chunk_tokens, ctypes.c_void_p(stream),
+                                   ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
     return out.value
 
 

@@ -194,11 +194,12 @@ dyna_status dyna_kv_channel_destroy(dyna_kv_channel_t ch) {
 }
 
 // Shared checks of push / place: geometry against the channel, ranges, a device table.
+// slice > 0: head-sliced push / place of `slice` bytes per token (H may differ from the channel's).
 static dyna_status chan_check(const dyna_kv_channel* ch, const dyna_block_table& t, dyna_range tr, dyna_range lr,
-                              int32_t c, bool* empty) {
+                              int32_t c, bool* empty, int64_t slice = 0) {
   if (!ch || !t.pool) return fail(DYNA_EINVAL, "NULL channel or pool");
   const dyna_kv_pool_desc &g = t.pool->desc, &cg = ch->desc;
-  if (g.num_layers != cg.num_layers || g.num_kv_heads != cg.num_kv_heads || g.head_dim != cg.head_dim ||
+  if (g.num_layers != cg.num_layers || (!slice && g.num_kv_heads != cg.num_kv_heads) || g.head_dim != cg.head_dim ||
       g.elem_bytes != cg.elem_bytes)
     return fail(DYNA_EGEOM, "pool geometry differs from the channel's");
   if (lr.begin < 0 || lr.begin > lr.end || lr.end > g.num_layers) return fail(DYNA_ERANGE, "bad layer range");
@@ -208,7 +209,7 @@ static dyna_status chan_check(const dyna_kv_channel* ch, const dyna_block_table&
   if (c <= 0) return fail(DYNA_ERANGE, "chunk_tokens must be > 0");
   if (tr.end > t.len * g.block_size) return fail(DYNA_ERANGE, "token range exceeds the block table");
   if (!t.block_ids) return fail(DYNA_EINVAL, "push/place need device block_ids");
-  if (chan_subchunk(ch, t.pool->row, (int)(lr.end - lr.begin), c) < 1)
+  if (chan_subchunk(ch, slice ? slice : t.pool->row, (int)(lr.end - lr.begin), c) < 1)
     return fail(DYNA_EINVAL, "a channel slot of %llu B cannot hold one token of this layer range",
                 (unsigned long long)ch->slot_bytes);
   if (t.host_block_ids) {
@@ -348,6 +349,163 @@ dyna_status dyna_kv_place(dyna_kv_channel_t ch, dyna_block_table dst, dyna_range
         p.epoch = x->epoch;
       }
       r = launch_copy(p, DYNA_ENGINE_VEC, o.max_ctas, kBulkStages, kVecU, D->dev, stream, 0);
+      launch_release_sys(ch->credit + slot, q + 1, stream);  // the slot may be refilled
+    }
+  }
+  if (!r) {
+    CUDA_TRY(cudaGetLastError());
+    r = record_completion(x, D->dev, stream);
+  }
+  if (r) {
+    delete x;
+    return r;
+  }
+  x->variant = DYNA_VARIANT_STAGED;
+  x->engine = DYNA_ENGINE_VEC;
+  x->launches = (int32_t)(g_launches.load() - launches0);
+  *out = x;
+  return DYNA_OK;
+}
+
+// ---------------------------------------------------------------- head-sliced channel (TP resharding)
+// The slot holds packed slices [l][kv][t][n_heads*d*e]: the sender gathers its heads
+// [h0, h0 + n) of every row, the receiver scatters them into its heads [hd0, hd0 + n).
+static dyna_status head_slice(const dyna_kv_pool_desc& g, int64_t h0, int64_t n, int64_t* slice) {
+  const int64_t he = (int64_t)g.head_dim * g.elem_bytes;
+  if (h0 < 0 || n <= 0 || h0 + n > g.num_kv_heads)
+    return fail(DYNA_ERANGE, "heads [%lld, %lld) outside [0, %d)", (long long)h0, (long long)(h0 + n), g.num_kv_heads);
+  if (he % 16) return fail(DYNA_EGEOM, "head slices must be multiples of 16 bytes (d*e = %lld)", (long long)he);
+  *slice = n * he;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_push_heads(dyna_block_table src, dyna_range tr, dyna_range lr, dyna_range src_heads, int32_t c,
+                               dyna_kv_channel_t ch, struct CUstream_st* stream_, dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  if (!src.pool) return fail(DYNA_EINVAL, "NULL pool");
+  int64_t slice = 0;
+  dyna_status r = head_slice(src.pool->desc, src_heads.begin, src_heads.end - src_heads.begin, &slice);
+  if (r) return r;
+  bool empty = false;
+  if ((r = chan_check(ch, src, tr, lr, c, &empty, slice))) return r;
+  dyna_kv_pool* S = src.pool;
+  auto* x = new dyna_kv_xfer();
+  x->dev = S->dev;
+  x->sender = ch->sender;
+  if (empty) {
+    x->empty = true;
+    *out = x;
+    return DYNA_OK;
+  }
+  if (ch->imported ? ch->dev != S->dev : (ch->dev != S->dev && (r = ensure_peer(S->dev, ch->dev)) != DYNA_OK)) {
+    delete x;
+    return r ? r : fail(DYNA_EPEER, "channel mapped on device %d, source on %d", ch->dev, S->dev);
+  }
+  std::lock_guard<std::mutex> lk(ch->mu);
+  if ((r = chan_counters(&ch->push_counters, S->dev))) {
+    delete x;
+    return r;
+  }
+  ch->push_counters_dev = S->dev;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  DeviceGuard guard(S->dev);
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  const int64_t sc = chan_subchunk(ch, slice, lm, c);
+  const int64_t he = (int64_t)S->desc.head_dim * S->desc.elem_bytes;
+  const uint64_t seq0 = ch->push_seq;
+  const uint64_t launches0 = g_launches.load();
+  for (int64_t a = tr.begin; a < tr.end && !r; a += c) {
+    const int64_t b = std::min<int64_t>(a + c, tr.end);
+    for (int64_t sa = a; sa < b && !r; sa += sc) {
+      const int64_t sb = std::min(sa + sc, b);
+      const uint64_t q = ch->push_seq++;
+      const int slot = (int)(q % ch->slots);
+      if (q >= (uint64_t)ch->slots) launch_wait_flag(ch->credit + slot, q - ch->slots + 1, ch->timeout_ns, stream);
+      Plan p = make_plan_sliced(paged(S, src.block_ids), linear(ch->base + (size_t)slot * ch->slot_bytes), slice,
+                                S->row, src_heads.begin * he, slice, 0, sa, sb, l0, lm, sb - sa, S->desc.block_size,
+                                kVecPiece);
+      p.counters = ch->push_counters;
+      p.flags = ch->full + slot;
+      p.epoch = q + 1;
+      p.sys_fence = 1;
+      r = launch_rows(p, 0, S->dev, stream);
+    }
+  }
+  if (!r) {
+    CUDA_TRY(cudaGetLastError());
+    r = record_completion(x, S->dev, stream);
+  }
+  if (r) {
+    delete x;
+    return r;
+  }
+  x->variant = DYNA_VARIANT_STAGED;
+  x->engine = DYNA_ENGINE_VEC;
+  x->nchunks = (int32_t)(ch->push_seq - seq0);
+  x->launches = (int32_t)(g_launches.load() - launches0);
+  *out = x;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_place_heads(dyna_kv_channel_t ch, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                                int32_t dst_head_begin, int32_t num_heads, int32_t c, struct CUstream_st* stream_,
+                                const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  if (!dst.pool) return fail(DYNA_EINVAL, "NULL pool");
+  int64_t slice = 0;
+  dyna_status r = head_slice(dst.pool->desc, dst_head_begin, num_heads, &slice);
+  if (r) return r;
+  bool empty = false;
+  if ((r = chan_check(ch, dst, tr, lr, c, &empty, slice))) return r;
+  if (ch->imported || dst.pool != ch->dst) return fail(DYNA_EINVAL, "place on the channel's owner, into its pool");
+  dyna_kv_opts o{};
+  if ((r = check_opts(opts, &o))) return r;
+  const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
+  dyna_kv_pool* D = dst.pool;
+  const int64_t nchunks = empty ? 0 : (tr.end - tr.begin + c - 1) / c;
+  if (signal && nchunks > DYNA_MAX_CHUNKS) return fail(DYNA_ERANGE, "too many chunks for signalling");
+  auto* x = new dyna_kv_xfer();
+  x->dev = D->dev;
+  x->sender = ch->sender;
+  x->nchunks = (int32_t)nchunks;
+  if (empty) {
+    x->empty = true;
+    *out = x;
+    return DYNA_OK;
+  }
+  std::lock_guard<std::mutex> lk(ch->mu);
+  if (signal) {
+    if ((r = chan_counters(&ch->place_counters, D->dev))) {
+      delete x;
+      return r;
+    }
+    x->epoch = next_epoch(ch->sender, D);
+  }
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  DeviceGuard guard(D->dev);
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  const int64_t sc = chan_subchunk(ch, slice, lm, c);
+  const int64_t he = (int64_t)D->desc.head_dim * D->desc.elem_bytes;
+  const uint64_t launches0 = g_launches.load();
+  for (int64_t a = tr.begin; a < tr.end && !r; a += c) {
+    const int64_t b = std::min<int64_t>(a + c, tr.end);
+    for (int64_t sa = a; sa < b && !r; sa += sc) {
+      const int64_t sb = std::min(sa + sc, b);
+      const uint64_t q = ch->place_seq++;
+      const int slot = (int)(q % ch->slots);
+      launch_wait_flag(ch->full + slot, q + 1, ch->timeout_ns, stream);
+      Plan p = make_plan_sliced(linear(ch->base + (size_t)slot * ch->slot_bytes), paged(D, dst.block_ids), slice,
+                                slice, 0, D->row, (int64_t)dst_head_begin * he, sa, sb, l0, lm, sb - sa,
+                                D->desc.block_size, kVecPiece);
+      set_chunking(p, tr.begin, tr.end, c);
+      if (signal) {
+        p.counters = ch->place_counters;
+        p.flags = D->inbox + (size_t)ch->sender * DYNA_MAX_CHUNKS;
+        p.epoch = x->epoch;
+      }
+      r = launch_rows(p, o.max_ctas, D->dev, stream);
       launch_release_sys(ch->credit + slot, q + 1, stream);  // the slot may be refilled
     }
   }

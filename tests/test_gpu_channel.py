@@ -110,3 +110,64 @@ def test_push_place_across_processes():
     dk.dyna_kv_wait(x)
     dk.dyna_kv_channel_destroy(ch)
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("slots,slot_bytes,c", [(2, 4 * 2 * 2 * 1024 * 8, 100), (3, 1 << 20, 256)])
+@pytest.mark.parametrize("signal", [False, True])
+def test_push_place_heads_tp1_to_tp2(slots, slot_bytes, c, signal):
+    """Receiver-steered TP resharding (reading R14): a TP-1 sender (8 heads) feeds two TP-2
+    receivers (4 heads each) through their own channels; each receiver places with its own
+    table.  Bit-exact against oracle.migrate_heads, flags per receiver."""
+    gd = G.with_(num_kv_heads=4, block_size=32, num_blocks=200)
+    ts, _ = kvgen.table_pair(17, 5000, G, G)
+    hs = kvgen.fill_bytes(1, G.pool_bytes)
+    tr = (7, 3333)
+    src = pool_from_host(G, hs)
+    st = dev_table(src, ts)
+    keep = []
+    for r in range(2):
+        hd = kvgen.fill_bytes(10 + r, gd.pool_bytes)
+        td = kvgen.table_pair(20 + r, 5000, gd, gd)[1]
+        want = hd.copy()
+        oracle.migrate_heads(hs, G, ts, want, gd, td, tr, None, (4 * r, 4 * r + 4), 0)
+        dst = pool_from_host(gd, hd)
+        ch = dk.dyna_kv_channel_create(dst.handle, 3, slots, slot_bytes)
+        dk.dyna_kv_channel_set_timeout(ch, 120_000_000_000)
+        try:
+            s_push, s_place = torch.cuda.Stream(), torch.cuda.Stream()
+            dt = dev_table(dst, td)
+            keep.append((dt, dst))
+            xp = dk.dyna_kv_push_heads(st, tr, (0, 4), (4 * r, 4 * r + 4), c, ch, s_push.cuda_stream)
+            xq = dk.dyna_kv_place_heads(ch, dt, tr, (0, 4), 0, 4, c, s_place.cuda_stream,
+                                        dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0))
+            epoch, nchunks, sender = dk.dyna_kv_xfer_info(xq)
+            dk.dyna_kv_wait(xp)
+            dk.dyna_kv_wait(xq)
+            assert np.array_equal(dst.tensor.cpu().numpy(), want)
+            if signal:
+                flags = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
+                dk.dyna_kv_copy_flags(dst.handle, sender, 0, nchunks, flags.data_ptr(), 0)
+                torch.cuda.synchronize()
+                assert sender == 3 and (flags.numpy() == epoch).all()
+        finally:
+            dk.dyna_kv_channel_destroy(ch)
+
+
+def test_push_place_heads_errors():
+    gd = G.with_(num_kv_heads=4)
+    src, dst = pool_from_host(G, kvgen.fill_bytes(1, G.pool_bytes)), pool_from_host(gd, kvgen.fill_bytes(2, gd.pool_bytes))
+    ts, td = kvgen.table_pair(7, 1000, G, gd)
+    ch = dk.dyna_kv_channel_create(dst.handle, 0, 2, 1 << 20)
+    try:
+        for heads in [(0, 9), (6, 9), (3, 3)]:
+            with pytest.raises(dk.DynaKVError) as e:
+                dk.dyna_kv_push_heads(dev_table(src, ts), (0, 100), (0, 4), heads, 32, ch, 0)
+            assert e.value.status == dk.DYNA_ERANGE
+        with pytest.raises(dk.DynaKVError) as e:        # receiver heads outside its pool
+            dk.dyna_kv_place_heads(ch, dev_table(dst, td), (0, 100), (0, 4), 2, 4, 32, 0)
+        assert e.value.status == dk.DYNA_ERANGE
+        with pytest.raises(dk.DynaKVError) as e:        # whole-row push into a 4-head channel: geometry differs
+            dk.dyna_kv_push(dev_table(src, ts), (0, 100), (0, 4), 32, ch, 0)
+        assert e.value.status == dk.DYNA_EGEOM
+    finally:
+        dk.dyna_kv_channel_destroy(ch)
