@@ -477,6 +477,7 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   auto* x = new dyna_kv_xfer();
   if (live.empty()) {
     x->empty = true;
+    if (signal) x->batch.assign(n, dyna_kv_xfer::BatchEntry{});  // every entry: 0 chunks
     *out = x;
     return DYNA_OK;
   }
