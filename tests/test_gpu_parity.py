@@ -354,3 +354,24 @@ def test_flag_litmus_chunk_visible_when_flagged(variant, engine):
         for k, snap in snaps.items():
             t = torch.arange(k * c, min((k + 1) * c, s), device="cuda")
             assert torch.equal(snap, S[:, :, Ts[t // g.block_size], t % g.block_size]), (rep, c, k)
+
+
+def test_max_chunks_with_flags():
+    """Degenerate maximum: DYNA_MAX_CHUNKS one-token chunks, every flag raised; one more is refused."""
+    g = Geom(1, 1, 128, 2, 16, 300)
+    src, dst = pool_filled(g, 41, instance=2), pool_filled(g, 42)
+    ts, td = kvgen.table_pair(43, 4112, g, g)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    n = dk.DYNA_MAX_CHUNKS
+    x = dk.migrate(st, dt, (0, n), (0, 1), 1, flags=dk.DYNA_MIGRATE_SIGNAL)
+    epoch, nck, sender = dk.dyna_kv_xfer_info(x)
+    dk.dyna_kv_wait(x)
+    assert nck == n
+    fl = torch.zeros(n, dtype=torch.int64).pin_memory()
+    dk.dyna_kv_copy_flags(dst.handle, sender, 0, n, fl.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert (fl.numpy() == epoch).all()
+    assert torch_rows_equal(src, ts, dst, td, (0, n), (0, 1))
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.migrate(st, dt, (0, n + 1), (0, 1), 1, flags=dk.DYNA_MIGRATE_SIGNAL)
+    assert e.value.status == dk.DYNA_ERANGE
