@@ -48,6 +48,8 @@ def main():
     ap.add_argument("--inc", default=os.path.join(ROOT, "gpurun_out", "calib_default.inc"))
     ap.add_argument("--min-ms", type=float, default=15.0)
     ap.add_argument("--select", help="re-run only the selection on a saved calibration.json")
+    ap.add_argument("--peer", action="store_true",
+                    help="also calibrate peer (NVLink) entries: source on cuda:0, destination on cuda:1 (needs 2 GPUs)")
     args = ap.parse_args()
     if args.select:
         d = json.load(open(args.select))
@@ -57,15 +59,24 @@ def main():
     stream = torch.cuda.Stream()
     cs = stream.cuda_stream
     rows, chosen = [], []
-    for row, g in GEOMS.items():
+    pairs = [(0, 0)]
+    if args.peer:
+        if torch.cuda.device_count() < 2:
+            print("--peer: fewer than 2 GPUs visible, peer entries skipped", file=sys.stderr)
+        else:
+            dk.dyna_kv_enable_peer(0, 1)
+            pairs.append((0, 1))
+    for (sdev, ddev), (row, g) in [(pr, rg) for pr in pairs for rg in GEOMS.items()]:
+        peer = int(sdev != ddev)
         ntok = g.num_blocks * g.block_size
-        src, dst = dk.Pool(g, 0), dk.Pool(g, 0)
+        src, dst = dk.Pool(g, sdev), dk.Pool(g, ddev)
         for p, seed in ((src, 1), (dst, 2)):
-            dk.dyna_kv_debug_fill(p.tensor.data_ptr(), p.tensor.numel(), seed, 0, cs)
+            dk.dyna_kv_debug_fill(p.tensor.data_ptr(), p.tensor.numel(), seed, 0, 0)
+        torch.cuda.synchronize(ddev)
         rng = np.random.default_rng(row)
         ts, td = rng.permutation(g.num_blocks).astype(np.int32), rng.permutation(g.num_blocks).astype(np.int32)
-        st = dk.table(src, torch.from_numpy(ts).cuda(), ts)
-        dt = dk.table(dst, torch.from_numpy(td).cuda(), td)
+        st = dk.table(src, torch.from_numpy(ts).to(f"cuda:{sdev}"), ts)
+        dt = dk.table(dst, torch.from_numpy(td).to(f"cuda:{ddev}"), td)
         tok_bytes = 2 * g.num_layers * g.row_bytes
         for c in CHUNKS:
             n_calls = min(2000, max(20, int(args.min_ms * 1e-3 * 3.0e12 / (c * tok_bytes))))
@@ -89,8 +100,8 @@ def main():
                 batch()  # warm-up
                 ms = min(batch() for _ in range(2))
                 gbps = c * tok_bytes / (ms / 1e3) / 1e9
-                r = {"row_bytes": row, "chunk": c, "variant": var, "engine": eng, "piece": piece, "stages": stages,
-                     "unroll": unroll, "ms_per_call": ms, "GBps": gbps}
+                r = {"row_bytes": row, "peer": peer, "chunk": c, "variant": var, "engine": eng, "piece": piece,
+                     "stages": stages, "unroll": unroll, "ms_per_call": ms, "GBps": gbps}
                 results.append(r)
                 rows.append(r)
                 print(json.dumps(r), flush=True)
@@ -107,14 +118,15 @@ def select(rows):
     per-bucket argmax flips between candidates that are within noise of each other."""
     import math
     chosen, entries = [], []
-    for row in sorted({r["row_bytes"] for r in rows}, reverse=True):
-        chunks = sorted({r["chunk"] for r in rows if r["row_bytes"] == row})
+    classes = sorted({(r["row_bytes"], r.get("peer", 0)) for r in rows}, key=lambda x: (x[1], -x[0]))
+    for row, peer in classes:
+        mine = [r for r in rows if r["row_bytes"] == row and r.get("peer", 0) == peer]
+        chunks = sorted({r["chunk"] for r in mine})
         key = lambda r: (r["variant"], r["engine"], r["piece"], r["stages"], r["unroll"])  # noqa: E731
         perf = {}
-        for r in rows:
-            if r["row_bytes"] == row:
-                perf[(r["chunk"], key(r))] = r["GBps"]
-        cands = sorted({key(r) for r in rows if r["row_bytes"] == row})
+        for r in mine:
+            perf[(r["chunk"], key(r))] = r["GBps"]
+        cands = sorted({key(r) for r in mine})
         seq = []
         for i, c in enumerate(chunks):
             win = chunks[max(0, i - 1): i + 2]
@@ -124,13 +136,13 @@ def select(rows):
             if seq and score[seq[-1][1]] >= score[best] + math.log(0.99):
                 best = seq[-1][1]
             seq.append((c, best, perf[(c, best)]))
-            chosen.append({"row_bytes": row, "chunk": c, "choice": best, "GBps": perf[(c, best)],
+            chosen.append({"row_bytes": row, "peer": peer, "chunk": c, "choice": best, "GBps": perf[(c, best)],
                            "best_single": max(perf[(c, k)] for k in cands)})
         for i, (c, best, _) in enumerate(seq):
             nxt = seq[i + 1] if i + 1 < len(seq) else None
             if nxt and nxt[1] == best:
                 continue
-            entries.append((row, 0, c if nxt else (1 << 30)) + tuple(best))
+            entries.append((row, peer, c if nxt else (1 << 30)) + tuple(best))
     return chosen, entries
 
 
@@ -141,16 +153,20 @@ def write_outputs(args, rows, device):
                "chosen": chosen, "entries": entries}, open(args.out, "w"), indent=1)
     with open(args.inc, "w") as f:
         f.write(f"// Built-in calibration table, generated by scripts/calibrate.py on {device}\n")
-        f.write("// (measurements and choices: profiles/*calibration*.json).  Same-GPU entries only;\n")
-        f.write("// peer (NVLink) migrations fall back to FUSED + VEC until measured on a multi-GPU box.\n")
+        if any(e[1] for e in entries):
+            f.write("// (measurements and choices: profiles/*calibration*.json).  Same-GPU and peer (NVLink) entries.\n")
+        else:
+            f.write("// (measurements and choices: profiles/*calibration*.json).  Same-GPU entries only;\n")
+            f.write("// peer (NVLink) migrations fall back to FUSED + VEC until measured on a multi-GPU box.\n")
         f.write("// row_bytes, peer, max_chunk_tokens, variant, engine, piece_bytes, stages, unroll\n")
         for e in entries:
             f.write("    {" + ", ".join(str(x) for x in e) + "},\n")
-        # generic fallback for other row sizes: the table of the most common (GQA, 2 KiB) row
-        gen = [e for e in entries if e[0] == 2048] or entries
-        f.write("    // generic fallback (row_bytes 0) = the 2 KiB-row choices\n")
-        for e in gen:
-            f.write("    {" + ", ".join(str(x) for x in (0,) + tuple(e[1:])) + "},\n")
+        # generic fallback for other row sizes: the table of the most common (GQA, 2 KiB) row, per locality
+        for peer in sorted({e[1] for e in entries}):
+            gen = [e for e in entries if e[0] == 2048 and e[1] == peer] or [e for e in entries if e[1] == peer]
+            f.write(f"    // generic fallback (row_bytes 0, peer {peer}) = the 2 KiB-row choices\n")
+            for e in gen:
+                f.write("    {" + ", ".join(str(x) for x in (0,) + tuple(e[1:])) + "},\n")
     print(json.dumps({"entries": entries}))
 
 

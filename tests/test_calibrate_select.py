@@ -45,3 +45,21 @@ def test_select_keeps_rows_separate():
     rows += [_row(2048, c, A, 5.0) for c in (16, 32)] + [_row(2048, c, B, 10.0) for c in (16, 32)]
     _, entries = cal.select(rows)
     assert (8192, 0, 1 << 30) + A in entries and (2048, 0, 1 << 30) + B in entries
+
+
+def test_select_keeps_same_gpu_and_peer_separate(tmp_path):
+    cal = _load()
+    A, B = (1, 1, 8192, 0, 8), (1, 2, 32768, 6, 0)
+    rows = [_row(2048, c, A, 10.0) for c in (16, 32)] + [_row(2048, c, B, 5.0) for c in (16, 32)]
+    peer = [dict(_row(2048, c, A, 5.0), peer=1) for c in (16, 32)] + [dict(_row(2048, c, B, 9.0), peer=1)
+                                                                        for c in (16, 32)]
+    _, entries = cal.select(rows + peer)
+    assert (2048, 0, 1 << 30) + A in entries and (2048, 1, 1 << 30) + B in entries
+
+    class Args:
+        out = str(tmp_path / "c.json")
+        inc = str(tmp_path / "c.inc")
+    cal.write_outputs(Args, rows + peer, "test")
+    inc = open(Args.inc).read()
+    assert "{0, 0, 1073741824, 1, 1, 8192, 0, 8}" in inc and "{0, 1, 1073741824, 1, 2, 32768, 6, 0}" in inc
+    assert "Same-GPU and peer (NVLink) entries" in inc
