@@ -1,0 +1,20 @@
+# Multi-GPU evidence (needs >= 2 GPUs on one node; nothing here runs on a one-GPU box).
+# NVLink forms of the path: ring-pair bench at N = 2/4/8 (weak scaling), configs[4] all pairs,
+# the NCCL send/recv baseline on the same data, peer calibration entries, the overlap
+# experiment with the destination on another GPU.
+set -x
+N=$(nvidia-smi -L | wc -l)
+for n in 2 4 8; do
+  [ $n -le $N ] || continue
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+      --master-port $((29600 + n)) bench.py --gpus $n --no-cpu-baseline > gpurun_out/bench_n$n.json 2> gpurun_out/bench_n$n.err
+  cat gpurun_out/bench_n$n.json
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+      --master-port $((29700 + n)) scripts/allpairs.py --steps 5 --warmup 2 --check 2>&1 | tail -2
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+      --master-port $((29800 + n)) scripts/nccl_baseline.py 2>&1 | tail -2
+done
+timeout 2700 python scripts/calibrate.py --peer --out gpurun_out/calibration_peer.json --inc gpurun_out/calib_peer.inc \
+    > gpurun_out/calibrate_peer.log 2>&1; tail -1 gpurun_out/calibrate_peer.log
+timeout 1800 python scripts/overlap.py --dst-device 1 --chunks 1024,4096 --budgets 0,16 --layers \
+    --out gpurun_out/overlap_nvlink.json 2>&1 | tail -4

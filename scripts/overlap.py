@@ -60,17 +60,20 @@ def main():
     ap.add_argument("--ready-ctas", type=int, default=8, help="CTA budget of the coupled launch when budget is 0")
     ap.add_argument("--layers", action="store_true", help="add the layer-granular modes")
     ap.add_argument("--dma", action="store_true", help="add per-chunk pushes on the copy engines (DYNA_ENGINE_DMA)")
+    ap.add_argument("--dst-device", type=int, default=0, help="destination pool's GPU (1: the NVLink form)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "overlap.json"))
     args = ap.parse_args()
     torch.cuda.set_device(0)
     g = kvgen.LLAMA3_8B.with_(num_blocks=4096)
     s = args.s
-    src, dst = dk.Pool(g, 0), dk.Pool(g, 0)
+    if args.dst_device:
+        dk.dyna_kv_enable_peer(0, args.dst_device)
+    src, dst = dk.Pool(g, 0), dk.Pool(g, args.dst_device)
     for p, seed in ((src, 1), (dst, 2)):
         dk.dyna_kv_debug_fill(p.tensor.data_ptr(), p.tensor.numel(), seed, 0, 0)
     ts, td = kvgen.table_pair(3, s, g, g)
     st = dk.table(src, torch.from_numpy(ts).cuda(), ts)
-    dt = dk.table(dst, torch.from_numpy(td).cuda(), td)
+    dt = dk.table(dst, torch.from_numpy(td).cuda(), td)   # read by the kernel on the source GPU (cuda:0)
     W = torch.randn(4096, 14336, dtype=torch.bfloat16, device="cuda") * 0.01
     prod, mig = torch.cuda.Stream(), torch.cuda.Stream()
     payload = s * 2 * g.num_layers * g.row_bytes
