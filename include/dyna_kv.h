@@ -155,7 +155,7 @@ typedef struct {
  * run time.  Two measured rules apply on top of the table when the engine is
  * AUTO: no BULK engine when a contiguous run (min(gcd(bs_src, bs_dst),
  * chunk_tokens) * row bytes) is shorter than 16 KiB, and the VEC engine when
- * per-chunk flags are requested. */
+ * per-chunk flags are requested for more than one chunk in one call. */
 typedef struct {
     int32_t row_bytes;
     int32_t peer;

@@ -247,9 +247,11 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int64_t c = chunk_tokens;
   const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
   Choice ch = choose(o, row, peer_dst, ntok, std::min<int64_t>(gcd64(gs.block_size, gd.block_size), c) * row);
-  if (signal && !o.engine && ch.engine != DYNA_ENGINE_VEC) {
+  if (signal && !o.engine && ch.engine != DYNA_ENGINE_VEC && nchunks > 1) {
     // measured (bench.py e2e, per-chunk flags on): the VEC engine's per-warp fences beat
-    // draining bulk-store groups before each chunk's count (2720 vs 2540 GB/s)
+    // BULK's release-add at every chunk switch (2720 vs 2540 GB/s); with ONE chunk per call
+    // (the paper's per-chunk push) BULK keeps the lead (182.8 vs 186.8 us per 512 MiB,
+    // scripts/sig_probe.py with C = S)
     ch.engine = DYNA_ENGINE_VEC;
     ch.unroll = kVecU;
     if (!o.piece_bytes) ch.piece = kVecPiece;
