@@ -135,7 +135,8 @@ typedef struct {
     int32_t max_ctas;   /* cap on CTAs per kernel (SM budget for overlap with a producer); 0 = no cap */
     int32_t flags;      /* DYNA_MIGRATE_* */
     int32_t piece_bytes;/* bytes per work item; 0 = engine default.  Multiple of 16. */
-    int32_t stages;     /* BULK: shared-memory ring depth (2..16); 0 = default */
+    int32_t stages;     /* BULK: shared-memory ring depth (2..16); 0 = default.  Cut to the depth that
+                           fits in one CTA's shared memory (DYNA_EINVAL if two pieces do not fit) */
     int32_t unroll;     /* VEC: 16-B loads in flight per lane (4, 8 or 16); 0 = default */
     int32_t schedule;   /* work distribution: 0 = default (static), DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC */
 } dyna_kv_opts;

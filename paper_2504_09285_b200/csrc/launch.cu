@@ -201,9 +201,22 @@ void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cuda
 template <bool SIG, class Src>
 dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, int64_t max_grid, int sms,
                         cudaStream_t st, unsigned long long* sched, bool ws) {
-  const size_t smem = (size_t)stages * piece;
   auto kern = ws ? k_copy_bulk_ws<SIG, Src> : k_copy_bulk<SIG, Src>;
   const int threads = ws ? 64 : 32;
+  {  // a ring deeper than the shared memory holds is cut to the stages that fit (at least 2)
+    static int avail = 0;
+    if (!avail) {
+      int dev = 0, optin = 0;
+      cudaFuncAttributes fa{};
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncGetAttributes(&fa, (const void*)k_copy_bulk_ws<true, SingleSource>);  // the largest static smem
+      avail = optin - (int)fa.sharedSizeBytes;
+    }
+    if ((int64_t)stages * piece > avail) stages = avail / piece;
+    if (stages < 2) return fail(DYNA_EINVAL, "BULK: two %d-B pieces do not fit in shared memory", piece);
+  }
+  const size_t smem = (size_t)stages * piece;
   int occ = 0;  // (the dynamic shared memory limit was raised once in preload_kernels)
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
   if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);

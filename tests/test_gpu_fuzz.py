@@ -1,0 +1,94 @@
+"""Seeded differential fuzzing of the CUDA path against the oracle: random geometries (layers,
+heads, head_dim, element size, block sizes on each side), random fragmented tables, random
+token / layer / head ranges, chunk sizes, variants, engines and engine shapes, with and
+without per-chunk flags.  Every case is compared byte for byte on the whole destination pool
+(and the source pool is checked unchanged)."""
+import numpy as np
+import pytest
+import torch
+
+import kvgen
+import oracle
+import paper_2504_09285_b200 as dk
+from kvgen import Geom
+from gpu_util import dev_table, pool_from_host
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(rng):
+    e = int(rng.choice([1, 2, 4]))
+    d = int(rng.choice([8, 16, 32, 64, 128])) * (2 // e if e < 2 else 1)
+    H = int(rng.integers(1, 9))
+    if (H * d * e) % 16:
+        d = 16 // e * int(rng.integers(1, 9))
+    L = int(rng.integers(1, 5))
+    bss, bsd = int(rng.choice([1, 2, 4, 8, 16, 24, 32])), int(rng.choice([1, 2, 4, 8, 16, 32]))
+    n_tok = int(rng.integers(1, 600))
+    gs = Geom(L, H, d, e, bss, kvgen.blocks_needed(n_tok, bss) + int(rng.integers(0, 20)))
+    gd = Geom(L, H, d, e, bsd, kvgen.blocks_needed(n_tok, bsd) + int(rng.integers(0, 20)))
+    t0 = int(rng.integers(0, n_tok))
+    t1 = int(rng.integers(t0, n_tok + 1))
+    l0 = int(rng.integers(0, L))
+    l1 = int(rng.integers(l0, L + 1))
+    c = int(rng.choice([1, 3, 16, 17, 64, 100, 257, 1000]))
+    variant = int(rng.choice([1, 2]))
+    engine = int(rng.choice([1, 2, 3]))
+    piece = int(rng.choice([0, 256, 1024, 4096, 16384, 32768]))
+    stages = int(rng.choice([0, 2, 3, 4, 6, 8]))
+    unroll = int(rng.choice([0, 4, 8, 16]))
+    signal = bool(rng.integers(0, 2))
+    return gs, gd, n_tok, (t0, t1), (l0, l1), c, dict(variant=variant, engine=engine, piece_bytes=piece,
+                                                        stages=stages, unroll=unroll,
+                                                        flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0)
+
+
+@pytest.mark.parametrize("block", range(8))
+def test_fuzz_migrate(block):
+    rng = np.random.default_rng(kvgen.MASTER_SEED + 500 + block)
+    for i in range(40):
+        gs, gd, n_tok, tr, lr, c, kw = _case(rng)
+        ts, td = kvgen.table_pair(int(rng.integers(1 << 30)), n_tok, gs, gd)
+        hs = kvgen.fill_bytes(int(rng.integers(1 << 30)), gs.pool_bytes)
+        hd = kvgen.fill_bytes(int(rng.integers(1 << 30)), gd.pool_bytes)
+        want = hd.copy()
+        oracle.migrate(hs, gs, ts, want, gd, td, tr, lr)
+        src, dst = pool_from_host(gs, hs, instance=int(rng.integers(0, 8))), pool_from_host(gd, hd)
+        st, dt = dev_table(src, ts), dev_table(dst, td)
+        x = dk.migrate(st, dt, tr, lr, c, **kw)
+        dk.dyna_kv_wait(x)
+        got = dst.tensor.cpu().numpy()
+        assert np.array_equal(src.tensor.cpu().numpy(), hs), (i, gs, gd, tr, lr, c, kw)
+        assert np.array_equal(got, want), (i, gs, gd, tr, lr, c, kw)
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_fuzz_migrate_heads(block):
+    rng = np.random.default_rng(kvgen.MASTER_SEED + 900 + block)
+    for i in range(40):
+        e = int(rng.choice([2, 4]))
+        d = 16 // e * int(rng.integers(1, 9))
+        Hs, Hd = int(rng.integers(1, 9)), int(rng.integers(1, 9))
+        n = int(rng.integers(0, min(Hs, Hd) + 1))
+        h0 = int(rng.integers(0, Hs - n + 1))
+        hd0 = int(rng.integers(0, Hd - n + 1))
+        L = int(rng.integers(1, 4))
+        bss, bsd = int(rng.choice([1, 4, 8, 16])), int(rng.choice([2, 8, 16, 32]))
+        n_tok = int(rng.integers(1, 500))
+        gs = Geom(L, Hs, d, e, bss, kvgen.blocks_needed(n_tok, bss) + 3)
+        gd = Geom(L, Hd, d, e, bsd, kvgen.blocks_needed(n_tok, bsd) + 3)
+        t0 = int(rng.integers(0, n_tok))
+        tr = (t0, int(rng.integers(t0, n_tok + 1)))
+        c = int(rng.choice([1, 7, 16, 100, 1000]))
+        piece = int(rng.choice([0, 256, 4096]))
+        sig = dk.DYNA_MIGRATE_SIGNAL if rng.integers(0, 2) else 0
+        ts, td = kvgen.table_pair(int(rng.integers(1 << 30)), n_tok, gs, gd)
+        hs = kvgen.fill_bytes(int(rng.integers(1 << 30)), gs.pool_bytes)
+        hdst = kvgen.fill_bytes(int(rng.integers(1 << 30)), gd.pool_bytes)
+        want = hdst.copy()
+        oracle.migrate_heads(hs, gs, ts, want, gd, td, tr, None, (h0, h0 + n), hd0)
+        src, dst = pool_from_host(gs, hs), pool_from_host(gd, hdst)
+        st, dt = dev_table(src, ts), dev_table(dst, td)
+        dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(st, dt, tr, (0, L), (h0, h0 + n), hd0, c, 0,
+                                                 dk.opts(piece_bytes=piece, flags=sig)))
+        assert np.array_equal(dst.tensor.cpu().numpy(), want), (i, gs, gd, tr, (h0, n, hd0), c, piece)
