@@ -92,3 +92,51 @@ def test_fuzz_migrate_heads(block):
         dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(st, dt, tr, (0, L), (h0, h0 + n), hd0, c, 0,
                                                  dk.opts(piece_bytes=piece, flags=sig)))
         assert np.array_equal(dst.tensor.cpu().numpy(), want), (i, gs, gd, tr, (h0, n, hd0), c, piece)
+
+
+@pytest.mark.parametrize("block", range(2))
+def test_fuzz_batch(block):
+    """Random batches: 1-12 requests with own ranges into one or two destination pools, random
+    engine / piece, with or without per-request flags (each request's flags checked)."""
+    rng = np.random.default_rng(kvgen.MASTER_SEED + 1300 + block)
+    for i in range(12):
+        H = int(rng.integers(1, 9))
+        gs = Geom(int(rng.integers(1, 4)), H, 64, 2, int(rng.choice([8, 16])), 900)
+        gd1 = gs.with_(block_size=int(rng.choice([8, 16, 32])), num_blocks=900)
+        gd2 = gs.with_(block_size=16, num_blocks=900)
+        nreq = int(rng.integers(1, 13))
+        lens = [int(rng.integers(0, 300)) for _ in range(nreq)]
+        hs = kvgen.fill_bytes(int(rng.integers(1 << 30)), gs.pool_bytes)
+        h1, h2 = kvgen.fill_bytes(int(rng.integers(1 << 30)), gd1.pool_bytes), kvgen.fill_bytes(7, gd2.pool_bytes)
+        w1, w2 = h1.copy(), h2.copy()
+        free_s, free1, free2 = np.arange(900), np.arange(900), np.arange(900)
+        ents = []
+        for n in lens:
+            t0 = int(rng.integers(0, 20))
+            which = int(rng.integers(0, 2))
+            gd = gd1 if which == 0 else gd2
+            ts, free_s = kvgen.fragmented_table(rng, free_s, kvgen.blocks_needed(t0 + n + 1, gs.block_size))
+            if which == 0:
+                td, free1 = kvgen.fragmented_table(rng, free1, kvgen.blocks_needed(t0 + n + 1, gd.block_size))
+            else:
+                td, free2 = kvgen.fragmented_table(rng, free2, kvgen.blocks_needed(t0 + n + 1, gd.block_size))
+            oracle.migrate(hs, gs, ts, w1 if which == 0 else w2, gd, td, (t0, t0 + n))
+            ents.append((ts, td, (t0, t0 + n), which))
+        src = pool_from_host(gs, hs, instance=1)
+        d1, d2 = pool_from_host(gd1, h1), pool_from_host(gd2, h2)
+        migs = [(dev_table(src, ts), dev_table(d1 if w == 0 else d2, td), tr) for ts, td, tr, w in ents]
+        sig = bool(rng.integers(0, 2))
+        c = int(rng.choice([16, 33, 128, 1000]))
+        kw = dict(flags=dk.DYNA_MIGRATE_SIGNAL) if sig else dict(engine=int(rng.choice([0, 1, 2, 3])),
+                                                                 piece_bytes=int(rng.choice([0, 1024, 16384])))
+        x = dk.migrate_batch(migs, (0, gs.num_layers), c, **kw)
+        infos = [dk.dyna_kv_batch_info(x, j) for j in range(len(migs))] if sig else []
+        dk.dyna_kv_wait(x)
+        assert np.array_equal(d1.tensor.cpu().numpy(), w1), (i, kw)
+        assert np.array_equal(d2.tensor.cpu().numpy(), w2), (i, kw)
+        for (ts, td, tr, w), (epoch, first, nck, sender) in zip(ents, infos):
+            if nck:
+                fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
+                dk.dyna_kv_copy_flags((d1 if w == 0 else d2).handle, sender, first, nck, fl.data_ptr(), 0)
+                torch.cuda.synchronize()
+                assert (fl.numpy() == epoch).all(), (i, first, nck)
