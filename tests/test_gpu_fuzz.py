@@ -140,3 +140,49 @@ def test_fuzz_batch(block):
                 dk.dyna_kv_copy_flags((d1 if w == 0 else d2).handle, sender, first, nck, fl.data_ptr(), 0)
                 torch.cuda.synchronize()
                 assert (fl.numpy() == epoch).all(), (i, first, nck)
+
+
+def test_fuzz_channel():
+    """Random receiver-steered transfers: slots, slot sizes (down to one token), chunk sizes,
+    ranges, whole rows or head slices; push and place on separate streams."""
+    rng = np.random.default_rng(kvgen.MASTER_SEED + 1700)
+    for i in range(12):
+        H = int(rng.choice([2, 4, 8]))
+        L = int(rng.integers(1, 4))
+        gs = Geom(L, H, 64, 2, int(rng.choice([8, 16])), 300)
+        heads = bool(rng.integers(0, 2))
+        n = int(rng.integers(1, H + 1)) if heads else H
+        h0 = int(rng.integers(0, H - n + 1)) if heads else 0
+        gd = gs.with_(num_kv_heads=n if heads else H, block_size=int(rng.choice([8, 16, 32])), num_blocks=300)
+        n_tok = int(rng.integers(1, 1500))
+        ts, td = kvgen.table_pair(int(rng.integers(1 << 30)), n_tok, gs, gd)
+        t0 = int(rng.integers(0, n_tok))
+        tr = (t0, int(rng.integers(t0 + 1, n_tok + 1)))
+        c = int(rng.choice([1, 16, 100, 512, 5000]))
+        tok = 2 * L * n * 128
+        slot_bytes = tok * int(rng.choice([1, 3, 64, 1000]))
+        slots = int(rng.integers(2, 5))
+        hs = kvgen.fill_bytes(int(rng.integers(1 << 30)), gs.pool_bytes)
+        hd = kvgen.fill_bytes(int(rng.integers(1 << 30)), gd.pool_bytes)
+        want = hd.copy()
+        if heads:
+            oracle.migrate_heads(hs, gs, ts, want, gd, td, tr, None, (h0, h0 + n), 0)
+        else:
+            oracle.migrate(hs, gs, ts, want, gd, td, tr)
+        src, dst = pool_from_host(gs, hs), pool_from_host(gd, hd)
+        st, dt = dev_table(src, ts), dev_table(dst, td)
+        ch = dk.dyna_kv_channel_create(dst.handle, 2, slots, slot_bytes)
+        dk.dyna_kv_channel_set_timeout(ch, 120_000_000_000)
+        try:
+            sp, sq = torch.cuda.Stream(), torch.cuda.Stream()
+            if heads:
+                xp = dk.dyna_kv_push_heads(st, tr, (0, L), (h0, h0 + n), c, ch, sp.cuda_stream)
+                xq = dk.dyna_kv_place_heads(ch, dt, tr, (0, L), 0, n, c, sq.cuda_stream)
+            else:
+                xp = dk.dyna_kv_push(st, tr, (0, L), c, ch, sp.cuda_stream)
+                xq = dk.dyna_kv_place(ch, dt, tr, (0, L), c, sq.cuda_stream)
+            dk.dyna_kv_wait(xp)
+            dk.dyna_kv_wait(xq)
+            assert np.array_equal(dst.tensor.cpu().numpy(), want), (i, heads, tr, c, slots, slot_bytes)
+        finally:
+            dk.dyna_kv_channel_destroy(ch)
