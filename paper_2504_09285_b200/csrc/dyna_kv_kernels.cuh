@@ -29,6 +29,10 @@
 
 #include "plan.cuh"
 
+#ifndef DYNA_VEC_MINB
+#define DYNA_VEC_MINB 3  // resident 256-thread CTAs per SM the VEC engine (U <= 8) is compiled for
+#endif
+
 #ifndef DYNA_BULK_DEFER
 #define DYNA_BULK_DEFER 4  // stores committed after a chunk switch before its bytes are counted
 #endif
@@ -395,7 +399,7 @@ __global__ void __launch_bounds__(256, 3) k_copy_rows(const Plan p) {
 }
 
 template <int U, bool SIGNAL, class Src, bool READY = false>
-__global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : 3) k_copy_vec(const Src src, unsigned long long* sched_ctr) {
+__global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : DYNA_VEC_MINB) k_copy_vec(const Src src, unsigned long long* sched_ctr) {
   pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
