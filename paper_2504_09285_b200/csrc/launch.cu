@@ -204,15 +204,14 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
   auto kern = ws ? k_copy_bulk_ws<SIG, Src> : k_copy_bulk<SIG, Src>;
   const int threads = ws ? 64 : 32;
   {  // a ring deeper than the shared memory holds is cut to the stages that fit (at least 2)
-    static int avail = 0;
-    if (!avail) {
+    static const int avail = [] {  // (thread-safe static initialisation)
       int dev = 0, optin = 0;
       cudaFuncAttributes fa{};
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
       cudaFuncGetAttributes(&fa, (const void*)k_copy_bulk_ws<true, SingleSource>);  // the largest static smem
-      avail = optin - (int)fa.sharedSizeBytes;
-    }
+      return optin - (int)fa.sharedSizeBytes;
+    }();
     if ((int64_t)stages * piece > avail) stages = avail / piece;
     if (stages < 2) return fail(DYNA_EINVAL, "BULK: two %d-B pieces do not fit in shared memory", piece);
   }
@@ -290,13 +289,12 @@ dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st) {
   if (p.n_items >= (int64_t(1) << 31)) return fail(DYNA_ERANGE, "too many work items in one launch");
   DevInfo* di = dev_info(dev);
   const bool sig = p.counters != nullptr;
-  static int occ[2] = {0, 0};
-  int& o = occ[sig ? 1 : 0];
-  if (!o) {
-    if (sig) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_copy_rows<8, true>, kVecThreads, 0);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_copy_rows<8, false>, kVecThreads, 0);
-    if (o <= 0) o = 1;
-  }
+  static const int occ[2] = {  // (thread-safe static initialisation)
+      [] { int o = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_copy_rows<8, false>, kVecThreads, 0);
+           return o > 0 ? o : 1; }(),
+      [] { int o = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_copy_rows<8, true>, kVecThreads, 0);
+           return o > 0 ? o : 1; }()};
+  const int o = occ[sig ? 1 : 0];
   int64_t cap = (int64_t)di->sms * o;
   if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
   constexpr int wpc = kVecThreads / 32;
