@@ -227,6 +227,29 @@ DYNA_API dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_tabl
                                            int32_t chunk_tokens, struct CUstream_st* stream,
                                            const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
 
+/* Chunk streams (§4.3 P:556 "once chunk k completes, its
+ * KV block is immediately DMA-pushed"; decoded tokens join the open chunk,
+ * which closes when full or when r^alpha ends).  A stream is one logical migration of
+ * tokens [begin, ...) whose end is not known yet: the caller reports tokens as their KV
+ * is written (prefill chunks, then decoded tokens) and every chunk that became full is
+ * pushed at once (one fused launch on `stream`, ordered after the producer's work on it);
+ * closing pushes the open partial chunk.  With DYNA_MIGRATE_SIGNAL, chunk k of the stream
+ * (tokens [begin + k*c, ...)) raises inbox slot [sender][k] to the stream's epoch, exactly
+ * as one dyna_kv_migrate_ex over the whole range would.  Tables must cover every token
+ * reported and stay valid until dyna_kv_chunkstream_finish; FUSED variant, SM engines. */
+typedef struct dyna_kv_chunkstream* dyna_kv_chunkstream_t;
+DYNA_API dyna_status dyna_kv_chunkstream_open(dyna_block_table src, dyna_block_table dst, int64_t begin,
+                                         dyna_range layer_range, int32_t chunk_tokens, struct CUstream_st* stream,
+                                         const dyna_kv_opts* opts, dyna_kv_chunkstream_t* out);
+/* n_tokens more tokens have KV; *pushed (may be NULL) = chunks pushed by this call. */
+DYNA_API dyna_status dyna_kv_chunkstream_produced(dyna_kv_chunkstream_t s, int64_t n_tokens, int32_t* pushed);
+/* r^alpha ended: push the open partial chunk (if any); later produced() calls fail. */
+DYNA_API dyna_status dyna_kv_chunkstream_close(dyna_kv_chunkstream_t s, int32_t* pushed);
+DYNA_API dyna_status dyna_kv_chunkstream_info(dyna_kv_chunkstream_t s, uint64_t* epoch, int32_t* sender,
+                                         int64_t* produced_end, int64_t* pushed_end, int32_t* num_pushed);
+/* Wait for every pushed chunk, free the stream; returns the first deferred error. */
+DYNA_API dyna_status dyna_kv_chunkstream_finish(dyna_kv_chunkstream_t s);
+
 /* Many migrations in ONE kernel launch (a batch of short
  * requests, e.g. configs[2]'s 64-request skewed batch).  Every non-empty entry
  * is validated like dyna_kv_migrate; all sources must live on one device (the

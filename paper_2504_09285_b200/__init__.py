@@ -44,6 +44,8 @@ EXPORTS = (
     "dyna_kv_channel_create", "dyna_kv_channel_export", "dyna_kv_channel_import", "dyna_kv_channel_destroy",
     "dyna_kv_push", "dyna_kv_place", "dyna_kv_channel_set_timeout", "dyna_kv_ready_cancel",
     "dyna_kv_migrate_heads", "dyna_kv_batch_info", "dyna_kv_push_heads", "dyna_kv_place_heads",
+    "dyna_kv_chunkstream_open", "dyna_kv_chunkstream_produced", "dyna_kv_chunkstream_close",
+    "dyna_kv_chunkstream_info", "dyna_kv_chunkstream_finish",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -106,6 +108,13 @@ def _load():
                                  p(vp)]),
         "dyna_kv_migrate_ex": (st, [dyna_block_table, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32,
                                     vp, p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_chunkstream_open": (st, [dyna_block_table, dyna_block_table, ctypes.c_int64, dyna_range,
+                                          ctypes.c_int32, vp, p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_chunkstream_produced": (st, [vp, ctypes.c_int64, p(ctypes.c_int32)]),
+        "dyna_kv_chunkstream_close": (st, [vp, p(ctypes.c_int32)]),
+        "dyna_kv_chunkstream_info": (st, [vp, p(ctypes.c_uint64), p(ctypes.c_int32), p(ctypes.c_int64),
+                                          p(ctypes.c_int64), p(ctypes.c_int32)]),
+        "dyna_kv_chunkstream_finish": (st, [vp]),
         "dyna_kv_push_heads": (st, [dyna_block_table, dyna_range, dyna_range, dyna_range, ctypes.c_int32, vp, vp,
                                     p(vp)]),
         "dyna_kv_place_heads": (st, [vp, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32, ctypes.c_int32,
@@ -312,6 +321,39 @@ def dyna_kv_place(ch: int, dst: dyna_block_table, token_range, layer_range, chun
                              chunk_tokens, ctypes.c_void_p(stream), ctypes.byref(opts) if opts is not None else None,
                              ctypes.byref(out)))
     return out.value
+
+
+def dyna_kv_chunkstream_open(src: dyna_block_table, dst: dyna_block_table, begin: int, layer_range,
+                             chunk_tokens: int, stream: int = 0, opts: dyna_kv_opts | None = None) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_chunkstream_open(src, dst, begin, dyna_range(*layer_range), chunk_tokens,
+                                        ctypes.c_void_p(stream), ctypes.byref(opts) if opts is not None else None,
+                                        ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_chunkstream_produced(s: int, n_tokens: int) -> int:
+    n = ctypes.c_int32()
+    _check(lib.dyna_kv_chunkstream_produced(ctypes.c_void_p(s), n_tokens, ctypes.byref(n)))
+    return n.value
+
+
+def dyna_kv_chunkstream_close(s: int) -> int:
+    n = ctypes.c_int32()
+    _check(lib.dyna_kv_chunkstream_close(ctypes.c_void_p(s), ctypes.byref(n)))
+    return n.value
+
+
+def dyna_kv_chunkstream_info(s: int) -> dict:
+    e, snd, pe, pu, n = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+    _check(lib.dyna_kv_chunkstream_info(ctypes.c_void_p(s), ctypes.byref(e), ctypes.byref(snd), ctypes.byref(pe),
+                                        ctypes.byref(pu), ctypes.byref(n)))
+    return {"epoch": e.value, "sender": snd.value, "produced_end": pe.value, "pushed_end": pu.value,
+            "num_pushed": n.value}
+
+
+def dyna_kv_chunkstream_finish(s: int) -> None:
+    _check(lib.dyna_kv_chunkstream_finish(ctypes.c_void_p(s)))
 
 
 def dyna_kv_push_heads(src: dyna_block_table, token_range, layer_range, src_heads, chunk_tokens: int, ch: int,

@@ -179,9 +179,16 @@ dyna_status dyna_kv_migrate(dyna_block_table src, dyna_block_table dst, dyna_ran
   return dyna_kv_migrate_ex(src, dst, tr, lr, chunk_tokens, stream, nullptr, out);
 }
 
+// A chunk stream's call: one chunk of a logical migration that started at mig_t0; its flag
+// goes to slot (t0 - mig_t0) / c of the stream's epoch (dyna_kv_stream_*).
+struct ChunkCtx {
+  int64_t mig_t0;
+  uint64_t epoch;
+};
 static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
                                 int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
-                                dyna_kv_ready* board, uint64_t ready_epoch, dyna_kv_xfer_t* out);
+                                dyna_kv_ready* board, uint64_t ready_epoch, dyna_kv_xfer_t* out,
+                                const ChunkCtx* ctx = nullptr);
 
 dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
                                int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
@@ -198,12 +205,18 @@ dyna_status dyna_kv_migrate_on_ready(dyna_block_table src, dyna_block_table dst,
 
 static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
                                 int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
-                                dyna_kv_ready* board, uint64_t ready_epoch, dyna_kv_xfer_t* out) {
+                                dyna_kv_ready* board, uint64_t ready_epoch, dyna_kv_xfer_t* out,
+                                const ChunkCtx* ctx) {
   if (!out) return fail(DYNA_EINVAL, "NULL out");
   *out = nullptr;
   dyna_kv_opts o{};
   dyna_status r = check_opts(opts, &o);
   if (r) return r;
+  if (ctx) {  // chunk streams: one fused launch per chunk, flags in the stream's slots
+    if (o.variant == DYNA_VARIANT_STAGED || o.engine == DYNA_ENGINE_DMA)
+      return fail(DYNA_ENOTSUP, "chunk stream: FUSED variant, SM engines only");
+    o.variant = DYNA_VARIANT_FUSED;
+  }
   bool empty = false;
   if ((r = validate_pair(src, dst, tr, lr, chunk_tokens, &empty))) return r;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
@@ -213,8 +226,10 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int64_t ntok = tr.end - tr.begin;
   const int64_t nchunks = empty ? 0 : (ntok + chunk_tokens - 1) / chunk_tokens;
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
-  if (signal && nchunks > DYNA_MAX_CHUNKS)
-    return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks, DYNA_MAX_CHUNKS);
+  const int64_t slot0 = ctx ? (tr.begin - ctx->mig_t0) / chunk_tokens : 0;
+  if (signal && slot0 + nchunks > DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)(slot0 + nchunks),
+                DYNA_MAX_CHUNKS);
   if (board) {
     if (board->dev != src.pool->dev) return fail(DYNA_EINVAL, "ready board must live on the source device");
     const int64_t nslots = nchunks * ((o.flags & DYNA_READY_PER_LAYER) ? (lr.end - lr.begin) : 1);
@@ -305,13 +320,14 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     // K4 / K4-local: source rows -> destination rows, one launch for all chunks.
     const int64_t g = gcd64(gs.block_size, gd.block_size);
     Plan p = make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
+    if (ctx) set_chunking(p, ctx->mig_t0, tr.end, c);
     if (signal) {
       if ((r = channel_counters(S, D, S->dev, &p.counters))) {
         delete x;
         return r;
       }
       p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
-      p.epoch = x->epoch = next_epoch(gs.instance, D);
+      p.epoch = x->epoch = ctx ? ctx->epoch : next_epoch(gs.instance, D);
       p.sys_fence = peer_dst;
     }
     if (board) {
@@ -341,6 +357,117 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     return r;
   }
   *out = x;
+  return DYNA_OK;
+}
+
+// ---------------------------------------------------------------- chunk streams
+}  // extern "C"
+struct dyna_kv_chunkstream {
+  dyna_block_table src{}, dst{};
+  int64_t begin = 0, produced_end = 0, pushed_end = 0;
+  dyna_range layers{};
+  int32_t c = 0;
+  cudaStream_t stream = nullptr;
+  dyna_kv_opts opts{};
+  uint64_t epoch = 0;
+  int32_t sender = 0;
+  bool closed = false;
+  std::vector<dyna_kv_xfer_t> pushed;
+  dyna_status first_error = DYNA_OK;
+  std::string error_msg;
+};
+extern "C" {
+
+static dyna_status stream_push(dyna_kv_chunkstream* s, int64_t a, int64_t b) {
+  ChunkCtx ctx{s->begin, s->epoch};
+  dyna_kv_xfer_t x = nullptr;
+  dyna_status r = migrate_impl(s->src, s->dst, dyna_range{a, b}, s->layers, s->c,
+                               reinterpret_cast<struct CUstream_st*>(s->stream), &s->opts, nullptr, 0, &x, &ctx);
+  if (r) return r;
+  s->pushed.push_back(x);
+  s->pushed_end = b;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_chunkstream_open(dyna_block_table src, dyna_block_table dst, int64_t begin, dyna_range layer_range,
+                                int32_t chunk_tokens, struct CUstream_st* stream, const dyna_kv_opts* opts,
+                                dyna_kv_chunkstream_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  if (!src.pool || !dst.pool) return fail(DYNA_EINVAL, "NULL pool in a block table");
+  if (begin < 0 || chunk_tokens <= 0) return fail(DYNA_ERANGE, "begin >= 0 and chunk_tokens > 0");
+  dyna_kv_opts o{};
+  dyna_status r = check_opts(opts, &o);
+  if (r) return r;
+  if (o.variant == DYNA_VARIANT_STAGED || o.engine == DYNA_ENGINE_DMA || (o.flags & DYNA_READY_PER_LAYER))
+    return fail(DYNA_ENOTSUP, "chunk stream: FUSED variant, SM engines, no ready board");
+  auto* s = new dyna_kv_chunkstream();
+  s->src = src;
+  s->dst = dst;
+  s->begin = s->produced_end = s->pushed_end = begin;
+  s->layers = layer_range;
+  s->c = chunk_tokens;
+  s->stream = reinterpret_cast<cudaStream_t>(stream);
+  s->opts = o;
+  s->sender = src.pool->desc.instance;
+  if (o.flags & DYNA_MIGRATE_SIGNAL) s->epoch = next_epoch(s->sender, dst.pool);
+  *out = s;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_chunkstream_produced(dyna_kv_chunkstream_t s, int64_t n_tokens, int32_t* pushed) {
+  if (!s) return fail(DYNA_EINVAL, "NULL stream");
+  if (pushed) *pushed = 0;
+  if (s->closed) return fail(DYNA_EINVAL, "stream closed");
+  if (n_tokens < 0) return fail(DYNA_EINVAL, "n_tokens >= 0");
+  s->produced_end += n_tokens;
+  int32_t n = 0;
+  while (s->pushed_end + s->c <= s->produced_end) {  // every chunk that became full goes now
+    dyna_status r = stream_push(s, s->pushed_end, s->pushed_end + s->c);
+    if (r) return r;
+    ++n;
+  }
+  if (pushed) *pushed = n;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_chunkstream_close(dyna_kv_chunkstream_t s, int32_t* pushed) {
+  if (!s) return fail(DYNA_EINVAL, "NULL stream");
+  if (pushed) *pushed = 0;
+  if (s->closed) return DYNA_OK;
+  s->closed = true;
+  if (s->produced_end > s->pushed_end) {  // alpha ended: the open partial chunk goes now
+    dyna_status r = stream_push(s, s->pushed_end, s->produced_end);
+    if (r) return r;
+    if (pushed) *pushed = 1;
+  }
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_chunkstream_info(dyna_kv_chunkstream_t s, uint64_t* epoch, int32_t* sender, int64_t* produced_end,
+                                int64_t* pushed_end, int32_t* num_pushed) {
+  if (!s) return fail(DYNA_EINVAL, "NULL stream");
+  if (epoch) *epoch = s->epoch;
+  if (sender) *sender = s->sender;
+  if (produced_end) *produced_end = s->produced_end;
+  if (pushed_end) *pushed_end = s->pushed_end;
+  if (num_pushed) *num_pushed = (int32_t)s->pushed.size();
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_chunkstream_finish(dyna_kv_chunkstream_t s) {
+  if (!s) return fail(DYNA_EINVAL, "NULL stream");
+  dyna_status first = DYNA_OK;
+  std::string msg;
+  for (dyna_kv_xfer_t x : s->pushed) {
+    dyna_status r = dyna_kv_wait(x);
+    if (r && !first) {
+      first = r;
+      msg = g_err;
+    }
+  }
+  delete s;
+  if (first) return fail(first, "%s", msg.c_str());
   return DYNA_OK;
 }
 

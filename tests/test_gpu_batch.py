@@ -317,3 +317,53 @@ def test_signalled_batch_limits_and_errors():
         dk.dyna_kv_batch_info(x, 0)
     assert e.value.status == dk.DYNA_EINVAL
     dk.dyna_kv_wait(x)
+
+
+# ---------------------------------------------------------------- native chunk streams
+@pytest.mark.parametrize("signal", [False, True])
+def test_native_chunkstream_prefill_then_decode(signal):
+    """A 600-token prompt prefilled in 256-token steps, then 5 decoded tokens (s = 605 > P), pushed
+    by the library's chunk stream: chunks close when full or at close(); every chunk's flag is in
+    the stream's slots; the destination equals one plain migration of [begin, begin + 605)."""
+    g = Geom(3, 8, 128, 2, 16, 200)
+    begin, c = 7, 128
+    ts, td = kvgen.table_pair(77, 800, g, g)
+    hs, hd = kvgen.fill_bytes(61, g.pool_bytes), kvgen.fill_bytes(62, g.pool_bytes)
+    want = hd.copy()
+    oracle.migrate(hs, g, ts, want, g, td, (begin, begin + 605))
+    src, dst = pool_from_host(g, hs, instance=3), pool_from_host(g, hd)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    o = dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0)
+    s = dk.dyna_kv_chunkstream_open(st, dt, begin, (0, 3), c, 0, o)
+    pushed = [dk.dyna_kv_chunkstream_produced(s, n) for n in (256, 256, 88, 1, 1, 1, 1, 1)]
+    assert pushed == [2, 2, 0, 0, 0, 0, 0, 0]           # 4 full chunks; [512, 605) still open
+    assert dk.dyna_kv_chunkstream_close(s) == 1
+    info = dk.dyna_kv_chunkstream_info(s)
+    assert info["num_pushed"] == 5 and info["pushed_end"] == begin + 605 and info["produced_end"] == begin + 605
+    with pytest.raises(dk.DynaKVError):
+        dk.dyna_kv_chunkstream_produced(s, 1)         # closed
+    dk.dyna_kv_chunkstream_finish(s)
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
+    if signal:
+        fl = torch.zeros(5, dtype=torch.int64).pin_memory()
+        dk.dyna_kv_copy_flags(dst.handle, info["sender"], 0, 5, fl.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert (fl.numpy() == info["epoch"]).all()
+
+
+def test_native_chunkstream_empty_and_errors():
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(1, 256, g, g)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    s = dk.dyna_kv_chunkstream_open(st, dt, 0, (0, 2), 32, 0, None)
+    assert dk.dyna_kv_chunkstream_close(s) == 0         # s = 0: nothing to ship (P:309)
+    dk.dyna_kv_chunkstream_finish(s)
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_chunkstream_open(st, dt, 0, (0, 2), 32, 0, dk.opts(variant=dk.DYNA_VARIANT_STAGED))
+    assert e.value.status == dk.DYNA_ENOTSUP
+    s = dk.dyna_kv_chunkstream_open(st, dt, 0, (0, 2), 32, 0, None)
+    with pytest.raises(dk.DynaKVError) as e:              # the chunk beyond the tables is refused
+        dk.dyna_kv_chunkstream_produced(s, 300)
+    assert e.value.status == dk.DYNA_ERANGE
+    dk.dyna_kv_chunkstream_finish(s)
