@@ -236,7 +236,8 @@ DYNA_API dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_tabl
  * closing pushes the open partial chunk.  With DYNA_MIGRATE_SIGNAL, chunk k of the stream
  * (tokens [begin + k*c, ...)) raises inbox slot [sender][k] to the stream's epoch, exactly
  * as one dyna_kv_migrate_ex over the whole range would.  Tables must cover every token
- * reported and stay valid until dyna_kv_chunkstream_finish; FUSED variant, SM engines. */
+ * reported and stay valid until dyna_kv_chunkstream_finish; FUSED variant, SM engines.
+ * One chunk stream is driven by one thread at a time (the object is not locked). */
 typedef struct dyna_kv_chunkstream* dyna_kv_chunkstream_t;
 DYNA_API dyna_status dyna_kv_chunkstream_open(dyna_block_table src, dyna_block_table dst, int64_t begin,
                                          dyna_range layer_range, int32_t chunk_tokens, struct CUstream_st* stream,
