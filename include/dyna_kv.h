@@ -27,6 +27,19 @@
  * i.e. [L][2][NB][bs][H][d].  One token's K (or V) in one layer is one
  * contiguous "row" of H*d*e bytes; a block is bs consecutive rows.
  *
+ * API map:
+ *   pools            dyna_kv_pool_bytes / _create / _destroy, _export / _import (CUDA IPC)
+ *   the push         dyna_kv_migrate / _ex (variant, engine, SM budget, per-chunk flags)
+ *   completion       dyna_kv_wait / _query / _stream_wait, _xfer_info, _stream_wait_chunk,
+ *                    _copy_flags, _xfer_plan, _poll_error
+ *   many requests    dyna_kv_migrate_batch (+ _batch_info for per-request flags)
+ *   producer-coupled dyna_kv_ready_* + dyna_kv_migrate_on_ready (per chunk or per layer,
+ *                    cancellable)
+ *   decode-side      dyna_kv_chunkstream_* (chunks pushed as the tokens are produced)
+ *   receiver-steered dyna_kv_channel_* + dyna_kv_push / _place (and _heads forms)
+ *   TP resharding    dyna_kv_migrate_heads, dyna_kv_push_heads / _place_heads
+ *   selection        dyna_kv_calib_set / _get (the measured AUTO table)
+ *
  * Errors: every call returns a dyna_status; negative values are errors and
  * dyna_kv_last_error() returns a thread-local message.  No call throws.
  * Synchronous errors leave nothing enqueued.
