@@ -3,6 +3,8 @@ heads, head_dim, element size, block sizes on each side), random fragmented tabl
 token / layer / head ranges, chunk sizes, variants, engines and engine shapes, with and
 without per-chunk flags.  Every case is compared byte for byte on the whole destination pool
 (and the source pool is checked unchanged)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -14,6 +16,7 @@ from kvgen import Geom
 from gpu_util import dev_table, pool_from_host
 
 pytestmark = pytest.mark.gpu
+SCALE = int(os.environ.get("DYNA_FUZZ_SCALE", "1"))   # longer campaigns: DYNA_FUZZ_SCALE=10
 
 
 def _case(rng):
@@ -43,7 +46,7 @@ def _case(rng):
                                                         flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0)
 
 
-@pytest.mark.parametrize("block", range(8))
+@pytest.mark.parametrize("block", range(8 * SCALE))
 def test_fuzz_migrate(block):
     rng = np.random.default_rng(kvgen.MASTER_SEED + 500 + block)
     for i in range(40):
@@ -62,7 +65,7 @@ def test_fuzz_migrate(block):
         assert np.array_equal(got, want), (i, gs, gd, tr, lr, c, kw)
 
 
-@pytest.mark.parametrize("block", range(4))
+@pytest.mark.parametrize("block", range(4 * SCALE))
 def test_fuzz_migrate_heads(block):
     rng = np.random.default_rng(kvgen.MASTER_SEED + 900 + block)
     for i in range(40):
@@ -94,7 +97,7 @@ def test_fuzz_migrate_heads(block):
         assert np.array_equal(dst.tensor.cpu().numpy(), want), (i, gs, gd, tr, (h0, n, hd0), c, piece)
 
 
-@pytest.mark.parametrize("block", range(2))
+@pytest.mark.parametrize("block", range(2 * SCALE))
 def test_fuzz_batch(block):
     """Random batches: 1-12 requests with own ranges into one or two destination pools, random
     engine / piece, with or without per-request flags (each request's flags checked)."""
