@@ -504,22 +504,74 @@ __device__ __forceinline__ void bulk_wait_all() {
 }
 
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Accountant hand-off (signalling, ACC kernels): the copying thread posts (chunk, bytes)
+// after its bulk groups completed and a proxy fence; mbarrier arrive = release at CTA scope,
+// wait = acquire, so the accountant's GPU-scope fence + count covers the poster's writes.
+constexpr int kMail = 8;
+struct Mailbox {
+  uint64_t full[kMail], empty[kMail];
+  int32_t k[kMail];
+  uint32_t acc[kMail];
+  __device__ __forceinline__ void init() {
+    for (int m = 0; m < kMail; ++m) {
+      mbar_init(&full[m], 1);
+      mbar_init(&empty[m], 1);
+    }
+  }
+  __device__ __forceinline__ void post(int64_t& n, int32_t kk, uint32_t a) {
+    const int m = (int)(n % kMail);
+    if (n >= kMail) mbar_wait(&empty[m], (uint32_t)(((n / kMail) - 1) & 1));
+    k[m] = kk;
+    acc[m] = a;
+    mbar_arrive(&full[m]);
+    ++n;
+  }
+  // the accountant's loop, until the poster's sentinel (chunk -1)
+  __device__ __forceinline__ void serve(const Plan& p) {
+    for (int64_t i = 0;; ++i) {
+      const int m = (int)(i % kMail);
+      mbar_wait(&full[m], (uint32_t)((i / kMail) & 1));
+      const int32_t kk = k[m];
+      const uint32_t a = acc[m];
+      mbar_arrive(&empty[m]);
+      if (kk < 0) return;
+      fence_for(p);
+      account_chunk(p, kk, a);
+    }
+  }
+};
+
 // One thread per CTA drives a ring of `stages` smem slots of p.piece bytes:
 // loads land in slots ahead of the store front; each slot is reloaded once
 // the store issued from it has been read out of shared memory.
-template <bool SIGNAL, class Src>
-__global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, unsigned long long* sched_ctr) {
+template <bool SIGNAL, class Src, bool ACC = false>
+__global__ void __launch_bounds__(ACC ? 64 : 32) k_copy_bulk(const Src src, int stages,
+                                                             unsigned long long* sched_ctr) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ char* pend_dst[kMaxStages];
   __shared__ uint32_t pend_n[kMaxStages];
   __shared__ int32_t pend_k[kMaxStages];
-  if (threadIdx.x != 0) return;
+  __shared__ __align__(8) Mailbox mail[1];  // (used by ACC kernels only)
+  if (threadIdx.x != 0 && !(ACC && threadIdx.x == 32)) return;
 
-  for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    if (ACC) mail[0].init();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (ACC) __syncthreads();
   pdl_enter();
+  if (ACC && threadIdx.x == 32) {  // the accountant (ACC: the issuing thread never counts)
+    mail[0].serve(src.locate_signal());
+    return;
+  }
+  int64_t posted = 0;
 
   // Static round-robin only: this single thread's loop is latency-critical and
   // measured ~12% slower with the dynamic-scheduling path compiled in.
@@ -570,11 +622,17 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, uns
 #endif
 #if defined(DYNA_DIAG_NO_COUNT)
     (void)park_k;
-#elif defined(DYNA_BULK_FENCED_COUNT)
-    fence_for(p);
-    account_chunk(p, park_k, park_acc);
 #else
-    account_chunk_release(p, park_k, park_acc);
+    if (ACC) {  // the accountant thread counts (and fences) on the issuer's behalf
+      mail[0].post(posted, park_k, park_acc);
+    } else {
+#if defined(DYNA_BULK_FENCED_COUNT)
+      fence_for(p);
+      account_chunk(p, park_k, park_acc);
+#else
+      account_chunk_release(p, park_k, park_acc);
+#endif
+    }
 #endif
     park_k = -1;
     park_acc = 0;
@@ -610,10 +668,16 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, uns
     if (park_acc) flush_park(true);
     if (cur_acc) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      fence_for(p);
-      account_chunk(p, cur_k, cur_acc);
+      if (ACC) {
+        mail[0].post(posted, cur_k, cur_acc);
+      } else {
+        fence_for(p);
+        account_chunk(p, cur_k, cur_acc);
+      }
     }
   }
+  if (ACC) mail[0].post(posted, -1, 0);  // the accountant may leave
+  (void)posted;
 }
 
 // ------------------------------------------------------------------ BULK engine, warp-specialised
@@ -622,32 +686,66 @@ __global__ void __launch_bounds__(32) k_copy_bulk(const Src src, int stages, uns
 // a TMA bulk store and hands the slot back.  full[s] completes when a load's
 // bytes land (complete_tx); empty[s] when the store has read the slot out.
 // The loader's decode latency no longer sits between consecutive stores.
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
-template <bool SIGNAL, class Src>
-__global__ void __launch_bounds__(64) k_copy_bulk_ws(const Src src, int stages, unsigned long long* sched_ctr) {
+// ACC (signalling only): a third warp (one lane) does the chunk accounting.  The storer
+// hands each finished chunk's byte count over a small shared-memory mailbox (mbarrier
+// arrive = release at CTA scope, after its bulk groups completed and a proxy fence); the
+// accountant's GPU-scope fence + count then covers the storer's writes (causality through
+// the CTA-scope hand-off) without stalling the storer's pipeline.
+template <bool SIGNAL, class Src, bool ACC = false>
+__global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_bulk_ws(const Src src, int stages,
+                                                                unsigned long long* sched_ctr) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ __align__(8) uint64_t empty[kMaxStages];
   __shared__ char* pend_dst[kMaxStages];
   __shared__ uint32_t pend_n[kMaxStages];
   __shared__ int32_t pend_k[kMaxStages];
+  __shared__ __align__(8) uint64_t mail_full[ACC ? kMail : 1];
+  __shared__ __align__(8) uint64_t mail_empty[ACC ? kMail : 1];
+  __shared__ int32_t mail_k[ACC ? kMail : 1];
+  __shared__ uint32_t mail_acc[ACC ? kMail : 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
+    if (ACC)
+      for (int m = 0; m < kMail; ++m) {
+        mbar_init(&mail_full[m], 1);
+        mbar_init(&mail_empty[m], 1);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
   pdl_enter();
-  if (warp == 1 && lane != 0) return;  // the storer is one thread; the loader is a whole warp
+  if (warp >= 1 && lane != 0) return;  // storer and accountant are one thread each; the loader a warp
   const Plan& p = src.locate_signal();
   const int64_t n_items = src.total();
+  if (ACC && warp == 2) {  // ---------------- accountant
+    for (int64_t i = 0;; ++i) {
+      const int m = (int)(i % kMail);
+      mbar_wait(&mail_full[m], (uint32_t)((i / kMail) & 1));
+      const int32_t k = mail_k[m];
+      const uint32_t acc = mail_acc[m];
+      mbar_arrive(&mail_empty[m]);
+      if (k < 0) break;
+      fence_for(p);
+      account_chunk(p, k, acc);
+    }
+    return;
+  }
+  int64_t posted = 0;
+  auto post = [&](int32_t k, uint32_t acc) {  // storer -> accountant
+    const int m = (int)(posted % kMail);
+    if (posted >= kMail) mbar_wait(&mail_empty[m], (uint32_t)(((posted / kMail) - 1) & 1));
+    mail_k[m] = k;
+    mail_acc[m] = acc;
+    mbar_arrive(&mail_full[m]);
+    ++posted;
+  };
 
   if (warp == 0) {  // ---------------- loader: 32 lanes decode, lane 0 issues
     (void)sched_ctr;  // static round-robin over CTAs: item(m) = blockIdx.x + m * gridDim.x
@@ -701,8 +799,12 @@ __global__ void __launch_bounds__(64) k_copy_bulk_ws(const Src src, int stages, 
     auto flush_park = [&](bool all) {
       if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      fence_for(p);
-      account_chunk(p, park_k, park_acc);
+      if (ACC) {
+        post(park_k, park_acc);
+      } else {
+        fence_for(p);
+        account_chunk(p, park_k, park_acc);
+      }
       park_k = -1;
       park_acc = 0;
     };
@@ -738,10 +840,15 @@ __global__ void __launch_bounds__(64) k_copy_bulk_ws(const Src src, int stages, 
       if (park_acc) flush_park(true);
       if (cur_acc) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        fence_for(p);
-        account_chunk(p, cur_k, cur_acc);
+        if (ACC) {
+          post(cur_k, cur_acc);
+        } else {
+          fence_for(p);
+          account_chunk(p, cur_k, cur_acc);
+        }
       }
     }
+    if (ACC) post(-1, 0);  // the accountant may leave
   }
 }
 

@@ -3,6 +3,8 @@
 // launch), the staged variant (K1 gather, K2 transfer, K3 scatter; SURVEY §8
 // a2-a4), producer-coupled launches, and the small flag / fill kernels.  The only
 // translation unit that includes the kernels.
+#include <type_traits>
+
 #include "dyna_kv_kernels.cuh"
 #include "runtime.cuh"
 
@@ -32,7 +34,8 @@ void preload_kernels() {
       (const void*)k_copy_bulk<false, SingleSource>, (const void*)k_copy_bulk<true, SingleSource>,
       (const void*)k_copy_bulk<false, BatchSource>,
       (const void*)k_copy_bulk_ws<false, SingleSource>, (const void*)k_copy_bulk_ws<true, SingleSource>,
-      (const void*)k_copy_bulk_ws<false, BatchSource>,
+      (const void*)k_copy_bulk_ws<false, BatchSource>, (const void*)k_copy_bulk_ws<true, SingleSource, true>,
+      (const void*)k_copy_bulk<true, SingleSource, true>,
       (const void*)k_copy_rows<8, false>, (const void*)k_copy_rows<8, true>,
   };
   for (const void* k : ks) cudaFuncGetAttributes(&a, k);
@@ -46,6 +49,7 @@ void preload_kernels() {
       (const void*)k_copy_bulk<false, SingleSource>, (const void*)k_copy_bulk<true, SingleSource>,
       (const void*)k_copy_bulk<false, BatchSource>,  (const void*)k_copy_bulk_ws<false, SingleSource>,
       (const void*)k_copy_bulk_ws<true, SingleSource>, (const void*)k_copy_bulk_ws<false, BatchSource>,
+      (const void*)k_copy_bulk_ws<true, SingleSource, true>, (const void*)k_copy_bulk<true, SingleSource, true>,
   };
   for (const void* k : bulk) {
     cudaFuncGetAttributes(&a, k);
@@ -201,8 +205,18 @@ void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cuda
 template <bool SIG, class Src>
 dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, int64_t max_grid, int sms,
                         cudaStream_t st, unsigned long long* sched, bool ws) {
-  auto kern = ws ? k_copy_bulk_ws<SIG, Src> : k_copy_bulk<SIG, Src>;
-  const int threads = ws ? 64 : 32;
+  // Signalling through an accountant thread (measured): on for BULK_WS (its
+  // storer no longer stalls on the GPU-scope release), off for BULK (slower with it).
+  // DYNA_KV_ACCOUNTANT=0: never; =all: BULK too.
+  static const int acc_mode = [] {
+    const char* e = std::getenv("DYNA_KV_ACCOUNTANT");
+    if (!e) return 1;
+    return e[0] == '0' ? 0 : (std::strcmp(e, "all") == 0 ? 2 : 1);
+  }();
+  const bool acc = SIG && std::is_same<Src, SingleSource>::value && (ws ? acc_mode >= 1 : acc_mode == 2);
+  auto kern = ws ? (acc ? k_copy_bulk_ws<SIG, Src, true> : k_copy_bulk_ws<SIG, Src>)
+                 : (acc ? k_copy_bulk<SIG, Src, true> : k_copy_bulk<SIG, Src>);
+  const int threads = ws ? (acc ? 96 : 64) : (acc ? 64 : 32);
   {  // a ring deeper than the shared memory holds is cut to the stages that fit (at least 2)
     static const int avail = [] {  // (thread-safe static initialisation)
       int dev = 0, optin = 0;
