@@ -168,8 +168,9 @@ typedef struct {
  * library starts with the table measured on B200 (profiles/), replaceable at
  * run time.  Two measured rules apply on top of the table when the engine is
  * AUTO: no BULK engine when a contiguous run (min(gcd(bs_src, bs_dst),
- * chunk_tokens) * row bytes) is shorter than 16 KiB, and the VEC engine when
- * per-chunk flags are requested for more than one chunk in one call. */
+ * chunk_tokens) * row bytes) is shorter than 16 KiB, and, when per-chunk
+ * flags are requested for more than one chunk in one call, BULK_WS (whose
+ * chunk counting runs on an accountant thread) instead of BULK. */
 typedef struct {
     int32_t row_bytes;
     int32_t peer;

@@ -263,13 +263,22 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
   Choice ch = choose(o, row, peer_dst, ntok, std::min<int64_t>(gcd64(gs.block_size, gd.block_size), c) * row);
   if (signal && !o.engine && ch.engine != DYNA_ENGINE_VEC && nchunks > 1) {
-    // measured (bench.py e2e, per-chunk flags on): the VEC engine's per-warp fences beat
-    // BULK's release-add at every chunk switch (2720 vs 2540 GB/s); with ONE chunk per call
-    // (the paper's per-chunk push) BULK keeps the lead (182.8 vs 186.8 us per 512 MiB,
-    // scripts/sig_probe.py with C = S)
-    ch.engine = DYNA_ENGINE_VEC;
-    ch.unroll = kVecU;
-    if (!o.piece_bytes) ch.piece = kVecPiece;
+    // measured (bench.py e2e, per-chunk flags on): BULK's release-add at every chunk switch
+    // stalls its single issuing thread (2540 GB/s), VEC's per-warp fences do not (2720); the
+    // warp-specialised BULK_WS with an accountant thread beats both (e2e 2880 -> 2923 GB/s vs
+    // VEC, profiles/r01_ab_signal_ws.log).  With ONE chunk per call (the paper's per-chunk
+    // push) plain BULK keeps the lead (182.8 vs 186.8 us per 512 MiB, sig_probe with C = S).
+    static const bool ws = [] {  // DYNA_KV_SIGNAL_WS=0: VEC instead of BULK_WS
+      const char* e = std::getenv("DYNA_KV_SIGNAL_WS");
+      return !(e && e[0] == '0');
+    }();
+    if (ws && ch.engine == DYNA_ENGINE_BULK) {
+      ch.engine = DYNA_ENGINE_BULK_WS;
+    } else {
+      ch.engine = DYNA_ENGINE_VEC;
+      ch.unroll = kVecU;
+      if (!o.piece_bytes) ch.piece = kVecPiece;
+    }
   }
   if (board) {  // producer-coupled: the VEC engine (each warp waits on its own chunk's mark)
     ch.variant = DYNA_VARIANT_FUSED;
