@@ -33,6 +33,10 @@
 #define DYNA_VEC_MINB 3  // resident 256-thread CTAs per SM the VEC engine (U <= 8) is compiled for
 #endif
 
+#ifndef DYNA_MAIL_SLEEP
+#define DYNA_MAIL_SLEEP 0  // accountant poll back-off (ns); 0 = spin
+#endif
+
 #ifndef DYNA_BULK_DEFER
 #define DYNA_BULK_DEFER 4  // stores committed after a chunk switch before its bytes are counted
 #endif
@@ -530,11 +534,28 @@ struct Mailbox {
     mbar_arrive(&full[m]);
     ++n;
   }
-  // the accountant's loop, until the poster's sentinel (chunk -1)
+  // the accountant's loop, until the poster's sentinel (chunk -1); it polls with a short
+  // sleep between tries (DYNA_MAIL_SLEEP ns; 0 = spin in try_wait)
   __device__ __forceinline__ void serve(const Plan& p) {
     for (int64_t i = 0;; ++i) {
       const int m = (int)(i % kMail);
+#if DYNA_MAIL_SLEEP > 0
+      for (;;) {
+        uint32_t done;
+        asm volatile(
+            "{\n .reg .pred P1;\n"
+            " mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(smem_u32(&full[m])), "r"((uint32_t)((i / kMail) & 1))
+            : "memory");
+        if (done) break;
+        __nanosleep(DYNA_MAIL_SLEEP);
+      }
+#else
       mbar_wait(&full[m], (uint32_t)((i / kMail) & 1));
+#endif
       const int32_t kk = k[m];
       const uint32_t a = acc[m];
       mbar_arrive(&empty[m]);
