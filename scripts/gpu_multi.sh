@@ -4,6 +4,7 @@
 # experiment with the destination on another GPU.
 set -x
 N=$(nvidia-smi -L | wc -l)
+if [ "$N" -lt 2 ]; then echo "gpu_multi.sh: $N GPU visible, nothing to do"; exit 0; fi
 for n in 2 4 8; do
   [ $n -le $N ] || continue
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
