@@ -301,9 +301,9 @@ def run_dyna(args, rank, world, local_rank):
         i = k % N_SETS
         st, dt_ = e2e_tables[i]
         x = dk.dyna_kv_migrate_ex(st, dt_, (0, S_SPLIT), (0, g.num_layers), CHUNK, cs, sig_opts)
-        epoch = dk.dyna_kv_xfer_info(x)[0]
+        epoch, _, _, first = dk.dyna_kv_xfer_info(x)
         dk.dyna_kv_stream_wait(x, flag_stream.cuda_stream)
-        dk.dyna_kv_copy_flags(flag_pool, sender, 0, nchunks, flags_host[i].data_ptr(), flag_stream.cuda_stream)
+        dk.dyna_kv_copy_flags(flag_pool, sender, first, nchunks, flags_host[i].data_ptr(), flag_stream.cuda_stream)
         ev = torch.cuda.Event()
         ev.record(flag_stream)
         return x, epoch, ev, i

@@ -67,11 +67,13 @@ struct CUstream_st; /* cudaStream_t == struct CUstream_st* ; NULL = legacy defau
 
 typedef int32_t dyna_status;
 #define DYNA_OK         0
-#define DYNA_EINVAL    (-1)  /* NULL handle/pointer, bad option value, misaligned base */
+#define DYNA_EINVAL    (-1)  /* NULL handle/pointer, bad option value, misaligned base, destination table
+                                without host ids (aliasing unchecked) and no DYNA_MIGRATE_UNCHECKED */
 #define DYNA_EGEOM     (-2)  /* geometry mismatch (L, H, d, e differ) or row bytes % 16 != 0 */
 #define DYNA_ERANGE    (-3)  /* token/layer range outside the tables/pool, block id out of range,
                                 chunk_tokens <= 0, too many chunks for signalling */
-#define DYNA_EALIAS    (-4)  /* two destination rows coincide, or dst rows overlap src rows of the same pool */
+#define DYNA_EALIAS    (-4)  /* two destination rows coincide (within a call or a batch), dst rows overlap
+                                src rows of the same pool, or two distinct pools overlap in memory */
 #define DYNA_EPEER     (-5)  /* destination memory not reachable from the source device (no P2P / IPC) */
 #define DYNA_ENOMEM    (-6)
 #define DYNA_ECUDA     (-7)  /* a CUDA runtime error (message in dyna_kv_last_error) */
@@ -95,7 +97,8 @@ typedef struct {
 } dyna_kv_pool_desc;
 
 #define DYNA_MAX_INSTANCES 64
-#define DYNA_MAX_CHUNKS    4096   /* per migration when per-chunk flags are written */
+#define DYNA_MAX_CHUNKS    4096   /* inbox slots per (sender, destination pool): the most chunks one
+                                     signalled migration may have; slot ranges recycle after this many */
 
 typedef struct dyna_kv_pool* dyna_kv_pool_t;
 typedef struct dyna_kv_xfer* dyna_kv_xfer_t;
@@ -110,12 +113,19 @@ typedef struct dyna_kv_xfer* dyna_kv_xfer_t;
  *                   given: the library then copies the entries the call needs
  *                   ([0, last touched block]) to the device itself, ordered on
  *                   `stream` (a scheduler's tables usually live on the host).
- *   host_block_ids  HOST copy of the same ids.  When given for both tables,
- *                   ids are range-checked and destination aliasing is
- *                   rejected synchronously (DYNA_ERANGE / DYNA_EALIAS); the
- *                   host array may be reused as soon as the call returns.
- *                   When NULL, ids are range-checked on the device: offending
- *                   rows are skipped and dyna_kv_wait returns DYNA_ERANGE. */
+ *   host_block_ids  HOST copy of the same ids.  Where given, ids are
+ *                   range-checked and destination aliasing (DESIGN.md reading
+ *                   R7: two writes of one destination row, or a destination
+ *                   row that is also read as a source row) is rejected
+ *                   synchronously (DYNA_ERANGE / DYNA_EALIAS); the host array
+ *                   may be reused as soon as the call returns.  The DESTINATION
+ *                   table must carry host ids (and the source table too when
+ *                   it reads the destination pool), else the call fails with
+ *                   DYNA_EINVAL — unless opts->flags has DYNA_MIGRATE_UNCHECKED
+ *                   (the caller guarantees fresh, distinct destination blocks,
+ *                   e.g. from its allocator).  Ids without a host copy are
+ *                   range-checked on the device: offending rows are skipped and
+ *                   dyna_kv_wait returns DYNA_ERANGE. */
 typedef struct {
     dyna_kv_pool_t pool;
     const int32_t* block_ids;
@@ -132,15 +142,14 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
 /* Copy engine inside the kernels. */
 #define DYNA_ENGINE_AUTO 0
 #define DYNA_ENGINE_VEC  1     /* warp-per-segment 16-B vector loads/stores (LDG.128 / STG.128) */
-#define DYNA_ENGINE_BULK 2     /* TMA bulk copies through a shared-memory ring (UBLKCP), one issuing thread */
-#define DYNA_ENGINE_BULK_WS 3  /* same ring, warp-specialised: a loader warp and a storer warp (mbarrier hand-off) */
-#define DYNA_ENGINE_DMA  4     /* copy engines, no SM: one cudaMemcpyBatchAsync per chunk over the contiguous
-                                  runs ("DMA-pushed"); FUSED variant only, needs host_block_ids on both
-                                  tables, not for producer-coupled migrations (DYNA_ENOTSUP otherwise); with
-                                  DYNA_MIGRATE_SIGNAL a one-thread kernel releases each chunk's flag after its batch */
+#define DYNA_ENGINE_BULK 2     /* TMA bulk copies through a shared-memory ring (UBLKCP): one issuing thread,
+                                  fed item descriptors by a decoder warp */
+#define DYNA_ENGINE_BULK_WS 3  /* alias of DYNA_ENGINE_BULK (round-1 warp-specialised kernel with DYNA_KV_RING=0) */
 /* flags */
 #define DYNA_MIGRATE_SIGNAL 1  /* write a per-chunk flag into the destination pool's inbox */
 #define DYNA_READY_PER_LAYER 2 /* dyna_kv_migrate_on_ready: one ready mark per (chunk, layer), see below */
+#define DYNA_MIGRATE_UNCHECKED 4 /* destination tables may come without host ids: the caller guarantees that
+                                    no destination row is written twice or read as a source row (R7) */
 
 typedef struct {
     int32_t variant;    /* DYNA_VARIANT_*  (0 = auto) */
@@ -248,8 +257,10 @@ DYNA_API dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_tabl
  * is written (prefill chunks, then decoded tokens) and every chunk that became full is
  * pushed at once (one fused launch on `stream`, ordered after the producer's work on it);
  * closing pushes the open partial chunk.  With DYNA_MIGRATE_SIGNAL, chunk k of the stream
- * (tokens [begin + k*c, ...)) raises inbox slot [sender][k] to the stream's epoch, exactly
- * as one dyna_kv_migrate_ex over the whole range would.  Tables must cover every token
+ * (tokens [begin + k*c, ...)) raises inbox slot [sender][first_slot + k] to the stream's
+ * epoch, exactly as one dyna_kv_migrate_ex over the whole range would; the stream reserves
+ * its slots at open, as many as the destination table can hold chunks (at most
+ * DYNA_MAX_CHUNKS; a push beyond them fails with DYNA_ERANGE).  Tables must cover every token
  * reported and stay valid until dyna_kv_chunkstream_finish; FUSED variant, SM engines.
  * One chunk stream is driven by one thread at a time (the object is not locked). */
 typedef struct dyna_kv_chunkstream* dyna_kv_chunkstream_t;
@@ -261,7 +272,8 @@ DYNA_API dyna_status dyna_kv_chunkstream_produced(dyna_kv_chunkstream_t s, int64
 /* r^alpha ended: push the open partial chunk (if any); later produced() calls fail. */
 DYNA_API dyna_status dyna_kv_chunkstream_close(dyna_kv_chunkstream_t s, int32_t* pushed);
 DYNA_API dyna_status dyna_kv_chunkstream_info(dyna_kv_chunkstream_t s, uint64_t* epoch, int32_t* sender,
-                                         int64_t* produced_end, int64_t* pushed_end, int32_t* num_pushed);
+                                              int32_t* first_slot, int64_t* produced_end, int64_t* pushed_end,
+                                              int32_t* num_pushed);
 /* Wait for every pushed chunk, free the stream; returns the first deferred error. */
 DYNA_API dyna_status dyna_kv_chunkstream_finish(dyna_kv_chunkstream_t s);
 
@@ -269,15 +281,16 @@ DYNA_API dyna_status dyna_kv_chunkstream_finish(dyna_kv_chunkstream_t s);
  * requests, e.g. configs[2]'s 64-request skewed batch).  Every non-empty entry
  * is validated like dyna_kv_migrate; all sources must live on one device (the
  * launching device, `stream`'s) and share one row size; destinations may be
- * any reachable pools.  FUSED variant only (DYNA_ENOTSUP otherwise; no DMA
- * engine).  n <= DYNA_MAX_BATCH.  The descriptors are copied before the call
- * returns; block tables follow dyna_block_table's rules.
+ * any reachable pools.  FUSED variant only (DYNA_ENOTSUP otherwise).
+ * n <= DYNA_MAX_BATCH.  The descriptors are copied before the call
+ * returns; block tables follow dyna_block_table's rules, and aliasing (R7) is
+ * checked across entries: no destination row written by two entries, none
+ * read as a source row by any entry.
  * Per-chunk signalling (opts->flags & DYNA_MIGRATE_SIGNAL; VEC engine): every
  * entry gets its own epoch and a disjoint range of inbox slots of its
  * (sender, destination pool) — see dyna_kv_batch_info — so each request's
- * r^beta can start as soon as its own chunks landed.  The signalled chunks of
- * one batch into one destination pool from one sender must fit in
- * DYNA_MAX_CHUNKS (DYNA_ERANGE otherwise). */
+ * r^beta can start as soon as its own chunks landed.  Each entry's chunks must
+ * fit in DYNA_MAX_CHUNKS (DYNA_ERANGE otherwise). */
 #define DYNA_MAX_BATCH 16384
 typedef struct {
     dyna_block_table src, dst;
@@ -317,7 +330,7 @@ DYNA_API dyna_status dyna_kv_batch_info(dyna_kv_xfer_t xfer, int32_t index, uint
  * run the producer's kernels once before the first coupled migration (or set
  * CUDA_MODULE_LOADING=EAGER).  Each chunk wait therefore gives up after the board's timeout
  * (default 10 s; dyna_kv_ready_set_timeout) and dyna_kv_wait then returns
- * DYNA_ETIMEDOUT (the rows of late chunks are then unspecified). */
+ * DYNA_ETIMEDOUT (a chunk whose wait timed out is skipped: no flag, rows unspecified). */
 typedef struct dyna_kv_ready* dyna_kv_ready_t;
 DYNA_API dyna_status dyna_kv_ready_create(int32_t device, int32_t max_chunks, dyna_kv_ready_t* out);
 DYNA_API dyna_status dyna_kv_ready_destroy(dyna_kv_ready_t board);
@@ -423,8 +436,11 @@ DYNA_API dyna_status dyna_kv_place_heads(dyna_kv_channel_t ch, dyna_block_table 
  * epoch assigned at capture time. */
 
 /* Block the host until every chunk is resident in the destination, report
- * deferred errors (DYNA_ECUDA, DYNA_ERANGE from device-side id checks), free
- * the handle. */
+ * deferred errors (DYNA_ECUDA; DYNA_ERANGE from device-side id checks,
+ * DYNA_ETIMEDOUT from device-side waits) of THIS migration — each handle has
+ * its own deferred-error word, so concurrent migrations never see each
+ * other's errors — and free the handle.  (Migrations captured into a CUDA
+ * graph report through dyna_kv_poll_error instead.) */
 DYNA_API dyna_status dyna_kv_wait(dyna_kv_xfer_t xfer);
 
 /* Non-blocking: DYNA_OK if complete, DYNA_EAGAIN if in flight.  Does not free. */
@@ -436,11 +452,19 @@ DYNA_API dyna_status dyna_kv_query(dyna_kv_xfer_t xfer);
 DYNA_API dyna_status dyna_kv_stream_wait(dyna_kv_xfer_t xfer, struct CUstream_st* stream);
 
 /* Per-chunk readiness (DYNA_MIGRATE_SIGNAL).  Each signalled migration gets
- * an epoch, monotone per (sender instance, destination pool).  Chunk k of
- * that migration is resident when the destination inbox slot [sender][k]
- * holds a value >= epoch.  Migrations from one sender into one destination
- * pool that request signalling must be ordered on one stream. */
-DYNA_API dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t xfer, uint64_t* epoch, int32_t* num_chunks, int32_t* sender);
+ * an epoch, monotone per (sender instance, destination pool), and its own
+ * range of consecutive inbox slots [first_slot, first_slot + num_chunks) of
+ * that (sender, destination pool).  Chunk k of the migration is resident when
+ * inbox slot [sender][first_slot + k] holds a value >= epoch.  Concurrent
+ * signalled migrations (any streams, any threads, chunk streams included) use
+ * disjoint slots; a slot is reused only after DYNA_MAX_CHUNKS further chunks
+ * were reserved by the same sender for the same pool, and flags are raised
+ * with an atomic max (never lowered).  Epochs and slots are keyed on the
+ * destination pool's identity, which an IPC export carries, and start above
+ * every flag already in the row, so a restarted sender or a re-imported pool
+ * never reuses an epoch.  Any pointer may be NULL. */
+DYNA_API dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t xfer, uint64_t* epoch, int32_t* num_chunks, int32_t* sender,
+                                       int32_t* first_slot);
 
 /* What a migration resolved to (AUTO choices included) and how many kernels
  * it launched — for logs and benchmarks.  Any pointer may be NULL. */
@@ -448,10 +472,11 @@ DYNA_API dyna_status dyna_kv_xfer_plan(dyna_kv_xfer_t xfer, int32_t* variant, in
                                        int32_t* stages, int32_t* unroll, int32_t* launches);
 
 /* Enqueue on `stream` (a stream of the DESTINATION pool's device) a device
- * wait (acquire, system scope) until chunk `chunk` from `sender` reaches
- * `epoch`; work after it on `stream` sees the chunk's rows.  timeout_ns 0 =
- * no timeout; on timeout the kernel records DYNA_ETIMEDOUT for the next
- * dyna_kv_wait / dyna_kv_poll_error on that process. */
+ * wait (acquire, system scope) until inbox slot `chunk` (= first_slot + k for
+ * chunk k of a migration, dyna_kv_xfer_info) from `sender` reaches `epoch`;
+ * work after it on `stream` sees the chunk's rows.  timeout_ns 0 = no
+ * timeout; on timeout the kernel records DYNA_ETIMEDOUT for the next
+ * dyna_kv_poll_error on that process. */
 DYNA_API dyna_status dyna_kv_stream_wait_chunk(dyna_kv_pool_t dst, int32_t sender, int32_t chunk,
                                       uint64_t epoch, uint64_t timeout_ns,
                                       struct CUstream_st* stream);
@@ -492,6 +517,7 @@ typedef struct {
     uint8_t inbox_mem[64];   /* cudaIpcMemHandle_t of the pool's flag inbox */
     uint64_t pool_offset;    /* byte offset of device_base inside its allocation */
     dyna_kv_pool_desc desc;  /* the owner's geometry */
+    uint64_t uid;            /* the pool's identity (flag epochs / slots and alias checks key on it) */
 } dyna_kv_ipc_handle;
 
 DYNA_API dyna_status dyna_kv_pool_export(dyna_kv_pool_t pool, dyna_kv_ipc_handle* out);

@@ -27,9 +27,10 @@ STATUS_NAMES = {0: "DYNA_OK", -1: "DYNA_EINVAL", -2: "DYNA_EGEOM", -3: "DYNA_ERA
                 -10: "DYNA_ENOTSUP", -11: "DYNA_ECANCELED"}
 DYNA_MAX_INSTANCES, DYNA_MAX_CHUNKS = 64, 4096
 DYNA_VARIANT_AUTO, DYNA_VARIANT_FUSED, DYNA_VARIANT_STAGED = 0, 1, 2
-DYNA_ENGINE_AUTO, DYNA_ENGINE_VEC, DYNA_ENGINE_BULK, DYNA_ENGINE_BULK_WS, DYNA_ENGINE_DMA = 0, 1, 2, 3, 4
+DYNA_ENGINE_AUTO, DYNA_ENGINE_VEC, DYNA_ENGINE_BULK, DYNA_ENGINE_BULK_WS = 0, 1, 2, 3
 DYNA_MIGRATE_SIGNAL = 1
 DYNA_READY_PER_LAYER = 2
+DYNA_MIGRATE_UNCHECKED = 4
 DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC = 1, 2
 
 # every symbol include/dyna_kv.h declares
@@ -80,7 +81,7 @@ class dyna_kv_calib_entry(ctypes.Structure):
 
 class dyna_kv_ipc_handle(ctypes.Structure):
     _fields_ = [("pool_mem", ctypes.c_uint8 * 64), ("inbox_mem", ctypes.c_uint8 * 64),
-                ("pool_offset", ctypes.c_uint64), ("desc", dyna_kv_pool_desc)]
+                ("pool_offset", ctypes.c_uint64), ("desc", dyna_kv_pool_desc), ("uid", ctypes.c_uint64)]
 
 
 class dyna_kv_channel_handle(ctypes.Structure):
@@ -112,8 +113,8 @@ def _load():
                                           ctypes.c_int32, vp, p(dyna_kv_opts), p(vp)]),
         "dyna_kv_chunkstream_produced": (st, [vp, ctypes.c_int64, p(ctypes.c_int32)]),
         "dyna_kv_chunkstream_close": (st, [vp, p(ctypes.c_int32)]),
-        "dyna_kv_chunkstream_info": (st, [vp, p(ctypes.c_uint64), p(ctypes.c_int32), p(ctypes.c_int64),
-                                          p(ctypes.c_int64), p(ctypes.c_int32)]),
+        "dyna_kv_chunkstream_info": (st, [vp, p(ctypes.c_uint64), p(ctypes.c_int32), p(ctypes.c_int32),
+                                          p(ctypes.c_int64), p(ctypes.c_int64), p(ctypes.c_int32)]),
         "dyna_kv_chunkstream_finish": (st, [vp]),
         "dyna_kv_push_heads": (st, [dyna_block_table, dyna_range, dyna_range, dyna_range, ctypes.c_int32, vp, vp,
                                     p(vp)]),
@@ -144,7 +145,7 @@ def _load():
         "dyna_kv_wait": (st, [vp]),
         "dyna_kv_query": (st, [vp]),
         "dyna_kv_stream_wait": (st, [vp, vp]),
-        "dyna_kv_xfer_info": (st, [vp, p(ctypes.c_uint64), p(ctypes.c_int32), p(ctypes.c_int32)]),
+        "dyna_kv_xfer_info": (st, [vp, p(ctypes.c_uint64), p(ctypes.c_int32), p(ctypes.c_int32), p(ctypes.c_int32)]),
         "dyna_kv_xfer_plan": (st, [vp] + [p(ctypes.c_int32)] * 6),
         "dyna_kv_stream_wait_chunk": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_uint64,
                                            vp]),
@@ -345,11 +346,12 @@ def dyna_kv_chunkstream_close(s: int) -> int:
 
 
 def dyna_kv_chunkstream_info(s: int) -> dict:
-    e, snd, pe, pu, n = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
-    _check(lib.dyna_kv_chunkstream_info(ctypes.c_void_p(s), ctypes.byref(e), ctypes.byref(snd), ctypes.byref(pe),
-                                        ctypes.byref(pu), ctypes.byref(n)))
-    return {"epoch": e.value, "sender": snd.value, "produced_end": pe.value, "pushed_end": pu.value,
-            "num_pushed": n.value}
+    e, snd, fs = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_int32()
+    pe, pu, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+    _check(lib.dyna_kv_chunkstream_info(ctypes.c_void_p(s), ctypes.byref(e), ctypes.byref(snd), ctypes.byref(fs),
+                                        ctypes.byref(pe), ctypes.byref(pu), ctypes.byref(n)))
+    return {"epoch": e.value, "sender": snd.value, "first_slot": fs.value, "produced_end": pe.value,
+            "pushed_end": pu.value, "num_pushed": n.value}
 
 
 def dyna_kv_chunkstream_finish(s: int) -> None:
@@ -389,10 +391,12 @@ def dyna_kv_stream_wait(xfer: int, stream: int) -> None:
     _check(lib.dyna_kv_stream_wait(ctypes.c_void_p(xfer), ctypes.c_void_p(stream)))
 
 
-def dyna_kv_xfer_info(xfer: int) -> tuple[int, int, int]:
-    e, n, s = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_int32()
-    _check(lib.dyna_kv_xfer_info(ctypes.c_void_p(xfer), ctypes.byref(e), ctypes.byref(n), ctypes.byref(s)))
-    return e.value, n.value, s.value
+def dyna_kv_xfer_info(xfer: int) -> tuple[int, int, int, int]:
+    """(epoch, num_chunks, sender, first_slot): chunk k's flag is inbox slot [sender][first_slot + k]."""
+    e, n, s, f = ctypes.c_uint64(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.dyna_kv_xfer_info(ctypes.c_void_p(xfer), ctypes.byref(e), ctypes.byref(n), ctypes.byref(s),
+                                 ctypes.byref(f)))
+    return e.value, n.value, s.value, f.value
 
 
 def dyna_kv_xfer_plan(xfer: int) -> dict:

@@ -238,18 +238,18 @@ dyna_status dyna_kv_push(dyna_block_table src, dyna_range tr, dyna_range lr, int
   dyna_status r = chan_check(ch, src, tr, lr, c, &empty);
   if (r) return r;
   dyna_kv_pool* S = src.pool;
-  auto* x = new dyna_kv_xfer();
-  x->dev = S->dev;
-  x->sender = ch->sender;
   if (empty) {
+    auto* x = new dyna_kv_xfer();
+    x->dev = S->dev;
+    x->sender = ch->sender;
     x->empty = true;
     *out = x;
     return DYNA_OK;
   }
-  if (ch->imported ? ch->dev != S->dev : (ch->dev != S->dev && (r = ensure_peer(S->dev, ch->dev)) != DYNA_OK)) {
-    delete x;
+  if (ch->imported ? ch->dev != S->dev : (ch->dev != S->dev && (r = ensure_peer(S->dev, ch->dev)) != DYNA_OK))
     return r ? r : fail(DYNA_EPEER, "channel mapped on device %d, source on %d", ch->dev, S->dev);
-  }
+  dyna_kv_xfer* x = nullptr;
+  if ((r = new_xfer(S->dev, ch->sender, reinterpret_cast<cudaStream_t>(stream_), &x))) return r;
   std::lock_guard<std::mutex> lk(ch->mu);
   if ((r = chan_counters(&ch->push_counters, S->dev))) {
     delete x;
@@ -269,11 +269,12 @@ dyna_status dyna_kv_push(dyna_block_table src, dyna_range tr, dyna_range lr, int
       const uint64_t q = ch->push_seq++;
       const int slot = (int)(q % ch->slots);
       if (q >= (uint64_t)ch->slots) {  // wait for the receiver's credit on this slot
-        launch_wait_flag(ch->credit + slot, q - ch->slots + 1, ch->timeout_ns, stream);
+        launch_wait_flag(ch->credit + slot, q - ch->slots + 1, ch->timeout_ns, stream, x->err);
       }
       // gather straight into the receiver's slot; the last writer releases full[slot] = q + 1
       Plan p = make_plan(paged(S, src.block_ids), linear(ch->base + (size_t)slot * ch->slot_bytes), S->row, sa,
                          sb, l0, lm, sb - sa, S->desc.block_size, kVecPiece);
+      p.err = x->err;
       p.counters = ch->push_counters;
       p.flags = ch->full + slot;
       p.epoch = q + 1;
@@ -311,22 +312,27 @@ dyna_status dyna_kv_place(dyna_kv_channel_t ch, dyna_block_table dst, dyna_range
   dyna_kv_pool* D = dst.pool;
   const int64_t nchunks = empty ? 0 : (tr.end - tr.begin + c - 1) / c;
   if (signal && nchunks > DYNA_MAX_CHUNKS) return fail(DYNA_ERANGE, "too many chunks for signalling");
-  auto* x = new dyna_kv_xfer();
-  x->dev = D->dev;
-  x->sender = ch->sender;
-  x->nchunks = (int32_t)nchunks;
   if (empty) {
+    auto* x = new dyna_kv_xfer();
+    x->dev = D->dev;
+    x->sender = ch->sender;
     x->empty = true;
     *out = x;
     return DYNA_OK;
   }
+  dyna_kv_xfer* x = nullptr;
+  if ((r = new_xfer(D->dev, ch->sender, reinterpret_cast<cudaStream_t>(stream_), &x))) return r;
+  x->nchunks = (int32_t)nchunks;
   std::lock_guard<std::mutex> lk(ch->mu);
+  unsigned long long *flags = nullptr, *counters = nullptr;
   if (signal) {
-    if ((r = chan_counters(&ch->place_counters, D->dev))) {
+    if ((r = chan_counters(&ch->place_counters, D->dev)) ||
+        (r = flag_reserve(ch->sender, D, nchunks, &x->epoch, &x->first_slot))) {
       delete x;
       return r;
     }
-    x->epoch = next_epoch(ch->sender, D);
+    flags = D->inbox + (size_t)ch->sender * DYNA_MAX_CHUNKS + x->first_slot;
+    counters = ch->place_counters + x->first_slot;
   }
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   DeviceGuard guard(D->dev);
@@ -339,13 +345,14 @@ dyna_status dyna_kv_place(dyna_kv_channel_t ch, dyna_block_table dst, dyna_range
       const int64_t sb = std::min(sa + sc, b);
       const uint64_t q = ch->place_seq++;
       const int slot = (int)(q % ch->slots);
-      launch_wait_flag(ch->full + slot, q + 1, ch->timeout_ns, stream);
+      launch_wait_flag(ch->full + slot, q + 1, ch->timeout_ns, stream, x->err);
       Plan p = make_plan(linear(ch->base + (size_t)slot * ch->slot_bytes), paged(D, dst.block_ids), D->row, sa, sb,
                          l0, lm, sb - sa, D->desc.block_size, kVecPiece);
       set_chunking(p, tr.begin, tr.end, c);
+      p.err = x->err;
       if (signal) {
-        p.counters = ch->place_counters;
-        p.flags = D->inbox + (size_t)ch->sender * DYNA_MAX_CHUNKS;
+        p.counters = counters;
+        p.flags = flags;
         p.epoch = x->epoch;
       }
       r = launch_copy(p, DYNA_ENGINE_VEC, o.max_ctas, kBulkStages, kVecU, D->dev, stream, 0);
@@ -390,18 +397,18 @@ dyna_status dyna_kv_push_heads(dyna_block_table src, dyna_range tr, dyna_range l
   bool empty = false;
   if ((r = chan_check(ch, src, tr, lr, c, &empty, slice))) return r;
   dyna_kv_pool* S = src.pool;
-  auto* x = new dyna_kv_xfer();
-  x->dev = S->dev;
-  x->sender = ch->sender;
   if (empty) {
+    auto* x = new dyna_kv_xfer();
+    x->dev = S->dev;
+    x->sender = ch->sender;
     x->empty = true;
     *out = x;
     return DYNA_OK;
   }
-  if (ch->imported ? ch->dev != S->dev : (ch->dev != S->dev && (r = ensure_peer(S->dev, ch->dev)) != DYNA_OK)) {
-    delete x;
+  if (ch->imported ? ch->dev != S->dev : (ch->dev != S->dev && (r = ensure_peer(S->dev, ch->dev)) != DYNA_OK))
     return r ? r : fail(DYNA_EPEER, "channel mapped on device %d, source on %d", ch->dev, S->dev);
-  }
+  dyna_kv_xfer* x = nullptr;
+  if ((r = new_xfer(S->dev, ch->sender, reinterpret_cast<cudaStream_t>(stream_), &x))) return r;
   std::lock_guard<std::mutex> lk(ch->mu);
   if ((r = chan_counters(&ch->push_counters, S->dev))) {
     delete x;
@@ -421,10 +428,11 @@ dyna_status dyna_kv_push_heads(dyna_block_table src, dyna_range tr, dyna_range l
       const int64_t sb = std::min(sa + sc, b);
       const uint64_t q = ch->push_seq++;
       const int slot = (int)(q % ch->slots);
-      if (q >= (uint64_t)ch->slots) launch_wait_flag(ch->credit + slot, q - ch->slots + 1, ch->timeout_ns, stream);
+      if (q >= (uint64_t)ch->slots) launch_wait_flag(ch->credit + slot, q - ch->slots + 1, ch->timeout_ns, stream, x->err);
       Plan p = make_plan_sliced(paged(S, src.block_ids), linear(ch->base + (size_t)slot * ch->slot_bytes), slice,
                                 S->row, src_heads.begin * he, slice, 0, sa, sb, l0, lm, sb - sa, S->desc.block_size,
                                 kVecPiece);
+      p.err = x->err;
       p.counters = ch->push_counters;
       p.flags = ch->full + slot;
       p.epoch = q + 1;
@@ -466,22 +474,27 @@ dyna_status dyna_kv_place_heads(dyna_kv_channel_t ch, dyna_block_table dst, dyna
   dyna_kv_pool* D = dst.pool;
   const int64_t nchunks = empty ? 0 : (tr.end - tr.begin + c - 1) / c;
   if (signal && nchunks > DYNA_MAX_CHUNKS) return fail(DYNA_ERANGE, "too many chunks for signalling");
-  auto* x = new dyna_kv_xfer();
-  x->dev = D->dev;
-  x->sender = ch->sender;
-  x->nchunks = (int32_t)nchunks;
   if (empty) {
+    auto* x = new dyna_kv_xfer();
+    x->dev = D->dev;
+    x->sender = ch->sender;
     x->empty = true;
     *out = x;
     return DYNA_OK;
   }
+  dyna_kv_xfer* x = nullptr;
+  if ((r = new_xfer(D->dev, ch->sender, reinterpret_cast<cudaStream_t>(stream_), &x))) return r;
+  x->nchunks = (int32_t)nchunks;
   std::lock_guard<std::mutex> lk(ch->mu);
+  unsigned long long *flags = nullptr, *counters = nullptr;
   if (signal) {
-    if ((r = chan_counters(&ch->place_counters, D->dev))) {
+    if ((r = chan_counters(&ch->place_counters, D->dev)) ||
+        (r = flag_reserve(ch->sender, D, nchunks, &x->epoch, &x->first_slot))) {
       delete x;
       return r;
     }
-    x->epoch = next_epoch(ch->sender, D);
+    flags = D->inbox + (size_t)ch->sender * DYNA_MAX_CHUNKS + x->first_slot;
+    counters = ch->place_counters + x->first_slot;
   }
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   DeviceGuard guard(D->dev);
@@ -495,14 +508,15 @@ dyna_status dyna_kv_place_heads(dyna_kv_channel_t ch, dyna_block_table dst, dyna
       const int64_t sb = std::min(sa + sc, b);
       const uint64_t q = ch->place_seq++;
       const int slot = (int)(q % ch->slots);
-      launch_wait_flag(ch->full + slot, q + 1, ch->timeout_ns, stream);
+      launch_wait_flag(ch->full + slot, q + 1, ch->timeout_ns, stream, x->err);
       Plan p = make_plan_sliced(linear(ch->base + (size_t)slot * ch->slot_bytes), paged(D, dst.block_ids), slice,
                                 slice, 0, D->row, (int64_t)dst_head_begin * he, sa, sb, l0, lm, sb - sa,
                                 D->desc.block_size, kVecPiece);
       set_chunking(p, tr.begin, tr.end, c);
+      p.err = x->err;
       if (signal) {
-        p.counters = ch->place_counters;
-        p.flags = D->inbox + (size_t)ch->sender * DYNA_MAX_CHUNKS;
+        p.counters = counters;
+        p.flags = flags;
         p.epoch = x->epoch;
       }
       r = launch_rows(p, o.max_ctas, D->dev, stream);

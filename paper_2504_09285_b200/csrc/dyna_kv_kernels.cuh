@@ -159,8 +159,11 @@ __device__ __forceinline__ SItem decode_item_sliced(const Plan& p, int64_t item)
   return it;
 }
 
-__device__ __forceinline__ void st_release_sys(unsigned long long* ptr, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(ptr), "l"(v) : "memory");
+// A chunk flag is raised, never lowered: max with release semantics at system scope (the
+// receiver may be another GPU).  Slot ranges recycle after DYNA_MAX_CHUNKS chunks; a late
+// writer of an older epoch then cannot move a newer flag backwards.
+__device__ __forceinline__ void raise_flag(unsigned long long* ptr, unsigned long long v) {
+  asm volatile("red.release.sys.global.max.u64 [%0], %1;" ::"l"(ptr), "l"(v) : "memory");
 }
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* ptr) {
   unsigned long long v;
@@ -179,7 +182,8 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
 // (chunk k, or (chunk k, layer l) when marks are per layer).  Returns false when
 // the migration was cancelled before the mark became visible: the caller skips
 // the slot's items.  A visible mark always wins, so a marked slot is copied by
-// every warp that owns part of it.
+// every warp that owns part of it.  A wait that times out is treated like a cancel
+// (ERR_TIMEOUT recorded): the slot's rows were never marked, so its chunk gets no flag.
 __device__ __forceinline__ bool wait_ready(const Plan& p, int32_t slot) {
   if (ld_acquire_gpu(p.ready + slot) >= p.ready_epoch) return true;
   unsigned long long t0, now;
@@ -191,7 +195,7 @@ __device__ __forceinline__ bool wait_ready(const Plan& p, int32_t slot) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     if (now - t0 > p.ready_timeout_ns) {  // never hang the device: report at dyna_kv_wait
       if (p.err) atomicOr(p.err, ERR_TIMEOUT);
-      return true;
+      return false;
     }
   }
   return true;
@@ -220,7 +224,7 @@ __device__ __forceinline__ void account_chunk(const Plan& p, int32_t k, unsigned
     *ctr = 0ull;
     if (now >= kPoison) return;  // a part of the chunk was skipped (cancelled): no flag
     __threadfence_system();
-    st_release_sys(p.flags + k, p.epoch);
+    raise_flag(p.flags + k, p.epoch);
   }
 }
 
@@ -286,7 +290,7 @@ __device__ __forceinline__ void account_chunk_release(const Plan& p, int32_t k, 
   if (old + n == total) {
     __threadfence_system();  // acquire the other contributors' releases before publishing
     *ctr = 0ull;
-    st_release_sys(p.flags + k, p.epoch);
+    raise_flag(p.flags + k, p.epoch);
   }
 }
 
@@ -871,6 +875,161 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_bulk_ws(const Src src, i
     }
     if (ACC) post(-1, 0);  // the accountant may leave
   }
+}
+
+// ------------------------------------------------------------------ BULK engine, decoder-fed ring
+// One thread (warp 0, lane 0) drives the TMA ring exactly as k_copy_bulk does, but it never
+// decodes: warp 1 decodes the CTA's items 32 at a time (one per lane: the divisions and the
+// two block-table loads of decode_item, and the batch's plan lookup) into a shared-memory
+// queue of descriptors, NQ batches ahead.  The issuer's loop is then: wait for a landed
+// slot, issue its store, wait for an older store to have read its slot, read the next
+// descriptor from shared memory, issue its load.  Measured with precomputed items
+// (scripts/native/copy_micro.cu, profiles/r02_copy_micro.jsonl): this loop moves random
+// 32-KiB blocks at 3120 GB/s payload, where the same loop with the decode inline reached
+// 2746 (r01_l3_probe.json).
+struct Desc {
+  const char* src;
+  char* dst;
+  uint32_t n;
+  int32_t k;
+};
+constexpr int kQ = 4;  // descriptor batches in flight (32 items each)
+
+template <bool SIGNAL, class Src, bool ACC = false>
+__global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int stages, int lag) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ __align__(8) uint64_t qfull[kQ], qempty[kQ];
+  __shared__ __align__(8) Desc q[kQ][32];
+  __shared__ int32_t qcount[kQ], qlast[kQ];
+  __shared__ char* pend_dst[kMaxStages];
+  __shared__ uint32_t pend_n[kMaxStages];
+  __shared__ int32_t pend_k[kMaxStages];
+  __shared__ __align__(8) Mailbox mail[1];  // (ACC only)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    for (int b = 0; b < kQ; ++b) {
+      mbar_init(&qfull[b], 1);
+      mbar_init(&qempty[b], 1);
+    }
+    if (ACC) mail[0].init();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_enter();
+  const Plan& p = src.locate_signal();  // per-launch fields (piece, signalling)
+  const int64_t n_items = src.total();
+  if (warp == 1) {  // ---------------- decoder
+    int64_t m = 0;
+    for (int64_t b = 0;; ++b) {
+      const int qb = (int)(b % kQ);
+      if (b >= kQ) mbar_wait(&qempty[qb], (uint32_t)(((b / kQ) - 1) & 1));
+      const int64_t gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
+      m += 32;
+      Item it{nullptr, nullptr, 0u, 0u, 0, 0};
+      if (gi < n_items) {
+        int64_t item = gi;
+        const Plan& ip = src.locate(item);
+        it = decode_item(ip, item);
+        if (SIGNAL && it.n == 0 && it.acc) account_chunk(p, it.k, it.acc);  // skipped (bad id): still closes the chunk
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, it.n != 0);
+      if (it.n) q[qb][__popc(mask & ((1u << lane) - 1u))] = Desc{it.src, it.dst, it.n, it.k};
+      const bool last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
+      __syncwarp();
+      if (lane == 0) {
+        qcount[qb] = __popc(mask);
+        qlast[qb] = last ? 1 : 0;
+        mbar_arrive(&qfull[qb]);  // release (CTA scope): the lanes' descriptor writes, ordered by __syncwarp
+      }
+      if (last) return;
+    }
+  }
+  if (ACC && warp == 2) {  // ---------------- accountant
+    if (lane == 0) mail[0].serve(p);
+    return;
+  }
+  if (lane != 0) return;
+  // ---------------- issuer (warp 0, lane 0)
+  const int64_t piece = p.piece;
+  int64_t qb = -1;
+  int pos = 0, cnt = 0;
+  bool qdone = false;
+  int64_t posted = 0;
+  auto refill = [&](int s) {
+    while (pos == cnt) {
+      if (qdone) {
+        pend_n[s] = 0;
+        return;
+      }
+      if (qb >= 0) mbar_arrive(&qempty[qb % kQ]);
+      ++qb;
+      const int qi = (int)(qb % kQ);
+      mbar_wait(&qfull[qi], (uint32_t)((qb / kQ) & 1));
+      cnt = qcount[qi];
+      qdone = qlast[qi] != 0;
+      pos = 0;
+    }
+    const Desc d = q[qb % kQ][pos++];
+    mbar_expect_tx(&full[s], d.n);
+    bulk_load(ring + s * piece, d.src, d.n, &full[s]);
+    pend_dst[s] = d.dst;
+    pend_n[s] = d.n;
+    pend_k[s] = d.k;
+  };
+  for (int s = 0; s < stages; ++s) refill(s);
+
+  constexpr int kDefer = DYNA_BULK_DEFER;
+  int32_t cur_k = -1, park_k = -1;
+  uint32_t cur_acc = 0, park_acc = 0;
+  int since_park = 0;
+  auto flush_park = [&](bool all) {
+    if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    if (ACC) mail[0].post(posted, park_k, park_acc);
+    else account_chunk_release(p, park_k, park_acc);
+    park_k = -1;
+    park_acc = 0;
+  };
+  for (int64_t iter = 0;; ++iter) {
+    const int s = (int)(iter % stages);
+    if (pend_n[s] == 0) break;
+    if (SIGNAL && pend_k[s] != cur_k) {
+      if (park_acc) flush_park(true);
+      park_k = cur_k;
+      park_acc = cur_acc;
+      since_park = 0;
+      cur_k = pend_k[s];
+      cur_acc = 0;
+    }
+    mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
+    bulk_store(pend_dst[s], ring + s * piece, pend_n[s]);
+    bulk_commit();
+    if (SIGNAL) {
+      cur_acc += pend_n[s];
+      if (park_acc && ++since_park == kDefer) flush_park(false);
+    }
+    if (iter >= lag) {
+      if (lag == 2) bulk_wait_read<2>(); else bulk_wait_read<1>();  // store iter-lag done reading smem
+      refill((int)((iter - lag) % stages));
+    }
+  }
+  bulk_wait_all<0>();
+  if (SIGNAL) {
+    if (park_acc) flush_park(true);
+    if (cur_acc) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      if (ACC) {
+        mail[0].post(posted, cur_k, cur_acc);
+      } else {
+        fence_for(p);
+        account_chunk(p, cur_k, cur_acc);
+      }
+    }
+  }
+  if (ACC) mail[0].post(posted, -1, 0);  // the accountant may leave
 }
 
 // ------------------------------------------------------------------ consumer-side chunk wait

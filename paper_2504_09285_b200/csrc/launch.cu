@@ -37,6 +37,9 @@ void preload_kernels() {
       (const void*)k_copy_bulk_ws<false, BatchSource>, (const void*)k_copy_bulk_ws<true, SingleSource, true>,
       (const void*)k_copy_bulk<true, SingleSource, true>,
       (const void*)k_copy_rows<8, false>, (const void*)k_copy_rows<8, true>,
+      (const void*)k_copy_ring<false, SingleSource>, (const void*)k_copy_ring<true, SingleSource>,
+      (const void*)k_copy_ring<true, SingleSource, true>, (const void*)k_copy_ring<false, BatchSource>,
+      (const void*)k_copy_ring<true, BatchSource>,
   };
   for (const void* k : ks) cudaFuncGetAttributes(&a, k);
   // Allow the BULK rings any dynamic shared memory the device offers, once, here: a
@@ -50,6 +53,9 @@ void preload_kernels() {
       (const void*)k_copy_bulk<false, BatchSource>,  (const void*)k_copy_bulk_ws<false, SingleSource>,
       (const void*)k_copy_bulk_ws<true, SingleSource>, (const void*)k_copy_bulk_ws<false, BatchSource>,
       (const void*)k_copy_bulk_ws<true, SingleSource, true>, (const void*)k_copy_bulk<true, SingleSource, true>,
+      (const void*)k_copy_ring<false, SingleSource>, (const void*)k_copy_ring<true, SingleSource>,
+      (const void*)k_copy_ring<true, SingleSource, true>, (const void*)k_copy_ring<false, BatchSource>,
+      (const void*)k_copy_ring<true, BatchSource>,
   };
   for (const void* k : bulk) {
     cudaFuncGetAttributes(&a, k);
@@ -202,6 +208,35 @@ void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cuda
   launch_kernel(k_copy_vec<U, SIG, Src, false>, (unsigned)grid, kVecThreads, 0, st, src, sched);
 }
 
+// Dynamic shared memory a kernel may use: the opt-in maximum minus the kernel's own
+// static shared memory (per kernel: the accountant variants carry a mailbox).
+int smem_avail(const void* kern) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, kern});
+  if (it != cache.end()) return it->second;
+  int optin = 0;
+  cudaFuncAttributes fa{};
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncGetAttributes(&fa, kern);
+  const int v = optin - (int)fa.sharedSizeBytes;
+  cache[{dev, kern}] = v;
+  return v;
+}
+
+// Ring kernel of the BULK engines.  DYNA_KV_RING=0 restores the round-1 kernels (decode on
+// the issuing thread: k_copy_bulk; warp-specialised loader/storer: k_copy_bulk_ws).
+bool ring_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYNA_KV_RING");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <bool SIG, class Src>
 dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, int64_t max_grid, int sms,
                         cudaStream_t st, unsigned long long* sched, bool ws) {
@@ -213,29 +248,36 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
     if (!e) return 1;
     return e[0] == '0' ? 0 : (std::strcmp(e, "all") == 0 ? 2 : 1);
   }();
-  const bool acc = SIG && std::is_same<Src, SingleSource>::value && (ws ? acc_mode >= 1 : acc_mode == 2);
-  auto kern = ws ? (acc ? k_copy_bulk_ws<SIG, Src, true> : k_copy_bulk_ws<SIG, Src>)
-                 : (acc ? k_copy_bulk<SIG, Src, true> : k_copy_bulk<SIG, Src>);
-  const int threads = ws ? (acc ? 96 : 64) : (acc ? 64 : 32);
-  {  // a ring deeper than the shared memory holds is cut to the stages that fit (at least 2)
-    static const int avail = [] {  // (thread-safe static initialisation)
-      int dev = 0, optin = 0;
-      cudaFuncAttributes fa{};
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-      cudaFuncGetAttributes(&fa, (const void*)k_copy_bulk_ws<true, SingleSource>);  // the largest static smem
-      return optin - (int)fa.sharedSizeBytes;
-    }();
-    if ((int64_t)stages * piece > avail) stages = avail / piece;
-    if (stages < 2) return fail(DYNA_EINVAL, "BULK: two %d-B pieces do not fit in shared memory", piece);
-  }
+  static const int lag_env = [] {  // experiment switch: slots refilled `lag` stores late (0 = by depth)
+    const char* e = std::getenv("DYNA_KV_LAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool single = std::is_same<Src, SingleSource>::value;
+  const bool ring = ring_enabled();
+  const bool acc = SIG && single && (ring || ws ? acc_mode >= 1 : acc_mode == 2);
+  void (*kbulk)(const Src, int, unsigned long long*) =
+      ws ? (acc ? k_copy_bulk_ws<SIG, Src, true> : k_copy_bulk_ws<SIG, Src>)
+         : (acc ? k_copy_bulk<SIG, Src, true> : k_copy_bulk<SIG, Src>);
+  void (*kring)(const Src, int, int) = acc ? k_copy_ring<SIG, Src, true> : k_copy_ring<SIG, Src>;
+  const void* kern = ring ? (const void*)kring : (const void*)kbulk;
+  const int threads = ring ? (acc ? 96 : 64) : ws ? (acc ? 96 : 64) : (acc ? 64 : 32);
+  // a ring deeper than the shared memory holds is cut to the stages that fit (at least 2)
+  const int avail = smem_avail(kern);
+  if ((int64_t)stages * piece > avail) stages = avail / piece;
+  if (stages < 2) return fail(DYNA_EINVAL, "BULK: two %d-B pieces do not fit in shared memory", piece);
   const size_t smem = (size_t)stages * piece;
   int occ = 0;  // (the dynamic shared memory limit was raised once in preload_kernels)
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
   if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
   int64_t cap = (int64_t)sms * occ;
   if (max_grid > 0) cap = std::min<int64_t>(cap, max_grid);
-  CUDA_TRY(launch_kernel(kern, (unsigned)balanced_workers(n_items, cap), threads, smem, st, src, stages, sched));
+  const unsigned grid = (unsigned)balanced_workers(n_items, cap);
+  if (ring) {
+    const int lag = lag_env > 0 ? std::min(lag_env, std::max(1, stages - 2)) : (stages >= 4 ? 2 : 1);
+    CUDA_TRY(launch_kernel(kring, grid, threads, smem, st, src, stages, lag));
+  } else {
+    CUDA_TRY(launch_kernel(kbulk, grid, threads, smem, st, src, stages, sched));
+  }
   return DYNA_OK;
 }
 
@@ -337,7 +379,8 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
                        int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
                        int max_ctas, cudaStream_t stream, dyna_kv_xfer* x, int schedule) {
   if (D->imported)
-    return fail(DYNA_ENOTSUP, "STAGED variant into an imported (cross-process) pool is not supported; use FUSED");
+    return fail(DYNA_ENOTSUP, "STAGED variant into an imported (cross-process) pool: use the receiver-steered "
+                              "channel (dyna_kv_push / dyna_kv_place) or FUSED");
   const int64_t row = S->row;
   const bool cross = D->dev != S->dev;
   const int64_t nchunks = (tr.end - tr.begin + c - 1) / c;
@@ -355,12 +398,23 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
   const int64_t sc = std::max<int64_t>(1, std::min<int64_t>(c, kStageSlotBytes / tok_bytes));
   const int64_t slot = sc * tok_bytes;
   char *sbuf = nullptr, *dbuf = nullptr;
-  dyna_status r = channel_staging(S, D, slot, &sbuf, &dbuf);
+  cudaEvent_t prev_done = nullptr;
+  dyna_status r = channel_staging(S, D, slot, &sbuf, &dbuf, &prev_done);
   if (r) return r;
+  // The staging slots belong to the (source, destination) pair: a STAGED migration on another
+  // stream of the same pair must finish with them first (device-side order, no host wait).
+  if (prev_done) CUDA_TRY(cudaStreamWaitEvent(stream, prev_done, 0));
   unsigned long long* counters = nullptr;
+  unsigned long long* flags = nullptr;
   if (signal) {
+    uint64_t epoch = 0;
+    int32_t first = 0;
+    if ((r = flag_reserve(S->desc.instance, D, nchunks, &epoch, &first))) return r;
     if ((r = channel_counters(S, D, D->dev, &counters))) return r;
-    x->epoch = next_epoch(S->desc.instance, D);
+    counters += first;
+    flags = D->inbox + (size_t)S->desc.instance * DYNA_MAX_CHUNKS + first;
+    x->epoch = epoch;
+    x->first_slot = first;
   }
   cudaEvent_t done_src[2] = {nullptr, nullptr};  // K2 of slot i finished (cross-device)
   cudaEvent_t done_dst[2] = {nullptr, nullptr};  // K3 of slot i finished (cross-device)
@@ -380,16 +434,19 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
       char* dslot = dbuf + si * slot;
       if (cross && sub >= 2) CUDA_TRY(cudaStreamWaitEvent(stream, done_dst[si], 0));
       Plan k1 = make_plan(paged(S, sids), linear(sslot), row, sa, sb, l0, lm, sb - sa, S->desc.block_size, piece);
+      k1.err = x->err;
       if ((r = launch_copy(k1, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
       // K2: the sub-chunk slot is [lm][2][n][row] = two contiguous halves
       // (K and V of all layers): a flat plan with one token of `half` bytes.
       Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
+      k2.err = x->err;
       if ((r = launch_copy(k2, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
       Plan k3 = make_plan(linear(dslot), paged(D, dids), row, sa, sb, l0, lm, sb - sa, D->desc.block_size, piece);
       set_chunking(k3, tr.begin, tr.end, c);
+      k3.err = x->err;
       if (signal) {
         k3.counters = counters;
-        k3.flags = D->inbox + (size_t)S->desc.instance * DYNA_MAX_CHUNKS;
+        k3.flags = flags;
         k3.epoch = x->epoch;
       }
       if (cross) {
@@ -412,6 +469,7 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
       put_event(D->dev, done_dst[i]);
     }
   }
+  if (!r) r = channel_staging_done(S, D, stream);
   return r;
 }
 
@@ -421,8 +479,8 @@ dyna_status launch_batch(const BatchSource& src, int64_t n_items, bool sig, int 
 }
 
 void launch_wait_flag(const unsigned long long* flag, unsigned long long epoch, unsigned long long timeout_ns,
-                      cudaStream_t st) {
-  k_wait_flag<<<1, 1, 0, st>>>(flag, epoch, timeout_ns, g_err_word);
+                      cudaStream_t st, unsigned int* err) {
+  k_wait_flag<<<1, 1, 0, st>>>(flag, epoch, timeout_ns, err);
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

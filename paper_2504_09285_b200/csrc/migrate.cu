@@ -10,6 +10,26 @@ using namespace dynakv::rt;
 namespace dynakv {
 namespace rt {
 
+static bool capturing(cudaStream_t stream) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
+}
+
+// A migration handle with its own deferred-error word (the process-wide word when the
+// stream is being captured: a graph's kernels keep writing after the handle is released).
+dyna_status new_xfer(int dev, int sender, cudaStream_t stream, dyna_kv_xfer** out) {
+  auto* x = new dyna_kv_xfer();
+  x->dev = dev;
+  x->sender = sender;
+  x->err = capturing(stream) ? err_word() : err_acquire();
+  if (!x->err) {
+    delete x;
+    return fail(DYNA_ENOMEM, "no deferred-error word");
+  }
+  *out = x;
+  return DYNA_OK;
+}
+
 // Completion event of a migration (none while the stream is being captured
 // into a CUDA graph: the captured work only runs at replay).
 dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream) {
@@ -28,7 +48,8 @@ dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream) {
 dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
   *o = dyna_kv_opts{};
   if (opts) *o = *opts;
-  if ((o->flags & ~(DYNA_MIGRATE_SIGNAL | DYNA_READY_PER_LAYER)) != 0 || o->variant < 0 || o->variant > 2 || o->engine < 0 || o->engine > DYNA_ENGINE_DMA || o->max_ctas < 0 || o->piece_bytes < 0 ||
+  if ((o->flags & ~(DYNA_MIGRATE_SIGNAL | DYNA_READY_PER_LAYER | DYNA_MIGRATE_UNCHECKED)) != 0 || o->variant < 0 ||
+      o->variant > 2 || o->engine < 0 || o->engine > DYNA_ENGINE_BULK_WS || o->max_ctas < 0 || o->piece_bytes < 0 ||
       o->piece_bytes % 16 || o->stages < 0 || o->stages == 1 || o->stages > kMaxStages ||
       (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16) || o->schedule < 0 ||
       o->schedule > DYNA_SCHED_DYNAMIC)
@@ -36,9 +57,15 @@ dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
   return DYNA_OK;
 }
 
-// Geometry, ranges, table presence and (with host ids) ids / aliasing.  *empty: nothing to move.
+// Geometry, ranges and table presence; with host ids, the id range checks and the rows for the
+// alias check of reading R7 (appended to dsp / ssp; the caller runs check_alias over a whole
+// call or batch).  Without DYNA_MIGRATE_UNCHECKED the destination table must carry host ids
+// (and so must the source table when it reads the destination pool), so that aliasing is
+// always checked.  src_spans: 0 = source rows only when source and destination pool coincide,
+// 1 = always (batches: another entry may write this source pool).  *empty: nothing to move.
 dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
-                          int32_t chunk_tokens, bool* empty, bool heads_may_differ) {
+                          int32_t chunk_tokens, bool unchecked, bool* empty, std::vector<Span>& dsp,
+                          std::vector<Span>& ssp, int src_spans, bool heads_may_differ) {
   if (!src.pool || !dst.pool) return fail(DYNA_EINVAL, "NULL pool in a block table");
   const dyna_kv_pool_desc &gs = src.pool->desc, &gd = dst.pool->desc;
   if (gs.num_layers != gd.num_layers || (!heads_may_differ && gs.num_kv_heads != gd.num_kv_heads) ||
@@ -58,7 +85,26 @@ dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& d
                 (long long)tr.end, (long long)(src.len * gs.block_size), (long long)(dst.len * gd.block_size));
   if ((!src.block_ids && !src.host_block_ids) || (!dst.block_ids && !dst.host_block_ids))
     return fail(DYNA_EINVAL, "a block table has neither device nor host block ids");
-  return check_host_tables(src, dst, tr.begin, tr.end);
+  bool same = false;
+  if (pools_overlap(src.pool, dst.pool, &same) && !same)
+    return fail(DYNA_EALIAS, "source and destination pools overlap in memory without being the same pool");
+  if (!unchecked && !dst.host_block_ids)
+    return fail(DYNA_EINVAL, "destination aliasing (reading R7) is checked on the host: give the destination "
+                             "table's host_block_ids, or pass DYNA_MIGRATE_UNCHECKED");
+  if (!unchecked && same && !src.host_block_ids)
+    return fail(DYNA_EINVAL, "source and destination are one pool: give the source table's host_block_ids "
+                             "too, or pass DYNA_MIGRATE_UNCHECKED");
+  dyna_status r;
+  if (dst.host_block_ids && (r = table_spans(dst, tr.begin, tr.end, dsp))) return r;
+  if (src.host_block_ids) {
+    if (src_spans || same) {
+      if ((r = table_spans(src, tr.begin, tr.end, ssp))) return r;
+    } else {
+      std::vector<Span> tmp;  // range check only
+      if ((r = table_spans(src, tr.begin, tr.end, tmp))) return r;
+    }
+  }
+  return DYNA_OK;
 }
 
 // The destination must be addressable from the source (launching) device.
@@ -105,73 +151,6 @@ size_t table_upload_bytes(const dyna_block_table& t, int64_t t1) {
 }  // namespace rt
 }  // namespace dynakv
 
-namespace dynakv {
-namespace rt {
-
-// DMA engine: the copy engines move the contiguous runs (one run = the rows of one
-// (layer, K|V) of a token-grid cell, contiguous on both sides; adjacent runs that stay
-// contiguous on both sides are merged), one cudaMemcpyBatchAsync per chunk in chunk
-// order, marked to overlap with compute.  No SM does any copying; with per-chunk flags a
-// one-thread kernel releases chunk k's flag after chunk k's batch (stream order: the
-// batch's copies are complete before it runs).
-dyna_status run_dma(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* hs, const int32_t* hd, dyna_range tr, int l0,
-                    int lm, int64_t c, unsigned long long* flags, uint64_t epoch, cudaStream_t stream) {
-  const int64_t row = S->row;
-  const int64_t bss = S->desc.block_size, bsd = D->desc.block_size;
-  const int64_t nbs = S->desc.num_blocks, nbd = D->desc.num_blocks;
-  const int64_t g = gcd64(bss, bsd);
-  std::vector<void*> dsts, srcs;
-  std::vector<size_t> sizes;
-  cudaMemcpyAttributes attr{};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  static const int mode = [] {  // experiment switch: 0 batch + overlap hint, 1 batch, 2 one cudaMemcpyAsync per run
-    const char* e = std::getenv("DYNA_KV_DMA_MODE");
-    return e ? std::atoi(e) : 0;
-  }();
-  attr.flags = mode == 0 ? cudaMemcpyFlagPreferOverlapWithCompute : 0;
-  size_t attr_idx = 0;
-  int32_t k = 0;
-  for (int64_t a = tr.begin; a < tr.end; a += c, ++k) {
-    const int64_t b = std::min<int64_t>(a + c, tr.end);
-    dsts.clear();
-    srcs.clear();
-    sizes.clear();
-    for (int l = l0; l < l0 + lm; ++l)
-      for (int kv = 0; kv < 2; ++kv)
-        for (int64_t t = a; t < b;) {
-          const int64_t te = std::min<int64_t>(b, (t / g + 1) * g);
-          char* sp = S->base + ((((int64_t)l * 2 + kv) * nbs + hs[t / bss]) * bss + t % bss) * row;
-          char* dp = D->base + ((((int64_t)l * 2 + kv) * nbd + hd[t / bsd]) * bsd + t % bsd) * row;
-          const size_t n = (size_t)((te - t) * row);
-          if (!sizes.empty() && (char*)srcs.back() + sizes.back() == sp && (char*)dsts.back() + sizes.back() == dp)
-            sizes.back() += n;  // still contiguous on both sides
-          else {
-            srcs.push_back(sp);
-            dsts.push_back(dp);
-            sizes.push_back(n);
-          }
-          t = te;
-        }
-    if (mode == 2 || stream == nullptr) {  // (the batch API refuses the legacy stream)
-      for (size_t i = 0; i < sizes.size(); ++i)
-        CUDA_TRY(cudaMemcpyAsync(dsts[i], srcs[i], sizes[i], cudaMemcpyDeviceToDevice, stream));
-    } else {
-      size_t fail_idx = 0;
-      cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx,
-                                           1, &fail_idx, stream);
-      if (e != cudaSuccess)
-        return fail(DYNA_ECUDA, "cudaMemcpyBatchAsync (%zu copies, failed at %zu): %s", sizes.size(), fail_idx,
-                    cudaGetErrorString(e));
-    }
-    if (flags) launch_release_sys(flags + k, epoch, stream);
-  }
-  if (flags) CUDA_TRY(cudaGetLastError());
-  return DYNA_OK;
-}
-
-}  // namespace rt
-}  // namespace dynakv
-
 extern "C" {
 
 dyna_status dyna_kv_migrate(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
@@ -180,10 +159,11 @@ dyna_status dyna_kv_migrate(dyna_block_table src, dyna_block_table dst, dyna_ran
 }
 
 // A chunk stream's call: one chunk of a logical migration that started at mig_t0; its flag
-// goes to slot (t0 - mig_t0) / c of the stream's epoch (dyna_kv_stream_*).
+// goes to slot first_slot + (t0 - mig_t0) / c of the stream's reserved slots (nslots of them).
 struct ChunkCtx {
   int64_t mig_t0;
   uint64_t epoch;
+  int32_t first_slot, nslots;
 };
 static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
                                 int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
@@ -203,6 +183,33 @@ dyna_status dyna_kv_migrate_on_ready(dyna_block_table src, dyna_block_table dst,
   return migrate_impl(src, dst, tr, lr, chunk_tokens, stream_, opts, board, epoch, out);
 }
 
+static dyna_kv_xfer* empty_xfer(const dyna_kv_pool* S) {
+  auto* x = new dyna_kv_xfer();
+  x->dev = S->dev;
+  x->sender = S->desc.instance;
+  x->empty = true;
+  return x;
+}
+
+// Host-resident tables (block_ids == NULL): upload the entries the kernels may read.
+static dyna_status upload_tables(RingLease& lease, const dyna_block_table& src, const dyna_block_table& dst,
+                                 int64_t t1, cudaStream_t stream, const int32_t** sids, const int32_t** dids) {
+  *sids = src.block_ids;
+  *dids = dst.block_ids;
+  if (*sids && *dids) return DYNA_OK;
+  const size_t sb = *sids ? 0 : (table_upload_bytes(src, t1) + 15) & ~size_t(15);
+  const size_t db = *dids ? 0 : table_upload_bytes(dst, t1);
+  char *base = nullptr, *h = nullptr;
+  dyna_status r = lease.reserve(sb + db, &base, &h, stream);
+  if (r) return r;
+  if (!*sids) std::memcpy(h, src.host_block_ids, table_upload_bytes(src, t1));
+  if (!*dids) std::memcpy(h + sb, dst.host_block_ids, db);
+  if ((r = lease.copy(stream))) return r;
+  if (!*sids) *sids = reinterpret_cast<const int32_t*>(base);
+  if (!*dids) *dids = reinterpret_cast<const int32_t*>(base + sb);
+  return DYNA_OK;
+}
+
 static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
                                 int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
                                 dyna_kv_ready* board, uint64_t ready_epoch, dyna_kv_xfer_t* out,
@@ -213,12 +220,14 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   dyna_status r = check_opts(opts, &o);
   if (r) return r;
   if (ctx) {  // chunk streams: one fused launch per chunk, flags in the stream's slots
-    if (o.variant == DYNA_VARIANT_STAGED || o.engine == DYNA_ENGINE_DMA)
-      return fail(DYNA_ENOTSUP, "chunk stream: FUSED variant, SM engines only");
+    if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "chunk stream: FUSED variant only");
     o.variant = DYNA_VARIANT_FUSED;
   }
   bool empty = false;
-  if ((r = validate_pair(src, dst, tr, lr, chunk_tokens, &empty))) return r;
+  std::vector<Span> dsp, ssp;
+  const bool unchecked = (o.flags & DYNA_MIGRATE_UNCHECKED) != 0;
+  if ((r = validate_pair(src, dst, tr, lr, chunk_tokens, unchecked, &empty, dsp, ssp, 0, false))) return r;
+  if (!empty && (r = check_alias(dsp, ssp))) return r;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   dyna_kv_pool* S = src.pool;
   dyna_kv_pool* D = dst.pool;
@@ -226,10 +235,11 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int64_t ntok = tr.end - tr.begin;
   const int64_t nchunks = empty ? 0 : (ntok + chunk_tokens - 1) / chunk_tokens;
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
-  const int64_t slot0 = ctx ? (tr.begin - ctx->mig_t0) / chunk_tokens : 0;
-  if (signal && slot0 + nchunks > DYNA_MAX_CHUNKS)
-    return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)(slot0 + nchunks),
+  if (signal && nchunks > DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks,
                 DYNA_MAX_CHUNKS);
+  if (ctx && signal && (tr.begin - ctx->mig_t0) / chunk_tokens + nchunks > ctx->nslots)
+    return fail(DYNA_ERANGE, "chunk stream: chunk beyond the %d flag slots reserved at open", ctx->nslots);
   if (board) {
     if (board->dev != src.pool->dev) return fail(DYNA_EINVAL, "ready board must live on the source device");
     const int64_t nslots = nchunks * ((o.flags & DYNA_READY_PER_LAYER) ? (lr.end - lr.begin) : 1);
@@ -241,17 +251,8 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   } else if (o.flags & DYNA_READY_PER_LAYER) {
     return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board (dyna_kv_migrate_on_ready)");
   }
-  if (o.engine == DYNA_ENGINE_DMA) {
-    if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "DMA engine: FUSED variant only");
-    if (!src.host_block_ids || !dst.host_block_ids)
-      return fail(DYNA_ENOTSUP, "DMA engine: the copy list is built on the host from host_block_ids (both tables)");
-  }
   if (empty) {  // s = 0 (or no layers) -> nothing to ship, nothing enqueued
-    auto* x = new dyna_kv_xfer();
-    x->dev = S->dev;
-    x->sender = gs.instance;
-    x->empty = true;
-    *out = x;
+    *out = empty_xfer(S);
     return DYNA_OK;
   }
   if ((r = check_reach(S, D))) return r;
@@ -262,12 +263,10 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int64_t c = chunk_tokens;
   const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
   Choice ch = choose(o, row, peer_dst, ntok, std::min<int64_t>(gcd64(gs.block_size, gd.block_size), c) * row);
-  if (signal && !o.engine && ch.engine != DYNA_ENGINE_VEC && nchunks > 1) {
-    // measured (bench.py e2e, per-chunk flags on): BULK's release-add at every chunk switch
-    // stalls its single issuing thread (2540 GB/s), VEC's per-warp fences do not (2720); the
-    // warp-specialised BULK_WS with an accountant thread beats both (e2e 2880 -> 2923 GB/s vs
-    // VEC, profiles/r01_ab_signal_ws.log).  With ONE chunk per call (the paper's per-chunk
-    // push) plain BULK keeps the lead (182.8 vs 186.8 us per 512 MiB, sig_probe with C = S).
+  if (signal && !o.engine && ch.engine != DYNA_ENGINE_VEC && nchunks > 1 && !ring_enabled()) {
+    // round-1 kernels (DYNA_KV_RING=0), measured: BULK's release-add at every chunk switch stalls
+    // its single issuing thread; BULK_WS with an accountant thread beats VEC and BULK
+    // (profiles/r01_ab_signal_ws.log).  The ring kernel counts through an accountant itself.
     static const bool ws = [] {  // DYNA_KV_SIGNAL_WS=0: VEC instead of BULK_WS
       const char* e = std::getenv("DYNA_KV_SIGNAL_WS");
       return !(e && e[0] == '0');
@@ -289,27 +288,14 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int variant = ch.variant, engine = ch.engine, piece = ch.piece, stages = ch.stages, unroll = ch.unroll;
 
   DeviceGuard guard(S->dev);
-  // Host-resident tables (block_ids == NULL): upload the entries the kernels may read.
+  if (variant == DYNA_VARIANT_STAGED && D->dev != S->dev && !dst.block_ids)
+    return fail(DYNA_ENOTSUP, "cross-device STAGED needs device block_ids for the destination");
   RingLease lease(S->dev);
-  const int32_t* sids = src.block_ids;
-  const int32_t* dids = dst.block_ids;
-  if ((!sids || !dids) && engine != DYNA_ENGINE_DMA) {  // (DMA reads the host ids itself)
-    if (variant == DYNA_VARIANT_STAGED && D->dev != S->dev)
-      return fail(DYNA_ENOTSUP, "cross-device STAGED needs device block_ids for the destination");
-    const size_t sb = sids ? 0 : (table_upload_bytes(src, tr.end) + 15) & ~size_t(15);
-    const size_t db = dids ? 0 : table_upload_bytes(dst, tr.end);
-    char *base = nullptr, *h = nullptr;
-    if ((r = lease.reserve(sb + db, &base, &h, stream))) return r;
-    if (!sids) std::memcpy(h, src.host_block_ids, table_upload_bytes(src, tr.end));
-    if (!dids) std::memcpy(h + sb, dst.host_block_ids, db);
-    if ((r = lease.copy(stream))) return r;
-    if (!sids) sids = reinterpret_cast<const int32_t*>(base);
-    if (!dids) dids = reinterpret_cast<const int32_t*>(base + sb);
-  }
+  const int32_t *sids = nullptr, *dids = nullptr;
+  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids))) return r;
 
-  auto* x = new dyna_kv_xfer();
-  x->dev = S->dev;
-  x->sender = gs.instance;
+  dyna_kv_xfer* x = nullptr;
+  if ((r = new_xfer(S->dev, gs.instance, stream, &x))) return r;
   x->nchunks = (int32_t)nchunks;
   x->variant = variant;
   x->engine = engine;
@@ -317,26 +303,30 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   x->stages = engine != DYNA_ENGINE_VEC ? stages : 0;
   x->unroll = engine == DYNA_ENGINE_VEC ? unroll : 0;
   const uint64_t launches0 = g_launches.load();
-  if (engine == DYNA_ENGINE_DMA) {
-    unsigned long long* flags = nullptr;
-    uint64_t epoch = 0;
-    if (signal) {
-      flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
-      epoch = x->epoch = next_epoch(gs.instance, D);
-    }
-    r = run_dma(S, D, src.host_block_ids, dst.host_block_ids, tr, l0, lm, c, flags, epoch, stream);
-  } else if (variant == DYNA_VARIANT_FUSED) {
+  if (variant == DYNA_VARIANT_FUSED) {
     // K4 / K4-local: source rows -> destination rows, one launch for all chunks.
     const int64_t g = gcd64(gs.block_size, gd.block_size);
     Plan p = make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
+    p.err = x->err;
     if (ctx) set_chunking(p, ctx->mig_t0, tr.end, c);
     if (signal) {
+      uint64_t epoch = 0;
+      int32_t first = 0;
+      if (ctx) {
+        epoch = ctx->epoch;
+        first = ctx->first_slot;
+      } else if ((r = flag_reserve(gs.instance, D, nchunks, &epoch, &first))) {
+        delete x;
+        return r;
+      }
       if ((r = channel_counters(S, D, S->dev, &p.counters))) {
         delete x;
         return r;
       }
-      p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
-      p.epoch = x->epoch = ctx ? ctx->epoch : next_epoch(gs.instance, D);
+      p.counters += first;
+      p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS + first;
+      p.epoch = x->epoch = epoch;
+      x->first_slot = first;
       p.sys_fence = peer_dst;
     }
     if (board) {
@@ -379,16 +369,14 @@ struct dyna_kv_chunkstream {
   cudaStream_t stream = nullptr;
   dyna_kv_opts opts{};
   uint64_t epoch = 0;
-  int32_t sender = 0;
+  int32_t sender = 0, first_slot = 0, nslots = 0;
   bool closed = false;
   std::vector<dyna_kv_xfer_t> pushed;
-  dyna_status first_error = DYNA_OK;
-  std::string error_msg;
 };
 extern "C" {
 
 static dyna_status stream_push(dyna_kv_chunkstream* s, int64_t a, int64_t b) {
-  ChunkCtx ctx{s->begin, s->epoch};
+  ChunkCtx ctx{s->begin, s->epoch, s->first_slot, s->nslots};
   dyna_kv_xfer_t x = nullptr;
   dyna_status r = migrate_impl(s->src, s->dst, dyna_range{a, b}, s->layers, s->c,
                                reinterpret_cast<struct CUstream_st*>(s->stream), &s->opts, nullptr, 0, &x, &ctx);
@@ -408,7 +396,7 @@ dyna_status dyna_kv_chunkstream_open(dyna_block_table src, dyna_block_table dst,
   dyna_kv_opts o{};
   dyna_status r = check_opts(opts, &o);
   if (r) return r;
-  if (o.variant == DYNA_VARIANT_STAGED || o.engine == DYNA_ENGINE_DMA || (o.flags & DYNA_READY_PER_LAYER))
+  if (o.variant == DYNA_VARIANT_STAGED || (o.flags & DYNA_READY_PER_LAYER))
     return fail(DYNA_ENOTSUP, "chunk stream: FUSED variant, SM engines, no ready board");
   auto* s = new dyna_kv_chunkstream();
   s->src = src;
@@ -419,7 +407,15 @@ dyna_status dyna_kv_chunkstream_open(dyna_block_table src, dyna_block_table dst,
   s->stream = reinterpret_cast<cudaStream_t>(stream);
   s->opts = o;
   s->sender = src.pool->desc.instance;
-  if (o.flags & DYNA_MIGRATE_SIGNAL) s->epoch = next_epoch(s->sender, dst.pool);
+  if (o.flags & DYNA_MIGRATE_SIGNAL) {
+    // the destination table bounds the tokens the stream can ever push: reserve that many slots
+    const int64_t cap_tok = std::max<int64_t>(0, dst.len * dst.pool->desc.block_size - begin);
+    s->nslots = (int32_t)std::min<int64_t>(DYNA_MAX_CHUNKS, (cap_tok + chunk_tokens - 1) / chunk_tokens);
+    if ((r = flag_reserve(s->sender, dst.pool, s->nslots, &s->epoch, &s->first_slot))) {
+      delete s;
+      return r;
+    }
+  }
   *out = s;
   return DYNA_OK;
 }
@@ -453,11 +449,12 @@ dyna_status dyna_kv_chunkstream_close(dyna_kv_chunkstream_t s, int32_t* pushed) 
   return DYNA_OK;
 }
 
-dyna_status dyna_kv_chunkstream_info(dyna_kv_chunkstream_t s, uint64_t* epoch, int32_t* sender, int64_t* produced_end,
-                                int64_t* pushed_end, int32_t* num_pushed) {
+dyna_status dyna_kv_chunkstream_info(dyna_kv_chunkstream_t s, uint64_t* epoch, int32_t* sender, int32_t* first_slot,
+                                     int64_t* produced_end, int64_t* pushed_end, int32_t* num_pushed) {
   if (!s) return fail(DYNA_EINVAL, "NULL stream");
   if (epoch) *epoch = s->epoch;
   if (sender) *sender = s->sender;
+  if (first_slot) *first_slot = s->first_slot;
   if (produced_end) *produced_end = s->produced_end;
   if (pushed_end) *pushed_end = s->pushed_end;
   if (num_pushed) *num_pushed = (int32_t)s->pushed.size();
@@ -490,7 +487,11 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
   if (r) return r;
   if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
   bool empty = false;
-  if ((r = validate_pair(src, dst, tr, lr, chunk_tokens, &empty, true))) return r;
+  std::vector<Span> dsp, ssp;
+  if ((r = validate_pair(src, dst, tr, lr, chunk_tokens, (o.flags & DYNA_MIGRATE_UNCHECKED) != 0, &empty, dsp, ssp,
+                         0, true)))
+    return r;
+  if (!empty && (r = check_alias(dsp, ssp))) return r;  // (rows, whatever their heads: conservative)
   dyna_kv_pool* S = src.pool;
   dyna_kv_pool* D = dst.pool;
   const dyna_kv_pool_desc &gs = S->desc, &gd = D->desc;
@@ -513,11 +514,7 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
   if (signal && nchunks > DYNA_MAX_CHUNKS)
     return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks, DYNA_MAX_CHUNKS);
   if (nchunks == 0) {
-    auto* x = new dyna_kv_xfer();
-    x->dev = S->dev;
-    x->sender = gs.instance;
-    x->empty = true;
-    *out = x;
+    *out = empty_xfer(S);
     return DYNA_OK;
   }
   if ((r = check_reach(S, D))) return r;
@@ -528,22 +525,10 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
 
   DeviceGuard guard(S->dev);
   RingLease lease(S->dev);
-  const int32_t* sids = src.block_ids;
-  const int32_t* dids = dst.block_ids;
-  if (!sids || !dids) {
-    const size_t sb = sids ? 0 : (table_upload_bytes(src, tr.end) + 15) & ~size_t(15);
-    const size_t db = dids ? 0 : table_upload_bytes(dst, tr.end);
-    char *base = nullptr, *h = nullptr;
-    if ((r = lease.reserve(sb + db, &base, &h, stream))) return r;
-    if (!sids) std::memcpy(h, src.host_block_ids, table_upload_bytes(src, tr.end));
-    if (!dids) std::memcpy(h + sb, dst.host_block_ids, db);
-    if ((r = lease.copy(stream))) return r;
-    if (!sids) sids = reinterpret_cast<const int32_t*>(base);
-    if (!dids) dids = reinterpret_cast<const int32_t*>(base + sb);
-  }
-  auto* x = new dyna_kv_xfer();
-  x->dev = S->dev;
-  x->sender = gs.instance;
+  const int32_t *sids = nullptr, *dids = nullptr;
+  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids))) return r;
+  dyna_kv_xfer* x = nullptr;
+  if ((r = new_xfer(S->dev, gs.instance, stream, &x))) return r;
   x->nchunks = (int32_t)nchunks;
   x->variant = DYNA_VARIANT_FUSED;
   x->engine = DYNA_ENGINE_VEC;
@@ -554,13 +539,19 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
   Plan p = make_plan_sliced(paged(S, sids), paged(D, dids), nh * head_bytes, S->row, src_heads.begin * head_bytes,
                             D->row, (int64_t)dst_head_begin * head_bytes, tr.begin, tr.end, l0, lm, chunk_tokens,
                             gcd64(gs.block_size, gd.block_size), piece);
+  p.err = x->err;
   if (signal) {
-    if ((r = channel_counters(S, D, S->dev, &p.counters))) {
+    uint64_t epoch = 0;
+    int32_t first = 0;
+    if ((r = flag_reserve(gs.instance, D, nchunks, &epoch, &first)) ||
+        (r = channel_counters(S, D, S->dev, &p.counters))) {
       delete x;
       return r;
     }
-    p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS;
-    p.epoch = x->epoch = next_epoch(gs.instance, D);
+    p.counters += first;
+    p.flags = D->inbox + (size_t)gs.instance * DYNA_MAX_CHUNKS + first;
+    p.epoch = x->epoch = epoch;
+    x->first_slot = first;
     p.sys_fence = peer_dst;
   }
   r = launch_rows(p, o.max_ctas, S->dev, stream);
@@ -589,21 +580,34 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "batch: FUSED variant only");
   if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
+  const bool unchecked = (o.flags & DYNA_MIGRATE_UNCHECKED) != 0;
   if (signal && o.engine && o.engine != DYNA_ENGINE_VEC)
     return fail(DYNA_ENOTSUP, "batch with per-chunk flags: VEC engine only");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  // Reading R7 across entries: one entry's source rows may be another entry's destination rows.
+  std::vector<uint64_t> dst_uids;
+  for (int32_t i = 0; i < n; ++i)
+    if (migs[i].dst.pool) dst_uids.push_back(migs[i].dst.pool->uid);
+  std::sort(dst_uids.begin(), dst_uids.end());
+  std::vector<Span> dsp, ssp;
   std::vector<int32_t> live;
   int64_t total_tok = 0;
   dyna_kv_pool* S0 = nullptr;
   int peer = 0;
   for (int32_t i = 0; i < n; ++i) {
     bool empty = false;
-    if ((r = validate_pair(migs[i].src, migs[i].dst, migs[i].token_range, lr, chunk_tokens, &empty))) {
+    const dyna_block_table &ms = migs[i].src, &md = migs[i].dst;
+    const bool src_is_dst = ms.pool && std::binary_search(dst_uids.begin(), dst_uids.end(), ms.pool->uid);
+    if ((r = validate_pair(ms, md, migs[i].token_range, lr, chunk_tokens, unchecked, &empty, dsp, ssp,
+                           src_is_dst ? 1 : 0, false))) {
       g_err = "migration " + std::to_string(i) + ": " + g_err;
       return r;
     }
     if (empty) continue;
-    dyna_kv_pool *S = migs[i].src.pool, *D = migs[i].dst.pool;
+    if (src_is_dst && !unchecked && !ms.host_block_ids)
+      return fail(DYNA_EINVAL, "migration %d: its source pool is written by this batch: give the source table's "
+                               "host_block_ids, or pass DYNA_MIGRATE_UNCHECKED", i);
+    dyna_kv_pool *S = ms.pool, *D = md.pool;
     if (!S0) S0 = S;
     if (S->dev != S0->dev || S->row != S0->row)
       return fail(DYNA_EINVAL, "batch: all sources on one device with one row size");
@@ -612,58 +616,48 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     total_tok += migs[i].token_range.end - migs[i].token_range.begin;
     live.push_back(i);
   }
-  auto* x = new dyna_kv_xfer();
+  if ((r = check_alias(dsp, ssp))) return r;
   if (live.empty()) {
+    auto* x = new dyna_kv_xfer();
     x->empty = true;
     if (signal) x->batch.assign(n, dyna_kv_xfer::BatchEntry{});  // every entry: 0 chunks
     *out = x;
     return DYNA_OK;
   }
-  if (!err_word()) {
-    delete x;
-    return fail(DYNA_ECUDA, "no error word");
-  }
-  x->dev = S0->dev;
-  x->sender = S0->desc.instance;
+  if (!err_word()) return fail(DYNA_ECUDA, "no error word");
   int64_t run_min = std::numeric_limits<int64_t>::max();  // shortest contiguous run in the batch
   for (int32_t i : live)
     run_min = std::min<int64_t>(run_min, std::min<int64_t>(gcd64(migs[i].src.pool->desc.block_size,
                                                                   migs[i].dst.pool->desc.block_size),
                                                             chunk_tokens) * S0->row);
   Choice ch = choose(o, S0->row, peer, total_tok, run_min);
-  if (ch.engine == DYNA_ENGINE_DMA) {
-    delete x;
-    return fail(DYNA_ENOTSUP, "batch: no DMA engine");
-  }
-  if (!o.engine && ch.engine != DYNA_ENGINE_VEC) {
-    // measured (scripts/batch_probe.py): with many plans the BULK engine's single issuing
-    // thread is latency-bound on per-item plan lookups; the warp-parallel VEC engine is not
+  if (signal || (!o.engine && ch.engine != DYNA_ENGINE_VEC && !ring_enabled())) {
+    // per-chunk accounting is per plan: VEC.  Round-1 BULK kernels decode (and look plans up)
+    // on the issuing thread, latency-bound with many plans (scripts/batch_probe.py); the ring
+    // kernel's decoder warp does the lookups (configs[2] batch: 3263 vs VEC 2966 GB/s,
+    // profiles/r02_engine_ab_ring.json).
     ch.engine = DYNA_ENGINE_VEC;
-    ch.unroll = kVecU;
+    ch.unroll = o.unroll ? o.unroll : kVecU;
     if (!o.piece_bytes) ch.piece = kVecPiece;
   }
+  DeviceGuard guard(S0->dev);
+  dyna_kv_xfer* x = nullptr;
+  if ((r = new_xfer(S0->dev, S0->desc.instance, stream, &x))) return r;
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
-  if (signal) {  // slot ranges: disjoint per (sender instance, destination pool) inside the batch
+  if (signal) {  // each entry: its own epoch and slot range of its (sender, destination pool)
     x->batch.assign(n, dyna_kv_xfer::BatchEntry{});
-    std::map<std::pair<int, const dyna_kv_pool*>, int64_t> next_slot;
     for (int32_t i : live) {
       dyna_kv_pool *S = migs[i].src.pool, *D = migs[i].dst.pool;
       const int64_t nck = (migs[i].token_range.end - migs[i].token_range.begin + chunk_tokens - 1) / chunk_tokens;
-      int64_t& slot = next_slot[{S->desc.instance, D}];
-      if (slot + nck > DYNA_MAX_CHUNKS) {
-        delete x;
-        return fail(DYNA_ERANGE, "batch: more than DYNA_MAX_CHUNKS (%d) signalled chunks from sender %d into one "
-                                 "destination pool", DYNA_MAX_CHUNKS, S->desc.instance);
-      }
       dyna_kv_xfer::BatchEntry& be = x->batch[i];
-      be.first_slot = (int32_t)slot;
+      if ((r = flag_reserve(S->desc.instance, D, nck, &be.epoch, &be.first_slot))) {
+        delete x;
+        return r;
+      }
       be.nchunks = (int32_t)nck;
       be.sender = S->desc.instance;
-      be.epoch = next_epoch(S->desc.instance, D);
-      slot += nck;
     }
   }
-  DeviceGuard guard(S0->dev);
   // One upload: [plans][item bases][host-resident tables].
   const size_t m = live.size();
   const size_t plans_b = ((m * sizeof(Plan)) + 15) & ~size_t(15);
@@ -698,6 +692,7 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     const int64_t g = gcd64(S->desc.block_size, D->desc.block_size);
     plans[k] = make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end, l0, lm,
                          chunk_tokens, g, ch.piece);
+    plans[k].err = x->err;
     if (signal) {  // entry k's chunk j: counter / inbox slot first_slot + j of its (sender, destination)
       dyna_kv_xfer::BatchEntry& be = x->batch[live[k]];
       unsigned long long* ctr = nullptr;
@@ -735,13 +730,6 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   x->stages = ch.engine != DYNA_ENGINE_VEC ? ch.stages : 0;
   x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
   x->launches = 1;
-  if (signal) {  // per-chunk accounting is per plan: the VEC engine only
-    ch.engine = DYNA_ENGINE_VEC;
-    x->engine = ch.engine;
-    x->stages = 0;
-    if (!ch.unroll) ch.unroll = kVecU;
-    x->unroll = ch.unroll;
-  }
   r = launch_batch(bsrc, total_items, signal, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev, stream,
                    o.schedule);
   if (!r) r = lease.finish(stream);
@@ -773,7 +761,7 @@ dyna_status dyna_kv_wait(dyna_kv_xfer_t x) {
     cudaError_t e = cudaEventSynchronize(x->ev);
     if (e != cudaSuccess) r = fail(DYNA_ECUDA, "migration failed: %s", cudaGetErrorString(e));
     put_event(x->dev, x->ev);
-    if (!r) r = take_device_error();
+    if (!r) r = err_take(x->err);  // this migration's own word
     if (!r && x->board && x->board->cancel_epoch.load() >= x->ready_epoch)
       r = fail(DYNA_ECANCELED, "migration cancelled (dyna_kv_ready_cancel)");
   }
@@ -789,8 +777,10 @@ dyna_status dyna_kv_stream_wait(dyna_kv_xfer_t x, struct CUstream_st* stream) {
   return DYNA_OK;
 }
 
-dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t x, uint64_t* epoch, int32_t* num_chunks, int32_t* sender) {
+dyna_status dyna_kv_xfer_info(dyna_kv_xfer_t x, uint64_t* epoch, int32_t* num_chunks, int32_t* sender,
+                              int32_t* first_slot) {
   if (!x) return fail(DYNA_EINVAL, "NULL xfer");
+  if (first_slot) *first_slot = x->first_slot;
   if (epoch) *epoch = x->epoch;
   if (num_chunks) *num_chunks = x->nchunks;
   if (sender) *sender = x->sender;
@@ -831,7 +821,7 @@ dyna_status dyna_kv_stream_wait_chunk(dyna_kv_pool_t dst, int32_t sender, int32_
   if (!err_word()) return fail(DYNA_ECUDA, "no error word");
   DeviceGuard g(dst->dev);
   launch_wait_flag(dst->inbox + (size_t)sender * DYNA_MAX_CHUNKS + chunk, epoch, timeout_ns,
-                   reinterpret_cast<cudaStream_t>(stream));
+                   reinterpret_cast<cudaStream_t>(stream), g_err_word);
   CUDA_TRY(cudaGetLastError());
   return DYNA_OK;
 }

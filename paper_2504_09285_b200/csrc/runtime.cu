@@ -2,6 +2,9 @@
 // access, the calibration table, signalling channels' counters and
 // staging, and the test-input fill.  Paper mapping: PAPER.md §3.1 P:352 (instances
 // exchange the required KV blocks).
+#include <chrono>
+#include <random>
+
 #include "runtime.cuh"
 
 using namespace dynakv;
@@ -39,13 +42,42 @@ unsigned int* err_word() {
   return g_err_word;
 }
 
-dyna_status take_device_error() {
-  unsigned int* w = err_word();
+dyna_status err_take(unsigned int* w) {
   if (!w) return DYNA_OK;
   const unsigned int bits = __atomic_exchange_n(w, 0u, __ATOMIC_ACQ_REL);
   if (bits & ERR_BAD_BLOCK) return fail(DYNA_ERANGE, "device-side check: block id outside [0, num_blocks)");
   if (bits & ERR_TIMEOUT) return fail(DYNA_ETIMEDOUT, "device-side chunk wait timed out");
   return DYNA_OK;
+}
+
+dyna_status take_device_error() { return err_take(err_word()); }
+
+// Per-migration words: slabs of mapped pinned host memory, never freed, words recycled.
+static std::mutex g_errpool_mu;
+static std::vector<unsigned int*> g_err_free;
+constexpr int kErrSlabWords = 4096;
+
+unsigned int* err_acquire() {
+  std::lock_guard<std::mutex> lk(g_errpool_mu);
+  if (g_err_free.empty()) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, sizeof(unsigned int) * kErrSlabWords, cudaHostAllocMapped | cudaHostAllocPortable) !=
+        cudaSuccess)
+      return nullptr;
+    std::memset(p, 0, sizeof(unsigned int) * kErrSlabWords);
+    unsigned int* w = static_cast<unsigned int*>(p);
+    for (int i = kErrSlabWords - 1; i >= 0; --i) g_err_free.push_back(w + i);
+  }
+  unsigned int* w = g_err_free.back();
+  g_err_free.pop_back();
+  __atomic_store_n(w, 0u, __ATOMIC_RELEASE);
+  return w;
+}
+
+void err_release(unsigned int* w) {
+  if (!w) return;
+  std::lock_guard<std::mutex> lk(g_errpool_mu);
+  g_err_free.push_back(w);
 }
 
 std::map<int, DevInfo> g_dev;
@@ -147,49 +179,51 @@ Side linear(char* base) {
   return s;
 }
 
-// Synchronous checks that need the host copies of the tables.
-dyna_status check_host_tables(const dyna_block_table& src, const dyna_block_table& dst, int64_t t0, int64_t t1) {
-  struct Span {
-    int32_t id;
-    int64_t lo, hi;  // slot range [lo, hi) inside block id
-  };
-  auto spans = [&](const dyna_block_table& t, std::vector<Span>& out) -> dyna_status {
-    const int64_t bs = t.pool->desc.block_size, nb = t.pool->desc.num_blocks;
-    for (int64_t j = t0 / bs; j <= (t1 - 1) / bs; ++j) {
-      const int32_t id = t.host_block_ids[j];
-      if (id < 0 || id >= nb) return fail(DYNA_ERANGE, "block_ids[%lld] = %d outside [0, %lld)", (long long)j, id, (long long)nb);
-      const int64_t lo = std::max(t0, j * bs) - j * bs, hi = std::min(t1, (j + 1) * bs) - j * bs;
-      out.push_back({id, lo, hi});
-    }
-    return DYNA_OK;
-  };
-  std::vector<Span> s, d;
-  if (src.host_block_ids) {
-    dyna_status r = spans(src, s);
-    if (r) return r;
-  }
-  if (dst.host_block_ids) {
-    dyna_status r = spans(dst, d);
-    if (r) return r;
-    auto by_id = [](const Span& a, const Span& b) { return a.id != b.id ? a.id < b.id : a.lo < b.lo; };
-    std::vector<Span> ds = d;
-    std::sort(ds.begin(), ds.end(), by_id);
-    for (size_t i = 1; i < ds.size(); ++i)
-      if (ds[i].id == ds[i - 1].id && ds[i].lo < ds[i - 1].hi)
-        return fail(DYNA_EALIAS, "destination block %d is reached twice by the token range", ds[i].id);
-    if (src.host_block_ids && src.pool->base == dst.pool->base) {
-      std::vector<Span> ss = s;
-      std::sort(ss.begin(), ss.end(), by_id);
-      size_t i = 0;
-      for (const Span& x : ds) {
-        while (i < ss.size() && ss[i].id < x.id) ++i;
-        for (size_t k = i; k < ss.size() && ss[k].id == x.id; ++k)
-          if (ss[k].lo < x.hi && x.lo < ss[k].hi)
-            return fail(DYNA_EALIAS, "same pool: destination rows of block %d overlap source rows", x.id);
-      }
-    }
+// Rows a table reaches for tokens [t0, t1), as (pool uid, block id, slot range) spans; ids
+// are range-checked on the way (DYNA_ERANGE).  Needs the host copy of the ids.
+dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out) {
+  const int64_t bs = t.pool->desc.block_size, nb = t.pool->desc.num_blocks;
+  for (int64_t j = t0 / bs; j <= (t1 - 1) / bs; ++j) {
+    const int32_t id = t.host_block_ids[j];
+    if (id < 0 || id >= nb) return fail(DYNA_ERANGE, "block_ids[%lld] = %d outside [0, %lld)", (long long)j, id, (long long)nb);
+    const int64_t lo = std::max(t0, j * bs) - j * bs, hi = std::min(t1, (j + 1) * bs) - j * bs;
+    out.push_back({t.pool->uid, id, lo, hi});
   }
   return DYNA_OK;
+}
+
+// Reading R7: destination rows must be distinct (no two writes of one row) and, where a
+// source pool is the destination pool, disjoint from the source rows being read.  Source
+// rows may repeat (shared prefix blocks).  All spans of one call or one batch together.
+dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src) {
+  auto by = [](const Span& a, const Span& b) {
+    return a.uid != b.uid ? a.uid < b.uid : a.id != b.id ? a.id < b.id : a.lo < b.lo;
+  };
+  std::sort(dst.begin(), dst.end(), by);
+  for (size_t i = 1; i < dst.size(); ++i)
+    if (dst[i].uid == dst[i - 1].uid && dst[i].id == dst[i - 1].id && dst[i].lo < dst[i - 1].hi)
+      return fail(DYNA_EALIAS, "destination block %d is reached twice", dst[i].id);
+  if (src.empty()) return DYNA_OK;
+  std::sort(src.begin(), src.end(), by);
+  size_t k = 0;
+  for (const Span& x : dst) {  // both sorted: one merge pass
+    while (k < src.size() && by(src[k], Span{x.uid, x.id, 0, 0})) ++k;
+    for (size_t m = k; m < src.size() && src[m].uid == x.uid && src[m].id == x.id; ++m)
+      if (src[m].lo < x.hi && x.lo < src[m].hi)
+        return fail(DYNA_EALIAS, "destination rows of block %d overlap source rows of the same pool", x.id);
+  }
+  return DYNA_OK;
+}
+
+// Two pool objects over the same memory: one uid (an imported mapping carries its owner's), or
+// local pools whose byte ranges overlap.  *same: identical layout (rows can be compared by id).
+bool pools_overlap(const dyna_kv_pool* a, const dyna_kv_pool* b, bool* same) {
+  *same = a->uid == b->uid || a->base == b->base;
+  if (*same) return true;
+  if (a->imported || b->imported || a->dev != b->dev) return false;
+  const char *a0 = a->base, *a1 = a0 + dyna_kv_pool_bytes(&a->desc);
+  const char *b0 = b->base, *b1 = b0 + dyna_kv_pool_bytes(&b->desc);
+  return a0 < b1 && b0 < a1;
 }
 
 dyna_status ensure_peer(int dev, int peer) {
@@ -207,13 +241,42 @@ dyna_status ensure_peer(int dev, int peer) {
   return DYNA_OK;
 }
 
-// Epochs are monotone per (sender instance, destination pool), whatever the
-// variant or the source pool object, so a flag never moves backwards.
-std::map<std::pair<int, const dyna_kv_pool*>, uint64_t> g_epochs;
+// Flag rows: per (sender instance, destination inbox uid), the next epoch and the next free
+// slot.  Slots are handed out in consecutive ranges and recycle after DYNA_MAX_CHUNKS chunks;
+// flags are raised with an atomic max, so a late writer never moves a flag backwards.
+struct FlagRow {
+  uint64_t epoch = 0;
+  int64_t cursor = 0;
+};
+static std::map<std::pair<int, uint64_t>, FlagRow> g_flag_rows;
 
-uint64_t next_epoch(int sender, const dyna_kv_pool* dst) {
+dyna_status flag_reserve(int sender, const dyna_kv_pool* dst, int64_t nchunks, uint64_t* epoch, int32_t* first_slot) {
+  if (sender < 0 || sender >= DYNA_MAX_INSTANCES) return fail(DYNA_EINVAL, "sender %d", sender);
+  if (nchunks > DYNA_MAX_CHUNKS)
+    return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS (%d) with signalling", (long long)nchunks, DYNA_MAX_CHUNKS);
   std::lock_guard<std::mutex> lk(g_mu);
-  return ++g_epochs[{sender, dst}];
+  auto key = std::make_pair(sender, dst->uid);
+  auto it = g_flag_rows.find(key);
+  if (it == g_flag_rows.end()) {  // first use in this process: start above every flag already in the row
+    std::vector<unsigned long long> row(DYNA_MAX_CHUNKS);
+    DeviceGuard g(dst->dev);
+    cudaStream_t s = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaError_t e = cudaMemcpyAsync(row.data(), dst->inbox + (size_t)sender * DYNA_MAX_CHUNKS,
+                                    sizeof(unsigned long long) * DYNA_MAX_CHUNKS, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (e != cudaSuccess) return fail(DYNA_ECUDA, "reading the inbox row: %s", cudaGetErrorString(e));
+    FlagRow fr;
+    for (unsigned long long v : row) fr.epoch = std::max<uint64_t>(fr.epoch, v);
+    it = g_flag_rows.emplace(key, fr).first;
+  }
+  FlagRow& fr = it->second;
+  if (fr.cursor + nchunks > DYNA_MAX_CHUNKS) fr.cursor = 0;
+  *first_slot = (int32_t)fr.cursor;
+  fr.cursor += nchunks;
+  *epoch = ++fr.epoch;
+  return DYNA_OK;
 }
 
 // Self-resetting per-chunk byte counters of channel src -> dst on device kdev.
@@ -230,24 +293,20 @@ dyna_status channel_counters(dyna_kv_pool* src, const dyna_kv_pool* dst, int kde
   return DYNA_OK;
 }
 
-// Staging slots of channel src -> dst (staged variant): 2 x slot on each side.
-dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t slot, char** sbuf, char** dbuf) {
+// Staging slots of channel src -> dst (staged variant): 2 x slot on each side.  *prev_done:
+// the end of the previous STAGED migration on this channel (its stream may differ), which
+// the caller orders its kernels after; growing the slots waits for it on the host first.
+dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t slot, char** sbuf, char** dbuf,
+                            cudaEvent_t* prev_done) {
   std::lock_guard<std::mutex> lk(src->mu);
   Channel& ch = src->channels[dst];
   if (ch.slot_bytes < slot) {
-    if (ch.sstage) {  // grow: the previous migration on this channel must be done with them
-      DeviceGuard g(ch.sdev);
-      cudaDeviceSynchronize();
-      cudaFree(ch.sstage);
-      ch.sstage = nullptr;
-    }
-    if (ch.dstage) {
-      DeviceGuard g(ch.ddev);
-      cudaDeviceSynchronize();
-      cudaFree(ch.dstage);
-      ch.dstage = nullptr;
-    }
+    if (ch.staged_done) CUDA_TRY(cudaEventSynchronize(ch.staged_done));  // the old slots are no longer read
+    retire(ch.sdev, ch.sstage, Mem::Device);
+    retire(ch.ddev, ch.dstage, Mem::Device);
+    ch.sstage = ch.dstage = nullptr;
     ch.slot_bytes = 0;
+    flush_retired();
     {
       DeviceGuard g(src->dev);
       if (cudaMalloc(&ch.sstage, 2 * slot) != cudaSuccess) return fail(DYNA_ENOMEM, "staging (source side)");
@@ -262,11 +321,36 @@ dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t 
   }
   *sbuf = ch.sstage;
   *dbuf = ch.dstage;
+  *prev_done = ch.staged_done;
+  return DYNA_OK;
+}
+
+// Record the end of a STAGED migration on `stream` (source device) as the channel's lease.
+dyna_status channel_staging_done(dyna_kv_pool* src, const dyna_kv_pool* dst, cudaStream_t stream) {
+  std::lock_guard<std::mutex> lk(src->mu);
+  Channel& ch = src->channels[dst];
+  if (!ch.staged_done) {
+    DeviceGuard g(src->dev);
+    CUDA_TRY(cudaEventCreateWithFlags(&ch.staged_done, cudaEventDisableTiming));
+  }
+  CUDA_TRY(cudaEventRecord(ch.staged_done, stream));
   return DYNA_OK;
 }
 
 std::mutex g_rings_mu;
 std::map<int, UploadRing*> g_rings;
+
+uint64_t new_uid() {
+  static std::atomic<uint64_t> seq{0};
+  static const uint64_t base = [] {
+    std::random_device rd;
+    return ((uint64_t)rd() << 32) ^ rd() ^ (uint64_t)std::chrono::steady_clock::now().time_since_epoch().count();
+  }();
+  uint64_t z = base + 0x9E3779B97F4A7C15ull * (seq.fetch_add(1) + 1);  // splitmix64 finaliser: distinct, well spread
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
 
 }  // namespace rt
 }  // namespace dynakv
@@ -356,6 +440,7 @@ dyna_status dyna_kv_pool_create(const dyna_kv_pool_desc* desc, void* device_base
     return fail(DYNA_EINVAL, "device_base is not device memory of device %d", desc->device);
   auto* p = new dyna_kv_pool();
   p->desc = *desc;
+  p->uid = new_uid();
   p->base = static_cast<char*>(device_base);
   p->dev = desc->device;
   p->row = row;
@@ -412,6 +497,7 @@ dyna_status dyna_kv_pool_export(dyna_kv_pool_t p, dyna_kv_ipc_handle* out) {
   static_assert(sizeof(h) <= 64, "ipc handle size");
   std::memcpy(out->pool_mem, &h, sizeof h);
   out->pool_offset = reinterpret_cast<unsigned long long>(p->base) - alloc_base;
+  out->uid = p->uid;
   cudaIpcMemHandle_t hi{};
   CUDA_TRY(cudaIpcGetMemHandle(&hi, p->inbox));
   std::memcpy(out->inbox_mem, &hi, sizeof hi);
@@ -438,6 +524,7 @@ dyna_status dyna_kv_pool_import(const dyna_kv_ipc_handle* h, int32_t local_devic
   }
   auto* p = new dyna_kv_pool();
   p->desc = h->desc;
+  p->uid = h->uid;
   p->base = static_cast<char*>(mp) + h->pool_offset;
   p->dev = local_device;
   p->imported = true;

@@ -40,8 +40,16 @@ extern thread_local std::string g_err;
 dyna_status fail(dyna_status s, const char* fmt, ...);
 extern std::atomic<uint64_t> g_launches;
 extern std::mutex g_mu;
+// Deferred device-side errors.  Every migration handle owns one word of mapped pinned host
+// memory that its kernels atomicOr ERR_* bits into; dyna_kv_wait reads and releases it, so a
+// migration's wait reports that migration's errors only.  g_err_word is the process-wide word
+// of work that has no handle of its own (dyna_kv_stream_wait_chunk) and of migrations captured
+// into CUDA graphs (their kernels outlive the handle): dyna_kv_poll_error reads it.
 extern unsigned int* g_err_word;
 unsigned int* err_word();
+unsigned int* err_acquire();  // a zeroed word (nullptr if none can be allocated)
+void err_release(unsigned int* w);
+dyna_status err_take(unsigned int* w);  // read-and-clear, as a status
 dyna_status take_device_error();
 
 // copy-engine defaults (the calibration table overrides them per call size)
@@ -49,7 +57,7 @@ constexpr int kVecU = 8;
 constexpr int kVecThreads = 256;
 constexpr int kVecPiece = 8192;
 constexpr int kBulkPiece = 32768;
-constexpr int kBulkStages = 6;
+constexpr int kBulkStages = 4;
 constexpr int64_t kMinBulkRun = 16384;  // AUTO never picks BULK below this contiguous run length
 constexpr int64_t kStageSlotBytes = 64ll << 20;  // staged variant: bytes per staging slot
 constexpr uint32_t kSchedSlots = 1u << 15;       // dynamic-scheduling counter slots per device
@@ -91,8 +99,21 @@ bool desc_valid(const dyna_kv_pool_desc* d);
 int64_t gcd64(int64_t a, int64_t b);
 bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out);
 dyna_status ensure_peer(int dev, int peer);
-uint64_t next_epoch(int sender, const dyna_kv_pool* dst);
-dyna_status check_host_tables(const dyna_block_table& src, const dyna_block_table& dst, int64_t t0, int64_t t1);
+// Per-chunk flags: each signalled logical migration gets a fresh epoch and its own range of
+// consecutive inbox slots of (sender instance, destination inbox).  Keyed on the inbox's uid
+// (carried in IPC handles, so every mapping of one pool shares it); on first use in a process
+// the epoch is seeded from the largest value in that inbox row, so a restarted sender or a
+// re-imported pool never hands out an epoch a stale flag already satisfies.
+uint64_t new_uid();
+dyna_status flag_reserve(int sender, const dyna_kv_pool* dst, int64_t nchunks, uint64_t* epoch, int32_t* first_slot);
+struct Span {  // the rows [lo, hi) of block `id` of the pool with this uid
+  uint64_t uid;
+  int32_t id;
+  int64_t lo, hi;
+};
+dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out);
+dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src);
+bool pools_overlap(const dyna_kv_pool* a, const dyna_kv_pool* b, bool* same);
 
 // Deferred release.  cudaFree / cudaFreeHost / cudaIpcCloseMemHandle may synchronise the
 // device, which deadlocks against a producer-coupled migration that is waiting for marks
@@ -113,10 +134,12 @@ struct Channel {  // sender pool -> destination pool
   char* dstage = nullptr;                      // staged variant: 2 slots on the destination device
   int64_t slot_bytes = 0;
   int sdev = -1, ddev = -1;
+  cudaEvent_t staged_done = nullptr;           // end of the last STAGED migration on this channel (source device)
 };
 
 struct dyna_kv_pool {
   dyna_kv_pool_desc desc{};
+  uint64_t uid = 0;          // identity of the pool's memory and inbox (random at create, carried by export)
   char* base = nullptr;
   int dev = 0;               // device on which `base` can be dereferenced
   bool imported = false;
@@ -165,6 +188,10 @@ struct dyna_kv_channel {
 };
 
 struct dyna_kv_xfer {
+  ~dyna_kv_xfer() {
+    if (err && err != dynakv::rt::g_err_word) dynakv::rt::err_release(err);
+  }
+  unsigned int* err = nullptr;  // this migration's deferred-error word (g_err_word when captured)
   cudaEvent_t ev = nullptr;
   bool captured = false;  // enqueued during CUDA-graph capture: the work runs at replay
   int32_t variant = 0, engine = 0, piece = 0, stages = 0, unroll = 0, launches = 0;
@@ -180,6 +207,7 @@ struct dyna_kv_xfer {
     int32_t first_slot = 0, nchunks = 0, sender = 0;
   };
   std::vector<BatchEntry> batch;
+  int32_t first_slot = 0;          // signalled: chunk k's flag is inbox slot [sender][first_slot + k]
 };
 
 
@@ -235,13 +263,24 @@ class RingLease {
     bytes = (bytes + 255) & ~size_t(255);
     if (bytes > kRingBytes) return fail(DYNA_ENOMEM, "host-resident inputs of %zu B exceed the upload ring", bytes);
     size_t b = R.head;
-    if (b + bytes > kRingBytes) b = 0;
+    if (b + bytes > kRingBytes) b = 0;  // wrap: the tail [head, end) is left unused this lap
     const size_t e = b + bytes;
-    // free every live span that overlaps [b, e) (spans sit in allocation order)
-    while (!R.live.empty() && R.live.front().b < e && b < R.live.front().e) {
-      cudaEventSynchronize(R.live.front().ev);
+    // Recycle finished spans from the front (oldest first), then wait for EVERY live span
+    // that overlaps [b, e), wherever it sits in the queue: after a wrap the front may hold an
+    // older span of the skipped tail while newer overlapping spans follow it, and spans of
+    // different streams need not complete in allocation order.
+    while (!R.live.empty() && cudaEventQuery(R.live.front().ev) == cudaSuccess) {
       R.free_ev.push_back(R.live.front().ev);
       R.live.pop_front();
+    }
+    for (auto it = R.live.begin(); it != R.live.end();) {
+      if (it->b < e && b < it->e) {
+        cudaEventSynchronize(it->ev);
+        R.free_ev.push_back(it->ev);
+        it = R.live.erase(it);
+      } else {
+        ++it;
+      }
     }
     R.head = e;
     span_b_ = b;
@@ -317,10 +356,13 @@ struct Choice {
 Side paged(const dyna_kv_pool* pool, const int32_t* ids);
 Side linear(char* base);
 dyna_status channel_counters(dyna_kv_pool* src, const dyna_kv_pool* dst, int kdev, unsigned long long** out);
-dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t slot, char** sbuf, char** dbuf);
+dyna_status channel_staging(dyna_kv_pool* src, const dyna_kv_pool* dst, int64_t slot, char** sbuf, char** dbuf,
+                            cudaEvent_t* prev_done);
+dyna_status channel_staging_done(dyna_kv_pool* src, const dyna_kv_pool* dst, cudaStream_t stream);
 
 // launch.cu — the only translation unit that instantiates and launches kernels
 void preload_kernels();
+bool ring_enabled();
 Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1, int l0, int lm, int64_t c,
                int64_t g, int piece);
 void set_chunking(Plan& p, int64_t mig_t0, int64_t mig_t1, int64_t sig_c);
@@ -337,22 +379,22 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
                        int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
                        int max_ctas, cudaStream_t stream, dyna_kv_xfer* x, int schedule);
 void launch_wait_flag(const unsigned long long* flag, unsigned long long epoch, unsigned long long timeout_ns,
-                      cudaStream_t st);
+                      cudaStream_t st, unsigned int* err);
 void launch_release_sys(unsigned long long* slot, unsigned long long v, cudaStream_t st);
 void launch_mark_ready(unsigned long long* slot, unsigned long long v, cudaStream_t st);
 dyna_status launch_fill(void* dst, uint64_t bytes, unsigned long long key, uint64_t first_word, int dev,
                         cudaStream_t st);
 
 // migrate.cu
+dyna_status new_xfer(int dev, int sender, cudaStream_t stream, dyna_kv_xfer** out);
 dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream);
 dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o);
 dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
-                          int32_t chunk_tokens, bool* empty, bool heads_may_differ = false);
+                          int32_t chunk_tokens, bool unchecked, bool* empty, std::vector<Span>& dsp,
+                          std::vector<Span>& ssp, int src_spans, bool heads_may_differ);
 dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D);
 Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok, int64_t run_bytes);
 size_t table_upload_bytes(const dyna_block_table& t, int64_t t1);
-dyna_status run_dma(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* hs, const int32_t* hd, dyna_range tr, int l0,
-                    int lm, int64_t c, unsigned long long* flags, uint64_t epoch, cudaStream_t stream);
 
 }  // namespace rt
 }  // namespace dynakv

@@ -33,8 +33,8 @@ V, B, W = dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK, dk.DYNA_ENGINE_BULK_WS
 CANDIDATES = [  # (variant, engine, piece, stages, unroll)
     (F, V, 8192, 0, 4), (F, V, 8192, 0, 8), (F, V, 4096, 0, 8), (F, V, 16384, 0, 8),
     (F, V, 16384, 0, 16), (F, V, 32768, 0, 16),
-    (F, B, 16384, 12, 0), (F, B, 24576, 8, 0), (F, B, 32768, 6, 0), (F, B, 49152, 4, 0), (F, B, 65536, 3, 0),
-    (F, W, 16384, 12, 0), (F, W, 32768, 6, 0), (F, W, 49152, 4, 0),
+    (F, B, 16384, 8, 0), (F, B, 24576, 6, 0), (F, B, 32768, 3, 0), (F, B, 32768, 4, 0), (F, B, 32768, 6, 0),
+    (F, B, 49152, 3, 0), (F, B, 49152, 4, 0), (F, B, 65536, 3, 0),
     (S, V, 8192, 0, 8), (S, B, 32768, 6, 0),
 ]
 GEOMS = {8192: kvgen.LLAMA2_7B, 2048: kvgen.LLAMA3_8B.with_(num_blocks=2048),

@@ -59,7 +59,6 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--ready-ctas", type=int, default=8, help="CTA budget of the coupled launch when budget is 0")
     ap.add_argument("--layers", action="store_true", help="add the layer-granular modes")
-    ap.add_argument("--dma", action="store_true", help="add per-chunk pushes on the copy engines (DYNA_ENGINE_DMA)")
     ap.add_argument("--dst-device", type=int, default=0, help="destination pool's GPU (1: the NVLink form)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "overlap.json"))
     args = ap.parse_args()
@@ -120,13 +119,12 @@ def main():
                 producer_chunk(X)
             if mode == "ready":
                 dk.dyna_kv_ready_mark(board, k, epoch, prod.cuda_stream)
-            if mode in ("chunked", "chunked_dma"):    # chunk k complete -> push it now
+            if mode == "chunked":    # chunk k complete -> push it now
                 ev = torch.cuda.Event()
                 ev.record(prod)
                 mig.wait_event(ev)
                 handles.append(dk.migrate(st, dt, (k * c, min((k + 1) * c, s)), (0, 32), c, stream=mig,
-                                          max_ctas=budget,
-                                          engine=dk.DYNA_ENGINE_DMA if mode == "chunked_dma" else 0))
+                                          max_ctas=budget))
         e_prod.record(prod)
         if mode == "whole":                           # no chunking: push everything after the prefill
             mig.wait_event(e_prod)
@@ -155,9 +153,6 @@ def main():
             run(c, "whole", budget)
             run(c, "chunked", budget)   # warm
             run(c, "ready", budget)
-            DM = []
-            if args.dma:
-                run(c, "chunked_dma", budget)
             if args.layers:
                 run(c, "layered", budget)
                 run(c, "ready_layers", budget)
@@ -165,8 +160,6 @@ def main():
                 W_.append(run(c, "whole", budget))
                 C_.append(run(c, "chunked", budget))
                 R_.append(run(c, "ready", budget))
-                if args.dma:
-                    DM.append(run(c, "chunked_dma", budget))
                 if args.layers:
                     LY.append(run(c, "layered", budget))
                     RL.append(run(c, "ready_layers", budget))
@@ -184,12 +177,6 @@ def main():
                  "ready_coupled": {"ctas": budget or args.ready_ctas, "exposed_ms": exp_r, "T_prod_ms": prod_r,
                                    "producer_slowdown": prod_r / prod_alone - 1,
                                    "reduction": 1 - exp_r / exp_w if exp_w > 0 else None}}
-            if args.dma:
-                exp_d = statistics.median(e for _, e in DM)
-                prod_d = statistics.median(p for p, _ in DM)
-                r["chunked_dma"] = {"exposed_ms": exp_d, "T_prod_ms": prod_d,
-                                    "producer_slowdown": prod_d / prod_alone - 1,
-                                    "reduction": 1 - exp_d / exp_w if exp_w > 0 else None}
             if args.layers:
                 for name, runs in (("layered", LY), ("ready_layers", RL)):
                     exp_l = statistics.median(e for _, e in runs)

@@ -9,6 +9,6 @@ ts, td = kvgen.table_pair(0, 4096, g, g)              # alpha's blocks, beta's f
 st = dk.table(src, torch.from_numpy(ts).cuda(), ts)   # device ids (+ host ids: synchronous range/alias checks)
 dt = dk.table(dst, None, td)                          # host-only ids: the library uploads them
 x = dk.migrate(st, dt, (0, 4096), (0, 32), 512, flags=dk.DYNA_MIGRATE_SIGNAL)
-epoch, nchunks, sender = dk.dyna_kv_xfer_info(x)      # chunk k landed when inbox[sender][k] >= epoch
+epoch, nchunks, sender, first = dk.dyna_kv_xfer_info(x)  # chunk k landed when inbox[sender][first + k] >= epoch
 dk.dyna_kv_wait(x)
 print("readme example ok", epoch, nchunks, sender)

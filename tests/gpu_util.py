@@ -28,6 +28,8 @@ def dev_table(pool: dk.Pool, ids, with_host: bool = True):
 
 def migrate_and_wait(src: dk.Pool, ts, dst: dk.Pool, td, tr, lr, c, with_host=True, **kw):
     st, dt = dev_table(src, ts, with_host), dev_table(dst, td, with_host)  # alive until the wait
+    if not with_host:  # device-only tables: the caller vouches for distinct destination rows
+        kw["flags"] = kw.get("flags", 0) | dk.DYNA_MIGRATE_UNCHECKED
     x = dk.migrate(st, dt, tr, lr, c, **kw)
     dk.dyna_kv_wait(x)
 

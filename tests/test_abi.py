@@ -52,16 +52,32 @@ def test_sass_has_bulk_copies_and_vector_moves():
     assert "HMMA" not in sass and "UTCHMMA" not in sass  # no contraction on this path
 
 
-def test_struct_layouts_match_header():
+def test_struct_layouts_match_header(tmp_path):
+    """Every struct the binding mirrors has the size and field offsets a C compiler gives the
+    header's declaration."""
     import paper_2504_09285_b200 as dk
-    assert ctypes.sizeof(dk.dyna_kv_pool_desc) == 32
-    assert ctypes.sizeof(dk.dyna_block_table) == 32
-    assert ctypes.sizeof(dk.dyna_range) == 16
-    assert ctypes.sizeof(dk.dyna_kv_opts) == 32
-    assert ctypes.sizeof(dk.dyna_kv_calib_entry) == 32
-    assert ctypes.sizeof(dk.dyna_kv_migration) == 32 + 32 + 16
-    assert ctypes.sizeof(dk.dyna_kv_channel_handle) == 64 + 8 + 4 + 4 + 32
-    assert ctypes.sizeof(dk.dyna_kv_ipc_handle) == 64 + 64 + 8 + 32
+    structs = {"dyna_kv_pool_desc": dk.dyna_kv_pool_desc, "dyna_block_table": dk.dyna_block_table,
+               "dyna_range": dk.dyna_range, "dyna_kv_opts": dk.dyna_kv_opts,
+               "dyna_kv_calib_entry": dk.dyna_kv_calib_entry, "dyna_kv_migration": dk.dyna_kv_migration,
+               "dyna_kv_channel_handle": dk.dyna_kv_channel_handle, "dyna_kv_ipc_handle": dk.dyna_kv_ipc_handle}
+    lines = []
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "dyna_kv.h"\nint main(void) {\n' +
+                   "\n".join(lines) + "\nreturn 0;\n}\n")
+    exe = tmp_path / "sz"
+    r = subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split("\n")
+               if line)
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, f"{name}.{f}"
 
 
 def test_status_constants_match_header():

@@ -54,6 +54,35 @@ def test_upload_ring_wraps_many_calls():
     assert torch_rows_equal(src, ts, dst, td, (0, 8192 * 16), (0, 1))
 
 
+def test_upload_ring_mixed_sizes_behind_long_kernel():
+    """Upload-ring reuse after misaligned wraps: host tables of mixed sizes
+    (256 B .. 300 KB) and different contents per call, all queued behind a long kernel so no
+    consumer has read its span when the ring wraps.  Every migration must read its own table:
+    the destination equals the oracle applying the same migrations in stream order."""
+    nb = 100_000
+    g = Geom(1, 1, 8, 2, 1, nb)             # row 16 B, block size 1: one table id per token
+    hs, hd = kvgen.fill_bytes(21, g.pool_bytes), kvgen.fill_bytes(22, g.pool_bytes)
+    want = hd.copy()
+    rng = np.random.default_rng(5)
+    calls = []
+    for i in range(90):
+        n = int(rng.choice([64, 700, 5000, 30_000, 75_000]))
+        ts = rng.choice(nb, n, replace=False).astype(np.int32)
+        td = rng.choice(nb, n, replace=False).astype(np.int32)
+        calls.append((ts, td, n))
+        oracle.migrate(hs, g, ts, want, g, td, (0, n))
+    src, dst = pool_from_host(g, hs), pool_from_host(g, hd)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)           # ~0.1 s: every queued migration waits behind it
+    xs = []
+    for ts, td, n in calls:
+        st, dt = host_table(src, ts), host_table(dst, td)
+        xs.append((dk.migrate(st, dt, (0, n), (0, 1), max(1, n // 3)), st, dt))
+    for x, _, _ in xs:
+        dk.dyna_kv_wait(x)
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
+
+
 @pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("host_tables", [False, True])
 def test_batch_matches_oracle(engine, host_tables):
@@ -346,7 +375,7 @@ def test_native_chunkstream_prefill_then_decode(signal):
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
     if signal:
         fl = torch.zeros(5, dtype=torch.int64).pin_memory()
-        dk.dyna_kv_copy_flags(dst.handle, info["sender"], 0, 5, fl.data_ptr(), 0)
+        dk.dyna_kv_copy_flags(dst.handle, info["sender"], info["first_slot"], 5, fl.data_ptr(), 0)
         torch.cuda.synchronize()
         assert (fl.numpy() == info["epoch"]).all()
 

@@ -36,13 +36,13 @@ def test_push_place_loopback(slots, slot_bytes, c, signal):
             xp = dk.dyna_kv_push(st, tr, (0, 4), c, ch, s_push.cuda_stream)
             xq = dk.dyna_kv_place(ch, dt, tr, (0, 4), c, s_place.cuda_stream,
                                   dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0))
-            epoch, nchunks, sender = dk.dyna_kv_xfer_info(xq)
+            epoch, nchunks, sender, first = dk.dyna_kv_xfer_info(xq)
             dk.dyna_kv_wait(xp)
             dk.dyna_kv_wait(xq)
             assert np.array_equal(dst.tensor.cpu().numpy(), want)
             if signal:
                 flags = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
-                dk.dyna_kv_copy_flags(dst.handle, sender, 0, nchunks, flags.data_ptr(), 0)
+                dk.dyna_kv_copy_flags(dst.handle, sender, first, nchunks, flags.data_ptr(), 0)
                 torch.cuda.synchronize()
                 assert sender == 9 and (flags.numpy() == epoch).all()
             dst.tensor.copy_(torch.from_numpy(hd).cuda())
@@ -140,13 +140,13 @@ def test_push_place_heads_tp1_to_tp2(slots, slot_bytes, c, signal):
             xp = dk.dyna_kv_push_heads(st, tr, (0, 4), (4 * r, 4 * r + 4), c, ch, s_push.cuda_stream)
             xq = dk.dyna_kv_place_heads(ch, dt, tr, (0, 4), 0, 4, c, s_place.cuda_stream,
                                         dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0))
-            epoch, nchunks, sender = dk.dyna_kv_xfer_info(xq)
+            epoch, nchunks, sender, first = dk.dyna_kv_xfer_info(xq)
             dk.dyna_kv_wait(xp)
             dk.dyna_kv_wait(xq)
             assert np.array_equal(dst.tensor.cpu().numpy(), want)
             if signal:
                 flags = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
-                dk.dyna_kv_copy_flags(dst.handle, sender, 0, nchunks, flags.data_ptr(), 0)
+                dk.dyna_kv_copy_flags(dst.handle, sender, first, nchunks, flags.data_ptr(), 0)
                 torch.cuda.synchronize()
                 assert sender == 3 and (flags.numpy() == epoch).all()
         finally:

@@ -25,6 +25,8 @@ def _heads_parity(gs, gd, n_tok, tr, lr, c, heads, hd0, seed=1, flags=0, piece=0
     oracle.migrate_heads(hs, gs, ts, want, gd, td, tr, lr, heads, hd0)
     src, dst = pool_from_host(gs, hs), pool_from_host(gd, hd)
     st, dt = dev_table(src, ts, with_host), dev_table(dst, td, with_host)
+    if not with_host:
+        flags |= dk.DYNA_MIGRATE_UNCHECKED
     x = dk.dyna_kv_migrate_heads(st, dt, tr, lr, heads, hd0, c, 0, dk.opts(flags=flags, piece_bytes=piece))
     info = dk.dyna_kv_xfer_info(x)
     dk.dyna_kv_wait(x)
@@ -66,11 +68,11 @@ def test_heads_reblocking(bss, bsd):
 
 
 def test_heads_signal_flags_and_host_tables():
-    src, dst, (epoch, nck, sender) = _heads_parity(G8, G4, 500, (0, 451), (0, 3), 64, (4, 8), 0,
-                                                   flags=dk.DYNA_MIGRATE_SIGNAL, with_host=False)
+    src, dst, (epoch, nck, sender, first) = _heads_parity(G8, G4, 500, (0, 451), (0, 3), 64, (4, 8), 0,
+                                                          flags=dk.DYNA_MIGRATE_SIGNAL, with_host=False)
     assert nck == 8 and epoch > 0
     fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
-    dk.dyna_kv_copy_flags(dst.handle, sender, 0, nck, fl.data_ptr(), 0)
+    dk.dyna_kv_copy_flags(dst.handle, sender, first, nck, fl.data_ptr(), 0)
     torch.cuda.synchronize()
     assert (fl.numpy() == epoch).all()
     ts, td = kvgen.table_pair(101, 500, G8, G4)

@@ -154,12 +154,12 @@ def test_signal_per_chunk_flags(variant, engine):
     for rep in range(3):
         x = dk.migrate(dev_table(src, ts), dev_table(dst, td), (0, s), (0, 4), c, variant=variant, engine=engine,
                        flags=dk.DYNA_MIGRATE_SIGNAL)
-        epoch, nchunks, sender = dk.dyna_kv_xfer_info(x)
+        epoch, nchunks, sender, first = dk.dyna_kv_xfer_info(x)
         assert nchunks == -(-s // c) and sender == 5
         epochs.append(epoch)
         consumer = torch.cuda.Stream()
         for k in range(nchunks):  # the destination waits chunk by chunk
-            dk.dyna_kv_stream_wait_chunk(dst.handle, sender, k, epoch, 5_000_000_000, consumer.cuda_stream)
+            dk.dyna_kv_stream_wait_chunk(dst.handle, sender, first + k, epoch, 5_000_000_000, consumer.cuda_stream)
         ev = torch.cuda.Event()
         ev.record(consumer)
         ev.synchronize()
@@ -217,7 +217,8 @@ def test_device_side_bad_block_id():
     bad = td.copy()
     bad[2] = -5
     for engine in ENGINES:
-        x = dk.migrate(dev_table(src, ts, False), dev_table(dst, bad, False), (0, 100), (0, 2), 32, engine=engine)
+        x = dk.migrate(dev_table(src, ts, False), dev_table(dst, bad, False), (0, 100), (0, 2), 32, engine=engine,
+                       flags=dk.DYNA_MIGRATE_UNCHECKED)
         _expect(dk.DYNA_ERANGE, lambda: dk.dyna_kv_wait(x))
 
 
@@ -341,11 +342,12 @@ def test_flag_litmus_chunk_visible_when_flagged(variant, engine):
         torch.cuda.synchronize()
         x = dk.migrate(st, dt, (0, s), (0, g.num_layers), c, variant=variant, engine=engine, max_ctas=2,
                        flags=dk.DYNA_MIGRATE_SIGNAL)
-        epoch, nchunks, sender = dk.dyna_kv_xfer_info(x)
+        epoch, nchunks, sender, first = dk.dyna_kv_xfer_info(x)
         snaps = {}
         with torch.cuda.stream(consumer):
             for k in rng.permutation(nchunks):
-                dk.dyna_kv_stream_wait_chunk(dst.handle, sender, int(k), epoch, 10_000_000_000, consumer.cuda_stream)
+                dk.dyna_kv_stream_wait_chunk(dst.handle, sender, first + int(k), epoch, 10_000_000_000,
+                                             consumer.cuda_stream)
                 t = torch.arange(int(k) * c, min((int(k) + 1) * c, s), device="cuda")
                 snaps[int(k)] = D[:, :, Td[t // g.block_size], t % g.block_size].clone()
         consumer.synchronize()
@@ -364,11 +366,11 @@ def test_max_chunks_with_flags():
     st, dt = dev_table(src, ts), dev_table(dst, td)
     n = dk.DYNA_MAX_CHUNKS
     x = dk.migrate(st, dt, (0, n), (0, 1), 1, flags=dk.DYNA_MIGRATE_SIGNAL)
-    epoch, nck, sender = dk.dyna_kv_xfer_info(x)
+    epoch, nck, sender, first = dk.dyna_kv_xfer_info(x)
     dk.dyna_kv_wait(x)
-    assert nck == n
+    assert nck == n and first == 0       # a whole inbox row: the reservation starts at slot 0
     fl = torch.zeros(n, dtype=torch.int64).pin_memory()
-    dk.dyna_kv_copy_flags(dst.handle, sender, 0, n, fl.data_ptr(), 0)
+    dk.dyna_kv_copy_flags(dst.handle, sender, first, n, fl.data_ptr(), 0)
     torch.cuda.synchronize()
     assert (fl.numpy() == epoch).all()
     assert torch_rows_equal(src, ts, dst, td, (0, n), (0, 1))

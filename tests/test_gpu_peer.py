@@ -40,14 +40,14 @@ def test_peer_parity(variant, engine, signal):
     torch.cuda.set_device(0)
     x = dk.dyna_kv_migrate_ex(st, dt, tr, (0, 4), 512, 0,
                               dk.opts(variant=variant, engine=engine, flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0))
-    epoch, nck, sender = dk.dyna_kv_xfer_info(x)
+    epoch, nck, sender, first = dk.dyna_kv_xfer_info(x)
     dk.dyna_kv_wait(x)
     torch.cuda.synchronize(1)
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
     if signal:
         fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
         with torch.cuda.device(1):
-            dk.dyna_kv_copy_flags(dst.handle, sender, 0, nck, fl.data_ptr(), 0)
+            dk.dyna_kv_copy_flags(dst.handle, sender, first, nck, fl.data_ptr(), 0)
             torch.cuda.synchronize()
         assert (fl.numpy() == epoch).all()
 

@@ -221,7 +221,7 @@ def test_per_layer_marks_copy_each_layer_after_its_mark(c):
         want = _oracle_expect(3, g, ts, 2, td, (0, s))
         assert np.array_equal(dst.tensor.cpu().numpy(), want)
         flags = torch.zeros(nck, dtype=torch.int64).pin_memory()
-        dk.dyna_kv_copy_flags(dst.handle, info[2], 0, nck, flags.data_ptr(), 0)
+        dk.dyna_kv_copy_flags(dst.handle, info[2], info[3], nck, flags.data_ptr(), 0)
         torch.cuda.synchronize()
         assert int(flags.min()) == info[0]
     finally:
@@ -273,7 +273,7 @@ def test_cancel_delivers_marked_chunks_and_stops(per_layer):
         epoch = dk.dyna_kv_ready_begin(board)
         x = dk.dyna_kv_migrate_on_ready(src_t, dst_t, (0, s), (0, lm), c, board, epoch, mig.cuda_stream,
                                         dk.opts(max_ctas=8, flags=flags))
-        ep, nchunks, sender = dk.dyna_kv_xfer_info(x)
+        ep, nchunks, sender, first = dk.dyna_kv_xfer_info(x)
         for k in range(m):
             for l in (range(lm) if per_layer else [0]):
                 dk.dyna_kv_ready_mark(board, dk.ready_slot(k, l, (0, lm)) if per_layer else k, epoch,
@@ -288,7 +288,7 @@ def test_cancel_delivers_marked_chunks_and_stops(per_layer):
         assert time.perf_counter() - t < 5.0
         torch.cuda.synchronize()
         fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
-        dk.dyna_kv_copy_flags(dst.handle, sender, 0, nck, fl.data_ptr(), 0)
+        dk.dyna_kv_copy_flags(dst.handle, sender, first, nck, fl.data_ptr(), 0)
         torch.cuda.synchronize()
         got = fl.numpy()
         assert (got[:m] == ep).all() and (got[m:] < ep).all(), got
@@ -301,9 +301,9 @@ def test_cancel_delivers_marked_chunks_and_stops(per_layer):
         # the next signalled migration over the same (src, dst) channel gets every flag
         dst2_seed = 2
         y = dk.dyna_kv_migrate_ex(src_t, dst_t, (0, s), (0, lm), c, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL))
-        ep2 = dk.dyna_kv_xfer_info(y)[0]
+        ep2, _, _, first2 = dk.dyna_kv_xfer_info(y)
         dk.dyna_kv_wait(y)
-        dk.dyna_kv_copy_flags(dst.handle, sender, 0, nck, fl.data_ptr(), 0)
+        dk.dyna_kv_copy_flags(dst.handle, sender, first2, nck, fl.data_ptr(), 0)
         torch.cuda.synchronize()
         assert (fl.numpy() == ep2).all()
         assert np.array_equal(dst.tensor.cpu().numpy(), _oracle_expect(1, g, ts, dst2_seed, td, (0, s)))

@@ -22,7 +22,7 @@ def _geom():
     return Geom(4, 8, 128, 2, 16, 400)
 
 
-def _sender(handle: bytes, q, engine: int):
+def _sender(handle: bytes, q, engine: int, reps: int = 1):
     try:
         import torch
 
@@ -36,9 +36,10 @@ def _sender(handle: bytes, q, engine: int):
         ts, td = kvgen.table_pair(9, 4000, g, g)
         src_t = dev_table(src, ts)
         dst_t = dk.table(dst, torch.from_numpy(td).cuda(), td)
-        x = dk.migrate(src_t, dst_t, (0, S), (0, 4), CHUNK, engine=engine, flags=dk.DYNA_MIGRATE_SIGNAL)
-        info = dk.dyna_kv_xfer_info(x)
-        dk.dyna_kv_wait(x)
+        for _ in range(reps):
+            x = dk.migrate(src_t, dst_t, (0, S), (0, 4), CHUNK, engine=engine, flags=dk.DYNA_MIGRATE_SIGNAL)
+            info = dk.dyna_kv_xfer_info(x)
+            dk.dyna_kv_wait(x)
         dst.close()
         q.put(("ok", info))
     except Exception as e:  # surface the failure to the parent
@@ -64,14 +65,14 @@ def test_ipc_push_with_chunk_flags(engine):
     status, info = q.get(timeout=300)
     p.join(timeout=60)
     assert status == "ok", info
-    epoch, nchunks, sender = info
+    epoch, nchunks, sender, first = info
     assert sender == SENDER and nchunks == -(-S // CHUNK) and epoch >= 1
     # the owner waits on every chunk flag (already released) and reads them back
     st = torch.cuda.current_stream()
     for k in range(nchunks):
-        dk.dyna_kv_stream_wait_chunk(dst.handle, sender, k, epoch, 2_000_000_000, st.cuda_stream)
+        dk.dyna_kv_stream_wait_chunk(dst.handle, sender, first + k, epoch, 2_000_000_000, st.cuda_stream)
     flags = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
-    dk.dyna_kv_copy_flags(dst.handle, sender, 0, nchunks, flags.data_ptr(), st.cuda_stream)
+    dk.dyna_kv_copy_flags(dst.handle, sender, first, nchunks, flags.data_ptr(), st.cuda_stream)
     torch.cuda.synchronize()
     dk.dyna_kv_poll_error()
     assert (flags.numpy() == epoch).all()
@@ -127,9 +128,9 @@ def test_ipc_head_reshard_with_chunk_flags():
     status, info = q.get(timeout=300)
     p.join(timeout=60)
     assert status == "ok", info
-    epoch, nchunks, sender = info
+    epoch, nchunks, sender, first = info
     flags = torch.zeros(nchunks, dtype=torch.int64).pin_memory()
-    dk.dyna_kv_copy_flags(dst.handle, sender, 0, nchunks, flags.data_ptr(), 0)
+    dk.dyna_kv_copy_flags(dst.handle, sender, first, nchunks, flags.data_ptr(), 0)
     torch.cuda.synchronize()
     assert (flags.numpy() == epoch).all()
     ts, _ = kvgen.table_pair(9, 4000, g, g)
@@ -137,3 +138,29 @@ def test_ipc_head_reshard_with_chunk_flags():
     want = kvgen.fill_bytes(DST_SEED, gd.pool_bytes)
     oracle.migrate_heads(kvgen.fill_bytes(SRC_SEED, g.pool_bytes), g, ts, want, gd, td, (0, S), None, (4, 8), 0)
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
+
+
+def test_restarted_sender_never_reuses_an_epoch():
+    """epochs were counted per importing process from 1, so a restarted
+    sender (same instance id, fresh import of the same pool) handed out epochs that stale
+    flags of its previous incarnation already satisfied.  Epochs now start above the inbox
+    row's largest flag: the second process's epoch exceeds every epoch of the first."""
+    import torch
+
+    import paper_2504_09285_b200 as dk
+    from gpu_util import pool_filled
+    torch.cuda.set_device(0)
+    dst = pool_filled(_geom(), DST_SEED)
+    torch.cuda.synchronize()
+    handle = dk.dyna_kv_pool_export(dst.handle)
+    ctx = mp.get_context("spawn")
+    infos = []
+    for reps in (3, 1):                       # first incarnation: three migrations; then a restart
+        q = ctx.Queue()
+        p = ctx.Process(target=_sender, args=(handle, q, 2, reps))
+        p.start()
+        status, info = q.get(timeout=300)
+        p.join(timeout=60)
+        assert status == "ok", info
+        infos.append(info)
+    assert infos[1][0] > infos[0][0], infos
