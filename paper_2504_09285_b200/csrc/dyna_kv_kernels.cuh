@@ -522,6 +522,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 constexpr int kMail = 8;
 struct Mailbox {
   uint64_t full[kMail], empty[kMail];
+  const Plan* pl[kMail];  // batches: the plan (request) the chunk belongs to; nullptr = the launch's plan
   int32_t k[kMail];
   uint32_t acc[kMail];
   __device__ __forceinline__ void init() {
@@ -530,9 +531,10 @@ struct Mailbox {
       mbar_init(&empty[m], 1);
     }
   }
-  __device__ __forceinline__ void post(int64_t& n, int32_t kk, uint32_t a) {
+  __device__ __forceinline__ void post(int64_t& n, int32_t kk, uint32_t a, const Plan* plan = nullptr) {
     const int m = (int)(n % kMail);
     if (n >= kMail) mbar_wait(&empty[m], (uint32_t)(((n / kMail) - 1) & 1));
+    pl[m] = plan;
     k[m] = kk;
     acc[m] = a;
     mbar_arrive(&full[m]);
@@ -562,10 +564,12 @@ struct Mailbox {
 #endif
       const int32_t kk = k[m];
       const uint32_t a = acc[m];
+      const Plan* plan = pl[m];
       mbar_arrive(&empty[m]);
       if (kk < 0) return;
-      fence_for(p);
-      account_chunk(p, kk, a);
+      const Plan& P = plan ? *plan : p;
+      fence_for(P);
+      account_chunk(P, kk, a);
     }
   }
 };
@@ -890,6 +894,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_bulk_ws(const Src src, i
 struct Desc {
   const char* src;
   char* dst;
+  const Plan* pl;  // batches: the item's plan (per-request chunk flags); unused for one plan
   uint32_t n;
   int32_t k;
 };
@@ -903,9 +908,11 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
   __shared__ __align__(8) Desc q[kQ][32];
   __shared__ int32_t qcount[kQ], qlast[kQ];
   __shared__ char* pend_dst[kMaxStages];
+  __shared__ const Plan* pend_pl[kMaxStages];
   __shared__ uint32_t pend_n[kMaxStages];
   __shared__ int32_t pend_k[kMaxStages];
   __shared__ __align__(8) Mailbox mail[1];  // (ACC only)
+  constexpr bool kBatch = std::is_same<Src, BatchSource>::value;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
@@ -929,14 +936,16 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
       const int64_t gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
       m += 32;
       Item it{nullptr, nullptr, 0u, 0u, 0, 0};
+      const Plan* ipl = nullptr;
       if (gi < n_items) {
         int64_t item = gi;
         const Plan& ip = src.locate(item);
+        ipl = kBatch ? &ip : nullptr;
         it = decode_item(ip, item);
-        if (SIGNAL && it.n == 0 && it.acc) account_chunk(p, it.k, it.acc);  // skipped (bad id): still closes the chunk
+        if (SIGNAL && it.n == 0 && it.acc) account_chunk(ip, it.k, it.acc);  // skipped (bad id): still closes the chunk
       }
       const unsigned mask = __ballot_sync(0xffffffffu, it.n != 0);
-      if (it.n) q[qb][__popc(mask & ((1u << lane) - 1u))] = Desc{it.src, it.dst, it.n, it.k};
+      if (it.n) q[qb][__popc(mask & ((1u << lane) - 1u))] = Desc{it.src, it.dst, ipl, it.n, it.k};
       const bool last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
       __syncwarp();
       if (lane == 0) {
@@ -978,30 +987,37 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
     pend_dst[s] = d.dst;
     pend_n[s] = d.n;
     pend_k[s] = d.k;
+    if (kBatch) pend_pl[s] = d.pl;
   };
   for (int s = 0; s < stages; ++s) refill(s);
 
+  // Signalling: stores are counted per chunk (per (plan, chunk) in a batch).  When the next
+  // store belongs to another chunk, the finished chunk's bytes are parked and counted once
+  // kDefer more stores were committed after them, behind a wait_group kDefer.
   constexpr int kDefer = DYNA_BULK_DEFER;
   int32_t cur_k = -1, park_k = -1;
+  const Plan *cur_pl = nullptr, *park_pl = nullptr;
   uint32_t cur_acc = 0, park_acc = 0;
   int since_park = 0;
   auto flush_park = [&](bool all) {
     if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    if (ACC) mail[0].post(posted, park_k, park_acc);
-    else account_chunk_release(p, park_k, park_acc);
+    if (ACC) mail[0].post(posted, park_k, park_acc, park_pl);
+    else account_chunk_release(kBatch ? *park_pl : p, park_k, park_acc);
     park_k = -1;
     park_acc = 0;
   };
   for (int64_t iter = 0;; ++iter) {
     const int s = (int)(iter % stages);
     if (pend_n[s] == 0) break;
-    if (SIGNAL && pend_k[s] != cur_k) {
+    if (SIGNAL && (pend_k[s] != cur_k || (kBatch && pend_pl[s] != cur_pl))) {
       if (park_acc) flush_park(true);
       park_k = cur_k;
+      park_pl = cur_pl;
       park_acc = cur_acc;
       since_park = 0;
       cur_k = pend_k[s];
+      if (kBatch) cur_pl = pend_pl[s];
       cur_acc = 0;
     }
     mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
@@ -1022,10 +1038,11 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
     if (cur_acc) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
       if (ACC) {
-        mail[0].post(posted, cur_k, cur_acc);
+        mail[0].post(posted, cur_k, cur_acc, cur_pl);
       } else {
-        fence_for(p);
-        account_chunk(p, cur_k, cur_acc);
+        const Plan& P = kBatch ? *cur_pl : p;
+        fence_for(P);
+        account_chunk(P, cur_k, cur_acc);
       }
     }
   }

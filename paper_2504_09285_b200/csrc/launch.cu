@@ -39,7 +39,7 @@ void preload_kernels() {
       (const void*)k_copy_rows<8, false>, (const void*)k_copy_rows<8, true>,
       (const void*)k_copy_ring<false, SingleSource>, (const void*)k_copy_ring<true, SingleSource>,
       (const void*)k_copy_ring<true, SingleSource, true>, (const void*)k_copy_ring<false, BatchSource>,
-      (const void*)k_copy_ring<true, BatchSource>,
+      (const void*)k_copy_ring<true, BatchSource>, (const void*)k_copy_ring<true, BatchSource, true>,
   };
   for (const void* k : ks) cudaFuncGetAttributes(&a, k);
   // Allow the BULK rings any dynamic shared memory the device offers, once, here: a
@@ -55,7 +55,7 @@ void preload_kernels() {
       (const void*)k_copy_bulk_ws<true, SingleSource, true>, (const void*)k_copy_bulk<true, SingleSource, true>,
       (const void*)k_copy_ring<false, SingleSource>, (const void*)k_copy_ring<true, SingleSource>,
       (const void*)k_copy_ring<true, SingleSource, true>, (const void*)k_copy_ring<false, BatchSource>,
-      (const void*)k_copy_ring<true, BatchSource>,
+      (const void*)k_copy_ring<true, BatchSource>, (const void*)k_copy_ring<true, BatchSource, true>,
   };
   for (const void* k : bulk) {
     cudaFuncGetAttributes(&a, k);
@@ -254,7 +254,7 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
   }();
   const bool single = std::is_same<Src, SingleSource>::value;
   const bool ring = ring_enabled();
-  const bool acc = SIG && single && (ring || ws ? acc_mode >= 1 : acc_mode == 2);
+  const bool acc = SIG && (ring ? acc_mode >= 1 : single && (ws ? acc_mode >= 1 : acc_mode == 2));
   void (*kbulk)(const Src, int, unsigned long long*) =
       ws ? (acc ? k_copy_bulk_ws<SIG, Src, true> : k_copy_bulk_ws<SIG, Src>)
          : (acc ? k_copy_bulk<SIG, Src, true> : k_copy_bulk<SIG, Src>);

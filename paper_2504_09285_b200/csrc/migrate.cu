@@ -65,7 +65,7 @@ dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
 // 1 = always (batches: another entry may write this source pool).  *empty: nothing to move.
 dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
                           int32_t chunk_tokens, bool unchecked, bool* empty, std::vector<Span>& dsp,
-                          std::vector<Span>& ssp, int src_spans, bool heads_may_differ) {
+                          std::vector<Span>& ssp, int src_spans, bool heads_may_differ, int32_t who) {
   if (!src.pool || !dst.pool) return fail(DYNA_EINVAL, "NULL pool in a block table");
   const dyna_kv_pool_desc &gs = src.pool->desc, &gd = dst.pool->desc;
   if (gs.num_layers != gd.num_layers || (!heads_may_differ && gs.num_kv_heads != gd.num_kv_heads) ||
@@ -95,13 +95,13 @@ dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& d
     return fail(DYNA_EINVAL, "source and destination are one pool: give the source table's host_block_ids "
                              "too, or pass DYNA_MIGRATE_UNCHECKED");
   dyna_status r;
-  if (dst.host_block_ids && (r = table_spans(dst, tr.begin, tr.end, dsp))) return r;
+  if (dst.host_block_ids && (r = table_spans(dst, tr.begin, tr.end, dsp, who))) return r;
   if (src.host_block_ids) {
     if (src_spans || same) {
-      if ((r = table_spans(src, tr.begin, tr.end, ssp))) return r;
+      if ((r = table_spans(src, tr.begin, tr.end, ssp, who))) return r;
     } else {
       std::vector<Span> tmp;  // range check only
-      if ((r = table_spans(src, tr.begin, tr.end, tmp))) return r;
+      if ((r = table_spans(src, tr.begin, tr.end, tmp, who))) return r;
     }
   }
   return DYNA_OK;
@@ -581,8 +581,8 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
   const bool unchecked = (o.flags & DYNA_MIGRATE_UNCHECKED) != 0;
-  if (signal && o.engine && o.engine != DYNA_ENGINE_VEC)
-    return fail(DYNA_ENOTSUP, "batch with per-chunk flags: VEC engine only");
+  if (signal && o.engine && o.engine != DYNA_ENGINE_VEC && !ring_enabled())
+    return fail(DYNA_ENOTSUP, "batch with per-chunk flags: VEC engine only (DYNA_KV_RING=0)");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   // Reading R7 across entries: one entry's source rows may be another entry's destination rows.
   std::vector<uint64_t> dst_uids;
@@ -599,7 +599,7 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     const dyna_block_table &ms = migs[i].src, &md = migs[i].dst;
     const bool src_is_dst = ms.pool && std::binary_search(dst_uids.begin(), dst_uids.end(), ms.pool->uid);
     if ((r = validate_pair(ms, md, migs[i].token_range, lr, chunk_tokens, unchecked, &empty, dsp, ssp,
-                           src_is_dst ? 1 : 0, false))) {
+                           src_is_dst ? 1 : 0, false, i))) {
       g_err = "migration " + std::to_string(i) + ": " + g_err;
       return r;
     }
@@ -631,10 +631,11 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
                                                                   migs[i].dst.pool->desc.block_size),
                                                             chunk_tokens) * S0->row);
   Choice ch = choose(o, S0->row, peer, total_tok, run_min);
-  if (signal || (!o.engine && ch.engine != DYNA_ENGINE_VEC && !ring_enabled())) {
-    // per-chunk accounting is per plan: VEC.  Round-1 BULK kernels decode (and look plans up)
-    // on the issuing thread, latency-bound with many plans (scripts/batch_probe.py); the ring
-    // kernel's decoder warp does the lookups (configs[2] batch: 3263 vs VEC 2966 GB/s,
+  if (!ring_enabled() && (signal || (!o.engine && ch.engine != DYNA_ENGINE_VEC))) {
+    // Round-1 BULK kernels (DYNA_KV_RING=0) count chunks for one plan only and decode (and look
+    // plans up) on the issuing thread, latency-bound with many plans (scripts/batch_probe.py):
+    // VEC.  The ring kernel counts per (plan, chunk) and its decoder warp does the lookups
+    // (configs[2] batch: 3263 vs VEC 2966 GB/s,
     // profiles/r02_engine_ab_ring.json).
     ch.engine = DYNA_ENGINE_VEC;
     ch.unroll = o.unroll ? o.unroll : kVecU;

@@ -181,13 +181,13 @@ Side linear(char* base) {
 
 // Rows a table reaches for tokens [t0, t1), as (pool uid, block id, slot range) spans; ids
 // are range-checked on the way (DYNA_ERANGE).  Needs the host copy of the ids.
-dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out) {
+dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out, int32_t who) {
   const int64_t bs = t.pool->desc.block_size, nb = t.pool->desc.num_blocks;
   for (int64_t j = t0 / bs; j <= (t1 - 1) / bs; ++j) {
     const int32_t id = t.host_block_ids[j];
     if (id < 0 || id >= nb) return fail(DYNA_ERANGE, "block_ids[%lld] = %d outside [0, %lld)", (long long)j, id, (long long)nb);
     const int64_t lo = std::max(t0, j * bs) - j * bs, hi = std::min(t1, (j + 1) * bs) - j * bs;
-    out.push_back({t.pool->uid, id, lo, hi});
+    out.push_back({t.pool->uid, id, lo, hi, who});
   }
   return DYNA_OK;
 }
@@ -199,18 +199,23 @@ dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src) {
   auto by = [](const Span& a, const Span& b) {
     return a.uid != b.uid ? a.uid < b.uid : a.id != b.id ? a.id < b.id : a.lo < b.lo;
   };
+  auto named = [](const Span& a, const Span& b, const char* what) {
+    if (a.who < 0) return fail(DYNA_EALIAS, "%s block %d", what, a.id);
+    return fail(DYNA_EALIAS, "migration %d: %s block %d (also migration %d)", std::max(a.who, b.who), what, a.id,
+                std::min(a.who, b.who));
+  };
   std::sort(dst.begin(), dst.end(), by);
   for (size_t i = 1; i < dst.size(); ++i)
     if (dst[i].uid == dst[i - 1].uid && dst[i].id == dst[i - 1].id && dst[i].lo < dst[i - 1].hi)
-      return fail(DYNA_EALIAS, "destination block %d is reached twice", dst[i].id);
+      return named(dst[i], dst[i - 1], "destination rows written twice in");
   if (src.empty()) return DYNA_OK;
   std::sort(src.begin(), src.end(), by);
   size_t k = 0;
   for (const Span& x : dst) {  // both sorted: one merge pass
-    while (k < src.size() && by(src[k], Span{x.uid, x.id, 0, 0})) ++k;
+    while (k < src.size() && by(src[k], Span{x.uid, x.id, 0, 0, -1})) ++k;
     for (size_t m = k; m < src.size() && src[m].uid == x.uid && src[m].id == x.id; ++m)
       if (src[m].lo < x.hi && x.lo < src[m].hi)
-        return fail(DYNA_EALIAS, "destination rows of block %d overlap source rows of the same pool", x.id);
+        return named(x, src[m], "destination rows that are also source rows in");
   }
   return DYNA_OK;
 }

@@ -110,8 +110,9 @@ struct Span {  // the rows [lo, hi) of block `id` of the pool with this uid
   uint64_t uid;
   int32_t id;
   int64_t lo, hi;
+  int32_t who;   // batch entry (-1: a single call)
 };
-dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out);
+dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out, int32_t who);
 dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src);
 bool pools_overlap(const dyna_kv_pool* a, const dyna_kv_pool* b, bool* same);
 
@@ -391,7 +392,7 @@ dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream);
 dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o);
 dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& dst, dyna_range tr, dyna_range lr,
                           int32_t chunk_tokens, bool unchecked, bool* empty, std::vector<Span>& dsp,
-                          std::vector<Span>& ssp, int src_spans, bool heads_may_differ);
+                          std::vector<Span>& ssp, int src_spans, bool heads_may_differ, int32_t who = -1);
 dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D);
 Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok, int64_t run_bytes);
 size_t table_upload_bytes(const dyna_block_table& t, int64_t t1);

@@ -276,8 +276,9 @@ def _flags(pool, sender, first, n):
     return fl.numpy()[:n]
 
 
+@pytest.mark.parametrize("engine", [0, dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK])
 @pytest.mark.parametrize("host_tables", [False, True])
-def test_signalled_batch_per_request_flags(host_tables):
+def test_signalled_batch_per_request_flags(host_tables, engine):
     """Each entry of a signalled batch gets its own epoch and slot range; every chunk flag of every
     request reaches its epoch, slot ranges of one (sender, destination) are disjoint, and the rows
     match the oracle.  Two destination pools, an empty entry, ragged starts."""
@@ -308,7 +309,7 @@ def test_signalled_batch_per_request_flags(host_tables):
     migs = [(T(src, ts), T(d1 if w == 0 else d2, td), tr) for ts, td, tr, w in entries]
     migs.insert(3, (T(src, entries[0][0]), T(d1, entries[0][1]), (7, 7)))     # empty entry
     c = 96
-    x = dk.migrate_batch(migs, (0, 2), c, flags=dk.DYNA_MIGRATE_SIGNAL)
+    x = dk.migrate_batch(migs, (0, 2), c, flags=dk.DYNA_MIGRATE_SIGNAL, engine=engine, piece_bytes=4096 if engine else 0)
     infos = [dk.dyna_kv_batch_info(x, i) for i in range(len(migs))]
     dk.dyna_kv_wait(x)
     assert infos[3][2] == 0

@@ -130,8 +130,9 @@ def test_fuzz_batch(block):
         migs = [(dev_table(src, ts), dev_table(d1 if w == 0 else d2, td), tr) for ts, td, tr, w in ents]
         sig = bool(rng.integers(0, 2))
         c = int(rng.choice([16, 33, 128, 1000]))
-        kw = dict(flags=dk.DYNA_MIGRATE_SIGNAL) if sig else dict(engine=int(rng.choice([0, 1, 2, 3])),
-                                                                 piece_bytes=int(rng.choice([0, 1024, 16384])))
+        kw = dict(engine=int(rng.choice([0, 1, 2, 3])), piece_bytes=int(rng.choice([0, 1024, 16384])))
+        if sig:
+            kw["flags"] = dk.DYNA_MIGRATE_SIGNAL
         x = dk.migrate_batch(migs, (0, gs.num_layers), c, **kw)
         infos = [dk.dyna_kv_batch_info(x, j) for j in range(len(migs))] if sig else []
         dk.dyna_kv_wait(x)
