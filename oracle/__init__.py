@@ -56,6 +56,10 @@ def lib():
         L.oracle_migrate_chunked.restype = None
         L.oracle_migrate_heads.argtypes = [u8p, gp, i32p, u8p, gp, i32p, i64, i64, i64, i64, i64, i64, i64]
         L.oracle_migrate_heads.restype = None
+        L.oracle_pack.argtypes = [u8p, gp, i32p, i64, i64, i64, i64, u8p]
+        L.oracle_pack.restype = None
+        L.oracle_unpack.argtypes = [u8p, u8p, gp, i32p, i64, i64, i64, i64]
+        L.oracle_unpack.restype = None
         _lib = L
     return _lib
 
@@ -137,3 +141,31 @@ def migrate_heads(Ps: np.ndarray, gs, Ts, Pd: np.ndarray, gd, Td, token_range, l
     td, tdp = _i32(Td)
     lib().oracle_migrate_heads(_u8(Ps), ctypes.byref(geom(gs)), tsp, _u8(Pd), ctypes.byref(geom(gd)), tdp,
                                token_range[0], token_range[1], layer_range[0], layer_range[1], h0, h1, dst_head_begin)
+
+
+def pack(Ps: np.ndarray, gs, Ts, token_range, layer_range=None) -> np.ndarray:
+    """The sender half of P:556 (dyna_kv_oracle.c oracle_pack): a new buffer
+    [l - l0][kv][t - t0][row] of the source rows reached through Ts."""
+    layer_range = layer_range or (0, gs.num_layers)
+    assert Ps.nbytes == pool_bytes(gs)
+    n = token_range[1] - token_range[0]
+    out = np.zeros(max(0, (layer_range[1] - layer_range[0]) * 2 * n * gs.row_bytes), np.uint8)
+    if n > 0:
+        assert len(Ts) * gs.block_size >= token_range[1]
+    ts, tsp = _i32(Ts)
+    lib().oracle_pack(_u8(Ps), ctypes.byref(geom(gs)), tsp, token_range[0], token_range[1], layer_range[0],
+                      layer_range[1], _u8(out) if out.size else None)
+    return out
+
+
+def unpack(buf: np.ndarray, Pd: np.ndarray, gd, Td, token_range, layer_range=None) -> None:
+    """In-place: the receiver half of P:556 (dyna_kv_oracle.c oracle_unpack)."""
+    layer_range = layer_range or (0, gd.num_layers)
+    assert Pd.nbytes == pool_bytes(gd)
+    n = token_range[1] - token_range[0]
+    assert buf.nbytes == max(0, (layer_range[1] - layer_range[0]) * 2 * n * gd.row_bytes)
+    if n > 0:
+        assert len(Td) * gd.block_size >= token_range[1]
+    td, tdp = _i32(Td)
+    lib().oracle_unpack(_u8(buf) if buf.size else None, _u8(Pd), ctypes.byref(geom(gd)), tdp, token_range[0],
+                        token_range[1], layer_range[0], layer_range[1])

@@ -147,3 +147,36 @@ void oracle_migrate_heads(const uint8_t* Ps, const oracle_geom* gs, const int32_
                                Ps + oracle_logical_off(gs, Ts, l, kv, t, h, i),
                                (size_t)gs->e);
 }
+
+/* The two halves of P:556's push on their own — "once chunk k completes, its KV
+ * block is ... pushed", placement "steered on the receiver side" — as the staged
+ * transfer and the NCCL baseline carry them: the sender packs
+ * tokens [t0,t1) x layers [l0,l1) of its pool through Ts into one contiguous
+ * buffer laid out [l - l0][kv][t - t0][h][i] (reading R3, the same canonical
+ * layout as oracle_migrate_chunked's staging), the receiver places that buffer
+ * through Td.  oracle_unpack(oracle_pack(...)) is oracle_migrate. */
+void oracle_pack(const uint8_t* Ps, const oracle_geom* gs, const int32_t* Ts,
+                 int64_t t0, int64_t t1, int64_t l0, int64_t l1, uint8_t* out)
+{
+    const int64_t n = t1 - t0, H = gs->H, d = gs->d, e = gs->e;
+    for (int64_t l = l0; l < l1; ++l)
+        for (int64_t kv = 0; kv < 2; ++kv)
+            for (int64_t t = t0; t < t1; ++t)
+                for (int64_t h = 0; h < H; ++h)
+                    for (int64_t i = 0; i < d; ++i)
+                        memcpy(out + (((((l - l0) * 2 + kv) * n + (t - t0)) * H + h) * d + i) * e,
+                               Ps + oracle_logical_off(gs, Ts, l, kv, t, h, i), (size_t)e);
+}
+
+void oracle_unpack(const uint8_t* in, uint8_t* Pd, const oracle_geom* gd, const int32_t* Td,
+                   int64_t t0, int64_t t1, int64_t l0, int64_t l1)
+{
+    const int64_t n = t1 - t0, H = gd->H, d = gd->d, e = gd->e;
+    for (int64_t l = l0; l < l1; ++l)
+        for (int64_t kv = 0; kv < 2; ++kv)
+            for (int64_t t = t0; t < t1; ++t)
+                for (int64_t h = 0; h < H; ++h)
+                    for (int64_t i = 0; i < d; ++i)
+                        memcpy(Pd + oracle_logical_off(gd, Td, l, kv, t, h, i),
+                               in + (((((l - l0) * 2 + kv) * n + (t - t0)) * H + h) * d + i) * e, (size_t)e);
+}

@@ -398,3 +398,47 @@ def test_heads_pins_detect_mutants():
             src = S[0, :, ts[t // 2], t % 2, a:b] if a < b else S[0, :, ts[t // 2], t % 2, [2, 1]]
             D[0, :, td[t // 2], t % 2, c:d_] = src
         assert not np.array_equal(D.reshape(-1), good)
+
+
+# ---------------------------------------------------------------- pack / unpack (P:556's two halves)
+def test_pack_brute_force_tiny_pools():
+    """oracle.pack == the logical tensor materialised by numpy fancy indexing (independent
+    formulation), laid out [l - l0][kv][t - t0][row]; unpack(pack) == migrate; and
+    oracle_unpack writes exactly what np_reference writes from the same buffer."""
+    rng = np.random.default_rng(11)
+    n_cases = 0
+    for gs, gd in _tiny_geoms():
+        Ps, Pd0 = pools(gs, gd, seed=n_cases + 5)
+        row = gs.row_bytes
+        S = Ps.reshape(gs.num_layers, 2, gs.num_blocks, gs.block_size, row)
+        for s in range(0, 9, 2):
+            ns, nd = kvgen.blocks_needed(s, gs.block_size), kvgen.blocks_needed(s, gd.block_size)
+            if ns > 6 or nd > 6:
+                continue
+            ts = rng.choice(6, ns, replace=True).astype(np.int32)
+            td = rng.permutation(6)[:nd].astype(np.int32)
+            t0 = int(rng.integers(0, s + 1))
+            for lr in ((0, gs.num_layers), (gs.num_layers - 1, gs.num_layers)):
+                buf = oracle.pack(Ps, gs, ts, (t0, s), lr)
+                t = np.arange(t0, s)
+                want = S[lr[0]:lr[1], :, ts[t // gs.block_size], t % gs.block_size, :] if len(t) else \
+                    np.zeros((lr[1] - lr[0], 2, 0, row), np.uint8)
+                assert np.array_equal(buf, np.ascontiguousarray(want).reshape(-1)), (gs, s, t0, lr)
+                a, b = Pd0.copy(), Pd0.copy()
+                oracle.unpack(buf, a, gd, td, (t0, s), lr)
+                oracle.migrate(Ps, gs, ts, b, gd, td, (t0, s), lr)
+                assert np.array_equal(a, b)
+                n_cases += 1
+    assert n_cases > 150
+
+
+def test_pack_identity_table_is_slab_concatenation():
+    """Identity table, block-aligned range: the packed buffer is each (l, kv) slab's first
+    s rows, concatenated (a plain memcpy per slab)."""
+    g = TOY.with_(num_blocks=16)
+    Ps, _ = pools(g, g, seed=31)
+    s = 5 * g.block_size
+    buf = oracle.pack(Ps, g, kvgen.contiguous_table(0, 5), (0, s))
+    slab, run = g.num_blocks * g.block_size * g.row_bytes, s * g.row_bytes
+    want = np.concatenate([Ps[lk * slab: lk * slab + run] for lk in range(g.num_layers * 2)])
+    assert np.array_equal(buf, want)
