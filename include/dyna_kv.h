@@ -38,6 +38,7 @@
  *   decode-side      dyna_kv_chunkstream_* (chunks pushed as the tokens are produced)
  *   receiver-steered dyna_kv_channel_* + dyna_kv_push / _place (and _heads forms)
  *   TP resharding    dyna_kv_migrate_heads, dyna_kv_push_heads / _place_heads
+ *   halves           dyna_kv_pack / _unpack (source rows -> contiguous buffer -> destination rows)
  *   selection        dyna_kv_calib_set / _get (the measured AUTO table)
  *
  * Errors: every call returns a dyna_status; negative values are errors and
@@ -276,6 +277,26 @@ DYNA_API dyna_status dyna_kv_chunkstream_info(dyna_kv_chunkstream_t s, uint64_t*
                                               int32_t* num_pushed);
 /* Wait for every pushed chunk, free the stream; returns the first deferred error. */
 DYNA_API dyna_status dyna_kv_chunkstream_finish(dyna_kv_chunkstream_t s);
+
+/* The push's two halves as calls of their own (§4.3 P:556:
+ * the sender packs the chunk, the receiver places it through its own table), for callers
+ * that carry the bytes between the two themselves — e.g. the NCCL send/recv baseline
+ * or a host/RDMA hop.  The buffer is contiguous device memory readable and
+ * writable from the pool's device, 16-B aligned, laid out [l - l0][kv][t - t0][row]
+ * (row = H*d*e bytes; reading R3), at least (l1-l0)*2*(t1-t0)*row bytes.
+ *   dyna_kv_pack    rows of `src` for token_range x layer_range (through its table) -> buf
+ *   dyna_kv_unpack  buf -> rows of `dst` (through its table); nothing else changes
+ * Enqueued on `stream` (the pool's device); opts select the engine / SM budget like
+ * dyna_kv_migrate_ex (no per-chunk flags: DYNA_EINVAL; no staged variant: DYNA_ENOTSUP).
+ * unpack's table follows the destination rules of dyna_block_table (host ids, or
+ * DYNA_MIGRATE_UNCHECKED).  Errors and completion as dyna_kv_migrate_ex; an empty range
+ * enqueues nothing. */
+DYNA_API dyna_status dyna_kv_pack(dyna_block_table src, dyna_range token_range, dyna_range layer_range,
+                                  void* buf, uint64_t buf_bytes, struct CUstream_st* stream,
+                                  const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
+DYNA_API dyna_status dyna_kv_unpack(const void* buf, uint64_t buf_bytes, dyna_block_table dst,
+                                    dyna_range token_range, dyna_range layer_range, struct CUstream_st* stream,
+                                    const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
 
 /* Many migrations in ONE kernel launch (a batch of short
  * requests, e.g. configs[2]'s 64-request skewed batch).  Every non-empty entry

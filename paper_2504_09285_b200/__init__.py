@@ -46,7 +46,7 @@ EXPORTS = (
     "dyna_kv_push", "dyna_kv_place", "dyna_kv_channel_set_timeout", "dyna_kv_ready_cancel",
     "dyna_kv_migrate_heads", "dyna_kv_batch_info", "dyna_kv_push_heads", "dyna_kv_place_heads",
     "dyna_kv_chunkstream_open", "dyna_kv_chunkstream_produced", "dyna_kv_chunkstream_close",
-    "dyna_kv_chunkstream_info", "dyna_kv_chunkstream_finish",
+    "dyna_kv_chunkstream_info", "dyna_kv_chunkstream_finish", "dyna_kv_pack", "dyna_kv_unpack",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -142,6 +142,10 @@ def _load():
         "dyna_kv_push": (st, [dyna_block_table, dyna_range, dyna_range, ctypes.c_int32, vp, vp, p(vp)]),
         "dyna_kv_place": (st, [vp, dyna_block_table, dyna_range, dyna_range, ctypes.c_int32, vp, p(dyna_kv_opts),
                                p(vp)]),
+        "dyna_kv_pack": (st, [dyna_block_table, dyna_range, dyna_range, vp, ctypes.c_uint64, vp, p(dyna_kv_opts),
+                              p(vp)]),
+        "dyna_kv_unpack": (st, [vp, ctypes.c_uint64, dyna_block_table, dyna_range, dyna_range, vp, p(dyna_kv_opts),
+                                p(vp)]),
         "dyna_kv_wait": (st, [vp]),
         "dyna_kv_query": (st, [vp]),
         "dyna_kv_stream_wait": (st, [vp, vp]),
@@ -372,6 +376,24 @@ def dyna_kv_place_heads(ch: int, dst: dyna_block_table, token_range, layer_range
     _check(lib.dyna_kv_place_heads(ctypes.c_void_p(ch), dst, dyna_range(*token_range), dyna_range(*layer_range),
                                    dst_head_begin, num_heads, chunk_tokens, ctypes.c_void_p(stream),
                                    ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_pack(src: dyna_block_table, token_range, layer_range, buf_ptr: int, buf_bytes: int, stream: int = 0,
+                 opts: dyna_kv_opts | None = None) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_pack(src, dyna_range(*token_range), dyna_range(*layer_range), ctypes.c_void_p(buf_ptr),
+                            buf_bytes, ctypes.c_void_p(stream), ctypes.byref(opts) if opts is not None else None,
+                            ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_unpack(buf_ptr: int, buf_bytes: int, dst: dyna_block_table, token_range, layer_range, stream: int = 0,
+                   opts: dyna_kv_opts | None = None) -> int:
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_unpack(ctypes.c_void_p(buf_ptr), buf_bytes, dst, dyna_range(*token_range),
+                              dyna_range(*layer_range), ctypes.c_void_p(stream),
+                              ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
     return out.value
 
 

@@ -569,6 +569,100 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
   return DYNA_OK;
 }
 
+// ---------------------------------------------------------------- pack / unpack (K1 / K3 as calls)
+// One side of the push against a caller's contiguous buffer [l - l0][kv][t - t0][row]:
+// pack = paged source rows -> buffer (the staged variant's K1 gather), unpack = buffer ->
+// paged destination rows (K3 scatter).  Same kernels and engine choice as a migration.
+static dyna_status pack_impl(bool to_buf, dyna_block_table t, dyna_range tr, dyna_range lr, char* buf,
+                             uint64_t buf_bytes, struct CUstream_st* stream_, const dyna_kv_opts* opts,
+                             dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  dyna_kv_opts o{};
+  dyna_status r = check_opts(opts, &o);
+  if (r) return r;
+  if (o.flags & (DYNA_MIGRATE_SIGNAL | DYNA_READY_PER_LAYER))
+    return fail(DYNA_EINVAL, "pack / unpack: no per-chunk flags or ready boards");
+  if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "pack / unpack: one kernel, no staged variant");
+  if (!t.pool) return fail(DYNA_EINVAL, "NULL pool");
+  dyna_kv_pool* P = t.pool;
+  const dyna_kv_pool_desc& g = P->desc;
+  if (lr.begin < 0 || lr.begin > lr.end || lr.end > g.num_layers) return fail(DYNA_ERANGE, "bad layer range");
+  if (tr.begin < 0 || tr.begin > tr.end || tr.end >= (int64_t(1) << 31)) return fail(DYNA_ERANGE, "bad token range");
+  const int64_t n = tr.end - tr.begin, lm = lr.end - lr.begin;
+  if (n == 0 || lm == 0) {
+    *out = empty_xfer(P);
+    return DYNA_OK;
+  }
+  const uint64_t need = (uint64_t)lm * 2 * n * P->row;
+  if (!buf || buf_bytes < need)
+    return fail(DYNA_EINVAL, "buffer of %llu B < the %llu B the range needs", (unsigned long long)buf_bytes,
+                (unsigned long long)need);
+  if (reinterpret_cast<uintptr_t>(buf) % 16) return fail(DYNA_EINVAL, "buffer not 16-B aligned");
+  if (tr.end > t.len * g.block_size) return fail(DYNA_ERANGE, "token range exceeds the block table");
+  if (!t.block_ids && !t.host_block_ids) return fail(DYNA_EINVAL, "a block table has neither device nor host block ids");
+  if (!to_buf && !(o.flags & DYNA_MIGRATE_UNCHECKED) && !t.host_block_ids)
+    return fail(DYNA_EINVAL, "destination aliasing (reading R7) is checked on the host: give the destination "
+                             "table's host_block_ids, or pass DYNA_MIGRATE_UNCHECKED");
+  if (t.host_block_ids) {
+    std::vector<Span> sp, none;
+    if ((r = table_spans(t, tr.begin, tr.end, sp, -1))) return r;
+    if (!to_buf && (r = check_alias(sp, none))) return r;
+  }
+  if (!err_word()) return fail(DYNA_ECUDA, "no error word");
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  Choice ch = choose(o, P->row, 0, n, std::min<int64_t>(g.block_size, n) * P->row);
+  DeviceGuard guard(P->dev);
+  RingLease lease(P->dev);
+  const int32_t* ids = t.block_ids;
+  if (!ids) {
+    char *base = nullptr, *h = nullptr;
+    const size_t tb = table_upload_bytes(t, tr.end);
+    if ((r = lease.reserve(tb, &base, &h, stream))) return r;
+    std::memcpy(h, t.host_block_ids, tb);
+    if ((r = lease.copy(stream))) return r;
+    ids = reinterpret_cast<const int32_t*>(base);
+  }
+  dyna_kv_xfer* x = nullptr;
+  if ((r = new_xfer(P->dev, g.instance, stream, &x))) return r;
+  x->variant = DYNA_VARIANT_FUSED;
+  x->engine = ch.engine;
+  x->piece = ch.piece;
+  x->stages = ch.engine != DYNA_ENGINE_VEC ? ch.stages : 0;
+  x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
+  const uint64_t launches0 = g_launches.load();
+  // one chunk of n tokens: the linear side's layout is [l - l0][kv][t - t0][row]
+  Plan p = to_buf ? make_plan(paged(P, ids), linear(buf), P->row, tr.begin, tr.end, (int)lr.begin, (int)lm, n,
+                              g.block_size, ch.piece)
+                  : make_plan(linear(buf), paged(P, ids), P->row, tr.begin, tr.end, (int)lr.begin, (int)lm, n,
+                              g.block_size, ch.piece);
+  p.err = x->err;
+  r = launch_copy(p, ch.engine, o.max_ctas, ch.stages, ch.unroll, P->dev, stream, o.schedule);
+  if (!r) r = lease.finish(stream);
+  if (r) {
+    delete x;
+    return r;
+  }
+  x->launches = (int32_t)(g_launches.load() - launches0);
+  if ((r = record_completion(x, P->dev, stream))) {
+    delete x;
+    return r;
+  }
+  *out = x;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_pack(dyna_block_table src, dyna_range tr, dyna_range lr, void* buf, uint64_t buf_bytes,
+                         struct CUstream_st* stream, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
+  return pack_impl(true, src, tr, lr, static_cast<char*>(buf), buf_bytes, stream, opts, out);
+}
+
+dyna_status dyna_kv_unpack(const void* buf, uint64_t buf_bytes, dyna_block_table dst, dyna_range tr, dyna_range lr,
+                           struct CUstream_st* stream, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
+  return pack_impl(false, dst, tr, lr, const_cast<char*>(static_cast<const char*>(buf)), buf_bytes, stream, opts,
+                   out);
+}
+
 dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna_range lr, int32_t chunk_tokens,
                                   struct CUstream_st* stream_, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
   if (!out) return fail(DYNA_EINVAL, "NULL out");
