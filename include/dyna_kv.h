@@ -310,8 +310,10 @@ DYNA_API dyna_status dyna_kv_unpack(const void* buf, uint64_t buf_bytes, dyna_bl
  * Per-chunk signalling (opts->flags & DYNA_MIGRATE_SIGNAL; VEC engine): every
  * entry gets its own epoch and a disjoint range of inbox slots of its
  * (sender, destination pool) — see dyna_kv_batch_info — so each request's
- * r^beta can start as soon as its own chunks landed.  Each entry's chunks must
- * fit in DYNA_MAX_CHUNKS (DYNA_ERANGE otherwise). */
+ * r^beta can start as soon as its own chunks landed.  The signalled chunks of
+ * one batch from one sender into one destination pool must fit in
+ * DYNA_MAX_CHUNKS (DYNA_ERANGE otherwise): the entries of one launch never
+ * share a slot. */
 #define DYNA_MAX_BATCH 16384
 typedef struct {
     dyna_block_table src, dst;
@@ -479,8 +481,9 @@ DYNA_API dyna_status dyna_kv_stream_wait(dyna_kv_xfer_t xfer, struct CUstream_st
  * inbox slot [sender][first_slot + k] holds a value >= epoch.  Concurrent
  * signalled migrations (any streams, any threads, chunk streams included) use
  * disjoint slots; a slot is reused only after DYNA_MAX_CHUNKS further chunks
- * were reserved by the same sender for the same pool, and flags are raised
- * with an atomic max (never lowered).  Epochs and slots are keyed on the
+ * were reserved by the same sender for the same pool (a migration must have
+ * completed by then: its per-slot byte counters are reused too), and flags
+ * are raised with an atomic max (never lowered).  Epochs and slots are keyed on the
  * destination pool's identity, which an IPC export carries, and start above
  * every flag already in the row, so a restarted sender or a re-imported pool
  * never reuses an epoch.  Any pointer may be NULL. */

@@ -740,6 +740,18 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   if ((r = new_xfer(S0->dev, S0->desc.instance, stream, &x))) return r;
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
   if (signal) {  // each entry: its own epoch and slot range of its (sender, destination pool)
+    // the entries of one launch must not share slots (their counters live there): at most
+    // DYNA_MAX_CHUNKS signalled chunks per (sender, destination pool) in one batch
+    std::map<std::pair<int, uint64_t>, int64_t> per_row;
+    for (int32_t i : live) {
+      int64_t& tot = per_row[{migs[i].src.pool->desc.instance, migs[i].dst.pool->uid}];
+      tot += (migs[i].token_range.end - migs[i].token_range.begin + chunk_tokens - 1) / chunk_tokens;
+      if (tot > DYNA_MAX_CHUNKS) {
+        delete x;
+        return fail(DYNA_ERANGE, "batch: more than DYNA_MAX_CHUNKS (%d) signalled chunks from sender %d into one "
+                                 "destination pool", DYNA_MAX_CHUNKS, migs[i].src.pool->desc.instance);
+      }
+    }
     x->batch.assign(n, dyna_kv_xfer::BatchEntry{});
     for (int32_t i : live) {
       dyna_kv_pool *S = migs[i].src.pool, *D = migs[i].dst.pool;

@@ -188,8 +188,8 @@ def test_cuda_graph_capture_and_replay():
 
 
 def test_chunk_stream_prefill_then_decode():
-    """ChunkStream: prefill chunks + decoded tokens (s > P) pushed chunk by chunk; bytes match the oracle."""
-    from paper_2504_09285_b200.stream import ChunkStream
+    """Native chunk stream: prefill chunks + decoded tokens (s > P) pushed chunk by chunk in
+    scheduler-sized steps; the last chunk is the partial one closed at the end; bytes match the oracle."""
     g = Geom(3, 8, 128, 2, 16, 200)
     hs, hd = kvgen.fill_bytes(91, g.pool_bytes), kvgen.fill_bytes(92, g.pool_bytes)
     ts, td = kvgen.table_pair(93, 1500, g, g)
@@ -198,16 +198,14 @@ def test_chunk_stream_prefill_then_decode():
     oracle.migrate(hs, g, ts, want, g, td, (0, P + decoded))
     src, dst = pool_from_host(g, hs), pool_from_host(g, hd)
     st, dt = dev_table(src, ts), dev_table(dst, td)
-    stream = torch.cuda.current_stream().cuda_stream
-    cs = ChunkStream(256, lambda tr: dk.dyna_kv_migrate_ex(st, dt, tr, (0, 3), tr[1] - tr[0], stream, None))
-    for n in (256, 256, 256, 256, 76):        # prefill of P = 1100 in scheduler-sized steps
-        cs.produced(n)
-    for _ in range(decoded):                  # alpha decodes past the prompt
-        cs.produced(1)
-    cs.close()
-    for x in cs.handles:
-        dk.dyna_kv_wait(x)
-    assert cs.chunks[-1] == (1024, P + decoded)
+    cs = dk.dyna_kv_chunkstream_open(st, dt, 0, (0, 3), 256, torch.cuda.current_stream().cuda_stream, None)
+    pushed = [dk.dyna_kv_chunkstream_produced(cs, n) for n in (256, 256, 256, 256, 76)]   # prefill of P = 1100
+    pushed += [dk.dyna_kv_chunkstream_produced(cs, 1) for _ in range(decoded)]          # alpha decodes on
+    assert sum(pushed) == 4
+    assert dk.dyna_kv_chunkstream_close(cs) == 1                                        # [1024, 1137)
+    info = dk.dyna_kv_chunkstream_info(cs)
+    assert info["pushed_end"] == P + decoded and info["num_pushed"] == 5
+    dk.dyna_kv_chunkstream_finish(cs)
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
 
 
@@ -333,15 +331,22 @@ def test_signalled_batch_limits_and_errors():
     g = Geom(1, 2, 64, 2, 16, 4200)
     src, dst = pool_filled(g, 1), pool_filled(g, 2)
     ts, td = kvgen.table_pair(1, 65536, g, g)
-    with pytest.raises(dk.DynaKVError) as e:        # 2 x 4096 chunks into one destination > DYNA_MAX_CHUNKS
+    with pytest.raises(dk.DynaKVError) as e:        # 2 x 4096 chunks into one destination: slots would be shared
         dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, 4096)),
                           (dev_table(src, ts), dev_table(dst, td), (4096, 8192))], (0, 1), 1,
                          flags=dk.DYNA_MIGRATE_SIGNAL)
     assert e.value.status == dk.DYNA_ERANGE
-    with pytest.raises(dk.DynaKVError) as e:
-        dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, 10))], (0, 1), 4,
-                         flags=dk.DYNA_MIGRATE_SIGNAL, engine=dk.DYNA_ENGINE_BULK)
-    assert e.value.status == dk.DYNA_ENOTSUP
+    # 2048 + 2048 one-token chunks fit: disjoint slot ranges, every flag raised (BULK ring, small pieces)
+    x = dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, 2048)),
+                          (dev_table(src, ts), dev_table(dst, td), (4096, 6144))], (0, 1), 1,
+                         flags=dk.DYNA_MIGRATE_SIGNAL, engine=dk.DYNA_ENGINE_BULK, piece_bytes=256)
+    infos = [dk.dyna_kv_batch_info(x, i) for i in range(2)]
+    dk.dyna_kv_wait(x)
+    (e0, f0, n0, snd), (e1, f1, n1, _) = infos
+    assert n0 == n1 == 2048 and (f0 + n0 <= f1 or f1 + n1 <= f0)
+    assert (_flags(dst, snd, f0, n0) == e0).all() and (_flags(dst, snd, f1, n1) == e1).all()
+    assert torch_rows_equal(src, ts, dst, td, (0, 2048), (0, 1))
+    assert torch_rows_equal(src, ts, dst, td, (4096, 6144), (0, 1))
     x = dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, 10))], (0, 1), 4)
     with pytest.raises(dk.DynaKVError) as e:         # not a signalled batch
         dk.dyna_kv_batch_info(x, 0)
