@@ -592,6 +592,10 @@ def run_dyna(args, rank, world, local_rank):
                 extra["target_4prime"] = {"per_pair_GBps_needed": 720.0, "chunk_ms_needed": 0.7457,
                                           "chunk_ms": total_ms / args.steps}
         cfg_extra["resolved_plan"] = plan_used
+        eng = {dk.DYNA_ENGINE_VEC: "VEC", dk.DYNA_ENGINE_BULK: "BULK", dk.DYNA_ENGINE_BULK_WS: "BULK"}
+        roof["engine"] = eng.get(plan_used["engine"], str(plan_used["engine"]))
+        if roof["engine"] == "VEC":
+            roof["kernel"] = roof["kernel"].replace("k_copy_ring<false,", "k_copy_lanes<8, false,")
         line = make_line(world=world, steps=args.steps, warmup=args.warmup, workload=workload,
                          payload_per_rank=payload_all / world, tokens_per_rank=tokens_all / world,
                          total_ms=total_ms, roofline=roof, e2e=e2e_line, launches=launches, clocks=clk,

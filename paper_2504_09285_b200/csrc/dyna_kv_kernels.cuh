@@ -33,6 +33,11 @@
 #define DYNA_VEC_MINB 3  // resident 256-thread CTAs per SM the VEC engine (U <= 8) is compiled for
 #endif
 
+#ifndef DYNA_LANES_MINB
+#define DYNA_LANES_MINB 2  // resident 256-thread CTAs per SM of k_copy_lanes (2: up to 128 registers, no spills;
+                           // precomputed-item micro-benchmark: 2 CTAs/SM 3100 vs 3 CTAs/SM 2900 GB/s)
+#endif
+
 #ifndef DYNA_MAIL_SLEEP
 #define DYNA_MAIL_SLEEP 0  // accountant poll back-off (ns); 0 = spin
 #endif
@@ -376,7 +381,9 @@ __device__ __forceinline__ void warp_copy_rows(const char* __restrict__ src, cha
 
 // Head-sliced fused copy (dyna_kv_migrate_heads): one warp per item, static
 // round-robin over a balanced persistent grid, per-(warp, chunk) signalling as
-// in k_copy_vec.
+// in k_copy_vec.  The warp decodes its next 32 items at once, one per lane (the
+// divisions and block-table loads of decode_item_sliced run in parallel, their
+// latency paid once per 32 items), then copies them one after the other.
 template <int U, bool SIGNAL>
 __global__ void __launch_bounds__(256, 3) k_copy_rows(const Plan p) {
   pdl_enter();
@@ -385,24 +392,89 @@ __global__ void __launch_bounds__(256, 3) k_copy_rows(const Plan p) {
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int32_t cur_k = -1;
   uint32_t cur_acc = 0;
-  for (int64_t item = warp; item < p.n_items; item += nwarps) {
-    const SItem it = decode_item_sliced(p, item);
-    if (SIGNAL && it.acc && it.k != cur_k) {
-      if (cur_acc) {
-        fence_for(p);
-        __syncwarp();
-        if (lane == 0) account_chunk(p, cur_k, cur_acc);
+  for (int64_t m = 0; warp + m * nwarps < p.n_items; m += 32) {
+    const int64_t gi = warp + (m + lane) * nwarps;
+    SItem mine{nullptr, nullptr, 0u, 0u, 0, 0};
+    if (gi < p.n_items) mine = decode_item_sliced(p, gi);
+    for (int j = 0; j < 32 && warp + (m + j) * nwarps < p.n_items; ++j) {
+      const char* isrc = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, (unsigned long long)mine.src, j));
+      char* idst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, (unsigned long long)mine.dst, j));
+      const uint32_t rows = __shfl_sync(0xffffffffu, mine.rows, j);
+      const uint32_t acc = __shfl_sync(0xffffffffu, mine.acc, j);
+      const int32_t k = __shfl_sync(0xffffffffu, mine.k, j);
+      if (SIGNAL && acc && k != cur_k) {
+        if (cur_acc) {
+          fence_for(p);
+          __syncwarp();
+          if (lane == 0) account_chunk(p, cur_k, cur_acc);
+        }
+        cur_k = k;
+        cur_acc = 0;
       }
-      cur_k = it.k;
-      cur_acc = 0;
+      if (rows) warp_copy_rows<U>(isrc, idst, rows, p, lane);
+      if (SIGNAL) cur_acc += acc;
     }
-    if (it.rows) warp_copy_rows<U>(it.src, it.dst, it.rows, p, lane);
-    if (SIGNAL) cur_acc += it.acc;
   }
   if (SIGNAL && cur_acc) {
     fence_for(p);
     __syncwarp();
     if (lane == 0) account_chunk(p, cur_k, cur_acc);
+  }
+}
+
+// VEC engine with warp-cooperative decode (static round-robin schedule, no ready board):
+// the warp's next 32 items are decoded at once, one per lane, then copied one after the
+// other with the fields broadcast by shuffles.  Same per-(warp, chunk) signalling as
+// k_copy_vec; batches carry each item's plan (per-request flags).
+template <int U, bool SIGNAL, class Src>
+__global__ void __launch_bounds__(256, DYNA_LANES_MINB) k_copy_lanes(const Src src) {
+  pdl_enter();
+  constexpr bool kBatch = std::is_same<Src, BatchSource>::value;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_items = src.total();
+  int32_t cur_k = -1;
+  const Plan* cur_p = nullptr;
+  unsigned long long cur_acc = 0;
+  for (int64_t m = 0; warp + m * nwarps < n_items; m += 32) {
+    const int64_t gi = warp + (m + lane) * nwarps;
+    Item mine{nullptr, nullptr, 0u, 0u, 0, 0};
+    const Plan* mp = nullptr;
+    if (gi < n_items) {
+      int64_t item = gi;
+      const Plan& ip = src.locate(item);
+      if (kBatch) mp = &ip;
+      mine = decode_item(ip, item);
+    }
+    for (int j = 0; j < 32 && warp + (m + j) * nwarps < n_items; ++j) {
+      const char* isrc = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, (unsigned long long)mine.src, j));
+      char* idst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, (unsigned long long)mine.dst, j));
+      const uint32_t n = __shfl_sync(0xffffffffu, mine.n, j);
+      const uint32_t acc = __shfl_sync(0xffffffffu, mine.acc, j);
+      const int32_t k = __shfl_sync(0xffffffffu, mine.k, j);
+      const Plan* pj = kBatch ? reinterpret_cast<const Plan*>(__shfl_sync(0xffffffffu, (unsigned long long)mp, j))
+                              : nullptr;
+      if (SIGNAL && acc && (k != cur_k || (kBatch && pj != cur_p))) {
+        if (cur_acc) {
+          const Plan& cp = kBatch ? *cur_p : src.locate_signal();
+          fence_for(cp);
+          __syncwarp();
+          if (lane == 0) account_chunk(cp, cur_k, cur_acc);
+        }
+        cur_k = k;
+        if (kBatch) cur_p = pj;
+        cur_acc = 0;
+      }
+      if (n) warp_copy<U>(isrc, idst, n, lane);
+      if (SIGNAL) cur_acc += acc;
+    }
+  }
+  if (SIGNAL && cur_acc) {
+    const Plan& cp = kBatch ? *cur_p : src.locate_signal();
+    fence_for(cp);
+    __syncwarp();
+    if (lane == 0) account_chunk(cp, cur_k, cur_acc);
   }
 }
 

@@ -40,6 +40,12 @@ void preload_kernels() {
       (const void*)k_copy_ring<false, SingleSource>, (const void*)k_copy_ring<true, SingleSource>,
       (const void*)k_copy_ring<true, SingleSource, true>, (const void*)k_copy_ring<false, BatchSource>,
       (const void*)k_copy_ring<true, BatchSource>, (const void*)k_copy_ring<true, BatchSource, true>,
+      (const void*)k_copy_lanes<4, false, SingleSource>, (const void*)k_copy_lanes<4, true, SingleSource>,
+      (const void*)k_copy_lanes<8, false, SingleSource>, (const void*)k_copy_lanes<8, true, SingleSource>,
+      (const void*)k_copy_lanes<16, false, SingleSource>, (const void*)k_copy_lanes<16, true, SingleSource>,
+      (const void*)k_copy_lanes<4, false, BatchSource>, (const void*)k_copy_lanes<4, true, BatchSource>,
+      (const void*)k_copy_lanes<8, false, BatchSource>, (const void*)k_copy_lanes<8, true, BatchSource>,
+      (const void*)k_copy_lanes<16, false, BatchSource>, (const void*)k_copy_lanes<16, true, BatchSource>,
   };
   for (const void* k : ks) cudaFuncGetAttributes(&a, k);
   // Allow the BULK rings any dynamic shared memory the device offers, once, here: a
@@ -164,19 +170,19 @@ cudaError_t launch_kernel(void (*kern)(KArgs...), unsigned grid, unsigned block,
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-template <int U, bool SIG, class Src>
-int vec_occupancy() {
-  static std::map<int, int> cache;  // per device
+// Resident 256-thread CTAs per SM of a VEC-family kernel (cached per device and kernel).
+int vec_occupancy(const void* kern) {
+  static std::map<std::pair<int, const void*>, int> cache;
   static std::mutex mu;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
-  auto it = cache.find(dev);
+  auto it = cache.find({dev, kern});
   if (it != cache.end()) return it->second;
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_copy_vec<U, SIG, Src>, kVecThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kVecThreads, 0);
   if (occ <= 0) occ = 1;
-  cache[dev] = occ;
+  cache[{dev, kern}] = occ;
   return occ;
 }
 
@@ -196,16 +202,31 @@ unsigned long long* sched_slot(DevInfo* di, int schedule) {
   return di->sched + 2 * (size_t)k;
 }
 
+// VEC launches: the warp-cooperative-decode kernel (k_copy_lanes) for the default static
+// schedule; k_copy_vec for dynamic scheduling (DYNA_KV_LANES=0 restores it for static too).
+bool lanes_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYNA_KV_LANES");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <int U, bool SIG, class Src>
 void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cudaStream_t st,
                 unsigned long long* sched) {
-  const int occ = vec_occupancy<U, SIG, Src>();
+  const bool lanes = !sched && lanes_enabled();
+  const int occ = vec_occupancy(lanes ? (const void*)k_copy_lanes<U, SIG, Src>
+                                      : (const void*)k_copy_vec<U, SIG, Src, false>);
   constexpr int wpc = kVecThreads / 32;  // warps per CTA
   int64_t max_ctas = (int64_t)sms * occ;
   if (max_grid > 0) max_ctas = std::min<int64_t>(max_ctas, max_grid);
   const int64_t warps = balanced_workers(n_items, max_ctas * wpc);
   const int64_t grid = (warps + wpc - 1) / wpc;
-  launch_kernel(k_copy_vec<U, SIG, Src, false>, (unsigned)grid, kVecThreads, 0, st, src, sched);
+  if (lanes)
+    launch_kernel(k_copy_lanes<U, SIG, Src>, (unsigned)grid, kVecThreads, 0, st, src);
+  else
+    launch_kernel(k_copy_vec<U, SIG, Src, false>, (unsigned)grid, kVecThreads, 0, st, src, sched);
 }
 
 // Dynamic shared memory a kernel may use: the opt-in maximum minus the kernel's own
