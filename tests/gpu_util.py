@@ -16,7 +16,8 @@ def pool_from_host(geom, host: np.ndarray, device: int = 0, instance: int = 0) -
 def pool_filled(geom, seed: int, device: int = 0, instance: int = 0) -> dk.Pool:
     """Pool filled on the device with the kvgen stream of `seed` (dyna_kv_debug_fill)."""
     p = dk.Pool(geom, device, instance)
-    dk.dyna_kv_debug_fill(p.tensor.data_ptr(), p.tensor.numel(), seed, 0, torch.cuda.current_stream().cuda_stream)
+    dk.dyna_kv_debug_fill(p.tensor.data_ptr(), p.tensor.numel(), seed, 0,
+                          torch.cuda.current_stream(device).cuda_stream)
     return p
 
 
