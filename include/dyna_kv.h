@@ -37,7 +37,8 @@
  *                    cancellable)
  *   decode-side      dyna_kv_chunkstream_* (chunks pushed as the tokens are produced)
  *   receiver-steered dyna_kv_channel_* + dyna_kv_push / _place (and _heads forms)
- *   TP resharding    dyna_kv_migrate_heads, dyna_kv_push_heads / _place_heads
+ *   TP resharding    dyna_kv_migrate_heads, dyna_kv_reshard (all rank pairs, one launch),
+ *                    dyna_kv_push_heads / _place_heads
  *   halves           dyna_kv_pack / _unpack (source rows -> contiguous buffer -> destination rows)
  *   selection        dyna_kv_calib_set / _get (the measured AUTO table)
  *
@@ -250,6 +251,28 @@ DYNA_API dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_tabl
                                            dyna_range src_heads, int32_t dst_head_begin,
                                            int32_t chunk_tokens, struct CUstream_st* stream,
                                            const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
+
+/* A whole TP reshard of one request in ONE launch (reading R14): n
+ * head-sliced migrations (e.g. the rank pairs of dist.tp_reshard_plan) over the same
+ * token_range, layer_range and chunk_tokens, each moving heads [src_heads) of its source rows
+ * into heads [dst_head_begin, ...) of its destination rows, exactly as dyna_kv_migrate_heads
+ * would.  All entries move slices of one size (n_heads*d*e) over one block grid
+ * (gcd(bs_src, bs_dst)) and have their sources on the launching device.  Their work items
+ * are interleaved, so the slices of one token row move together (one launch instead of n,
+ * and the DRAM rows of a token are touched once, not once per call).  Destination aliasing
+ * (R7) is checked per head: entries may write different heads of the same rows.  Per-chunk
+ * signalling gives every entry its own epoch and slots (dyna_kv_batch_info with the entry's
+ * index).  VEC engine, FUSED variant (DYNA_ENOTSUP otherwise); other rules as
+ * dyna_kv_migrate_batch. */
+typedef struct {
+    dyna_block_table src, dst;
+    dyna_range src_heads;
+    int32_t dst_head_begin;
+    int32_t reserved;        /* 0 */
+} dyna_kv_head_migration;
+DYNA_API dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_range token_range,
+                                     dyna_range layer_range, int32_t chunk_tokens, struct CUstream_st* stream,
+                                     const dyna_kv_opts* opts, dyna_kv_xfer_t* out);
 
 /* Chunk streams (§4.3 P:556 "once chunk k completes, its
  * KV block is immediately DMA-pushed"; decoded tokens join the open chunk,

@@ -46,7 +46,7 @@ EXPORTS = (
     "dyna_kv_push", "dyna_kv_place", "dyna_kv_channel_set_timeout", "dyna_kv_ready_cancel",
     "dyna_kv_migrate_heads", "dyna_kv_batch_info", "dyna_kv_push_heads", "dyna_kv_place_heads",
     "dyna_kv_chunkstream_open", "dyna_kv_chunkstream_produced", "dyna_kv_chunkstream_close",
-    "dyna_kv_chunkstream_info", "dyna_kv_chunkstream_finish", "dyna_kv_pack", "dyna_kv_unpack",
+    "dyna_kv_chunkstream_info", "dyna_kv_chunkstream_finish", "dyna_kv_pack", "dyna_kv_unpack", "dyna_kv_reshard",
 )
 DYNA_MAX_BATCH = 16384
 
@@ -67,6 +67,11 @@ class dyna_range(ctypes.Structure):
 
 class dyna_kv_migration(ctypes.Structure):
     _fields_ = [("src", dyna_block_table), ("dst", dyna_block_table), ("token_range", dyna_range)]
+
+
+class dyna_kv_head_migration(ctypes.Structure):
+    _fields_ = [("src", dyna_block_table), ("dst", dyna_block_table), ("src_heads", dyna_range),
+                ("dst_head_begin", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class dyna_kv_opts(ctypes.Structure):
@@ -146,6 +151,8 @@ def _load():
                               p(vp)]),
         "dyna_kv_unpack": (st, [vp, ctypes.c_uint64, dyna_block_table, dyna_range, dyna_range, vp, p(dyna_kv_opts),
                                 p(vp)]),
+        "dyna_kv_reshard": (st, [p(dyna_kv_head_migration), ctypes.c_int32, dyna_range, dyna_range, ctypes.c_int32,
+                                 vp, p(dyna_kv_opts), p(vp)]),
         "dyna_kv_wait": (st, [vp]),
         "dyna_kv_query": (st, [vp]),
         "dyna_kv_stream_wait": (st, [vp, vp]),
@@ -394,6 +401,18 @@ def dyna_kv_unpack(buf_ptr: int, buf_bytes: int, dst: dyna_block_table, token_ra
     _check(lib.dyna_kv_unpack(ctypes.c_void_p(buf_ptr), buf_bytes, dst, dyna_range(*token_range),
                               dyna_range(*layer_range), ctypes.c_void_p(stream),
                               ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_reshard(migs, token_range, layer_range, chunk_tokens: int, stream: int = 0,
+                    opts: dyna_kv_opts | None = None) -> int:
+    """migs: list of (src dyna_block_table, dst dyna_block_table, (h0, h1), dst_head_begin)."""
+    arr = (dyna_kv_head_migration * max(1, len(migs)))(
+        *[dyna_kv_head_migration(a, b, dyna_range(*hr), hd, 0) for a, b, hr, hd in migs])
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_reshard(arr, len(migs), dyna_range(*token_range), dyna_range(*layer_range), chunk_tokens,
+                               ctypes.c_void_p(stream), ctypes.byref(opts) if opts is not None else None,
+                               ctypes.byref(out)))
     return out.value
 
 

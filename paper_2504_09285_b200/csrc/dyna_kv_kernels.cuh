@@ -379,46 +379,44 @@ __device__ __forceinline__ void warp_copy_rows(const char* __restrict__ src, cha
   }
 }
 
-// Head-sliced fused copy (dyna_kv_migrate_heads): one warp per item, static
-// round-robin over a balanced persistent grid, per-(warp, chunk) signalling as
-// in k_copy_vec.  The warp decodes its next 32 items at once, one per lane (the
-// divisions and block-table loads of decode_item_sliced run in parallel, their
-// latency paid once per 32 items), then copies them one after the other.
-template <int U, bool SIGNAL>
-__global__ void __launch_bounds__(256, 3) k_copy_rows(const Plan p) {
+// Head-sliced fused copy (dyna_kv_migrate_heads, dyna_kv_reshard): one warp per item, static
+// round-robin over a balanced persistent grid, per-(warp, plan, chunk) signalling as in
+// k_copy_vec.  (A lane-parallel decode of 32 items at once, as k_copy_lanes does, measured
+// 3-7% slower here on 256-B slices: profiles/r02_reshard_lanes.json.)
+template <int U, bool SIGNAL, class Src>
+__global__ void __launch_bounds__(256, 3) k_copy_rows(const Src src) {
   pdl_enter();
+  constexpr bool kMulti = !std::is_same<Src, SingleSource>::value;
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_items = src.total();
   int32_t cur_k = -1;
+  const Plan* cur_p = nullptr;
   uint32_t cur_acc = 0;
-  for (int64_t m = 0; warp + m * nwarps < p.n_items; m += 32) {
-    const int64_t gi = warp + (m + lane) * nwarps;
-    SItem mine{nullptr, nullptr, 0u, 0u, 0, 0};
-    if (gi < p.n_items) mine = decode_item_sliced(p, gi);
-    for (int j = 0; j < 32 && warp + (m + j) * nwarps < p.n_items; ++j) {
-      const char* isrc = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, (unsigned long long)mine.src, j));
-      char* idst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, (unsigned long long)mine.dst, j));
-      const uint32_t rows = __shfl_sync(0xffffffffu, mine.rows, j);
-      const uint32_t acc = __shfl_sync(0xffffffffu, mine.acc, j);
-      const int32_t k = __shfl_sync(0xffffffffu, mine.k, j);
-      if (SIGNAL && acc && k != cur_k) {
-        if (cur_acc) {
-          fence_for(p);
-          __syncwarp();
-          if (lane == 0) account_chunk(p, cur_k, cur_acc);
-        }
-        cur_k = k;
-        cur_acc = 0;
+  for (int64_t g = warp; g < n_items; g += nwarps) {
+    int64_t item = g;
+    const Plan& p = src.locate(item);
+    const SItem it = decode_item_sliced(p, item);
+    if (SIGNAL && it.acc && (it.k != cur_k || (kMulti && &p != cur_p))) {
+      if (cur_acc) {
+        const Plan& cp = kMulti ? *cur_p : p;
+        fence_for(cp);
+        __syncwarp();
+        if (lane == 0) account_chunk(cp, cur_k, cur_acc);
       }
-      if (rows) warp_copy_rows<U>(isrc, idst, rows, p, lane);
-      if (SIGNAL) cur_acc += acc;
+      cur_k = it.k;
+      if (kMulti) cur_p = &p;
+      cur_acc = 0;
     }
+    if (it.rows) warp_copy_rows<U>(it.src, it.dst, it.rows, p, lane);
+    if (SIGNAL) cur_acc += it.acc;
   }
   if (SIGNAL && cur_acc) {
-    fence_for(p);
+    const Plan& cp = kMulti ? *cur_p : src.locate_signal();
+    fence_for(cp);
     __syncwarp();
-    if (lane == 0) account_chunk(p, cur_k, cur_acc);
+    if (lane == 0) account_chunk(cp, cur_k, cur_acc);
   }
 }
 

@@ -36,7 +36,8 @@ void preload_kernels() {
       (const void*)k_copy_bulk_ws<false, SingleSource>, (const void*)k_copy_bulk_ws<true, SingleSource>,
       (const void*)k_copy_bulk_ws<false, BatchSource>, (const void*)k_copy_bulk_ws<true, SingleSource, true>,
       (const void*)k_copy_bulk<true, SingleSource, true>,
-      (const void*)k_copy_rows<8, false>, (const void*)k_copy_rows<8, true>,
+      (const void*)k_copy_rows<8, false, SingleSource>, (const void*)k_copy_rows<8, true, SingleSource>,
+      (const void*)k_copy_rows<8, false, InterleavedSource>, (const void*)k_copy_rows<8, true, InterleavedSource>,
       (const void*)k_copy_ring<false, SingleSource>, (const void*)k_copy_ring<true, SingleSource>,
       (const void*)k_copy_ring<true, SingleSource, true>, (const void*)k_copy_ring<false, BatchSource>,
       (const void*)k_copy_ring<true, BatchSource>, (const void*)k_copy_ring<true, BatchSource, true>,
@@ -361,26 +362,29 @@ dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st, 
 }
 
 // Head-sliced fused copy: warp-per-item VEC engine over a balanced persistent grid.
-dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st) {
-  if (p.n_items == 0) return DYNA_OK;
-  if (p.n_items >= (int64_t(1) << 31)) return fail(DYNA_ERANGE, "too many work items in one launch");
+template <class Src>
+dyna_status launch_rows_src(const Src& src, int64_t n_items, bool sig, int max_ctas, int dev, cudaStream_t st) {
+  if (n_items == 0) return DYNA_OK;
+  if (n_items >= (int64_t(1) << 31)) return fail(DYNA_ERANGE, "too many work items in one launch");
   DevInfo* di = dev_info(dev);
-  const bool sig = p.counters != nullptr;
-  static const int occ[2] = {  // (thread-safe static initialisation)
-      [] { int o = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_copy_rows<8, false>, kVecThreads, 0);
-           return o > 0 ? o : 1; }(),
-      [] { int o = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_copy_rows<8, true>, kVecThreads, 0);
-           return o > 0 ? o : 1; }()};
-  const int o = occ[sig ? 1 : 0];
+  const int o = vec_occupancy(sig ? (const void*)k_copy_rows<8, true, Src> : (const void*)k_copy_rows<8, false, Src>);
   int64_t cap = (int64_t)di->sms * o;
   if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
   constexpr int wpc = kVecThreads / 32;
-  const int64_t warps = balanced_workers(p.n_items, cap * wpc);
+  const int64_t warps = balanced_workers(n_items, cap * wpc);
   const unsigned grid = (unsigned)((warps + wpc - 1) / wpc);
-  if (sig) CUDA_TRY(launch_kernel(k_copy_rows<8, true>, grid, kVecThreads, 0, st, p));
-  else CUDA_TRY(launch_kernel(k_copy_rows<8, false>, grid, kVecThreads, 0, st, p));
+  if (sig) CUDA_TRY(launch_kernel(k_copy_rows<8, true, Src>, grid, kVecThreads, 0, st, src));
+  else CUDA_TRY(launch_kernel(k_copy_rows<8, false, Src>, grid, kVecThreads, 0, st, src));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DYNA_OK;
+}
+
+dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st) {
+  return launch_rows_src(SingleSource{p}, p.n_items, p.counters != nullptr, max_ctas, dev, st);
+}
+
+dyna_status launch_rows_interleaved(const InterleavedSource& src, bool sig, int max_ctas, int dev, cudaStream_t st) {
+  return launch_rows_src(src, src.total_items, sig, max_ctas, dev, st);
 }
 
 dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev,

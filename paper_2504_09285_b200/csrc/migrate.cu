@@ -491,7 +491,6 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
   if ((r = validate_pair(src, dst, tr, lr, chunk_tokens, (o.flags & DYNA_MIGRATE_UNCHECKED) != 0, &empty, dsp, ssp,
                          0, true)))
     return r;
-  if (!empty && (r = check_alias(dsp, ssp))) return r;  // (rows, whatever their heads: conservative)
   dyna_kv_pool* S = src.pool;
   dyna_kv_pool* D = dst.pool;
   const dyna_kv_pool_desc &gs = S->desc, &gd = D->desc;
@@ -501,6 +500,9 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
     return fail(DYNA_ERANGE, "heads [%lld, %lld) of %d -> [%d, %lld) of %d", (long long)src_heads.begin,
                 (long long)src_heads.end, gs.num_kv_heads, dst_head_begin, (long long)(dst_head_begin + nh),
                 gd.num_kv_heads);
+  for (Span& x : dsp) x.h0 = dst_head_begin, x.h1 = (int32_t)(dst_head_begin + nh);  // only these heads change
+  for (Span& x : ssp) x.h0 = (int32_t)src_heads.begin, x.h1 = (int32_t)src_heads.end;
+  if (!empty && (r = check_alias(dsp, ssp))) return r;
   const int64_t head_bytes = (int64_t)gs.head_dim * gs.elem_bytes;
   if ((nh * head_bytes) % 16 || head_bytes % 16)
     return fail(DYNA_EGEOM, "head slices must be multiples of 16 bytes (d*e = %lld)", (long long)head_bytes);
@@ -661,6 +663,166 @@ dyna_status dyna_kv_unpack(const void* buf, uint64_t buf_bytes, dyna_block_table
                            struct CUstream_st* stream, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
   return pack_impl(false, dst, tr, lr, const_cast<char*>(static_cast<const char*>(buf)), buf_bytes, stream, opts,
                    out);
+}
+
+// ---------------------------------------------------------------- reshard: one request's head slices, one launch
+// Every entry moves heads [src_heads) of its source rows into heads [dst_head_begin, ...) of its
+// destination rows, for the same tokens, layers and chunking; all entries' slices have one size,
+// so their work items line up and are interleaved (InterleavedSource): the warps running side
+// by side move the different slices of the same token rows together.
+dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_range tr, dyna_range lr,
+                            int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
+                            dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  if (n < 0 || (n > 0 && !migs) || n > DYNA_MAX_BATCH) return fail(DYNA_EINVAL, "0 <= n <= DYNA_MAX_BATCH");
+  dyna_kv_opts o{};
+  dyna_status r = check_opts(opts, &o);
+  if (r) return r;
+  if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
+  if (o.variant == DYNA_VARIANT_STAGED || (o.engine && o.engine != DYNA_ENGINE_VEC))
+    return fail(DYNA_ENOTSUP, "reshard: FUSED variant, VEC engine only");
+  const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
+  const bool unchecked = (o.flags & DYNA_MIGRATE_UNCHECKED) != 0;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  std::vector<Span> dsp, ssp;
+  dyna_kv_pool* S0 = nullptr;
+  int64_t slice = -1, g = -1;
+  bool empty = true;
+  for (int32_t i = 0; i < n; ++i) {
+    const dyna_kv_head_migration& m = migs[i];
+    bool e = false;
+    const size_t d0 = dsp.size(), s0 = ssp.size();
+    if ((r = validate_pair(m.src, m.dst, tr, lr, chunk_tokens, unchecked, &e, dsp, ssp, 1, true, i))) {
+      g_err = "migration " + std::to_string(i) + ": " + g_err;
+      return r;
+    }
+    const dyna_kv_pool_desc &gs = m.src.pool->desc, &gd = m.dst.pool->desc;
+    const int64_t nh = m.src_heads.end - m.src_heads.begin;
+    if (m.src_heads.begin < 0 || nh <= 0 || m.src_heads.end > gs.num_kv_heads || m.dst_head_begin < 0 ||
+        m.dst_head_begin + nh > gd.num_kv_heads)
+      return fail(DYNA_ERANGE, "migration %d: heads [%lld, %lld) of %d -> [%d, ...) of %d", i,
+                  (long long)m.src_heads.begin, (long long)m.src_heads.end, gs.num_kv_heads, m.dst_head_begin,
+                  gd.num_kv_heads);
+    for (size_t k = d0; k < dsp.size(); ++k) dsp[k].h0 = m.dst_head_begin, dsp[k].h1 = (int32_t)(m.dst_head_begin + nh);
+    for (size_t k = s0; k < ssp.size(); ++k) ssp[k].h0 = (int32_t)m.src_heads.begin, ssp[k].h1 = (int32_t)m.src_heads.end;
+    const int64_t he = (int64_t)gs.head_dim * gs.elem_bytes;
+    if (he % 16) return fail(DYNA_EGEOM, "head slices must be multiples of 16 bytes (d*e = %lld)", (long long)he);
+    const int64_t sl = nh * he, gi = gcd64(gs.block_size, gd.block_size);
+    if (slice < 0) slice = sl, g = gi;
+    if (sl != slice || gi != g)
+      return fail(DYNA_EINVAL, "reshard: every entry must move slices of one size over one block grid");
+    if (!S0) S0 = m.src.pool;
+    if (m.src.pool->dev != S0->dev) return fail(DYNA_EINVAL, "reshard: all sources on one device");
+    if (!e && (r = check_reach(m.src.pool, m.dst.pool))) return r;
+    empty &= e;
+  }
+  if ((r = check_alias(dsp, ssp))) return r;
+  if (empty) {
+    auto* x = new dyna_kv_xfer();
+    x->empty = true;
+    if (signal) x->batch.assign(n, dyna_kv_xfer::BatchEntry{});
+    *out = x;
+    return DYNA_OK;
+  }
+  if (!err_word()) return fail(DYNA_ECUDA, "no error word");
+  const int64_t ntok = tr.end - tr.begin;
+  const int64_t nchunks = (ntok + chunk_tokens - 1) / chunk_tokens;
+  if (signal) {
+    if (nchunks > DYNA_MAX_CHUNKS) return fail(DYNA_ERANGE, "%lld chunks > DYNA_MAX_CHUNKS", (long long)nchunks);
+    std::map<std::pair<int, uint64_t>, int64_t> per_row;
+    for (int32_t i = 0; i < n; ++i)
+      if ((per_row[{migs[i].src.pool->desc.instance, migs[i].dst.pool->uid}] += nchunks) > DYNA_MAX_CHUNKS)
+        return fail(DYNA_ERANGE, "reshard: more than DYNA_MAX_CHUNKS signalled chunks into one destination pool");
+  }
+  DeviceGuard guard(S0->dev);
+  dyna_kv_xfer* x = nullptr;
+  if ((r = new_xfer(S0->dev, S0->desc.instance, stream, &x))) return r;
+  if (signal) {
+    x->batch.assign(n, dyna_kv_xfer::BatchEntry{});
+    for (int32_t i = 0; i < n; ++i) {
+      dyna_kv_xfer::BatchEntry& be = x->batch[i];
+      if ((r = flag_reserve(migs[i].src.pool->desc.instance, migs[i].dst.pool, nchunks, &be.epoch, &be.first_slot))) {
+        delete x;
+        return r;
+      }
+      be.nchunks = (int32_t)nchunks;
+      be.sender = migs[i].src.pool->desc.instance;
+    }
+  }
+  const int piece = o.piece_bytes ? o.piece_bytes : kVecPiece;
+  const size_t plans_b = ((n * sizeof(Plan)) + 15) & ~size_t(15);
+  std::vector<size_t> soff(n, 0), doff(n, 0);
+  size_t tab_b = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    if (!migs[i].src.block_ids) {
+      soff[i] = plans_b + tab_b;
+      tab_b += (table_upload_bytes(migs[i].src, tr.end) + 15) & ~size_t(15);
+    }
+    if (!migs[i].dst.block_ids) {
+      doff[i] = plans_b + tab_b;
+      tab_b += (table_upload_bytes(migs[i].dst, tr.end) + 15) & ~size_t(15);
+    }
+  }
+  RingLease lease(S0->dev);
+  char *dbase = nullptr, *h = nullptr;
+  if ((r = lease.reserve(plans_b + tab_b, &dbase, &h, stream))) {
+    delete x;
+    return r;
+  }
+  std::vector<Plan> plans(n);
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  for (int32_t i = 0; i < n; ++i) {
+    const dyna_kv_head_migration& m = migs[i];
+    dyna_kv_pool *S = m.src.pool, *D = m.dst.pool;
+    const int64_t he = (int64_t)S->desc.head_dim * S->desc.elem_bytes;
+    const int32_t* sids = m.src.block_ids ? m.src.block_ids : reinterpret_cast<const int32_t*>(dbase + soff[i]);
+    const int32_t* dids = m.dst.block_ids ? m.dst.block_ids : reinterpret_cast<const int32_t*>(dbase + doff[i]);
+    plans[i] = make_plan_sliced(paged(S, sids), paged(D, dids), slice, S->row, m.src_heads.begin * he, D->row,
+                                (int64_t)m.dst_head_begin * he, tr.begin, tr.end, l0, lm, chunk_tokens, g, piece);
+    plans[i].err = x->err;
+    if (signal) {
+      const dyna_kv_xfer::BatchEntry& be = x->batch[i];
+      unsigned long long* ctr = nullptr;
+      if ((r = channel_counters(S, D, S0->dev, &ctr))) {
+        delete x;
+        return r;
+      }
+      plans[i].counters = ctr + be.first_slot;
+      plans[i].flags = D->inbox + (size_t)S->desc.instance * DYNA_MAX_CHUNKS + be.first_slot;
+      plans[i].epoch = be.epoch;
+      plans[i].sys_fence = (D->dev != S->dev || D->imported) ? 1 : 0;
+    }
+  }
+  std::memcpy(h, plans.data(), n * sizeof(Plan));
+  for (int32_t i = 0; i < n; ++i) {
+    if (!migs[i].src.block_ids) std::memcpy(h + soff[i], migs[i].src.host_block_ids, table_upload_bytes(migs[i].src, tr.end));
+    if (!migs[i].dst.block_ids) std::memcpy(h + doff[i], migs[i].dst.host_block_ids, table_upload_bytes(migs[i].dst, tr.end));
+  }
+  if ((r = lease.copy(stream))) {
+    delete x;
+    return r;
+  }
+  InterleavedSource isrc{reinterpret_cast<const Plan*>(dbase), n, plans[0].n_items * n};
+  x->variant = DYNA_VARIANT_FUSED;
+  x->engine = DYNA_ENGINE_VEC;
+  x->piece = piece;
+  x->unroll = 8;
+  x->nchunks = (int32_t)nchunks;
+  const uint64_t launches0 = g_launches.load();
+  r = launch_rows_interleaved(isrc, signal, o.max_ctas, S0->dev, stream);
+  if (!r) r = lease.finish(stream);
+  if (r) {
+    delete x;
+    return r;
+  }
+  x->launches = (int32_t)(g_launches.load() - launches0);
+  if ((r = record_completion(x, S0->dev, stream))) {
+    delete x;
+    return r;
+  }
+  *out = x;
+  return DYNA_OK;
 }
 
 dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna_range lr, int32_t chunk_tokens,

@@ -92,5 +92,21 @@ struct BatchSource {
   }
   __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }
 };
+// n plans with identical item structure (dyna_kv_reshard: one request's head slices between
+// TP ranks), items interleaved: global item g is item g / n of plan g % n, so warps working
+// side by side move the slices of the same token rows at the same time.
+struct InterleavedSource {
+  const Plan* plans;
+  int32_t n;
+  int64_t total_items;
+  __device__ __forceinline__ int64_t total() const { return total_items; }
+  __device__ __forceinline__ const Plan& locate(int64_t& item) const {
+    const int64_t q = item / n;
+    const int32_t r = (int32_t)(item - q * n);
+    item = q;
+    return plans[r];
+  }
+  __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }
+};
 
 }  // namespace dynakv

@@ -181,23 +181,29 @@ Side linear(char* base) {
 
 // Rows a table reaches for tokens [t0, t1), as (pool uid, block id, slot range) spans; ids
 // are range-checked on the way (DYNA_ERANGE).  Needs the host copy of the ids.
-dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out, int32_t who) {
+dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out, int32_t who,
+                        int32_t h0, int32_t h1) {
   const int64_t bs = t.pool->desc.block_size, nb = t.pool->desc.num_blocks;
   for (int64_t j = t0 / bs; j <= (t1 - 1) / bs; ++j) {
     const int32_t id = t.host_block_ids[j];
     if (id < 0 || id >= nb) return fail(DYNA_ERANGE, "block_ids[%lld] = %d outside [0, %lld)", (long long)j, id, (long long)nb);
     const int64_t lo = std::max(t0, j * bs) - j * bs, hi = std::min(t1, (j + 1) * bs) - j * bs;
-    out.push_back({t.pool->uid, id, lo, hi, who});
+    out.push_back({t.pool->uid, id, lo, hi, who, h0, h1});
   }
   return DYNA_OK;
 }
 
-// Reading R7: destination rows must be distinct (no two writes of one row) and, where a
-// source pool is the destination pool, disjoint from the source rows being read.  Source
-// rows may repeat (shared prefix blocks).  All spans of one call or one batch together.
+// Reading R7: destination rows (heads) must be distinct (no two writes of one byte) and, where
+// a source pool is a destination pool, disjoint from the source rows (heads) being read.
+// Source rows may repeat (shared prefix blocks).  All spans of one call or one batch together;
+// spans of one block are compared pairwise (few per block).
 dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src) {
   auto by = [](const Span& a, const Span& b) {
     return a.uid != b.uid ? a.uid < b.uid : a.id != b.id ? a.id < b.id : a.lo < b.lo;
+  };
+  auto same_block = [](const Span& a, const Span& b) { return a.uid == b.uid && a.id == b.id; };
+  auto overlap = [](const Span& a, const Span& b) {
+    return a.lo < b.hi && b.lo < a.hi && a.h0 < b.h1 && b.h0 < a.h1;
   };
   auto named = [](const Span& a, const Span& b, const char* what) {
     if (a.who < 0) return fail(DYNA_EALIAS, "%s block %d", what, a.id);
@@ -205,17 +211,21 @@ dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src) {
                 std::min(a.who, b.who));
   };
   std::sort(dst.begin(), dst.end(), by);
-  for (size_t i = 1; i < dst.size(); ++i)
-    if (dst[i].uid == dst[i - 1].uid && dst[i].id == dst[i - 1].id && dst[i].lo < dst[i - 1].hi)
-      return named(dst[i], dst[i - 1], "destination rows written twice in");
+  for (size_t i = 0; i < dst.size();) {
+    size_t e = i;
+    while (e < dst.size() && same_block(dst[e], dst[i])) ++e;
+    for (size_t a = i; a < e; ++a)
+      for (size_t b = a + 1; b < e && dst[b].lo < dst[a].hi; ++b)
+        if (overlap(dst[a], dst[b])) return named(dst[b], dst[a], "destination rows written twice in");
+    i = e;
+  }
   if (src.empty()) return DYNA_OK;
   std::sort(src.begin(), src.end(), by);
   size_t k = 0;
-  for (const Span& x : dst) {  // both sorted: one merge pass
-    while (k < src.size() && by(src[k], Span{x.uid, x.id, 0, 0, -1})) ++k;
-    for (size_t m = k; m < src.size() && src[m].uid == x.uid && src[m].id == x.id; ++m)
-      if (src[m].lo < x.hi && x.lo < src[m].hi)
-        return named(x, src[m], "destination rows that are also source rows in");
+  for (const Span& x : dst) {  // both sorted: one merge pass over the blocks
+    while (k < src.size() && (src[k].uid < x.uid || (src[k].uid == x.uid && src[k].id < x.id))) ++k;
+    for (size_t m = k; m < src.size() && same_block(src[m], x); ++m)
+      if (overlap(src[m], x)) return named(x, src[m], "destination rows that are also source rows in");
   }
   return DYNA_OK;
 }

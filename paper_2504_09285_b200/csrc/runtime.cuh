@@ -106,13 +106,15 @@ dyna_status ensure_peer(int dev, int peer);
 // re-imported pool never hands out an epoch a stale flag already satisfies.
 uint64_t new_uid();
 dyna_status flag_reserve(int sender, const dyna_kv_pool* dst, int64_t nchunks, uint64_t* epoch, int32_t* first_slot);
-struct Span {  // the rows [lo, hi) of block `id` of the pool with this uid
+struct Span {  // the rows [lo, hi) of block `id` of the pool with this uid, heads [h0, h1) of them
   uint64_t uid;
   int32_t id;
   int64_t lo, hi;
   int32_t who;   // batch entry (-1: a single call)
+  int32_t h0, h1;
 };
-dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out, int32_t who);
+dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::vector<Span>& out, int32_t who,
+                        int32_t h0 = 0, int32_t h1 = std::numeric_limits<int32_t>::max());
 dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src);
 bool pools_overlap(const dyna_kv_pool* a, const dyna_kv_pool* b, bool* same);
 
@@ -376,6 +378,7 @@ dyna_status launch_ready(const Plan& p, int max_ctas, int dev, cudaStream_t st, 
 Plan make_plan_sliced(const Side& s, const Side& d, int64_t slice, int64_t spitch, int64_t scol, int64_t dpitch,
                       int64_t dcol, int64_t t0, int64_t t1, int l0, int lm, int64_t c, int64_t g, int piece);
 dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st);
+dyna_status launch_rows_interleaved(const InterleavedSource& src, bool sig, int max_ctas, int dev, cudaStream_t st);
 dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, const int32_t* dids, dyna_range tr,
                        int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
                        int max_ctas, cudaStream_t stream, dyna_kv_xfer* x, int schedule);

@@ -10,7 +10,7 @@ Workloads (one B200, intra-device form, fragmented tables, working set > L2):
 
 Each workload is repeated back to back (`--reps`) between two CUDA events on the launch
 stream; GB/s = payload / (region time / reps).  Candidates are engine option sets given
-as name=engine:piece:stages:unroll:max_ctas (0 = AUTO/default), e.g.
+as name=engine:piece:stages:unroll:max_ctas[:flags] (0 = AUTO/default), e.g.
     python scripts/engine_ab.py --cand auto=0:0:0:0:0 --cand vec2=1:8192:0:8:296
 Environment switches (DYNA_KV_RING, DYNA_KV_LAG, ...) are set by the caller per process.
 """
@@ -41,8 +41,10 @@ def main():
     cands = []
     for c in args.cand or ["auto=0:0:0:0:0"]:
         name, spec = c.split("=")
-        e, p, s, u, m = (int(x) for x in spec.split(":"))
-        cands.append((name, dk.opts(engine=e, piece_bytes=p, stages=s, unroll=u, max_ctas=m)))
+        f = [int(x) for x in spec.split(":")]
+        e, p, s, u, m = f[:5]
+        fl = f[5] if len(f) > 5 else 0          # optional 6th field: opts.flags (1 = per-chunk flags)
+        cands.append((name, dk.opts(engine=e, piece_bytes=p, stages=s, unroll=u, max_ctas=m, flags=fl)))
     torch.cuda.set_device(0)
     stream = torch.cuda.Stream()
     cs = stream.cuda_stream

@@ -56,7 +56,8 @@ def main():
     ap.add_argument("round")
     ap.add_argument("reps", nargs="+")
     ap.add_argument("--launches")
-    ap.add_argument("--dominant", default="k_copy_vec<8, 0>")
+    ap.add_argument("--dominant", default="k_copy_ring")
+    ap.add_argument("--workload", default="c2", help="bench.py workload id the dominant capture belongs to")
     a = ap.parse_args()
     md = [f"# ncu summary — {a.round}", "",
           "Captured with `ncu --set full --clock-control none --import-source on -k regex:k_copy` on one B200",
@@ -77,7 +78,7 @@ def main():
                 rd = to_bytes(*r["dram__bytes_read.sum"])
                 wr = to_bytes(*r["dram__bytes_write.sum"])
                 traffic = traffic or {"kernel": name, "bytes_per_launch": rd + wr, "read": rd, "write": wr,
-                                      "source": os.path.basename(rep), "round": a.round}
+                                      "source": os.path.basename(rep), "round": a.round, "workload": a.workload}
             md.append("")
     if a.launches:
         agg = collections.defaultdict(list)

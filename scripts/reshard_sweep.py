@@ -53,24 +53,8 @@ def main():
     cases += [("Qwen2-72B", kvgen.QWEN2_72B, tp) for tp in [(1, 1), (4, 8), (8, 4), (2, 8)]]
     if args.quick:
         cases = [cases[i] for i in (2, 3, 6, 8, 13)]
-    for name, g0, (ts_, td_) in cases:
-        H, L = g0.num_kv_heads, g0.num_layers
-        nb = 2 * kvgen.blocks_needed(s, g0.block_size) + 16
-        gs = g0.with_(num_kv_heads=H // ts_, num_blocks=nb)
-        gd = g0.with_(num_kv_heads=H // td_, num_blocks=nb)
-        src = [dk.Pool(gs, 0) for _ in range(ts_)]
-        dst = [dk.Pool(gd, 0) for _ in range(td_)]
-        for i, p in enumerate(src + dst):
-            dk.dyna_kv_debug_fill(p.tensor.data_ptr(), p.tensor.numel(), 100 + i, 0, cs)
-        st = [dk.table(p, torch.from_numpy(t).cuda(), t) for p, t in
-              ((p, kvgen.table_pair(10 + i, s, gs, gs)[0]) for i, p in enumerate(src))]
-        dt = [dk.table(p, torch.from_numpy(t).cuda(), t) for p, t in
-              ((p, kvgen.table_pair(20 + i, s, gd, gd)[1]) for i, p in enumerate(dst))]
-        plan = dd.tp_reshard_plan(H, ts_, td_)
 
-        def once():
-            return [dk.dyna_kv_migrate_heads(st[a], dt[b], (0, s), (0, L), heads, hd0, c, cs)
-                    for a, b, heads, hd0 in plan]
+    def measure(name, g0, gs, gd, ts_, td_, plan, mode, once):
         for _ in range(3):
             for x in once():
                 dk.dyna_kv_wait(x)
@@ -86,13 +70,40 @@ def main():
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
         ms = statistics.median(ts)
-        payload = s * 2 * L * g0.row_bytes
+        payload = s * 2 * g0.num_layers * g0.row_bytes
         gb = payload / (ms / 1e3) / 1e9
-        r = {"model": name, "tp_src": ts_, "tp_dst": td_, "s": s, "chunk": c, "calls": len(plan),
+        r = {"model": name, "tp_src": ts_, "tp_dst": td_, "mode": mode, "s": s, "chunk": c, "calls": len(plan),
              "slice_bytes": min(gs.row_bytes, gd.row_bytes), "payload_bytes": payload, "ms": ms, "GBps": gb,
              "hbm_rw_GBps": 2 * gb, "frac_of_measured_hbm": 2 * gb / pk}
         print(json.dumps(r), flush=True)
         out.append(r)
+
+    for name, g0, (ts_, td_) in cases:
+        H, L = g0.num_kv_heads, g0.num_layers
+        nb = 2 * kvgen.blocks_needed(s, g0.block_size) + 16
+        gs = g0.with_(num_kv_heads=H // ts_, num_blocks=nb)
+        gd = g0.with_(num_kv_heads=H // td_, num_blocks=nb)
+        src = [dk.Pool(gs, 0) for _ in range(ts_)]
+        dst = [dk.Pool(gd, 0) for _ in range(td_)]
+        for i, p in enumerate(src + dst):
+            dk.dyna_kv_debug_fill(p.tensor.data_ptr(), p.tensor.numel(), 100 + i, 0, cs)
+        st = [dk.table(p, torch.from_numpy(t).cuda(), t) for p, t in
+              ((p, kvgen.table_pair(10 + i, s, gs, gs)[0]) for i, p in enumerate(src))]
+        dt = [dk.table(p, torch.from_numpy(t).cuda(), t) for p, t in
+              ((p, kvgen.table_pair(20 + i, s, gd, gd)[1]) for i, p in enumerate(dst))]
+        plan = dd.tp_reshard_plan(H, ts_, td_)
+
+        def calls():
+            return [dk.dyna_kv_migrate_heads(st[a], dt[b], (0, s), (0, L), heads, hd0, c, cs)
+                    for a, b, heads, hd0 in plan]
+
+        def fused():
+            return [dk.dyna_kv_reshard([(st[a], dt[b], heads, hd0) for a, b, heads, hd0 in plan], (0, s), (0, L), c,
+                                       cs)]
+        for mode, once in (("calls", calls), ("one_launch", fused)):
+            if mode == "one_launch" and len(plan) == 1 and ts_ == td_ == 1:
+                continue
+            measure(name, g0, gs, gd, ts_, td_, plan, mode, once)
         del src, dst, st, dt
         torch.cuda.empty_cache()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)

@@ -59,7 +59,8 @@ def test_struct_layouts_match_header(tmp_path):
     structs = {"dyna_kv_pool_desc": dk.dyna_kv_pool_desc, "dyna_block_table": dk.dyna_block_table,
                "dyna_range": dk.dyna_range, "dyna_kv_opts": dk.dyna_kv_opts,
                "dyna_kv_calib_entry": dk.dyna_kv_calib_entry, "dyna_kv_migration": dk.dyna_kv_migration,
-               "dyna_kv_channel_handle": dk.dyna_kv_channel_handle, "dyna_kv_ipc_handle": dk.dyna_kv_ipc_handle}
+               "dyna_kv_channel_handle": dk.dyna_kv_channel_handle, "dyna_kv_ipc_handle": dk.dyna_kv_ipc_handle,
+               "dyna_kv_head_migration": dk.dyna_kv_head_migration}
     lines = []
     for name, cls in structs.items():
         lines.append(f'printf("{name} %zu\\n", sizeof({name}));')

@@ -198,3 +198,66 @@ def test_full_size_qwen72b_tp4_to_tp8_sampled():
         assert torch.equal(D[~mask], ref.view_as(D)[~mask])
         del dst, ref, D
         torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- dyna_kv_reshard: the whole plan, one launch
+@pytest.mark.parametrize("tp_s,tp_d", [(1, 8), (8, 1), (2, 4), (4, 2), (2, 8), (8, 2), (1, 2), (4, 4)])
+@pytest.mark.parametrize("signal", [False, True])
+def test_reshard_one_launch_matches_oracle(tp_s, tp_d, signal):
+    """Every rank pair of dd.tp_reshard_plan in ONE dyna_kv_reshard launch (interleaved items):
+    every destination shard equals the oracle applying oracle.migrate_heads per pair; with
+    signalling every entry's flags reach its own epoch."""
+    H, L, s, c = 8, 3, 700, 128
+    g = Geom(L, H, 64, 2, 16, 60)
+    gs = g.with_(num_kv_heads=H // tp_s)
+    gd = g.with_(num_kv_heads=H // tp_d, block_size=8, num_blocks=120)
+    hs = [kvgen.fill_bytes(200 + r, gs.pool_bytes) for r in range(tp_s)]
+    hd = [kvgen.fill_bytes(300 + r, gd.pool_bytes) for r in range(tp_d)]
+    ts = [kvgen.table_pair(10 + r, s, gs, gs)[0] for r in range(tp_s)]
+    td = [kvgen.table_pair(20 + r, s, gd, gd)[1] for r in range(tp_d)]
+    plan = dd.tp_reshard_plan(H, tp_s, tp_d)
+    want = [h.copy() for h in hd]
+    for a, b, heads, hd0 in plan:
+        oracle.migrate_heads(hs[a], gs, ts[a], want[b], gd, td[b], (0, s), (0, L), heads, hd0)
+    src = [pool_from_host(gs, h, instance=a) for a, h in enumerate(hs)]
+    dst = [pool_from_host(gd, h) for h in hd]
+    st = [dev_table(p, t) for p, t in zip(src, ts)]
+    dt = [dev_table(p, t) for p, t in zip(dst, td)]
+    migs = [(st[a], dt[b], heads, hd0) for a, b, heads, hd0 in plan]
+    n0 = dk.dyna_kv_launch_count()
+    x = dk.dyna_kv_reshard(migs, (0, s), (0, L), c, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0))
+    infos = [dk.dyna_kv_batch_info(x, i) for i in range(len(migs))] if signal else []
+    dk.dyna_kv_wait(x)
+    assert dk.dyna_kv_launch_count() - n0 == 1
+    for b in range(tp_d):
+        assert np.array_equal(dst[b].tensor.cpu().numpy(), want[b]), b
+    for a in range(tp_s):
+        assert np.array_equal(src[a].tensor.cpu().numpy(), hs[a])
+    for (a, b, _, _), (epoch, first, nck, sender) in zip(plan, infos):
+        fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
+        dk.dyna_kv_copy_flags(dst[b].handle, sender, first, nck, fl.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert sender == a and nck == -(-s // c) and (fl.numpy() == epoch).all()
+
+
+def test_reshard_head_aware_alias_checks():
+    """Entries may write different heads of the same destination rows (a gather of TP ranks);
+    overlapping heads of one row are refused (R7 per head), as are mismatched slice sizes."""
+    H, L, s = 8, 2, 100
+    g = Geom(L, H, 64, 2, 16, 40)
+    g1 = g.with_(num_kv_heads=1)
+    g2 = g.with_(num_kv_heads=2)
+    src1 = [pool_filled(g1, 1 + r, instance=r) for r in range(2)]
+    dst = pool_filled(g, 9)
+    ts = kvgen.table_pair(3, s, g1, g1)[0]
+    td = kvgen.table_pair(4, s, g, g)[1]
+    st = [dev_table(p, ts) for p in src1]
+    dt = dev_table(dst, td)
+    dk.dyna_kv_wait(dk.dyna_kv_reshard([(st[0], dt, (0, 1), 0), (st[1], dt, (0, 1), 1)], (0, s), (0, L), 32))
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_reshard([(st[0], dt, (0, 1), 3), (st[1], dt, (0, 1), 3)], (0, s), (0, L), 32)
+    assert e.value.status == dk.DYNA_EALIAS and "migration 1" in str(e.value)
+    src2 = pool_filled(g2, 5)
+    with pytest.raises(dk.DynaKVError) as e:          # 1-head and 2-head slices in one launch
+        dk.dyna_kv_reshard([(st[0], dt, (0, 1), 0), (dev_table(src2, ts), dt, (0, 2), 2)], (0, s), (0, L), 32)
+    assert e.value.status == dk.DYNA_EINVAL
