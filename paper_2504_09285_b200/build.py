@@ -32,22 +32,31 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB):
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Build libdyna_kv.so (or, for A/B experiments, a variant with extra -D defines at `out`,
+    loaded by the binding through DYNA_KV_LIB)."""
+    if not force and os.path.exists(out) and not defines:
         newest = max(os.path.getmtime(p) for p in DEPS)
-        if os.path.getmtime(LIB) >= newest:
-            return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-shared", "-o", LIB + ".tmp", *SOURCES,
-           "-cudart", "static"]
+        if os.path.getmtime(out) >= newest:
+            return out
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-shared",
+           "-o", out + ".tmp", *SOURCES, "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libdyna_kv.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out", default=LIB, help="output path (A/B variants: e.g. ab_libs/libdyna_kv_x.so)")
+    ap.add_argument("-D", action="append", default=[], dest="defines", help="extra preprocessor define")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, out=os.path.abspath(a.out), defines=a.defines))

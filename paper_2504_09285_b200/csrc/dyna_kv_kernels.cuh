@@ -351,15 +351,14 @@ __device__ __forceinline__ void warp_copy(const char* __restrict__ src, char* __
   }
 }
 
-// A warp copies `rows` slices of p.row bytes (16-B vectors), source rows p.spitch
-// apart, destination rows p.dpitch apart: lane-major over the flattened vector
-// index, U loads in flight per lane.
+// A warp copies `rows` slices of vps 16-B vectors, source rows spitch bytes apart, destination
+// rows dpitch apart: lane-major over the flattened vector index, U loads in flight per lane.
+// The geometry comes in by value: read through a Plan in global memory (batches), every field
+// would be reloaded after each store (the stores' asm clobbers memory).
 template <int U>
 __device__ __forceinline__ void warp_copy_rows(const char* __restrict__ src, char* __restrict__ dst, uint32_t rows,
-                                               const Plan& p, int lane) {
-  const uint32_t vps = (uint32_t)p.vps;
+                                               uint32_t vps, int sh, int64_t spitch, int64_t dpitch, int lane) {
   const uint32_t nv = rows * vps;
-  const int sh = p.vps_shift;
   for (uint32_t base = 0; base < nv; base += 32 * U) {
     int4 v[U];
     uint32_t r[U], c[U];
@@ -369,12 +368,12 @@ __device__ __forceinline__ void warp_copy_rows(const char* __restrict__ src, cha
       r[u] = sh >= 0 ? (idx >> sh) : idx / vps;
       c[u] = idx - r[u] * vps;
       if (idx < nv)
-        v[u] = ld_nc_v4(reinterpret_cast<const int4*>(src + (int64_t)r[u] * p.spitch + (int64_t)c[u] * 16));
+        v[u] = ld_nc_v4(reinterpret_cast<const int4*>(src + (int64_t)r[u] * spitch + (int64_t)c[u] * 16));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint32_t idx = base + u * 32 + lane;
-      if (idx < nv) st_v4(reinterpret_cast<int4*>(dst + (int64_t)r[u] * p.dpitch + (int64_t)c[u] * 16), v[u]);
+      if (idx < nv) st_v4(reinterpret_cast<int4*>(dst + (int64_t)r[u] * dpitch + (int64_t)c[u] * 16), v[u]);
     }
   }
 }
@@ -409,7 +408,7 @@ __global__ void __launch_bounds__(256, 3) k_copy_rows(const Src src) {
       if (kMulti) cur_p = &p;
       cur_acc = 0;
     }
-    if (it.rows) warp_copy_rows<U>(it.src, it.dst, it.rows, p, lane);
+    if (it.rows) warp_copy_rows<U>(it.src, it.dst, it.rows, (uint32_t)p.vps, p.vps_shift, p.spitch, p.dpitch, lane);
     if (SIGNAL) cur_acc += it.acc;
   }
   if (SIGNAL && cur_acc) {
