@@ -382,10 +382,44 @@ __device__ __forceinline__ void warp_copy_rows(const char* __restrict__ src, cha
 // round-robin over a balanced persistent grid, per-(warp, plan, chunk) signalling as in
 // k_copy_vec.  (A lane-parallel decode of 32 items at once, as k_copy_lanes does, measured
 // 3-7% slower here on 256-B slices: profiles/r02_reshard_lanes.json.)
+// Plans of an interleaved launch staged in shared memory (up to kSmemPlans of them): every
+// item's decode reads ~20 plan fields, from global memory reloaded after each store.
+constexpr int kSmemPlans = 32;
+
+template <class Src>
+struct PlanView {  // SingleSource: the kernel parameter itself
+  const Src& s;
+  __device__ __forceinline__ PlanView(const Src& src, Plan*) : s(src) {}
+  __device__ __forceinline__ const Plan& locate(int64_t& item) const { return s.locate(item); }
+};
+template <>
+struct PlanView<InterleavedSource> {
+  const InterleavedSource& s;
+  const Plan* plans;
+  __device__ __forceinline__ PlanView(const InterleavedSource& src, Plan* smem) : s(src), plans(src.plans) {
+    if (src.n <= kSmemPlans) {
+      const int words = (int)(src.n * sizeof(Plan) / 4);
+      const uint32_t* g = reinterpret_cast<const uint32_t*>(src.plans);
+      uint32_t* d = reinterpret_cast<uint32_t*>(smem);
+      for (int i = threadIdx.x; i < words; i += blockDim.x) d[i] = g[i];
+      plans = smem;
+    }
+    __syncthreads();
+  }
+  __device__ __forceinline__ const Plan& locate(int64_t& item) const {
+    const int64_t q = item / s.n;
+    const int32_t r = (int32_t)(item - q * s.n);
+    item = q;
+    return plans[r];
+  }
+};
+
 template <int U, bool SIGNAL, class Src>
 __global__ void __launch_bounds__(256, 3) k_copy_rows(const Src src) {
-  pdl_enter();
   constexpr bool kMulti = !std::is_same<Src, SingleSource>::value;
+  __shared__ __align__(16) Plan splans[kMulti ? kSmemPlans : 1];
+  pdl_enter();
+  const PlanView<Src> view(src, splans);
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -395,7 +429,7 @@ __global__ void __launch_bounds__(256, 3) k_copy_rows(const Src src) {
   uint32_t cur_acc = 0;
   for (int64_t g = warp; g < n_items; g += nwarps) {
     int64_t item = g;
-    const Plan& p = src.locate(item);
+    const Plan& p = view.locate(item);
     const SItem it = decode_item_sliced(p, item);
     if (SIGNAL && it.acc && (it.k != cur_k || (kMulti && &p != cur_p))) {
       if (cur_acc) {
@@ -1069,10 +1103,16 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
   uint32_t cur_acc = 0, park_acc = 0;
   int since_park = 0;
   auto flush_park = [&](bool all) {
+#ifndef DYNA_DIAG_NO_WAIT  // (DYNA_DIAG_*: unsafe diagnostic builds that drop one step each)
     if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
+#endif
+#ifndef DYNA_DIAG_NO_PROXY
     asm volatile("fence.proxy.async.global;" ::: "memory");
+#endif
+#ifndef DYNA_DIAG_NO_COUNT
     if (ACC) mail[0].post(posted, park_k, park_acc, park_pl);
     else account_chunk_release(kBatch ? *park_pl : p, park_k, park_acc);
+#endif
     park_k = -1;
     park_acc = 0;
   };
