@@ -618,6 +618,21 @@ def locals_for_b1(workload, loc):
     return {k: loc[k] for k in keys}
 
 
+def b1_exchange(plan, rank, tok_bytes):
+    """configs[4] B1 exchange of one rank: per peer, the migrations it packs for that peer (in
+    plan order) and the ones it unpacks from it (in plan order, i.e. the sender's order), and
+    the buffer bytes of each (tests/test_dist_gloo.py checks both sides agree)."""
+    out, inn = {}, {}
+    for m in plan:
+        if m.src_rank == rank:
+            out.setdefault(m.dst_rank, []).append(m)
+        if m.dst_rank == rank:
+            inn.setdefault(m.src_rank, []).append(m)
+    return {"out": out, "in": inn,
+            "send_bytes": {p: sum(m.req.s for m in v) * tok_bytes for p, v in out.items()},
+            "recv_bytes": {p: sum(m.req.s for m in v) * tok_bytes for p, v in inn.items()}}
+
+
 def run_b1(ctx, workload, g, d, args):
     """SURVEY §2c B1, the paper's "fully offloaded to NCCL" transfer on identical
     bytes: the sender packs its rows with the library's K1 (dyna_kv_pack) into one contiguous
@@ -644,16 +659,10 @@ def run_b1(ctx, workload, g, d, args):
         def pieces_in(i):
             return {peer: [(rcv_tab[i % T4_SETS], (0, n))]}
     else:
-        plan = d["plan"]
-        out_m = [m for m in plan if m.src_rank == ctx.rank]
-        in_m = [m for m in plan if m.dst_rank == ctx.rank]
-        o_t = {}
-        for m in out_m:
-            o_t.setdefault(m.dst_rank, []).append((dev_tab(d["src"], m.src_table, dev), (0, m.req.s)))
-        i_t = {}
-        for m in in_m:
-            i_t.setdefault(m.src_rank, []).append(
-                (dk.table(d["mine"], torch.from_numpy(m.dst_table).to(f"cuda:{dev}"), m.dst_table), (0, m.req.s)))
+        ex = b1_exchange(d["plan"], ctx.rank, tok_bytes)
+        o_t = {p: [(dev_tab(d["src"], m.src_table, dev), (0, m.req.s)) for m in v] for p, v in ex["out"].items()}
+        i_t = {p: [(dk.table(d["mine"], torch.from_numpy(m.dst_table).to(f"cuda:{dev}"), m.dst_table), (0, m.req.s))
+                   for m in v] for p, v in ex["in"].items()}
 
         def pieces_out(i):
             return o_t

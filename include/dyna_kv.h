@@ -257,9 +257,8 @@ DYNA_API dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_tabl
  * token_range, layer_range and chunk_tokens, each moving heads [src_heads) of its source rows
  * into heads [dst_head_begin, ...) of its destination rows, exactly as dyna_kv_migrate_heads
  * would.  All entries move slices of one size (n_heads*d*e) over one block grid
- * (gcd(bs_src, bs_dst)) and have their sources on the launching device.  Their work items
- * are interleaved, so the slices of one token row move together (one launch instead of n,
- * and the DRAM rows of a token are touched once, not once per call).  Destination aliasing
+ * (gcd(bs_src, bs_dst)) and have their sources on the launching device.  One launch
+ * instead of n (entries one after the other in the launch's work order).  Destination aliasing
  * (R7) is checked per head: entries may write different heads of the same rows.  Per-chunk
  * signalling gives every entry its own epoch and slots (dyna_kv_batch_info with the entry's
  * index).  VEC engine, FUSED variant (DYNA_ENOTSUP otherwise); other rules as

@@ -407,9 +407,9 @@ struct PlanView<InterleavedSource> {
     __syncthreads();
   }
   __device__ __forceinline__ const Plan& locate(int64_t& item) const {
-    const int64_t q = item / s.n;
-    const int32_t r = (int32_t)(item - q * s.n);
-    item = q;
+    const int64_t per = s.total_items / s.n;
+    const int32_t r = (int32_t)(item / per);
+    item -= (int64_t)r * per;
     return plans[r];
   }
 };
@@ -622,7 +622,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // Accountant hand-off (signalling, ACC kernels): the copying thread posts (chunk, bytes)
 // after its bulk groups completed and a proxy fence; mbarrier arrive = release at CTA scope,
 // wait = acquire, so the accountant's GPU-scope fence + count covers the poster's writes.
-constexpr int kMail = 8;
+constexpr int kMail = 16;
 struct Mailbox {
   uint64_t full[kMail], empty[kMail];
   const Plan* pl[kMail];  // batches: the plan (request) the chunk belongs to; nullptr = the launch's plan
@@ -643,36 +643,55 @@ struct Mailbox {
     mbar_arrive(&full[m]);
     ++n;
   }
-  // the accountant's loop, until the poster's sentinel (chunk -1); it polls with a short
-  // sleep between tries (DYNA_MAIL_SLEEP ns; 0 = spin in try_wait)
+  // the accountant's loop, until the poster's sentinel (chunk -1).  It takes every entry that
+  // has already arrived, then fences ONCE for all of them and counts them: the GPU-scope fence
+  // (which must cover the poster's bulk stores) is the expensive step, so under load one fence
+  // serves many chunks (measured: DESIGN.md §6b, r02 signalling rows).
+  __device__ __forceinline__ bool ready(int64_t i) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(&full[i % kMail])), "r"((uint32_t)((i / kMail) & 1))
+        : "memory");
+    return done != 0;
+  }
   __device__ __forceinline__ void serve(const Plan& p) {
-    for (int64_t i = 0;; ++i) {
-      const int m = (int)(i % kMail);
+    for (int64_t i = 0;;) {
 #if DYNA_MAIL_SLEEP > 0
-      for (;;) {
-        uint32_t done;
-        asm volatile(
-            "{\n .reg .pred P1;\n"
-            " mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, P1;\n"
-            "}\n"
-            : "=r"(done)
-            : "r"(smem_u32(&full[m])), "r"((uint32_t)((i / kMail) & 1))
-            : "memory");
-        if (done) break;
-        __nanosleep(DYNA_MAIL_SLEEP);
-      }
+      while (!ready(i)) __nanosleep(DYNA_MAIL_SLEEP);
 #else
-      mbar_wait(&full[m], (uint32_t)((i / kMail) & 1));
+      mbar_wait(&full[i % kMail], (uint32_t)((i / kMail) & 1));
 #endif
-      const int32_t kk = k[m];
-      const uint32_t a = acc[m];
-      const Plan* plan = pl[m];
-      mbar_arrive(&empty[m]);
-      if (kk < 0) return;
-      const Plan& P = plan ? *plan : p;
-      fence_for(P);
-      account_chunk(P, kk, a);
+      int n = 1;
+      while (n < kMail && ready(i + n)) ++n;
+      int32_t kk[kMail];
+      uint32_t aa[kMail];
+      const Plan* pp[kMail];
+      bool last = false;
+      int m = 0;
+      for (; m < n; ++m) {
+        const int s = (int)((i + m) % kMail);
+        kk[m] = k[s];
+        aa[m] = acc[s];
+        pp[m] = pl[s];
+        mbar_arrive(&empty[s]);
+        if (kk[m] < 0) {
+          last = true;
+          break;
+        }
+      }
+      if (m > 0) {
+        bool sys = false;
+        for (int j = 0; j < m; ++j) sys |= (pp[j] ? pp[j]->sys_fence : p.sys_fence) != 0;
+        if (sys) __threadfence_system(); else __threadfence();
+        for (int j = 0; j < m; ++j) account_chunk(pp[j] ? *pp[j] : p, kk[j], aa[j]);
+      }
+      if (last) return;
+      i += n;
     }
   }
 };

@@ -668,8 +668,7 @@ dyna_status dyna_kv_unpack(const void* buf, uint64_t buf_bytes, dyna_block_table
 // ---------------------------------------------------------------- reshard: one request's head slices, one launch
 // Every entry moves heads [src_heads) of its source rows into heads [dst_head_begin, ...) of its
 // destination rows, for the same tokens, layers and chunking; all entries' slices have one size,
-// so their work items line up and are interleaved (InterleavedSource): the warps running side
-// by side move the different slices of the same token rows together.
+// so their work items line up: one launch (InterleavedSource, entries one after the other).
 dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_range tr, dyna_range lr,
                             int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
                             dyna_kv_xfer_t* out) {

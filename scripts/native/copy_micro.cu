@@ -288,6 +288,44 @@ __global__ void __launch_bounds__(256) k_ldg_bulkst(const It* __restrict__ items
   if (lane == 0) bwait0();
 }
 
+// ---- F: head-sliced rows: an item = `rows` rows of `slice` bytes at `spitch` (source) / `dpitch`
+// (destination) strides, copied lane-major over 16-B vectors, U in flight per lane (k_copy_rows).
+template <int U>
+__global__ void __launch_bounds__(256, 3) k_rows(const It* __restrict__ items, int64_t n, const char* S, char* D,
+                                                 int rows, int slice, int spitch, int dpitch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int vps = slice >> 4;
+  const int nv = rows * vps;
+  for (int64_t i = warp; i < n; i += nw) {
+    const It it = items[i];
+    for (int b = 0; b < nv; b += 32 * U) {
+      int4 v[U];
+      int r[U], c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = b + u * 32 + lane;
+        r[u] = idx / vps;
+        c[u] = idx - r[u] * vps;
+        if (idx < nv)
+          asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                       : "l"(S + it.s + (int64_t)r[u] * spitch + c[u] * 16));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = b + u * 32 + lane;
+        if (idx < nv)
+          asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(D + it.d + (int64_t)r[u] * dpitch +
+                                                                                     c[u] * 16),
+                       "r"(v[u].x), "r"(v[u].y), "r"(v[u].z), "r"(v[u].w)
+                       : "memory");
+      }
+    }
+  }
+}
+
 struct Bench {
   char *S, *D;
   It* items;
@@ -398,6 +436,44 @@ int main(int argc, char** argv) {
     fflush(stdout);
   };
   const char* only = argc > 1 ? argv[1] : "";
+  if (*only == 'F') {  // head slices: 16-row items of `slice` bytes out of 2-KiB rows (Llama-3-8B), 512 MiB payload
+    CK(cudaFuncSetAttribute((const void*)k_rows<8>, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    for (int slice : {2048, 1024, 512, 256})
+      for (int dcontig : {0, 1})
+        for (int contig : {0, 1}) {
+          // source: blocks of 16 rows x 2 KiB at random block slots; an item reads `slice` bytes of
+          // each row at a random column; destination: rows of `slice` (dcontig) or 2 KiB pitch
+          const int64_t blk = 16 * 2048, nblk_pool = pool / blk;
+          const int64_t nitems = (int64_t)payload / (16 * slice);
+          std::vector<int64_t> ps(nblk_pool), pd(nblk_pool);
+          std::iota(ps.begin(), ps.end(), 0);
+          std::iota(pd.begin(), pd.end(), 0);
+          if (!contig) {
+            std::shuffle(ps.begin(), ps.end(), rng);
+            std::shuffle(pd.begin(), pd.end(), rng);
+          }
+          const int per = 2048 / slice;  // slices per row
+          std::vector<It> v;
+          for (int64_t i = 0; i < nitems; ++i) {
+            const int64_t b = i / per, col = (i % per) * slice;   // all slices of a block, one after the other
+            v.push_back({ps[b % nblk_pool] * blk + col,
+                         dcontig ? (pd[b % nblk_pool] * blk + col * 16) : (pd[b % nblk_pool] * blk + col)});
+          }
+          CK(cudaMemcpy(dItems, v.data(), sizeof(It) * v.size(), cudaMemcpyHostToDevice));
+          Bench bb{S, D, dItems, (int64_t)v.size(), slice};
+          struct FCfg { int slice, dpitch; } fc{slice, dcontig ? slice : 2048};
+          auto run_f = [](const Bench& b, void* a) {
+            const FCfg& c = *(const FCfg*)a;
+            int sms = 0;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+            k_rows<8><<<sms * 3, 256>>>(b.items, b.n, b.S, b.D, 16, c.slice, 2048, c.dpitch);
+          };
+          char cfg[128];
+          snprintf(cfg, sizeof cfg, "slice%d dst_%s", slice, dcontig ? "contig" : "pitch2048");
+          report("rows", cfg, blk, slice, contig, time_it(run_f, bb, &fc));
+        }
+    return 0;
+  }
   char cfg[256];
   {
     Bench b = make(32768, 32768, true);

@@ -71,49 +71,28 @@ def test_load_aware_bound_brute_force():
         assert dd.load_aware_bound_s(pb, 1.0) == n - 1 == dd.aggregate_bound_s(pb, n, 1.0)
 
 
-def _baseline_worker(rank, world, port, q):
-    import importlib.util
-
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
+@pytest.mark.parametrize("world", [3, 4, 8])
+def test_b1_exchange_plan_matches_between_ranks(world):
+    """bench.py's NCCL baseline (B1) for configs[4]: what rank i packs for rank j, in order, is
+    exactly what rank j unpacks from rank i, and the buffers are sized for those bytes."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
     import kvgen
-    import oracle
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-        spec = importlib.util.spec_from_file_location("nb", os.path.join(root, "scripts", "nccl_baseline.py"))
-        nb = importlib.util.module_from_spec(spec)
-        spec.loader.exec_module(nb)
-        g, s, chunk = kvgen.TOY, 100, 32
-        src = torch.from_numpy(kvgen.fill_bytes(10 + rank, g.pool_bytes))
-        dst0 = kvgen.fill_bytes(20 + rank, g.pool_bytes)
-        dst = torch.from_numpy(dst0.copy())
-        ts, _ = kvgen.table_pair(500 + rank, 256, g, g)
-        prv = (rank - 1) % world
-        ts_prv, td_in = kvgen.table_pair(500 + prv, 256, g, g)
-        nb.push_chunks(rank, world, src, dst, g, torch.from_numpy(ts), torch.from_numpy(td_in), s, chunk)
-        want = dst0.copy()
-        oracle.migrate(kvgen.fill_bytes(10 + prv, g.pool_bytes), g, ts_prv, want, g, td_in, (0, s))
-        q.put((rank, bool(np.array_equal(dst.numpy(), want))))
-    finally:
-        dist.destroy_process_group()
-
-
-def test_nccl_baseline_logic_matches_oracle_under_gloo():
-    """B1 baseline (gather -> send/recv -> scatter) produces the oracle's bytes."""
-    world, port = 2, _free_port()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    ps = [ctx.Process(target=_baseline_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in ps:
-        p.start()
-    res = sorted(q.get(timeout=180) for _ in range(world))
-    for p in ps:
-        p.join(timeout=60)
-    assert res == [(0, True), (1, True)]
+    g = kvgen.QWEN2_72B
+    plan = kvgen.allpairs_plan(world, g, bench.C4_REQS, bench.C4_SEED)
+    tok = 2 * g.num_layers * g.row_bytes
+    ex = [bench.b1_exchange(plan, r, tok) for r in range(world)]
+    for i in range(world):
+        for j in range(world):
+            if i == j:
+                continue
+            sent = [(m.src_rank, m.dst_rank, m.req.s) for m in ex[i]["out"].get(j, [])]
+            got = [(m.src_rank, m.dst_rank, m.req.s) for m in ex[j]["in"].get(i, [])]
+            assert sent == got
+            assert ex[i]["send_bytes"].get(j, 0) == ex[j]["recv_bytes"].get(i, 0) == sum(s for _, _, s in sent) * tok
+    assert sum(sum(e["send_bytes"].values()) for e in ex) == sum(m.req.s for m in plan) * tok
 
 
 # ---------------------------------------------------------------- TP head resharding plan (host logic)
