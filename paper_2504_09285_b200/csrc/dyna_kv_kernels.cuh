@@ -378,81 +378,6 @@ __device__ __forceinline__ void warp_copy_rows(const char* __restrict__ src, cha
   }
 }
 
-// Head-sliced fused copy (dyna_kv_migrate_heads, dyna_kv_reshard): one warp per item, static
-// round-robin over a balanced persistent grid, per-(warp, plan, chunk) signalling as in
-// k_copy_vec.  (A lane-parallel decode of 32 items at once, as k_copy_lanes does, measured
-// 3-7% slower here on 256-B slices: profiles/r02_reshard_lanes.json.)
-// Plans of an interleaved launch staged in shared memory (up to kSmemPlans of them): every
-// item's decode reads ~20 plan fields, from global memory reloaded after each store.
-constexpr int kSmemPlans = 32;
-
-template <class Src>
-struct PlanView {  // SingleSource: the kernel parameter itself
-  const Src& s;
-  __device__ __forceinline__ PlanView(const Src& src, Plan*) : s(src) {}
-  __device__ __forceinline__ const Plan& locate(int64_t& item) const { return s.locate(item); }
-};
-template <>
-struct PlanView<InterleavedSource> {
-  const InterleavedSource& s;
-  const Plan* plans;
-  __device__ __forceinline__ PlanView(const InterleavedSource& src, Plan* smem) : s(src), plans(src.plans) {
-    if (src.n <= kSmemPlans) {
-      const int words = (int)(src.n * sizeof(Plan) / 4);
-      const uint32_t* g = reinterpret_cast<const uint32_t*>(src.plans);
-      uint32_t* d = reinterpret_cast<uint32_t*>(smem);
-      for (int i = threadIdx.x; i < words; i += blockDim.x) d[i] = g[i];
-      plans = smem;
-    }
-    __syncthreads();
-  }
-  __device__ __forceinline__ const Plan& locate(int64_t& item) const {
-    const int64_t per = s.total_items / s.n;
-    const int32_t r = (int32_t)(item / per);
-    item -= (int64_t)r * per;
-    return plans[r];
-  }
-};
-
-template <int U, bool SIGNAL, class Src>
-__global__ void __launch_bounds__(256, 3) k_copy_rows(const Src src) {
-  constexpr bool kMulti = !std::is_same<Src, SingleSource>::value;
-  __shared__ __align__(16) Plan splans[kMulti ? kSmemPlans : 1];
-  pdl_enter();
-  const PlanView<Src> view(src, splans);
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n_items = src.total();
-  int32_t cur_k = -1;
-  const Plan* cur_p = nullptr;
-  uint32_t cur_acc = 0;
-  for (int64_t g = warp; g < n_items; g += nwarps) {
-    int64_t item = g;
-    const Plan& p = view.locate(item);
-    const SItem it = decode_item_sliced(p, item);
-    if (SIGNAL && it.acc && (it.k != cur_k || (kMulti && &p != cur_p))) {
-      if (cur_acc) {
-        const Plan& cp = kMulti ? *cur_p : p;
-        fence_for(cp);
-        __syncwarp();
-        if (lane == 0) account_chunk(cp, cur_k, cur_acc);
-      }
-      cur_k = it.k;
-      if (kMulti) cur_p = &p;
-      cur_acc = 0;
-    }
-    if (it.rows) warp_copy_rows<U>(it.src, it.dst, it.rows, (uint32_t)p.vps, p.vps_shift, p.spitch, p.dpitch, lane);
-    if (SIGNAL) cur_acc += it.acc;
-  }
-  if (SIGNAL && cur_acc) {
-    const Plan& cp = kMulti ? *cur_p : src.locate_signal();
-    fence_for(cp);
-    __syncwarp();
-    if (lane == 0) account_chunk(cp, cur_k, cur_acc);
-  }
-}
-
 // VEC engine with warp-cooperative decode (static round-robin schedule, no ready board):
 // the warp's next 32 items are decoded at once, one per lane, then copied one after the
 // other with the fields broadcast by shuffles.  Same per-(warp, chunk) signalling as
@@ -1175,6 +1100,123 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
     }
   }
   if (ACC) mail[0].post(posted, -1, 0);  // the accountant may leave
+}
+
+// ------------------------------------------------------------------ head-sliced rows, decoder-fed
+// dyna_kv_migrate_heads / dyna_kv_reshard: a token's bytes are a slice of a row, so an item is
+// `rows` slices at a stride (4 KiB for 16 tokens x 256 B) — small items, where the per-item
+// decode (five 64-bit divisions, two dependent block-table loads; for a reshard also the plan
+// lookup) used to sit between a warp's copies.  Warp 0 of each CTA decodes the CTA's items 32
+// at a time (one per lane) into a shared-memory queue, kQ batches ahead; the other kCopiers
+// warps take descriptors round-robin and only copy (lane-major over 16-B vectors, U loads in
+// flight per lane).  A micro-benchmark of the same access pattern with precomputed items moves
+// 256-B slices of 2-KiB rows at 2790-2880 GB/s payload (profiles/r02_copy_micro_rows.jsonl).
+struct SDesc {
+  const char* src;
+  char* dst;
+  const Plan* pl;    // multi-plan launches: the item's plan (per-entry chunk flags)
+  int64_t spitch, dpitch;
+  uint32_t rows, acc;
+  int32_t k;
+  uint16_t vps;
+  int16_t sh;
+};
+constexpr int kCopiers = 7;
+
+template <int U, bool SIGNAL, class Src>
+__global__ void __launch_bounds__(32 * (kCopiers + 1), 3) k_copy_rows(const Src src) {
+  constexpr bool kMulti = !std::is_same<Src, SingleSource>::value;
+  __shared__ __align__(16) SDesc q[kQ][32];
+  __shared__ int32_t qcount[kQ], qlast[kQ];
+  __shared__ __align__(8) uint64_t qfull[kQ], qempty[kQ];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kQ; ++b) {
+      mbar_init(&qfull[b], 1);
+      mbar_init(&qempty[b], kCopiers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_enter();
+  const int64_t n_items = src.total();
+  if (warp == 0) {  // ---------------- decoder
+    int64_t m = 0;
+    for (int64_t b = 0;; ++b) {
+      const int qb = (int)(b % kQ);
+      if (b >= kQ) mbar_wait(&qempty[qb], (uint32_t)(((b / kQ) - 1) & 1));
+      const int64_t gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
+      m += 32;
+      SItem it{nullptr, nullptr, 0u, 0u, 0, 0};
+      const Plan* ipl = nullptr;
+      if (gi < n_items) {
+        int64_t item = gi;
+        const Plan& ip = src.locate(item);
+        ipl = &ip;
+        it = decode_item_sliced(ip, item);
+        if (SIGNAL && it.rows == 0 && it.acc) account_chunk(ip, it.k, it.acc);  // skipped (bad id)
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, it.rows != 0);
+      if (it.rows) {
+        SDesc d;
+        d.src = it.src;
+        d.dst = it.dst;
+        d.pl = kMulti ? ipl : nullptr;
+        d.spitch = ipl->spitch;
+        d.dpitch = ipl->dpitch;
+        d.rows = it.rows;
+        d.acc = it.acc;
+        d.k = it.k;
+        d.vps = (uint16_t)ipl->vps;
+        d.sh = (int16_t)ipl->vps_shift;
+        q[qb][__popc(mask & ((1u << lane) - 1u))] = d;
+      }
+      const bool last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;
+      __syncwarp();
+      if (lane == 0) {
+        qcount[qb] = __popc(mask);
+        qlast[qb] = last ? 1 : 0;
+        mbar_arrive(&qfull[qb]);
+      }
+      if (last) return;
+    }
+  }
+  // ---------------- copiers: descriptor i of each batch goes to copier i % kCopiers
+  const int cw = warp - 1;
+  int32_t cur_k = -1;
+  const Plan* cur_p = nullptr;
+  uint32_t cur_acc = 0;
+  const Plan* single = kMulti ? nullptr : &src.locate_signal();
+  for (int64_t b = 0;; ++b) {
+    const int qb = (int)(b % kQ);
+    mbar_wait(&qfull[qb], (uint32_t)((b / kQ) & 1));
+    const int cnt = qcount[qb];
+    const bool last = qlast[qb] != 0;
+    for (int i = cw; i < cnt; i += kCopiers) {
+      const SDesc d = q[qb][i];
+      const Plan* dp = kMulti ? d.pl : single;
+      if (SIGNAL && d.acc && (d.k != cur_k || (kMulti && dp != cur_p))) {
+        if (cur_acc) {
+          fence_for(*cur_p);
+          __syncwarp();
+          if (lane == 0) account_chunk(*cur_p, cur_k, cur_acc);
+        }
+        cur_k = d.k;
+        cur_p = dp;
+        cur_acc = 0;
+      }
+      warp_copy_rows<U>(d.src, d.dst, d.rows, d.vps, d.sh, d.spitch, d.dpitch, lane);
+      if (SIGNAL) cur_acc += d.acc;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&qempty[qb]);
+    if (last) break;
+  }
+  if (SIGNAL && cur_acc) {
+    fence_for(*cur_p);
+    __syncwarp();
+    if (lane == 0) account_chunk(*cur_p, cur_k, cur_acc);
+  }
 }
 
 // ------------------------------------------------------------------ consumer-side chunk wait

@@ -367,14 +367,16 @@ dyna_status launch_rows_src(const Src& src, int64_t n_items, bool sig, int max_c
   if (n_items == 0) return DYNA_OK;
   if (n_items >= (int64_t(1) << 31)) return fail(DYNA_ERANGE, "too many work items in one launch");
   DevInfo* di = dev_info(dev);
-  const int o = vec_occupancy(sig ? (const void*)k_copy_rows<8, true, Src> : (const void*)k_copy_rows<8, false, Src>);
-  int64_t cap = (int64_t)di->sms * o;
+  constexpr int threads = 32 * (kCopiers + 1);  // a decoder warp + the copier warps
+  int o = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &o, sig ? (const void*)k_copy_rows<8, true, Src> : (const void*)k_copy_rows<8, false, Src>, threads, 0);
+  int64_t cap = (int64_t)di->sms * std::max(o, 1);
   if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
-  constexpr int wpc = kVecThreads / 32;
-  const int64_t warps = balanced_workers(n_items, cap * wpc);
-  const unsigned grid = (unsigned)((warps + wpc - 1) / wpc);
-  if (sig) CUDA_TRY(launch_kernel(k_copy_rows<8, true, Src>, grid, kVecThreads, 0, st, src));
-  else CUDA_TRY(launch_kernel(k_copy_rows<8, false, Src>, grid, kVecThreads, 0, st, src));
+  // items go to CTAs round-robin (the decoder decodes 32 of its CTA's items at a time)
+  const unsigned grid = (unsigned)balanced_workers((n_items + kCopiers - 1) / kCopiers, cap);
+  if (sig) CUDA_TRY(launch_kernel(k_copy_rows<8, true, Src>, grid, threads, 0, st, src));
+  else CUDA_TRY(launch_kernel(k_copy_rows<8, false, Src>, grid, threads, 0, st, src));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DYNA_OK;
 }
