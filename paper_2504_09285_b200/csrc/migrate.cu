@@ -685,6 +685,10 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   const bool unchecked = (o.flags & DYNA_MIGRATE_UNCHECKED) != 0;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   std::vector<Span> dsp, ssp;
+  std::vector<uint64_t> dst_uids;  // a source pool that some entry writes needs its rows checked too
+  for (int32_t i = 0; i < n; ++i)
+    if (migs[i].dst.pool) dst_uids.push_back(migs[i].dst.pool->uid);
+  std::sort(dst_uids.begin(), dst_uids.end());
   dyna_kv_pool* S0 = nullptr;
   int64_t slice = -1, g = -1;
   bool empty = true;
@@ -692,7 +696,9 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
     const dyna_kv_head_migration& m = migs[i];
     bool e = false;
     const size_t d0 = dsp.size(), s0 = ssp.size();
-    if ((r = validate_pair(m.src, m.dst, tr, lr, chunk_tokens, unchecked, &e, dsp, ssp, 1, true, i))) {
+    const bool src_is_dst = m.src.pool && std::binary_search(dst_uids.begin(), dst_uids.end(), m.src.pool->uid);
+    if ((r = validate_pair(m.src, m.dst, tr, lr, chunk_tokens, unchecked, &e, dsp, ssp, src_is_dst ? 1 : 0, true,
+                           i))) {
       g_err = "migration " + std::to_string(i) + ": " + g_err;
       return r;
     }

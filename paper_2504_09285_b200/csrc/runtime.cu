@@ -195,37 +195,64 @@ dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::
 
 // Reading R7: destination rows (heads) must be distinct (no two writes of one byte) and, where
 // a source pool is a destination pool, disjoint from the source rows (heads) being read.
-// Source rows may repeat (shared prefix blocks).  All spans of one call or one batch together;
-// spans of one block are compared pairwise (few per block).
+// Source rows may repeat (shared prefix blocks).  All spans of one call or one batch together.
+// Spans are ordered by a packed 64-bit key (pool, block id, first row) — a sort of plain
+// integers, several times cheaper than sorting the structs — and the spans of one block are
+// compared pairwise (few per block).
 dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src) {
-  auto by = [](const Span& a, const Span& b) {
-    return a.uid != b.uid ? a.uid < b.uid : a.id != b.id ? a.id < b.id : a.lo < b.lo;
+  if (dst.empty()) return DYNA_OK;
+  std::vector<uint64_t> uids;  // few distinct pools per call
+  auto uid_index = [&](uint64_t u) -> uint64_t {
+    for (size_t i = 0; i < uids.size(); ++i)
+      if (uids[i] == u) return i;
+    uids.push_back(u);
+    return uids.size() - 1;
   };
-  auto same_block = [](const Span& a, const Span& b) { return a.uid == b.uid && a.id == b.id; };
+  auto keyed = [&](const std::vector<Span>& v, std::vector<std::pair<uint64_t, uint32_t>>& out, bool only_known) {
+    out.clear();
+    out.reserve(v.size());
+    for (uint32_t i = 0; i < v.size(); ++i) {
+      uint64_t u = 0;
+      if (only_known) {  // source spans: only pools that are also destinations matter
+        size_t k = 0;
+        while (k < uids.size() && uids[k] != v[i].uid) ++k;
+        if (k == uids.size()) continue;
+        u = k;
+      } else {
+        u = uid_index(v[i].uid);
+      }
+      out.emplace_back((u << 56) | ((uint64_t)(uint32_t)v[i].id << 24) | ((uint64_t)v[i].lo & 0xFFFFFF), i);
+    }
+    std::sort(out.begin(), out.end());
+  };
+  auto blk = [](uint64_t key) { return key >> 24; };
   auto overlap = [](const Span& a, const Span& b) {
-    return a.lo < b.hi && b.lo < a.hi && a.h0 < b.h1 && b.h0 < a.h1;
+    return a.uid == b.uid && a.id == b.id && a.lo < b.hi && b.lo < a.hi && a.h0 < b.h1 && b.h0 < a.h1;
   };
   auto named = [](const Span& a, const Span& b, const char* what) {
     if (a.who < 0) return fail(DYNA_EALIAS, "%s block %d", what, a.id);
     return fail(DYNA_EALIAS, "migration %d: %s block %d (also migration %d)", std::max(a.who, b.who), what, a.id,
                 std::min(a.who, b.who));
   };
-  std::sort(dst.begin(), dst.end(), by);
-  for (size_t i = 0; i < dst.size();) {
+  std::vector<std::pair<uint64_t, uint32_t>> kd, ks;
+  keyed(dst, kd, false);
+  for (size_t i = 0; i < kd.size();) {
     size_t e = i;
-    while (e < dst.size() && same_block(dst[e], dst[i])) ++e;
+    while (e < kd.size() && blk(kd[e].first) == blk(kd[i].first)) ++e;
     for (size_t a = i; a < e; ++a)
-      for (size_t b = a + 1; b < e && dst[b].lo < dst[a].hi; ++b)
-        if (overlap(dst[a], dst[b])) return named(dst[b], dst[a], "destination rows written twice in");
+      for (size_t b = a + 1; b < e && dst[kd[b].second].lo < dst[kd[a].second].hi; ++b)
+        if (overlap(dst[kd[a].second], dst[kd[b].second]))
+          return named(dst[kd[b].second], dst[kd[a].second], "destination rows written twice in");
     i = e;
   }
   if (src.empty()) return DYNA_OK;
-  std::sort(src.begin(), src.end(), by);
+  keyed(src, ks, true);
   size_t k = 0;
-  for (const Span& x : dst) {  // both sorted: one merge pass over the blocks
-    while (k < src.size() && (src[k].uid < x.uid || (src[k].uid == x.uid && src[k].id < x.id))) ++k;
-    for (size_t m = k; m < src.size() && same_block(src[m], x); ++m)
-      if (overlap(src[m], x)) return named(x, src[m], "destination rows that are also source rows in");
+  for (const auto& x : kd) {  // both sorted: one merge pass over the blocks
+    while (k < ks.size() && blk(ks[k].first) < blk(x.first)) ++k;
+    for (size_t m = k; m < ks.size() && blk(ks[m].first) == blk(x.first); ++m)
+      if (overlap(src[ks[m].second], dst[x.second]))
+        return named(dst[x.second], src[ks[m].second], "destination rows that are also source rows in");
   }
   return DYNA_OK;
 }

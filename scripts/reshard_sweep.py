@@ -18,6 +18,7 @@ import json
 import os
 import statistics
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -38,7 +39,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--s", type=int, default=4096)
     ap.add_argument("--chunk", type=int, default=1024)
-    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--quick", action="store_true", help="a few representative cases (A/B runs)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "reshard.json"))
     args = ap.parse_args()
@@ -55,26 +56,29 @@ def main():
         cases = [cases[i] for i in (2, 3, 6, 8, 13)]
 
     def measure(name, g0, gs, gd, ts_, td_, plan, mode, once):
+        # reps back to back between two events (the host issues rep k+1 while rep k runs, as a
+        # serving loop would); the host time per rep is reported beside it
         for _ in range(3):
             for x in once():
                 dk.dyna_kv_wait(x)
-        ts = []
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t = time.perf_counter()
+        e0.record(stream)
+        xs = []
         for _ in range(args.reps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            e0.record(stream)
-            xs = once()
-            e1.record(stream)
-            for x in xs:
-                dk.dyna_kv_wait(x)
-            e1.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        ms = statistics.median(ts)
+            xs += once()
+        e1.record(stream)
+        host_ms = (time.perf_counter() - t) * 1e3 / args.reps
+        for x in xs:
+            dk.dyna_kv_wait(x)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / args.reps
         payload = s * 2 * g0.num_layers * g0.row_bytes
         gb = payload / (ms / 1e3) / 1e9
         r = {"model": name, "tp_src": ts_, "tp_dst": td_, "mode": mode, "s": s, "chunk": c, "calls": len(plan),
              "slice_bytes": min(gs.row_bytes, gd.row_bytes), "payload_bytes": payload, "ms": ms, "GBps": gb,
-             "hbm_rw_GBps": 2 * gb, "frac_of_measured_hbm": 2 * gb / pk}
+             "hbm_rw_GBps": 2 * gb, "frac_of_measured_hbm": 2 * gb / pk, "host_ms_per_reshard": host_ms}
         print(json.dumps(r), flush=True)
         out.append(r)
 
