@@ -38,6 +38,7 @@ void preload_kernels() {
       (const void*)k_copy_bulk<true, SingleSource, true>,
       (const void*)k_copy_rows<8, false, SingleSource>, (const void*)k_copy_rows<8, true, SingleSource>,
       (const void*)k_copy_rows<8, false, InterleavedSource>, (const void*)k_copy_rows<8, true, InterleavedSource>,
+      (const void*)k_copy_rows<8, false, BatchSource>, (const void*)k_copy_rows<8, true, BatchSource>,
       (const void*)k_copy_ring<false, SingleSource>, (const void*)k_copy_ring<true, SingleSource>,
       (const void*)k_copy_ring<true, SingleSource, true>, (const void*)k_copy_ring<false, BatchSource>,
       (const void*)k_copy_ring<true, BatchSource>, (const void*)k_copy_ring<true, BatchSource, true>,
@@ -387,6 +388,20 @@ dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st) {
 
 dyna_status launch_rows_interleaved(const InterleavedSource& src, bool sig, int max_ctas, int dev, cudaStream_t st) {
   return launch_rows_src(src, src.total_items, sig, max_ctas, dev, st);
+}
+
+dyna_status launch_rows_batch(const BatchSource& src, bool sig, int max_ctas, int dev, cudaStream_t st) {
+  return launch_rows_src(src, src.total_items, sig, max_ctas, dev, st);
+}
+
+// The VEC engine on whole rows through the decoder-fed row kernel (a row is a slice of itself):
+// DYNA_KV_FED_VEC=1 (experiment switch).
+bool fed_vec_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYNA_KV_FED_VEC");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev,

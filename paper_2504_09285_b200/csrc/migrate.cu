@@ -306,7 +306,10 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   if (variant == DYNA_VARIANT_FUSED) {
     // K4 / K4-local: source rows -> destination rows, one launch for all chunks.
     const int64_t g = gcd64(gs.block_size, gd.block_size);
-    Plan p = make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
+    const bool fed = engine == DYNA_ENGINE_VEC && !board && o.schedule != DYNA_SCHED_DYNAMIC && fed_vec_enabled();
+    Plan p = fed ? make_plan_sliced(paged(S, sids), paged(D, dids), row, row, 0, row, 0, tr.begin, tr.end, l0, lm, c,
+                                    g, piece)
+                 : make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
     p.err = x->err;
     if (ctx) set_chunking(p, ctx->mig_t0, tr.end, c);
     if (signal) {
@@ -339,7 +342,8 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
       x->ready_epoch = ready_epoch;
       r = launch_ready(p, o.max_ctas, S->dev, stream, o.schedule);
     } else {
-      r = launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream, o.schedule);
+      r = fed ? launch_rows(p, o.max_ctas, S->dev, stream)
+              : launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream, o.schedule);
     }
   } else {
     r = run_staged(S, D, sids, dids, tr, l0, lm, c, signal, engine, piece, stages, unroll, o.max_ctas, stream, x,
@@ -906,6 +910,7 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   dyna_kv_xfer* x = nullptr;
   if ((r = new_xfer(S0->dev, S0->desc.instance, stream, &x))) return r;
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  const bool fed = ch.engine == DYNA_ENGINE_VEC && o.schedule != DYNA_SCHED_DYNAMIC && fed_vec_enabled();
   if (signal) {  // each entry: its own epoch and slot range of its (sender, destination pool)
     // the entries of one launch must not share slots (their counters live there): at most
     // DYNA_MAX_CHUNKS signalled chunks per (sender, destination pool) in one batch
@@ -964,8 +969,10 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     const int32_t* sids = mg.src.block_ids ? mg.src.block_ids : reinterpret_cast<const int32_t*>(dbase + soff[k]);
     const int32_t* dids = mg.dst.block_ids ? mg.dst.block_ids : reinterpret_cast<const int32_t*>(dbase + doff[k]);
     const int64_t g = gcd64(S->desc.block_size, D->desc.block_size);
-    plans[k] = make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end, l0, lm,
-                         chunk_tokens, g, ch.piece);
+    plans[k] = fed ? make_plan_sliced(paged(S, sids), paged(D, dids), S->row, S->row, 0, D->row, 0,
+                                      mg.token_range.begin, mg.token_range.end, l0, lm, chunk_tokens, g, ch.piece)
+                   : make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end, l0,
+                               lm, chunk_tokens, g, ch.piece);
     plans[k].err = x->err;
     if (signal) {  // entry k's chunk j: counter / inbox slot first_slot + j of its (sender, destination)
       dyna_kv_xfer::BatchEntry& be = x->batch[live[k]];
@@ -1004,8 +1011,9 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   x->stages = ch.engine != DYNA_ENGINE_VEC ? ch.stages : 0;
   x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
   x->launches = 1;
-  r = launch_batch(bsrc, total_items, signal, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev, stream,
-                   o.schedule);
+  r = fed ? launch_rows_batch(bsrc, signal, o.max_ctas, S0->dev, stream)
+          : launch_batch(bsrc, total_items, signal, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev,
+                         stream, o.schedule);
   if (!r) r = lease.finish(stream);
   if (r) {
     delete x;

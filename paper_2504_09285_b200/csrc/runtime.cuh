@@ -379,6 +379,8 @@ Plan make_plan_sliced(const Side& s, const Side& d, int64_t slice, int64_t spitc
                       int64_t dcol, int64_t t0, int64_t t1, int l0, int lm, int64_t c, int64_t g, int piece);
 dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st);
 dyna_status launch_rows_interleaved(const InterleavedSource& src, bool sig, int max_ctas, int dev, cudaStream_t st);
+dyna_status launch_rows_batch(const BatchSource& src, bool sig, int max_ctas, int dev, cudaStream_t st);
+bool fed_vec_enabled();
 dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, const int32_t* dids, dyna_range tr,
                        int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
                        int max_ctas, cudaStream_t stream, dyna_kv_xfer* x, int schedule);

@@ -142,6 +142,18 @@ def main():
                 ms = timeit(step, 64, args.reps)
                 report("c3c512", name, 32768 * 2 * 32 * g.row_bytes, ms, plan_of(step(0)[0]))
         del src, dst
+    if "q8" in works:   # TP-8 Qwen2-72B shard: 1 KV head per rank, 256-B rows (4-KiB block runs), 8192 tokens
+        g = kvgen.QWEN2_72B.with_(num_kv_heads=1, num_blocks=2048)
+        src, dst = pools(g, 9, 10)
+        tabs = kvgen.batch_tables(4, [8192] * 4, g, g)
+        T = [(tab(src, a), tab(dst, b)) for a, b in tabs]
+        for name, o in cands:
+            def step(i, o=o):
+                t = T[i % 4]
+                return [dk.dyna_kv_migrate_ex(t[0], t[1], (0, 8192), (0, 80), 1024, cs, o)]
+            ms = timeit(step, 1, args.reps * 2)
+            report("q8", name, 8192 * 2 * 80 * g.row_bytes, ms, plan_of(step(0)[0]))
+        del src, dst, T
     out = os.path.join(ROOT, "gpurun_out", f"engine_ab{('_' + args.tag) if args.tag else ''}.json")
     json.dump(res, open(out, "w"), indent=1)
 
