@@ -57,12 +57,16 @@ static void run(const char* name, dyna_kv_pool_desc d, int ntok, int chunk, int 
   dyna_block_table ts_host = {ps, NULL, hs, nb}, td_host = {pd, NULL, hd, nb};
   dyna_range tr = {0, ntok}, lr = {0, d.num_layers};
   dyna_kv_xfer_t* xs = (dyna_kv_xfer_t*)malloc(sizeof(dyna_kv_xfer_t) * reps);
-  struct { const char* n; dyna_block_table s, t; } modes[] = {
-      {"device ids", ts_dev, td_dev}, {"device+host ids (host checks)", ts_both, td_both},
-      {"host ids only (upload)", ts_host, td_host}};
+  dyna_kv_opts unchecked;
+  memset(&unchecked, 0, sizeof unchecked);
+  unchecked.flags = DYNA_MIGRATE_UNCHECKED;   /* device-only tables: the caller vouches for distinct rows */
+  struct { const char* n; dyna_block_table s, t; const dyna_kv_opts* o; } modes[] = {
+      {"device ids (DYNA_MIGRATE_UNCHECKED)", ts_dev, td_dev, &unchecked},
+      {"device+host ids (host checks)", ts_both, td_both, NULL},
+      {"host ids only (upload)", ts_host, td_host, NULL}};
   for (int m = 0; m < 3; ++m) {
     for (int i = 0; i < 50; ++i) {  /* warm */
-      CK(dyna_kv_migrate(modes[m].s, modes[m].t, tr, lr, chunk, st, &xs[0]));
+      CK(dyna_kv_migrate_ex(modes[m].s, modes[m].t, tr, lr, chunk, st, modes[m].o, &xs[0]));
       CK(dyna_kv_wait(xs[0]));
     }
     cudaEvent_t e0, e1;
@@ -72,7 +76,7 @@ static void run(const char* name, dyna_kv_pool_desc d, int ntok, int chunk, int 
     /* (1) host cost per enqueued call, (2) device time for the back-to-back calls */
     cudaEventRecord(e0, st);
     double t0 = now_us();
-    for (int i = 0; i < reps; ++i) CK(dyna_kv_migrate(modes[m].s, modes[m].t, tr, lr, chunk, st, &xs[i]));
+    for (int i = 0; i < reps; ++i) CK(dyna_kv_migrate_ex(modes[m].s, modes[m].t, tr, lr, chunk, st, modes[m].o, &xs[i]));
     double t1 = now_us();
     cudaEventRecord(e1, st);
     for (int i = 0; i < reps; ++i) CK(dyna_kv_wait(xs[i]));
@@ -83,7 +87,7 @@ static void run(const char* name, dyna_kv_pool_desc d, int ntok, int chunk, int 
     /* (3) latency of one call + wait, serial */
     double lat0 = now_us();
     for (int i = 0; i < reps; ++i) {
-      CK(dyna_kv_migrate(modes[m].s, modes[m].t, tr, lr, chunk, st, &xs[0]));
+      CK(dyna_kv_migrate_ex(modes[m].s, modes[m].t, tr, lr, chunk, st, modes[m].o, &xs[0]));
       CK(dyna_kv_wait(xs[0]));
     }
     double lat1 = now_us();
