@@ -964,7 +964,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
     for (int b = 0; b < kQ; ++b) {
-      mbar_init(&qfull[b], 1);
+      mbar_init(&qfull[b], 32);  // one arrive per decoder lane
       mbar_init(&qempty[b], 1);
     }
     if (ACC) mail[0].init();
@@ -994,12 +994,11 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
       const unsigned mask = __ballot_sync(0xffffffffu, it.n != 0);
       if (it.n) q[qb][__popc(mask & ((1u << lane) - 1u))] = Desc{it.src, it.dst, ipl, it.n, it.k};
       const bool last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
-      __syncwarp();
       if (lane == 0) {
         qcount[qb] = __popc(mask);
         qlast[qb] = last ? 1 : 0;
-        mbar_arrive(&qfull[qb]);  // release (CTA scope): the lanes' descriptor writes, ordered by __syncwarp
       }
+      mbar_arrive(&qfull[qb]);  // every lane releases its own descriptor write (CTA scope)
       if (last) return;
     }
   }
@@ -1132,8 +1131,8 @@ __global__ void __launch_bounds__(32 * (kCopiers + 1), 3) k_copy_rows(const Src 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int b = 0; b < kQ; ++b) {
-      mbar_init(&qfull[b], 1);
-      mbar_init(&qempty[b], kCopiers);
+      mbar_init(&qfull[b], 32);  // one arrive per decoder lane
+      mbar_init(&qempty[b], 32 * kCopiers);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1172,12 +1171,11 @@ __global__ void __launch_bounds__(32 * (kCopiers + 1), 3) k_copy_rows(const Src 
         q[qb][__popc(mask & ((1u << lane) - 1u))] = d;
       }
       const bool last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;
-      __syncwarp();
       if (lane == 0) {
         qcount[qb] = __popc(mask);
         qlast[qb] = last ? 1 : 0;
-        mbar_arrive(&qfull[qb]);
       }
+      mbar_arrive(&qfull[qb]);  // every lane releases its own descriptor write (CTA scope)
       if (last) return;
     }
   }
@@ -1208,8 +1206,7 @@ __global__ void __launch_bounds__(32 * (kCopiers + 1), 3) k_copy_rows(const Src 
       warp_copy_rows<U>(d.src, d.dst, d.rows, d.vps, d.sh, d.spitch, d.dpitch, lane);
       if (SIGNAL) cur_acc += d.acc;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&qempty[qb]);
+    mbar_arrive(&qempty[qb]);  // every copier lane releases its own descriptor reads
     if (last) break;
   }
   if (SIGNAL && cur_acc) {
@@ -1217,6 +1214,251 @@ __global__ void __launch_bounds__(32 * (kCopiers + 1), 3) k_copy_rows(const Src 
     __syncwarp();
     if (lane == 0) account_chunk(*cur_p, cur_k, cur_acc);
   }
+}
+
+// ------------------------------------------------------------------ head slices as TMA tensor tiles
+// The BULK engine for head slices (dyna_kv_migrate_heads / dyna_kv_reshard).  A 256-B slice of
+// a 2-KiB row is too small for one bulk op, and k_copy_rows' 16-B loads stop at ~0.88 of the
+// copy peak even with precomputed items (profiles/r02_copy_micro_rows.jsonl).  But the slices a
+// run needs form a regular lattice in both pools: `rows` slices at the row pitch, and the same
+// rows of every (layer, K|V) slab at the slab pitch (NB*bs*pitch; the layout is
+// [l][kv][block][token][row]).  A 4-D tensor map per side
+// (slice elements, -, row in slab, slab) turns one run across `lkb` slabs into ONE tensor load
+// (strided global -> dense shared memory) and ONE tensor store (dense shared -> strided global),
+// e.g. 16 rows x 256 B x 8 slabs = 32 KiB per op, with the TMA unit doing the striding.
+// A run shorter than the box (ragged chunk boundary or range end) is moved as one single-row
+// box per row (maps 2 and 3).  lkb divides 2*lm, so no box is ever clipped.
+// Decode, queue, issuer loop and signalling are k_copy_ring's.
+struct TDesc {
+  const char* tm;   // the item's TileMaps
+  const Plan* pl;   // multi-plan launches: the item's plan (per-entry chunk flags)
+  int32_t ys, yd;   // row coordinates (within a slab) in the source / destination maps
+  int32_t lk;       // first slab of the box (relative to 2*l0)
+  uint32_t rows;    // == g: one run box; < g: one row box per row
+  uint32_t acc;     // bytes counted for the item's chunk
+  int32_t k;
+};
+
+__device__ __forceinline__ void tma_load_4d(void* sdst, const char* tmap, int c2, int c3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5}], [%6];" ::"r"(smem_u32(sdst)),
+      "l"(tmap), "r"(0), "r"(0), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const char* tmap, const void* ssrc, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tmap),
+               "r"(0), "r"(0), "r"(c2), "r"(c3), "r"(smem_u32(ssrc))
+               : "memory");
+}
+
+// Item = (chunk k, slab group, run j), runs fastest.  Paged sides only (tile plans are never linear).
+__device__ __forceinline__ TDesc decode_item_tile(const Plan& p, int64_t item, bool& skipped) {
+  TDesc d{p.tmaps, nullptr, 0, 0, 0, 0u, 0u, 0};
+  skipped = false;
+  const int64_t k = item / p.items_per_chunk;
+  const int64_t i = item - k * p.items_per_chunk;
+  const int32_t j = (int32_t)(i % p.R);
+  const int32_t lkg = (int32_t)(i / p.R);
+  const int64_t a = p.t0 + k * p.c;
+  const int64_t b = min(a + (int64_t)p.c, p.t1);
+  const int64_t G = a / p.g + j;
+  const int64_t ta = max(a, G * p.g);
+  const int64_t tb = min(b, (G + 1) * p.g);
+  d.k = p.k_direct ? (int32_t)k + p.k_base : (int32_t)((a - p.mig_t0) / p.sig_c);
+  if (ta >= tb) return d;
+  d.lk = lkg * p.lkb;
+  d.acc = (uint32_t)((tb - ta) * p.row * p.lkb);
+  const int64_t js = ta / p.src.bs, jd = ta / p.dst.bs;
+  const int32_t bsrc = __ldg(p.src.table + js), bdst = __ldg(p.dst.table + jd);
+  if (bsrc < 0 || (int64_t)bsrc >= p.src.nb || bdst < 0 || (int64_t)bdst >= p.dst.nb) {
+    if (p.err) atomicOr(p.err, ERR_BAD_BLOCK);
+    skipped = true;
+    return d;
+  }
+  d.ys = (int32_t)((int64_t)bsrc * p.src.bs + (ta - js * p.src.bs));
+  d.yd = (int32_t)((int64_t)bdst * p.dst.bs + (ta - jd * p.dst.bs));
+  d.rows = (uint32_t)(tb - ta);
+  return d;
+}
+
+template <bool SIGNAL, class Src, bool ACC = false>
+__global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int stages, int lag) {
+  extern __shared__ __align__(1024) unsigned char ring[];
+  __shared__ __align__(8) uint64_t full[kMaxStages];
+  __shared__ __align__(8) uint64_t qfull[kQ], qempty[kQ];
+  __shared__ __align__(8) TDesc q[kQ][32];
+  __shared__ int32_t qcount[kQ], qlast[kQ];
+  __shared__ TDesc pend[kMaxStages];
+  __shared__ __align__(8) Mailbox mail[1];  // (ACC only)
+  constexpr bool kMulti = !std::is_same<Src, SingleSource>::value;
+  constexpr bool kRR = std::is_same<Src, RoundRobinSource>::value;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    for (int b = 0; b < kQ; ++b) {
+      mbar_init(&qfull[b], 32);  // one arrive per decoder lane
+      mbar_init(&qempty[b], 1);
+    }
+    if (ACC) mail[0].init();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_enter();
+  const Plan& p = src.locate_signal();  // per-launch fields (box geometry, signalling)
+  const int64_t n_items = src.total();
+  if (warp == 1) {  // ---------------- decoder
+    int64_t m = 0;
+    int64_t rr_n = 1;
+    if constexpr (kRR) rr_n = src.n;
+    for (int64_t b = 0;; ++b) {
+      const int qb = (int)(b % kQ);
+      if (b >= kQ) mbar_wait(&qempty[qb], (uint32_t)(((b / kQ) - 1) & 1));
+      // RoundRobinSource: the CTA's j-th item is entry j % n of its (j / n)-th local item, so the
+      // issuer moves the same rows of every entry back to back (a TP gather writes whole rows)
+      const int64_t gi = kRR ? (blockIdx.x + ((m + lane) / rr_n) * (int64_t)gridDim.x) * rr_n + (m + lane) % rr_n
+                             : blockIdx.x + (m + lane) * (int64_t)gridDim.x;
+      m += 32;
+      TDesc d{nullptr, nullptr, 0, 0, 0, 0u, 0u, 0};
+      if (gi < n_items) {
+        int64_t item = gi;
+        const Plan& ip = src.locate(item);
+        bool skipped = false;
+        d = decode_item_tile(ip, item, skipped);
+        d.pl = kMulti ? &ip : nullptr;
+        if (SIGNAL && skipped) account_chunk(ip, d.k, d.acc);  // bad id: still closes the chunk
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, d.rows != 0);
+      if (d.rows) q[qb][__popc(mask & ((1u << lane) - 1u))] = d;
+      const bool last = kRR ? (blockIdx.x + (m / rr_n) * (int64_t)gridDim.x) * rr_n >= n_items
+                            : blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
+      if (lane == 0) {
+        qcount[qb] = __popc(mask);
+        qlast[qb] = last ? 1 : 0;
+      }
+      mbar_arrive(&qfull[qb]);  // every lane releases its own descriptor write (CTA scope)
+      if (last) return;
+    }
+  }
+  if (ACC && warp == 2) {  // ---------------- accountant
+    if (lane == 0) mail[0].serve(p);
+    return;
+  }
+  if (lane != 0) return;
+  // ---------------- issuer (warp 0, lane 0)
+  const int32_t slot = p.tile_bytes;
+  const uint32_t g = (uint32_t)p.g;
+  const uint32_t row_box = (uint32_t)(p.row * p.lkb);  // bytes of one single-row box
+  // Maps were written by a host copy: acquire them for the tensormap proxy before first use.  Up to
+  // 64 plans all at once here (round-robin launches change plans every item), else lazily.
+  const char* fenced = nullptr;
+  bool all_fenced = false;
+  if constexpr (kMulti) {
+    if (src.n <= 64) {
+      for (int r = 0; r < src.n; ++r)
+        for (int t = 0; t < kTileMaps; ++t)
+          asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(src.plans[r].tmaps +
+                                                                                      t * kTileMapBytes)
+                       : "memory");
+      all_fenced = true;
+    }
+  }
+  int64_t qb = -1;
+  int pos = 0, cnt = 0;
+  bool qdone = false;
+  int64_t posted = 0;
+  auto refill = [&](int s) {
+    while (pos == cnt) {
+      if (qdone) {
+        pend[s].rows = 0;
+        return;
+      }
+      if (qb >= 0) mbar_arrive(&qempty[qb % kQ]);
+      ++qb;
+      const int qi = (int)(qb % kQ);
+      mbar_wait(&qfull[qi], (uint32_t)((qb / kQ) & 1));
+      cnt = qcount[qi];
+      qdone = qlast[qi] != 0;
+      pos = 0;
+    }
+    const TDesc d = q[qb % kQ][pos++];
+    if (!all_fenced && d.tm != fenced) {
+      for (int t = 0; t < kTileMaps; ++t)
+        asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;" ::"l"(d.tm + t * kTileMapBytes)
+                     : "memory");
+      fenced = d.tm;
+    }
+    unsigned char* sl = ring + (size_t)s * slot;
+    mbar_expect_tx(&full[s], d.rows * row_box);
+    if (d.rows == g) {
+      tma_load_4d(sl, d.tm, d.ys, d.lk, &full[s]);
+    } else {
+      for (uint32_t r = 0; r < d.rows; ++r) tma_load_4d(sl + r * row_box, d.tm + 2 * kTileMapBytes, d.ys + r, d.lk, &full[s]);
+    }
+    pend[s] = d;
+  };
+  for (int s = 0; s < stages; ++s) refill(s);
+
+  constexpr int kDefer = DYNA_BULK_DEFER;
+  int32_t cur_k = -1, park_k = -1;
+  const Plan *cur_pl = nullptr, *park_pl = nullptr;
+  uint32_t cur_acc = 0, park_acc = 0;
+  int since_park = 0;
+  auto flush_park = [&](bool all) {
+    if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    if (ACC) mail[0].post(posted, park_k, park_acc, park_pl);
+    else account_chunk_release(kMulti ? *park_pl : p, park_k, park_acc);
+    park_k = -1;
+    park_acc = 0;
+  };
+  for (int64_t iter = 0;; ++iter) {
+    const int s = (int)(iter % stages);
+    const TDesc d = pend[s];
+    if (d.rows == 0) break;
+    if (SIGNAL && (d.k != cur_k || (kMulti && d.pl != cur_pl))) {
+      if (park_acc) flush_park(true);
+      park_k = cur_k;
+      park_pl = cur_pl;
+      park_acc = cur_acc;
+      since_park = 0;
+      cur_k = d.k;
+      if (kMulti) cur_pl = d.pl;
+      cur_acc = 0;
+    }
+    mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
+    const unsigned char* sl = ring + (size_t)s * slot;
+    if (d.rows == g) {
+      tma_store_4d(d.tm + kTileMapBytes, sl, d.yd, d.lk);
+    } else {
+      for (uint32_t r = 0; r < d.rows; ++r) tma_store_4d(d.tm + 3 * kTileMapBytes, sl + r * row_box, d.yd + r, d.lk);
+    }
+    bulk_commit();
+    if (SIGNAL) {
+      cur_acc += d.acc;
+      if (park_acc && ++since_park == kDefer) flush_park(false);
+    }
+    if (iter >= lag) {
+      if (lag == 2) bulk_wait_read<2>(); else bulk_wait_read<1>();  // store iter-lag done reading smem
+      refill((int)((iter - lag) % stages));
+    }
+  }
+  bulk_wait_all<0>();
+  if (SIGNAL) {
+    if (park_acc) flush_park(true);
+    if (cur_acc) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      if (ACC) {
+        mail[0].post(posted, cur_k, cur_acc, cur_pl);
+      } else {
+        const Plan& P = kMulti ? *cur_pl : p;
+        fence_for(P);
+        account_chunk(P, cur_k, cur_acc);
+      }
+    }
+  }
+  if (ACC) mail[0].post(posted, -1, 0);  // the accountant may leave
 }
 
 // ------------------------------------------------------------------ consumer-side chunk wait

@@ -3,6 +3,9 @@
 // launch), the staged variant (K1 gather, K2 transfer, K3 scatter; SURVEY §8
 // a2-a4), producer-coupled launches, and the small flag / fill kernels.  The only
 // translation unit that includes the kernels.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <type_traits>
 
 #include "dyna_kv_kernels.cuh"
@@ -48,6 +51,9 @@ void preload_kernels() {
       (const void*)k_copy_lanes<4, false, BatchSource>, (const void*)k_copy_lanes<4, true, BatchSource>,
       (const void*)k_copy_lanes<8, false, BatchSource>, (const void*)k_copy_lanes<8, true, BatchSource>,
       (const void*)k_copy_lanes<16, false, BatchSource>, (const void*)k_copy_lanes<16, true, BatchSource>,
+      (const void*)k_copy_tiles<false, SingleSource>, (const void*)k_copy_tiles<true, SingleSource, true>,
+      (const void*)k_copy_tiles<false, InterleavedSource>, (const void*)k_copy_tiles<true, InterleavedSource, true>,
+      (const void*)k_copy_tiles<false, RoundRobinSource>, (const void*)k_copy_tiles<true, RoundRobinSource, true>,
   };
   for (const void* k : ks) cudaFuncGetAttributes(&a, k);
   // Allow the BULK rings any dynamic shared memory the device offers, once, here: a
@@ -64,6 +70,9 @@ void preload_kernels() {
       (const void*)k_copy_ring<false, SingleSource>, (const void*)k_copy_ring<true, SingleSource>,
       (const void*)k_copy_ring<true, SingleSource, true>, (const void*)k_copy_ring<false, BatchSource>,
       (const void*)k_copy_ring<true, BatchSource>, (const void*)k_copy_ring<true, BatchSource, true>,
+      (const void*)k_copy_tiles<false, SingleSource>, (const void*)k_copy_tiles<true, SingleSource, true>,
+      (const void*)k_copy_tiles<false, InterleavedSource>, (const void*)k_copy_tiles<true, InterleavedSource, true>,
+      (const void*)k_copy_tiles<false, RoundRobinSource>, (const void*)k_copy_tiles<true, RoundRobinSource, true>,
   };
   for (const void* k : bulk) {
     cudaFuncGetAttributes(&a, k);
@@ -392,6 +401,151 @@ dyna_status launch_rows_interleaved(const InterleavedSource& src, bool sig, int 
 
 dyna_status launch_rows_batch(const BatchSource& src, bool sig, int max_ctas, int dev, cudaStream_t st) {
   return launch_rows_src(src, src.total_items, sig, max_ctas, dev, st);
+}
+
+// ------------------------------------------------------------------ head slices as TMA tensor tiles
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+bool tiles_enabled() {  // DYNA_KV_TILES=0: head slices on the VEC row kernel even when AUTO
+  static const bool on = [] {
+    const char* e = std::getenv("DYNA_KV_TILES");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+static int tile_l2_promotion() {  // experiment switch DYNA_KV_TILE_L2 (0 none, 1 64B, 2 128B (default), 3 256B)
+  static const int v = [] {
+    const char* e = std::getenv("DYNA_KV_TILE_L2");
+    return e ? std::atoi(e) : 2;
+  }();
+  return v;
+}
+
+static bool tile_rr() {  // experiment switch DYNA_KV_TILE_RR=1: reshard entries dealt round-robin
+  static const bool v = [] {
+    const char* e = std::getenv("DYNA_KV_TILE_RR");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+static int tile_target_bytes() {  // experiment switch DYNA_KV_TILE_BYTES (default 32 KiB per box)
+  static const int v = [] {
+    const char* e = std::getenv("DYNA_KV_TILE_BYTES");
+    const int x = e ? std::atoi(e) : 0;
+    return x > 0 ? x : 32768;
+  }();
+  return v;
+}
+
+// One side's map: 4-D (e0 x 8-B elements, e1, row in slab, slab) over the slabs [2*l0, 2*(l0+lm)) of a
+// paged pool, starting at byte `col` of each row; box (e0, e1, rows, lkb).
+static bool encode_side(CUtensorMap* m, const Side& s, int64_t pitch, int64_t col, int l0, int lm, int64_t slice,
+                        int64_t e0, int64_t rows, int64_t lkb) {
+  const int64_t slab_rows = s.nb * (int64_t)s.bs;
+  char* base = s.base + (int64_t)2 * l0 * slab_rows * pitch + col;
+  const cuuint64_t dims[4] = {(cuuint64_t)e0, (cuuint64_t)(slice / (e0 * 8)), (cuuint64_t)slab_rows,
+                              (cuuint64_t)(2 * (int64_t)lm)};
+  const cuuint64_t strides[3] = {(cuuint64_t)(e0 * 8), (cuuint64_t)pitch, (cuuint64_t)(slab_rows * pitch)};
+  const cuuint32_t box[4] = {(cuuint32_t)e0, (cuuint32_t)(slice / (e0 * 8)), (cuuint32_t)rows, (cuuint32_t)lkb};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return encode_tiled()(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, base, dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        (CUtensorMapL2promotion)tile_l2_promotion(),
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Turn a head-sliced plan (make_plan_sliced, paged -> paged) into a tile plan: slabs per box, item
+// counts, and the four maps written to `maps` (host memory, 4 x 128 B; the caller copies them to
+// 64-B-aligned device memory and sets p.tmaps).  False when the geometry does not fit a tensor map
+// or shared memory (the caller then uses the VEC row kernel).
+bool tile_plan(Plan& p, void* maps) {
+  if (p.src.linear || p.dst.linear || !encode_tiled()) return false;
+  const int64_t slice = p.row, g = p.g;
+  if (slice % 16 || p.scol % 16 || p.dcol % 16 || p.spitch % 16 || p.dpitch % 16) return false;
+  const int64_t e0 = slice <= 2048 ? slice / 8 : 256;
+  if (slice % (e0 * 8) || slice / (e0 * 8) > 256 || g < 1 || g > 256) return false;
+  if (p.src.nb * (int64_t)p.src.bs >= (int64_t(1) << 31) || p.dst.nb * (int64_t)p.dst.bs >= (int64_t(1) << 31))
+    return false;
+  const int avail = smem_avail((const void*)k_copy_tiles<true, InterleavedSource, true>);
+  const int64_t run = g * slice;
+  if (2 * run > avail) return false;
+  const int64_t nlk = 2 * (int64_t)p.lm;
+  int64_t lkb = 1;
+  for (int64_t d = 1; d <= std::min<int64_t>(nlk, 256); ++d)
+    if (nlk % d == 0 && (d == 1 || run * d <= tile_target_bytes()) && 2 * run * d <= avail) lkb = d;
+  CUtensorMap* m = static_cast<CUtensorMap*>(maps);
+  if (!encode_side(&m[0], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, g, lkb) ||
+      !encode_side(&m[1], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, g, lkb) ||
+      !encode_side(&m[2], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, 1, lkb) ||
+      !encode_side(&m[3], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, 1, lkb))
+    return false;
+  p.lkb = (int32_t)lkb;
+  p.tile_bytes = (int32_t)(run * lkb);
+  p.P = 1;
+  p.items_per_chunk = (nlk / lkb) * p.R;
+  p.n_items = p.items_per_chunk * p.nchunks;
+  return true;
+}
+
+template <bool SIG, class Src>
+dyna_status launch_tiles_t(const Src& src, int64_t n_items, int tile_bytes, int stages, int max_ctas, int dev,
+                           cudaStream_t st) {
+  DevInfo* di = dev_info(dev);
+  void (*kern)(const Src, int, int) = SIG ? k_copy_tiles<SIG, Src, true> : k_copy_tiles<SIG, Src, false>;
+  const int threads = SIG ? 96 : 64;
+  if (stages <= 0) stages = 4;
+  stages = std::min(stages, kMaxStages);
+  const int avail = smem_avail((const void*)kern);
+  if ((int64_t)stages * tile_bytes > avail) stages = avail / tile_bytes;
+  if (stages < 2) return fail(DYNA_EINVAL, "tiles: two %d-B boxes do not fit in shared memory", tile_bytes);
+  const size_t smem = (size_t)stages * tile_bytes;
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  if (occ <= 0) return fail(DYNA_EINVAL, "tiles: %zu B of shared memory per CTA does not fit", smem);
+  int64_t cap = (int64_t)di->sms * occ;
+  if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
+  // round-robin sources: CTAs take local items (all n entries of one each)
+  int64_t units = n_items;
+  if constexpr (std::is_same<Src, RoundRobinSource>::value) units = n_items / src.n;
+  const unsigned grid = (unsigned)balanced_workers(units, cap);
+  const int lag = stages >= 4 ? 2 : 1;
+  CUDA_TRY(launch_kernel(kern, grid, threads, smem, st, src, stages, lag));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return DYNA_OK;
+}
+
+template <class Src>
+dyna_status launch_tiles_src(const Src& src, int64_t n_items, bool sig, int tile_bytes, int stages, int max_ctas,
+                             int dev, cudaStream_t st) {
+  if (n_items == 0) return DYNA_OK;
+  if (n_items >= (int64_t(1) << 31)) return fail(DYNA_ERANGE, "too many work items in one launch");
+  return sig ? launch_tiles_t<true>(src, n_items, tile_bytes, stages, max_ctas, dev, st)
+             : launch_tiles_t<false>(src, n_items, tile_bytes, stages, max_ctas, dev, st);
+}
+
+dyna_status launch_tiles(const Plan& p, int stages, int max_ctas, int dev, cudaStream_t st) {
+  return launch_tiles_src(SingleSource{p}, p.n_items, p.counters != nullptr, p.tile_bytes, stages, max_ctas, dev, st);
+}
+
+dyna_status launch_tiles_interleaved(const InterleavedSource& src, bool sig, int tile_bytes, int stages, int max_ctas,
+                                     int dev, cudaStream_t st) {
+  if (tile_rr())
+    return launch_tiles_src(RoundRobinSource{src.plans, src.n, src.total_items}, src.total_items, sig, tile_bytes,
+                            stages, max_ctas, dev, st);
+  return launch_tiles_src(src, src.total_items, sig, tile_bytes, stages, max_ctas, dev, st);
 }
 
 // The VEC engine on whole rows through the decoder-fed row kernel (a row is a slice of itself):

@@ -192,22 +192,40 @@ static dyna_kv_xfer* empty_xfer(const dyna_kv_pool* S) {
 }
 
 // Host-resident tables (block_ids == NULL): upload the entries the kernels may read.
+// Host-resident tables (and, for tile plans, `head_bytes` of tensor maps at the front, 256-B
+// aligned on the device: *dhead) go up in one upload-ring span on the stream.
 static dyna_status upload_tables(RingLease& lease, const dyna_block_table& src, const dyna_block_table& dst,
-                                 int64_t t1, cudaStream_t stream, const int32_t** sids, const int32_t** dids) {
+                                 int64_t t1, cudaStream_t stream, const int32_t** sids, const int32_t** dids,
+                                 const void* head = nullptr, size_t head_bytes = 0, const char** dhead = nullptr) {
   *sids = src.block_ids;
   *dids = dst.block_ids;
-  if (*sids && *dids) return DYNA_OK;
+  if (*sids && *dids && head_bytes == 0) return DYNA_OK;
+  const size_t hb = (head_bytes + 255) & ~size_t(255);
   const size_t sb = *sids ? 0 : (table_upload_bytes(src, t1) + 15) & ~size_t(15);
   const size_t db = *dids ? 0 : table_upload_bytes(dst, t1);
   char *base = nullptr, *h = nullptr;
-  dyna_status r = lease.reserve(sb + db, &base, &h, stream);
+  dyna_status r = lease.reserve(hb + sb + db, &base, &h, stream);
   if (r) return r;
-  if (!*sids) std::memcpy(h, src.host_block_ids, table_upload_bytes(src, t1));
-  if (!*dids) std::memcpy(h + sb, dst.host_block_ids, db);
+  if (head_bytes) std::memcpy(h, head, head_bytes);
+  if (!*sids) std::memcpy(h + hb, src.host_block_ids, table_upload_bytes(src, t1));
+  if (!*dids) std::memcpy(h + hb + sb, dst.host_block_ids, db);
   if ((r = lease.copy(stream))) return r;
-  if (!*sids) *sids = reinterpret_cast<const int32_t*>(base);
-  if (!*dids) *dids = reinterpret_cast<const int32_t*>(base + sb);
+  if (!*sids) *sids = reinterpret_cast<const int32_t*>(base + hb);
+  if (!*dids) *dids = reinterpret_cast<const int32_t*>(base + hb + sb);
+  if (dhead) *dhead = base;
   return DYNA_OK;
+}
+
+// Head slices: the TMA tile engine (k_copy_tiles) for DYNA_ENGINE_BULK / BULK_WS, and for AUTO
+// when the geometry fits a tensor map and the stream is not capturing (tile plans upload their maps
+// through the upload ring, which a graph replay would recycle); otherwise the VEC row kernel.
+static bool stream_capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
+}
+static bool want_tiles(const dyna_kv_opts& o, cudaStream_t st) {
+  if (o.engine == DYNA_ENGINE_BULK || o.engine == DYNA_ENGINE_BULK_WS) return true;
+  return o.engine == DYNA_ENGINE_AUTO && tiles_enabled() && !stream_capturing(st);
 }
 
 static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
@@ -512,8 +530,7 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
     return fail(DYNA_EGEOM, "head slices must be multiples of 16 bytes (d*e = %lld)", (long long)head_bytes);
   if (nh == gs.num_kv_heads && nh == gd.num_kv_heads)  // whole rows on both sides: the plain migration
     return migrate_impl(src, dst, tr, lr, chunk_tokens, stream_, opts, nullptr, 0, out);
-  if (o.variant == DYNA_VARIANT_STAGED || (o.engine && o.engine != DYNA_ENGINE_VEC))
-    return fail(DYNA_ENOTSUP, "head-sliced migration: FUSED variant, VEC engine only");
+  if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "head-sliced migration: FUSED variant only");
   const int64_t ntok = tr.end - tr.begin;
   const int64_t nchunks = (empty || nh == 0) ? 0 : (ntok + chunk_tokens - 1) / chunk_tokens;
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
@@ -530,21 +547,33 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
   const int piece = o.piece_bytes ? o.piece_bytes : kVecPiece;
 
   DeviceGuard guard(S->dev);
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  Plan p = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), nh * head_bytes, S->row,
+                            src_heads.begin * head_bytes, D->row, (int64_t)dst_head_begin * head_bytes, tr.begin,
+                            tr.end, l0, lm, chunk_tokens, gcd64(gs.block_size, gd.block_size), piece);
+  alignas(64) char maps[kTileMaps * kTileMapBytes];
+  const bool tiles = want_tiles(o, stream) && tile_plan(p, maps);
+  if (!tiles && o.engine != DYNA_ENGINE_AUTO && o.engine != DYNA_ENGINE_VEC)
+    return fail(DYNA_ENOTSUP, "head slices of %lld B on the BULK engine: the geometry does not fit a TMA tensor map "
+                              "(or the stream is capturing); use DYNA_ENGINE_VEC", (long long)(nh * head_bytes));
   RingLease lease(S->dev);
   const int32_t *sids = nullptr, *dids = nullptr;
-  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids))) return r;
+  const char* dmaps = nullptr;
+  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids, tiles ? maps : nullptr,
+                         tiles ? sizeof(maps) : 0, &dmaps)))
+    return r;
+  p.src.table = sids;
+  p.dst.table = dids;
+  if (tiles) p.tmaps = dmaps;
   dyna_kv_xfer* x = nullptr;
   if ((r = new_xfer(S->dev, gs.instance, stream, &x))) return r;
   x->nchunks = (int32_t)nchunks;
   x->variant = DYNA_VARIANT_FUSED;
-  x->engine = DYNA_ENGINE_VEC;
-  x->piece = piece;
-  x->unroll = 8;
+  x->engine = tiles ? DYNA_ENGINE_BULK : DYNA_ENGINE_VEC;
+  x->piece = tiles ? p.tile_bytes : piece;
+  x->unroll = tiles ? 0 : 8;
+  x->stages = tiles ? (o.stages ? o.stages : 4) : 0;
   const uint64_t launches0 = g_launches.load();
-  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
-  Plan p = make_plan_sliced(paged(S, sids), paged(D, dids), nh * head_bytes, S->row, src_heads.begin * head_bytes,
-                            D->row, (int64_t)dst_head_begin * head_bytes, tr.begin, tr.end, l0, lm, chunk_tokens,
-                            gcd64(gs.block_size, gd.block_size), piece);
   p.err = x->err;
   if (signal) {
     uint64_t epoch = 0;
@@ -560,7 +589,7 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
     x->first_slot = first;
     p.sys_fence = peer_dst;
   }
-  r = launch_rows(p, o.max_ctas, S->dev, stream);
+  r = tiles ? launch_tiles(p, o.stages, o.max_ctas, S->dev, stream) : launch_rows(p, o.max_ctas, S->dev, stream);
   if (!r) r = lease.finish(stream);
   if (r) {
     delete x;
@@ -683,8 +712,7 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   dyna_status r = check_opts(opts, &o);
   if (r) return r;
   if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
-  if (o.variant == DYNA_VARIANT_STAGED || (o.engine && o.engine != DYNA_ENGINE_VEC))
-    return fail(DYNA_ENOTSUP, "reshard: FUSED variant, VEC engine only");
+  if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "reshard: FUSED variant only");
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
   const bool unchecked = (o.flags & DYNA_MIGRATE_UNCHECKED) != 0;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
@@ -760,7 +788,39 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
     }
   }
   const int piece = o.piece_bytes ? o.piece_bytes : kVecPiece;
-  const size_t plans_b = ((n * sizeof(Plan)) + 15) & ~size_t(15);
+  // Plans first (tables and maps patched in once the upload span is known): a tile launch needs
+  // every entry's geometry to fit a tensor map.
+  std::vector<Plan> plans(n);
+  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
+  std::vector<char> maps_h;
+  bool tiles = want_tiles(o, stream);
+  if (tiles) maps_h.resize((size_t)n * kTileMaps * kTileMapBytes + 64);
+  char* maps = tiles ? reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(maps_h.data()) + 63) & ~uintptr_t(63))
+                     : nullptr;
+  for (int32_t i = 0; i < n; ++i) {
+    const dyna_kv_head_migration& m = migs[i];
+    dyna_kv_pool *S = m.src.pool, *D = m.dst.pool;
+    const int64_t he = (int64_t)S->desc.head_dim * S->desc.elem_bytes;
+    plans[i] = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), slice, S->row, m.src_heads.begin * he, D->row,
+                                (int64_t)m.dst_head_begin * he, tr.begin, tr.end, l0, lm, chunk_tokens, g, piece);
+    if (tiles) tiles = tile_plan(plans[i], maps + (size_t)i * kTileMaps * kTileMapBytes);
+  }
+  if (!tiles && o.engine != DYNA_ENGINE_AUTO && o.engine != DYNA_ENGINE_VEC) {
+    delete x;
+    return fail(DYNA_ENOTSUP, "reshard slices of %lld B on the BULK engine: the geometry does not fit a TMA tensor "
+                              "map (or the stream is capturing); use DYNA_ENGINE_VEC", (long long)slice);
+  }
+  if (!tiles)  // an entry that did not fit: every entry back on the row kernel's plan
+    for (int32_t i = 0; i < n; ++i) {
+      const dyna_kv_head_migration& m = migs[i];
+      dyna_kv_pool *S = m.src.pool, *D = m.dst.pool;
+      const int64_t he = (int64_t)S->desc.head_dim * S->desc.elem_bytes;
+      plans[i] = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), slice, S->row, m.src_heads.begin * he,
+                                  D->row, (int64_t)m.dst_head_begin * he, tr.begin, tr.end, l0, lm, chunk_tokens, g,
+                                  piece);
+    }
+  const size_t maps_b = tiles ? (size_t)n * kTileMaps * kTileMapBytes : 0;  // multiple of 256
+  const size_t plans_b = maps_b + (((n * sizeof(Plan)) + 15) & ~size_t(15));
   std::vector<size_t> soff(n, 0), doff(n, 0);
   size_t tab_b = 0;
   for (int32_t i = 0; i < n; ++i) {
@@ -779,16 +839,12 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
     delete x;
     return r;
   }
-  std::vector<Plan> plans(n);
-  const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
   for (int32_t i = 0; i < n; ++i) {
     const dyna_kv_head_migration& m = migs[i];
     dyna_kv_pool *S = m.src.pool, *D = m.dst.pool;
-    const int64_t he = (int64_t)S->desc.head_dim * S->desc.elem_bytes;
-    const int32_t* sids = m.src.block_ids ? m.src.block_ids : reinterpret_cast<const int32_t*>(dbase + soff[i]);
-    const int32_t* dids = m.dst.block_ids ? m.dst.block_ids : reinterpret_cast<const int32_t*>(dbase + doff[i]);
-    plans[i] = make_plan_sliced(paged(S, sids), paged(D, dids), slice, S->row, m.src_heads.begin * he, D->row,
-                                (int64_t)m.dst_head_begin * he, tr.begin, tr.end, l0, lm, chunk_tokens, g, piece);
+    plans[i].src.table = m.src.block_ids ? m.src.block_ids : reinterpret_cast<const int32_t*>(dbase + soff[i]);
+    plans[i].dst.table = m.dst.block_ids ? m.dst.block_ids : reinterpret_cast<const int32_t*>(dbase + doff[i]);
+    if (tiles) plans[i].tmaps = dbase + (size_t)i * kTileMaps * kTileMapBytes;
     plans[i].err = x->err;
     if (signal) {
       const dyna_kv_xfer::BatchEntry& be = x->batch[i];
@@ -803,7 +859,8 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
       plans[i].sys_fence = (D->dev != S->dev || D->imported) ? 1 : 0;
     }
   }
-  std::memcpy(h, plans.data(), n * sizeof(Plan));
+  if (tiles) std::memcpy(h, maps, maps_b);
+  std::memcpy(h + maps_b, plans.data(), n * sizeof(Plan));
   for (int32_t i = 0; i < n; ++i) {
     if (!migs[i].src.block_ids) std::memcpy(h + soff[i], migs[i].src.host_block_ids, table_upload_bytes(migs[i].src, tr.end));
     if (!migs[i].dst.block_ids) std::memcpy(h + doff[i], migs[i].dst.host_block_ids, table_upload_bytes(migs[i].dst, tr.end));
@@ -812,14 +869,16 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
     delete x;
     return r;
   }
-  InterleavedSource isrc{reinterpret_cast<const Plan*>(dbase), n, plans[0].n_items * n};
+  InterleavedSource isrc{reinterpret_cast<const Plan*>(dbase + maps_b), n, plans[0].n_items * n};
   x->variant = DYNA_VARIANT_FUSED;
-  x->engine = DYNA_ENGINE_VEC;
-  x->piece = piece;
-  x->unroll = 8;
+  x->engine = tiles ? DYNA_ENGINE_BULK : DYNA_ENGINE_VEC;
+  x->piece = tiles ? plans[0].tile_bytes : piece;
+  x->unroll = tiles ? 0 : 8;
+  x->stages = tiles ? (o.stages ? o.stages : 4) : 0;
   x->nchunks = (int32_t)nchunks;
   const uint64_t launches0 = g_launches.load();
-  r = launch_rows_interleaved(isrc, signal, o.max_ctas, S0->dev, stream);
+  r = tiles ? launch_tiles_interleaved(isrc, signal, plans[0].tile_bytes, o.stages, o.max_ctas, S0->dev, stream)
+            : launch_rows_interleaved(isrc, signal, o.max_ctas, S0->dev, stream);
   if (!r) r = lease.finish(stream);
   if (r) {
     delete x;

@@ -55,7 +55,16 @@ struct Plan {
   int32_t scol, dcol;       // byte offset of the slice inside a row
   int32_t tpp;              // tokens per work item
   int32_t vps, vps_shift;   // 16-B vectors per slice; log2(vps) or -1
+  // TMA tensor tiles (k_copy_tiles: head slices on the BULK engine).  An item is one run of a
+  // chunk across `lkb` consecutive (layer, K|V) slabs: a box of slice x rows x lkb, moved by
+  // one tensor load and one tensor store through the maps at `tmaps` (global memory, 64-B
+  // aligned: source run box, destination run box, source row box, destination row box).
+  const char* tmaps;        // nullptr: not a tile plan
+  int32_t lkb;              // slabs per box (divides 2*lm)
+  int32_t tile_bytes;       // bytes of a full-run box: g * row * lkb
 };
+constexpr int kTileMapBytes = 128;  // sizeof(CUtensorMap)
+constexpr int kTileMaps = 4;        // per plan
 
 enum : unsigned { ERR_BAD_BLOCK = 1u, ERR_TIMEOUT = 2u };
 
@@ -106,6 +115,22 @@ struct InterleavedSource {
     const int64_t per = total_items / n;
     const int32_t r = (int32_t)(item / per);
     item -= (int64_t)r * per;
+    return plans[r];
+  }
+  __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }
+};
+
+// The same n plans, items grouped by local item: global item g is item g / n of plan g % n, and
+// the tile kernel hands a CTA all n entries of one local item back to back, so the same token rows
+// of every entry are read (a TP scatter) or written (a TP gather) together.  Tile kernel only.
+struct RoundRobinSource {
+  const Plan* plans;
+  int32_t n;
+  int64_t total_items;
+  __device__ __forceinline__ int64_t total() const { return total_items; }
+  __device__ __forceinline__ const Plan& locate(int64_t& item) const {
+    const int32_t r = (int32_t)(item % n);
+    item /= n;
     return plans[r];
   }
   __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }

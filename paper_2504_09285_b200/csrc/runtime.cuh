@@ -381,6 +381,12 @@ dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st);
 dyna_status launch_rows_interleaved(const InterleavedSource& src, bool sig, int max_ctas, int dev, cudaStream_t st);
 dyna_status launch_rows_batch(const BatchSource& src, bool sig, int max_ctas, int dev, cudaStream_t st);
 bool fed_vec_enabled();
+// head slices as TMA tensor tiles (k_copy_tiles)
+bool tiles_enabled();
+bool tile_plan(Plan& p, void* maps);  // maps: kTileMaps x kTileMapBytes of host memory
+dyna_status launch_tiles(const Plan& p, int stages, int max_ctas, int dev, cudaStream_t st);
+dyna_status launch_tiles_interleaved(const InterleavedSource& src, bool sig, int tile_bytes, int stages, int max_ctas,
+                                     int dev, cudaStream_t st);
 dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, const int32_t* dids, dyna_range tr,
                        int l0, int lm, int64_t c, bool signal, int engine, int piece, int stages, int unroll,
                        int max_ctas, cudaStream_t stream, dyna_kv_xfer* x, int schedule);

@@ -41,6 +41,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=1024)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--quick", action="store_true", help="a few representative cases (A/B runs)")
+    ap.add_argument("--engines", default="rows,tiles", help="rows (VEC row kernel) and/or tiles (TMA tensor tiles)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "reshard.json"))
     args = ap.parse_args()
     torch.cuda.set_device(0)
@@ -55,7 +56,10 @@ def main():
     if args.quick:
         cases = [cases[i] for i in (2, 3, 6, 8, 13)]
 
-    def measure(name, g0, gs, gd, ts_, td_, plan, mode, once):
+    engines = {"rows": dk.DYNA_ENGINE_VEC, "tiles": dk.DYNA_ENGINE_BULK}
+    engines = {k: engines[k] for k in args.engines.split(",")}
+
+    def measure(name, g0, gs, gd, ts_, td_, plan, mode, once, eng):
         # reps back to back between two events (the host issues rep k+1 while rep k runs, as a
         # serving loop would); the host time per rep is reported beside it
         for _ in range(3):
@@ -63,9 +67,11 @@ def main():
                 dk.dyna_kv_wait(x)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t = time.perf_counter()
+        # one untimed rep is enqueued first, so the device is busy when e0 is reached and the timed
+        # region does not start with one call's host latency (validation, uploads) of idle device
+        xs = once()
         e0.record(stream)
-        xs = []
+        t = time.perf_counter()
         for _ in range(args.reps):
             xs += once()
         e1.record(stream)
@@ -76,7 +82,7 @@ def main():
         ms = e0.elapsed_time(e1) / args.reps
         payload = s * 2 * g0.num_layers * g0.row_bytes
         gb = payload / (ms / 1e3) / 1e9
-        r = {"model": name, "tp_src": ts_, "tp_dst": td_, "mode": mode, "s": s, "chunk": c, "calls": len(plan),
+        r = {"model": name, "tp_src": ts_, "tp_dst": td_, "mode": mode, "engine": eng, "s": s, "chunk": c, "calls": len(plan),
              "slice_bytes": min(gs.row_bytes, gd.row_bytes), "payload_bytes": payload, "ms": ms, "GBps": gb,
              "hbm_rw_GBps": 2 * gb, "frac_of_measured_hbm": 2 * gb / pk, "host_ms_per_reshard": host_ms}
         print(json.dumps(r), flush=True)
@@ -97,17 +103,20 @@ def main():
               ((p, kvgen.table_pair(20 + i, s, gd, gd)[1]) for i, p in enumerate(dst))]
         plan = dd.tp_reshard_plan(H, ts_, td_)
 
-        def calls():
-            return [dk.dyna_kv_migrate_heads(st[a], dt[b], (0, s), (0, L), heads, hd0, c, cs)
-                    for a, b, heads, hd0 in plan]
+        for eng, e in engines.items():
+            o = dk.opts(engine=e)
 
-        def fused():
-            return [dk.dyna_kv_reshard([(st[a], dt[b], heads, hd0) for a, b, heads, hd0 in plan], (0, s), (0, L), c,
-                                       cs)]
-        for mode, once in (("calls", calls), ("one_launch", fused)):
-            if mode == "one_launch" and len(plan) == 1 and ts_ == td_ == 1:
-                continue
-            measure(name, g0, gs, gd, ts_, td_, plan, mode, once)
+            def calls():
+                return [dk.dyna_kv_migrate_heads(st[a], dt[b], (0, s), (0, L), heads, hd0, c, cs, o)
+                        for a, b, heads, hd0 in plan]
+
+            def fused():
+                return [dk.dyna_kv_reshard([(st[a], dt[b], heads, hd0) for a, b, heads, hd0 in plan], (0, s), (0, L),
+                                           c, cs, o)]
+            for mode, once in (("calls", calls), ("one_launch", fused)):
+                if ts_ == td_ == 1 and (mode == "one_launch" or eng != "rows"):
+                    continue   # whole rows: the plain migration (ring), one line
+                measure(name, g0, gs, gd, ts_, td_, plan, mode, once, eng)
         del src, dst, st, dt
         torch.cuda.empty_cache()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)

@@ -18,7 +18,11 @@ from gpu_util import dev_table, pool_filled, pool_from_host
 pytestmark = pytest.mark.gpu
 
 
-def _heads_parity(gs, gd, n_tok, tr, lr, c, heads, hd0, seed=1, flags=0, piece=0, with_host=True):
+ENGINES = [dk.DYNA_ENGINE_AUTO, dk.DYNA_ENGINE_VEC]   # AUTO = the TMA tile kernel where the geometry fits
+ENGINE_IDS = ["tiles", "rows"]
+
+
+def _heads_parity(gs, gd, n_tok, tr, lr, c, heads, hd0, seed=1, flags=0, piece=0, with_host=True, engine=0):
     ts, td = kvgen.table_pair(seed + 100, n_tok, gs, gd)
     hs, hd = kvgen.fill_bytes(seed, gs.pool_bytes), kvgen.fill_bytes(seed + 1, gd.pool_bytes)
     want = hd.copy()
@@ -27,8 +31,11 @@ def _heads_parity(gs, gd, n_tok, tr, lr, c, heads, hd0, seed=1, flags=0, piece=0
     st, dt = dev_table(src, ts, with_host), dev_table(dst, td, with_host)
     if not with_host:
         flags |= dk.DYNA_MIGRATE_UNCHECKED
-    x = dk.dyna_kv_migrate_heads(st, dt, tr, lr, heads, hd0, c, 0, dk.opts(flags=flags, piece_bytes=piece))
+    x = dk.dyna_kv_migrate_heads(st, dt, tr, lr, heads, hd0, c, 0, dk.opts(flags=flags, piece_bytes=piece,
+                                                                            engine=engine))
     info = dk.dyna_kv_xfer_info(x)
+    if engine == dk.DYNA_ENGINE_AUTO and heads[1] - heads[0] not in (0, gs.num_kv_heads):
+        assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_BULK, "AUTO head slices should run as TMA tiles"
     dk.dyna_kv_wait(x)
     got = dst.tensor.cpu().numpy()
     assert np.array_equal(src.tensor.cpu().numpy(), hs), "source pool modified"
@@ -50,26 +57,42 @@ G1 = Geom(3, 1, 64, 2, 32, 24)      # TP-8 shard
     (G2, G4, (0, 2), 1), (G8, G8, (3, 6), 1), (G8, G8, (0, 8), 0), (G4, G4, (2, 3), 2),
 ])
 @pytest.mark.parametrize("c", [7, 16, 64, 500])
-def test_heads_parity(gs, gd, heads, hd0, c):
-    _heads_parity(gs, gd, 500, (0, 451), (0, 3), c, heads, hd0)
+@pytest.mark.parametrize("engine", ENGINES, ids=ENGINE_IDS)
+def test_heads_parity(gs, gd, heads, hd0, c, engine):
+    _heads_parity(gs, gd, 500, (0, 451), (0, 3), c, heads, hd0, engine=engine)
 
 
 @pytest.mark.parametrize("tr,lr", [((13, 400), (0, 3)), ((0, 1), (1, 2)), ((31, 33), (2, 3)), ((0, 500), (0, 3))])
 @pytest.mark.parametrize("piece", [0, 256, 1024, 65536])
-def test_heads_subranges_and_pieces(tr, lr, piece):
-    _heads_parity(G8, G2, 500, tr, lr, 48, (5, 7), 0, piece=piece)
+@pytest.mark.parametrize("engine", ENGINES, ids=ENGINE_IDS)
+def test_heads_subranges_and_pieces(tr, lr, piece, engine):
+    _heads_parity(G8, G2, 500, tr, lr, 48, (5, 7), 0, piece=piece, engine=engine)
 
 
 @pytest.mark.parametrize("bss,bsd", [(16, 32), (32, 16), (16, 24), (8, 16)])
-def test_heads_reblocking(bss, bsd):
+@pytest.mark.parametrize("engine", ENGINES, ids=ENGINE_IDS)
+def test_heads_reblocking(bss, bsd, engine):
     gs = G8.with_(block_size=bss, num_blocks=40 * 16 // bss)
     gd = G2.with_(block_size=bsd, num_blocks=96 * 8 // bsd + 8)
-    _heads_parity(gs, gd, 500, (3, 467), (0, 3), 40, (4, 6), 0)
+    _heads_parity(gs, gd, 500, (3, 467), (0, 3), 40, (4, 6), 0, engine=engine)
 
 
-def test_heads_signal_flags_and_host_tables():
+@pytest.mark.parametrize("L,lr", [(5, (0, 5)), (5, (1, 4)), (7, (2, 7)), (40, (0, 40)), (40, (3, 38))])
+@pytest.mark.parametrize("slice_heads", [1, 3, 4])
+def test_tiles_slab_groups(L, lr, slice_heads):
+    """The tile kernel's boxes span lkb (layer, K|V) slabs, lkb a divisor of 2*lm: odd layer counts,
+    layer sub-ranges, prime slab counts (2*lm = 6, 10, 70) and 1..4-head slices (box bytes from 2 KiB to
+    48 KiB before the slab factor) against the oracle."""
+    gs = Geom(L, 8, 64, 2, 16, 24)
+    gd = Geom(L, 4, 64, 2, 16, 30)
+    _heads_parity(gs, gd, 300, (5, 290), lr, 64, (1, 1 + slice_heads), 4 - slice_heads, seed=L + slice_heads)
+
+
+@pytest.mark.parametrize("engine", ENGINES, ids=ENGINE_IDS)
+def test_heads_signal_flags_and_host_tables(engine):
     src, dst, (epoch, nck, sender, first) = _heads_parity(G8, G4, 500, (0, 451), (0, 3), 64, (4, 8), 0,
-                                                          flags=dk.DYNA_MIGRATE_SIGNAL, with_host=False)
+                                                          flags=dk.DYNA_MIGRATE_SIGNAL, with_host=False,
+                                                          engine=engine)
     assert nck == 8 and epoch > 0
     fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
     dk.dyna_kv_copy_flags(dst.handle, sender, first, nck, fl.data_ptr(), 0)
@@ -81,7 +104,7 @@ def test_heads_signal_flags_and_host_tables():
     hd = dst.tensor.cpu().numpy()
     want = hd.copy()
     oracle.migrate_heads(src.tensor.cpu().numpy(), G8, ts, want, G4, td, (100, 300), (1, 3), (0, 2), 2)
-    dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(st, dt, (100, 300), (1, 3), (0, 2), 2, 32, 0, None))
+    dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(st, dt, (100, 300), (1, 3), (0, 2), 2, 32, 0, dk.opts(engine=engine)))
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
 
 
@@ -100,8 +123,12 @@ def test_heads_empty_and_errors():
     with pytest.raises(dk.DynaKVError) as e:
         dk.dyna_kv_migrate_heads(st, dt, (0, 100), (0, 3), (0, 2), 0, 32, 0, dk.opts(variant=dk.DYNA_VARIANT_STAGED))
     assert e.value.status == dk.DYNA_ENOTSUP
-    with pytest.raises(dk.DynaKVError) as e:
-        dk.dyna_kv_migrate_heads(st, dt, (0, 100), (0, 3), (0, 2), 0, 32, 0, dk.opts(engine=dk.DYNA_ENGINE_BULK))
+    gw = Geom(3, 20, 64, 2, 16, 48)          # 2304-B slices: more than one 2-KiB box row, not a multiple of it
+    wide_s, wide_d = pool_filled(gw, 4), pool_filled(gw, 5)
+    tw = kvgen.table_pair(6, 200, gw, gw)
+    with pytest.raises(dk.DynaKVError) as e:  # the BULK (tile) engine refuses a slice no tensor map can describe
+        dk.dyna_kv_migrate_heads(dev_table(wide_s, tw[0]), dev_table(wide_d, tw[1]), (0, 100), (0, 3), (0, 18), 1, 32,
+                                 0, dk.opts(engine=dk.DYNA_ENGINE_BULK))
     assert e.value.status == dk.DYNA_ENOTSUP
     other = pool_filled(Geom(2, 4, 64, 2, 16, 48), 3)
     with pytest.raises(dk.DynaKVError) as e:               # L differs
@@ -112,7 +139,8 @@ def test_heads_empty_and_errors():
 
 
 @pytest.mark.parametrize("tp_s,tp_d", [(1, 4), (4, 1), (2, 4), (4, 2), (2, 8)])
-def test_tp_reshard_round_trip_full_llama3_rows(tp_s, tp_d):
+@pytest.mark.parametrize("engine", ENGINES, ids=ENGINE_IDS)
+def test_tp_reshard_round_trip_full_llama3_rows(tp_s, tp_d, engine):
     """Llama-3-8B rows (8 KV heads, d128, bf16): a request's KV sharded over tp_s source ranks is
     resharded onto tp_d destination ranks with dd.tp_reshard_plan (one dyna_kv_migrate_heads per
     overlapping rank pair, all on one GPU here), then gathered back into a TP-1 pool: the result
@@ -136,7 +164,7 @@ def test_tp_reshard_round_trip_full_llama3_rows(tp_s, tp_d):
     for a, b, heads, hd0 in dd.tp_reshard_plan(H, tp_s, tp_d):     # the reshard under test
         t = (dev_table(src_pools[a], src_tabs[a]), dev_table(dst_pools[b], dst_tabs[b]))
         keep.append(t)
-        xs.append(dk.dyna_kv_migrate_heads(*t, (0, s), (0, L), heads, hd0, 256, 0))
+        xs.append(dk.dyna_kv_migrate_heads(*t, (0, s), (0, L), heads, hd0, 256, 0, dk.opts(engine=engine)))
     for x in xs:
         dk.dyna_kv_wait(x)
     back = pool_filled(g1, 60)
@@ -203,7 +231,8 @@ def test_full_size_qwen72b_tp4_to_tp8_sampled():
 # ---------------------------------------------------------------- dyna_kv_reshard: the whole plan, one launch
 @pytest.mark.parametrize("tp_s,tp_d", [(1, 8), (8, 1), (2, 4), (4, 2), (2, 8), (8, 2), (1, 2), (4, 4)])
 @pytest.mark.parametrize("signal", [False, True])
-def test_reshard_one_launch_matches_oracle(tp_s, tp_d, signal):
+@pytest.mark.parametrize("engine", ENGINES, ids=ENGINE_IDS)
+def test_reshard_one_launch_matches_oracle(tp_s, tp_d, signal, engine):
     """Every rank pair of dd.tp_reshard_plan in ONE dyna_kv_reshard launch (interleaved items):
     every destination shard equals the oracle applying oracle.migrate_heads per pair; with
     signalling every entry's flags reach its own epoch."""
@@ -225,7 +254,10 @@ def test_reshard_one_launch_matches_oracle(tp_s, tp_d, signal):
     dt = [dev_table(p, t) for p, t in zip(dst, td)]
     migs = [(st[a], dt[b], heads, hd0) for a, b, heads, hd0 in plan]
     n0 = dk.dyna_kv_launch_count()
-    x = dk.dyna_kv_reshard(migs, (0, s), (0, L), c, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0))
+    x = dk.dyna_kv_reshard(migs, (0, s), (0, L), c, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0,
+                                                                engine=engine))
+    if engine == dk.DYNA_ENGINE_AUTO and tp_s != tp_d:
+        assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_BULK
     infos = [dk.dyna_kv_batch_info(x, i) for i in range(len(migs))] if signal else []
     dk.dyna_kv_wait(x)
     assert dk.dyna_kv_launch_count() - n0 == 1
