@@ -1350,6 +1350,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
   const int32_t slot = p.tile_bytes;
   const uint32_t g = (uint32_t)p.g;
   const uint32_t row_box = (uint32_t)(p.row * p.lkb);  // bytes of one single-row box
+  const uint32_t rstride = (uint32_t)p.tile_rstride;   // its smem stride (128-B aligned)
   // Maps were written by a host copy: acquire them for the tensormap proxy before first use.  Up to
   // 64 plans all at once here (round-robin launches change plans every item), else lazily.
   const char* fenced = nullptr;
@@ -1394,7 +1395,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
     if (d.rows == g) {
       tma_load_4d(sl, d.tm, d.ys, d.lk, &full[s]);
     } else {
-      for (uint32_t r = 0; r < d.rows; ++r) tma_load_4d(sl + r * row_box, d.tm + 2 * kTileMapBytes, d.ys + r, d.lk, &full[s]);
+      for (uint32_t r = 0; r < d.rows; ++r) tma_load_4d(sl + r * rstride, d.tm + 2 * kTileMapBytes, d.ys + r, d.lk, &full[s]);
     }
     pend[s] = d;
   };
@@ -1432,7 +1433,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
     if (d.rows == g) {
       tma_store_4d(d.tm + kTileMapBytes, sl, d.yd, d.lk);
     } else {
-      for (uint32_t r = 0; r < d.rows; ++r) tma_store_4d(d.tm + 3 * kTileMapBytes, sl + r * row_box, d.yd + r, d.lk);
+      for (uint32_t r = 0; r < d.rows; ++r) tma_store_4d(d.tm + 3 * kTileMapBytes, sl + r * rstride, d.yd + r, d.lk);
     }
     bulk_commit();
     if (SIGNAL) {

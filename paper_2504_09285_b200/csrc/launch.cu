@@ -481,11 +481,11 @@ bool tile_plan(Plan& p, void* maps) {
     return false;
   const int avail = smem_avail((const void*)k_copy_tiles<true, InterleavedSource, true>);
   const int64_t run = g * slice;
-  if (2 * run > avail) return false;
+  if (2 * (run + 1024) > avail) return false;
   const int64_t nlk = 2 * (int64_t)p.lm;
   int64_t lkb = 1;
   for (int64_t d = 1; d <= std::min<int64_t>(nlk, 256); ++d)
-    if (nlk % d == 0 && (d == 1 || run * d <= tile_target_bytes()) && 2 * run * d <= avail) lkb = d;
+    if (nlk % d == 0 && (d == 1 || run * d <= tile_target_bytes()) && 2 * (run * d + 1024) <= avail) lkb = d;
   CUtensorMap* m = static_cast<CUtensorMap*>(maps);
   if (!encode_side(&m[0], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, g, lkb) ||
       !encode_side(&m[1], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, g, lkb) ||
@@ -493,7 +493,8 @@ bool tile_plan(Plan& p, void* maps) {
       !encode_side(&m[3], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, 1, lkb))
     return false;
   p.lkb = (int32_t)lkb;
-  p.tile_bytes = (int32_t)(run * lkb);
+  p.tile_rstride = (int32_t)((slice * lkb + 127) / 128 * 128);
+  p.tile_bytes = (int32_t)((std::max<int64_t>(run * lkb, (g - 1) * p.tile_rstride) + 1023) / 1024 * 1024);
   p.P = 1;
   p.items_per_chunk = (nlk / lkb) * p.R;
   p.n_items = p.items_per_chunk * p.nchunks;

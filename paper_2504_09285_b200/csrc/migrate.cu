@@ -303,6 +303,23 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     ch.unroll = 8;
     if (!o.piece_bytes) ch.piece = kVecPiece;
   }
+  const int64_t g = gcd64(gs.block_size, gd.block_size);
+  // Short contiguous runs (small rows: e.g. one KV head per TP rank, 256-B rows in 4-KiB blocks) on
+  // the same device: AUTO moves whole rows as TMA tiles (a row is a slice of itself; one box spans
+  // several (layer, K|V) slabs, so items are ~32 KiB whatever the block).
+  alignas(64) char maps[kTileMaps * kTileMapBytes];
+  Plan tp{};
+  const bool tiles = ch.variant == DYNA_VARIANT_FUSED && !board && !peer_dst && !o.engine &&
+                     o.schedule != DYNA_SCHED_DYNAMIC && std::min<int64_t>(g, c) * row < kTileRunMax &&
+                     tiles_enabled() && !stream_capturing(stream) &&
+                     tile_plan(tp = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), row, row, 0, row, 0,
+                                                     tr.begin, tr.end, l0, lm, c, g, ch.piece),
+                               maps);
+  if (tiles) {
+    ch.engine = DYNA_ENGINE_BULK;
+    ch.piece = tp.tile_bytes;
+    ch.stages = o.stages ? o.stages : 4;
+  }
   const int variant = ch.variant, engine = ch.engine, piece = ch.piece, stages = ch.stages, unroll = ch.unroll;
 
   DeviceGuard guard(S->dev);
@@ -310,7 +327,10 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     return fail(DYNA_ENOTSUP, "cross-device STAGED needs device block_ids for the destination");
   RingLease lease(S->dev);
   const int32_t *sids = nullptr, *dids = nullptr;
-  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids))) return r;
+  const char* dmaps = nullptr;
+  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids, tiles ? maps : nullptr,
+                         tiles ? sizeof(maps) : 0, &dmaps)))
+    return r;
 
   dyna_kv_xfer* x = nullptr;
   if ((r = new_xfer(S->dev, gs.instance, stream, &x))) return r;
@@ -323,11 +343,17 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const uint64_t launches0 = g_launches.load();
   if (variant == DYNA_VARIANT_FUSED) {
     // K4 / K4-local: source rows -> destination rows, one launch for all chunks.
-    const int64_t g = gcd64(gs.block_size, gd.block_size);
-    const bool fed = engine == DYNA_ENGINE_VEC && !board && o.schedule != DYNA_SCHED_DYNAMIC && fed_vec_enabled();
-    Plan p = fed ? make_plan_sliced(paged(S, sids), paged(D, dids), row, row, 0, row, 0, tr.begin, tr.end, l0, lm, c,
-                                    g, piece)
-                 : make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
+    const bool fed = !tiles && engine == DYNA_ENGINE_VEC && !board && o.schedule != DYNA_SCHED_DYNAMIC &&
+                     fed_vec_enabled();
+    Plan p = tiles ? tp
+             : fed ? make_plan_sliced(paged(S, sids), paged(D, dids), row, row, 0, row, 0, tr.begin, tr.end, l0, lm,
+                                      c, g, piece)
+                   : make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
+    if (tiles) {
+      p.src.table = sids;
+      p.dst.table = dids;
+      p.tmaps = dmaps;
+    }
     p.err = x->err;
     if (ctx) set_chunking(p, ctx->mig_t0, tr.end, c);
     if (signal) {
@@ -360,8 +386,9 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
       x->ready_epoch = ready_epoch;
       r = launch_ready(p, o.max_ctas, S->dev, stream, o.schedule);
     } else {
-      r = fed ? launch_rows(p, o.max_ctas, S->dev, stream)
-              : launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream, o.schedule);
+      r = tiles ? launch_tiles(p, stages, o.max_ctas, S->dev, stream)
+          : fed ? launch_rows(p, o.max_ctas, S->dev, stream)
+                : launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream, o.schedule);
     }
   } else {
     r = run_staged(S, D, sids, dids, tr, l0, lm, c, signal, engine, piece, stages, unroll, o.max_ctas, stream, x,

@@ -61,7 +61,9 @@ struct Plan {
   // aligned: source run box, destination run box, source row box, destination row box).
   const char* tmaps;        // nullptr: not a tile plan
   int32_t lkb;              // slabs per box (divides 2*lm)
-  int32_t tile_bytes;       // bytes of a full-run box: g * row * lkb
+  int32_t tile_bytes;       // shared-memory ring slot: a full-run box (g * row * lkb B), or the single-row
+                            // boxes of a shorter run at tile_rstride apart, rounded up to 1 KiB
+  int32_t tile_rstride;     // smem stride of single-row boxes: row * lkb rounded up to 128 B (TMA alignment)
 };
 constexpr int kTileMapBytes = 128;  // sizeof(CUtensorMap)
 constexpr int kTileMaps = 4;        // per plan

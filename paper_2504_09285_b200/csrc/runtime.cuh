@@ -59,6 +59,7 @@ constexpr int kVecPiece = 8192;
 constexpr int kBulkPiece = 32768;
 constexpr int kBulkStages = 4;
 constexpr int64_t kMinBulkRun = 16384;  // AUTO never picks BULK below this contiguous run length
+constexpr int64_t kTileRunMax = 32768;  // AUTO moves whole rows as TMA tiles below this contiguous run length
 constexpr int64_t kStageSlotBytes = 64ll << 20;  // staged variant: bytes per staging slot
 constexpr uint32_t kSchedSlots = 1u << 15;       // dynamic-scheduling counter slots per device
 constexpr size_t kInboxBytes = sizeof(unsigned long long) * DYNA_MAX_INSTANCES * DYNA_MAX_CHUNKS;

@@ -79,12 +79,13 @@ def test_heads_reblocking(bss, bsd, engine):
 
 @pytest.mark.parametrize("L,lr", [(5, (0, 5)), (5, (1, 4)), (7, (2, 7)), (40, (0, 40)), (40, (3, 38))])
 @pytest.mark.parametrize("slice_heads", [1, 3, 4])
-def test_tiles_slab_groups(L, lr, slice_heads):
+@pytest.mark.parametrize("d", [64, 8], ids=["128B-heads", "16B-heads"])
+def test_tiles_slab_groups(L, lr, slice_heads, d):
     """The tile kernel's boxes span lkb (layer, K|V) slabs, lkb a divisor of 2*lm: odd layer counts,
     layer sub-ranges, prime slab counts (2*lm = 6, 10, 70) and 1..4-head slices (box bytes from 2 KiB to
     48 KiB before the slab factor) against the oracle."""
-    gs = Geom(L, 8, 64, 2, 16, 24)
-    gd = Geom(L, 4, 64, 2, 16, 30)
+    gs = Geom(L, 8, d, 2, 16, 24)
+    gd = Geom(L, 4, d, 2, 16, 30)
     _heads_parity(gs, gd, 300, (5, 290), lr, 64, (1, 1 + slice_heads), 4 - slice_heads, seed=L + slice_heads)
 
 

@@ -377,3 +377,65 @@ def test_max_chunks_with_flags():
     with pytest.raises(dk.DynaKVError) as e:
         dk.migrate(st, dt, (0, n + 1), (0, 1), 1, flags=dk.DYNA_MIGRATE_SIGNAL)
     assert e.value.status == dk.DYNA_ERANGE
+
+
+# ------------------------------------------------ AUTO: short runs (small rows) move as TMA tiles
+TP8_ROWS = Geom(5, 1, 128, 2, 16, 200)   # one Llama-3-8B KV head per TP-8 rank: 256-B rows, 4-KiB blocks
+TP2_ROWS = Geom(3, 4, 128, 2, 16, 200)   # TP-2: 1-KiB rows, 16-KiB blocks
+
+
+@pytest.mark.parametrize("gs,gd", [(kvgen.TOY, kvgen.TOY), (TP8_ROWS, TP8_ROWS),
+                                   (TP8_ROWS, TP8_ROWS.with_(block_size=8, num_blocks=400)),
+                                   (TP2_ROWS, TP2_ROWS.with_(block_size=32, num_blocks=100)),
+                                   (Geom(3, 1, 8, 2, 16, 200), Geom(3, 1, 8, 2, 16, 200))],
+                         ids=["toy", "tp8", "tp8-reblock", "tp2-reblock", "16B-rows"])
+@pytest.mark.parametrize("tr,lr,c", [((0, 100), None, 32), ((13, 777), None, 64), ((0, 1), None, 16),
+                                     ((5, 900), (1, 2), 7), ((0, 1024), None, 1024)])
+@pytest.mark.parametrize("flags", [0, dk.DYNA_MIGRATE_SIGNAL], ids=["plain", "signal"])
+def test_auto_small_rows_as_tiles(gs, gd, tr, lr, c, flags):
+    """Whole rows whose contiguous run (min(g, c) x row) is under 32 KiB: AUTO resolves to the TMA tile
+    kernel (engine BULK, piece = the box), which must equal the oracle on the whole pool for ragged
+    ranges, chunk sizes that split blocks, layer sub-ranges and reblocking; with signalling every
+    chunk flag reaches the epoch."""
+    n_tok = min(1024, gs.num_blocks * gs.block_size, gd.num_blocks * gd.block_size)
+    tr = (tr[0], min(tr[1], n_tok))
+    lr = lr or (0, gs.num_layers)
+    ts, td = kvgen.table_pair(7, n_tok, gs, gd)
+    hs, hd = kvgen.fill_bytes(8, gs.pool_bytes), kvgen.fill_bytes(9, gd.pool_bytes)
+    want = hd.copy()
+    oracle.migrate(hs, gs, ts, want, gd, td, tr, lr)
+    src, dst = pool_from_host(gs, hs), pool_from_host(gd, hd)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    x = dk.migrate(st, dt, tr, lr, c, flags=flags)
+    plan = dk.dyna_kv_xfer_plan(x)
+    info = dk.dyna_kv_xfer_info(x)
+    dk.dyna_kv_wait(x)
+    assert plan["engine"] == dk.DYNA_ENGINE_BULK, plan
+    assert np.array_equal(dst.tensor.cpu().numpy(), want)
+    assert np.array_equal(src.tensor.cpu().numpy(), hs)
+    if flags:
+        epoch, nck, sender, first = info
+        fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
+        dk.dyna_kv_copy_flags(dst.handle, sender, first, nck, fl.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert nck == -(-(tr[1] - tr[0]) // c) and (fl.numpy() == epoch).all()
+
+
+def test_tiles_not_under_graph_capture():
+    """Under CUDA-graph capture AUTO does not pick the tile kernel (its maps go through the upload ring,
+    which a replay would recycle): the captured migration runs on VEC and replays bit-exact."""
+    g = TP8_ROWS
+    src, dst = pool_filled(g, 71), pool_filled(g, 72)
+    ts, td = kvgen.table_pair(73, 800, g, g)
+    st, dt = dev_table(src, ts, False), dev_table(dst, td, False)
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        x = dk.dyna_kv_migrate_ex(st, dt, (0, 800), (0, 5), 128, s.cuda_stream,
+                                  dk.opts(flags=dk.DYNA_MIGRATE_UNCHECKED))
+    assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_VEC
+    dk.dyna_kv_wait(x)
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch_rows_equal(src, ts, dst, td, (0, 800), (0, 5))
