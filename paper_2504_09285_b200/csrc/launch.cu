@@ -54,6 +54,7 @@ void preload_kernels() {
       (const void*)k_copy_tiles<false, SingleSource>, (const void*)k_copy_tiles<true, SingleSource, true>,
       (const void*)k_copy_tiles<false, InterleavedSource>, (const void*)k_copy_tiles<true, InterleavedSource, true>,
       (const void*)k_copy_tiles<false, RoundRobinSource>, (const void*)k_copy_tiles<true, RoundRobinSource, true>,
+      (const void*)k_copy_tiles<false, BatchSource>, (const void*)k_copy_tiles<true, BatchSource, true>,
   };
   for (const void* k : ks) cudaFuncGetAttributes(&a, k);
   // Allow the BULK rings any dynamic shared memory the device offers, once, here: a
@@ -73,6 +74,7 @@ void preload_kernels() {
       (const void*)k_copy_tiles<false, SingleSource>, (const void*)k_copy_tiles<true, SingleSource, true>,
       (const void*)k_copy_tiles<false, InterleavedSource>, (const void*)k_copy_tiles<true, InterleavedSource, true>,
       (const void*)k_copy_tiles<false, RoundRobinSource>, (const void*)k_copy_tiles<true, RoundRobinSource, true>,
+      (const void*)k_copy_tiles<false, BatchSource>, (const void*)k_copy_tiles<true, BatchSource, true>,
   };
   for (const void* k : bulk) {
     cudaFuncGetAttributes(&a, k);
@@ -467,11 +469,10 @@ static bool encode_side(CUtensorMap* m, const Side& s, int64_t pitch, int64_t co
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Turn a head-sliced plan (make_plan_sliced, paged -> paged) into a tile plan: slabs per box, item
-// counts, and the four maps written to `maps` (host memory, 4 x 128 B; the caller copies them to
-// 64-B-aligned device memory and sets p.tmaps).  False when the geometry does not fit a tensor map
-// or shared memory (the caller then uses the VEC row kernel).
-bool tile_plan(Plan& p, void* maps) {
+// Turn a head-sliced plan (make_plan_sliced, paged -> paged) into a tile plan: slabs per box, ring
+// slot, item counts.  False when the geometry does not fit a tensor map or shared memory (the caller
+// then uses the VEC row kernel).
+bool tile_shape(Plan& p) {
   if (p.src.linear || p.dst.linear || !encode_tiled()) return false;
   const int64_t slice = p.row, g = p.g;
   if (slice % 16 || p.scol % 16 || p.dcol % 16 || p.spitch % 16 || p.dpitch % 16) return false;
@@ -486,12 +487,6 @@ bool tile_plan(Plan& p, void* maps) {
   int64_t lkb = 1;
   for (int64_t d = 1; d <= std::min<int64_t>(nlk, 256); ++d)
     if (nlk % d == 0 && (d == 1 || run * d <= tile_target_bytes()) && 2 * (run * d + 1024) <= avail) lkb = d;
-  CUtensorMap* m = static_cast<CUtensorMap*>(maps);
-  if (!encode_side(&m[0], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, g, lkb) ||
-      !encode_side(&m[1], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, g, lkb) ||
-      !encode_side(&m[2], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, 1, lkb) ||
-      !encode_side(&m[3], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, 1, lkb))
-    return false;
   p.lkb = (int32_t)lkb;
   p.tile_rstride = (int32_t)((slice * lkb + 127) / 128 * 128);
   p.tile_bytes = (int32_t)((std::max<int64_t>(run * lkb, (g - 1) * p.tile_rstride) + 1023) / 1024 * 1024);
@@ -500,6 +495,19 @@ bool tile_plan(Plan& p, void* maps) {
   p.n_items = p.items_per_chunk * p.nchunks;
   return true;
 }
+
+// The four maps of a tile plan (after tile_shape) into `maps` (host memory, 4 x 128 B; the caller
+// copies them to 64-B-aligned device memory and sets p.tmaps).
+bool tile_encode(const Plan& p, void* maps) {
+  const int64_t slice = p.row, e0 = slice <= 2048 ? slice / 8 : 256;
+  CUtensorMap* m = static_cast<CUtensorMap*>(maps);
+  return encode_side(&m[0], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, p.g, p.lkb) &&
+         encode_side(&m[1], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, p.g, p.lkb) &&
+         encode_side(&m[2], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, 1, p.lkb) &&
+         encode_side(&m[3], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, 1, p.lkb);
+}
+
+bool tile_plan(Plan& p, void* maps) { return tile_shape(p) && tile_encode(p, maps); }
 
 template <bool SIG, class Src>
 dyna_status launch_tiles_t(const Src& src, int64_t n_items, int tile_bytes, int stages, int max_ctas, int dev,
@@ -539,6 +547,11 @@ dyna_status launch_tiles_src(const Src& src, int64_t n_items, bool sig, int tile
 
 dyna_status launch_tiles(const Plan& p, int stages, int max_ctas, int dev, cudaStream_t st) {
   return launch_tiles_src(SingleSource{p}, p.n_items, p.counters != nullptr, p.tile_bytes, stages, max_ctas, dev, st);
+}
+
+dyna_status launch_tiles_batch(const BatchSource& src, bool sig, int tile_bytes, int stages, int max_ctas, int dev,
+                               cudaStream_t st) {
+  return launch_tiles_src(src, src.total_items, sig, tile_bytes, stages, max_ctas, dev, st);
 }
 
 dyna_status launch_tiles_interleaved(const InterleavedSource& src, bool sig, int tile_bytes, int stages, int max_ctas,

@@ -217,15 +217,26 @@ static dyna_status upload_tables(RingLease& lease, const dyna_block_table& src, 
 }
 
 // Head slices: the TMA tile engine (k_copy_tiles) for DYNA_ENGINE_BULK / BULK_WS, and for AUTO
-// when the geometry fits a tensor map and the stream is not capturing (tile plans upload their maps
-// through the upload ring, which a graph replay would recycle); otherwise the VEC row kernel.
+// when the geometry fits a tensor map; otherwise the VEC row kernel.
 static bool stream_capturing(cudaStream_t st) {
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   return cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
 }
-static bool want_tiles(const dyna_kv_opts& o, cudaStream_t st) {
+static bool want_tiles(const dyna_kv_opts& o) {
   if (o.engine == DYNA_ENGINE_BULK || o.engine == DYNA_ENGINE_BULK_WS) return true;
-  return o.engine == DYNA_ENGINE_AUTO && tiles_enabled() && !stream_capturing(st);
+  return o.engine == DYNA_ENGINE_AUTO && tiles_enabled();
+}
+
+// Where a tile plan's maps come from: the channel's cached device copy (*cached), else the host
+// copy in `maps`, uploaded with the call's tables (not under capture: a replay would read recycled
+// upload-ring staging).  False: neither (the caller does not tile).
+static dyna_status tile_maps(dyna_kv_pool* S, const dyna_kv_pool* D, const Plan& p, cudaStream_t st,
+                             const char** cached, char* maps, bool* ok) {
+  *ok = false;
+  dyna_status r = channel_tile_maps(S, D, p, S->dev, st, cached);
+  if (r) return r;
+  *ok = *cached || (!stream_capturing(st) && tile_encode(p, maps));
+  return DYNA_OK;
 }
 
 static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna_range tr, dyna_range lr,
@@ -309,12 +320,13 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   // several (layer, K|V) slabs, so items are ~32 KiB whatever the block).
   alignas(64) char maps[kTileMaps * kTileMapBytes];
   Plan tp{};
-  const bool tiles = ch.variant == DYNA_VARIANT_FUSED && !board && !peer_dst && !o.engine &&
-                     o.schedule != DYNA_SCHED_DYNAMIC && std::min<int64_t>(g, c) * row < kTileRunMax &&
-                     tiles_enabled() && !stream_capturing(stream) &&
-                     tile_plan(tp = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), row, row, 0, row, 0,
-                                                     tr.begin, tr.end, l0, lm, c, g, ch.piece),
-                               maps);
+  const char* cached = nullptr;
+  bool tiles = ch.variant == DYNA_VARIANT_FUSED && !board && !peer_dst && !o.engine &&
+               o.schedule != DYNA_SCHED_DYNAMIC && std::min<int64_t>(g, c) * row < kTileRunMax && tiles_enabled() &&
+               tile_shape(tp = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), row, row, 0, row, 0, tr.begin,
+                                                tr.end, l0, lm, c, g, ch.piece));
+  if (tiles && (r = tile_maps(S, D, tp, stream, &cached, maps, &tiles))) return r;
+  const bool up_maps = tiles && !cached;
   if (tiles) {
     ch.engine = DYNA_ENGINE_BULK;
     ch.piece = tp.tile_bytes;
@@ -328,8 +340,8 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   RingLease lease(S->dev);
   const int32_t *sids = nullptr, *dids = nullptr;
   const char* dmaps = nullptr;
-  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids, tiles ? maps : nullptr,
-                         tiles ? sizeof(maps) : 0, &dmaps)))
+  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids, up_maps ? maps : nullptr,
+                         up_maps ? sizeof(maps) : 0, &dmaps)))
     return r;
 
   dyna_kv_xfer* x = nullptr;
@@ -352,7 +364,7 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
     if (tiles) {
       p.src.table = sids;
       p.dst.table = dids;
-      p.tmaps = dmaps;
+      p.tmaps = cached ? cached : dmaps;
     }
     p.err = x->err;
     if (ctx) set_chunking(p, ctx->mig_t0, tr.end, c);
@@ -579,19 +591,27 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
                             src_heads.begin * head_bytes, D->row, (int64_t)dst_head_begin * head_bytes, tr.begin,
                             tr.end, l0, lm, chunk_tokens, gcd64(gs.block_size, gd.block_size), piece);
   alignas(64) char maps[kTileMaps * kTileMapBytes];
-  const bool tiles = want_tiles(o, stream) && tile_plan(p, maps);
+  const char* cached = nullptr;
+  bool tiles = want_tiles(o) && tile_shape(p);
+  if (tiles && (r = tile_maps(S, D, p, stream, &cached, maps, &tiles))) return r;
   if (!tiles && o.engine != DYNA_ENGINE_AUTO && o.engine != DYNA_ENGINE_VEC)
     return fail(DYNA_ENOTSUP, "head slices of %lld B on the BULK engine: the geometry does not fit a TMA tensor map "
-                              "(or the stream is capturing); use DYNA_ENGINE_VEC", (long long)(nh * head_bytes));
+                              "(or the stream is capturing without cached maps); use DYNA_ENGINE_VEC",
+                (long long)(nh * head_bytes));
+  if (!tiles)  // tile_shape may have reshaped the plan: the row kernel's plan
+    p = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), nh * head_bytes, S->row, src_heads.begin * head_bytes,
+                         D->row, (int64_t)dst_head_begin * head_bytes, tr.begin, tr.end, l0, lm, chunk_tokens,
+                         gcd64(gs.block_size, gd.block_size), piece);
+  const bool up_maps = tiles && !cached;
   RingLease lease(S->dev);
   const int32_t *sids = nullptr, *dids = nullptr;
   const char* dmaps = nullptr;
-  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids, tiles ? maps : nullptr,
-                         tiles ? sizeof(maps) : 0, &dmaps)))
+  if ((r = upload_tables(lease, src, dst, tr.end, stream, &sids, &dids, up_maps ? maps : nullptr,
+                         up_maps ? sizeof(maps) : 0, &dmaps)))
     return r;
   p.src.table = sids;
   p.dst.table = dids;
-  if (tiles) p.tmaps = dmaps;
+  if (tiles) p.tmaps = cached ? cached : dmaps;
   dyna_kv_xfer* x = nullptr;
   if ((r = new_xfer(S->dev, gs.instance, stream, &x))) return r;
   x->nchunks = (int32_t)nchunks;
@@ -820,7 +840,8 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   std::vector<Plan> plans(n);
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
   std::vector<char> maps_h;
-  bool tiles = want_tiles(o, stream);
+  std::vector<const char*> cached(n, nullptr);  // channel-cached device maps per entry (else uploaded)
+  bool tiles = want_tiles(o);
   if (tiles) maps_h.resize((size_t)n * kTileMaps * kTileMapBytes + 64);
   char* maps = tiles ? reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(maps_h.data()) + 63) & ~uintptr_t(63))
                      : nullptr;
@@ -830,7 +851,11 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
     const int64_t he = (int64_t)S->desc.head_dim * S->desc.elem_bytes;
     plans[i] = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), slice, S->row, m.src_heads.begin * he, D->row,
                                 (int64_t)m.dst_head_begin * he, tr.begin, tr.end, l0, lm, chunk_tokens, g, piece);
-    if (tiles) tiles = tile_plan(plans[i], maps + (size_t)i * kTileMaps * kTileMapBytes);
+    if (tiles && (tiles = tile_shape(plans[i])) &&
+        (r = tile_maps(S, D, plans[i], stream, &cached[i], maps + (size_t)i * kTileMaps * kTileMapBytes, &tiles))) {
+      delete x;
+      return r;
+    }
   }
   if (!tiles && o.engine != DYNA_ENGINE_AUTO && o.engine != DYNA_ENGINE_VEC) {
     delete x;
@@ -871,7 +896,7 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
     dyna_kv_pool *S = m.src.pool, *D = m.dst.pool;
     plans[i].src.table = m.src.block_ids ? m.src.block_ids : reinterpret_cast<const int32_t*>(dbase + soff[i]);
     plans[i].dst.table = m.dst.block_ids ? m.dst.block_ids : reinterpret_cast<const int32_t*>(dbase + doff[i]);
-    if (tiles) plans[i].tmaps = dbase + (size_t)i * kTileMaps * kTileMapBytes;
+    if (tiles) plans[i].tmaps = cached[i] ? cached[i] : dbase + (size_t)i * kTileMaps * kTileMapBytes;
     plans[i].err = x->err;
     if (signal) {
       const dyna_kv_xfer::BatchEntry& be = x->batch[i];
@@ -1023,9 +1048,55 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
       be.sender = S->desc.instance;
     }
   }
-  // One upload: [plans][item bases][host-resident tables].
   const size_t m = live.size();
-  const size_t plans_b = ((m * sizeof(Plan)) + 15) & ~size_t(15);
+  // Short contiguous runs on the same device (AUTO): every entry as a tile plan, one map set per
+  // distinct (source pool, destination pool), all entries with one ring slot.
+  std::vector<Plan> tplans;
+  std::vector<char> maps_h;
+  std::vector<int32_t> map_of(m, 0);
+  std::vector<size_t> pair_rep;               // a plan of each distinct (source, destination) pair
+  std::vector<const char*> pair_cached;       // its channel-cached device maps (else uploaded)
+  bool tiles = !o.engine && !peer && run_min < kTileRunMax && o.schedule != DYNA_SCHED_DYNAMIC && tiles_enabled();
+  if (tiles) {
+    std::map<std::pair<const dyna_kv_pool*, const dyna_kv_pool*>, int32_t> pair_idx;
+    tplans.resize(m);
+    for (size_t k = 0; k < m && tiles; ++k) {
+      const dyna_kv_migration& mg = migs[live[k]];
+      dyna_kv_pool *S = mg.src.pool, *D = mg.dst.pool;
+      const int64_t g = gcd64(S->desc.block_size, D->desc.block_size);
+      tplans[k] = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), S->row, S->row, 0, D->row, 0,
+                                   mg.token_range.begin, mg.token_range.end, l0, lm, chunk_tokens, g, ch.piece);
+      tiles = tile_shape(tplans[k]) && tplans[k].tile_bytes == tplans[0].tile_bytes;
+      auto it = pair_idx.find({S, D});
+      if (it == pair_idx.end()) {
+        it = pair_idx.emplace(std::make_pair(S, D), (int32_t)pair_rep.size()).first;
+        pair_rep.push_back(k);
+      }
+      map_of[k] = it->second;
+    }
+    if (tiles) {
+      maps_h.resize(pair_rep.size() * kTileMaps * kTileMapBytes + 64);
+      char* mp = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(maps_h.data()) + 63) & ~uintptr_t(63));
+      pair_cached.assign(pair_rep.size(), nullptr);
+      for (size_t q = 0; q < pair_rep.size() && tiles; ++q) {
+        const dyna_kv_migration& mg = migs[live[pair_rep[q]]];
+        if ((r = tile_maps(mg.src.pool, mg.dst.pool, tplans[pair_rep[q]], stream, &pair_cached[q],
+                           mp + q * kTileMaps * kTileMapBytes, &tiles))) {
+          delete x;
+          return r;
+        }
+      }
+    }
+  }
+  const size_t npairs = tiles ? pair_rep.size() : 0;
+  const size_t maps_b = npairs * kTileMaps * kTileMapBytes;  // multiple of 256
+  if (tiles) {
+    ch.engine = DYNA_ENGINE_BULK;
+    ch.piece = tplans[0].tile_bytes;
+    ch.stages = o.stages ? o.stages : 4;
+  }
+  // One upload: [tile maps][plans][item bases][host-resident tables].
+  const size_t plans_b = maps_b + (((m * sizeof(Plan)) + 15) & ~size_t(15));
   const size_t bases_b = ((m * sizeof(int64_t)) + 15) & ~size_t(15);
   std::vector<size_t> soff(m, 0), doff(m, 0);
   size_t tab_b = 0;
@@ -1055,10 +1126,18 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     const int32_t* sids = mg.src.block_ids ? mg.src.block_ids : reinterpret_cast<const int32_t*>(dbase + soff[k]);
     const int32_t* dids = mg.dst.block_ids ? mg.dst.block_ids : reinterpret_cast<const int32_t*>(dbase + doff[k]);
     const int64_t g = gcd64(S->desc.block_size, D->desc.block_size);
-    plans[k] = fed ? make_plan_sliced(paged(S, sids), paged(D, dids), S->row, S->row, 0, D->row, 0,
-                                      mg.token_range.begin, mg.token_range.end, l0, lm, chunk_tokens, g, ch.piece)
-                   : make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end, l0,
-                               lm, chunk_tokens, g, ch.piece);
+    if (tiles) {
+      plans[k] = tplans[k];
+      plans[k].src.table = sids;
+      plans[k].dst.table = dids;
+      plans[k].tmaps = pair_cached[map_of[k]] ? pair_cached[map_of[k]]
+                                              : dbase + (size_t)map_of[k] * kTileMaps * kTileMapBytes;
+    } else {
+      plans[k] = fed ? make_plan_sliced(paged(S, sids), paged(D, dids), S->row, S->row, 0, D->row, 0,
+                                        mg.token_range.begin, mg.token_range.end, l0, lm, chunk_tokens, g, ch.piece)
+                     : make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end,
+                                 l0, lm, chunk_tokens, g, ch.piece);
+    }
     plans[k].err = x->err;
     if (signal) {  // entry k's chunk j: counter / inbox slot first_slot + j of its (sender, destination)
       dyna_kv_xfer::BatchEntry& be = x->batch[live[k]];
@@ -1076,7 +1155,10 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     total_items += plans[k].n_items;
   }
   // fill the pinned staging now that the device pointers are known, then one copy
-  std::memcpy(h, plans.data(), m * sizeof(Plan));
+  if (tiles)
+    std::memcpy(h, reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(maps_h.data()) + 63) & ~uintptr_t(63)),
+                maps_b);
+  std::memcpy(h + maps_b, plans.data(), m * sizeof(Plan));
   std::memcpy(h + plans_b, bases.data(), m * sizeof(int64_t));
   for (size_t k = 0; k < m; ++k) {
     const dyna_kv_migration& mg = migs[live[k]];
@@ -1089,7 +1171,7 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     delete x;
     return r;
   }
-  BatchSource bsrc{reinterpret_cast<const Plan*>(dbase), reinterpret_cast<const int64_t*>(dbase + plans_b),
+  BatchSource bsrc{reinterpret_cast<const Plan*>(dbase + maps_b), reinterpret_cast<const int64_t*>(dbase + plans_b),
                    (int32_t)m, total_items};
   x->variant = DYNA_VARIANT_FUSED;
   x->engine = ch.engine;
@@ -1097,9 +1179,10 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   x->stages = ch.engine != DYNA_ENGINE_VEC ? ch.stages : 0;
   x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
   x->launches = 1;
-  r = fed ? launch_rows_batch(bsrc, signal, o.max_ctas, S0->dev, stream)
-          : launch_batch(bsrc, total_items, signal, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll, S0->dev,
-                         stream, o.schedule);
+  r = tiles ? launch_tiles_batch(bsrc, signal, ch.piece, ch.stages, o.max_ctas, S0->dev, stream)
+      : fed ? launch_rows_batch(bsrc, signal, o.max_ctas, S0->dev, stream)
+            : launch_batch(bsrc, total_items, signal, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll,
+                           S0->dev, stream, o.schedule);
   if (!r) r = lease.finish(stream);
   if (r) {
     delete x;

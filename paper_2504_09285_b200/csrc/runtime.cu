@@ -335,6 +335,47 @@ dyna_status channel_counters(dyna_kv_pool* src, const dyna_kv_pool* dst, int kde
   return DYNA_OK;
 }
 
+dyna_status channel_tile_maps(dyna_kv_pool* S, const dyna_kv_pool* D, const Plan& p, int kdev, cudaStream_t st,
+                              const char** out) {
+  *out = nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  const bool capturing = cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
+  const TileKey key{D->uid, D->base, p.row, p.spitch, p.dpitch, p.scol, p.dcol, p.l0, p.lm, p.g, p.lkb};
+  constexpr size_t set_b = (size_t)kTileMaps * kTileMapBytes;
+  std::lock_guard<std::mutex> lk(S->mu);
+  Channel& ch = S->channels[D];
+  for (size_t i = 0; i < ch.tkeys.size(); ++i)
+    if (ch.tkeys[i] == key) {
+      *out = ch.tmaps + i * set_b;
+      return DYNA_OK;
+    }
+  // a miss: fill the next set (not under capture: the fill synchronises with the host)
+  if (capturing || ch.tkeys.size() >= (size_t)kTileCacheSets) return DYNA_OK;
+  DevInfo* di = dev_info(kdev);
+  DeviceGuard g(kdev);
+  if (!ch.tmaps) {
+    if (cudaMalloc(&ch.tmaps, kTileCacheSets * set_b) != cudaSuccess)
+      return fail(DYNA_ENOMEM, "tile map cache (device)");
+    if (cudaHostAlloc(&ch.tmaps_host, kTileCacheSets * set_b, cudaHostAllocPortable) != cudaSuccess)
+      return fail(DYNA_ENOMEM, "tile map cache (pinned)");
+    ch.tdev = kdev;
+  }
+  if (kdev != ch.tdev) return DYNA_OK;
+  {
+    std::lock_guard<std::mutex> lk2(g_mu);
+    if (!di->maps) CUDA_TRY(cudaStreamCreateWithFlags(&di->maps, cudaStreamNonBlocking));
+  }
+  const size_t i = ch.tkeys.size();
+  if (!tile_encode(p, ch.tmaps_host + i * set_b)) return DYNA_OK;
+  // its own non-blocking stream, waited for on the host: the set is complete before any kernel can
+  // name it, whatever stream that kernel runs on (no device-wide synchronisation involved)
+  CUDA_TRY(cudaMemcpyAsync(ch.tmaps + i * set_b, ch.tmaps_host + i * set_b, set_b, cudaMemcpyHostToDevice, di->maps));
+  CUDA_TRY(cudaStreamSynchronize(di->maps));
+  ch.tkeys.push_back(key);
+  *out = ch.tmaps + i * set_b;
+  return DYNA_OK;
+}
+
 // Staging slots of channel src -> dst (staged variant): 2 x slot on each side.  *prev_done:
 // the end of the previous STAGED migration on this channel (its stream may differ), which
 // the caller orders its kernels after; growing the slots waits for it on the host first.
@@ -505,6 +546,8 @@ dyna_status dyna_kv_pool_destroy(dyna_kv_pool_t p) {
     for (auto& c : kv.second.counters) retire(c.first, c.second, Mem::Device);
     retire(kv.second.sdev, kv.second.sstage, Mem::Device);
     retire(kv.second.ddev, kv.second.dstage, Mem::Device);
+    retire(kv.second.tdev, kv.second.tmaps, Mem::Device);
+    retire(kv.second.tdev, kv.second.tmaps_host, Mem::Host);
   }
   if (p->own_inbox) retire(p->dev, p->inbox, Mem::Device);
   if (p->imported) {

@@ -87,6 +87,7 @@ struct DevInfo {
   int sms = 0;
   cudaStream_t aux = nullptr;  // library stream for destination-side kernels (staged, cross-device)
   cudaStream_t upload = nullptr;  // library stream for host-resident table uploads (overlap the previous kernel)
+  cudaStream_t maps = nullptr;    // library stream for tile-map cache fills (host-synchronised, once per key)
   unsigned long long* sched = nullptr;  // [kSchedSlots][2] dynamic-scheduling counters, zero at rest
   std::atomic<uint32_t> sched_seq{0};
 };
@@ -132,8 +133,27 @@ void flush_retired();
 }  // namespace dynakv
 
 // ---------------------------------------------------------------- objects behind the opaque handles
+// Tile-map cache key: everything the four maps of a tile plan encode besides the channel's own
+// source pool (the destination's identity and base too: a channel outlives a destroyed destination).
+struct TileKey {
+  uint64_t duid;
+  const char* dbase;
+  int64_t slice, spitch, dpitch;
+  int32_t scol, dcol, l0, lm, g, lkb;
+  bool operator==(const TileKey& o) const {
+    return duid == o.duid && dbase == o.dbase && slice == o.slice && spitch == o.spitch && dpitch == o.dpitch &&
+           scol == o.scol && dcol == o.dcol && l0 == o.l0 && lm == o.lm && g == o.g && lkb == o.lkb;
+  }
+};
+constexpr int kTileCacheSets = 64;  // map sets cached per channel (then calls upload their maps)
+
 struct Channel {  // sender pool -> destination pool
   std::map<int, unsigned long long*> counters;  // per kernel device: [DYNA_MAX_CHUNKS], zero at rest
+  // tile maps, written once per key and never changed while cached: device copy + its pinned source
+  char* tmaps = nullptr;
+  char* tmaps_host = nullptr;
+  int tdev = -1;
+  std::vector<TileKey> tkeys;       // set i is complete on the device once listed here
   char* sstage = nullptr;                      // staged variant: 2 slots on the source device
   char* dstage = nullptr;                      // staged variant: 2 slots on the destination device
   int64_t slot_bytes = 0;
@@ -384,7 +404,17 @@ dyna_status launch_rows_batch(const BatchSource& src, bool sig, int max_ctas, in
 bool fed_vec_enabled();
 // head slices as TMA tensor tiles (k_copy_tiles)
 bool tiles_enabled();
-bool tile_plan(Plan& p, void* maps);  // maps: kTileMaps x kTileMapBytes of host memory
+bool tile_shape(Plan& p);                    // box geometry + item counts (false: not a tile geometry)
+bool tile_encode(const Plan& p, void* maps);  // maps: kTileMaps x kTileMapBytes of host memory
+bool tile_plan(Plan& p, void* maps);          // both
+// The device copy of a tile plan's maps cached on channel S -> D (kernel device kdev), written at
+// first use by a host-synchronised copy on a library stream; *out = nullptr when not available (a
+// miss under capture, or the cache is full): the caller then uploads the maps with the call's
+// tables, or does not tile.
+dyna_status channel_tile_maps(dyna_kv_pool* S, const dyna_kv_pool* D, const Plan& p, int kdev, cudaStream_t st,
+                              const char** out);
+dyna_status launch_tiles_batch(const BatchSource& src, bool sig, int tile_bytes, int stages, int max_ctas, int dev,
+                               cudaStream_t st);
 dyna_status launch_tiles(const Plan& p, int stages, int max_ctas, int dev, cudaStream_t st);
 dyna_status launch_tiles_interleaved(const InterleavedSource& src, bool sig, int tile_bytes, int stages, int max_ctas,
                                      int dev, cudaStream_t st);

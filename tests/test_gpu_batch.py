@@ -209,7 +209,7 @@ def test_chunk_stream_prefill_then_decode():
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES + [dk.DYNA_ENGINE_AUTO])
 def test_tp_sharded_rows(engine):
     """TP-8 shard of Qwen2-72B (1 KV head per rank: 256-B rows, 4-KiB segments) — SURVEY §8f NEXT-3."""
     g = Geom(8, 1, 128, 2, 16, 300)
@@ -402,3 +402,41 @@ def test_native_chunkstream_empty_and_errors():
         dk.dyna_kv_chunkstream_produced(s, 300)
     assert e.value.status == dk.DYNA_ERANGE
     dk.dyna_kv_chunkstream_finish(s)
+
+
+@pytest.mark.parametrize("signal", [False, True])
+@pytest.mark.parametrize("host_tables", [False, True])
+def test_batch_small_rows_as_tiles(signal, host_tables):
+    """A batch of TP-8-shard migrations (256-B rows, 4-KiB blocks) between two source and two destination
+    pools: AUTO runs it as ONE tile launch (one map set per (source, destination) pool pair, per-request
+    chunk flags), equal to the oracle applying every request in order."""
+    g = Geom(6, 1, 128, 2, 16, 400)
+    reqs = kvgen.migrating(kvgen.skewed_batch(17, 16))
+    lens = [min(r.s, 900) for r in reqs]
+    hs = [kvgen.fill_bytes(40 + i, g.pool_bytes) for i in range(2)]
+    hd = [kvgen.fill_bytes(50 + i, g.pool_bytes) for i in range(2)]
+    tabs = [kvgen.batch_tables(60 + i, [n + 16 for n in lens[i::2]], g, g) for i in range(2)]
+    want = [h.copy() for h in hd]
+    src = [pool_from_host(g, h) for h in hs]
+    dst = [pool_from_host(g, h) for h in hd]
+    T = host_table if host_tables else dev_table
+    migs, where = [], []
+    rng = np.random.default_rng(3)
+    for i in range(2):                       # pair (src i -> dst i) for even/odd requests
+        for n, (ts, td) in zip(lens[i::2], tabs[i]):
+            t0 = int(rng.integers(0, 16))
+            oracle.migrate(hs[i], g, ts, want[i], g, td, (t0, t0 + n))
+            migs.append((T(src[i], ts), T(dst[i], td), (t0, t0 + n)))
+            where.append(i)
+    x = dk.migrate_batch(migs, (0, 6), 128, flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0)
+    assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_BULK
+    infos = [dk.dyna_kv_batch_info(x, k) for k in range(len(migs))] if signal else []
+    dk.dyna_kv_wait(x)
+    for i in range(2):
+        assert np.array_equal(dst[i].tensor.cpu().numpy(), want[i]), i
+        assert np.array_equal(src[i].tensor.cpu().numpy(), hs[i]), i
+    for (_, _, tr), i, (epoch, first, nck, sender) in zip(migs, where, infos):
+        fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
+        dk.dyna_kv_copy_flags(dst[i].handle, sender, first, nck, fl.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert nck == -(-(tr[1] - tr[0]) // 128) and (fl.numpy() == epoch).all()

@@ -421,21 +421,29 @@ def test_auto_small_rows_as_tiles(gs, gd, tr, lr, c, flags):
         assert nck == -(-(tr[1] - tr[0]) // c) and (fl.numpy() == epoch).all()
 
 
-def test_tiles_not_under_graph_capture():
-    """Under CUDA-graph capture AUTO does not pick the tile kernel (its maps go through the upload ring,
-    which a replay would recycle): the captured migration runs on VEC and replays bit-exact."""
+def test_tiles_under_graph_capture_need_cached_maps():
+    """Tile maps live in a per-(source, destination) device cache written at first use.  Under CUDA-graph
+    capture a miss cannot be filled (the copy would only run at replay), so the first captured migration
+    runs on VEC; once an uncaptured call has cached the maps, a captured migration runs as tiles.  Both
+    graphs replay bit-exact."""
     g = TP8_ROWS
     src, dst = pool_filled(g, 71), pool_filled(g, 72)
     ts, td = kvgen.table_pair(73, 800, g, g)
     st, dt = dev_table(src, ts, False), dev_table(dst, td, False)
+    o = dk.opts(flags=dk.DYNA_MIGRATE_UNCHECKED)
     s = torch.cuda.Stream()
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=s):
-        x = dk.dyna_kv_migrate_ex(st, dt, (0, 800), (0, 5), 128, s.cuda_stream,
-                                  dk.opts(flags=dk.DYNA_MIGRATE_UNCHECKED))
-    assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_VEC
-    dk.dyna_kv_wait(x)
-    graph.replay()
-    torch.cuda.synchronize()
-    assert torch_rows_equal(src, ts, dst, td, (0, 800), (0, 5))
+    engines = []
+    for warm in (False, True):
+        if warm:   # the same geometry outside capture: fills the channel's map cache
+            dk.dyna_kv_wait(dk.dyna_kv_migrate_ex(st, dt, (0, 800), (0, 5), 128, s.cuda_stream, o))
+        dst.tensor.zero_()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            x = dk.dyna_kv_migrate_ex(st, dt, (0, 800), (0, 5), 128, s.cuda_stream, o)
+        engines.append(dk.dyna_kv_xfer_plan(x)["engine"])
+        dk.dyna_kv_wait(x)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch_rows_equal(src, ts, dst, td, (0, 800), (0, 5))
+    assert engines == [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK]
