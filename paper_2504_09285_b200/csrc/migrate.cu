@@ -99,9 +99,14 @@ dyna_status validate_pair(const dyna_block_table& src, const dyna_block_table& d
   if (src.host_block_ids) {
     if (src_spans || same) {
       if ((r = table_spans(src, tr.begin, tr.end, ssp, who))) return r;
-    } else {
-      std::vector<Span> tmp;  // range check only
-      if ((r = table_spans(src, tr.begin, tr.end, tmp, who))) return r;
+    } else {  // range check only
+      const int64_t bs = gs.block_size;
+      for (int64_t j = tr.begin / bs; j <= (tr.end - 1) / bs; ++j) {
+        const int32_t id = src.host_block_ids[j];
+        if (id < 0 || id >= gs.num_blocks)
+          return fail(DYNA_ERANGE, "block_ids[%lld] = %d outside [0, %lld)", (long long)j, id,
+                      (long long)gs.num_blocks);
+      }
     }
   }
   return DYNA_OK;

@@ -196,36 +196,27 @@ dyna_status table_spans(const dyna_block_table& t, int64_t t0, int64_t t1, std::
 // Reading R7: destination rows (heads) must be distinct (no two writes of one byte) and, where
 // a source pool is a destination pool, disjoint from the source rows (heads) being read.
 // Source rows may repeat (shared prefix blocks).  All spans of one call or one batch together.
-// Spans are ordered by a packed 64-bit key (pool, block id, first row) — a sort of plain
-// integers, several times cheaper than sorting the structs — and the spans of one block are
-// compared pairwise (few per block).
+// O(spans): per destination pool (few per call) a block-indexed table, valid for this call only
+// through a per-thread generation stamp, chains the spans of each block; a new span is compared
+// with the spans already chained on its block (few: one per head range / row range of the block).
 dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src) {
   if (dst.empty()) return DYNA_OK;
-  std::vector<uint64_t> uids;  // few distinct pools per call
-  auto uid_index = [&](uint64_t u) -> uint64_t {
-    for (size_t i = 0; i < uids.size(); ++i)
-      if (uids[i] == u) return i;
-    uids.push_back(u);
-    return uids.size() - 1;
+  struct Index {
+    std::vector<uint32_t> stamp;  // == gen: head[] is valid for this call
+    std::vector<int32_t> head;    // last span chained on the block
   };
-  auto keyed = [&](const std::vector<Span>& v, std::vector<std::pair<uint64_t, uint32_t>>& out, bool only_known) {
-    out.clear();
-    out.reserve(v.size());
-    for (uint32_t i = 0; i < v.size(); ++i) {
-      uint64_t u = 0;
-      if (only_known) {  // source spans: only pools that are also destinations matter
-        size_t k = 0;
-        while (k < uids.size() && uids[k] != v[i].uid) ++k;
-        if (k == uids.size()) continue;
-        u = k;
-      } else {
-        u = uid_index(v[i].uid);
-      }
-      out.emplace_back((u << 56) | ((uint64_t)(uint32_t)v[i].id << 24) | ((uint64_t)v[i].lo & 0xFFFFFF), i);
-    }
-    std::sort(out.begin(), out.end());
+  thread_local std::vector<Index> tables;
+  thread_local uint32_t gen = 0;
+  if (++gen == 0) {  // wrapped: forget every stamp
+    for (Index& x : tables) std::fill(x.stamp.begin(), x.stamp.end(), 0u);
+    gen = 1;
+  }
+  std::vector<uint64_t> uids;  // destination pools of this call -> tables[k]
+  auto slot = [&](uint64_t u) -> int {
+    for (size_t k = 0; k < uids.size(); ++k)
+      if (uids[k] == u) return (int)k;
+    return -1;
   };
-  auto blk = [](uint64_t key) { return key >> 24; };
   auto overlap = [](const Span& a, const Span& b) {
     return a.uid == b.uid && a.id == b.id && a.lo < b.hi && b.lo < a.hi && a.h0 < b.h1 && b.h0 < a.h1;
   };
@@ -234,25 +225,38 @@ dyna_status check_alias(std::vector<Span>& dst, std::vector<Span>& src) {
     return fail(DYNA_EALIAS, "migration %d: %s block %d (also migration %d)", std::max(a.who, b.who), what, a.id,
                 std::min(a.who, b.who));
   };
-  std::vector<std::pair<uint64_t, uint32_t>> kd, ks;
-  keyed(dst, kd, false);
-  for (size_t i = 0; i < kd.size();) {
-    size_t e = i;
-    while (e < kd.size() && blk(kd[e].first) == blk(kd[i].first)) ++e;
-    for (size_t a = i; a < e; ++a)
-      for (size_t b = a + 1; b < e && dst[kd[b].second].lo < dst[kd[a].second].hi; ++b)
-        if (overlap(dst[kd[a].second], dst[kd[b].second]))
-          return named(dst[kd[b].second], dst[kd[a].second], "destination rows written twice in");
-    i = e;
+  std::vector<int32_t> next(dst.size());
+  for (size_t i = 0; i < dst.size(); ++i) {
+    const Span& d = dst[i];
+    int k = slot(d.uid);
+    if (k < 0) {
+      k = (int)uids.size();
+      uids.push_back(d.uid);
+      if (tables.size() <= (size_t)k) tables.resize(k + 1);
+    }
+    Index& t = tables[k];
+    const size_t id = (size_t)(uint32_t)d.id;
+    if (t.stamp.size() <= id) {
+      t.stamp.resize(id + 1, 0u);
+      t.head.resize(id + 1, -1);
+    }
+    if (t.stamp[id] != gen) {
+      t.stamp[id] = gen;
+      t.head[id] = -1;
+    }
+    for (int32_t j = t.head[id]; j >= 0; j = next[j])
+      if (overlap(d, dst[j])) return named(d, dst[j], "destination rows written twice in");
+    next[i] = t.head[id];
+    t.head[id] = (int32_t)i;
   }
-  if (src.empty()) return DYNA_OK;
-  keyed(src, ks, true);
-  size_t k = 0;
-  for (const auto& x : kd) {  // both sorted: one merge pass over the blocks
-    while (k < ks.size() && blk(ks[k].first) < blk(x.first)) ++k;
-    for (size_t m = k; m < ks.size() && blk(ks[m].first) == blk(x.first); ++m)
-      if (overlap(src[ks[m].second], dst[x.second]))
-        return named(dst[x.second], src[ks[m].second], "destination rows that are also source rows in");
+  for (const Span& s : src) {  // only source rows of pools this call writes matter
+    const int k = slot(s.uid);
+    if (k < 0) continue;
+    const Index& t = tables[k];
+    const size_t id = (size_t)(uint32_t)s.id;
+    if (id >= t.stamp.size() || t.stamp[id] != gen) continue;
+    for (int32_t j = t.head[id]; j >= 0; j = next[j])
+      if (overlap(s, dst[j])) return named(dst[j], s, "destination rows that are also source rows in");
   }
   return DYNA_OK;
 }

@@ -32,25 +32,27 @@ def peak():
 
 
 def run_set(stream, calls, reps=10, warm=3):
-    """calls: list of zero-arg functions each enqueuing one migrate and returning its handle."""
+    """calls: list of zero-arg functions each enqueuing one migrate and returning its handle.
+    Device time per set of calls, sets issued back to back (as a serving loop issues them): one
+    untimed set is enqueued before the start event, so the timed region does not open with one
+    call's host latency on an idle device; the host issues set k+1 while set k runs."""
     def once():
         xs = [c() for c in calls]
         return xs
     for _ in range(warm):
         for x in once():
             dk.dyna_kv_wait(x)
-    ts = []
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    xs = once()
+    a.record(stream)
     for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        a.record(stream)
-        xs = once()
-        b.record(stream)
-        for x in xs:
-            dk.dyna_kv_wait(x)
-        b.synchronize()
-        ts.append(a.elapsed_time(b))
-    return statistics.median(ts)
+        xs += once()
+    b.record(stream)
+    for x in xs:
+        dk.dyna_kv_wait(x)
+    b.synchronize()
+    return a.elapsed_time(b) / reps
 
 
 def main():
