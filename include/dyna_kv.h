@@ -177,11 +177,12 @@ typedef struct {
  * chunk size).  Entries for the exact row size are preferred over generic
  * ones; within each class the smallest covering max_chunk_tokens wins.  The
  * library starts with the table measured on B200 (profiles/), replaceable at
- * run time.  Two measured rules apply on top of the table when the engine is
- * AUTO: no BULK engine when a contiguous run (min(gcd(bs_src, bs_dst),
- * chunk_tokens) * row bytes) is shorter than 16 KiB, and, when per-chunk
- * flags are requested for more than one chunk in one call, BULK_WS (whose
- * chunk counting runs on an accountant thread) instead of BULK. */
+ * run time.  Measured rules apply on top of the table when the engine is
+ * AUTO: a contiguous run (min(gcd(bs_src, bs_dst), chunk_tokens) * row bytes)
+ * shorter than 32 KiB with the destination on the source device moves as TMA
+ * tensor tiles (reported as DYNA_ENGINE_BULK with the tile box as piece_bytes;
+ * not under CUDA-graph capture before the library's tile-map cache holds the
+ * geometry); otherwise no BULK engine for runs shorter than 16 KiB. */
 typedef struct {
     int32_t row_bytes;
     int32_t peer;
@@ -241,8 +242,14 @@ DYNA_API dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table d
  * of the destination row, and every other row, is untouched.  Pools must agree
  * on L, d and e; H may differ.  The head slice (n*d*e bytes) and d*e must be
  * multiples of 16.  When both slices are whole rows (n == H_src == H_dst) this
- * is dyna_kv_migrate_ex.  Otherwise: FUSED variant, VEC engine (DYNA_ENOTSUP
- * for others); per-chunk signalling (DYNA_MIGRATE_SIGNAL) as for
+ * is dyna_kv_migrate_ex.  Otherwise: FUSED variant (DYNA_ENOTSUP for STAGED).
+ * Engines: DYNA_ENGINE_BULK / BULK_WS = TMA tensor tiles (a block's slices of
+ * several (layer, K|V) slabs per tensor load / store; DYNA_ENOTSUP when no tensor
+ * map can describe the slice: slices over 2 KiB that are not a multiple of
+ * 2 KiB, or a miss of the library's tile-map cache under CUDA-graph capture);
+ * DYNA_ENGINE_VEC = 16-B vector copies; AUTO = tiles when they apply and the
+ * destination is on the source device, else VEC.  Per-chunk signalling
+ * (DYNA_MIGRATE_SIGNAL) as for
  * dyna_kv_migrate_ex, with a chunk's bytes counted as its slices.  An empty
  * head range is an empty migration.  Errors as dyna_kv_migrate_ex, plus
  * DYNA_ERANGE for head ranges outside either pool. */
@@ -261,8 +268,8 @@ DYNA_API dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_tabl
  * instead of n (entries one after the other in the launch's work order).  Destination aliasing
  * (R7) is checked per head: entries may write different heads of the same rows.  Per-chunk
  * signalling gives every entry its own epoch and slots (dyna_kv_batch_info with the entry's
- * index).  VEC engine, FUSED variant (DYNA_ENOTSUP otherwise); other rules as
- * dyna_kv_migrate_batch. */
+ * index).  FUSED variant (DYNA_ENOTSUP otherwise); engines as dyna_kv_migrate_heads
+ * (one engine for the whole launch); other rules as dyna_kv_migrate_batch. */
 typedef struct {
     dyna_block_table src, dst;
     dyna_range src_heads;

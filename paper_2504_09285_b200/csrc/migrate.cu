@@ -227,9 +227,11 @@ static bool stream_capturing(cudaStream_t st) {
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   return cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
 }
-static bool want_tiles(const dyna_kv_opts& o) {
+// AUTO keeps peer destinations (another GPU, or an imported pool) on VEC: tensor stores into peer
+// memory have not been measured on a multi-GPU box; explicit BULK allows them.
+static bool want_tiles(const dyna_kv_opts& o, bool peer) {
   if (o.engine == DYNA_ENGINE_BULK || o.engine == DYNA_ENGINE_BULK_WS) return true;
-  return o.engine == DYNA_ENGINE_AUTO && tiles_enabled();
+  return o.engine == DYNA_ENGINE_AUTO && tiles_enabled() && !peer;
 }
 
 // Where a tile plan's maps come from: the channel's cached device copy (*cached), else the host
@@ -597,7 +599,7 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
                             tr.end, l0, lm, chunk_tokens, gcd64(gs.block_size, gd.block_size), piece);
   alignas(64) char maps[kTileMaps * kTileMapBytes];
   const char* cached = nullptr;
-  bool tiles = want_tiles(o) && tile_shape(p);
+  bool tiles = want_tiles(o, peer_dst != 0) && tile_shape(p);
   if (tiles && (r = tile_maps(S, D, p, stream, &cached, maps, &tiles))) return r;
   if (!tiles && o.engine != DYNA_ENGINE_AUTO && o.engine != DYNA_ENGINE_VEC)
     return fail(DYNA_ENOTSUP, "head slices of %lld B on the BULK engine: the geometry does not fit a TMA tensor map "
@@ -846,7 +848,10 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
   std::vector<char> maps_h;
   std::vector<const char*> cached(n, nullptr);  // channel-cached device maps per entry (else uploaded)
-  bool tiles = want_tiles(o);
+  bool any_peer = false;
+  for (int32_t i = 0; i < n; ++i)
+    any_peer |= migs[i].dst.pool->dev != migs[i].src.pool->dev || migs[i].dst.pool->imported;
+  bool tiles = want_tiles(o, any_peer);
   if (tiles) maps_h.resize((size_t)n * kTileMaps * kTileMapBytes + 64);
   char* maps = tiles ? reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(maps_h.data()) + 63) & ~uintptr_t(63))
                      : nullptr;
