@@ -1346,7 +1346,8 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
     return;
   }
   if (lane != 0) return;
-  // ---------------- issuer (warp 0, lane 0)
+  // ---------------- issuer (warp 0, lane 0); the box geometry is the launch's (every plan of a
+  // multi-plan tile launch has the same g, row, lkb and slot: checked on the host)
   const int32_t slot = p.tile_bytes;
   const uint32_t g = (uint32_t)p.g;
   const uint32_t row_box = (uint32_t)(p.row * p.lkb);  // bytes of one single-row box

@@ -1076,7 +1076,11 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
       const int64_t g = gcd64(S->desc.block_size, D->desc.block_size);
       tplans[k] = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), S->row, S->row, 0, D->row, 0,
                                    mg.token_range.begin, mg.token_range.end, l0, lm, chunk_tokens, g, ch.piece);
-      tiles = tile_shape(tplans[k]) && tplans[k].tile_bytes == tplans[0].tile_bytes;
+      // one box geometry for the whole launch (the kernel's issuer takes g, the slab count and the
+      // slot from the launch's first plan): entries must agree on the run grid too
+      tiles = tile_shape(tplans[k]) && tplans[k].tile_bytes == tplans[0].tile_bytes &&
+              tplans[k].g == tplans[0].g && tplans[k].lkb == tplans[0].lkb &&
+              tplans[k].tile_rstride == tplans[0].tile_rstride;
       auto it = pair_idx.find({S, D});
       if (it == pair_idx.end()) {
         it = pair_idx.emplace(std::make_pair(S, D), (int32_t)pair_rep.size()).first;

@@ -440,3 +440,25 @@ def test_batch_small_rows_as_tiles(signal, host_tables):
         dk.dyna_kv_copy_flags(dst[i].handle, sender, first, nck, fl.data_ptr(), 0)
         torch.cuda.synchronize()
         assert nck == -(-(tr[1] - tr[0]) // 128) and (fl.numpy() == epoch).all()
+
+
+def test_batch_tiles_need_one_run_grid():
+    """Regression (seeded fuzzing): entries whose run grids differ (16- vs 8-token destination
+    blocks) can still produce equal tile boxes (16 rows x 2 slabs = 8 rows x 4 slabs = 32 KiB of
+    1-KiB rows); one tile launch takes its box geometry from its first plan, so such a batch must
+    not be tiled.  It runs (on another engine) bit-exact."""
+    gs = Geom(2, 8, 64, 2, 16, 300)                        # 1-KiB rows
+    gd1, gd2 = gs.with_(block_size=16), gs.with_(block_size=8, num_blocks=600)
+    hs = kvgen.fill_bytes(1, gs.pool_bytes)
+    h1, h2 = kvgen.fill_bytes(2, gd1.pool_bytes), kvgen.fill_bytes(3, gd2.pool_bytes)
+    (ta, t1), (tb, t2) = kvgen.table_pair(4, 700, gs, gd1), kvgen.table_pair(5, 700, gs, gd2)
+    tb = (tb + 150) % 300
+    w1, w2 = h1.copy(), h2.copy()
+    oracle.migrate(hs, gs, ta, w1, gd1, t1, (0, 600))
+    oracle.migrate(hs, gs, tb, w2, gd2, t2, (3, 650))
+    src, d1, d2 = pool_from_host(gs, hs), pool_from_host(gd1, h1), pool_from_host(gd2, h2)
+    x = dk.migrate_batch([(dev_table(src, ta), dev_table(d1, t1), (0, 600)),
+                          (dev_table(src, tb), dev_table(d2, t2), (3, 650))], (0, 2), 128)
+    dk.dyna_kv_wait(x)
+    assert np.array_equal(d1.tensor.cpu().numpy(), w1)
+    assert np.array_equal(d2.tensor.cpu().numpy(), w2)

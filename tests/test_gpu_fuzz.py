@@ -36,7 +36,7 @@ def _case(rng):
     l1 = int(rng.integers(l0, L + 1))
     c = int(rng.choice([1, 3, 16, 17, 64, 100, 257, 1000]))
     variant = int(rng.choice([1, 2]))
-    engine = int(rng.choice([1, 2, 3]))
+    engine = int(rng.choice([0, 1, 2, 3]))        # 0 = AUTO: short runs as TMA tiles
     piece = int(rng.choice([0, 256, 1024, 4096, 16384, 32768]))
     stages = int(rng.choice([0, 2, 3, 4, 6, 8]))
     unroll = int(rng.choice([0, 4, 8, 16]))
@@ -85,6 +85,7 @@ def test_fuzz_migrate_heads(block):
         c = int(rng.choice([1, 7, 16, 100, 1000]))
         piece = int(rng.choice([0, 256, 4096]))
         sig = dk.DYNA_MIGRATE_SIGNAL if rng.integers(0, 2) else 0
+        engine = int(rng.choice([0, 1]))          # AUTO (TMA tiles) / VEC (row kernel)
         ts, td = kvgen.table_pair(int(rng.integers(1 << 30)), n_tok, gs, gd)
         hs = kvgen.fill_bytes(int(rng.integers(1 << 30)), gs.pool_bytes)
         hdst = kvgen.fill_bytes(int(rng.integers(1 << 30)), gd.pool_bytes)
@@ -93,8 +94,8 @@ def test_fuzz_migrate_heads(block):
         src, dst = pool_from_host(gs, hs), pool_from_host(gd, hdst)
         st, dt = dev_table(src, ts), dev_table(dst, td)
         dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(st, dt, tr, (0, L), (h0, h0 + n), hd0, c, 0,
-                                                 dk.opts(piece_bytes=piece, flags=sig)))
-        assert np.array_equal(dst.tensor.cpu().numpy(), want), (i, gs, gd, tr, (h0, n, hd0), c, piece)
+                                                 dk.opts(piece_bytes=piece, flags=sig, engine=engine)))
+        assert np.array_equal(dst.tensor.cpu().numpy(), want), (i, gs, gd, tr, (h0, n, hd0), c, piece, engine)
 
 
 @pytest.mark.parametrize("block", range(2 * SCALE))
