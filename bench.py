@@ -530,6 +530,23 @@ def run_dyna(args, rank, world, local_rank):
         cfg_extra["functional_run"] = "DYNA_BENCH_SMALL=1: reduced pools, not a measurement"
     torch.cuda.synchronize()
 
+    # N > 1 with AUTO: the built-in calibration has no NVLink entries (measured on one GPU), so the
+    # engine for the peer stores is chosen here, before the timed region, from a short device-timed
+    # run of each candidate (max over ranks, so every rank picks the same one)
+    if world > 1 and args.engine == 0:
+        cands = [("auto", dk.opts(piece_bytes=args.piece, stages=args.stages)),
+                 ("vec", dk.opts(engine=dk.DYNA_ENGINE_VEC, piece_bytes=args.piece)),
+                 ("ring", dk.opts(engine=dk.DYNA_ENGINE_BULK, piece_bytes=args.piece, stages=args.stages))]
+        probe_ms = {}
+        for name, o in cands:
+            mopts = o
+            probe_ms[name] = ctx.timed(step, 4, 2)[0] / 4
+        best = min(probe_ms, key=probe_ms.get)
+        mopts = dict(cands)[best]
+        sig_opts = dk.opts(engine=mopts.engine, piece_bytes=args.piece, stages=args.stages, flags=sig)
+        extra["engine_probe"] = {"ms_per_step": probe_ms, "chosen": best,
+                                 "how": "4 device-timed steps per candidate after 2 warm-up, max over ranks"}
+
     probe = step(0)
     plan_used = dk.dyna_kv_xfer_plan(probe)
     dk.dyna_kv_wait(probe)
