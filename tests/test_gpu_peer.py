@@ -52,7 +52,8 @@ def test_peer_parity(variant, engine, signal):
         assert (fl.numpy() == epoch).all()
 
 
-def test_peer_head_reshard():
+@pytest.mark.parametrize("engine", [0, 1, 2], ids=["auto", "vec", "tiles"])
+def test_peer_head_reshard(engine):
     gd = G.with_(num_kv_heads=2, block_size=32, num_blocks=200)
     ts, _ = kvgen.table_pair(8, 3000, G, G)
     td = kvgen.table_pair(9, 3000, gd, gd)[1]
@@ -62,7 +63,8 @@ def test_peer_head_reshard():
     dk.dyna_kv_enable_peer(0, 1)
     src, dst = pool_from_host(G, hs, device=0), pool_from_host(gd, hd, device=1)
     torch.cuda.set_device(0)
-    dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(_tab(src, ts, 0), _tab(dst, td, 0), (0, 2500), (0, 4), (6, 8), 0, 256, 0))
+    dk.dyna_kv_wait(dk.dyna_kv_migrate_heads(_tab(src, ts, 0), _tab(dst, td, 0), (0, 2500), (0, 4), (6, 8), 0, 256, 0,
+                                             dk.opts(engine=engine)))
     torch.cuda.synchronize(1)
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
 

@@ -83,7 +83,7 @@ def test_ipc_push_with_chunk_flags(engine):
     assert untouched_equal(dst, DST_SEED, mapped_mask(g, [(td, (0, S))]))
 
 
-def _heads_sender(handle: bytes, q):
+def _heads_sender(handle: bytes, q, engine: int = 0):
     """TP-1 sender (8 heads) pushes heads [4, 8) into the importer's TP-2 rank-1 pool (4 heads)."""
     try:
         import torch
@@ -98,8 +98,9 @@ def _heads_sender(handle: bytes, q):
         ts, _ = kvgen.table_pair(9, 4000, g, g)
         _, td = kvgen.table_pair(10, 4000, g.with_(num_kv_heads=4), g.with_(num_kv_heads=4))
         x = dk.dyna_kv_migrate_heads(dev_table(src, ts), dk.table(dst, torch.from_numpy(td).cuda(), td), (0, S),
-                                     (0, 4), (4, 8), 0, CHUNK, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL))
+                                     (0, 4), (4, 8), 0, CHUNK, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL, engine=engine))
         info = dk.dyna_kv_xfer_info(x)
+        assert engine != dk.DYNA_ENGINE_BULK or dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_BULK
         dk.dyna_kv_wait(x)
         dst.close()
         q.put(("ok", info))
@@ -107,8 +108,11 @@ def _heads_sender(handle: bytes, q):
         q.put(("err", repr(e)))
 
 
-def test_ipc_head_reshard_with_chunk_flags():
-    """TP resharding across processes (reading R14): bit-exact against oracle.migrate_heads."""
+@pytest.mark.parametrize("engine", [0, 2], ids=["auto", "tiles"])
+def test_ipc_head_reshard_with_chunk_flags(engine):
+    """TP resharding across processes (reading R14): bit-exact against oracle.migrate_heads.  AUTO keeps
+    an imported destination on VEC; explicit BULK runs the TMA tile kernel's tensor stores into the
+    IPC-mapped pool (on a multi-GPU box: over NVLink)."""
     import torch
 
     import kvgen
@@ -123,7 +127,7 @@ def test_ipc_head_reshard_with_chunk_flags():
     handle = dk.dyna_kv_pool_export(dst.handle)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    p = ctx.Process(target=_heads_sender, args=(handle, q))
+    p = ctx.Process(target=_heads_sender, args=(handle, q, engine))
     p.start()
     status, info = q.get(timeout=300)
     p.join(timeout=60)
