@@ -28,6 +28,9 @@ Reported per (c, SM budget), all from CUDA events inside the same run:
   layered          pushes (chunk k, layer l) as soon as layer l of chunk k is done
                    (one dyna_kv_migrate per chunk x layer, host-enqueued)
   ready_layers     one coupled launch with DYNA_READY_PER_LAYER marks
+  ready_tail       a coupled launch (per-chunk marks) for every chunk but the last, and the
+                   last chunk pushed by a full-width dyna_kv_migrate once the producer ends
+                   (the coupled kernel's CTA budget no longer caps the tail)
 On one GPU the migration is an intra-device reblock (HBM); on the 8-GPU box
 the same script with a peer destination measures the NVLink form.
 """
@@ -74,7 +77,7 @@ def main():
     st = dk.table(src, torch.from_numpy(ts).cuda(), ts)
     dt = dk.table(dst, torch.from_numpy(td).cuda(), td)   # read by the kernel on the source GPU (cuda:0)
     W = torch.randn(4096, 14336, dtype=torch.bfloat16, device="cuda") * 0.01
-    prod, mig = torch.cuda.Stream(), torch.cuda.Stream()
+    prod, mig, mig2 = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     payload = s * 2 * g.num_layers * g.row_bytes
     results = []
 
@@ -96,11 +99,14 @@ def main():
         e0.record(prod)
         mig.wait_event(e0)
         handles = []
-        if mode in ("ready", "ready_layers"):   # one launch for the whole range; waits on the device for marks
+        if mode in ("ready", "ready_layers", "ready_tail"):   # one launch; waits on the device for marks
             epoch = dk.dyna_kv_ready_begin(board)
             fl = dk.DYNA_READY_PER_LAYER if mode == "ready_layers" else 0
-            handles.append(dk.dyna_kv_migrate_on_ready(st, dt, (0, s), (0, 32), c, board, epoch, mig.cuda_stream,
-                                                       dk.opts(max_ctas=budget or args.ready_ctas, flags=fl)))
+            end = (nck - 1) * c if mode == "ready_tail" else s
+            if end > 0:
+                handles.append(dk.dyna_kv_migrate_on_ready(st, dt, (0, end), (0, 32), c, board, epoch,
+                                                           mig.cuda_stream,
+                                                           dk.opts(max_ctas=budget or args.ready_ctas, flags=fl)))
         for k in range(nck):
             if mode in ("layered", "ready_layers"):
                 for l in range(g.num_layers):
@@ -117,8 +123,16 @@ def main():
                 continue
             with torch.cuda.stream(prod):
                 producer_chunk(X)
-            if mode == "ready":
+            if mode == "ready" or (mode == "ready_tail" and k < nck - 1):
                 dk.dyna_kv_ready_mark(board, k, epoch, prod.cuda_stream)
+            if mode == "ready_tail" and k == nck - 1:   # the last chunk: full width, beside the coupled kernel
+                ev = torch.cuda.Event()
+                ev.record(prod)
+                mig2.wait_event(ev)
+                handles.append(dk.migrate(st, dt, (k * c, s), (0, 32), c, stream=mig2, max_ctas=budget))
+                e_tail = torch.cuda.Event(enable_timing=True)
+                e_tail.record(mig2)
+                mig.wait_event(e_tail)
             if mode == "chunked":    # chunk k complete -> push it now
                 ev = torch.cuda.Event()
                 ev.record(prod)
@@ -149,10 +163,11 @@ def main():
         t_mig = a0.elapsed_time(a1)
         prod_alone = statistics.median(run(c, "none", 0)[0] for _ in range(args.reps))
         for budget in [int(x) for x in args.budgets.split(",")]:
-            W_, C_, R_, LY, RL = [], [], [], [], []
+            W_, C_, R_, LY, RL, RT = [], [], [], [], [], []
             run(c, "whole", budget)
             run(c, "chunked", budget)   # warm
             run(c, "ready", budget)
+            run(c, "ready_tail", budget)
             if args.layers:
                 run(c, "layered", budget)
                 run(c, "ready_layers", budget)
@@ -160,6 +175,7 @@ def main():
                 W_.append(run(c, "whole", budget))
                 C_.append(run(c, "chunked", budget))
                 R_.append(run(c, "ready", budget))
+                RT.append(run(c, "ready_tail", budget))
                 if args.layers:
                     LY.append(run(c, "layered", budget))
                     RL.append(run(c, "ready_layers", budget))
@@ -177,6 +193,11 @@ def main():
                  "ready_coupled": {"ctas": budget or args.ready_ctas, "exposed_ms": exp_r, "T_prod_ms": prod_r,
                                    "producer_slowdown": prod_r / prod_alone - 1,
                                    "reduction": 1 - exp_r / exp_w if exp_w > 0 else None}}
+            exp_t = statistics.median(e for _, e in RT)
+            prod_t = statistics.median(p for p, _ in RT)
+            r["ready_tail"] = {"ctas": budget or args.ready_ctas, "exposed_ms": exp_t, "T_prod_ms": prod_t,
+                               "producer_slowdown": prod_t / prod_alone - 1,
+                               "reduction": 1 - exp_t / exp_w if exp_w > 0 else None}
             if args.layers:
                 for name, runs in (("layered", LY), ("ready_layers", RL)):
                     exp_l = statistics.median(e for _, e in runs)
