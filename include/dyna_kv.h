@@ -398,6 +398,11 @@ DYNA_API dyna_status dyna_kv_ready_mark(dyna_kv_ready_t board, int32_t chunk, ui
  * written its KV, and those rows move as soon as that mark is visible, while
  * the prefill still computes the chunk's later layers.  The board then needs
  * num_chunks*(l1-l0) slots.
+ * Tail: with one mark per chunk, the chunk marked last is moved by the capped
+ * grid after the producer ends (at 512-MiB chunks that exposes more than one
+ * whole-range push).  Cover every chunk but the last with the
+ * coupled launch and push the last chunk with dyna_kv_migrate (full width) on
+ * a stream that waits for the producer — or mark per (chunk, layer).
  * Cancellation (when r^alpha ends before s, "its
  * transfer is aborted"): see dyna_kv_ready_cancel.  The board must outlive
  * every migration launched on it (until dyna_kv_wait returns). */
