@@ -530,22 +530,24 @@ def run_dyna(args, rank, world, local_rank):
         cfg_extra["functional_run"] = "DYNA_BENCH_SMALL=1: reduced pools, not a measurement"
     torch.cuda.synchronize()
 
-    # N > 1 with AUTO: the built-in calibration has no NVLink entries (measured on one GPU), so the
-    # engine for the peer stores is chosen here, before the timed region, from a short device-timed
-    # run of each candidate (max over ranks, so every rank picks the same one)
+    # N > 1 with AUTO: the built-in calibration has no NVLink entries (it was measured on one GPU), so
+    # before the timed region each rank measures its own peer pair with the library's native
+    # calibration (dyna_kv_calibrate: every candidate variant x engine at the workload's chunk size,
+    # device-timed) and AUTO then uses the installed choice
     if world > 1 and args.engine == 0:
-        cands = [("auto", dk.opts(piece_bytes=args.piece, stages=args.stages)),
-                 ("vec", dk.opts(engine=dk.DYNA_ENGINE_VEC, piece_bytes=args.piece)),
-                 ("ring", dk.opts(engine=dk.DYNA_ENGINE_BULK, piece_bytes=args.piece, stages=args.stages))]
-        probe_ms = {}
-        for name, o in cands:
-            mopts = o
-            probe_ms[name] = ctx.timed(step, 4, 2)[0] / 4
-        best = min(probe_ms, key=probe_ms.get)
-        mopts = dict(cands)[best]
-        sig_opts = dk.opts(engine=mopts.engine, piece_bytes=args.piece, stages=args.stages, flags=sig)
-        extra["engine_probe"] = {"ms_per_step": probe_ms, "chosen": best,
-                                 "how": "4 device-timed steps per candidate after 2 warm-up, max over ranks"}
+        if workload == "t4":
+            cal_st, cal_dt, cal_c = dtabs[0][0], dtabs[0][1], n_tok
+        else:
+            big = max(range(len(out_m)), key=lambda k: out_m[k].req.s)
+            cal_st, cal_dt, cal_c = migs[big][0], migs[big][1], min(C4_CHUNK, out_m[big].req.s)
+        entries, rates = dk.dyna_kv_calibrate(cal_st, cal_dt, [cal_c], reps=4, stream=cs)
+        names = ["FUSED VEC 4K U8", "FUSED VEC 8K U4", "FUSED VEC 16K U16", "FUSED BULK ring 32K x4",
+                 "STAGED VEC 8K U8", "STAGED BULK 32K x4"]
+        extra["calibration"] = {"chunk_tokens": cal_c, "entry": entries[0],
+                                "GBps": dict(zip(names, [round(x, 1) for x in rates[0]])),
+                                "how": "dyna_kv_calibrate on this rank's peer pair before the timed region "
+                                       "(4 device-timed calls per candidate; 0 = not applicable)"}
+        ctx.barrier()
 
     probe = step(0)
     plan_used = dk.dyna_kv_xfer_plan(probe)

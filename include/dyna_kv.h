@@ -40,7 +40,7 @@
  *   TP resharding    dyna_kv_migrate_heads, dyna_kv_reshard (all rank pairs, one launch),
  *                    dyna_kv_push_heads / _place_heads
  *   halves           dyna_kv_pack / _unpack (source rows -> contiguous buffer -> destination rows)
- *   selection        dyna_kv_calib_set / _get (the measured AUTO table)
+ *   selection        dyna_kv_calib_set / _get (the measured AUTO table), dyna_kv_calibrate (measure it here)
  *
  * Errors: every call returns a dyna_status; negative values are errors and
  * dyna_kv_last_error() returns a thread-local message.  No call throws.
@@ -550,6 +550,30 @@ DYNA_API dyna_status dyna_kv_copy_flags(dyna_kv_pool_t dst, int32_t sender, int3
 DYNA_API dyna_status dyna_kv_calib_set(const dyna_kv_calib_entry* entries, int32_t n);
 /* Copy up to cap entries of the current table into out; returns the entry count (>= 0). */
 DYNA_API int32_t dyna_kv_calib_get(dyna_kv_calib_entry* out, int32_t cap);
+
+/* Measure AUTO's choice on this hardware for one (source pool, destination pool) pair and
+ * install it (north_star item 4: the fused variant "chosen over the staged variant
+ * per chunk size by measured bandwidth").  For each of the n chunk sizes chunk_tokens[i], every
+ * candidate below migrates `reps` calls of that many tokens (all layers; token offsets cycling
+ * through the tables so a call does not find the previous one's rows in L2) back to back while
+ * the stream is held by a device-side gate, so the CUDA events around them time device work
+ * only; the fastest candidate becomes the entry (row bytes of the pair, its locality: same
+ * GPU = 0, other GPU or imported pool = 1, max_chunk_tokens = chunk_tokens[i]; the largest size
+ * also covers every longer call), replacing the table's entries for that (row bytes, locality).
+ * Candidates, in order (DYNA_CALIB_CANDIDATES): FUSED VEC 4 KiB x U8, FUSED VEC 8 KiB x U4,
+ * FUSED VEC 16 KiB x U16, FUSED BULK ring 32 KiB x 4, STAGED VEC 8 KiB x U8, STAGED BULK
+ * 32 KiB x 4 (STAGED is skipped — 0 GB/s — into an imported pool or a destination table without
+ * device ids on another GPU).  out[i] receives the entry for chunk_tokens[i]; gbps (NULL or
+ * n x DYNA_CALIB_CANDIDATES floats) the payload GB/s of every candidate.  Tables: as
+ * dyna_kv_migrate_ex (host ids or DYNA_MIGRATE_UNCHECKED semantics: the destination rows must
+ * be distinct); both must cover at least the largest chunk size.  The call OVERWRITES the
+ * destination rows its tables map, and synchronises `stream` (a startup-time call).  Errors:
+ * DYNA_EINVAL (n <= 0, chunk sizes <= 0 or not ascending, reps < 1), DYNA_ERANGE (a chunk size
+ * longer than the tables), or any error of the migrations it runs. */
+#define DYNA_CALIB_CANDIDATES 6
+DYNA_API dyna_status dyna_kv_calibrate(dyna_block_table src, dyna_block_table dst, const int32_t* chunk_tokens,
+                                       int32_t n, int32_t reps, struct CUstream_st* stream,
+                                       dyna_kv_calib_entry* out, float* gbps);
 
 /* Thread-local description of the last error on this thread. */
 DYNA_API const char* dyna_kv_last_error(void);

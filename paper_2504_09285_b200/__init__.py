@@ -39,7 +39,7 @@ EXPORTS = (
     "dyna_kv_migrate_ex", "dyna_kv_wait", "dyna_kv_query", "dyna_kv_stream_wait", "dyna_kv_xfer_info",
     "dyna_kv_stream_wait_chunk", "dyna_kv_last_error", "dyna_kv_poll_error", "dyna_kv_launch_count",
     "dyna_kv_enable_peer", "dyna_kv_pool_export", "dyna_kv_pool_import", "dyna_kv_debug_fill",
-    "dyna_kv_copy_flags", "dyna_kv_calib_set", "dyna_kv_calib_get", "dyna_kv_migrate_batch",
+    "dyna_kv_copy_flags", "dyna_kv_calib_set", "dyna_kv_calib_get", "dyna_kv_calibrate", "dyna_kv_migrate_batch",
     "dyna_kv_xfer_plan", "dyna_kv_ready_create", "dyna_kv_ready_destroy", "dyna_kv_ready_begin",
     "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready", "dyna_kv_ready_set_timeout",
     "dyna_kv_channel_create", "dyna_kv_channel_export", "dyna_kv_channel_import", "dyna_kv_channel_destroy",
@@ -163,6 +163,8 @@ def _load():
         "dyna_kv_copy_flags": (st, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp]),
         "dyna_kv_calib_set": (st, [p(dyna_kv_calib_entry), ctypes.c_int32]),
         "dyna_kv_calib_get": (ctypes.c_int32, [p(dyna_kv_calib_entry), ctypes.c_int32]),
+        "dyna_kv_calibrate": (st, [dyna_block_table, dyna_block_table, p(ctypes.c_int32), ctypes.c_int32,
+                                   ctypes.c_int32, vp, p(dyna_kv_calib_entry), p(ctypes.c_float)]),
         "dyna_kv_last_error": (ctypes.c_char_p, []),
         "dyna_kv_poll_error": (st, []),
         "dyna_kv_launch_count": (ctypes.c_uint64, []),
@@ -470,6 +472,23 @@ def dyna_kv_calib_get() -> list:
     arr = (dyna_kv_calib_entry * max(1, n))()
     lib.dyna_kv_calib_get(arr, n)
     return [tuple(getattr(arr[i], f) for f, _ in dyna_kv_calib_entry._fields_) for i in range(n)]
+
+
+DYNA_CALIB_CANDIDATES = 6
+
+
+def dyna_kv_calibrate(src: dyna_block_table, dst: dyna_block_table, chunk_tokens, reps: int = 8,
+                      stream: int = 0) -> tuple[list, list]:
+    """Measure and install AUTO's per-chunk-size choice for this pool pair.  Returns (entries, GB/s per
+    candidate per chunk size)."""
+    n = len(chunk_tokens)
+    ct = (ctypes.c_int32 * n)(*chunk_tokens)
+    out = (dyna_kv_calib_entry * n)()
+    gb = (ctypes.c_float * (n * DYNA_CALIB_CANDIDATES))()
+    _check(lib.dyna_kv_calibrate(src, dst, ct, n, reps, ctypes.c_void_p(stream), out, gb))
+    entries = [tuple(getattr(out[i], f) for f, _ in dyna_kv_calib_entry._fields_) for i in range(n)]
+    rates = [[gb[i * DYNA_CALIB_CANDIDATES + k] for k in range(DYNA_CALIB_CANDIDATES)] for i in range(n)]
+    return entries, rates
 
 
 def dyna_kv_last_error() -> str:

@@ -1210,6 +1210,98 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   return DYNA_OK;
 }
 
+// ---------------------------------------------------------------- a6: measure the AUTO table here
+dyna_status dyna_kv_calibrate(dyna_block_table src, dyna_block_table dst, const int32_t* chunk_tokens, int32_t n,
+                              int32_t reps, struct CUstream_st* stream_, dyna_kv_calib_entry* out, float* gbps) {
+  if (n <= 0 || !chunk_tokens || !out || reps < 1) return fail(DYNA_EINVAL, "calibrate: n > 0, chunk sizes, out, reps >= 1");
+  for (int32_t i = 0; i < n; ++i)
+    if (chunk_tokens[i] <= 0 || (i && chunk_tokens[i] <= chunk_tokens[i - 1]))
+      return fail(DYNA_EINVAL, "calibrate: chunk sizes must be positive and ascending");
+  if (!src.pool || !dst.pool) return fail(DYNA_EINVAL, "NULL pool in a block table");
+  dyna_kv_pool *S = src.pool, *D = dst.pool;
+  const int64_t T = std::min<int64_t>(src.len * S->desc.block_size, dst.len * D->desc.block_size);
+  if (chunk_tokens[n - 1] > T)
+    return fail(DYNA_ERANGE, "calibrate: chunk of %d tokens > the tables' %lld tokens", chunk_tokens[n - 1],
+                (long long)T);
+  struct Cand { int32_t variant, engine, piece, stages, unroll; };
+  static const Cand kCands[DYNA_CALIB_CANDIDATES] = {
+      {DYNA_VARIANT_FUSED, DYNA_ENGINE_VEC, 4096, 0, 8},   {DYNA_VARIANT_FUSED, DYNA_ENGINE_VEC, 8192, 0, 4},
+      {DYNA_VARIANT_FUSED, DYNA_ENGINE_VEC, 16384, 0, 16}, {DYNA_VARIANT_FUSED, DYNA_ENGINE_BULK, 32768, 4, 0},
+      {DYNA_VARIANT_STAGED, DYNA_ENGINE_VEC, 8192, 0, 8},  {DYNA_VARIANT_STAGED, DYNA_ENGINE_BULK, 32768, 4, 0}};
+  const int peer = (D->dev != S->dev || D->imported) ? 1 : 0;
+  const bool staged_ok = !D->imported && (D->dev == S->dev || dst.block_ids);
+  const int64_t L = S->desc.num_layers;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  DeviceGuard guard(S->dev);
+  // the gate: a one-thread kernel spinning on a mapped host word holds the stream while the host
+  // enqueues a candidate's calls, so the events around them see device time only
+  unsigned long long* gate = nullptr;
+  CUDA_TRY(cudaHostAlloc(&gate, sizeof(unsigned long long), cudaHostAllocMapped | cudaHostAllocPortable));
+  *gate = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  dyna_status r = DYNA_OK;
+  std::vector<dyna_kv_calib_entry> chosen;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+    r = fail(DYNA_ECUDA, "calibrate: events");
+  unsigned long long open = 0;
+  for (int32_t i = 0; i < n && !r; ++i) {
+    const int64_t c = chunk_tokens[i];
+    float best_ms = 0.f;
+    int best = -1;
+    for (int k = 0; k < DYNA_CALIB_CANDIDATES && !r; ++k) {
+      const Cand& cd = kCands[k];
+      if (gbps) gbps[i * DYNA_CALIB_CANDIDATES + k] = 0.f;
+      if (cd.variant == DYNA_VARIANT_STAGED && !staged_ok) continue;
+      dyna_kv_opts o{cd.variant, cd.engine, 0, 0, cd.piece, cd.stages, cd.unroll, 0};
+      for (int pass = 0; pass < 2 && !r; ++pass) {
+        // pass 0, ungated, warms up whatever a first call allocates (staging, error words): an
+        // allocation that synchronises the device must not meet a closed gate
+        if (pass == 1) {
+          ++open;
+          launch_wait_flag(gate, open, 10ull * 1000 * 1000 * 1000, stream, nullptr);
+          if (cudaEventRecord(e0, stream) != cudaSuccess) r = fail(DYNA_ECUDA, "calibrate: event");
+        }
+        std::vector<dyna_kv_xfer_t> xs;
+        for (int32_t j = 0; j < (pass ? reps : 1) && !r; ++j) {
+          const int64_t span = T - c + 1;
+          const int64_t t0 = ((int64_t)j * c) % span;
+          dyna_kv_xfer_t x = nullptr;
+          r = dyna_kv_migrate_ex(src, dst, dyna_range{t0, t0 + c}, dyna_range{0, L}, (int32_t)c, stream_, &o, &x);
+          if (!r) xs.push_back(x);
+        }
+        if (pass == 1 && !r && cudaEventRecord(e1, stream) != cudaSuccess) r = fail(DYNA_ECUDA, "calibrate: event");
+        if (pass == 1) __atomic_store_n(gate, open, __ATOMIC_RELEASE);  // open: the queued calls run back to back
+        for (dyna_kv_xfer_t x : xs) {
+          const dyna_status w = dyna_kv_wait(x);
+          if (!r) r = w;
+        }
+      }
+      if (r) break;
+      float ms = 0.f;
+      CUDA_TRY(cudaEventSynchronize(e1));
+      CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      ms /= (float)reps;
+      const double bytes = (double)c * 2 * L * S->row;
+      if (gbps) gbps[i * DYNA_CALIB_CANDIDATES + k] = (float)(bytes / (ms * 1e-3) / 1e9);
+      if (best < 0 || ms < best_ms) best_ms = ms, best = k;
+    }
+    if (!r && best >= 0) {
+      const Cand& cd = kCands[best];
+      out[i] = dyna_kv_calib_entry{(int32_t)S->row, peer, i == n - 1 ? (int32_t)1073741824 : (int32_t)c,
+                                   cd.variant, cd.engine, cd.piece, cd.stages, cd.unroll};
+      chosen.push_back(out[i]);
+    }
+  }
+  __atomic_store_n(gate, ~0ull, __ATOMIC_RELEASE);
+  cudaStreamSynchronize(stream);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  cudaFreeHost(gate);
+  if (r) return r;
+  calib_install(S->row, peer, chosen);
+  return DYNA_OK;
+}
+
 dyna_status dyna_kv_query(dyna_kv_xfer_t x) {
   if (!x) return fail(DYNA_EINVAL, "NULL xfer");
   if (x->empty || x->captured) return DYNA_OK;

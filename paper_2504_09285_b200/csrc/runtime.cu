@@ -162,6 +162,16 @@ bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out) {
   return false;
 }
 
+// Replace the entries of one (row bytes, locality) class by measured ones (dyna_kv_calibrate).
+void calib_install(int64_t row, int peer, const std::vector<dyna_kv_calib_entry>& es) {
+  std::lock_guard<std::mutex> lk(g_calib_mu);
+  std::vector<dyna_kv_calib_entry> keep;
+  for (const auto& e : g_calib)
+    if (!(e.row_bytes == row && e.peer == peer)) keep.push_back(e);
+  keep.insert(keep.end(), es.begin(), es.end());
+  g_calib.swap(keep);
+}
+
 Side paged(const dyna_kv_pool* pool, const int32_t* ids) {
   Side s{};
   s.base = pool->base;

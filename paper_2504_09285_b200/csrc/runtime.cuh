@@ -100,6 +100,7 @@ void put_event(int dev, cudaEvent_t ev);
 bool desc_valid(const dyna_kv_pool_desc* d);
 int64_t gcd64(int64_t a, int64_t b);
 bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out);
+void calib_install(int64_t row, int peer, const std::vector<dyna_kv_calib_entry>& es);
 dyna_status ensure_peer(int dev, int peer);
 // Per-chunk flags: each signalled logical migration gets a fresh epoch and its own range of
 // consecutive inbox slots of (sender instance, destination inbox).  Keyed on the inbox's uid
