@@ -580,6 +580,14 @@ dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int
 }
 
 // ------------------------------------------------------------------ staged variant (a2, a3, a4)
+static bool k2_dma() {
+  static const bool on = [] {
+    const char* e = std::getenv("DYNA_KV_K2_KERNEL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 // K1 gather -> source staging slot, K2 slot -> destination-side slot, K3 scatter
 // slot -> destination rows (+ per-chunk flag).  Chunks are cut into sub-chunks
 // that fit one staging slot; two slots per side alternate.  Same device:
@@ -646,11 +654,17 @@ dyna_status run_staged(dyna_kv_pool* S, dyna_kv_pool* D, const int32_t* sids, co
       Plan k1 = make_plan(paged(S, sids), linear(sslot), row, sa, sb, l0, lm, sb - sa, S->desc.block_size, piece);
       k1.err = x->err;
       if ((r = launch_copy(k1, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
-      // K2: the sub-chunk slot is [lm][2][n][row] = two contiguous halves
-      // (K and V of all layers): a flat plan with one token of `half` bytes.
-      Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
-      k2.err = x->err;
-      if ((r = launch_copy(k2, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
+      // K2: the sub-chunk slot [lm][2][n][row] is one contiguous range.  By default ONE copy-engine
+      // transfer moves it (across devices a peer copy over NVLink: the paper's "DMA-pushed"),
+      // which occupies no SM beside the producer; DYNA_KV_K2_KERNEL=1 moves it with the copy kernel
+      // (a flat plan: two halves, K and V of all layers, of one `half`-byte token each).
+      if (k2_dma()) {
+        CUDA_TRY(cudaMemcpyAsync(dslot, sslot, (size_t)(2 * (sb - sa) * row * lm), cudaMemcpyDeviceToDevice, stream));
+      } else {
+        Plan k2 = make_plan(linear(sslot), linear(dslot), (sb - sa) * row * lm, 0, 1, 0, 1, 1, 1, piece);
+        k2.err = x->err;
+        if ((r = launch_copy(k2, engine, max_ctas, stages, unroll, S->dev, stream, schedule))) break;
+      }
       Plan k3 = make_plan(linear(dslot), paged(D, dids), row, sa, sb, l0, lm, sb - sa, D->desc.block_size, piece);
       set_chunking(k3, tr.begin, tr.end, c);
       k3.err = x->err;
