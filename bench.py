@@ -542,7 +542,7 @@ def run_dyna(args, rank, world, local_rank):
             cal_st, cal_dt, cal_c = migs[big][0], migs[big][1], min(C4_CHUNK, out_m[big].req.s)
         entries, rates = dk.dyna_kv_calibrate(cal_st, cal_dt, [cal_c], reps=4, stream=cs)
         names = ["FUSED VEC 4K U8", "FUSED VEC 8K U4", "FUSED VEC 16K U16", "FUSED BULK ring 32K x4",
-                 "STAGED VEC 8K U8", "STAGED BULK 32K x4"]
+                 "STAGED VEC 8K U8", "STAGED BULK 32K x4", "FUSED TILES"]
         extra["calibration"] = {"chunk_tokens": cal_c, "entry": entries[0],
                                 "GBps": dict(zip(names, [round(x, 1) for x in rates[0]])),
                                 "how": "dyna_kv_calibrate on this rank's peer pair before the timed region "
@@ -611,7 +611,8 @@ def run_dyna(args, rank, world, local_rank):
                 extra["target_4prime"] = {"per_pair_GBps_needed": 720.0, "chunk_ms_needed": 0.7457,
                                           "chunk_ms": total_ms / args.steps}
         cfg_extra["resolved_plan"] = plan_used
-        eng = {dk.DYNA_ENGINE_VEC: "VEC", dk.DYNA_ENGINE_BULK: "BULK", dk.DYNA_ENGINE_BULK_WS: "BULK"}
+        eng = {dk.DYNA_ENGINE_VEC: "VEC", dk.DYNA_ENGINE_BULK: "BULK", dk.DYNA_ENGINE_BULK_WS: "BULK",
+               dk.DYNA_ENGINE_TILES: "TILES"}
         roof["engine"] = eng.get(plan_used["engine"], str(plan_used["engine"]))
         if roof["engine"] == "VEC":
             roof["kernel"] = roof["kernel"].replace("k_copy_ring<false,", "k_copy_lanes<8, false,")

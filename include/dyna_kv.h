@@ -147,6 +147,11 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
 #define DYNA_ENGINE_BULK 2     /* TMA bulk copies through a shared-memory ring (UBLKCP): one issuing thread,
                                   fed item descriptors by a decoder warp */
 #define DYNA_ENGINE_BULK_WS 3  /* alias of DYNA_ENGINE_BULK (round-1 warp-specialised kernel with DYNA_KV_RING=0) */
+#define DYNA_ENGINE_TILES 4    /* TMA tensor tiles (UTMALDG / UTMASTG): a block's rows (or head slices) of several
+                                  (layer, K|V) slabs per 4-D tensor load / store, one issuing thread fed by a decoder
+                                  warp.  Fused variant only (the staged variant's K1 / K3 then use VEC); DYNA_ENOTSUP
+                                  when no tensor map can describe the rows.  AUTO picks it for
+                                  contiguous runs under 32 KiB on one device and for head slices. */
 /* flags */
 #define DYNA_MIGRATE_SIGNAL 1  /* write a per-chunk flag into the destination pool's inbox */
 #define DYNA_READY_PER_LAYER 2 /* dyna_kv_migrate_on_ready: one ready mark per (chunk, layer), see below */
@@ -180,7 +185,7 @@ typedef struct {
  * run time.  Measured rules apply on top of the table when the engine is
  * AUTO: a contiguous run (min(gcd(bs_src, bs_dst), chunk_tokens) * row bytes)
  * shorter than 32 KiB with the destination on the source device moves as TMA
- * tensor tiles (reported as DYNA_ENGINE_BULK with the tile box as piece_bytes;
+ * tensor tiles (DYNA_ENGINE_TILES, with the ring slot as piece_bytes;
  * not under CUDA-graph capture before the library's tile-map cache holds the
  * geometry); otherwise no BULK engine for runs shorter than 16 KiB. */
 typedef struct {
@@ -188,7 +193,7 @@ typedef struct {
     int32_t peer;
     int32_t max_chunk_tokens;
     int32_t variant;      /* DYNA_VARIANT_FUSED / STAGED */
-    int32_t engine;       /* DYNA_ENGINE_VEC / BULK / BULK_WS */
+    int32_t engine;       /* DYNA_ENGINE_VEC / BULK / BULK_WS / TILES */
     int32_t piece_bytes;  /* 0 = engine default */
     int32_t stages;
     int32_t unroll;
@@ -243,7 +248,7 @@ DYNA_API dyna_status dyna_kv_migrate_ex(dyna_block_table src, dyna_block_table d
  * on L, d and e; H may differ.  The head slice (n*d*e bytes) and d*e must be
  * multiples of 16.  When both slices are whole rows (n == H_src == H_dst) this
  * is dyna_kv_migrate_ex.  Otherwise: FUSED variant (DYNA_ENOTSUP for STAGED).
- * Engines: DYNA_ENGINE_BULK / BULK_WS = TMA tensor tiles (a block's slices of
+ * Engines: DYNA_ENGINE_TILES (and BULK / BULK_WS, its aliases here) = TMA tensor tiles (a block's slices of
  * several (layer, K|V) slabs per tensor load / store; DYNA_ENOTSUP when no tensor
  * map can describe the slice: slices over 2 KiB that are not a multiple of
  * 2 KiB, or a miss of the library's tile-map cache under CUDA-graph capture);
@@ -562,15 +567,15 @@ DYNA_API int32_t dyna_kv_calib_get(dyna_kv_calib_entry* out, int32_t cap);
  * also covers every longer call), replacing the table's entries for that (row bytes, locality).
  * Candidates, in order (DYNA_CALIB_CANDIDATES): FUSED VEC 4 KiB x U8, FUSED VEC 8 KiB x U4,
  * FUSED VEC 16 KiB x U16, FUSED BULK ring 32 KiB x 4, STAGED VEC 8 KiB x U8, STAGED BULK
- * 32 KiB x 4 (STAGED is skipped — 0 GB/s — into an imported pool or a destination table without
- * device ids on another GPU).  out[i] receives the entry for chunk_tokens[i]; gbps (NULL or
+ * 32 KiB x 4, FUSED TILES (STAGED is skipped — 0 GB/s — into an imported pool or a destination
+ * table without device ids on another GPU; TILES when no tensor map fits the rows).  out[i] receives the entry for chunk_tokens[i]; gbps (NULL or
  * n x DYNA_CALIB_CANDIDATES floats) the payload GB/s of every candidate.  Tables: as
  * dyna_kv_migrate_ex (host ids or DYNA_MIGRATE_UNCHECKED semantics: the destination rows must
  * be distinct); both must cover at least the largest chunk size.  The call OVERWRITES the
  * destination rows its tables map, and synchronises `stream` (a startup-time call).  Errors:
  * DYNA_EINVAL (n <= 0, chunk sizes <= 0 or not ascending, reps < 1), DYNA_ERANGE (a chunk size
  * longer than the tables), or any error of the migrations it runs. */
-#define DYNA_CALIB_CANDIDATES 6
+#define DYNA_CALIB_CANDIDATES 7
 DYNA_API dyna_status dyna_kv_calibrate(dyna_block_table src, dyna_block_table dst, const int32_t* chunk_tokens,
                                        int32_t n, int32_t reps, struct CUstream_st* stream,
                                        dyna_kv_calib_entry* out, float* gbps);

@@ -27,7 +27,7 @@ STATUS_NAMES = {0: "DYNA_OK", -1: "DYNA_EINVAL", -2: "DYNA_EGEOM", -3: "DYNA_ERA
                 -10: "DYNA_ENOTSUP", -11: "DYNA_ECANCELED"}
 DYNA_MAX_INSTANCES, DYNA_MAX_CHUNKS = 64, 4096
 DYNA_VARIANT_AUTO, DYNA_VARIANT_FUSED, DYNA_VARIANT_STAGED = 0, 1, 2
-DYNA_ENGINE_AUTO, DYNA_ENGINE_VEC, DYNA_ENGINE_BULK, DYNA_ENGINE_BULK_WS = 0, 1, 2, 3
+DYNA_ENGINE_AUTO, DYNA_ENGINE_VEC, DYNA_ENGINE_BULK, DYNA_ENGINE_BULK_WS, DYNA_ENGINE_TILES = 0, 1, 2, 3, 4
 DYNA_MIGRATE_SIGNAL = 1
 DYNA_READY_PER_LAYER = 2
 DYNA_MIGRATE_UNCHECKED = 4
@@ -474,7 +474,7 @@ def dyna_kv_calib_get() -> list:
     return [tuple(getattr(arr[i], f) for f, _ in dyna_kv_calib_entry._fields_) for i in range(n)]
 
 
-DYNA_CALIB_CANDIDATES = 6
+DYNA_CALIB_CANDIDATES = 7
 
 
 def dyna_kv_calibrate(src: dyna_block_table, dst: dyna_block_table, chunk_tokens, reps: int = 8,

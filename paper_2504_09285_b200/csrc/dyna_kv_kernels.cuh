@@ -1252,19 +1252,22 @@ __device__ __forceinline__ void tma_store_4d(const char* tmap, const void* ssrc,
                : "memory");
 }
 
-// Item = (chunk k, slab group, run j), runs fastest.  Paged sides only (tile plans are never linear).
+// Item = (chunk k, slab group, run j, piece pp), pieces fastest; a piece is tile_rows rows of the run
+// (all of it unless a run's rows do not fit one box).  Paged sides only (tile plans are never linear).
 __device__ __forceinline__ TDesc decode_item_tile(const Plan& p, int64_t item, bool& skipped) {
   TDesc d{p.tmaps, nullptr, 0, 0, 0, 0u, 0u, 0};
   skipped = false;
   const int64_t k = item / p.items_per_chunk;
-  const int64_t i = item - k * p.items_per_chunk;
+  int64_t i = item - k * p.items_per_chunk;
+  const int32_t pp = (int32_t)(i % p.P);
+  i /= p.P;
   const int32_t j = (int32_t)(i % p.R);
   const int32_t lkg = (int32_t)(i / p.R);
   const int64_t a = p.t0 + k * p.c;
   const int64_t b = min(a + (int64_t)p.c, p.t1);
   const int64_t G = a / p.g + j;
-  const int64_t ta = max(a, G * p.g);
-  const int64_t tb = min(b, (G + 1) * p.g);
+  const int64_t ra = max(a, G * p.g) + (int64_t)pp * p.tile_rows;
+  const int64_t ta = ra, tb = min(min(b, (G + 1) * p.g), ra + p.tile_rows);
   d.k = p.k_direct ? (int32_t)k + p.k_base : (int32_t)((a - p.mig_t0) / p.sig_c);
   if (ta >= tb) return d;
   d.lk = lkg * p.lkb;
@@ -1349,7 +1352,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
   // ---------------- issuer (warp 0, lane 0); the box geometry is the launch's (every plan of a
   // multi-plan tile launch has the same g, row, lkb and slot: checked on the host)
   const int32_t slot = p.tile_bytes;
-  const uint32_t g = (uint32_t)p.g;
+  const uint32_t g = (uint32_t)p.tile_rows;  // rows of a full box
   const uint32_t row_box = (uint32_t)(p.row * p.lkb);  // bytes of one single-row box
   const uint32_t rstride = (uint32_t)p.tile_rstride;   // its smem stride (128-B aligned)
   // Maps were written by a host copy: acquire them for the tensormap proxy before first use.  Up to

@@ -481,17 +481,30 @@ bool tile_shape(Plan& p) {
   if (p.src.nb * (int64_t)p.src.bs >= (int64_t(1) << 31) || p.dst.nb * (int64_t)p.dst.bs >= (int64_t(1) << 31))
     return false;
   const int avail = smem_avail((const void*)k_copy_tiles<true, InterleavedSource, true>);
-  const int64_t run = g * slice;
+  // box rows: all g rows of a run when they fit the box target (or at least two ring slots), else the
+  // largest divisor of g that does (a run is then several items of `rows` rows each)
+  int64_t rows = 1;
+  for (int64_t d = 1; d <= g; ++d)
+    if (g % d == 0 && (d == 1 || d * slice <= std::max<int64_t>(tile_target_bytes(), g * slice)) &&
+        2 * (d * slice + 1024) <= avail)
+      rows = d;
+  if (rows < g && rows * slice * 2 < tile_target_bytes()) {  // g rows did not fit: aim at the box target
+    rows = 1;
+    for (int64_t d = 1; d <= g; ++d)
+      if (g % d == 0 && (d == 1 || d * slice <= tile_target_bytes())) rows = d;
+  }
+  const int64_t run = rows * slice;
   if (2 * (run + 1024) > avail) return false;
   const int64_t nlk = 2 * (int64_t)p.lm;
   int64_t lkb = 1;
   for (int64_t d = 1; d <= std::min<int64_t>(nlk, 256); ++d)
     if (nlk % d == 0 && (d == 1 || run * d <= tile_target_bytes()) && 2 * (run * d + 1024) <= avail) lkb = d;
   p.lkb = (int32_t)lkb;
+  p.tile_rows = (int32_t)rows;
   p.tile_rstride = (int32_t)((slice * lkb + 127) / 128 * 128);
-  p.tile_bytes = (int32_t)((std::max<int64_t>(run * lkb, (g - 1) * p.tile_rstride) + 1023) / 1024 * 1024);
-  p.P = 1;
-  p.items_per_chunk = (nlk / lkb) * p.R;
+  p.tile_bytes = (int32_t)((std::max<int64_t>(run * lkb, (rows - 1) * p.tile_rstride) + 1023) / 1024 * 1024);
+  p.P = (int32_t)(g / rows);  // pieces of a run
+  p.items_per_chunk = (nlk / lkb) * p.R * p.P;
   p.n_items = p.items_per_chunk * p.nchunks;
   return true;
 }
@@ -501,8 +514,8 @@ bool tile_shape(Plan& p) {
 bool tile_encode(const Plan& p, void* maps) {
   const int64_t slice = p.row, e0 = slice <= 2048 ? slice / 8 : 256;
   CUtensorMap* m = static_cast<CUtensorMap*>(maps);
-  return encode_side(&m[0], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, p.g, p.lkb) &&
-         encode_side(&m[1], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, p.g, p.lkb) &&
+  return encode_side(&m[0], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, p.tile_rows, p.lkb) &&
+         encode_side(&m[1], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, p.tile_rows, p.lkb) &&
          encode_side(&m[2], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, 1, p.lkb) &&
          encode_side(&m[3], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, 1, p.lkb);
 }

@@ -49,7 +49,7 @@ dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
   *o = dyna_kv_opts{};
   if (opts) *o = *opts;
   if ((o->flags & ~(DYNA_MIGRATE_SIGNAL | DYNA_READY_PER_LAYER | DYNA_MIGRATE_UNCHECKED)) != 0 || o->variant < 0 ||
-      o->variant > 2 || o->engine < 0 || o->engine > DYNA_ENGINE_BULK_WS || o->max_ctas < 0 || o->piece_bytes < 0 ||
+      o->variant > 2 || o->engine < 0 || o->engine > DYNA_ENGINE_TILES || o->max_ctas < 0 || o->piece_bytes < 0 ||
       o->piece_bytes % 16 || o->stages < 0 || o->stages == 1 || o->stages > kMaxStages ||
       (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16) || o->schedule < 0 ||
       o->schedule > DYNA_SCHED_DYNAMIC)
@@ -137,7 +137,12 @@ Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok, int64_
                                                      : (c.engine == DYNA_ENGINE_VEC ? kVecPiece : kBulkPiece));
   c.stages = o.stages ? o.stages : (use_ce && ce.stages ? ce.stages : kBulkStages);
   c.unroll = o.unroll ? o.unroll : (use_ce && ce.unroll ? ce.unroll : kVecU);
-  if (!o.engine && c.engine != DYNA_ENGINE_VEC && run_bytes < kMinBulkRun) {
+  if (c.engine == DYNA_ENGINE_TILES && c.variant == DYNA_VARIANT_STAGED) {  // tiles are a fused-variant engine
+    c.engine = DYNA_ENGINE_VEC;
+    c.unroll = kVecU;
+    if (!o.piece_bytes) c.piece = kVecPiece;
+  }
+  if (!o.engine && c.engine != DYNA_ENGINE_VEC && c.engine != DYNA_ENGINE_TILES && run_bytes < kMinBulkRun) {
     // a BULK item never spans two blocks; with short contiguous runs (e.g. one KV
     // head per TP rank: 256-B rows, 4-KiB blocks) its single issuing thread is
     // bound by items, not bytes (measured: 341 GB/s) — many warps do better
@@ -230,7 +235,7 @@ static bool stream_capturing(cudaStream_t st) {
 // AUTO keeps peer destinations (another GPU, or an imported pool) on VEC: tensor stores into peer
 // memory have not been measured on a multi-GPU box; explicit BULK allows them.
 static bool want_tiles(const dyna_kv_opts& o, bool peer) {
-  if (o.engine == DYNA_ENGINE_BULK || o.engine == DYNA_ENGINE_BULK_WS) return true;
+  if (o.engine == DYNA_ENGINE_BULK || o.engine == DYNA_ENGINE_BULK_WS || o.engine == DYNA_ENGINE_TILES) return true;
   return o.engine == DYNA_ENGINE_AUTO && tiles_enabled() && !peer;
 }
 
@@ -328,14 +333,29 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   alignas(64) char maps[kTileMaps * kTileMapBytes];
   Plan tp{};
   const char* cached = nullptr;
-  bool tiles = ch.variant == DYNA_VARIANT_FUSED && !board && !peer_dst && !o.engine &&
-               o.schedule != DYNA_SCHED_DYNAMIC && std::min<int64_t>(g, c) * row < kTileRunMax && tiles_enabled() &&
+  // tiles: asked for (DYNA_ENGINE_TILES), chosen by the calibration table, or AUTO's rule for short
+  // runs on one device
+  const bool tiles_asked = o.engine == DYNA_ENGINE_TILES;
+  const bool tiles_auto = !o.engine && (ch.engine == DYNA_ENGINE_TILES ||
+                                        (!peer_dst && std::min<int64_t>(g, c) * row < kTileRunMax && tiles_enabled()));
+  bool tiles = (tiles_asked || tiles_auto) && ch.variant == DYNA_VARIANT_FUSED && !board &&
+               o.schedule != DYNA_SCHED_DYNAMIC &&
                tile_shape(tp = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), row, row, 0, row, 0, tr.begin,
                                                 tr.end, l0, lm, c, g, ch.piece));
   if (tiles && (r = tile_maps(S, D, tp, stream, &cached, maps, &tiles))) return r;
+  if (tiles_asked && !tiles)
+    return fail(DYNA_ENOTSUP, "DYNA_ENGINE_TILES: %s", ch.variant != DYNA_VARIANT_FUSED ? "fused variant only"
+                                                       : board ? "not with a ready board"
+                                                               : "rows no tensor map can describe (or capturing "
+                                                                 "without cached maps)");
+  if (!tiles && ch.engine == DYNA_ENGINE_TILES) {  // calibrated tiles that do not apply here: VEC
+    ch.engine = DYNA_ENGINE_VEC;
+    ch.unroll = kVecU;
+    if (!o.piece_bytes) ch.piece = kVecPiece;
+  }
   const bool up_maps = tiles && !cached;
   if (tiles) {
-    ch.engine = DYNA_ENGINE_BULK;
+    ch.engine = DYNA_ENGINE_TILES;
     ch.piece = tp.tile_bytes;
     ch.stages = o.stages ? o.stages : 4;
   }
@@ -623,7 +643,7 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
   if ((r = new_xfer(S->dev, gs.instance, stream, &x))) return r;
   x->nchunks = (int32_t)nchunks;
   x->variant = DYNA_VARIANT_FUSED;
-  x->engine = tiles ? DYNA_ENGINE_BULK : DYNA_ENGINE_VEC;
+  x->engine = tiles ? DYNA_ENGINE_TILES : DYNA_ENGINE_VEC;
   x->piece = tiles ? p.tile_bytes : piece;
   x->unroll = tiles ? 0 : 8;
   x->stages = tiles ? (o.stages ? o.stages : 4) : 0;
@@ -933,7 +953,7 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   }
   InterleavedSource isrc{reinterpret_cast<const Plan*>(dbase + maps_b), n, plans[0].n_items * n};
   x->variant = DYNA_VARIANT_FUSED;
-  x->engine = tiles ? DYNA_ENGINE_BULK : DYNA_ENGINE_VEC;
+  x->engine = tiles ? DYNA_ENGINE_TILES : DYNA_ENGINE_VEC;
   x->piece = tiles ? plans[0].tile_bytes : piece;
   x->unroll = tiles ? 0 : 8;
   x->stages = tiles ? (o.stages ? o.stages : 4) : 0;
@@ -1066,7 +1086,10 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   std::vector<int32_t> map_of(m, 0);
   std::vector<size_t> pair_rep;               // a plan of each distinct (source, destination) pair
   std::vector<const char*> pair_cached;       // its channel-cached device maps (else uploaded)
-  bool tiles = !o.engine && !peer && run_min < kTileRunMax && o.schedule != DYNA_SCHED_DYNAMIC && tiles_enabled();
+  const bool tiles_asked = o.engine == DYNA_ENGINE_TILES;
+  bool tiles = (tiles_asked || (!o.engine && (ch.engine == DYNA_ENGINE_TILES ||
+                                              (!peer && run_min < kTileRunMax && tiles_enabled())))) &&
+               o.schedule != DYNA_SCHED_DYNAMIC;
   if (tiles) {
     std::map<std::pair<const dyna_kv_pool*, const dyna_kv_pool*>, int32_t> pair_idx;
     tplans.resize(m);
@@ -1080,6 +1103,7 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
       // slot from the launch's first plan): entries must agree on the run grid too
       tiles = tile_shape(tplans[k]) && tplans[k].tile_bytes == tplans[0].tile_bytes &&
               tplans[k].g == tplans[0].g && tplans[k].lkb == tplans[0].lkb &&
+              tplans[k].tile_rows == tplans[0].tile_rows &&
               tplans[k].tile_rstride == tplans[0].tile_rstride;
       auto it = pair_idx.find({S, D});
       if (it == pair_idx.end()) {
@@ -1102,10 +1126,20 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
       }
     }
   }
+  if (tiles_asked && !tiles) {
+    delete x;
+    return fail(DYNA_ENOTSUP, "DYNA_ENGINE_TILES: the batch's rows do not fit one tensor-map geometry (or capturing "
+                              "without cached maps)");
+  }
+  if (!tiles && ch.engine == DYNA_ENGINE_TILES) {  // calibrated tiles that do not apply to this batch: VEC
+    ch.engine = DYNA_ENGINE_VEC;
+    ch.unroll = o.unroll ? o.unroll : kVecU;
+    if (!o.piece_bytes) ch.piece = kVecPiece;
+  }
   const size_t npairs = tiles ? pair_rep.size() : 0;
   const size_t maps_b = npairs * kTileMaps * kTileMapBytes;  // multiple of 256
   if (tiles) {
-    ch.engine = DYNA_ENGINE_BULK;
+    ch.engine = DYNA_ENGINE_TILES;
     ch.piece = tplans[0].tile_bytes;
     ch.stages = o.stages ? o.stages : 4;
   }
@@ -1227,7 +1261,8 @@ dyna_status dyna_kv_calibrate(dyna_block_table src, dyna_block_table dst, const 
   static const Cand kCands[DYNA_CALIB_CANDIDATES] = {
       {DYNA_VARIANT_FUSED, DYNA_ENGINE_VEC, 4096, 0, 8},   {DYNA_VARIANT_FUSED, DYNA_ENGINE_VEC, 8192, 0, 4},
       {DYNA_VARIANT_FUSED, DYNA_ENGINE_VEC, 16384, 0, 16}, {DYNA_VARIANT_FUSED, DYNA_ENGINE_BULK, 32768, 4, 0},
-      {DYNA_VARIANT_STAGED, DYNA_ENGINE_VEC, 8192, 0, 8},  {DYNA_VARIANT_STAGED, DYNA_ENGINE_BULK, 32768, 4, 0}};
+      {DYNA_VARIANT_STAGED, DYNA_ENGINE_VEC, 8192, 0, 8},  {DYNA_VARIANT_STAGED, DYNA_ENGINE_BULK, 32768, 4, 0},
+      {DYNA_VARIANT_FUSED, DYNA_ENGINE_TILES, 0, 4, 0}};
   const int peer = (D->dev != S->dev || D->imported) ? 1 : 0;
   const bool staged_ok = !D->imported && (D->dev == S->dev || dst.block_ids);
   const int64_t L = S->desc.num_layers;
@@ -1253,6 +1288,7 @@ dyna_status dyna_kv_calibrate(dyna_block_table src, dyna_block_table dst, const 
       if (gbps) gbps[i * DYNA_CALIB_CANDIDATES + k] = 0.f;
       if (cd.variant == DYNA_VARIANT_STAGED && !staged_ok) continue;
       dyna_kv_opts o{cd.variant, cd.engine, 0, 0, cd.piece, cd.stages, cd.unroll, 0};
+      bool skip = false;
       for (int pass = 0; pass < 2 && !r; ++pass) {
         // pass 0, ungated, warms up whatever a first call allocates (staging, error words): an
         // allocation that synchronises the device must not meet a closed gate
@@ -1269,6 +1305,11 @@ dyna_status dyna_kv_calibrate(dyna_block_table src, dyna_block_table dst, const 
           r = dyna_kv_migrate_ex(src, dst, dyna_range{t0, t0 + c}, dyna_range{0, L}, (int32_t)c, stream_, &o, &x);
           if (!r) xs.push_back(x);
         }
+        if (r == DYNA_ENOTSUP && pass == 0 && cd.engine == DYNA_ENGINE_TILES) {  // no tensor map fits: skip
+          r = DYNA_OK;
+          skip = true;
+          break;
+        }
         if (pass == 1 && !r && cudaEventRecord(e1, stream) != cudaSuccess) r = fail(DYNA_ECUDA, "calibrate: event");
         if (pass == 1) __atomic_store_n(gate, open, __ATOMIC_RELEASE);  // open: the queued calls run back to back
         for (dyna_kv_xfer_t x : xs) {
@@ -1277,6 +1318,7 @@ dyna_status dyna_kv_calibrate(dyna_block_table src, dyna_block_table dst, const 
         }
       }
       if (r) break;
+      if (skip) continue;
       float ms = 0.f;
       CUDA_TRY(cudaEventSynchronize(e1));
       CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));

@@ -64,6 +64,7 @@ struct Plan {
   int32_t tile_bytes;       // shared-memory ring slot: a full-run box (g * row * lkb B), or the single-row
                             // boxes of a shorter run at tile_rstride apart, rounded up to 1 KiB
   int32_t tile_rstride;     // smem stride of single-row boxes: row * lkb rounded up to 128 B (TMA alignment)
+  int32_t tile_rows;        // rows of a full box: g, or a divisor of g when g rows do not fit (pieces of a run)
 };
 constexpr int kTileMapBytes = 128;  // sizeof(CUtensorMap)
 constexpr int kTileMaps = 4;        // per plan

@@ -354,7 +354,7 @@ dyna_status channel_tile_maps(dyna_kv_pool* S, const dyna_kv_pool* D, const Plan
   *out = nullptr;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   const bool capturing = cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
-  const TileKey key{D->uid, D->base, p.row, p.spitch, p.dpitch, p.scol, p.dcol, p.l0, p.lm, p.g, p.lkb};
+  const TileKey key{D->uid, D->base, p.row, p.spitch, p.dpitch, p.scol, p.dcol, p.l0, p.lm, p.tile_rows, p.lkb};
   constexpr size_t set_b = (size_t)kTileMaps * kTileMapBytes;
   std::lock_guard<std::mutex> lk(S->mu);
   Channel& ch = S->channels[D];
@@ -494,7 +494,7 @@ dyna_status dyna_kv_calib_set(const dyna_kv_calib_entry* entries, int32_t n) {
   for (int32_t i = 0; i < n; ++i) {
     const auto& e = entries[i];
     if (e.row_bytes < 0 || e.peer < 0 || e.peer > 1 || e.max_chunk_tokens <= 0 || e.variant < 0 || e.variant > 2 ||
-        e.engine < 0 || e.engine > 3 || e.piece_bytes < 0 || e.piece_bytes % 16 || e.stages < 0 || e.stages == 1 ||
+        e.engine < 0 || e.engine > DYNA_ENGINE_TILES || e.piece_bytes < 0 || e.piece_bytes % 16 || e.stages < 0 || e.stages == 1 ||
         e.stages > kMaxStages || (e.unroll != 0 && e.unroll != 4 && e.unroll != 8 && e.unroll != 16))
       return fail(DYNA_EINVAL, "calibration entry %d invalid", i);
   }

@@ -140,7 +140,7 @@ struct TileKey {
   uint64_t duid;
   const char* dbase;
   int64_t slice, spitch, dpitch;
-  int32_t scol, dcol, l0, lm, g, lkb;
+  int32_t scol, dcol, l0, lm, g, lkb;  // g: rows of a full box (tile_rows)
   bool operator==(const TileKey& o) const {
     return duid == o.duid && dbase == o.dbase && slice == o.slice && spitch == o.spitch && dpitch == o.dpitch &&
            scol == o.scol && dcol == o.dcol && l0 == o.l0 && lm == o.lm && g == o.g && lkb == o.lkb;

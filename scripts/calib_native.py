@@ -19,7 +19,7 @@ import kvgen  # noqa: E402
 import paper_2504_09285_b200 as dk  # noqa: E402
 
 NAMES = ["FUSED VEC 4K U8", "FUSED VEC 8K U4", "FUSED VEC 16K U16", "FUSED BULK ring 32K x4",
-         "STAGED VEC 8K U8", "STAGED BULK 32K x4"]
+         "STAGED VEC 8K U8", "STAGED BULK 32K x4", "FUSED TILES"]
 GEOMS = {"Llama-2-7B rows (8 KiB)": kvgen.LLAMA2_7B,
          "Llama-3-8B rows (2 KiB)": kvgen.LLAMA3_8B.with_(num_blocks=4096),
          "TP-8 shard rows (256 B)": kvgen.QWEN2_72B.with_(num_kv_heads=1, num_blocks=6144)}

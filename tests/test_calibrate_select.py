@@ -87,7 +87,7 @@ def test_native_calibrate_installs_measured_choice():
         entries, rates = dk.dyna_kv_calibrate(st, dt, [64, 512, 4096], reps=4)
         assert [e[:3] for e in entries] == [(2048, 0, 64), (2048, 0, 512), (2048, 0, 1 << 30)]
         cands = [(1, 1, 4096, 0, 8), (1, 1, 8192, 0, 4), (1, 1, 16384, 0, 16), (1, 2, 32768, 4, 0),
-                 (2, 1, 8192, 0, 8), (2, 2, 32768, 4, 0)]
+                 (2, 1, 8192, 0, 8), (2, 2, 32768, 4, 0), (1, 4, 0, 4, 0)]
         for e, r in zip(entries, rates):
             assert all(x > 0 for x in r), r
             assert e[3:] == cands[max(range(len(r)), key=lambda k: r[k])], (e, r)

@@ -429,7 +429,7 @@ def test_batch_small_rows_as_tiles(signal, host_tables):
             migs.append((T(src[i], ts), T(dst[i], td), (t0, t0 + n)))
             where.append(i)
     x = dk.migrate_batch(migs, (0, 6), 128, flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0)
-    assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_BULK
+    assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_TILES
     infos = [dk.dyna_kv_batch_info(x, k) for k in range(len(migs))] if signal else []
     dk.dyna_kv_wait(x)
     for i in range(2):

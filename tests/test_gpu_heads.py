@@ -35,7 +35,7 @@ def _heads_parity(gs, gd, n_tok, tr, lr, c, heads, hd0, seed=1, flags=0, piece=0
                                                                             engine=engine))
     info = dk.dyna_kv_xfer_info(x)
     if engine == dk.DYNA_ENGINE_AUTO and heads[1] - heads[0] not in (0, gs.num_kv_heads):
-        assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_BULK, "AUTO head slices should run as TMA tiles"
+        assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_TILES, "AUTO head slices should run as TMA tiles"
     dk.dyna_kv_wait(x)
     got = dst.tensor.cpu().numpy()
     assert np.array_equal(src.tensor.cpu().numpy(), hs), "source pool modified"
@@ -258,7 +258,7 @@ def test_reshard_one_launch_matches_oracle(tp_s, tp_d, signal, engine):
     x = dk.dyna_kv_reshard(migs, (0, s), (0, L), c, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL if signal else 0,
                                                                 engine=engine))
     if engine == dk.DYNA_ENGINE_AUTO and tp_s != tp_d:
-        assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_BULK
+        assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_TILES
     infos = [dk.dyna_kv_batch_info(x, i) for i in range(len(migs))] if signal else []
     dk.dyna_kv_wait(x)
     assert dk.dyna_kv_launch_count() - n0 == 1

@@ -410,7 +410,7 @@ def test_auto_small_rows_as_tiles(gs, gd, tr, lr, c, flags):
     plan = dk.dyna_kv_xfer_plan(x)
     info = dk.dyna_kv_xfer_info(x)
     dk.dyna_kv_wait(x)
-    assert plan["engine"] == dk.DYNA_ENGINE_BULK, plan
+    assert plan["engine"] == dk.DYNA_ENGINE_TILES, plan
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
     assert np.array_equal(src.tensor.cpu().numpy(), hs)
     if flags:
@@ -446,4 +446,34 @@ def test_tiles_under_graph_capture_need_cached_maps():
         graph.replay()
         torch.cuda.synchronize()
         assert torch_rows_equal(src, ts, dst, td, (0, 800), (0, 5))
-    assert engines == [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK]
+    assert engines == [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_TILES]
+
+
+# ------------------------------------------------ DYNA_ENGINE_TILES asked for explicitly (any row size)
+@pytest.mark.parametrize("gs,gd", [(LLAMA3_ROWS, LLAMA3_ROWS.with_(num_blocks=420)),
+                                   (LLAMA2_ROWS, LLAMA2_ROWS.with_(block_size=32, num_blocks=90)),
+                                   (kvgen.TOY, kvgen.TOY.with_(block_size=8, num_blocks=128)),
+                                   (TP8_ROWS, TP8_ROWS)],
+                         ids=["llama3-2KiB", "llama2-8KiB-reblock", "toy-reblock", "tp8-256B"])
+@pytest.mark.parametrize("c", [17, 256, 4096])
+@pytest.mark.parametrize("flags", [0, dk.DYNA_MIGRATE_SIGNAL], ids=["plain", "signal"])
+def test_explicit_tiles_engine(gs, gd, c, flags):
+    """Whole rows through the tile kernel on request, including 8-KiB rows (a 4-D box of 2-KiB
+    element rows x 4) and runs larger than AUTO would tile; bit-exact vs the oracle on the whole pool."""
+    n_tok = min(gs.num_blocks * gs.block_size, gd.num_blocks * gd.block_size, 5000)
+    tr = (3, n_tok - 5)
+    _parity(gs, gd, n_tok, tr, (0, gs.num_layers), c, engine=dk.DYNA_ENGINE_TILES, flags=flags)
+
+
+def test_explicit_tiles_engine_refusals():
+    g = kvgen.TOY
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(3, 256, g, g)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.migrate(st, dt, (0, 100), (0, 2), 32, engine=dk.DYNA_ENGINE_TILES, variant=dk.DYNA_VARIANT_STAGED)
+    assert e.value.status == dk.DYNA_ENOTSUP
+    x = dk.migrate(st, dt, (0, 100), (0, 2), 32, engine=dk.DYNA_ENGINE_TILES)
+    assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_TILES
+    dk.dyna_kv_wait(x)
+    assert torch_rows_equal(src, ts, dst, td, (0, 100), (0, 2))

@@ -100,7 +100,7 @@ def _heads_sender(handle: bytes, q, engine: int = 0):
         x = dk.dyna_kv_migrate_heads(dev_table(src, ts), dk.table(dst, torch.from_numpy(td).cuda(), td), (0, S),
                                      (0, 4), (4, 8), 0, CHUNK, 0, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL, engine=engine))
         info = dk.dyna_kv_xfer_info(x)
-        assert engine != dk.DYNA_ENGINE_BULK or dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_BULK
+        assert engine != dk.DYNA_ENGINE_BULK or dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_TILES
         dk.dyna_kv_wait(x)
         dst.close()
         q.put(("ok", info))
