@@ -146,7 +146,7 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
 #define DYNA_ENGINE_VEC  1     /* warp-per-segment 16-B vector loads/stores (LDG.128 / STG.128) */
 #define DYNA_ENGINE_BULK 2     /* TMA bulk copies through a shared-memory ring (UBLKCP): one issuing thread,
                                   fed item descriptors by a decoder warp */
-#define DYNA_ENGINE_BULK_WS 3  /* alias of DYNA_ENGINE_BULK (round-1 warp-specialised kernel with DYNA_KV_RING=0) */
+#define DYNA_ENGINE_BULK_WS 3  /* alias of DYNA_ENGINE_BULK (kept for callers of the round-1 warp-specialised kernel) */
 #define DYNA_ENGINE_TILES 4    /* TMA tensor tiles (UTMALDG / UTMASTG): a block's rows (or head slices) of several
                                   (layer, K|V) slabs per 4-D tensor load / store, one issuing thread fed by a decoder
                                   warp.  Fused variant only (the staged variant's K1 / K3 then use VEC); DYNA_ENOTSUP

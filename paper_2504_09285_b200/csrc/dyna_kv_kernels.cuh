@@ -621,316 +621,11 @@ struct Mailbox {
   }
 };
 
-// One thread per CTA drives a ring of `stages` smem slots of p.piece bytes:
-// loads land in slots ahead of the store front; each slot is reloaded once
-// the store issued from it has been read out of shared memory.
-template <bool SIGNAL, class Src, bool ACC = false>
-__global__ void __launch_bounds__(ACC ? 64 : 32) k_copy_bulk(const Src src, int stages,
-                                                             unsigned long long* sched_ctr) {
-  extern __shared__ __align__(128) unsigned char ring[];
-  __shared__ __align__(8) uint64_t full[kMaxStages];
-  __shared__ char* pend_dst[kMaxStages];
-  __shared__ uint32_t pend_n[kMaxStages];
-  __shared__ int32_t pend_k[kMaxStages];
-  __shared__ __align__(8) Mailbox mail[1];  // (used by ACC kernels only)
-  if (threadIdx.x != 0 && !(ACC && threadIdx.x == 32)) return;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
-    if (ACC) mail[0].init();
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (ACC) __syncthreads();
-  pdl_enter();
-  if (ACC && threadIdx.x == 32) {  // the accountant (ACC: the issuing thread never counts)
-    mail[0].serve(src.locate_signal());
-    return;
-  }
-  int64_t posted = 0;
-
-  // Static round-robin only: this single thread's loop is latency-critical and
-  // measured ~12% slower with the dynamic-scheduling path compiled in.
-  (void)sched_ctr;
-  int64_t next = blockIdx.x;
-  const int64_t stride = gridDim.x;
-  const int64_t n_items = src.total();
-  const Plan& p = src.locate_signal();  // used only for per-launch fields (piece, signalling)
-
-  // Load the next non-empty item of this CTA into slot s (pend_n[s] = 0 if none).
-  auto refill = [&](int s) {
-    while (next < n_items) {
-      int64_t item = next;
-      next += stride;
-      const Plan& ip = src.locate(item);
-      const Item it = decode_item(ip, item);
-      if (it.n == 0) {
-        if (SIGNAL && it.acc) account_chunk(p, it.k, it.acc);  // skipped (bad id): still closes the chunk
-        continue;
-      }
-      mbar_expect_tx(&full[s], it.n);
-      bulk_load(ring + (size_t)s * p.piece, it.src, it.n, &full[s]);
-      pend_dst[s] = it.dst;
-      pend_n[s] = it.n;
-      pend_k[s] = it.k;
-      return;
-    }
-    pend_n[s] = 0;
-  };
-
-  for (int s = 0; s < stages; ++s) refill(s);
-
-  // Signalling: stores are counted per chunk.  When the next store belongs to
-  // another chunk, the finished chunk's bytes are parked; they are counted
-  // once kDefer more stores have been committed after it, behind a
-  // `cp.async.bulk.wait_group kDefer` (all older groups complete) — by then
-  // they have normally landed, so the pipeline does not drain.
-  constexpr int kDefer = DYNA_BULK_DEFER;
-  int32_t cur_k = -1, park_k = -1;
-  uint32_t cur_acc = 0, park_acc = 0;
-  int since_park = 0;
-  auto flush_park = [&](bool all) {
-#ifndef DYNA_DIAG_NO_WAIT  // (DYNA_DIAG_*: unsafe diagnostic builds that drop one step each)
-    if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
-#endif
-#ifndef DYNA_DIAG_NO_PROXY
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-#endif
-#if defined(DYNA_DIAG_NO_COUNT)
-    (void)park_k;
-#else
-    if (ACC) {  // the accountant thread counts (and fences) on the issuer's behalf
-      mail[0].post(posted, park_k, park_acc);
-    } else {
-#if defined(DYNA_BULK_FENCED_COUNT)
-      fence_for(p);
-      account_chunk(p, park_k, park_acc);
-#else
-      account_chunk_release(p, park_k, park_acc);
-#endif
-    }
-#endif
-    park_k = -1;
-    park_acc = 0;
-  };
-  // A slot is refilled `lag` stores after its own store was issued, so up to
-  // lag+1 stores drain while stages-lag-1 loads are in flight.
-  const int lag = stages >= 4 ? 2 : 1;
-  for (int64_t iter = 0;; ++iter) {
-    const int s = (int)(iter % stages);
-    if (pend_n[s] == 0) break;
-    if (SIGNAL && pend_k[s] != cur_k) {
-      if (park_acc) flush_park(true);  // chunks shorter than kDefer stores per CTA
-      park_k = cur_k;
-      park_acc = cur_acc;
-      since_park = 0;
-      cur_k = pend_k[s];
-      cur_acc = 0;
-    }
-    mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
-    bulk_store(pend_dst[s], ring + (size_t)s * p.piece, pend_n[s]);
-    bulk_commit();
-    if (SIGNAL) {
-      cur_acc += pend_n[s];
-      if (park_acc && ++since_park == kDefer) flush_park(false);
-    }
-    if (iter >= lag) {
-      if (lag == 2) bulk_wait_read<2>(); else bulk_wait_read<1>();  // store iter-lag done reading smem
-      refill((int)((iter - lag) % stages));
-    }
-  }
-  bulk_wait_all<0>();
-  if (SIGNAL) {
-    if (park_acc) flush_park(true);
-    if (cur_acc) {
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      if (ACC) {
-        mail[0].post(posted, cur_k, cur_acc);
-      } else {
-        fence_for(p);
-        account_chunk(p, cur_k, cur_acc);
-      }
-    }
-  }
-  if (ACC) mail[0].post(posted, -1, 0);  // the accountant may leave
-  (void)posted;
-}
-
-// ------------------------------------------------------------------ BULK engine, warp-specialised
-// Warp 0 (one elected lane) decodes items and issues TMA bulk loads into a
-// ring of `stages` smem slots; warp 1 (one lane) drains each landed slot with
-// a TMA bulk store and hands the slot back.  full[s] completes when a load's
-// bytes land (complete_tx); empty[s] when the store has read the slot out.
-// The loader's decode latency no longer sits between consecutive stores.
-
-// ACC (signalling only): a third warp (one lane) does the chunk accounting.  The storer
-// hands each finished chunk's byte count over a small shared-memory mailbox (mbarrier
-// arrive = release at CTA scope, after its bulk groups completed and a proxy fence); the
-// accountant's GPU-scope fence + count then covers the storer's writes (causality through
-// the CTA-scope hand-off) without stalling the storer's pipeline.
-template <bool SIGNAL, class Src, bool ACC = false>
-__global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_bulk_ws(const Src src, int stages,
-                                                                unsigned long long* sched_ctr) {
-  extern __shared__ __align__(128) unsigned char ring[];
-  __shared__ __align__(8) uint64_t full[kMaxStages];
-  __shared__ __align__(8) uint64_t empty[kMaxStages];
-  __shared__ char* pend_dst[kMaxStages];
-  __shared__ uint32_t pend_n[kMaxStages];
-  __shared__ int32_t pend_k[kMaxStages];
-  __shared__ __align__(8) uint64_t mail_full[ACC ? kMail : 1];
-  __shared__ __align__(8) uint64_t mail_empty[ACC ? kMail : 1];
-  __shared__ int32_t mail_k[ACC ? kMail : 1];
-  __shared__ uint32_t mail_acc[ACC ? kMail : 1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    if (ACC)
-      for (int m = 0; m < kMail; ++m) {
-        mbar_init(&mail_full[m], 1);
-        mbar_init(&mail_empty[m], 1);
-      }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-  pdl_enter();
-  if (warp >= 1 && lane != 0) return;  // storer and accountant are one thread each; the loader a warp
-  const Plan& p = src.locate_signal();
-  const int64_t n_items = src.total();
-  if (ACC && warp == 2) {  // ---------------- accountant
-    for (int64_t i = 0;; ++i) {
-      const int m = (int)(i % kMail);
-      mbar_wait(&mail_full[m], (uint32_t)((i / kMail) & 1));
-      const int32_t k = mail_k[m];
-      const uint32_t acc = mail_acc[m];
-      mbar_arrive(&mail_empty[m]);
-      if (k < 0) break;
-      fence_for(p);
-      account_chunk(p, k, acc);
-    }
-    return;
-  }
-  int64_t posted = 0;
-  auto post = [&](int32_t k, uint32_t acc) {  // storer -> accountant
-    const int m = (int)(posted % kMail);
-    if (posted >= kMail) mbar_wait(&mail_empty[m], (uint32_t)(((posted / kMail) - 1) & 1));
-    mail_k[m] = k;
-    mail_acc[m] = acc;
-    mbar_arrive(&mail_full[m]);
-    ++posted;
-  };
-
-  if (warp == 0) {  // ---------------- loader: 32 lanes decode, lane 0 issues
-    (void)sched_ctr;  // static round-robin over CTAs: item(m) = blockIdx.x + m * gridDim.x
-    int64_t m = 0;
-    Item mine{nullptr, nullptr, 0u, 0u, 0};
-    uint32_t todo = 0;      // lanes whose decoded item still has to be issued
-    bool drained = false;
-    for (int64_t iter = 0;; ++iter) {
-      const int s = (int)(iter % stages);
-      while (todo == 0 && !drained) {  // decode the CTA's next 32 items, one per lane
-        const int64_t gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
-        m += 32;
-        mine = Item{nullptr, nullptr, 0u, 0u, 0};
-        if (gi < n_items) {
-          int64_t item = gi;
-          const Plan& ip = src.locate(item);
-          mine = decode_item(ip, item);
-          if (SIGNAL && mine.n == 0 && mine.acc) account_chunk(p, mine.k, mine.acc);  // skipped (bad id)
-        }
-        todo = __ballot_sync(0xffffffffu, mine.n != 0);
-        drained = __ballot_sync(0xffffffffu, gi >= n_items) != 0;
-      }
-      const bool have = todo != 0;  // warp-uniform
-      const int from = have ? __ffs(todo) - 1 : 0;
-      if (have) todo &= todo - 1;
-      const uint64_t isrc = __shfl_sync(0xffffffffu, (unsigned long long)mine.src, from);
-      const uint64_t idst = __shfl_sync(0xffffffffu, (unsigned long long)mine.dst, from);
-      const uint32_t in = __shfl_sync(0xffffffffu, mine.n, from);
-      const int32_t ik = __shfl_sync(0xffffffffu, mine.k, from);
-      const uint32_t n = have ? in : 0u;  // 0: no work left
-      if (lane == 0) {
-        if (iter >= stages) mbar_wait(&empty[s], (uint32_t)(((iter / stages) - 1) & 1));
-        pend_dst[s] = reinterpret_cast<char*>(idst);
-        pend_n[s] = n;
-        pend_k[s] = ik;
-        if (n == 0) {
-          mbar_arrive(&full[s]);  // no more work: a plain arrive tells the storer
-        } else {
-          mbar_expect_tx(&full[s], n);
-          bulk_load(ring + (size_t)s * p.piece, reinterpret_cast<const char*>(isrc), n, &full[s]);
-        }
-      }
-      __syncwarp();
-      if (n == 0) break;
-    }
-  } else {  // ---------------- storer
-    constexpr int kDefer = 4;
-    int32_t cur_k = -1, park_k = -1;
-    uint32_t cur_acc = 0, park_acc = 0;
-    int since_park = 0;
-    auto flush_park = [&](bool all) {
-      if (all) bulk_wait_all<0>(); else bulk_wait_all<kDefer>();
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      if (ACC) {
-        post(park_k, park_acc);
-      } else {
-        fence_for(p);
-        account_chunk(p, park_k, park_acc);
-      }
-      park_k = -1;
-      park_acc = 0;
-    };
-    // a slot goes back to the loader `lag` stores after its own store was issued, so up
-    // to lag+1 stores drain at once (measured on the single-thread engine: lag 2 >> lag 1)
-    const int lag = stages >= 4 ? 2 : 1;
-    for (int64_t iter = 0;; ++iter) {
-      const int s = (int)(iter % stages);
-      mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
-      const uint32_t n = pend_n[s];
-      if (n == 0) break;
-      if (SIGNAL && pend_k[s] != cur_k) {
-        if (park_acc) flush_park(true);
-        park_k = cur_k;
-        park_acc = cur_acc;
-        since_park = 0;
-        cur_k = pend_k[s];
-        cur_acc = 0;
-      }
-      bulk_store(pend_dst[s], ring + (size_t)s * p.piece, n);
-      bulk_commit();
-      if (SIGNAL) {
-        cur_acc += n;
-        if (park_acc && ++since_park == kDefer) flush_park(false);
-      }
-      if (iter >= lag) {  // store iter-lag has read its slot out: hand it back
-        if (lag == 2) bulk_wait_read<2>(); else bulk_wait_read<1>();
-        mbar_arrive(&empty[(int)((iter - lag) % stages)]);
-      }
-    }
-    bulk_wait_all<0>();
-    if (SIGNAL) {
-      if (park_acc) flush_park(true);
-      if (cur_acc) {
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        if (ACC) {
-          post(cur_k, cur_acc);
-        } else {
-          fence_for(p);
-          account_chunk(p, cur_k, cur_acc);
-        }
-      }
-    }
-    if (ACC) post(-1, 0);  // the accountant may leave
-  }
-}
-
 // ------------------------------------------------------------------ BULK engine, decoder-fed ring
-// One thread (warp 0, lane 0) drives the TMA ring exactly as k_copy_bulk does, but it never
-// decodes: warp 1 decodes the CTA's items 32 at a time (one per lane: the divisions and the
+// One thread (warp 0, lane 0) drives a ring of `stages` shared-memory slots of p.piece bytes:
+// loads (cp.async.bulk, completing on the slot's mbarrier) land ahead of the store front, and a
+// slot is reloaded once the bulk store issued from it has read it out.  It never decodes
+// (round 1's kernels did, on the same thread): warp 1 decodes the CTA's items 32 at a time (one per lane: the divisions and the
 // two block-table loads of decode_item, and the batch's plan lookup) into a shared-memory
 // queue of descriptors, NQ batches ahead.  The issuer's loop is then: wait for a landed
 // slot, issue its store, wait for an older store to have read its slot, read the next
@@ -1295,7 +990,6 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
   __shared__ TDesc pend[kMaxStages];
   __shared__ __align__(8) Mailbox mail[1];  // (ACC only)
   constexpr bool kMulti = !std::is_same<Src, SingleSource>::value;
-  constexpr bool kRR = std::is_same<Src, RoundRobinSource>::value;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
@@ -1313,15 +1007,10 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
   const int64_t n_items = src.total();
   if (warp == 1) {  // ---------------- decoder
     int64_t m = 0;
-    int64_t rr_n = 1;
-    if constexpr (kRR) rr_n = src.n;
     for (int64_t b = 0;; ++b) {
       const int qb = (int)(b % kQ);
       if (b >= kQ) mbar_wait(&qempty[qb], (uint32_t)(((b / kQ) - 1) & 1));
-      // RoundRobinSource: the CTA's j-th item is entry j % n of its (j / n)-th local item, so the
-      // issuer moves the same rows of every entry back to back (a TP gather writes whole rows)
-      const int64_t gi = kRR ? (blockIdx.x + ((m + lane) / rr_n) * (int64_t)gridDim.x) * rr_n + (m + lane) % rr_n
-                             : blockIdx.x + (m + lane) * (int64_t)gridDim.x;
+      const int64_t gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
       m += 32;
       TDesc d{nullptr, nullptr, 0, 0, 0, 0u, 0u, 0};
       if (gi < n_items) {
@@ -1334,8 +1023,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
       }
       const unsigned mask = __ballot_sync(0xffffffffu, d.rows != 0);
       if (d.rows) q[qb][__popc(mask & ((1u << lane) - 1u))] = d;
-      const bool last = kRR ? (blockIdx.x + (m / rr_n) * (int64_t)gridDim.x) * rr_n >= n_items
-                            : blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
+      const bool last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
       if (lane == 0) {
         qcount[qb] = __popc(mask);
         qlast[qb] = last ? 1 : 0;

@@ -34,11 +34,6 @@ void preload_kernels() {
       (const void*)k_copy_vec<4, true, BatchSource, false>, (const void*)k_copy_vec<8, true, BatchSource, false>,
       (const void*)k_copy_vec<16, true, BatchSource, false>,
       (const void*)k_copy_vec<16, false, BatchSource, false>,
-      (const void*)k_copy_bulk<false, SingleSource>, (const void*)k_copy_bulk<true, SingleSource>,
-      (const void*)k_copy_bulk<false, BatchSource>,
-      (const void*)k_copy_bulk_ws<false, SingleSource>, (const void*)k_copy_bulk_ws<true, SingleSource>,
-      (const void*)k_copy_bulk_ws<false, BatchSource>, (const void*)k_copy_bulk_ws<true, SingleSource, true>,
-      (const void*)k_copy_bulk<true, SingleSource, true>,
       (const void*)k_copy_rows<8, false, SingleSource>, (const void*)k_copy_rows<8, true, SingleSource>,
       (const void*)k_copy_rows<8, false, InterleavedSource>, (const void*)k_copy_rows<8, true, InterleavedSource>,
       (const void*)k_copy_rows<8, false, BatchSource>, (const void*)k_copy_rows<8, true, BatchSource>,
@@ -53,7 +48,6 @@ void preload_kernels() {
       (const void*)k_copy_lanes<16, false, BatchSource>, (const void*)k_copy_lanes<16, true, BatchSource>,
       (const void*)k_copy_tiles<false, SingleSource>, (const void*)k_copy_tiles<true, SingleSource, true>,
       (const void*)k_copy_tiles<false, InterleavedSource>, (const void*)k_copy_tiles<true, InterleavedSource, true>,
-      (const void*)k_copy_tiles<false, RoundRobinSource>, (const void*)k_copy_tiles<true, RoundRobinSource, true>,
       (const void*)k_copy_tiles<false, BatchSource>, (const void*)k_copy_tiles<true, BatchSource, true>,
   };
   for (const void* k : ks) cudaFuncGetAttributes(&a, k);
@@ -64,16 +58,11 @@ void preload_kernels() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const void* bulk[] = {
-      (const void*)k_copy_bulk<false, SingleSource>, (const void*)k_copy_bulk<true, SingleSource>,
-      (const void*)k_copy_bulk<false, BatchSource>,  (const void*)k_copy_bulk_ws<false, SingleSource>,
-      (const void*)k_copy_bulk_ws<true, SingleSource>, (const void*)k_copy_bulk_ws<false, BatchSource>,
-      (const void*)k_copy_bulk_ws<true, SingleSource, true>, (const void*)k_copy_bulk<true, SingleSource, true>,
       (const void*)k_copy_ring<false, SingleSource>, (const void*)k_copy_ring<true, SingleSource>,
       (const void*)k_copy_ring<true, SingleSource, true>, (const void*)k_copy_ring<false, BatchSource>,
       (const void*)k_copy_ring<true, BatchSource>, (const void*)k_copy_ring<true, BatchSource, true>,
       (const void*)k_copy_tiles<false, SingleSource>, (const void*)k_copy_tiles<true, SingleSource, true>,
       (const void*)k_copy_tiles<false, InterleavedSource>, (const void*)k_copy_tiles<true, InterleavedSource, true>,
-      (const void*)k_copy_tiles<false, RoundRobinSource>, (const void*)k_copy_tiles<true, RoundRobinSource, true>,
       (const void*)k_copy_tiles<false, BatchSource>, (const void*)k_copy_tiles<true, BatchSource, true>,
   };
   for (const void* k : bulk) {
@@ -261,57 +250,36 @@ int smem_avail(const void* kern) {
   return v;
 }
 
-// Ring kernel of the BULK engines.  DYNA_KV_RING=0 restores the round-1 kernels (decode on
-// the issuing thread: k_copy_bulk; warp-specialised loader/storer: k_copy_bulk_ws).
-bool ring_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("DYNA_KV_RING");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
+// The BULK engine: the decoder-fed TMA ring (k_copy_ring).  With per-chunk signalling a third
+// warp is the accountant (the issuer posts finished chunks to it instead of fencing itself;
+// measured); DYNA_KV_ACCOUNTANT=0 makes the issuer count with a release RMW.
 template <bool SIG, class Src>
 dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, int64_t max_grid, int sms,
-                        cudaStream_t st, unsigned long long* sched, bool ws) {
-  // Signalling through an accountant thread (measured): on for BULK_WS (its
-  // storer no longer stalls on the GPU-scope release), off for BULK (slower with it).
-  // DYNA_KV_ACCOUNTANT=0: never; =all: BULK too.
-  static const int acc_mode = [] {
+                        cudaStream_t st) {
+  static const bool acc_on = [] {
     const char* e = std::getenv("DYNA_KV_ACCOUNTANT");
-    if (!e) return 1;
-    return e[0] == '0' ? 0 : (std::strcmp(e, "all") == 0 ? 2 : 1);
+    return !(e && e[0] == '0');
   }();
   static const int lag_env = [] {  // experiment switch: slots refilled `lag` stores late (0 = by depth)
     const char* e = std::getenv("DYNA_KV_LAG");
     return e ? std::atoi(e) : 0;
   }();
-  const bool single = std::is_same<Src, SingleSource>::value;
-  const bool ring = ring_enabled();
-  const bool acc = SIG && (ring ? acc_mode >= 1 : single && (ws ? acc_mode >= 1 : acc_mode == 2));
-  void (*kbulk)(const Src, int, unsigned long long*) =
-      ws ? (acc ? k_copy_bulk_ws<SIG, Src, true> : k_copy_bulk_ws<SIG, Src>)
-         : (acc ? k_copy_bulk<SIG, Src, true> : k_copy_bulk<SIG, Src>);
+  const bool acc = SIG && acc_on;
   void (*kring)(const Src, int, int) = acc ? k_copy_ring<SIG, Src, true> : k_copy_ring<SIG, Src>;
-  const void* kern = ring ? (const void*)kring : (const void*)kbulk;
-  const int threads = ring ? (acc ? 96 : 64) : ws ? (acc ? 96 : 64) : (acc ? 64 : 32);
+  const int threads = acc ? 96 : 64;
   // a ring deeper than the shared memory holds is cut to the stages that fit (at least 2)
-  const int avail = smem_avail(kern);
+  const int avail = smem_avail((const void*)kring);
   if ((int64_t)stages * piece > avail) stages = avail / piece;
   if (stages < 2) return fail(DYNA_EINVAL, "BULK: two %d-B pieces do not fit in shared memory", piece);
   const size_t smem = (size_t)stages * piece;
   int occ = 0;  // (the dynamic shared memory limit was raised once in preload_kernels)
-  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kring, threads, smem));
   if (occ <= 0) return fail(DYNA_EINVAL, "BULK: %zu B of shared memory per CTA does not fit", smem);
   int64_t cap = (int64_t)sms * occ;
   if (max_grid > 0) cap = std::min<int64_t>(cap, max_grid);
   const unsigned grid = (unsigned)balanced_workers(n_items, cap);
-  if (ring) {
-    const int lag = lag_env > 0 ? std::min(lag_env, std::max(1, stages - 2)) : (stages >= 4 ? 2 : 1);
-    CUDA_TRY(launch_kernel(kring, grid, threads, smem, st, src, stages, lag));
-  } else {
-    CUDA_TRY(launch_kernel(kbulk, grid, threads, smem, st, src, stages, sched));
-  }
+  const int lag = lag_env > 0 ? std::min(lag_env, std::max(1, stages - 2)) : (stages >= 4 ? 2 : 1);
+  CUDA_TRY(launch_kernel(kring, grid, threads, smem, st, src, stages, lag));
   return DYNA_OK;
 }
 
@@ -327,9 +295,8 @@ dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int
   DevInfo* di = dev_info(dev);
   unsigned long long* sc = sched_slot(di, schedule);
   if (engine == DYNA_ENGINE_BULK || engine == DYNA_ENGINE_BULK_WS) {
-    const bool ws = engine == DYNA_ENGINE_BULK_WS;
-    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st, sc, ws)
-                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st, sc, ws);
+    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st)
+                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st);
     if (r) return r;
   } else if (unroll == 4) {
     sig ? launch_vec<4, true>(src, n_items, max_ctas, di->sms, st, sc)
@@ -401,9 +368,6 @@ dyna_status launch_rows_interleaved(const InterleavedSource& src, bool sig, int 
   return launch_rows_src(src, src.total_items, sig, max_ctas, dev, st);
 }
 
-dyna_status launch_rows_batch(const BatchSource& src, bool sig, int max_ctas, int dev, cudaStream_t st) {
-  return launch_rows_src(src, src.total_items, sig, max_ctas, dev, st);
-}
 
 // ------------------------------------------------------------------ head slices as TMA tensor tiles
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda).
@@ -431,14 +395,6 @@ static int tile_l2_promotion() {  // experiment switch DYNA_KV_TILE_L2 (0 none, 
   static const int v = [] {
     const char* e = std::getenv("DYNA_KV_TILE_L2");
     return e ? std::atoi(e) : 2;
-  }();
-  return v;
-}
-
-static bool tile_rr() {  // experiment switch DYNA_KV_TILE_RR=1: reshard entries dealt round-robin
-  static const bool v = [] {
-    const char* e = std::getenv("DYNA_KV_TILE_RR");
-    return e && e[0] == '1';
   }();
   return v;
 }
@@ -539,10 +495,7 @@ dyna_status launch_tiles_t(const Src& src, int64_t n_items, int tile_bytes, int 
   if (occ <= 0) return fail(DYNA_EINVAL, "tiles: %zu B of shared memory per CTA does not fit", smem);
   int64_t cap = (int64_t)di->sms * occ;
   if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
-  // round-robin sources: CTAs take local items (all n entries of one each)
-  int64_t units = n_items;
-  if constexpr (std::is_same<Src, RoundRobinSource>::value) units = n_items / src.n;
-  const unsigned grid = (unsigned)balanced_workers(units, cap);
+  const unsigned grid = (unsigned)balanced_workers(n_items, cap);
   const int lag = stages >= 4 ? 2 : 1;
   CUDA_TRY(launch_kernel(kern, grid, threads, smem, st, src, stages, lag));
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -569,20 +522,7 @@ dyna_status launch_tiles_batch(const BatchSource& src, bool sig, int tile_bytes,
 
 dyna_status launch_tiles_interleaved(const InterleavedSource& src, bool sig, int tile_bytes, int stages, int max_ctas,
                                      int dev, cudaStream_t st) {
-  if (tile_rr())
-    return launch_tiles_src(RoundRobinSource{src.plans, src.n, src.total_items}, src.total_items, sig, tile_bytes,
-                            stages, max_ctas, dev, st);
   return launch_tiles_src(src, src.total_items, sig, tile_bytes, stages, max_ctas, dev, st);
-}
-
-// The VEC engine on whole rows through the decoder-fed row kernel (a row is a slice of itself):
-// DYNA_KV_FED_VEC=1 (experiment switch).
-bool fed_vec_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("DYNA_KV_FED_VEC");
-    return e && e[0] == '1';
-  }();
-  return on;
 }
 
 dyna_status launch_copy(const Plan& p, int engine, int max_ctas, int stages, int unroll, int dev,

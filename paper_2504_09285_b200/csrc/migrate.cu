@@ -304,22 +304,6 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int64_t c = chunk_tokens;
   const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
   Choice ch = choose(o, row, peer_dst, ntok, std::min<int64_t>(gcd64(gs.block_size, gd.block_size), c) * row);
-  if (signal && !o.engine && ch.engine != DYNA_ENGINE_VEC && nchunks > 1 && !ring_enabled()) {
-    // round-1 kernels (DYNA_KV_RING=0), measured: BULK's release-add at every chunk switch stalls
-    // its single issuing thread; BULK_WS with an accountant thread beats VEC and BULK
-    // (profiles/r01_ab_signal_ws.log).  The ring kernel counts through an accountant itself.
-    static const bool ws = [] {  // DYNA_KV_SIGNAL_WS=0: VEC instead of BULK_WS
-      const char* e = std::getenv("DYNA_KV_SIGNAL_WS");
-      return !(e && e[0] == '0');
-    }();
-    if (ws && ch.engine == DYNA_ENGINE_BULK) {
-      ch.engine = DYNA_ENGINE_BULK_WS;
-    } else {
-      ch.engine = DYNA_ENGINE_VEC;
-      ch.unroll = kVecU;
-      if (!o.piece_bytes) ch.piece = kVecPiece;
-    }
-  }
   if (board) {  // producer-coupled: the VEC engine (each warp waits on its own chunk's mark)
     ch.variant = DYNA_VARIANT_FUSED;
     ch.engine = DYNA_ENGINE_VEC;
@@ -382,12 +366,7 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const uint64_t launches0 = g_launches.load();
   if (variant == DYNA_VARIANT_FUSED) {
     // K4 / K4-local: source rows -> destination rows, one launch for all chunks.
-    const bool fed = !tiles && engine == DYNA_ENGINE_VEC && !board && o.schedule != DYNA_SCHED_DYNAMIC &&
-                     fed_vec_enabled();
-    Plan p = tiles ? tp
-             : fed ? make_plan_sliced(paged(S, sids), paged(D, dids), row, row, 0, row, 0, tr.begin, tr.end, l0, lm,
-                                      c, g, piece)
-                   : make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
+    Plan p = tiles ? tp : make_plan(paged(S, sids), paged(D, dids), row, tr.begin, tr.end, l0, lm, c, g, piece);
     if (tiles) {
       p.src.table = sids;
       p.dst.table = dids;
@@ -426,7 +405,6 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
       r = launch_ready(p, o.max_ctas, S->dev, stream, o.schedule);
     } else {
       r = tiles ? launch_tiles(p, stages, o.max_ctas, S->dev, stream)
-          : fed ? launch_rows(p, o.max_ctas, S->dev, stream)
                 : launch_copy(p, engine, o.max_ctas, stages, unroll, S->dev, stream, o.schedule);
     }
   } else {
@@ -987,8 +965,6 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
   const bool unchecked = (o.flags & DYNA_MIGRATE_UNCHECKED) != 0;
-  if (signal && o.engine && o.engine != DYNA_ENGINE_VEC && !ring_enabled())
-    return fail(DYNA_ENOTSUP, "batch with per-chunk flags: VEC engine only (DYNA_KV_RING=0)");
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   // Reading R7 across entries: one entry's source rows may be another entry's destination rows.
   std::vector<uint64_t> dst_uids;
@@ -1037,21 +1013,10 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
                                                                   migs[i].dst.pool->desc.block_size),
                                                             chunk_tokens) * S0->row);
   Choice ch = choose(o, S0->row, peer, total_tok, run_min);
-  if (!ring_enabled() && (signal || (!o.engine && ch.engine != DYNA_ENGINE_VEC))) {
-    // Round-1 BULK kernels (DYNA_KV_RING=0) count chunks for one plan only and decode (and look
-    // plans up) on the issuing thread, latency-bound with many plans (scripts/batch_probe.py):
-    // VEC.  The ring kernel counts per (plan, chunk) and its decoder warp does the lookups
-    // (configs[2] batch: 3263 vs VEC 2966 GB/s,
-    // profiles/r02_engine_ab_ring.json).
-    ch.engine = DYNA_ENGINE_VEC;
-    ch.unroll = o.unroll ? o.unroll : kVecU;
-    if (!o.piece_bytes) ch.piece = kVecPiece;
-  }
   DeviceGuard guard(S0->dev);
   dyna_kv_xfer* x = nullptr;
   if ((r = new_xfer(S0->dev, S0->desc.instance, stream, &x))) return r;
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
-  const bool fed = ch.engine == DYNA_ENGINE_VEC && o.schedule != DYNA_SCHED_DYNAMIC && fed_vec_enabled();
   if (signal) {  // each entry: its own epoch and slot range of its (sender, destination pool)
     // the entries of one launch must not share slots (their counters live there): at most
     // DYNA_MAX_CHUNKS signalled chunks per (sender, destination pool) in one batch
@@ -1181,10 +1146,8 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
       plans[k].tmaps = pair_cached[map_of[k]] ? pair_cached[map_of[k]]
                                               : dbase + (size_t)map_of[k] * kTileMaps * kTileMapBytes;
     } else {
-      plans[k] = fed ? make_plan_sliced(paged(S, sids), paged(D, dids), S->row, S->row, 0, D->row, 0,
-                                        mg.token_range.begin, mg.token_range.end, l0, lm, chunk_tokens, g, ch.piece)
-                     : make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end,
-                                 l0, lm, chunk_tokens, g, ch.piece);
+      plans[k] = make_plan(paged(S, sids), paged(D, dids), S->row, mg.token_range.begin, mg.token_range.end, l0, lm,
+                           chunk_tokens, g, ch.piece);
     }
     plans[k].err = x->err;
     if (signal) {  // entry k's chunk j: counter / inbox slot first_slot + j of its (sender, destination)
@@ -1228,7 +1191,6 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
   x->launches = 1;
   r = tiles ? launch_tiles_batch(bsrc, signal, ch.piece, ch.stages, o.max_ctas, S0->dev, stream)
-      : fed ? launch_rows_batch(bsrc, signal, o.max_ctas, S0->dev, stream)
             : launch_batch(bsrc, total_items, signal, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll,
                            S0->dev, stream, o.schedule);
   if (!r) r = lease.finish(stream);

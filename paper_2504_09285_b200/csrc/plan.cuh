@@ -123,20 +123,4 @@ struct InterleavedSource {
   __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }
 };
 
-// The same n plans, items grouped by local item: global item g is item g / n of plan g % n, and
-// the tile kernel hands a CTA all n entries of one local item back to back, so the same token rows
-// of every entry are read (a TP scatter) or written (a TP gather) together.  Tile kernel only.
-struct RoundRobinSource {
-  const Plan* plans;
-  int32_t n;
-  int64_t total_items;
-  __device__ __forceinline__ int64_t total() const { return total_items; }
-  __device__ __forceinline__ const Plan& locate(int64_t& item) const {
-    const int32_t r = (int32_t)(item % n);
-    item /= n;
-    return plans[r];
-  }
-  __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }
-};
-
 }  // namespace dynakv

@@ -387,7 +387,6 @@ dyna_status channel_staging_done(dyna_kv_pool* src, const dyna_kv_pool* dst, cud
 
 // launch.cu — the only translation unit that instantiates and launches kernels
 void preload_kernels();
-bool ring_enabled();
 Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1, int l0, int lm, int64_t c,
                int64_t g, int piece);
 void set_chunking(Plan& p, int64_t mig_t0, int64_t mig_t1, int64_t sig_c);
@@ -401,8 +400,6 @@ Plan make_plan_sliced(const Side& s, const Side& d, int64_t slice, int64_t spitc
                       int64_t dcol, int64_t t0, int64_t t1, int l0, int lm, int64_t c, int64_t g, int piece);
 dyna_status launch_rows(const Plan& p, int max_ctas, int dev, cudaStream_t st);
 dyna_status launch_rows_interleaved(const InterleavedSource& src, bool sig, int max_ctas, int dev, cudaStream_t st);
-dyna_status launch_rows_batch(const BatchSource& src, bool sig, int max_ctas, int dev, cudaStream_t st);
-bool fed_vec_enabled();
 // head slices as TMA tensor tiles (k_copy_tiles)
 bool tiles_enabled();
 bool tile_shape(Plan& p);                    // box geometry + item counts (false: not a tile geometry)
