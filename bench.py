@@ -156,8 +156,23 @@ def make_line(*, world, steps, warmup, workload, payload_per_rank, tokens_per_ra
     }
     if impl:
         line["impl"] = impl
+    else:
+        line["paper_context"] = PAPER_CONTEXT
     line.update(extra or {})
     return line
+
+
+# The paper's own numbers on this path (context, not the target: it reports no
+# transfer GB/s, latency or tokens/s).
+PAPER_CONTEXT = {
+    "non_overlapped_transfer_reduction_by_chunking": "94% (PAPER.md §6.6 P:738; 2 servers x 4 A100-80GB, NVLink "
+                                                     "600 GB/s bidirectional, Mini-Reasoning, Qwen-2.5; chunk size "
+                                                     "not stated)",
+    "kv_tokens_transferred_decode_merged_vs_disaggregation": "3x (P:369)",
+    "transfer_mechanism": "fully offloaded to NCCL or Mooncake (P:556); no kernel-level figure",
+    "this_build_analogue": "profiles/r02_overlap.json: per-chunk pushes cut exposed transfer by 86.8-98.3%, "
+                           "per-(chunk, layer) pushes by 98.8-99.8% (configs[3], one B200)",
+}
 
 
 # ---------------------------------------------------------------------------- oracle (CPU) timing
