@@ -1282,8 +1282,12 @@ dyna_status dyna_kv_calibrate(dyna_block_table src, dyna_block_table dst, const 
       if (r) break;
       if (skip) continue;
       float ms = 0.f;
-      CUDA_TRY(cudaEventSynchronize(e1));
-      CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+      cudaError_t ce = cudaEventSynchronize(e1);  // (no early return: the gate below must open)
+      if (ce == cudaSuccess) ce = cudaEventElapsedTime(&ms, e0, e1);
+      if (ce != cudaSuccess) {
+        r = fail(DYNA_ECUDA, "calibrate: %s", cudaGetErrorString(ce));
+        break;
+      }
       ms /= (float)reps;
       const double bytes = (double)c * 2 * L * S->row;
       if (gbps) gbps[i * DYNA_CALIB_CANDIDATES + k] = (float)(bytes / (ms * 1e-3) / 1e9);
