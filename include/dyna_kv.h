@@ -379,7 +379,11 @@ DYNA_API dyna_status dyna_kv_batch_info(dyna_kv_xfer_t xfer, int32_t index, uint
  * HAZARD: while such a migration waits, anything that synchronises the whole
  * device (cudaDeviceSynchronize, cudaMalloc/cudaFree that sync — including
  * this library's create / import calls, which allocate — synchronous copies
- * on the legacy stream) before the last chunk is marked deadlocks: the
+ * on the legacy stream, e.g. a framework's host-to-device copy on the default
+ * stream when the coupled migration runs there) before the last chunk is marked
+ * deadlocks (this library's migration calls themselves initialise what they
+ * create on first use — a pool pair's chunk counters, tile-map cache entries —
+ * on a non-blocking library stream, never on the legacy stream): the
  * device waits for the migration, the migration for a mark that is never
  * issued.  The same holds for the FIRST launch of any kernel in the process
  * while the migration waits: CUDA loads kernels lazily and a module load

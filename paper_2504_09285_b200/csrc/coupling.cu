@@ -224,10 +224,7 @@ static dyna_status chan_check(const dyna_kv_channel* ch, const dyna_block_table&
 
 static dyna_status chan_counters(unsigned long long** c, int dev) {
   if (*c) return DYNA_OK;
-  DeviceGuard g(dev);
-  CUDA_TRY(cudaMalloc(c, sizeof(unsigned long long) * DYNA_MAX_CHUNKS));
-  CUDA_TRY(cudaMemset(*c, 0, sizeof(unsigned long long) * DYNA_MAX_CHUNKS));
-  return DYNA_OK;
+  return zeroed_alloc(reinterpret_cast<void**>(c), sizeof(unsigned long long) * DYNA_MAX_CHUNKS, dev);
 }
 
 dyna_status dyna_kv_push(dyna_block_table src, dyna_range tr, dyna_range lr, int32_t c, dyna_kv_channel_t ch,

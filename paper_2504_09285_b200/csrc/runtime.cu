@@ -335,15 +335,30 @@ dyna_status flag_reserve(int sender, const dyna_kv_pool* dst, int64_t nchunks, u
   return DYNA_OK;
 }
 
+// Zeroed device memory allocated during a call: zeroed on a non-blocking library stream, waited
+// for on the host.  (A plain cudaMemset runs on the legacy stream, which would wait for a
+// producer-coupled migration still waiting for its marks on a blocking stream.)
+dyna_status zeroed_alloc(void** p, size_t bytes, int dev) {
+  DeviceGuard g(dev);
+  DevInfo* di = dev_info(dev);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!di->maps) CUDA_TRY(cudaStreamCreateWithFlags(&di->maps, cudaStreamNonBlocking));
+  }
+  CUDA_TRY(cudaMalloc(p, bytes));
+  CUDA_TRY(cudaMemsetAsync(*p, 0, bytes, di->maps));
+  CUDA_TRY(cudaStreamSynchronize(di->maps));
+  return DYNA_OK;
+}
+
 // Self-resetting per-chunk byte counters of channel src -> dst on device kdev.
 dyna_status channel_counters(dyna_kv_pool* src, const dyna_kv_pool* dst, int kdev, unsigned long long** out) {
   std::lock_guard<std::mutex> lk(src->mu);
   Channel& ch = src->channels[dst];
   unsigned long long*& c = ch.counters[kdev];
   if (!c) {
-    DeviceGuard g(kdev);
-    CUDA_TRY(cudaMalloc(&c, sizeof(unsigned long long) * DYNA_MAX_CHUNKS));
-    CUDA_TRY(cudaMemset(c, 0, sizeof(unsigned long long) * DYNA_MAX_CHUNKS));
+    dyna_status r = zeroed_alloc(reinterpret_cast<void**>(&c), sizeof(unsigned long long) * DYNA_MAX_CHUNKS, kdev);
+    if (r) return r;
   }
   *out = c;
   return DYNA_OK;
@@ -357,36 +372,28 @@ dyna_status channel_tile_maps(dyna_kv_pool* S, const dyna_kv_pool* D, const Plan
   const TileKey key{D->uid, D->base, p.row, p.spitch, p.dpitch, p.scol, p.dcol, p.l0, p.lm, p.tile_rows, p.lkb};
   constexpr size_t set_b = (size_t)kTileMaps * kTileMapBytes;
   std::lock_guard<std::mutex> lk(S->mu);
-  Channel& ch = S->channels[D];
-  for (size_t i = 0; i < ch.tkeys.size(); ++i)
-    if (ch.tkeys[i] == key) {
-      *out = ch.tmaps + i * set_b;
+  if (!S->tmaps || kdev != S->dev) return DYNA_OK;
+  for (size_t i = 0; i < S->tkeys.size(); ++i)
+    if (S->tkeys[i] == key) {
+      *out = S->tmaps + i * set_b;
       return DYNA_OK;
     }
   // a miss: fill the next set (not under capture: the fill synchronises with the host)
-  if (capturing || ch.tkeys.size() >= (size_t)kTileCacheSets) return DYNA_OK;
+  if (capturing || S->tkeys.size() >= (size_t)kTileCacheSets) return DYNA_OK;
   DevInfo* di = dev_info(kdev);
   DeviceGuard g(kdev);
-  if (!ch.tmaps) {
-    if (cudaMalloc(&ch.tmaps, kTileCacheSets * set_b) != cudaSuccess)
-      return fail(DYNA_ENOMEM, "tile map cache (device)");
-    if (cudaHostAlloc(&ch.tmaps_host, kTileCacheSets * set_b, cudaHostAllocPortable) != cudaSuccess)
-      return fail(DYNA_ENOMEM, "tile map cache (pinned)");
-    ch.tdev = kdev;
-  }
-  if (kdev != ch.tdev) return DYNA_OK;
   {
     std::lock_guard<std::mutex> lk2(g_mu);
     if (!di->maps) CUDA_TRY(cudaStreamCreateWithFlags(&di->maps, cudaStreamNonBlocking));
   }
-  const size_t i = ch.tkeys.size();
-  if (!tile_encode(p, ch.tmaps_host + i * set_b)) return DYNA_OK;
+  const size_t i = S->tkeys.size();
+  if (!tile_encode(p, S->tmaps_host + i * set_b)) return DYNA_OK;
   // its own non-blocking stream, waited for on the host: the set is complete before any kernel can
   // name it, whatever stream that kernel runs on (no device-wide synchronisation involved)
-  CUDA_TRY(cudaMemcpyAsync(ch.tmaps + i * set_b, ch.tmaps_host + i * set_b, set_b, cudaMemcpyHostToDevice, di->maps));
+  CUDA_TRY(cudaMemcpyAsync(S->tmaps + i * set_b, S->tmaps_host + i * set_b, set_b, cudaMemcpyHostToDevice, di->maps));
   CUDA_TRY(cudaStreamSynchronize(di->maps));
-  ch.tkeys.push_back(key);
-  *out = ch.tmaps + i * set_b;
+  S->tkeys.push_back(key);
+  *out = S->tmaps + i * set_b;
   return DYNA_OK;
 }
 
@@ -547,6 +554,13 @@ dyna_status dyna_kv_pool_create(const dyna_kv_pool_desc* desc, void* device_base
       delete p;
       return fail(DYNA_ENOMEM, "cannot allocate the %zu B chunk-flag inbox", kInboxBytes);
     }
+    const size_t tb = (size_t)kTileCacheSets * kTileMaps * kTileMapBytes;
+    if (cudaMalloc(&p->tmaps, tb) != cudaSuccess || cudaHostAlloc(&p->tmaps_host, tb, cudaHostAllocPortable) != cudaSuccess) {
+      cudaFree(p->inbox);
+      if (p->tmaps) cudaFree(p->tmaps);
+      delete p;
+      return fail(DYNA_ENOMEM, "cannot allocate the %zu B tile-map cache", tb);
+    }
   }
   p->own_inbox = true;
   dev_info(desc->device);
@@ -560,9 +574,9 @@ dyna_status dyna_kv_pool_destroy(dyna_kv_pool_t p) {
     for (auto& c : kv.second.counters) retire(c.first, c.second, Mem::Device);
     retire(kv.second.sdev, kv.second.sstage, Mem::Device);
     retire(kv.second.ddev, kv.second.dstage, Mem::Device);
-    retire(kv.second.tdev, kv.second.tmaps, Mem::Device);
-    retire(kv.second.tdev, kv.second.tmaps_host, Mem::Host);
   }
+  retire(p->dev, p->tmaps, Mem::Device);
+  retire(p->dev, p->tmaps_host, Mem::Host);
   if (p->own_inbox) retire(p->dev, p->inbox, Mem::Device);
   if (p->imported) {
     retire(p->dev, p->ipc_pool_map, Mem::Ipc);

@@ -101,6 +101,7 @@ bool desc_valid(const dyna_kv_pool_desc* d);
 int64_t gcd64(int64_t a, int64_t b);
 bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out);
 void calib_install(int64_t row, int peer, const std::vector<dyna_kv_calib_entry>& es);
+dyna_status zeroed_alloc(void** p, size_t bytes, int dev);  // no legacy-stream synchronisation
 dyna_status ensure_peer(int dev, int peer);
 // Per-chunk flags: each signalled logical migration gets a fresh epoch and its own range of
 // consecutive inbox slots of (sender instance, destination inbox).  Keyed on the inbox's uid
@@ -146,15 +147,10 @@ struct TileKey {
            scol == o.scol && dcol == o.dcol && l0 == o.l0 && lm == o.lm && g == o.g && lkb == o.lkb;
   }
 };
-constexpr int kTileCacheSets = 64;  // map sets cached per channel (then calls upload their maps)
+constexpr int kTileCacheSets = 128;  // map sets cached per source pool (then calls upload their maps)
 
 struct Channel {  // sender pool -> destination pool
   std::map<int, unsigned long long*> counters;  // per kernel device: [DYNA_MAX_CHUNKS], zero at rest
-  // tile maps, written once per key and never changed while cached: device copy + its pinned source
-  char* tmaps = nullptr;
-  char* tmaps_host = nullptr;
-  int tdev = -1;
-  std::vector<TileKey> tkeys;       // set i is complete on the device once listed here
   char* sstage = nullptr;                      // staged variant: 2 slots on the source device
   char* dstage = nullptr;                      // staged variant: 2 slots on the destination device
   int64_t slot_bytes = 0;
@@ -175,6 +171,11 @@ struct dyna_kv_pool {
   int64_t row = 0;
   std::mutex mu;
   std::map<const dyna_kv_pool*, Channel> channels;  // keyed by destination pool
+  // tile maps of migrations from this pool, allocated at create (a migration never allocates them:
+  // an allocation may synchronise the device), written once per key, never changed
+  char* tmaps = nullptr;       // device, kTileCacheSets x kTileMaps x kTileMapBytes (nullptr: imported)
+  char* tmaps_host = nullptr;  // their pinned source
+  std::vector<TileKey> tkeys;  // set i is complete on the device once listed here
 };
 
 struct dyna_kv_ready {
@@ -405,10 +406,10 @@ bool tiles_enabled();
 bool tile_shape(Plan& p);                    // box geometry + item counts (false: not a tile geometry)
 bool tile_encode(const Plan& p, void* maps);  // maps: kTileMaps x kTileMapBytes of host memory
 bool tile_plan(Plan& p, void* maps);          // both
-// The device copy of a tile plan's maps cached on channel S -> D (kernel device kdev), written at
-// first use by a host-synchronised copy on a library stream; *out = nullptr when not available (a
-// miss under capture, or the cache is full): the caller then uploads the maps with the call's
-// tables, or does not tile.
+// The device copy of a tile plan's maps from pool S to D, cached with S (kernel device kdev) and
+// written at first use by a host-synchronised copy on a library stream; *out = nullptr when not
+// available (a miss under capture, the cache is full, or S has none): the caller then uploads the
+// maps with the call's tables, or does not tile.
 dyna_status channel_tile_maps(dyna_kv_pool* S, const dyna_kv_pool* D, const Plan& p, int kdev, cudaStream_t st,
                               const char** out);
 dyna_status launch_tiles_batch(const BatchSource& src, bool sig, int tile_bytes, int stages, int max_ctas, int dev,

@@ -376,3 +376,40 @@ def test_destroy_during_coupled_wait_does_not_deadlock():
         extra.close()
     finally:
         dk.dyna_kv_ready_destroy(board)
+
+
+def test_first_use_of_a_channel_during_coupled_wait_does_not_deadlock():
+    """While a producer-coupled migration waits on the device for its marks, the FIRST signalled
+    (and small-row, tiled) migration of a new pool pair allocates that pair's chunk counters and
+    fills the source pool's tile-map cache.  Those fills run on a non-blocking library stream and
+    are waited for on the host; a legacy-stream cudaMemset there would wait for the coupled
+    kernel, whose marks this thread only issues afterwards (a deadlock until the board timeout)."""
+    import time
+    g = Geom(4, 8, 128, 2, 16, 300)
+    gs = Geom(3, 1, 128, 2, 16, 300)                     # 256-B rows: AUTO tiles
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(5, 1200, g, g)
+    a, b = pool_filled(gs, 3), pool_filled(gs, 4)        # a pair never used before
+    ta, tb = kvgen.table_pair(6, 1200, gs, gs)
+    prod = torch.cuda.Stream()
+    side = torch.cuda.Stream()
+    board = dk.dyna_kv_ready_create(0, 64)
+    dk.dyna_kv_ready_set_timeout(board, 8_000_000_000)
+    # every torch allocation / copy before the coupled launch: torch's own H2D copies run on the
+    # legacy stream, which the coupled kernel below occupies until its marks arrive
+    st, dt, at, bt = dev_table(src, ts), dev_table(dst, td), dev_table(a, ta), dev_table(b, tb)
+    torch.cuda.synchronize()
+    epoch = dk.dyna_kv_ready_begin(board)
+    x = dk.dyna_kv_migrate_on_ready(st, dt, (0, 1000), (0, 4), 250, board, epoch,
+                                    torch.cuda.default_stream().cuda_stream, dk.opts(max_ctas=8))
+    t0 = time.perf_counter()
+    y = dk.dyna_kv_migrate_ex(at, bt, (0, 1000), (0, 3), 250, side.cuda_stream, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL))
+    issue_s = time.perf_counter() - t0
+    for k in range(4):
+        dk.dyna_kv_ready_mark(board, k, epoch, prod.cuda_stream)
+    dk.dyna_kv_wait(y)
+    dk.dyna_kv_wait(x)                                   # DYNA_ETIMEDOUT here would mean the fill blocked
+    assert issue_s < 4.0, issue_s
+    assert torch_rows_equal(src, ts, dst, td, (0, 1000), (0, 4))
+    assert torch_rows_equal(a, ta, b, tb, (0, 1000), (0, 3))
+    dk.dyna_kv_ready_destroy(board)
