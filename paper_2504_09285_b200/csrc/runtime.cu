@@ -444,6 +444,25 @@ dyna_status channel_staging_done(dyna_kv_pool* src, const dyna_kv_pool* dst, cud
 std::mutex g_rings_mu;
 std::map<int, UploadRing*> g_rings;
 
+// The device's upload ring, allocated when its first pool is created rather than by the first
+// migration with host tables (an allocation during a producer-coupled wait may synchronise).
+dyna_status ensure_upload_ring(int dev) {
+  UploadRing* r = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_rings_mu);
+    UploadRing*& slot = g_rings[dev];
+    if (!slot) slot = new UploadRing();
+    r = slot;
+  }
+  std::lock_guard<std::mutex> lk(r->mu);
+  if (r->host) return DYNA_OK;
+  DeviceGuard g(dev);
+  if (cudaHostAlloc(&r->host, kRingBytes, cudaHostAllocPortable) != cudaSuccess ||
+      cudaMalloc(&r->dev, kRingBytes) != cudaSuccess)
+    return fail(DYNA_ENOMEM, "upload ring (%zu B pinned + device)", kRingBytes);
+  return DYNA_OK;
+}
+
 uint64_t new_uid() {
   static std::atomic<uint64_t> seq{0};
   static const uint64_t base = [] {
@@ -564,6 +583,11 @@ dyna_status dyna_kv_pool_create(const dyna_kv_pool_desc* desc, void* device_base
   }
   p->own_inbox = true;
   dev_info(desc->device);
+  dyna_status r = ensure_upload_ring(desc->device);
+  if (r) {
+    dyna_kv_pool_destroy(p);
+    return r;
+  }
   *out = p;
   return DYNA_OK;
 }

@@ -256,6 +256,7 @@ struct UploadRing {
 
 extern std::mutex g_rings_mu;
 extern std::map<int, UploadRing*> g_rings;
+dyna_status ensure_upload_ring(int dev);
 
 // Holds the ring's lock from upload() until finish() records the release event.
 class RingLease {
