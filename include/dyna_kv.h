@@ -41,6 +41,7 @@
  *                    dyna_kv_push_heads / _place_heads
  *   halves           dyna_kv_pack / _unpack (source rows -> contiguous buffer -> destination rows)
  *   selection        dyna_kv_calib_set / _get (the measured AUTO table), dyna_kv_calibrate (measure it here)
+ *   plan once        dyna_kv_prepare_batch / _prepared_launch / _prepared_destroy (CUDA-graph friendly batches)
  *
  * Errors: every call returns a dyna_status; negative values are errors and
  * dyna_kv_last_error() returns a thread-local message.  No call throws.
@@ -363,6 +364,24 @@ DYNA_API dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_
  * for a handle that is not a signalled batch. */
 DYNA_API dyna_status dyna_kv_batch_info(dyna_kv_xfer_t xfer, int32_t index, uint64_t* epoch, int32_t* first_slot,
                                         int32_t* num_chunks, int32_t* sender);
+
+/* Prepared batches: plan once, launch many (CUDA-graph friendly).  dyna_kv_prepare_batch
+ * validates the batch exactly as dyna_kv_migrate_batch (same rules and errors; R7 checked once,
+ * here), resolves the engine, and uploads the plans, item bases, tile maps and any host-resident
+ * block tables into device memory owned by the handle (a synchronous, startup-time call: it
+ * allocates).  dyna_kv_prepared_launch enqueues the whole batch on `stream` with ONE kernel and no
+ * host-side validation, upload or allocation, so it can be captured into a CUDA graph and
+ * replayed; each launch re-reads the rows and the device block tables as they are then (the tables
+ * must keep their entries).  No per-chunk flags (DYNA_EINVAL with DYNA_MIGRATE_SIGNAL).  The
+ * launches of one handle share its deferred-error word: dyna_kv_wait of any of them reports, and
+ * clears, the errors of every earlier launch.  The handle must outlive every launch made from it
+ * (until dyna_kv_wait); dyna_kv_prepared_destroy never synchronises the device. */
+typedef struct dyna_kv_prepared* dyna_kv_prepared_t;
+DYNA_API dyna_status dyna_kv_prepare_batch(const dyna_kv_migration* migs, int32_t n, dyna_range layer_range,
+                                           int32_t chunk_tokens, const dyna_kv_opts* opts, dyna_kv_prepared_t* out);
+DYNA_API dyna_status dyna_kv_prepared_launch(dyna_kv_prepared_t prepared, struct CUstream_st* stream,
+                                             dyna_kv_xfer_t* out);
+DYNA_API dyna_status dyna_kv_prepared_destroy(dyna_kv_prepared_t prepared);
 
 /* Producer-coupled push (§4.3: "once chunk
  * k completes, its KV block is immediately DMA-pushed ... while Server1

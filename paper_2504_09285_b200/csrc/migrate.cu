@@ -953,10 +953,13 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   return DYNA_OK;
 }
 
-dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna_range lr, int32_t chunk_tokens,
-                                  struct CUstream_st* stream_, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
-  if (!out) return fail(DYNA_EINVAL, "NULL out");
-  *out = nullptr;
+}  // extern "C"
+
+// A batch, launched now (prep == nullptr: *out receives the migration) or planned and uploaded into
+// memory owned by *prep for later launches (dyna_kv_prepare_batch; out unused).
+static dyna_status batch_impl(const dyna_kv_migration* migs, int32_t n, dyna_range lr, int32_t chunk_tokens,
+                              struct CUstream_st* stream_, const dyna_kv_opts* opts, dyna_kv_xfer_t* out,
+                              dyna_kv_prepared* prep) {
   if (n < 0 || (n > 0 && !migs) || n > DYNA_MAX_BATCH) return fail(DYNA_EINVAL, "0 <= n <= DYNA_MAX_BATCH");
   dyna_kv_opts o{};
   dyna_status r = check_opts(opts, &o);
@@ -964,6 +967,8 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "batch: FUSED variant only");
   if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
+  if (prep && signal)
+    return fail(DYNA_EINVAL, "prepared batch: no per-chunk flags (every launch would need fresh epochs and slots)");
   const bool unchecked = (o.flags & DYNA_MIGRATE_UNCHECKED) != 0;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   // Reading R7 across entries: one entry's source rows may be another entry's destination rows.
@@ -1000,6 +1005,10 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   }
   if ((r = check_alias(dsp, ssp))) return r;
   if (live.empty()) {
+    if (prep) {
+      prep->empty = true;
+      return DYNA_OK;
+    }
     auto* x = new dyna_kv_xfer();
     x->empty = true;
     if (signal) x->batch.assign(n, dyna_kv_xfer::BatchEntry{});  // every entry: 0 chunks
@@ -1016,6 +1025,10 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   DeviceGuard guard(S0->dev);
   dyna_kv_xfer* x = nullptr;
   if ((r = new_xfer(S0->dev, S0->desc.instance, stream, &x))) return r;
+  if (prep) {  // the plans' error word belongs to the prepared handle
+    prep->err = x->err;
+    x->own_err = false;
+  }
   const int l0 = (int)lr.begin, lm = (int)(lr.end - lr.begin);
   if (signal) {  // each entry: its own epoch and slot range of its (sender, destination pool)
     // the entries of one launch must not share slots (their counters live there): at most
@@ -1127,7 +1140,16 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   RingLease lease(S0->dev);
   int64_t total_items = 0;
   char *dbase = nullptr, *h = nullptr;
-  if ((r = lease.reserve(plans_b + bases_b + tab_b, &dbase, &h, stream))) {
+  std::vector<char> prep_host;
+  if (prep) {  // memory of its own, uploaded once below
+    prep_host.assign(plans_b + bases_b + tab_b, 0);
+    h = prep_host.data();
+    if (cudaMalloc(&prep->mem, prep_host.size()) != cudaSuccess) {
+      delete x;
+      return fail(DYNA_ENOMEM, "prepared batch: %zu B of device memory", prep_host.size());
+    }
+    dbase = prep->mem;
+  } else if ((r = lease.reserve(plans_b + bases_b + tab_b, &dbase, &h, stream))) {
     delete x;
     return r;
   }
@@ -1178,7 +1200,18 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     if (!mg.dst.block_ids)
       std::memcpy(h + doff[k], mg.dst.host_block_ids, table_upload_bytes(mg.dst, mg.token_range.end));
   }
-  if ((r = lease.copy(stream))) {
+  if (prep) {  // one host-synchronised copy on a library stream (no legacy-stream synchronisation)
+    DevInfo* di = dev_info(S0->dev);
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      if (!di->maps && cudaStreamCreateWithFlags(&di->maps, cudaStreamNonBlocking) != cudaSuccess) di->maps = nullptr;
+    }
+    if (!di->maps || cudaMemcpyAsync(dbase, h, prep_host.size(), cudaMemcpyHostToDevice, di->maps) != cudaSuccess ||
+        cudaStreamSynchronize(di->maps) != cudaSuccess) {
+      delete x;
+      return fail(DYNA_ECUDA, "prepared batch: upload");
+    }
+  } else if ((r = lease.copy(stream))) {
     delete x;
     return r;
   }
@@ -1190,6 +1223,20 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
   x->stages = ch.engine != DYNA_ENGINE_VEC ? ch.stages : 0;
   x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
   x->launches = 1;
+  if (prep) {
+    prep->dev = S0->dev;
+    prep->sender = S0->desc.instance;
+    prep->src = bsrc;
+    prep->tiles = tiles;
+    prep->engine = ch.engine;
+    prep->piece = ch.piece;
+    prep->stages = ch.stages;
+    prep->unroll = ch.unroll;
+    prep->max_ctas = o.max_ctas;
+    prep->schedule = o.schedule;
+    delete x;
+    return DYNA_OK;
+  }
   r = tiles ? launch_tiles_batch(bsrc, signal, ch.piece, ch.stages, o.max_ctas, S0->dev, stream)
             : launch_batch(bsrc, total_items, signal, ch.piece, ch.engine, o.max_ctas, ch.stages, ch.unroll,
                            S0->dev, stream, o.schedule);
@@ -1203,6 +1250,75 @@ dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna
     return r;
   }
   *out = x;
+  return DYNA_OK;
+}
+
+extern "C" {
+
+dyna_status dyna_kv_migrate_batch(const dyna_kv_migration* migs, int32_t n, dyna_range lr, int32_t chunk_tokens,
+                                  struct CUstream_st* stream, const dyna_kv_opts* opts, dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  return batch_impl(migs, n, lr, chunk_tokens, stream, opts, out, nullptr);
+}
+
+// ---------------------------------------------------------------- prepared batches (plan once, launch many)
+dyna_status dyna_kv_prepare_batch(const dyna_kv_migration* migs, int32_t n, dyna_range lr, int32_t chunk_tokens,
+                                  const dyna_kv_opts* opts, dyna_kv_prepared_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  auto* p = new dyna_kv_prepared();
+  const dyna_status r = batch_impl(migs, n, lr, chunk_tokens, nullptr, opts, nullptr, p);
+  if (r) {
+    if (p->mem) retire(p->dev, p->mem, Mem::Device);
+    if (p->err) err_release(p->err);
+    delete p;
+    return r;
+  }
+  *out = p;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_prepared_launch(dyna_kv_prepared_t p, struct CUstream_st* stream_, dyna_kv_xfer_t* out) {
+  if (!p || !out) return fail(DYNA_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (p->empty) {
+    auto* x = new dyna_kv_xfer();
+    x->empty = true;
+    *out = x;
+    return DYNA_OK;
+  }
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  DeviceGuard guard(p->dev);
+  dyna_kv_xfer* x = nullptr;
+  dyna_status r = new_xfer(p->dev, p->sender, stream, &x);
+  if (r) return r;
+  if (x->err != g_err_word) err_release(x->err);
+  x->err = p->err;  // its kernels report into the handle's word
+  x->own_err = false;
+  x->variant = DYNA_VARIANT_FUSED;
+  x->engine = p->engine;
+  x->piece = p->piece;
+  x->stages = p->engine != DYNA_ENGINE_VEC ? p->stages : 0;
+  x->unroll = p->engine == DYNA_ENGINE_VEC ? p->unroll : 0;
+  x->launches = 1;
+  r = p->tiles ? launch_tiles_batch(p->src, false, p->piece, p->stages, p->max_ctas, p->dev, stream)
+               : launch_batch(p->src, p->src.total_items, false, p->piece, p->engine, p->max_ctas, p->stages,
+                              p->unroll, p->dev, stream, p->schedule);
+  if (!r) r = record_completion(x, p->dev, stream);
+  if (r) {
+    delete x;
+    return r;
+  }
+  *out = x;
+  return DYNA_OK;
+}
+
+dyna_status dyna_kv_prepared_destroy(dyna_kv_prepared_t p) {
+  if (!p) return fail(DYNA_EINVAL, "NULL prepared");
+  if (p->mem) retire(p->dev, p->mem, Mem::Device);  // never synchronises (see pool_destroy)
+  if (p->err) err_release(p->err);
+  delete p;
   return DYNA_OK;
 }
 

@@ -215,9 +215,10 @@ struct dyna_kv_channel {
 
 struct dyna_kv_xfer {
   ~dyna_kv_xfer() {
-    if (err && err != dynakv::rt::g_err_word) dynakv::rt::err_release(err);
+    if (err && own_err && err != dynakv::rt::g_err_word) dynakv::rt::err_release(err);
   }
   unsigned int* err = nullptr;  // this migration's deferred-error word (g_err_word when captured)
+  bool own_err = true;          // false: the word belongs to a prepared migration (dyna_kv_prepared)
   cudaEvent_t ev = nullptr;
   bool captured = false;  // enqueued during CUDA-graph capture: the work runs at replay
   int32_t variant = 0, engine = 0, piece = 0, stages = 0, unroll = 0, launches = 0;
@@ -236,6 +237,18 @@ struct dyna_kv_xfer {
   int32_t first_slot = 0;          // signalled: chunk k's flag is inbox slot [sender][first_slot + k]
 };
 
+
+// A batch planned and uploaded once (dyna_kv_prepare_batch): device memory with its plans, item
+// bases, tile maps and host-resident tables, launched any number of times.
+struct dyna_kv_prepared {
+  bool empty = false;
+  int dev = 0, sender = 0;
+  char* mem = nullptr;             // device: [tile maps][plans][item bases][tables]
+  unsigned int* err = nullptr;     // the deferred-error word its kernels write (shared by its launches)
+  dynakv::BatchSource src{};
+  bool tiles = false;
+  int32_t engine = 0, piece = 0, stages = 0, unroll = 0, max_ctas = 0, schedule = 0;
+};
 
 namespace dynakv {
 namespace rt {

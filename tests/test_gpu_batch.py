@@ -462,3 +462,68 @@ def test_batch_tiles_need_one_run_grid():
     dk.dyna_kv_wait(x)
     assert np.array_equal(d1.tensor.cpu().numpy(), w1)
     assert np.array_equal(d2.tensor.cpu().numpy(), w2)
+
+
+# ---------------------------------------------------------------- prepared batches (plan once, launch many)
+@pytest.mark.parametrize("rows", ["2KiB", "256B"])
+def test_prepared_batch_launches_and_graph_replay(rows):
+    """dyna_kv_prepare_batch plans and uploads a batch once; every dyna_kv_prepared_launch (and every
+    replay of a CUDA graph that captured one) moves the rows as they are at that launch: the source
+    is rewritten between launches and the destination must follow it, bit-exact vs the oracle.  Host
+    tables are copied at prepare time (later edits of the host arrays do not matter)."""
+    g = Geom(3, 8, 128, 2, 16, 600) if rows == "2KiB" else Geom(3, 1, 128, 2, 16, 600)
+    reqs = kvgen.migrating(kvgen.skewed_batch(23, 12))
+    lens = [min(r.s, 700) for r in reqs]
+    tabs = kvgen.batch_tables(24, [n + 16 for n in lens], g, g)
+    dst = pool_filled(g, 2)
+    src = pool_filled(g, 1)
+    migs = [(host_table(src, ts.copy()), dev_table(dst, td), (3, 3 + n)) for n, (ts, td) in zip(lens, tabs)]
+    prep = dk.dyna_kv_prepare_batch(migs, (0, 3), 128)
+    for m in migs:                                        # host arrays edited after prepare: irrelevant
+        m[0]._keep[1][:] = 0                              # (the numpy array behind host_block_ids)
+    s = torch.cuda.Stream()
+    try:
+        for seed in (31, 32):
+            dk.dyna_kv_debug_fill(src.tensor.data_ptr(), src.tensor.numel(), seed, 0, 0)
+            torch.cuda.synchronize()
+            x = dk.dyna_kv_prepared_launch(prep, s.cuda_stream)
+            plan = dk.dyna_kv_xfer_plan(x)
+            dk.dyna_kv_wait(x)
+            assert plan["launches"] == 1
+            if rows == "256B":
+                assert plan["engine"] == dk.DYNA_ENGINE_TILES
+            want = kvgen.fill_bytes(2, g.pool_bytes) if seed == 31 else want
+            for n, (ts, td) in zip(lens, tabs):
+                oracle.migrate(kvgen.fill_bytes(seed, g.pool_bytes), g, ts, want, g, td, (3, 3 + n))
+            assert np.array_equal(dst.tensor.cpu().numpy(), want), seed
+        graph = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=s):
+            xg = dk.dyna_kv_prepared_launch(prep, s.cuda_stream)
+        dk.dyna_kv_wait(xg)
+        for seed in (33, 34):
+            dk.dyna_kv_debug_fill(src.tensor.data_ptr(), src.tensor.numel(), seed, 0, 0)
+            torch.cuda.synchronize()
+            graph.replay()
+            torch.cuda.synchronize()
+            for n, (ts, td) in zip(lens, tabs):
+                oracle.migrate(kvgen.fill_bytes(seed, g.pool_bytes), g, ts, want, g, td, (3, 3 + n))
+            assert np.array_equal(dst.tensor.cpu().numpy(), want), seed
+    finally:
+        dk.dyna_kv_prepared_destroy(prep)
+
+
+def test_prepared_batch_errors_and_empty():
+    g = Geom(2, 8, 128, 2, 16, 100)
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    ts, td = kvgen.table_pair(3, 200, g, g)
+    migs = [(dev_table(src, ts), dev_table(dst, td), (0, 100))]
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_prepare_batch(migs, (0, 2), 32, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL))
+    assert e.value.status == dk.DYNA_EINVAL
+    with pytest.raises(dk.DynaKVError) as e:         # R7 is checked at prepare time
+        dk.dyna_kv_prepare_batch(migs + [(dev_table(src, ts), dev_table(dst, td), (50, 60))], (0, 2), 32)
+    assert e.value.status == dk.DYNA_EALIAS
+    empty = dk.dyna_kv_prepare_batch([(dev_table(src, ts), dev_table(dst, td), (5, 5))], (0, 2), 32)
+    dk.dyna_kv_wait(dk.dyna_kv_prepared_launch(empty, 0))
+    dk.dyna_kv_prepared_destroy(empty)
