@@ -379,6 +379,10 @@ DYNA_API dyna_status dyna_kv_batch_info(dyna_kv_xfer_t xfer, int32_t index, uint
 typedef struct dyna_kv_prepared* dyna_kv_prepared_t;
 DYNA_API dyna_status dyna_kv_prepare_batch(const dyna_kv_migration* migs, int32_t n, dyna_range layer_range,
                                            int32_t chunk_tokens, const dyna_kv_opts* opts, dyna_kv_prepared_t* out);
+/* The same for a whole TP reshard (dyna_kv_reshard's arguments and rules; one launch). */
+DYNA_API dyna_status dyna_kv_prepare_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_range token_range,
+                                             dyna_range layer_range, int32_t chunk_tokens, const dyna_kv_opts* opts,
+                                             dyna_kv_prepared_t* out);
 DYNA_API dyna_status dyna_kv_prepared_launch(dyna_kv_prepared_t prepared, struct CUstream_st* stream,
                                              dyna_kv_xfer_t* out);
 DYNA_API dyna_status dyna_kv_prepared_destroy(dyna_kv_prepared_t prepared);

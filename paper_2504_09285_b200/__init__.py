@@ -40,7 +40,7 @@ EXPORTS = (
     "dyna_kv_stream_wait_chunk", "dyna_kv_last_error", "dyna_kv_poll_error", "dyna_kv_launch_count",
     "dyna_kv_enable_peer", "dyna_kv_pool_export", "dyna_kv_pool_import", "dyna_kv_debug_fill",
     "dyna_kv_copy_flags", "dyna_kv_calib_set", "dyna_kv_calib_get", "dyna_kv_calibrate", "dyna_kv_migrate_batch",
-    "dyna_kv_prepare_batch", "dyna_kv_prepared_launch", "dyna_kv_prepared_destroy",
+    "dyna_kv_prepare_batch", "dyna_kv_prepare_reshard", "dyna_kv_prepared_launch", "dyna_kv_prepared_destroy",
     "dyna_kv_xfer_plan", "dyna_kv_ready_create", "dyna_kv_ready_destroy", "dyna_kv_ready_begin",
     "dyna_kv_ready_mark", "dyna_kv_migrate_on_ready", "dyna_kv_ready_set_timeout",
     "dyna_kv_channel_create", "dyna_kv_channel_export", "dyna_kv_channel_import", "dyna_kv_channel_destroy",
@@ -166,6 +166,8 @@ def _load():
         "dyna_kv_calib_get": (ctypes.c_int32, [p(dyna_kv_calib_entry), ctypes.c_int32]),
         "dyna_kv_prepare_batch": (st, [p(dyna_kv_migration), ctypes.c_int32, dyna_range, ctypes.c_int32,
                                        p(dyna_kv_opts), p(vp)]),
+        "dyna_kv_prepare_reshard": (st, [p(dyna_kv_head_migration), ctypes.c_int32, dyna_range, dyna_range,
+                                         ctypes.c_int32, p(dyna_kv_opts), p(vp)]),
         "dyna_kv_prepared_launch": (st, [vp, vp, p(vp)]),
         "dyna_kv_prepared_destroy": (st, [vp]),
         "dyna_kv_calibrate": (st, [dyna_block_table, dyna_block_table, p(ctypes.c_int32), ctypes.c_int32,
@@ -261,6 +263,17 @@ def dyna_kv_prepare_batch(migs, layer_range, chunk_tokens: int, opts: dyna_kv_op
     out = ctypes.c_void_p()
     _check(lib.dyna_kv_prepare_batch(arr, len(migs), dyna_range(*layer_range), chunk_tokens,
                                      ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
+    return out.value
+
+
+def dyna_kv_prepare_reshard(migs, token_range, layer_range, chunk_tokens: int, opts: dyna_kv_opts | None = None) -> int:
+    """Plan + upload a TP reshard once; migs as dyna_kv_reshard."""
+    arr = (dyna_kv_head_migration * max(1, len(migs)))(
+        *[dyna_kv_head_migration(a, b, dyna_range(*hr), hd, 0) for a, b, hr, hd in migs])
+    out = ctypes.c_void_p()
+    _check(lib.dyna_kv_prepare_reshard(arr, len(migs), dyna_range(*token_range), dyna_range(*layer_range),
+                                       chunk_tokens, ctypes.byref(opts) if opts is not None else None,
+                                       ctypes.byref(out)))
     return out.value
 
 

@@ -754,11 +754,12 @@ dyna_status dyna_kv_unpack(const void* buf, uint64_t buf_bytes, dyna_block_table
 // Every entry moves heads [src_heads) of its source rows into heads [dst_head_begin, ...) of its
 // destination rows, for the same tokens, layers and chunking; all entries' slices have one size,
 // so their work items line up: one launch (InterleavedSource, entries one after the other).
-dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_range tr, dyna_range lr,
-                            int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
-                            dyna_kv_xfer_t* out) {
-  if (!out) return fail(DYNA_EINVAL, "NULL out");
-  *out = nullptr;
+}  // extern "C"
+
+// A reshard, launched now (prep == nullptr) or planned and uploaded into *prep for later launches.
+static dyna_status reshard_impl(const dyna_kv_head_migration* migs, int32_t n, dyna_range tr, dyna_range lr,
+                                int32_t chunk_tokens, struct CUstream_st* stream_, const dyna_kv_opts* opts,
+                                dyna_kv_xfer_t* out, dyna_kv_prepared* prep) {
   if (n < 0 || (n > 0 && !migs) || n > DYNA_MAX_BATCH) return fail(DYNA_EINVAL, "0 <= n <= DYNA_MAX_BATCH");
   dyna_kv_opts o{};
   dyna_status r = check_opts(opts, &o);
@@ -766,6 +767,8 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   if (o.flags & DYNA_READY_PER_LAYER) return fail(DYNA_EINVAL, "DYNA_READY_PER_LAYER needs a ready board");
   if (o.variant == DYNA_VARIANT_STAGED) return fail(DYNA_ENOTSUP, "reshard: FUSED variant only");
   const bool signal = (o.flags & DYNA_MIGRATE_SIGNAL) != 0;
+  if (prep && signal)
+    return fail(DYNA_EINVAL, "prepared reshard: no per-chunk flags (every launch would need fresh epochs and slots)");
   const bool unchecked = (o.flags & DYNA_MIGRATE_UNCHECKED) != 0;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   std::vector<Span> dsp, ssp;
@@ -807,6 +810,10 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
     empty &= e;
   }
   if ((r = check_alias(dsp, ssp))) return r;
+  if (empty && prep) {
+    prep->empty = true;
+    return DYNA_OK;
+  }
   if (empty) {
     auto* x = new dyna_kv_xfer();
     x->empty = true;
@@ -827,6 +834,10 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   DeviceGuard guard(S0->dev);
   dyna_kv_xfer* x = nullptr;
   if ((r = new_xfer(S0->dev, S0->desc.instance, stream, &x))) return r;
+  if (prep) {  // the plans' error word belongs to the prepared handle
+    prep->err = x->err;
+    x->own_err = false;
+  }
   if (signal) {
     x->batch.assign(n, dyna_kv_xfer::BatchEntry{});
     for (int32_t i = 0; i < n; ++i) {
@@ -895,7 +906,16 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   }
   RingLease lease(S0->dev);
   char *dbase = nullptr, *h = nullptr;
-  if ((r = lease.reserve(plans_b + tab_b, &dbase, &h, stream))) {
+  std::vector<char> prep_host;
+  if (prep) {  // memory of its own, uploaded once below
+    prep_host.assign(plans_b + tab_b, 0);
+    h = prep_host.data();
+    if (cudaMalloc(&prep->mem, prep_host.size()) != cudaSuccess) {
+      delete x;
+      return fail(DYNA_ENOMEM, "prepared reshard: %zu B of device memory", prep_host.size());
+    }
+    dbase = prep->mem;
+  } else if ((r = lease.reserve(plans_b + tab_b, &dbase, &h, stream))) {
     delete x;
     return r;
   }
@@ -925,7 +945,12 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
     if (!migs[i].src.block_ids) std::memcpy(h + soff[i], migs[i].src.host_block_ids, table_upload_bytes(migs[i].src, tr.end));
     if (!migs[i].dst.block_ids) std::memcpy(h + doff[i], migs[i].dst.host_block_ids, table_upload_bytes(migs[i].dst, tr.end));
   }
-  if ((r = lease.copy(stream))) {
+  if (prep) {
+    if ((r = upload_sync(S0->dev, dbase, h, prep_host.size()))) {
+      delete x;
+      return r;
+    }
+  } else if ((r = lease.copy(stream))) {
     delete x;
     return r;
   }
@@ -936,6 +961,19 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
   x->unroll = tiles ? 0 : 8;
   x->stages = tiles ? (o.stages ? o.stages : 4) : 0;
   x->nchunks = (int32_t)nchunks;
+  if (prep) {
+    prep->reshard = true;
+    prep->dev = S0->dev;
+    prep->sender = S0->desc.instance;
+    prep->isrc = isrc;
+    prep->tiles = tiles;
+    prep->engine = x->engine;
+    prep->piece = tiles ? plans[0].tile_bytes : piece;
+    prep->stages = o.stages;
+    prep->max_ctas = o.max_ctas;
+    delete x;
+    return DYNA_OK;
+  }
   const uint64_t launches0 = g_launches.load();
   r = tiles ? launch_tiles_interleaved(isrc, signal, plans[0].tile_bytes, o.stages, o.max_ctas, S0->dev, stream)
             : launch_rows_interleaved(isrc, signal, o.max_ctas, S0->dev, stream);
@@ -950,6 +988,32 @@ dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_
     return r;
   }
   *out = x;
+  return DYNA_OK;
+}
+
+extern "C" {
+
+dyna_status dyna_kv_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_range tr, dyna_range lr,
+                            int32_t chunk_tokens, struct CUstream_st* stream, const dyna_kv_opts* opts,
+                            dyna_kv_xfer_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  return reshard_impl(migs, n, tr, lr, chunk_tokens, stream, opts, out, nullptr);
+}
+
+dyna_status dyna_kv_prepare_reshard(const dyna_kv_head_migration* migs, int32_t n, dyna_range tr, dyna_range lr,
+                                    int32_t chunk_tokens, const dyna_kv_opts* opts, dyna_kv_prepared_t* out) {
+  if (!out) return fail(DYNA_EINVAL, "NULL out");
+  *out = nullptr;
+  auto* p = new dyna_kv_prepared();
+  const dyna_status r = reshard_impl(migs, n, tr, lr, chunk_tokens, nullptr, opts, nullptr, p);
+  if (r) {
+    if (p->mem) retire(p->dev, p->mem, Mem::Device);
+    if (p->err) err_release(p->err);
+    delete p;
+    return r;
+  }
+  *out = p;
   return DYNA_OK;
 }
 
@@ -1200,16 +1264,10 @@ static dyna_status batch_impl(const dyna_kv_migration* migs, int32_t n, dyna_ran
     if (!mg.dst.block_ids)
       std::memcpy(h + doff[k], mg.dst.host_block_ids, table_upload_bytes(mg.dst, mg.token_range.end));
   }
-  if (prep) {  // one host-synchronised copy on a library stream (no legacy-stream synchronisation)
-    DevInfo* di = dev_info(S0->dev);
-    {
-      std::lock_guard<std::mutex> lk(g_mu);
-      if (!di->maps && cudaStreamCreateWithFlags(&di->maps, cudaStreamNonBlocking) != cudaSuccess) di->maps = nullptr;
-    }
-    if (!di->maps || cudaMemcpyAsync(dbase, h, prep_host.size(), cudaMemcpyHostToDevice, di->maps) != cudaSuccess ||
-        cudaStreamSynchronize(di->maps) != cudaSuccess) {
+  if (prep) {
+    if ((r = upload_sync(S0->dev, dbase, h, prep_host.size()))) {
       delete x;
-      return fail(DYNA_ECUDA, "prepared batch: upload");
+      return r;
     }
   } else if ((r = lease.copy(stream))) {
     delete x;
@@ -1302,9 +1360,13 @@ dyna_status dyna_kv_prepared_launch(dyna_kv_prepared_t p, struct CUstream_st* st
   x->stages = p->engine != DYNA_ENGINE_VEC ? p->stages : 0;
   x->unroll = p->engine == DYNA_ENGINE_VEC ? p->unroll : 0;
   x->launches = 1;
-  r = p->tiles ? launch_tiles_batch(p->src, false, p->piece, p->stages, p->max_ctas, p->dev, stream)
-               : launch_batch(p->src, p->src.total_items, false, p->piece, p->engine, p->max_ctas, p->stages,
-                              p->unroll, p->dev, stream, p->schedule);
+  if (p->reshard)
+    r = p->tiles ? launch_tiles_interleaved(p->isrc, false, p->piece, p->stages, p->max_ctas, p->dev, stream)
+                 : launch_rows_interleaved(p->isrc, false, p->max_ctas, p->dev, stream);
+  else
+    r = p->tiles ? launch_tiles_batch(p->src, false, p->piece, p->stages, p->max_ctas, p->dev, stream)
+                 : launch_batch(p->src, p->src.total_items, false, p->piece, p->engine, p->max_ctas, p->stages,
+                                p->unroll, p->dev, stream, p->schedule);
   if (!r) r = record_completion(x, p->dev, stream);
   if (r) {
     delete x;

@@ -351,6 +351,19 @@ dyna_status zeroed_alloc(void** p, size_t bytes, int dev) {
   return DYNA_OK;
 }
 
+// A host image copied to device memory and waited for on the host, on a non-blocking library stream.
+dyna_status upload_sync(int dev, void* dst, const void* src, size_t bytes) {
+  DeviceGuard g(dev);
+  DevInfo* di = dev_info(dev);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!di->maps) CUDA_TRY(cudaStreamCreateWithFlags(&di->maps, cudaStreamNonBlocking));
+  }
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, di->maps));
+  CUDA_TRY(cudaStreamSynchronize(di->maps));
+  return DYNA_OK;
+}
+
 // Self-resetting per-chunk byte counters of channel src -> dst on device kdev.
 dyna_status channel_counters(dyna_kv_pool* src, const dyna_kv_pool* dst, int kdev, unsigned long long** out) {
   std::lock_guard<std::mutex> lk(src->mu);

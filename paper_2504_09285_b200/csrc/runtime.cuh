@@ -102,6 +102,7 @@ int64_t gcd64(int64_t a, int64_t b);
 bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out);
 void calib_install(int64_t row, int peer, const std::vector<dyna_kv_calib_entry>& es);
 dyna_status zeroed_alloc(void** p, size_t bytes, int dev);  // no legacy-stream synchronisation
+dyna_status upload_sync(int dev, void* dst, const void* src, size_t bytes);  // likewise
 dyna_status ensure_peer(int dev, int peer);
 // Per-chunk flags: each signalled logical migration gets a fresh epoch and its own range of
 // consecutive inbox slots of (sender instance, destination inbox).  Keyed on the inbox's uid
@@ -245,7 +246,9 @@ struct dyna_kv_prepared {
   int dev = 0, sender = 0;
   char* mem = nullptr;             // device: [tile maps][plans][item bases][tables]
   unsigned int* err = nullptr;     // the deferred-error word its kernels write (shared by its launches)
+  bool reshard = false;            // dyna_kv_prepare_reshard: isrc, else src
   dynakv::BatchSource src{};
+  dynakv::InterleavedSource isrc{};
   bool tiles = false;
   int32_t engine = 0, piece = 0, stages = 0, unroll = 0, max_ctas = 0, schedule = 0;
 };

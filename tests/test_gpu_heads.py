@@ -294,3 +294,53 @@ def test_reshard_head_aware_alias_checks():
     with pytest.raises(dk.DynaKVError) as e:          # 1-head and 2-head slices in one launch
         dk.dyna_kv_reshard([(st[0], dt, (0, 1), 0), (dev_table(src2, ts), dt, (0, 2), 2)], (0, s), (0, L), 32)
     assert e.value.status == dk.DYNA_EINVAL
+
+
+@pytest.mark.parametrize("engine", ENGINES, ids=ENGINE_IDS)
+def test_prepared_reshard_launch_and_graph_replay(engine):
+    """dyna_kv_prepare_reshard: a TP 2 -> 8 reshard planned once; launches and CUDA-graph replays move
+    the source rows as they are at that launch (the sources are rewritten in between), bit-exact."""
+    H, L, s, c = 8, 3, 600, 128
+    g = Geom(L, H, 64, 2, 16, 60)
+    gs, gd = g.with_(num_kv_heads=4), g.with_(num_kv_heads=1, block_size=8, num_blocks=120)
+    src = [pool_filled(gs, 200 + r, instance=r) for r in range(2)]
+    dst = [pool_filled(gd, 300 + r) for r in range(8)]
+    ts = [kvgen.table_pair(10 + r, s, gs, gs)[0] for r in range(2)]
+    td = [kvgen.table_pair(20 + r, s, gd, gd)[1] for r in range(8)]
+    plan = dd.tp_reshard_plan(H, 2, 8)
+    st = [dev_table(p, t) for p, t in zip(src, ts)]
+    dt = [dev_table(p, t) for p, t in zip(dst, td)]
+    prep = dk.dyna_kv_prepare_reshard([(st[a], dt[b], heads, hd0) for a, b, heads, hd0 in plan], (0, s), (0, L), c,
+                                      dk.opts(engine=engine))
+    want = [kvgen.fill_bytes(300 + r, gd.pool_bytes) for r in range(8)]
+    stream = torch.cuda.Stream()
+
+    def expect(seed):
+        for a, b, heads, hd0 in plan:
+            oracle.migrate_heads(kvgen.fill_bytes(seed + a, gs.pool_bytes), gs, ts[a], want[b], gd, td[b], (0, s),
+                                 (0, L), heads, hd0)
+        for b in range(8):
+            assert np.array_equal(dst[b].tensor.cpu().numpy(), want[b]), (seed, b)
+
+    def refill(seed):
+        for a in range(2):
+            dk.dyna_kv_debug_fill(src[a].tensor.data_ptr(), src[a].tensor.numel(), seed + a, 0, 0)
+        torch.cuda.synchronize()
+
+    try:
+        for seed in (400, 410):
+            refill(seed)
+            x = dk.dyna_kv_prepared_launch(prep, stream.cuda_stream)
+            assert dk.dyna_kv_xfer_plan(x)["engine"] == (dk.DYNA_ENGINE_TILES if engine == 0 else dk.DYNA_ENGINE_VEC)
+            dk.dyna_kv_wait(x)
+            expect(seed)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            xg = dk.dyna_kv_prepared_launch(prep, stream.cuda_stream)
+        dk.dyna_kv_wait(xg)
+        refill(420)
+        graph.replay()
+        torch.cuda.synchronize()
+        expect(420)
+    finally:
+        dk.dyna_kv_prepared_destroy(prep)
