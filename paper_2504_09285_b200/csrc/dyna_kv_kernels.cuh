@@ -967,15 +967,26 @@ __device__ __forceinline__ TDesc decode_item_tile(const Plan& p, int64_t item, b
   if (ta >= tb) return d;
   d.lk = lkg * p.lkb;
   d.acc = (uint32_t)((tb - ta) * p.row * p.lkb);
-  const int64_t js = ta / p.src.bs, jd = ta / p.dst.bs;
-  const int32_t bsrc = __ldg(p.src.table + js), bdst = __ldg(p.dst.table + jd);
-  if (bsrc < 0 || (int64_t)bsrc >= p.src.nb || bdst < 0 || (int64_t)bdst >= p.dst.nb) {
+  // row coordinate in a side's map: the paged row through the block table, or the chunk-relative
+  // row of a linear side (a tile plan with a linear side has one chunk: a = t0)
+  bool bad = false;
+  auto row_of = [&](const Side& sd) -> int32_t {
+    if (sd.linear) return (int32_t)(ta - a);
+    const int64_t jb = ta / sd.bs;
+    const int32_t blk = __ldg(sd.table + jb);
+    if (blk < 0 || (int64_t)blk >= sd.nb) {
+      bad = true;
+      return 0;
+    }
+    return (int32_t)((int64_t)blk * sd.bs + (ta - jb * sd.bs));
+  };
+  d.ys = row_of(p.src);
+  d.yd = row_of(p.dst);
+  if (bad) {
     if (p.err) atomicOr(p.err, ERR_BAD_BLOCK);
     skipped = true;
     return d;
   }
-  d.ys = (int32_t)((int64_t)bsrc * p.src.bs + (ta - js * p.src.bs));
-  d.yd = (int32_t)((int64_t)bdst * p.dst.bs + (ta - jd * p.dst.bs));
   d.rows = (uint32_t)(tb - ta);
   return d;
 }

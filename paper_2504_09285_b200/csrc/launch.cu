@@ -410,10 +410,13 @@ static int tile_target_bytes() {  // experiment switch DYNA_KV_TILE_BYTES (defau
 
 // One side's map: 4-D (e0 x 8-B elements, e1, row in slab, slab) over the slabs [2*l0, 2*(l0+lm)) of a
 // paged pool, starting at byte `col` of each row; box (e0, e1, rows, lkb).
+// A linear side (one packed chunk [l - l0][kv][t - a][slice], dyna_kv_pack / unpack) is the same
+// lattice with `clen` rows per slab, starting at its base.
 static bool encode_side(CUtensorMap* m, const Side& s, int64_t pitch, int64_t col, int l0, int lm, int64_t slice,
-                        int64_t e0, int64_t rows, int64_t lkb) {
-  const int64_t slab_rows = s.nb * (int64_t)s.bs;
-  char* base = s.base + (int64_t)2 * l0 * slab_rows * pitch + col;
+                        int64_t e0, int64_t rows, int64_t lkb, int64_t clen) {
+  const int64_t slab_rows = s.linear ? clen : s.nb * (int64_t)s.bs;
+  if (s.linear) pitch = slice, col = 0;
+  char* base = s.linear ? s.base : s.base + (int64_t)2 * l0 * slab_rows * pitch + col;
   const cuuint64_t dims[4] = {(cuuint64_t)e0, (cuuint64_t)(slice / (e0 * 8)), (cuuint64_t)slab_rows,
                               (cuuint64_t)(2 * (int64_t)lm)};
   const cuuint64_t strides[3] = {(cuuint64_t)(e0 * 8), (cuuint64_t)pitch, (cuuint64_t)(slab_rows * pitch)};
@@ -429,12 +432,16 @@ static bool encode_side(CUtensorMap* m, const Side& s, int64_t pitch, int64_t co
 // slot, item counts.  False when the geometry does not fit a tensor map or shared memory (the caller
 // then uses the VEC row kernel).
 bool tile_shape(Plan& p) {
-  if (p.src.linear || p.dst.linear || !encode_tiled()) return false;
+  // a linear side holds exactly one chunk (pack / unpack): its rows are chunk-relative
+  if ((p.src.linear && p.dst.linear) || ((p.src.linear || p.dst.linear) && p.nchunks != 1) || !encode_tiled())
+    return false;
   const int64_t slice = p.row, g = p.g;
   if (slice % 16 || p.scol % 16 || p.dcol % 16 || p.spitch % 16 || p.dpitch % 16) return false;
   const int64_t e0 = slice <= 2048 ? slice / 8 : 256;
   if (slice % (e0 * 8) || slice / (e0 * 8) > 256 || g < 1 || g > 256) return false;
-  if (p.src.nb * (int64_t)p.src.bs >= (int64_t(1) << 31) || p.dst.nb * (int64_t)p.dst.bs >= (int64_t(1) << 31))
+  const int64_t lim = int64_t(1) << 31;
+  if ((!p.src.linear && p.src.nb * (int64_t)p.src.bs >= lim) || (!p.dst.linear && p.dst.nb * (int64_t)p.dst.bs >= lim) ||
+      p.t1 - p.t0 >= lim)
     return false;
   const int avail = smem_avail((const void*)k_copy_tiles<true, InterleavedSource, true>);
   // box rows: all g rows of a run when they fit the box target (or at least two ring slots), else the
@@ -470,10 +477,11 @@ bool tile_shape(Plan& p) {
 bool tile_encode(const Plan& p, void* maps) {
   const int64_t slice = p.row, e0 = slice <= 2048 ? slice / 8 : 256;
   CUtensorMap* m = static_cast<CUtensorMap*>(maps);
-  return encode_side(&m[0], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, p.tile_rows, p.lkb) &&
-         encode_side(&m[1], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, p.tile_rows, p.lkb) &&
-         encode_side(&m[2], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, 1, p.lkb) &&
-         encode_side(&m[3], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, 1, p.lkb);
+  const int64_t clen = p.t1 - p.t0;  // linear sides: one chunk
+  return encode_side(&m[0], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, p.tile_rows, p.lkb, clen) &&
+         encode_side(&m[1], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, p.tile_rows, p.lkb, clen) &&
+         encode_side(&m[2], p.src, p.spitch, p.scol, p.l0, p.lm, slice, e0, 1, p.lkb, clen) &&
+         encode_side(&m[3], p.dst, p.dpitch, p.dcol, p.l0, p.lm, slice, e0, 1, p.lkb, clen);
 }
 
 bool tile_plan(Plan& p, void* maps) { return tile_shape(p) && tile_encode(p, maps); }

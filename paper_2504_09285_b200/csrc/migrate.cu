@@ -700,15 +700,46 @@ static dyna_status pack_impl(bool to_buf, dyna_block_table t, dyna_range tr, dyn
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   Choice ch = choose(o, P->row, 0, n, std::min<int64_t>(g.block_size, n) * P->row);
   DeviceGuard guard(P->dev);
+  // Short runs as TMA tiles (the packed side is one chunk: a linear map of its own), as migrations
+  // do; the maps travel with the call (the buffer is the caller's), so not under capture.
+  const int l0 = (int)lr.begin;
+  alignas(64) char maps[kTileMaps * kTileMapBytes];
+  Plan tp{};
+  const bool tiles_asked = o.engine == DYNA_ENGINE_TILES;
+  bool tiles = (tiles_asked || (!o.engine && std::min<int64_t>(g.block_size, n) * P->row < kTileRunMax &&
+                                tiles_enabled())) &&
+               o.schedule != DYNA_SCHED_DYNAMIC && !stream_capturing(stream);
+  if (tiles) {
+    tp = to_buf ? make_plan_sliced(paged(P, nullptr), linear(buf), P->row, P->row, 0, P->row, 0, tr.begin, tr.end, l0,
+                                   (int)lm, n, g.block_size, ch.piece)
+                : make_plan_sliced(linear(buf), paged(P, nullptr), P->row, P->row, 0, P->row, 0, tr.begin, tr.end, l0,
+                                   (int)lm, n, g.block_size, ch.piece);
+    tiles = tile_shape(tp) && tile_encode(tp, maps);
+  }
+  if (tiles_asked && !tiles)
+    return fail(DYNA_ENOTSUP, "DYNA_ENGINE_TILES: rows no tensor map can describe (or the stream is capturing)");
+  if (tiles) {
+    ch.engine = DYNA_ENGINE_TILES;
+    ch.piece = tp.tile_bytes;
+    ch.stages = o.stages ? o.stages : 4;
+  } else if (ch.engine == DYNA_ENGINE_TILES) {
+    ch.engine = DYNA_ENGINE_VEC;
+    ch.unroll = kVecU;
+    if (!o.piece_bytes) ch.piece = kVecPiece;
+  }
   RingLease lease(P->dev);
   const int32_t* ids = t.block_ids;
-  if (!ids) {
+  const char* dmaps = nullptr;
+  if (!ids || tiles) {
     char *base = nullptr, *h = nullptr;
-    const size_t tb = table_upload_bytes(t, tr.end);
-    if ((r = lease.reserve(tb, &base, &h, stream))) return r;
-    std::memcpy(h, t.host_block_ids, tb);
+    const size_t hb = tiles ? sizeof(maps) : 0;  // 512: keeps the table 16-B aligned
+    const size_t tb = ids ? 0 : table_upload_bytes(t, tr.end);
+    if ((r = lease.reserve(hb + tb, &base, &h, stream))) return r;
+    if (tiles) std::memcpy(h, maps, hb);
+    if (!ids) std::memcpy(h + hb, t.host_block_ids, tb);
     if ((r = lease.copy(stream))) return r;
-    ids = reinterpret_cast<const int32_t*>(base);
+    if (!ids) ids = reinterpret_cast<const int32_t*>(base + hb);
+    dmaps = base;
   }
   dyna_kv_xfer* x = nullptr;
   if ((r = new_xfer(P->dev, g.instance, stream, &x))) return r;
@@ -719,12 +750,18 @@ static dyna_status pack_impl(bool to_buf, dyna_block_table t, dyna_range tr, dyn
   x->unroll = ch.engine == DYNA_ENGINE_VEC ? ch.unroll : 0;
   const uint64_t launches0 = g_launches.load();
   // one chunk of n tokens: the linear side's layout is [l - l0][kv][t - t0][row]
-  Plan p = to_buf ? make_plan(paged(P, ids), linear(buf), P->row, tr.begin, tr.end, (int)lr.begin, (int)lm, n,
-                              g.block_size, ch.piece)
-                  : make_plan(linear(buf), paged(P, ids), P->row, tr.begin, tr.end, (int)lr.begin, (int)lm, n,
-                              g.block_size, ch.piece);
+  Plan p = tiles ? tp
+           : to_buf ? make_plan(paged(P, ids), linear(buf), P->row, tr.begin, tr.end, (int)lr.begin, (int)lm, n,
+                                g.block_size, ch.piece)
+                    : make_plan(linear(buf), paged(P, ids), P->row, tr.begin, tr.end, (int)lr.begin, (int)lm, n,
+                                g.block_size, ch.piece);
+  if (tiles) {
+    (to_buf ? p.src : p.dst).table = ids;
+    p.tmaps = dmaps;
+  }
   p.err = x->err;
-  r = launch_copy(p, ch.engine, o.max_ctas, ch.stages, ch.unroll, P->dev, stream, o.schedule);
+  r = tiles ? launch_tiles(p, ch.stages, o.max_ctas, P->dev, stream)
+            : launch_copy(p, ch.engine, o.max_ctas, ch.stages, ch.unroll, P->dev, stream, o.schedule);
   if (!r) r = lease.finish(stream);
   if (r) {
     delete x;

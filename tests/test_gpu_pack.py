@@ -11,7 +11,7 @@ from kvgen import Geom
 from gpu_util import dev_table, pool_filled, pool_from_host, torch_rows_equal
 
 pytestmark = pytest.mark.gpu
-ENGINES = [0, dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK]
+ENGINES = [0, dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK, dk.DYNA_ENGINE_TILES]
 
 
 @pytest.mark.parametrize("engine", ENGINES)
@@ -86,3 +86,21 @@ def test_pack_unpack_full_4prime_shape():
     dk.dyna_kv_wait(x)
     dk.dyna_kv_wait(y)
     assert torch_rows_equal(src, ts, dst, td, (0, 4096), (0, 32))
+
+
+def test_pack_small_rows_run_as_tiles():
+    """AUTO packs / unpacks short contiguous runs (one-head rows) with the tile kernel: the packed
+    chunk is a linear tensor map of its own."""
+    g = Geom(3, 1, 128, 2, 16, 200)
+    ts, td = kvgen.table_pair(7, 3000, g, g)
+    src, dst = pool_filled(g, 1), pool_filled(g, 2)
+    tr, lr = (7, 2900), (0, 3)
+    need = 2 * 3 * (tr[1] - tr[0]) * g.row_bytes
+    buf = torch.zeros(need, dtype=torch.uint8, device="cuda")
+    x = dk.dyna_kv_pack(dev_table(src, ts), tr, lr, buf.data_ptr(), need, 0)
+    assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_TILES
+    dk.dyna_kv_wait(x)
+    y = dk.dyna_kv_unpack(buf.data_ptr(), need, dev_table(dst, td), tr, lr, 0)
+    assert dk.dyna_kv_xfer_plan(y)["engine"] == dk.DYNA_ENGINE_TILES
+    dk.dyna_kv_wait(y)
+    assert torch_rows_equal(src, ts, dst, td, tr, lr)
