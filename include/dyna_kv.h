@@ -595,7 +595,8 @@ DYNA_API int32_t dyna_kv_calib_get(dyna_kv_calib_entry* out, int32_t cap);
  * Candidates, in order (DYNA_CALIB_CANDIDATES): FUSED VEC 4 KiB x U8, FUSED VEC 8 KiB x U4,
  * FUSED VEC 16 KiB x U16, FUSED BULK ring 32 KiB x 4, STAGED VEC 8 KiB x U8, STAGED BULK
  * 32 KiB x 4, FUSED TILES (STAGED is skipped — 0 GB/s — into an imported pool or a destination
- * table without device ids on another GPU; TILES when no tensor map fits the rows).  out[i] receives the entry for chunk_tokens[i]; gbps (NULL or
+ * table without device ids on another GPU; TILES when no tensor map fits the rows, and for
+ * destinations on another GPU or imported).  out[i] receives the entry for chunk_tokens[i]; gbps (NULL or
  * n x DYNA_CALIB_CANDIDATES floats) the payload GB/s of every candidate.  Tables: as
  * dyna_kv_migrate_ex (host ids or DYNA_MIGRATE_UNCHECKED semantics: the destination rows must
  * be distinct); both must cover at least the largest chunk size.  The call OVERWRITES the

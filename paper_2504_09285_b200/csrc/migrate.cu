@@ -1464,6 +1464,9 @@ dyna_status dyna_kv_calibrate(dyna_block_table src, dyna_block_table dst, const 
       const Cand& cd = kCands[k];
       if (gbps) gbps[i * DYNA_CALIB_CANDIDATES + k] = 0.f;
       if (cd.variant == DYNA_VARIANT_STAGED && !staged_ok) continue;
+      // tensor-map stores into peer memory are unmeasured: not a candidate across
+      // GPUs, as AUTO never tiles there either (explicit DYNA_ENGINE_TILES still may)
+      if (cd.engine == DYNA_ENGINE_TILES && peer) continue;
       dyna_kv_opts o{cd.variant, cd.engine, 0, 0, cd.piece, cd.stages, cd.unroll, 0};
       bool skip = false;
       for (int pass = 0; pass < 2 && !r; ++pass) {
