@@ -183,12 +183,16 @@ typedef struct {
  * chunk size).  Entries for the exact row size are preferred over generic
  * ones; within each class the smallest covering max_chunk_tokens wins.  The
  * library starts with the table measured on B200 (profiles/), replaceable at
- * run time.  Measured rules apply on top of the table when the engine is
- * AUTO: a contiguous run (min(gcd(bs_src, bs_dst), chunk_tokens) * row bytes)
- * shorter than 32 KiB with the destination on the source device moves as TMA
- * tensor tiles (DYNA_ENGINE_TILES, with the ring slot as piece_bytes;
- * not under CUDA-graph capture before the library's tile-map cache holds the
- * geometry); otherwise no BULK engine for runs shorter than 16 KiB. */
+ * run time (or measured on the caller's own pools: dyna_kv_calibrate).  An
+ * entry may name DYNA_ENGINE_TILES (the built-in one does for long calls of
+ * small rows).  Measured rules apply on top of the table when the engine is
+ * AUTO: for a row size without an exact entry, a contiguous run
+ * (min(gcd(bs_src, bs_dst), chunk_tokens) * row bytes) shorter than 32 KiB in
+ * a call of at least 1024 tokens with the destination on the source device
+ * moves as TMA tensor tiles (DYNA_ENGINE_TILES, with the ring slot as
+ * piece_bytes); tiles never run under CUDA-graph capture before the library's
+ * tile-map cache holds the geometry; otherwise no BULK engine for runs shorter
+ * than 16 KiB. */
 typedef struct {
     int32_t row_bytes;
     int32_t peer;

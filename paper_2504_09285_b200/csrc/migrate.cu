@@ -126,9 +126,11 @@ dyna_status check_reach(const dyna_kv_pool* S, const dyna_kv_pool* D) {
 // bytes, locality and call size), else FUSED + VEC.
 Choice choose(const dyna_kv_opts& o, int64_t row, int peer, int64_t ntok, int64_t run_bytes) {
   dyna_kv_calib_entry ce{};
+  bool exact = false;
   const bool calibrated =
-      (o.variant == DYNA_VARIANT_AUTO || o.engine == DYNA_ENGINE_AUTO) && calib_lookup(row, peer, ntok, &ce);
+      (o.variant == DYNA_VARIANT_AUTO || o.engine == DYNA_ENGINE_AUTO) && calib_lookup(row, peer, ntok, &ce, &exact);
   Choice c{};
+  c.exact = calibrated && exact;
   c.variant = o.variant ? o.variant : (calibrated && ce.variant ? ce.variant : DYNA_VARIANT_FUSED);
   c.engine = o.engine ? o.engine : (calibrated && ce.engine ? ce.engine : DYNA_ENGINE_VEC);
   const bool use_ce = calibrated && (!o.engine || o.engine == ce.engine);
@@ -321,7 +323,8 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   // runs on one device
   const bool tiles_asked = o.engine == DYNA_ENGINE_TILES;
   const bool tiles_auto = !o.engine && (ch.engine == DYNA_ENGINE_TILES ||
-                                        (!peer_dst && std::min<int64_t>(g, c) * row < kTileRunMax && tiles_enabled()));
+                                        (!ch.exact && !peer_dst && ntok >= kTileMinTokens &&
+                                         std::min<int64_t>(g, c) * row < kTileRunMax && tiles_enabled()));
   bool tiles = (tiles_asked || tiles_auto) && ch.variant == DYNA_VARIANT_FUSED && !board &&
                o.schedule != DYNA_SCHED_DYNAMIC &&
                tile_shape(tp = make_plan_sliced(paged(S, nullptr), paged(D, nullptr), row, row, 0, row, 0, tr.begin,
@@ -706,8 +709,10 @@ static dyna_status pack_impl(bool to_buf, dyna_block_table t, dyna_range tr, dyn
   alignas(64) char maps[kTileMaps * kTileMapBytes];
   Plan tp{};
   const bool tiles_asked = o.engine == DYNA_ENGINE_TILES;
-  bool tiles = (tiles_asked || (!o.engine && std::min<int64_t>(g.block_size, n) * P->row < kTileRunMax &&
-                                tiles_enabled())) &&
+  bool tiles = (tiles_asked || (!o.engine && (ch.engine == DYNA_ENGINE_TILES ||
+                                              (!ch.exact && n >= kTileMinTokens &&
+                                               std::min<int64_t>(g.block_size, n) * P->row < kTileRunMax &&
+                                               tiles_enabled())))) &&
                o.schedule != DYNA_SCHED_DYNAMIC && !stream_capturing(stream);
   if (tiles) {
     tp = to_buf ? make_plan_sliced(paged(P, nullptr), linear(buf), P->row, P->row, 0, P->row, 0, tr.begin, tr.end, l0,
@@ -1167,7 +1172,8 @@ static dyna_status batch_impl(const dyna_kv_migration* migs, int32_t n, dyna_ran
   std::vector<const char*> pair_cached;       // its channel-cached device maps (else uploaded)
   const bool tiles_asked = o.engine == DYNA_ENGINE_TILES;
   bool tiles = (tiles_asked || (!o.engine && (ch.engine == DYNA_ENGINE_TILES ||
-                                              (!peer && run_min < kTileRunMax && tiles_enabled())))) &&
+                                              (!ch.exact && !peer && total_tok >= kTileMinTokens &&
+                                               run_min < kTileRunMax && tiles_enabled())))) &&
                o.schedule != DYNA_SCHED_DYNAMIC;
   if (tiles) {
     std::map<std::pair<const dyna_kv_pool*, const dyna_kv_pool*>, int32_t> pair_idx;

@@ -145,9 +145,10 @@ std::vector<dyna_kv_calib_entry> g_calib(std::begin(kCalibDefault), std::end(kCa
 // Best calibrated entry for (row bytes, locality, call tokens): entries for this
 // exact row size first, generic (row_bytes == 0) ones only if none matches;
 // within a class the smallest max_chunk_tokens that covers the call wins.
-bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out) {
+bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out, bool* exact) {
   std::lock_guard<std::mutex> lk(g_calib_mu);
   for (int pass = 0; pass < 2; ++pass) {
+    if (exact) *exact = pass == 0;
     const dyna_kv_calib_entry* best = nullptr;
     for (const auto& e : g_calib) {
       const bool row_ok = pass == 0 ? e.row_bytes == row : e.row_bytes == 0;

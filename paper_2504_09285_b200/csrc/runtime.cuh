@@ -60,6 +60,8 @@ constexpr int kBulkPiece = 32768;
 constexpr int kBulkStages = 4;
 constexpr int64_t kMinBulkRun = 16384;  // AUTO never picks BULK below this contiguous run length
 constexpr int64_t kTileRunMax = 32768;  // AUTO moves whole rows as TMA tiles below this contiguous run length
+constexpr int64_t kTileMinTokens = 1024;  // ... in calls of at least this many tokens (below, VEC is faster:
+                                          // profiles/r02_calib_native_full.json) when no exact-row entry decides
 constexpr int64_t kStageSlotBytes = 64ll << 20;  // staged variant: bytes per staging slot
 constexpr uint32_t kSchedSlots = 1u << 15;       // dynamic-scheduling counter slots per device
 constexpr size_t kInboxBytes = sizeof(unsigned long long) * DYNA_MAX_INSTANCES * DYNA_MAX_CHUNKS;
@@ -99,7 +101,7 @@ cudaError_t get_event(int dev, cudaEvent_t* ev);
 void put_event(int dev, cudaEvent_t ev);
 bool desc_valid(const dyna_kv_pool_desc* d);
 int64_t gcd64(int64_t a, int64_t b);
-bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out);
+bool calib_lookup(int64_t row, int peer, int64_t c, dyna_kv_calib_entry* out, bool* exact = nullptr);
 void calib_install(int64_t row, int peer, const std::vector<dyna_kv_calib_entry>& es);
 dyna_status zeroed_alloc(void** p, size_t bytes, int dev);  // no legacy-stream synchronisation
 dyna_status upload_sync(int dev, void* dst, const void* src, size_t bytes);  // likewise
@@ -394,6 +396,7 @@ class RingLease {
 
 struct Choice {
   int variant, engine, piece, stages, unroll;
+  bool exact;  // chosen by a calibration entry for this exact row size (not a generic one)
 };
 
 Side paged(const dyna_kv_pool* pool, const int32_t* ids);

@@ -22,10 +22,13 @@ NAMES = ["FUSED VEC 4K U8", "FUSED VEC 8K U4", "FUSED VEC 16K U16", "FUSED BULK 
          "STAGED VEC 8K U8", "STAGED BULK 32K x4", "FUSED TILES"]
 GEOMS = {"Llama-2-7B rows (8 KiB)": kvgen.LLAMA2_7B,
          "Llama-3-8B rows (2 KiB)": kvgen.LLAMA3_8B.with_(num_blocks=4096),
-         "TP-8 shard rows (256 B)": kvgen.QWEN2_72B.with_(num_kv_heads=1, num_blocks=6144)}
+         "TP-8 shard rows (256 B)": kvgen.QWEN2_72B.with_(num_kv_heads=1, num_blocks=6144),
+         "TP-4 shard rows (512 B)": kvgen.LLAMA3_8B.with_(num_kv_heads=2, num_blocks=8192),
+         "TP-2 shard rows (1 KiB)": kvgen.LLAMA3_8B.with_(num_kv_heads=4, num_blocks=8192)}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--chunks", default="64,256,1024,4096")
+ap.add_argument("--only", default="", help="comma-separated geometry name prefixes")
 ap.add_argument("--reps", type=int, default=8)
 ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "calib_native.json"))
 a = ap.parse_args()
@@ -34,6 +37,8 @@ torch.cuda.set_device(0)
 s = torch.cuda.Stream()
 out = []
 for name, g in GEOMS.items():
+    if a.only and not any(name.startswith(x) for x in a.only.split(",")):
+        continue
     src, dst = dk.Pool(g, 0), dk.Pool(g, 0)
     for p, seed in ((src, 1), (dst, 2)):
         dk.dyna_kv_debug_fill(p.tensor.data_ptr(), p.tensor.numel(), seed, 0, 0)

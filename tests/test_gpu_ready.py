@@ -390,7 +390,7 @@ def test_first_use_of_a_channel_during_coupled_wait_does_not_deadlock():
     src, dst = pool_filled(g, 1), pool_filled(g, 2)
     ts, td = kvgen.table_pair(5, 1200, g, g)
     a, b = pool_filled(gs, 3), pool_filled(gs, 4)        # a pair never used before
-    ta, tb = kvgen.table_pair(6, 1200, gs, gs)
+    ta, tb = kvgen.table_pair(6, 3200, gs, gs)
     prod = torch.cuda.Stream()
     side = torch.cuda.Stream()
     board = dk.dyna_kv_ready_create(0, 64)
@@ -403,7 +403,7 @@ def test_first_use_of_a_channel_during_coupled_wait_does_not_deadlock():
     x = dk.dyna_kv_migrate_on_ready(st, dt, (0, 1000), (0, 4), 250, board, epoch,
                                     torch.cuda.default_stream().cuda_stream, dk.opts(max_ctas=8))
     t0 = time.perf_counter()
-    y = dk.dyna_kv_migrate_ex(at, bt, (0, 1000), (0, 3), 250, side.cuda_stream, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL))
+    y = dk.dyna_kv_migrate_ex(at, bt, (0, 3000), (0, 3), 750, side.cuda_stream, dk.opts(flags=dk.DYNA_MIGRATE_SIGNAL))
     issue_s = time.perf_counter() - t0
     for k in range(4):
         dk.dyna_kv_ready_mark(board, k, epoch, prod.cuda_stream)
@@ -411,5 +411,5 @@ def test_first_use_of_a_channel_during_coupled_wait_does_not_deadlock():
     dk.dyna_kv_wait(x)                                   # DYNA_ETIMEDOUT here would mean the fill blocked
     assert issue_s < 4.0, issue_s
     assert torch_rows_equal(src, ts, dst, td, (0, 1000), (0, 4))
-    assert torch_rows_equal(a, ta, b, tb, (0, 1000), (0, 3))
+    assert torch_rows_equal(a, ta, b, tb, (0, 3000), (0, 3))
     dk.dyna_kv_ready_destroy(board)
