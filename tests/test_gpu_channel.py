@@ -102,11 +102,15 @@ def test_push_place_across_processes():
     p = ctx.Process(target=_sender, args=(dk.dyna_kv_channel_export(ch), q))
     p.start()
     assert q.get(timeout=300) == "ready"
-    # place concurrently: the receiver's kernels wait on the device for each slot's full word
-    dt = dev_table(dst, td)
-    x = dk.dyna_kv_place(ch, dt, (0, 3000), (0, 4), 512)
+    # On one GPU the receiver's place kernel is launched only after the sender's push finished:
+    # kernels of two processes that spin on each other's words are not guaranteed to be
+    # co-scheduled on one device (B200_PROFILING: Xid 109 under context switching).  Every slot
+    # is full by then, so place finds each full word already raised; on two GPUs the two
+    # processes run concurrently (test_gpu_peer.py).
     assert q.get(timeout=300) == "ok"
     p.join(timeout=60)
+    dt = dev_table(dst, td)
+    x = dk.dyna_kv_place(ch, dt, (0, 3000), (0, 4), 512)
     dk.dyna_kv_wait(x)
     dk.dyna_kv_channel_destroy(ch)
     assert np.array_equal(dst.tensor.cpu().numpy(), want)
