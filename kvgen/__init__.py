@@ -218,3 +218,22 @@ def allpairs_plan(world: int, g: Geom, n_req: int = 4, seed_base: int = 1000) ->
                                                   blocks_needed(m.req.s, g.block_size))
         res.append(replace(m, dst_table=td))
     return res
+
+
+def compact_plan(plan: list[PairMigration], spare: int = 0):
+    """The same all-pairs plan with every rank's block ids relabelled onto [0, used + spare).
+
+    configs[4]'s pools are 30 GiB per rank and side; sixteen of them do not fit one GPU.  For the
+    one-GPU emulation each rank's used source blocks (and, separately, its used destination
+    blocks) are renumbered in increasing order, so a table keeps its block order and its
+    fragmentation relative to the other requests of that rank; `spare` unused blocks at the end of
+    every pool hold rows no migration may touch.  Returns (plan', src_blocks[rank],
+    dst_blocks[rank]) — the pool sizes to allocate."""
+    ranks = sorted({m.src_rank for m in plan} | {m.dst_rank for m in plan})
+    used_s = {r: np.unique(np.concatenate([m.src_table for m in plan if m.src_rank == r] or [np.zeros(0, np.int32)]))
+              for r in ranks}
+    used_d = {r: np.unique(np.concatenate([m.dst_table for m in plan if m.dst_rank == r] or [np.zeros(0, np.int32)]))
+              for r in ranks}
+    out = [replace(m, src_table=np.searchsorted(used_s[m.src_rank], m.src_table).astype(np.int32),
+                   dst_table=np.searchsorted(used_d[m.dst_rank], m.dst_table).astype(np.int32)) for m in plan]
+    return out, {r: len(used_s[r]) + spare for r in ranks}, {r: len(used_d[r]) + spare for r in ranks}

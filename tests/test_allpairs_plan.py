@@ -27,3 +27,20 @@ def test_plan_is_deterministic_injective_and_balanced_enough():
         pb[(m.src_rank, m.dst_rank)] = pb.get((m.src_rank, m.dst_rank), 0) + m.req.s * tok_bytes
     bound = dd.load_aware_bound_s(pb, 900e9)
     assert bound >= dd.aggregate_bound_s(pb, 8, 900e9) > 0
+
+
+def test_compact_plan_relabels_order_preserving_and_injective():
+    """The one-GPU emulation's relabelling keeps every table's block order, never merges two blocks
+    of a pool, and sizes each pool to its used blocks plus the spare ones."""
+    g = kvgen.QWEN2_72B
+    plan = kvgen.allpairs_plan(4, g)
+    cp, ns, nd = kvgen.compact_plan(plan, spare=3)
+    assert [(m.src_rank, m.dst_rank, m.req) for m in cp] == [(m.src_rank, m.dst_rank, m.req) for m in plan]
+    for r in range(4):
+        for side, n in (("src", ns), ("dst", nd)):
+            orig = np.concatenate([getattr(m, side + "_table") for m in plan if getattr(m, side + "_rank") == r])
+            new = np.concatenate([getattr(m, side + "_table") for m in cp if getattr(m, side + "_rank") == r])
+            assert len(np.unique(new)) == len(new) == len(orig)         # injective
+            assert sorted(new.tolist()) == list(range(n[r] - 3))        # dense onto [0, used)
+            o = np.argsort(orig)
+            assert np.all(np.diff(new[o]) > 0)                          # monotone in the old ids
