@@ -75,6 +75,50 @@ def bytes_at(seed: int, byte_offset: int, nbytes: int) -> np.ndarray:
 
 
 # --------------------------------------------------------------------------
+# Coordinate tags (SURVEY §8d "debug coordinate tag mode"): every 16-B vector of a
+# pool holds its own coordinates, so a misplaced vector names where it came from.
+# --------------------------------------------------------------------------
+TAG_MAGIC = 0xA5
+
+
+def tag_fill(pool_id: int, g: "Geom") -> np.ndarray:
+    """A pool image ([L][2][NB][bs][row]) whose 16-B vector v of row (l, kv, b, slot)
+    holds word0 = A5 | pool_id | l | kv | b and word1 = slot | v (little-endian u64 pair)."""
+    if g.row_bytes % 16:
+        raise ValueError("row bytes must be a multiple of 16")
+    vpr = g.row_bytes // 16
+    n = g.pool_bytes // 16
+    i = np.arange(n, dtype=np.uint64)
+    v = i % np.uint64(vpr)
+    r = i // np.uint64(vpr)
+    slot = r % np.uint64(g.block_size)
+    r //= np.uint64(g.block_size)
+    b = r % np.uint64(g.num_blocks)
+    r //= np.uint64(g.num_blocks)
+    kv = r % np.uint64(2)
+    layer = r // np.uint64(2)
+    out = np.empty((n, 2), dtype=np.uint64)
+    out[:, 0] = ((np.uint64(TAG_MAGIC) << np.uint64(56)) | (np.uint64(pool_id & 0xFF) << np.uint64(48))
+                 | (layer << np.uint64(40)) | (kv << np.uint64(32)) | b)
+    out[:, 1] = (slot << np.uint64(32)) | v
+    return out.view(np.uint8).reshape(-1)
+
+
+def tag_decode(img: np.ndarray) -> dict[str, np.ndarray]:
+    """Per 16-B vector of a tag-filled image: pool, l, kv, block, slot, vec (int64 arrays) and
+    `ok` (the magic byte is intact)."""
+    w = np.ascontiguousarray(img).view(np.uint64).reshape(-1, 2)
+    w0, w1 = w[:, 0], w[:, 1]
+    return {"ok": (w0 >> np.uint64(56)) == TAG_MAGIC,
+            "pool": ((w0 >> np.uint64(48)) & np.uint64(0xFF)).astype(np.int64),
+            "l": ((w0 >> np.uint64(40)) & np.uint64(0xFF)).astype(np.int64),
+            "kv": ((w0 >> np.uint64(32)) & np.uint64(0xFF)).astype(np.int64),
+            "block": (w0 & np.uint64(0xFFFFFFFF)).astype(np.int64),
+            "slot": (w1 >> np.uint64(32)).astype(np.int64),
+            "vec": (w1 & np.uint64(0xFFFFFFFF)).astype(np.int64)}
+
+
+# --------------------------------------------------------------------------
 # Geometry presets (BASELINE.json configs) — shapes only.
 # --------------------------------------------------------------------------
 @dataclass(frozen=True)
