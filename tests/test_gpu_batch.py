@@ -10,7 +10,8 @@ import kvgen
 import oracle
 import paper_2504_09285_b200 as dk
 from kvgen import Geom
-from gpu_util import dev_table, mapped_mask, pool_filled, pool_from_host, torch_rows_equal, untouched_equal
+from gpu_util import (dev_table, mapped_mask, pool_filled, pool_from_host, sampled_rows_match, torch_rows_equal,
+                      untouched_equal)
 
 pytestmark = pytest.mark.gpu
 ENGINES = [dk.DYNA_ENGINE_VEC, dk.DYNA_ENGINE_BULK, dk.DYNA_ENGINE_BULK_WS]
@@ -149,10 +150,15 @@ def test_config3_batch_full_size():
     n0 = dk.dyna_kv_launch_count()
     x = dk.migrate_batch([(dev_table(src, ts), dev_table(dst, td), (0, r.s)) for r, (ts, td) in zip(reqs, tabs)],
                          (0, 32), 256)
+    plan = dk.dyna_kv_xfer_plan(x)
     dk.dyna_kv_wait(x)
     assert dk.dyna_kv_launch_count() - n0 == 1
+    assert (plan["variant"], plan["engine"]) == (dk.DYNA_VARIANT_FUSED, dk.DYNA_ENGINE_BULK)   # bench.py's kernel
+    rng = np.random.default_rng(7)
     for r, (ts, td) in zip(reqs, tabs):
         assert torch_rows_equal(src, ts, dst, td, (0, r.s), (0, 32))
+        # sampled rows against the oracle's offsets and the kvgen stream (independent of torch indexing)
+        assert sampled_rows_match(31, g, ts, dst, g, td, (0, r.s), (0, 32), 8, rng) == 0
     assert untouched_equal(dst, 32, mapped_mask(g, [(td, (0, r.s)) for r, (ts, td) in zip(reqs, tabs)]))
 
 

@@ -260,8 +260,10 @@ def test_config3_llama3_skewed_batch_full_size(engine):
           for r, (ts, td) in zip(reqs, tabs)]
     for x in xs:
         dk.dyna_kv_wait(x)
+    rng = np.random.default_rng(engine)
     for r, (ts, td) in zip(reqs, tabs):
         assert torch_rows_equal(src, ts, dst, td, (0, r.s), (0, 32))
+        assert sampled_rows_match(31, g, ts, dst, g, td, (0, r.s), (0, 32), 4, rng) == 0
     assert untouched_equal(dst, 32, mapped_mask(g, [(td, (0, r.s)) for r, (ts, td) in zip(reqs, tabs)]))
 
 
