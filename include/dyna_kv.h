@@ -158,6 +158,26 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
 #define DYNA_READY_PER_LAYER 2 /* dyna_kv_migrate_on_ready: one ready mark per (chunk, layer), see below */
 #define DYNA_MIGRATE_UNCHECKED 4 /* destination tables may come without host ids: the caller guarantees that
                                     no destination row is written twice or read as a source row (R7) */
+#define DYNA_MIGRATE_OVERLAP_PREV 8 /* the caller guarantees that this call neither reads nor writes memory
+                                    that the kernel enqueued immediately before it on `stream` writes, nor
+                                    writes memory that kernel reads — nor, when that kernel was itself a call
+                                    with this flag, the kernel before it, and so on (a run of flagged calls
+                                    may execute concurrently: it must be mutually independent).  E.g. chunk
+                                    k+1 of a request pushed after chunk k, or another request's migration:
+                                    disjoint destination rows, tables and sources not produced by those
+                                    kernels.  The copy kernel then starts moving
+                                    bytes while that kernel drains (programmatic dependent launch without the
+                                    grid-dependency wait) instead of after it: the ~4-5 us bubble between
+                                    back-to-back migrations disappears.  Stream order is
+                                    otherwise kept: the kernel waits for its predecessor before it touches
+                                    chunk counters / flags and before it exits, so work enqueued after it,
+                                    events, dyna_kv_wait and flags still imply the predecessor's completion.
+                                    Work before the predecessor is ordered as usual (an event the stream waits
+                                    for, e.g. the producer's, is a full dependency).  Applies to FUSED
+                                    migrations, batches, head migrations, reshards, pack / unpack and
+                                    prepared launches; ignored (the launch waits) for the STAGED chain,
+                                    producer-coupled launches and DYNA_SCHED_DYNAMIC.  Violating the promise
+                                    gives unspecified destination bytes, as a data race would. */
 
 typedef struct {
     int32_t variant;    /* DYNA_VARIANT_*  (0 = auto) */

@@ -31,6 +31,7 @@ DYNA_ENGINE_AUTO, DYNA_ENGINE_VEC, DYNA_ENGINE_BULK, DYNA_ENGINE_BULK_WS, DYNA_E
 DYNA_MIGRATE_SIGNAL = 1
 DYNA_READY_PER_LAYER = 2
 DYNA_MIGRATE_UNCHECKED = 4
+DYNA_MIGRATE_OVERLAP_PREV = 8
 DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC = 1, 2
 
 # every symbol include/dyna_kv.h declares

@@ -220,8 +220,12 @@ __device__ __forceinline__ void fence_for(const Plan& p) {
 // Called by ONE thread once an item's bytes are complete and visible at
 // the destination's scope (the caller fenced).  The thread that closes chunk k resets
 // the counter (self-cleaning channel) and releases the flag.
+// wait for the previous grid on the stream to complete, its memory visible (PdlScope below)
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void account_chunk(const Plan& p, int32_t k, unsigned long long n) {
   if (n == 0) return;
+  if (p.overlap_prev & kOverlapCounters) griddep_wait();  // slots still counted by an earlier launch (PdlScope)
   unsigned long long* ctr = p.counters + k;
   const unsigned long long total = chunk_bytes(p, k);
   const unsigned long long now = atomicAdd(ctr, n) + n;
@@ -239,10 +243,31 @@ __device__ __forceinline__ void account_chunk(const Plan& p, int32_t k, unsigned
 // start launching at once, then waits for the previous grid to complete (and
 // its memory to be visible) before touching any global memory.  Without the
 // launch attribute both instructions are no-ops.
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-}
+//
+// DYNA_MIGRATE_OVERLAP_PREV (the caller's promise that this launch neither reads nor writes what
+// the previous kernel on the stream writes, nor writes what it reads): the copies start without
+// that wait, so back-to-back independent migrations do not drain and refill the memory pipeline
+// between launches (measured: the ~4-5 us bubble per launch).  The wait still
+// happens (a) before the first touch of the library's chunk counters and flags when the host saw
+// the launch's slots reserved recently by another launch that may still count them
+// (kOverlapCounters, griddep_wait in account_chunk*), and (b) in CTA 0 before it exits
+// (PdlScope's destructor), so the grid never completes before the previous kernel: work after it
+// on the stream, events and dyna_kv_wait keep plain stream order.  Only CTA 0 holds its SM for
+// that: the other CTAs exit when their copies are done, so the next launch's CTAs take their SMs
+// at once (a per-thread exit wait measured most of the gain away: profiles/r02_overlap_prev_probe).
+
+struct PdlScope {  // no state: CTA 0's exit wait is unconditional (a no-op once the entry wait has run)
+  template <class Src>
+  __device__ __forceinline__ explicit PdlScope(const Src& src) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifndef DYNA_DIAG_PDL_NOWAIT  // diagnostic builds only (A/B of the launch bubble): every launch overlaps
+    if (!src.overlap()) griddep_wait();
+#endif
+  }
+  __device__ __forceinline__ ~PdlScope() {
+    if (blockIdx.x == 0) griddep_wait();
+  }
+};
 
 // ------------------------------------------------------------------ work distribution
 // Static round-robin (ctr == nullptr) or dynamic: workers grab the next item
@@ -285,6 +310,7 @@ struct Sched {
 // instead of a full fence followed by a relaxed add.
 __device__ __forceinline__ void account_chunk_release(const Plan& p, int32_t k, uint32_t n) {
   if (n == 0) return;
+  if (p.overlap_prev & kOverlapCounters) griddep_wait();  // (as account_chunk)
   unsigned long long* ctr = p.counters + k;
   const unsigned long long total = chunk_bytes(p, k);
   unsigned long long old;
@@ -384,7 +410,7 @@ __device__ __forceinline__ void warp_copy_rows(const char* __restrict__ src, cha
 // k_copy_vec; batches carry each item's plan (per-request flags).
 template <int U, bool SIGNAL, class Src>
 __global__ void __launch_bounds__(256, DYNA_LANES_MINB) k_copy_lanes(const Src src) {
-  pdl_enter();
+  PdlScope pdl(src);
   constexpr bool kBatch = std::is_same<Src, BatchSource>::value;
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -436,7 +462,7 @@ __global__ void __launch_bounds__(256, DYNA_LANES_MINB) k_copy_lanes(const Src s
 
 template <int U, bool SIGNAL, class Src, bool READY = false>
 __global__ void __launch_bounds__(256, (U >= 16 || READY) ? 2 : DYNA_VEC_MINB) k_copy_vec(const Src src, unsigned long long* sched_ctr) {
-  pdl_enter();
+  PdlScope pdl(src);
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -667,7 +693,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-  pdl_enter();
+  PdlScope pdl(src);
   const Plan& p = src.locate_signal();  // per-launch fields (piece, signalling)
   const int64_t n_items = src.total();
   if (warp == 1) {  // ---------------- decoder
@@ -832,7 +858,7 @@ __global__ void __launch_bounds__(32 * (kCopiers + 1), 3) k_copy_rows(const Src 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  pdl_enter();
+  PdlScope pdl(src);
   const int64_t n_items = src.total();
   if (warp == 0) {  // ---------------- decoder
     int64_t m = 0;
@@ -1013,7 +1039,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
-  pdl_enter();
+  PdlScope pdl(src);
   const Plan& p = src.locate_signal();  // per-launch fields (box geometry, signalling)
   const int64_t n_items = src.total();
   if (warp == 1) {  // ---------------- decoder

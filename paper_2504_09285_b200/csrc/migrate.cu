@@ -48,13 +48,21 @@ dyna_status record_completion(dyna_kv_xfer* x, int dev, cudaStream_t stream) {
 dyna_status check_opts(const dyna_kv_opts* opts, dyna_kv_opts* o) {
   *o = dyna_kv_opts{};
   if (opts) *o = *opts;
-  if ((o->flags & ~(DYNA_MIGRATE_SIGNAL | DYNA_READY_PER_LAYER | DYNA_MIGRATE_UNCHECKED)) != 0 || o->variant < 0 ||
+  if ((o->flags & ~(DYNA_MIGRATE_SIGNAL | DYNA_READY_PER_LAYER | DYNA_MIGRATE_UNCHECKED | DYNA_MIGRATE_OVERLAP_PREV)) != 0 ||
+      o->variant < 0 ||
       o->variant > 2 || o->engine < 0 || o->engine > DYNA_ENGINE_TILES || o->max_ctas < 0 || o->piece_bytes < 0 ||
       o->piece_bytes % 16 || o->stages < 0 || o->stages == 1 || o->stages > kMaxStages ||
       (o->unroll != 0 && o->unroll != 4 && o->unroll != 8 && o->unroll != 16) || o->schedule < 0 ||
       o->schedule > DYNA_SCHED_DYNAMIC)
     return fail(DYNA_EINVAL, "invalid dyna_kv_opts");
   return DYNA_OK;
+}
+
+// DYNA_MIGRATE_OVERLAP_PREV -> Plan::overlap_prev.  Not for dynamically scheduled launches (their
+// per-launch counter slots are recycled by the previous launch's last CTA), producer-coupled ones
+// (resident waiters) or the staged chain (its kernels depend on each other): those keep the wait.
+static int32_t overlap_of(const dyna_kv_opts& o) {
+  return (o.flags & DYNA_MIGRATE_OVERLAP_PREV) && o.schedule != DYNA_SCHED_DYNAMIC ? 1 : 0;
 }
 
 // Geometry, ranges and table presence; with host ids, the id range checks and the rows for the
@@ -376,6 +384,7 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
       p.tmaps = cached ? cached : dmaps;
     }
     p.err = x->err;
+    p.overlap_prev = board ? 0 : overlap_of(o);
     if (ctx) set_chunking(p, ctx->mig_t0, tr.end, c);
     if (signal) {
       uint64_t epoch = 0;
@@ -396,6 +405,8 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
       p.epoch = x->epoch = epoch;
       x->first_slot = first;
       p.sys_fence = peer_dst;
+      if (p.overlap_prev && (ctx || flag_slots_shared_recently(gs.instance, D, first, nchunks)))
+        p.overlap_prev |= kOverlapCounters;  // (a chunk stream's pushes share one reservation: always wait)
     }
     if (board) {
       p.ready = board->slots;
@@ -630,6 +641,7 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
   x->stages = tiles ? (o.stages ? o.stages : 4) : 0;
   const uint64_t launches0 = g_launches.load();
   p.err = x->err;
+  p.overlap_prev = overlap_of(o);
   if (signal) {
     uint64_t epoch = 0;
     int32_t first = 0;
@@ -643,6 +655,8 @@ dyna_status dyna_kv_migrate_heads(dyna_block_table src, dyna_block_table dst, dy
     p.epoch = x->epoch = epoch;
     x->first_slot = first;
     p.sys_fence = peer_dst;
+    if (p.overlap_prev && flag_slots_shared_recently(gs.instance, D, first, nchunks))
+      p.overlap_prev |= kOverlapCounters;
   }
   r = tiles ? launch_tiles(p, o.stages, o.max_ctas, S->dev, stream) : launch_rows(p, o.max_ctas, S->dev, stream);
   if (!r) r = lease.finish(stream);
@@ -765,6 +779,7 @@ static dyna_status pack_impl(bool to_buf, dyna_block_table t, dyna_range tr, dyn
     p.tmaps = dmaps;
   }
   p.err = x->err;
+  p.overlap_prev = overlap_of(o);
   r = tiles ? launch_tiles(p, ch.stages, o.max_ctas, P->dev, stream)
             : launch_copy(p, ch.engine, o.max_ctas, ch.stages, ch.unroll, P->dev, stream, o.schedule);
   if (!r) r = lease.finish(stream);
@@ -968,6 +983,7 @@ static dyna_status reshard_impl(const dyna_kv_head_migration* migs, int32_t n, d
     plans[i].dst.table = m.dst.block_ids ? m.dst.block_ids : reinterpret_cast<const int32_t*>(dbase + doff[i]);
     if (tiles) plans[i].tmaps = cached[i] ? cached[i] : dbase + (size_t)i * kTileMaps * kTileMapBytes;
     plans[i].err = x->err;
+    plans[i].overlap_prev = overlap_of(o);
     if (signal) {
       const dyna_kv_xfer::BatchEntry& be = x->batch[i];
       unsigned long long* ctr = nullptr;
@@ -979,6 +995,8 @@ static dyna_status reshard_impl(const dyna_kv_head_migration* migs, int32_t n, d
       plans[i].flags = D->inbox + (size_t)S->desc.instance * DYNA_MAX_CHUNKS + be.first_slot;
       plans[i].epoch = be.epoch;
       plans[i].sys_fence = (D->dev != S->dev || D->imported) ? 1 : 0;
+      if (plans[i].overlap_prev && flag_slots_shared_recently(S->desc.instance, D, be.first_slot, nchunks))
+        plans[i].overlap_prev |= kOverlapCounters;
     }
   }
   if (tiles) std::memcpy(h, maps, maps_b);
@@ -1279,6 +1297,7 @@ static dyna_status batch_impl(const dyna_kv_migration* migs, int32_t n, dyna_ran
                            chunk_tokens, g, ch.piece);
     }
     plans[k].err = x->err;
+    plans[k].overlap_prev = overlap_of(o);
     if (signal) {  // entry k's chunk j: counter / inbox slot first_slot + j of its (sender, destination)
       dyna_kv_xfer::BatchEntry& be = x->batch[live[k]];
       unsigned long long* ctr = nullptr;
@@ -1290,6 +1309,8 @@ static dyna_status batch_impl(const dyna_kv_migration* migs, int32_t n, dyna_ran
       plans[k].flags = D->inbox + (size_t)S->desc.instance * DYNA_MAX_CHUNKS + be.first_slot;
       plans[k].epoch = be.epoch;
       plans[k].sys_fence = (D->dev != S->dev || D->imported) ? 1 : 0;
+      if (plans[k].overlap_prev && flag_slots_shared_recently(S->desc.instance, D, be.first_slot, be.nchunks))
+        plans[k].overlap_prev |= kOverlapCounters;
     }
     bases[k] = total_items;
     total_items += plans[k].n_items;

@@ -65,7 +65,12 @@ struct Plan {
                             // boxes of a shorter run at tile_rstride apart, rounded up to 1 KiB
   int32_t tile_rstride;     // smem stride of single-row boxes: row * lkb rounded up to 128 B (TMA alignment)
   int32_t tile_rows;        // rows of a full box: g, or a divisor of g when g rows do not fit (pieces of a run)
+  // DYNA_MIGRATE_OVERLAP_PREV: kOverlapCopy = the launch does not wait for the previous kernel on
+  // its stream before copying (CTA 0 waits before it exits: see PdlScope); kOverlapCounters = its
+  // flag slots were reserved recently by another launch, so it also waits before it touches them
+  int32_t overlap_prev;
 };
+constexpr int32_t kOverlapCopy = 1, kOverlapCounters = 2;
 constexpr int kTileMapBytes = 128;  // sizeof(CUtensorMap)
 constexpr int kTileMaps = 4;        // per plan
 
@@ -86,6 +91,7 @@ struct SingleSource {
   __device__ __forceinline__ int64_t total() const { return p.n_items; }
   __device__ __forceinline__ const Plan& locate(int64_t& item) const { return p; }
   __device__ __forceinline__ const Plan& locate_signal() const { return p; }
+  __device__ __forceinline__ bool overlap() const { return p.overlap_prev != 0; }
 };
 struct BatchSource {
   const Plan* plans;
@@ -103,6 +109,9 @@ struct BatchSource {
     return plans[lo];
   }
   __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }
+  // plans live in library memory written by a copy the launch fully depends on: readable before the
+  // grid-dependency wait
+  __device__ __forceinline__ bool overlap() const { return plans[0].overlap_prev != 0; }
 };
 // n plans with identical item structure (dyna_kv_reshard: one request's head slices between
 // TP ranks), one launch, items entry-major: global item g is item g % per of plan g / per.
@@ -121,6 +130,9 @@ struct InterleavedSource {
     return plans[r];
   }
   __device__ __forceinline__ const Plan& locate_signal() const { return plans[0]; }
+  // plans live in library memory written by a copy the launch fully depends on: readable before the
+  // grid-dependency wait
+  __device__ __forceinline__ bool overlap() const { return plans[0].overlap_prev != 0; }
 };
 
 }  // namespace dynakv

@@ -3,6 +3,7 @@
 // staging, and the test-input fill.  Paper mapping: PAPER.md §3.1 P:352 (instances
 // exchange the required KV blocks).
 #include <chrono>
+#include <deque>
 #include <random>
 
 #include "runtime.cuh"
@@ -301,9 +302,11 @@ dyna_status ensure_peer(int dev, int peer) {
 // Flag rows: per (sender instance, destination inbox uid), the next epoch and the next free
 // slot.  Slots are handed out in consecutive ranges and recycle after DYNA_MAX_CHUNKS chunks;
 // flags are raised with an atomic max, so a late writer never moves a flag backwards.
+constexpr size_t kRecentReservations = 128;
 struct FlagRow {
   uint64_t epoch = 0;
   int64_t cursor = 0;
+  std::deque<std::pair<int64_t, int64_t>> recent;  // (first slot, slots) of the latest reservations
 };
 static std::map<std::pair<int, uint64_t>, FlagRow> g_flag_rows;
 
@@ -331,9 +334,26 @@ dyna_status flag_reserve(int sender, const dyna_kv_pool* dst, int64_t nchunks, u
   FlagRow& fr = it->second;
   if (fr.cursor + nchunks > DYNA_MAX_CHUNKS) fr.cursor = 0;
   *first_slot = (int32_t)fr.cursor;
+  fr.recent.emplace_back(fr.cursor, nchunks);
+  if (fr.recent.size() > kRecentReservations + 1) fr.recent.pop_front();
   fr.cursor += nchunks;
   *epoch = ++fr.epoch;
   return DYNA_OK;
+}
+
+bool flag_slots_shared_recently(int sender, const dyna_kv_pool* dst, int32_t first, int64_t n) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_flag_rows.find(std::make_pair(sender, dst->uid));
+  if (it == g_flag_rows.end()) return true;
+  bool self_skipped = false;
+  for (const auto& rv : it->second.recent) {
+    if (!self_skipped && rv.first == first && rv.second == n) {  // the caller's own reservation
+      self_skipped = true;
+      continue;
+    }
+    if (rv.first < first + n && first < rv.first + rv.second) return true;
+  }
+  return false;
 }
 
 // Zeroed device memory allocated during a call: zeroed on a non-blocking library stream, waited

@@ -243,7 +243,7 @@ def test_per_layer_errors():
                                   dk.opts(flags=dk.DYNA_READY_PER_LAYER))
         assert e.value.status == dk.DYNA_EINVAL
         with pytest.raises(dk.DynaKVError) as e:       # unknown flag bits
-            dk.dyna_kv_migrate_ex(dev_table(src, ts), dev_table(dst, td), (0, 100), (0, 2), 32, 0, dk.opts(flags=8))
+            dk.dyna_kv_migrate_ex(dev_table(src, ts), dev_table(dst, td), (0, 100), (0, 2), 32, 0, dk.opts(flags=16))
         assert e.value.status == dk.DYNA_EINVAL
     finally:
         dk.dyna_kv_ready_destroy(board)
