@@ -770,6 +770,16 @@ def secondary_n1(ctx, src, dst, dtabs, reqs, g, mopts, args):
     ms, _, n = ctx.timed(lambda i: _Multi(per_req(i)), k, 2)
     out["configs2_per_request_calls"] = {"GBps": payload / (ms / k / 1e3) / 1e9, "ms_per_step": ms / k,
                                          "launches_per_step": n // k}
+    # the same calls with DYNA_MIGRATE_OVERLAP_PREV: the requests' rows are disjoint, so each call may
+    # start while the previous one drains
+    ov = dk.opts(engine=args.engine, piece_bytes=args.piece, stages=args.stages, flags=dk.DYNA_MIGRATE_OVERLAP_PREV)
+
+    def per_req_ov(i):
+        return [dk.dyna_kv_migrate_ex(a, b, (0, r.s), (0, 32), C2_CHUNK, cs, ov) for r, (a, b) in zip(reqs, dtabs)]
+
+    ms, _, n = ctx.timed(lambda i: _Multi(per_req_ov(i)), k, 2)
+    out["configs2_per_request_calls_overlap_prev"] = {"GBps": payload / (ms / k / 1e3) / 1e9, "ms_per_step": ms / k,
+                                                      "launches_per_step": n // k}
     # 4' shape, 1-GPU form: 4096-token chunks of the same pools (8 disjoint placements)
     ts, td = kvgen.table_pair(3, 8 * 4096, g.with_(num_blocks=4096), g.with_(num_blocks=4096))
     st, dt = dev_tab(src, ts, ctx.dev), dev_tab(dst, td, ctx.dev)
@@ -781,6 +791,14 @@ def secondary_n1(ctx, src, dst, dtabs, reqs, g, mopts, args):
     ms, _, _ = ctx.timed(t4, 4 * k, 3)
     out["t4prime_1gpu_form"] = {"GBps": 4096 * 2 * 32 * g.row_bytes / (ms / (4 * k) / 1e3) / 1e9,
                                 "ms_per_chunk": ms / (4 * k)}
+
+    def t4_ov(i):
+        j = i % 8
+        return dk.dyna_kv_migrate_ex(st, dt, (j * 4096, (j + 1) * 4096), (0, 32), 4096, cs, ov)
+
+    ms, _, _ = ctx.timed(t4_ov, 4 * k, 3)
+    out["t4prime_1gpu_form_overlap_prev"] = {"GBps": 4096 * 2 * 32 * g.row_bytes / (ms / (4 * k) / 1e3) / 1e9,
+                                             "ms_per_chunk": ms / (4 * k)}
     # configs[1]: Llama-2-7B rows, s = 1024 of 2048, chunk 256 (round 1's bench step)
     g2 = kvgen.LLAMA2_7B
     s2, d2 = dk.Pool(g2, ctx.dev), dk.Pool(g2, ctx.dev)

@@ -25,6 +25,8 @@ import torch  # noqa: E402
 import kvgen  # noqa: E402
 import paper_2504_09285_b200 as dk  # noqa: E402
 
+OV = dk.opts(flags=dk.DYNA_MIGRATE_OVERLAP_PREV)  # the requests / chunks of each set are disjoint
+
 
 def peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -113,6 +115,10 @@ def main():
     ms = run_set(stream, calls, reps=5)
     report(f"configs[2] Llama-3-8B skewed batch ({len(reqs)} migrating of 64, sum s={tot}) c=256",
            tot * 2 * 32 * g.row_bytes, ms, tot, len(calls), "one dyna_kv_migrate per request")
+    calls = [lambda t=t: dk.dyna_kv_migrate_ex(t[0], t[1], (0, t[2]), (0, 32), 256, cs, OV) for t in T]
+    ms = run_set(stream, calls, reps=5)
+    report(f"configs[2] Llama-3-8B skewed batch ({len(reqs)} migrating of 64, sum s={tot}) c=256, OVERLAP_PREV",
+           tot * 2 * 32 * g.row_bytes, ms, tot, len(calls), "one dyna_kv_migrate per request, overlapping each other")
     migs = [(t[0], t[1], (0, t[2])) for t in T]
     ms = run_set(stream, [lambda: dk.dyna_kv_migrate_batch(migs, (0, 32), 256, cs, None)], reps=5)
     report(f"configs[2] Llama-3-8B skewed batch ({len(reqs)} migrating of 64, sum s={tot}) c=256, batched",
@@ -130,6 +136,11 @@ def main():
                  for k in range(32768 // c)]
         ms = run_set(stream, calls, reps=5)
         report(f"configs[3] Llama-3-8B s=32768 per-chunk calls c={c}", payload, ms, 32768, len(calls))
+        calls = [lambda k=k, c=c: dk.dyna_kv_migrate_ex(st, dt, (k * c, (k + 1) * c), (0, 32), c, cs, OV)
+                 for k in range(32768 // c)]
+        ms = run_set(stream, calls, reps=5)
+        report(f"configs[3] Llama-3-8B s=32768 per-chunk calls c={c}, OVERLAP_PREV", payload, ms, 32768, len(calls),
+               "chunks are disjoint: each call starts while the previous drains")
     ms = run_set(stream, [lambda: dk.dyna_kv_migrate_ex(st, dt, (0, 32768), (0, 32), 1024, cs, None)], reps=5)
     report("configs[3] Llama-3-8B s=32768 one call c=1024", payload, ms, 32768, 1)
     # 4' target shape: one 4096-token chunk (here intra-device; the target is 2 GPUs over NVLink)
@@ -137,6 +148,11 @@ def main():
              for k in range(8)]
     ms = run_set(stream, calls, reps=5)
     report("target 4' shape: 4096-token Llama-3-8B chunk (1-GPU form)", payload, ms, 32768, 8,
+           "NVLink form needs 2 GPUs")
+    calls = [lambda k=k: dk.dyna_kv_migrate_ex(st, dt, (k * 4096, (k + 1) * 4096), (0, 32), 4096, cs, OV)
+             for k in range(8)]
+    ms = run_set(stream, calls, reps=5)
+    report("target 4' shape: 4096-token Llama-3-8B chunk (1-GPU form), OVERLAP_PREV", payload, ms, 32768, 8,
            "NVLink form needs 2 GPUs")
     del src, dst
 
@@ -151,6 +167,10 @@ def main():
     ms = run_set(stream, calls, reps=5)
     report(f"configs[4] Qwen2-72B shard, one pair's {len(reqs)} requests (sum s={tot}) c=1024",
            tot * 2 * 80 * g.row_bytes, ms, tot, len(calls), "all-pairs 8-GPU form needs 8 GPUs")
+    calls = [lambda t=t: dk.dyna_kv_migrate_ex(t[0], t[1], (0, t[2]), (0, 80), 1024, cs, OV) for t in T]
+    ms = run_set(stream, calls, reps=5)
+    report(f"configs[4] Qwen2-72B shard, one pair's {len(reqs)} requests (sum s={tot}) c=1024, OVERLAP_PREV",
+           tot * 2 * 80 * g.row_bytes, ms, tot, len(calls), "per-request calls overlapping each other")
     migs = [(t[0], t[1], (0, t[2])) for t in T]
     ms = run_set(stream, [lambda: dk.dyna_kv_migrate_batch(migs, (0, 80), 1024, cs, None)], reps=5)
     report(f"configs[4] Qwen2-72B shard, one pair's {len(reqs)} requests (sum s={tot}) c=1024, batched",
@@ -165,6 +185,10 @@ def main():
     ms = run_set(stream, calls, reps=5)
     report(f"TP-8 Qwen2-72B shard (1 KV head, 256-B rows), {len(reqs)} requests (sum s={tot}) c=1024",
            tot * 2 * 80 * g.row_bytes, ms, tot, len(calls))
+    calls = [lambda t=t: dk.dyna_kv_migrate_ex(t[0], t[1], (0, t[2]), (0, 80), 1024, cs, OV) for t in T]
+    ms = run_set(stream, calls, reps=5)
+    report(f"TP-8 Qwen2-72B shard (1 KV head, 256-B rows), {len(reqs)} requests (sum s={tot}) c=1024, OVERLAP_PREV",
+           tot * 2 * 80 * g.row_bytes, ms, tot, len(calls), "per-request calls overlapping each other")
     migs = [(t[0], t[1], (0, t[2])) for t in T]
     ms = run_set(stream, [lambda: dk.dyna_kv_migrate_batch(migs, (0, 80), 1024, cs, None)], reps=5)
     report(f"TP-8 Qwen2-72B shard (1 KV head, 256-B rows), {len(reqs)} requests (sum s={tot}) c=1024, batched",
