@@ -191,3 +191,30 @@ def test_fuzz_channel():
             assert np.array_equal(dst.tensor.cpu().numpy(), want), (i, heads, tr, c, slots, slot_bytes)
         finally:
             dk.dyna_kv_channel_destroy(ch)
+
+
+@pytest.mark.parametrize("block", range(4 * SCALE))
+def test_fuzz_overlapped_chains(block):
+    """Random chains of DYNA_MIGRATE_OVERLAP_PREV calls: one request cut at random points into
+    consecutive calls (each its own chunk size, variant, engine and flags), all enqueued back to back
+    after a plain first call; the destination equals one oracle migration of the whole range."""
+    rng = np.random.default_rng(kvgen.MASTER_SEED + 1300 + block)
+    for i in range(20):
+        gs, gd, n_tok, (t0, t1), lr, _, _ = _case(rng)
+        ts, td = kvgen.table_pair(int(rng.integers(1 << 30)), n_tok, gs, gd)
+        hs = kvgen.fill_bytes(int(rng.integers(1 << 30)), gs.pool_bytes)
+        hd = kvgen.fill_bytes(int(rng.integers(1 << 30)), gd.pool_bytes)
+        want = hd.copy()
+        oracle.migrate(hs, gs, ts, want, gd, td, (t0, t1), lr)
+        src, dst = pool_from_host(gs, hs, instance=int(rng.integers(0, 8))), pool_from_host(gd, hd)
+        st, dt = dev_table(src, ts), dev_table(dst, td)
+        cuts = sorted(set([t0, t1] + [int(x) for x in rng.integers(t0, t1 + 1, int(rng.integers(0, 6)))]))
+        xs = []
+        for j, (a, b) in enumerate(zip(cuts[:-1], cuts[1:])):
+            kw = _case(rng)[6]
+            kw["flags"] |= dk.DYNA_MIGRATE_OVERLAP_PREV if j else 0
+            xs.append(dk.migrate(st, dt, (a, b), lr, int(rng.choice([1, 7, 16, 64, 300])), **kw))
+        for x in xs:
+            dk.dyna_kv_wait(x)
+        assert np.array_equal(src.tensor.cpu().numpy(), hs), (i, gs, gd, cuts, lr)
+        assert np.array_equal(dst.tensor.cpu().numpy(), want), (i, gs, gd, cuts, lr)
