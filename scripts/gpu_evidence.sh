@@ -12,7 +12,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_copy_ring -s 20 -c 1 -o gpurun_out/prof_e0 \
     python bench.py --steps 20 --warmup 5 --quick --no-cpu-baseline > /dev/null 2>&1; ls gpurun_out/prof_e0*
 timeout 900 python scripts/configs_sweep.py > gpurun_out/configs.log 2>&1; tail -3 gpurun_out/configs.log
-bash scripts/sanitize.sh
 nvcc -O2 -o /tmp/latency_probe scripts/native/latency_probe.c -I include -L paper_2504_09285_b200 -ldyna_kv \
     -Xlinker -rpath=$PWD/paper_2504_09285_b200 && timeout 300 /tmp/latency_probe > gpurun_out/latency_probe.jsonl; cat gpurun_out/latency_probe.jsonl
 timeout 1500 python scripts/overlap.py --chunks 512,1024,4096 --budgets 0,16 --layers --out gpurun_out/overlap.json 2>&1 | tail -4

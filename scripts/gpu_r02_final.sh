@@ -11,5 +11,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_copy_ring -s 20 -c 1 -o gpurun_out/prof_e0 \
     python bench.py --steps 20 --warmup 5 --quick --no-cpu-baseline > /dev/null 2>&1; ls gpurun_out/prof_e0*
 timeout 900 python scripts/configs_sweep.py > gpurun_out/configs.log 2>&1; tail -3 gpurun_out/configs.log
-bash scripts/sanitize.sh
 DYNA_FUZZ_SCALE=10 timeout 1500 python -m pytest tests/test_gpu_fuzz.py -q -p no:cacheprovider > gpurun_out/fuzz_x10.log 2>&1; tail -2 gpurun_out/fuzz_x10.log

@@ -1,4 +1,6 @@
 # compute-sanitizer on small configs (memcheck, racecheck, synccheck); summaries in gpurun_out/sanitizer_*.log
+# NOTE: compute-sanitizer has since been closed on this pool (runs under it left GPUs needing a reset);
+# the round-1 / round-2 logs in profiles/ come from earlier boxes.  Not part of the evidence scripts.
 for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool --error-exitcode 99 --print-limit 20 \
       python -m pytest tests/test_gpu_parity.py tests/test_gpu_heads.py tests/test_gpu_ready.py tests/test_gpu_batch.py \
