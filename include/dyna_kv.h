@@ -176,7 +176,10 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
                                     for, e.g. the producer's, is a full dependency).  Applies to FUSED
                                     migrations, batches, head migrations, reshards, pack / unpack and
                                     prepared launches; ignored (the launch waits) for the STAGED chain,
-                                    producer-coupled launches and DYNA_SCHED_DYNAMIC.  Violating the promise
+                                    producer-coupled launches and DYNA_SCHED_DYNAMIC.  With the AUTO
+                                    engine a same-device migration with this flag runs on the VEC
+                                    engine (measured best for overlapped calls; 8-KiB rows from 4096
+                                    tokens keep the table's ring).  Violating the promise
                                     gives unspecified destination bytes, as a data race would. */
 
 typedef struct {

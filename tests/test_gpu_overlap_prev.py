@@ -168,3 +168,20 @@ def test_overlap_flag_ignored_where_it_cannot_apply():
         for x in xs:
             dk.dyna_kv_wait(x)
         assert np.array_equal(dst.tensor.cpu().numpy(), want), kw
+
+
+def test_auto_picks_vec_for_overlapped_calls():
+    """AUTO's rule for overlapped calls (measured): the VEC engine — 8 KiB x U4 for
+    2-KiB rows, 4 KiB x U8 below — except 8-KiB rows from 4096 tokens, which keep the ring."""
+    for g, n, want in ((Geom(2, 8, 128, 2, 16, 300), 1024, (dk.DYNA_ENGINE_VEC, 8192)),
+                       (Geom(2, 1, 128, 2, 16, 300), 2048, (dk.DYNA_ENGINE_VEC, 4096)),
+                       (Geom(2, 32, 128, 2, 16, 300), 4096, (dk.DYNA_ENGINE_BULK, 32768))):
+        src, dst = pool_filled(g, 1), pool_filled(g, 2)
+        ts, td = kvgen.table_pair(3, n, g, g)
+        st, dt = dev_table(src, ts), dev_table(dst, td)
+        torch.cuda.synchronize()
+        x = dk.migrate(st, dt, (0, n), (0, 2), n, flags=OV)
+        plan = dk.dyna_kv_xfer_plan(x)
+        dk.dyna_kv_wait(x)
+        assert (plan["engine"], plan["piece_bytes"]) == want, (g, plan)
+        assert torch_rows_equal(src, ts, dst, td, (0, n), (0, 2))
