@@ -194,8 +194,11 @@ typedef struct {
     int32_t schedule;   /* work distribution: 0 = default (static), DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC */
 } dyna_kv_opts;
 #define DYNA_SCHED_STATIC  1   /* round-robin items over a balanced persistent grid */
-#define DYNA_SCHED_DYNAMIC 2   /* workers grab items from a per-launch atomic counter (measured slower than
-                                  static on B200; VEC only, kept as an option) */
+#define DYNA_SCHED_DYNAMIC 2   /* workers grab items from a per-launch atomic counter: the BULK ring's decoder
+                                  warp grabs up to 32 consecutive items per atomic, fewer towards the end
+                                  (guided), and is the default (0) for ring launches of >= 24 items per SM
+                                  outside graph capture (measured +1-3%); the VEC engine grabs per item
+                                  (measured slower than static; kept as an option) */
 
 /* Calibration table used by DYNA_VARIANT_AUTO / DYNA_ENGINE_AUTO (SURVEY §8 a6:
  * "chosen over the staged variant per chunk size by measured bandwidth").

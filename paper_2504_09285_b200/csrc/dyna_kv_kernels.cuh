@@ -669,7 +669,8 @@ struct Desc {
 constexpr int kQ = 4;  // descriptor batches in flight (32 items each)
 
 template <bool SIGNAL, class Src, bool ACC = false>
-__global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int stages, int lag) {
+__global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int stages, int lag,
+                                                              unsigned long long* sched) {
   extern __shared__ __align__(128) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ __align__(8) uint64_t qfull[kQ], qempty[kQ];
@@ -698,11 +699,31 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
   const int64_t n_items = src.total();
   if (warp == 1) {  // ---------------- decoder
     int64_t m = 0;
+    int64_t seen = 0;  // dynamic: the counter as last observed (guides the grab size)
     for (int64_t b = 0;; ++b) {
       const int qb = (int)(b % kQ);
       if (b >= kQ) mbar_wait(&qempty[qb], (uint32_t)(((b / kQ) - 1) & 1));
-      const int64_t gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
-      m += 32;
+      int64_t gi;
+      bool last;
+      if (sched) {
+        // dynamic (guided) grabs: up to 32 consecutive items per atomic while plenty remain, fewer
+        // towards the end so the CTAs finish together even when SMs run at different rates
+        unsigned long long base = 0, grab = 0;
+        if (lane == 0) {
+          const int64_t rem = n_items - seen;
+          grab = (unsigned long long)max((int64_t)1, min((int64_t)32, rem / (4 * (int64_t)gridDim.x)));
+          base = atomicAdd(sched, grab);
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        grab = __shfl_sync(0xffffffffu, grab, 0);
+        seen = (int64_t)(base + grab);
+        gi = (unsigned long long)lane < grab ? (int64_t)base + lane : n_items;
+        last = seen >= n_items;  // the counter has passed the end: every later grab is empty
+      } else {
+        gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
+        m += 32;
+        last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
+      }
       Item it{nullptr, nullptr, 0u, 0u, 0, 0};
       const Plan* ipl = nullptr;
       if (gi < n_items) {
@@ -714,13 +735,20 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
       }
       const unsigned mask = __ballot_sync(0xffffffffu, it.n != 0);
       if (it.n) q[qb][__popc(mask & ((1u << lane) - 1u))] = Desc{it.src, it.dst, ipl, it.n, it.k};
-      const bool last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
       if (lane == 0) {
         qcount[qb] = __popc(mask);
         qlast[qb] = last ? 1 : 0;
       }
       mbar_arrive(&qfull[qb]);  // every lane releases its own descriptor write (CTA scope)
-      if (last) return;
+      if (last) {
+        if (sched && lane == 0 && atomicAdd(sched + 1, 1ull) == gridDim.x - 1) {
+          // the last CTA past the end resets the launch's counter slot (every grab of this launch is done:
+          // each CTA counted itself only after its final grab returned)
+          sched[0] = 0ull;
+          sched[1] = 0ull;
+        }
+        return;
+      }
     }
   }
   if (ACC && warp == 2) {  // ---------------- accountant

@@ -255,7 +255,7 @@ int smem_avail(const void* kern) {
 // measured); DYNA_KV_ACCOUNTANT=0 makes the issuer count with a release RMW.
 template <bool SIG, class Src>
 dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, int64_t max_grid, int sms,
-                        cudaStream_t st) {
+                        cudaStream_t st, unsigned long long* sched) {
   static const bool acc_on = [] {
     const char* e = std::getenv("DYNA_KV_ACCOUNTANT");
     return !(e && e[0] == '0');
@@ -265,7 +265,7 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
     return e ? std::atoi(e) : 0;
   }();
   const bool acc = SIG && acc_on;
-  void (*kring)(const Src, int, int) = acc ? k_copy_ring<SIG, Src, true> : k_copy_ring<SIG, Src>;
+  void (*kring)(const Src, int, int, unsigned long long*) = acc ? k_copy_ring<SIG, Src, true> : k_copy_ring<SIG, Src>;
   const int threads = acc ? 96 : 64;
   // a ring deeper than the shared memory holds is cut to the stages that fit (at least 2)
   const int avail = smem_avail((const void*)kring);
@@ -279,9 +279,11 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
   if (max_grid > 0) cap = std::min<int64_t>(cap, max_grid);
   const unsigned grid = (unsigned)balanced_workers(n_items, cap);
   const int lag = lag_env > 0 ? std::min(lag_env, std::max(1, stages - 2)) : (stages >= 4 ? 2 : 1);
-  CUDA_TRY(launch_kernel(kring, grid, threads, smem, st, src, stages, lag));
+  CUDA_TRY(launch_kernel(kring, grid, threads, smem, st, src, stages, lag, sched));
   return DYNA_OK;
 }
+
+constexpr int64_t kRingDynMinItemsPerSm = 24;
 
 // Launch one copy kernel over `src` (n_items items; piece bytes per item).
 // engine: DYNA_ENGINE_VEC / BULK.  SIG: per-chunk signalling (single plan only).
@@ -293,10 +295,21 @@ dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int
     return fail(DYNA_ERANGE, "%lld work items in one launch (item math is 32-bit); use a larger piece or split the range",
                 (long long)n_items);
   DevInfo* di = dev_info(dev);
+  const bool ring = engine == DYNA_ENGINE_BULK || engine == DYNA_ENGINE_BULK_WS;
+  if (ring && schedule == 0 && n_items >= kRingDynMinItemsPerSm * (int64_t)di->sms) {
+    // The ring takes guided dynamic grabs by default from ~24 items per SM: static round-robin gives
+    // every CTA the same bytes, so SMs that run slower finish last (measured: dynamic +1-3% from 4096
+    // items, e.g. the configs[2] batch 1.006 -> 1.019 of the copy peak; below, the first atomic's latency
+    // costs more than the tail it saves: profiles/r02_dyn_threshold.jsonl).  Not under graph capture: a
+    // captured slot would be shared by concurrent replays.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone)
+      schedule = DYNA_SCHED_DYNAMIC;
+  }
   unsigned long long* sc = sched_slot(di, schedule);
-  if (engine == DYNA_ENGINE_BULK || engine == DYNA_ENGINE_BULK_WS) {
-    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st)
-                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st);
+  if (ring) {
+    dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st, sc)
+                        : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st, sc);
     if (r) return r;
   } else if (unroll == 4) {
     sig ? launch_vec<4, true>(src, n_items, max_ctas, di->sms, st, sc)

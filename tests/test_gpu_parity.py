@@ -483,3 +483,26 @@ def test_explicit_tiles_engine_refusals():
     assert dk.dyna_kv_xfer_plan(x)["engine"] == dk.DYNA_ENGINE_TILES
     dk.dyna_kv_wait(x)
     assert torch_rows_equal(src, ts, dst, td, (0, 100), (0, 2))
+
+
+@pytest.mark.parametrize("signal", [False, True])
+def test_default_ring_guided_dynamic_large_call(signal):
+    """A ring call of >= 24 items per SM takes guided dynamic grabs by default (16000 items here):
+    every row lands, every chunk flag reaches its epoch, and back-to-back launches reuse counter slots."""
+    g = kvgen.Geom(8, 8, 128, 2, 16, 1100)
+    src, dst = pool_filled(g, 61), pool_filled(g, 62)
+    ts, td = kvgen.table_pair(12, 17000, g, g)
+    st, dt = dev_table(src, ts), dev_table(dst, td)
+    flags = dk.DYNA_MIGRATE_SIGNAL if signal else 0
+    xs = [dk.migrate(st, dt, (a, a + 16000), (0, 8), 1000, engine=dk.DYNA_ENGINE_BULK, flags=flags) for a in (0, 500, 7)]
+    infos = [dk.dyna_kv_xfer_info(x) for x in xs]
+    for x in xs:
+        dk.dyna_kv_wait(x)
+    assert torch_rows_equal(src, ts, dst, td, (0, 16500), (0, 8))
+    assert untouched_equal(dst, 62, mapped_mask(g, [(td, (0, 16500))]))
+    if signal:
+        for epoch, nck, sender, first in infos:
+            fl = torch.zeros(nck, dtype=torch.int64).pin_memory()
+            dk.dyna_kv_copy_flags(dst.handle, sender, first, nck, fl.data_ptr(), 0)
+            torch.cuda.synchronize()
+            assert nck == 16 and (fl.numpy() == epoch).all()
