@@ -85,8 +85,11 @@ Plan make_plan(const Side& s, const Side& d, int64_t row, int64_t t0, int64_t t1
   p.lm = lm;
   p.c = (int32_t)c;
   p.g = (int32_t)g;
-  const bool aligned = (t0 % g == 0) && (c % g == 0);
-  p.R = aligned ? (int32_t)(c / g) : (int32_t)((c - 1) / g + 2);
+  // runs per chunk: sized by the chunk length, or by the range when the whole range is one shorter chunk
+  // (a 141-token request in 1024-token chunks would otherwise leave ~86% of its item slots empty)
+  const int64_t ce = std::max<int64_t>(1, std::min<int64_t>(c, t1 - t0));
+  const bool aligned = (t0 % g == 0) && (ce % g == 0);
+  p.R = aligned ? (int32_t)(ce / g) : (int32_t)((ce - 1) / g + 2);
   const int64_t run_max = std::min(g, c) * row;
   p.piece = piece;
   p.P = (int32_t)((run_max + piece - 1) / piece);
@@ -284,6 +287,10 @@ dyna_status launch_bulk(const Src& src, int64_t n_items, int piece, int stages, 
 }
 
 constexpr int64_t kRingDynMinItemsPerSm = 24;
+// bytes a launch moves: the item space is sized per chunk (runs x pieces of a full chunk), so short
+// ranges leave most items empty — the dynamic-grab threshold counts real bytes
+static int64_t payload_of(const SingleSource& s) { return (s.p.t1 - s.p.t0) * s.p.lm * 2 * s.p.row; }
+static int64_t payload_of(const BatchSource& s) { return s.payload; }
 
 // Launch one copy kernel over `src` (n_items items; piece bytes per item).
 // engine: DYNA_ENGINE_VEC / BULK.  SIG: per-chunk signalling (single plan only).
@@ -296,12 +303,20 @@ dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int
                 (long long)n_items);
   DevInfo* di = dev_info(dev);
   const bool ring = engine == DYNA_ENGINE_BULK || engine == DYNA_ENGINE_BULK_WS;
-  if (ring && schedule == 0 && n_items >= kRingDynMinItemsPerSm * (int64_t)di->sms) {
-    // The ring takes guided dynamic grabs by default from ~24 items per SM: static round-robin gives
+  static const int64_t dyn_min = [] {  // experiment switch DYNA_KV_RING_DYN: items per SM (0 = never dynamic)
+    const char* e = std::getenv("DYNA_KV_RING_DYN");
+    return e ? (int64_t)std::atoll(e) : kRingDynMinItemsPerSm;
+  }();
+  const int64_t payload = payload_of(src);
+  if (ring && schedule == 0 && dyn_min > 0 && payload >= dyn_min * (int64_t)di->sms * piece &&
+      n_items * piece <= payload + payload / 4) {
+    // The ring takes guided dynamic grabs by default from ~24 pieces per SM: static round-robin gives
     // every CTA the same bytes, so SMs that run slower finish last (measured: dynamic +1-3% from 4096
     // items, e.g. the configs[2] batch 1.006 -> 1.019 of the copy peak; below, the first atomic's latency
-    // costs more than the tail it saves: profiles/r02_dyn_threshold.jsonl).  Not under graph capture: a
-    // captured slot would be shared by concurrent replays.
+    // costs more than the tail it saves: profiles/r02_dyn_threshold.jsonl).  Not when more than a
+    // fifth of the item slots are empty (a short last chunk: grabs would walk empty slots at the end,
+    // where the tail is decided), nor under graph capture (a captured slot would be shared by
+    // concurrent replays).
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone)
       schedule = DYNA_SCHED_DYNAMIC;

@@ -1348,8 +1348,10 @@ static dyna_status batch_impl(const dyna_kv_migration* migs, int32_t n, dyna_ran
     delete x;
     return r;
   }
+  int64_t payload = 0;
+  for (size_t k = 0; k < m; ++k) payload += (plans[k].t1 - plans[k].t0) * plans[k].lm * 2 * plans[k].row;
   BatchSource bsrc{reinterpret_cast<const Plan*>(dbase + maps_b), reinterpret_cast<const int64_t*>(dbase + plans_b),
-                   (int32_t)m, total_items};
+                   (int32_t)m, total_items, payload};
   x->variant = DYNA_VARIANT_FUSED;
   x->engine = ch.engine;
   x->piece = ch.piece;

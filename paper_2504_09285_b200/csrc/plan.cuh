@@ -98,6 +98,7 @@ struct BatchSource {
   const int64_t* base;  // base[r] = first global item of plan r; nondecreasing
   int32_t n;
   int64_t total_items;
+  int64_t payload;      // bytes the batch moves (host-side launch decisions; item slots can be empty)
   __device__ __forceinline__ int64_t total() const { return total_items; }
   __device__ __forceinline__ const Plan& locate(int64_t& item) const {
     int lo = 0, hi = n - 1;  // the last r with base[r] <= item
