@@ -53,6 +53,9 @@ import paper_2504_09285_b200 as dk  # noqa: E402
 N_GEMM = 128   # 4 per layer: ~= the dense prefill FLOPs of Llama-3-8B per chunk (2 * ~7e9 * c)
 
 
+OV = dk.DYNA_MIGRATE_OVERLAP_PREV
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--s", type=int, default=32768)
@@ -108,7 +111,7 @@ def main():
                                                            mig.cuda_stream,
                                                            dk.opts(max_ctas=budget or args.ready_ctas, flags=fl)))
         for k in range(nck):
-            if mode in ("layered", "ready_layers"):
+            if mode in ("layered", "ready_layers", "layered_ov"):
                 for l in range(g.num_layers):
                     with torch.cuda.stream(prod):
                         producer_layer(X)
@@ -119,7 +122,7 @@ def main():
                         ev.record(prod)
                         mig.wait_event(ev)
                         handles.append(dk.migrate(st, dt, (k * c, min((k + 1) * c, s)), (l, l + 1), c, stream=mig,
-                                                  max_ctas=budget))
+                                                  max_ctas=budget, flags=OV if mode == "layered_ov" else 0))
                 continue
             with torch.cuda.stream(prod):
                 producer_chunk(X)
@@ -133,12 +136,13 @@ def main():
                 e_tail = torch.cuda.Event(enable_timing=True)
                 e_tail.record(mig2)
                 mig.wait_event(e_tail)
-            if mode == "chunked":    # chunk k complete -> push it now
+            if mode in ("chunked", "chunked_ov"):    # chunk k complete -> push it now
                 ev = torch.cuda.Event()
                 ev.record(prod)
                 mig.wait_event(ev)
+                # chunked_ov: DYNA_MIGRATE_OVERLAP_PREV — push k may start while push k-1 drains (disjoint rows)
                 handles.append(dk.migrate(st, dt, (k * c, min((k + 1) * c, s)), (0, 32), c, stream=mig,
-                                          max_ctas=budget))
+                                          max_ctas=budget, flags=OV if mode == "chunked_ov" else 0))
         e_prod.record(prod)
         if mode == "whole":                           # no chunking: push everything after the prefill
             mig.wait_event(e_prod)
@@ -163,21 +167,25 @@ def main():
         t_mig = a0.elapsed_time(a1)
         prod_alone = statistics.median(run(c, "none", 0)[0] for _ in range(args.reps))
         for budget in [int(x) for x in args.budgets.split(",")]:
-            W_, C_, R_, LY, RL, RT = [], [], [], [], [], []
+            W_, C_, R_, LY, RL, RT, CO, LO = [], [], [], [], [], [], [], []
             run(c, "whole", budget)
             run(c, "chunked", budget)   # warm
+            run(c, "chunked_ov", budget)
             run(c, "ready", budget)
             run(c, "ready_tail", budget)
             if args.layers:
                 run(c, "layered", budget)
+                run(c, "layered_ov", budget)
                 run(c, "ready_layers", budget)
             for _ in range(args.reps):  # interleaved so drift hits all modes alike
                 W_.append(run(c, "whole", budget))
                 C_.append(run(c, "chunked", budget))
+                CO.append(run(c, "chunked_ov", budget))
                 R_.append(run(c, "ready", budget))
                 RT.append(run(c, "ready_tail", budget))
                 if args.layers:
                     LY.append(run(c, "layered", budget))
+                    LO.append(run(c, "layered_ov", budget))
                     RL.append(run(c, "ready_layers", budget))
             exp_w = statistics.median(e for _, e in W_)
             exp_c = statistics.median(e for _, e in C_)
@@ -198,8 +206,13 @@ def main():
             r["ready_tail"] = {"ctas": budget or args.ready_ctas, "exposed_ms": exp_t, "T_prod_ms": prod_t,
                                "producer_slowdown": prod_t / prod_alone - 1,
                                "reduction": 1 - exp_t / exp_w if exp_w > 0 else None}
+            exp_o = statistics.median(e for _, e in CO)
+            prod_o = statistics.median(p for p, _ in CO)
+            r["chunked_overlap_prev"] = {"exposed_ms": exp_o, "T_prod_ms": prod_o,
+                                         "producer_slowdown": prod_o / prod_alone - 1,
+                                         "reduction": 1 - exp_o / exp_w if exp_w > 0 else None}
             if args.layers:
-                for name, runs in (("layered", LY), ("ready_layers", RL)):
+                for name, runs in (("layered", LY), ("layered_overlap_prev", LO), ("ready_layers", RL)):
                     exp_l = statistics.median(e for _, e in runs)
                     prod_l = statistics.median(p for p, _ in runs)
                     r[name] = {"exposed_ms": exp_l, "T_prod_ms": prod_l, "producer_slowdown": prod_l / prod_alone - 1,
