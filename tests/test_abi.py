@@ -88,6 +88,19 @@ def test_status_constants_match_header():
         assert getattr(dk, name) == int(val), name
 
 
+def test_flag_engine_variant_schedule_constants_match_header():
+    """Every DYNA_MIGRATE_* / DYNA_READY_* flag, engine, variant and schedule the header defines has the
+    same value in the binding (a flag added to one side only would silently change meaning)."""
+    import paper_2504_09285_b200 as dk
+    src = open(HEADER).read()
+    found = re.findall(r"#define (DYNA_(?:MIGRATE|READY|ENGINE|VARIANT|SCHED)_\w+)\s+(\d+)", src)
+    assert len(found) >= 14 and ("DYNA_MIGRATE_OVERLAP_PREV", "8") in found
+    for name, val in found:
+        assert getattr(dk, name) == int(val), name
+    flags = [int(v) for n, v in found if n.startswith(("DYNA_MIGRATE_", "DYNA_READY_"))]
+    assert all(f & (f - 1) == 0 for f in flags) and len(set(flags)) == len(flags)   # distinct single bits
+
+
 def test_host_validation_without_gpu():
     import paper_2504_09285_b200 as dk
     bad = dk.dyna_kv_pool_desc(2, 2, 64, 2, 16, 64, 0, 0)
