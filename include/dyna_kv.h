@@ -177,9 +177,9 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
                                     migrations, batches, head migrations, reshards, pack / unpack and
                                     prepared launches; ignored (the launch waits) for the STAGED chain,
                                     producer-coupled launches and DYNA_SCHED_DYNAMIC.  With the AUTO
-                                    engine a same-device migration with this flag runs on the VEC
-                                    engine (measured best for overlapped calls; 8-KiB rows from 4096
-                                    tokens keep the table's ring).  Violating the promise
+                                    engine a same-device migration with this flag and no max_ctas runs
+                                    on the VEC engine (measured best for overlapped calls; 8-KiB rows from
+                                    4096 tokens keep the table's ring).  Violating the promise
                                     gives unspecified destination bytes, as a data race would. */
 
 typedef struct {

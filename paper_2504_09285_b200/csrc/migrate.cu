@@ -314,12 +314,14 @@ static dyna_status migrate_impl(dyna_block_table src, dyna_block_table dst, dyna
   const int64_t c = chunk_tokens;
   const int peer_dst = (D->dev != S->dev || D->imported) ? 1 : 0;
   Choice ch = choose(o, row, peer_dst, ntok, std::min<int64_t>(gcd64(gs.block_size, gd.block_size), c) * row);
-  if ((o.flags & DYNA_MIGRATE_OVERLAP_PREV) && !o.engine && !peer_dst && !board && o.schedule != DYNA_SCHED_DYNAMIC &&
-      ch.variant == DYNA_VARIANT_FUSED && !(row >= 8192 && ntok >= 4096)) {
+  if ((o.flags & DYNA_MIGRATE_OVERLAP_PREV) && !o.engine && !o.max_ctas && !peer_dst && !board &&
+      o.schedule != DYNA_SCHED_DYNAMIC && ch.variant == DYNA_VARIANT_FUSED && !(row >= 8192 && ntok >= 4096)) {
     // Overlapped calls: the VEC engine (two shared-memory-free CTAs per SM, so the next call's CTAs
     // share an SM with this call's tail; per-warp chunk counts) beats the ring / tiles, signalled or
     // not (profiles/r02_ov_shapes.jsonl: 2-KiB rows, 256-token signalled calls 0.67 -> 0.97 of the copy
-    // peak); 8-KiB rows from 4096 tokens keep the table's ring (1.02 vs 0.96-1.00)
+    // peak); 8-KiB rows from 4096 tokens keep the table's ring (1.02 vs 0.96-1.00), and so do calls
+    // under an SM budget (max_ctas: a few ring CTAs keep more bytes in flight than a few VEC CTAs,
+    // profiles/r02_overlap_b.json)
     ch.engine = DYNA_ENGINE_VEC;
     ch.exact = true;  // a measured choice: no tile rule on top
     if (!o.piece_bytes) ch.piece = row < 2048 ? 4096 : 8192;
