@@ -668,6 +668,41 @@ struct Desc {
 };
 constexpr int kQ = 4;  // descriptor batches in flight (32 items each)
 
+// The decoder warp's next 32 item indices (gi per lane; n_items = none).  Static: round-robin over the
+// grid.  Dynamic (sched != nullptr, a per-launch counter slot): guided grabs — lane 0 takes up to 32
+// consecutive items per atomic while plenty remain, fewer towards the end, so the CTAs finish together
+// even when SMs run at different rates.  Returns true once this CTA has no items left (warp-uniform).
+__device__ __forceinline__ bool next_items(unsigned long long* sched, int64_t n_items, int64_t& m, int64_t& seen,
+                                           int lane, int64_t& gi) {
+  if (sched) {
+    unsigned long long base = 0, grab = 0;
+    if (lane == 0) {
+      const int64_t rem = n_items - seen;
+      grab = (unsigned long long)max((int64_t)1, min((int64_t)32, rem / (4 * (int64_t)gridDim.x)));
+      base = atomicAdd(sched, grab);
+    }
+    base = __shfl_sync(0xffffffffu, base, 0);
+    grab = __shfl_sync(0xffffffffu, grab, 0);
+    seen = (int64_t)(base + grab);
+    gi = (unsigned long long)lane < grab ? (int64_t)base + lane : n_items;
+    return seen >= n_items;  // the counter has passed the end: every later grab is empty
+  }
+  gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
+  m += 32;
+  return blockIdx.x + m * (int64_t)gridDim.x >= n_items;
+}
+
+// A decoder done with its grabs counts its CTA out; the last CTA past the end resets the launch's
+// counter slot (every grab of the launch has returned by then: a CTA counts itself only after its
+// final grab).
+__device__ __forceinline__ void release_grabs(unsigned long long* sched, int lane) {
+  if (sched && lane == 0 && atomicAdd(sched + 1, 1ull) == gridDim.x - 1) {
+    sched[0] = 0ull;
+    sched[1] = 0ull;
+  }
+}
+
+
 template <bool SIGNAL, class Src, bool ACC = false>
 __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int stages, int lag,
                                                               unsigned long long* sched) {
@@ -704,26 +739,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
       const int qb = (int)(b % kQ);
       if (b >= kQ) mbar_wait(&qempty[qb], (uint32_t)(((b / kQ) - 1) & 1));
       int64_t gi;
-      bool last;
-      if (sched) {
-        // dynamic (guided) grabs: up to 32 consecutive items per atomic while plenty remain, fewer
-        // towards the end so the CTAs finish together even when SMs run at different rates
-        unsigned long long base = 0, grab = 0;
-        if (lane == 0) {
-          const int64_t rem = n_items - seen;
-          grab = (unsigned long long)max((int64_t)1, min((int64_t)32, rem / (4 * (int64_t)gridDim.x)));
-          base = atomicAdd(sched, grab);
-        }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        grab = __shfl_sync(0xffffffffu, grab, 0);
-        seen = (int64_t)(base + grab);
-        gi = (unsigned long long)lane < grab ? (int64_t)base + lane : n_items;
-        last = seen >= n_items;  // the counter has passed the end: every later grab is empty
-      } else {
-        gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
-        m += 32;
-        last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
-      }
+      const bool last = next_items(sched, n_items, m, seen, lane, gi);
       Item it{nullptr, nullptr, 0u, 0u, 0, 0};
       const Plan* ipl = nullptr;
       if (gi < n_items) {
@@ -741,12 +757,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_ring(const Src src, int 
       }
       mbar_arrive(&qfull[qb]);  // every lane releases its own descriptor write (CTA scope)
       if (last) {
-        if (sched && lane == 0 && atomicAdd(sched + 1, 1ull) == gridDim.x - 1) {
-          // the last CTA past the end resets the launch's counter slot (every grab of this launch is done:
-          // each CTA counted itself only after its final grab returned)
-          sched[0] = 0ull;
-          sched[1] = 0ull;
-        }
+        release_grabs(sched, lane);
         return;
       }
     }
@@ -1046,7 +1057,8 @@ __device__ __forceinline__ TDesc decode_item_tile(const Plan& p, int64_t item, b
 }
 
 template <bool SIGNAL, class Src, bool ACC = false>
-__global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int stages, int lag) {
+__global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int stages, int lag,
+                                                               unsigned long long* sched) {
   extern __shared__ __align__(1024) unsigned char ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ __align__(8) uint64_t qfull[kQ], qempty[kQ];
@@ -1071,12 +1083,12 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
   const Plan& p = src.locate_signal();  // per-launch fields (box geometry, signalling)
   const int64_t n_items = src.total();
   if (warp == 1) {  // ---------------- decoder
-    int64_t m = 0;
+    int64_t m = 0, seen = 0;
     for (int64_t b = 0;; ++b) {
       const int qb = (int)(b % kQ);
       if (b >= kQ) mbar_wait(&qempty[qb], (uint32_t)(((b / kQ) - 1) & 1));
-      const int64_t gi = blockIdx.x + (m + lane) * (int64_t)gridDim.x;
-      m += 32;
+      int64_t gi;
+      const bool last = next_items(sched, n_items, m, seen, lane, gi);
       TDesc d{nullptr, nullptr, 0, 0, 0, 0u, 0u, 0};
       if (gi < n_items) {
         int64_t item = gi;
@@ -1088,13 +1100,15 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
       }
       const unsigned mask = __ballot_sync(0xffffffffu, d.rows != 0);
       if (d.rows) q[qb][__popc(mask & ((1u << lane) - 1u))] = d;
-      const bool last = blockIdx.x + m * (int64_t)gridDim.x >= n_items;  // warp-uniform
       if (lane == 0) {
         qcount[qb] = __popc(mask);
         qlast[qb] = last ? 1 : 0;
       }
       mbar_arrive(&qfull[qb]);  // every lane releases its own descriptor write (CTA scope)
-      if (last) return;
+      if (last) {
+        release_grabs(sched, lane);
+        return;
+      }
     }
   }
   if (ACC && warp == 2) {  // ---------------- accountant

@@ -291,6 +291,22 @@ constexpr int64_t kRingDynMinItemsPerSm = 24;
 // ranges leave most items empty — the dynamic-grab threshold counts real bytes
 static int64_t payload_of(const SingleSource& s) { return (s.p.t1 - s.p.t0) * s.p.lm * 2 * s.p.row; }
 static int64_t payload_of(const BatchSource& s) { return s.payload; }
+static int64_t payload_of(const InterleavedSource& s) { return s.payload; }
+
+// Guided dynamic grabs for a TMA-issuer launch (ring or tiles): from kRingDynMinItemsPerSm pieces per
+// SM of real bytes, when at most a fifth of the item slots are empty, outside graph capture.
+static unsigned long long* ring_dyn_slot(DevInfo* di, int64_t payload, int64_t n_items, int64_t piece,
+                                         cudaStream_t st) {
+  static const int64_t dyn_min = [] {  // experiment switch DYNA_KV_RING_DYN: pieces per SM (0 = never dynamic)
+    const char* e = std::getenv("DYNA_KV_RING_DYN");
+    return e ? (int64_t)std::atoll(e) : kRingDynMinItemsPerSm;
+  }();
+  if (dyn_min <= 0 || payload < dyn_min * (int64_t)di->sms * piece || n_items * piece > payload + payload / 4)
+    return nullptr;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return nullptr;
+  return sched_slot(di, DYNA_SCHED_DYNAMIC);
+}
 
 // Launch one copy kernel over `src` (n_items items; piece bytes per item).
 // engine: DYNA_ENGINE_VEC / BULK.  SIG: per-chunk signalling (single plan only).
@@ -303,25 +319,15 @@ dyna_status launch_src(const Src& src, int64_t n_items, bool sig, int piece, int
                 (long long)n_items);
   DevInfo* di = dev_info(dev);
   const bool ring = engine == DYNA_ENGINE_BULK || engine == DYNA_ENGINE_BULK_WS;
-  static const int64_t dyn_min = [] {  // experiment switch DYNA_KV_RING_DYN: items per SM (0 = never dynamic)
-    const char* e = std::getenv("DYNA_KV_RING_DYN");
-    return e ? (int64_t)std::atoll(e) : kRingDynMinItemsPerSm;
-  }();
-  const int64_t payload = payload_of(src);
-  if (ring && schedule == 0 && dyn_min > 0 && payload >= dyn_min * (int64_t)di->sms * piece &&
-      n_items * piece <= payload + payload / 4) {
-    // The ring takes guided dynamic grabs by default from ~24 pieces per SM: static round-robin gives
-    // every CTA the same bytes, so SMs that run slower finish last (measured: dynamic +1-3% from 4096
-    // items, e.g. the configs[2] batch 1.006 -> 1.019 of the copy peak; below, the first atomic's latency
-    // costs more than the tail it saves: profiles/r02_dyn_threshold.jsonl).  Not when more than a
-    // fifth of the item slots are empty (a short last chunk: grabs would walk empty slots at the end,
-    // where the tail is decided), nor under graph capture (a captured slot would be shared by
-    // concurrent replays).
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone)
-      schedule = DYNA_SCHED_DYNAMIC;
-  }
-  unsigned long long* sc = sched_slot(di, schedule);
+  // The ring takes guided dynamic grabs by default from ~24 pieces per SM: static round-robin gives
+  // every CTA the same bytes, so SMs that run slower finish last (measured: dynamic +1-3% from 4096
+  // items, e.g. the configs[2] batch 1.006 -> 1.019 of the copy peak; below, the first atomic's latency
+  // costs more than the tail it saves: profiles/r02_dyn_threshold.jsonl).  Not when more than a
+  // fifth of the item slots are empty (a short last chunk: grabs would walk empty slots at the end,
+  // where the tail is decided), nor under graph capture (a captured slot would be shared by
+  // concurrent replays).
+  unsigned long long* dyn = ring && schedule == 0 ? ring_dyn_slot(di, payload_of(src), n_items, piece, st) : nullptr;
+  unsigned long long* sc = dyn ? dyn : sched_slot(di, schedule);
   if (ring) {
     dyna_status r = sig ? launch_bulk<true>(src, n_items, piece, stages, max_ctas, di->sms, st, sc)
                         : launch_bulk<false>(src, n_items, piece, stages, max_ctas, di->sms, st, sc);
@@ -518,7 +524,8 @@ template <bool SIG, class Src>
 dyna_status launch_tiles_t(const Src& src, int64_t n_items, int tile_bytes, int stages, int max_ctas, int dev,
                            cudaStream_t st) {
   DevInfo* di = dev_info(dev);
-  void (*kern)(const Src, int, int) = SIG ? k_copy_tiles<SIG, Src, true> : k_copy_tiles<SIG, Src, false>;
+  void (*kern)(const Src, int, int, unsigned long long*) = SIG ? k_copy_tiles<SIG, Src, true>
+                                                               : k_copy_tiles<SIG, Src, false>;
   const int threads = SIG ? 96 : 64;
   if (stages <= 0) stages = 4;
   stages = std::min(stages, kMaxStages);
@@ -533,7 +540,8 @@ dyna_status launch_tiles_t(const Src& src, int64_t n_items, int tile_bytes, int 
   if (max_ctas > 0) cap = std::min<int64_t>(cap, max_ctas);
   const unsigned grid = (unsigned)balanced_workers(n_items, cap);
   const int lag = stages >= 4 ? 2 : 1;
-  CUDA_TRY(launch_kernel(kern, grid, threads, smem, st, src, stages, lag));
+  unsigned long long* dyn = ring_dyn_slot(di, payload_of(src), n_items, tile_bytes, st);  // (as the ring)
+  CUDA_TRY(launch_kernel(kern, grid, threads, smem, st, src, stages, lag, dyn));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DYNA_OK;
 }

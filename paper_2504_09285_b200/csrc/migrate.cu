@@ -1027,7 +1027,9 @@ static dyna_status reshard_impl(const dyna_kv_head_migration* migs, int32_t n, d
     delete x;
     return r;
   }
-  InterleavedSource isrc{reinterpret_cast<const Plan*>(dbase + maps_b), n, plans[0].n_items * n};
+  int64_t payload = 0;
+  for (int32_t i = 0; i < n; ++i) payload += (plans[i].t1 - plans[i].t0) * plans[i].lm * 2 * plans[i].row;
+  InterleavedSource isrc{reinterpret_cast<const Plan*>(dbase + maps_b), n, plans[0].n_items * n, payload};
   x->variant = DYNA_VARIANT_FUSED;
   x->engine = tiles ? DYNA_ENGINE_TILES : DYNA_ENGINE_VEC;
   x->piece = tiles ? plans[0].tile_bytes : piece;

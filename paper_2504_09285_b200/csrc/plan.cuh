@@ -123,6 +123,7 @@ struct InterleavedSource {
   const Plan* plans;
   int32_t n;
   int64_t total_items;
+  int64_t payload;      // bytes the launch moves (host-side launch decisions)
   __device__ __forceinline__ int64_t total() const { return total_items; }
   __device__ __forceinline__ const Plan& locate(int64_t& item) const {
     const int64_t per = total_items / n;
