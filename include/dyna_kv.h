@@ -194,9 +194,10 @@ typedef struct {
     int32_t schedule;   /* work distribution: 0 = default (static), DYNA_SCHED_STATIC, DYNA_SCHED_DYNAMIC */
 } dyna_kv_opts;
 #define DYNA_SCHED_STATIC  1   /* round-robin items over a balanced persistent grid */
-#define DYNA_SCHED_DYNAMIC 2   /* workers grab items from a per-launch atomic counter: the BULK ring's decoder
-                                  warp grabs up to 32 consecutive items per atomic, fewer towards the end
-                                  (guided), and is the default (0) for ring launches of >= 24 items per SM
+#define DYNA_SCHED_DYNAMIC 2   /* workers grab items from a per-launch atomic counter: the decoder warp of the
+                                  BULK ring and of the tile kernel grabs up to 32 consecutive items per atomic,
+                                  fewer towards the end (guided) — the default (0) for those launches from 24
+                                  pieces per SM of payload with at most a fifth of the item slots empty,
                                   outside graph capture (measured +1-3%); the VEC engine grabs per item
                                   (measured slower than static; kept as an option) */
 

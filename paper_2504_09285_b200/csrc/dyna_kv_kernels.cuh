@@ -1059,7 +1059,7 @@ __device__ __forceinline__ TDesc decode_item_tile(const Plan& p, int64_t item, b
 template <bool SIGNAL, class Src, bool ACC = false>
 __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int stages, int lag,
                                                                unsigned long long* sched) {
-  extern __shared__ __align__(1024) unsigned char ring[];
+  extern __shared__ __align__(1024) unsigned char tile_ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages];
   __shared__ __align__(8) uint64_t qfull[kQ], qempty[kQ];
   __shared__ __align__(8) TDesc q[kQ][32];
@@ -1161,7 +1161,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
                      : "memory");
       fenced = d.tm;
     }
-    unsigned char* sl = ring + (size_t)s * slot;
+    unsigned char* sl = tile_ring + (size_t)s * slot;
     mbar_expect_tx(&full[s], d.rows * row_box);
     if (d.rows == g) {
       tma_load_4d(sl, d.tm, d.ys, d.lk, &full[s]);
@@ -1200,7 +1200,7 @@ __global__ void __launch_bounds__(ACC ? 96 : 64) k_copy_tiles(const Src src, int
       cur_acc = 0;
     }
     mbar_wait(&full[s], (uint32_t)((iter / stages) & 1));
-    const unsigned char* sl = ring + (size_t)s * slot;
+    const unsigned char* sl = tile_ring + (size_t)s * slot;
     if (d.rows == g) {
       tma_store_4d(d.tm + kTileMapBytes, sl, d.yd, d.lk);
     } else {
