@@ -506,3 +506,48 @@ def test_default_ring_guided_dynamic_large_call(signal):
             dk.dyna_kv_copy_flags(dst.handle, sender, first, nck, fl.data_ptr(), 0)
             torch.cuda.synchronize()
             assert nck == 16 and (fl.numpy() == epoch).all()
+
+
+_FORCED_DYN = r"""
+import sys
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import numpy as np, kvgen, oracle, paper_2504_09285_b200 as dk
+from kvgen import Geom
+from gpu_util import dev_table, pool_from_host
+rng = np.random.default_rng(5)
+bad = 0
+for i in range(24):
+    H = int(rng.choice([1, 2, 8])); bss = int(rng.choice([4, 16])); bsd = int(rng.choice([8, 16, 32]))
+    g_s, g_d = Geom(3, H, 128, 2, bss, 900 // bss + 4), Geom(3, H, 128, 2, bsd, 900 // bsd + 4)
+    ts, td = kvgen.table_pair(int(rng.integers(1 << 30)), 900, g_s, g_d)
+    hs, hd = kvgen.fill_bytes(i + 1, g_s.pool_bytes), kvgen.fill_bytes(i + 100, g_d.pool_bytes)
+    t0 = int(rng.integers(0, 300)); t1 = int(rng.integers(t0 + 1, 901)); c = int(rng.choice([17, 100, 512]))
+    want = hd.copy(); oracle.migrate(hs, g_s, ts, want, g_d, td, (t0, t1))
+    src, dst = pool_from_host(g_s, hs), pool_from_host(g_d, hd)
+    engine = int(rng.choice([dk.DYNA_ENGINE_BULK, dk.DYNA_ENGINE_TILES]))
+    flags = int(rng.choice([0, dk.DYNA_MIGRATE_SIGNAL]))
+    try:
+        x = dk.migrate(dev_table(src, ts), dev_table(dst, td), (t0, t1), (0, 3), c, engine=engine, flags=flags)
+    except dk.DynaKVError as e:
+        if e.status == dk.DYNA_ENOTSUP:
+            continue
+        raise
+    dk.dyna_kv_wait(x)
+    bad += int(not np.array_equal(dst.tensor.cpu().numpy(), want))
+print("BAD", bad)
+"""
+
+
+def test_dynamic_grabs_forced_on_small_launches():
+    """DYNA_KV_RING_DYN=1 makes nearly every ring / tile launch take guided dynamic grabs (normally only
+    launches of >= 24 pieces per SM do): random small migrations on both engines, plain and signalled,
+    stay bit-exact against the oracle (a fresh process: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DYNA_KV_RING_DYN="1")
+    r = subprocess.run([sys.executable, "-c", _FORCED_DYN.format(root=root, tests=os.path.join(root, "tests"))],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().splitlines()[-1] == "BAD 0", r.stdout[-2000:]
