@@ -169,14 +169,16 @@ typedef struct { int64_t begin, end; } dyna_range;  /* half-open [begin, end) */
                                     bytes while that kernel drains (programmatic dependent launch without the
                                     grid-dependency wait) instead of after it: the ~4-5 us bubble between
                                     back-to-back migrations disappears.  Stream order is
-                                    otherwise kept: the kernel waits for its predecessor before it touches
-                                    chunk counters / flags and before it exits, so work enqueued after it,
-                                    events, dyna_kv_wait and flags still imply the predecessor's completion.
+                                    otherwise kept: one CTA of the kernel waits for its predecessor before
+                                    the grid can complete (and every thread does before touching chunk
+                                    counters whose slots another launch reserved recently), so work
+                                    enqueued after it, events, dyna_kv_wait and flags still imply the
+                                    predecessor's completion.
                                     Work before the predecessor is ordered as usual (an event the stream waits
                                     for, e.g. the producer's, is a full dependency).  Applies to FUSED
                                     migrations, batches, head migrations, reshards, pack / unpack and
                                     prepared launches; ignored (the launch waits) for the STAGED chain,
-                                    producer-coupled launches and DYNA_SCHED_DYNAMIC.  With the AUTO
+                                    producer-coupled launches and an explicit DYNA_SCHED_DYNAMIC.  With the AUTO
                                     engine a same-device migration with this flag and no max_ctas runs
                                     on the VEC engine (measured best for overlapped calls; 8-KiB rows from
                                     4096 tokens keep the table's ring).  Violating the promise
