@@ -29,7 +29,8 @@
  *
  * API map:
  *   pools            dyna_kv_pool_bytes / _create / _destroy, _export / _import (CUDA IPC)
- *   the push         dyna_kv_migrate / _ex (variant, engine, SM budget, per-chunk flags)
+ *   the push         dyna_kv_migrate / _ex (variant, engine, SM budget, per-chunk flags,
+ *                    overlap with the previous independent call)
  *   completion       dyna_kv_wait / _query / _stream_wait, _xfer_info, _stream_wait_chunk,
  *                    _copy_flags, _xfer_plan, _poll_error
  *   many requests    dyna_kv_migrate_batch (+ _batch_info for per-request flags)
