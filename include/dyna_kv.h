@@ -201,8 +201,10 @@ typedef struct {
                                   BULK ring and of the tile kernel grabs up to 32 consecutive items per atomic,
                                   fewer towards the end (guided) — the default (0) for those launches from 24
                                   pieces per SM of payload with at most a fifth of the item slots empty,
-                                  outside graph capture (measured +1-3%); the VEC engine grabs per item
-                                  (measured slower than static; kept as an option) */
+                                  outside graph capture (measured +1-3%).  Asked for explicitly on the VEC
+                                  engine, each warp grabs up to 32 items per atomic the same way: faster
+                                  than static on long single calls (one 4-GiB call 0.93 -> 1.01 of the copy
+                                  peak), slower on short or overlapped ones — an option, not a default */
 
 /* Calibration table used by DYNA_VARIANT_AUTO / DYNA_ENGINE_AUTO (SURVEY §8 a6:
  * "chosen over the staged variant per chunk size by measured bandwidth").

@@ -409,7 +409,7 @@ __device__ __forceinline__ void warp_copy_rows(const char* __restrict__ src, cha
 // other with the fields broadcast by shuffles.  Same per-(warp, chunk) signalling as
 // k_copy_vec; batches carry each item's plan (per-request flags).
 template <int U, bool SIGNAL, class Src>
-__global__ void __launch_bounds__(256, DYNA_LANES_MINB) k_copy_lanes(const Src src) {
+__global__ void __launch_bounds__(256, DYNA_LANES_MINB) k_copy_lanes(const Src src, unsigned long long* sched) {
   PdlScope pdl(src);
   constexpr bool kBatch = std::is_same<Src, BatchSource>::value;
   const int lane = threadIdx.x & 31;
@@ -419,8 +419,31 @@ __global__ void __launch_bounds__(256, DYNA_LANES_MINB) k_copy_lanes(const Src s
   int32_t cur_k = -1;
   const Plan* cur_p = nullptr;
   unsigned long long cur_acc = 0;
-  for (int64_t m = 0; warp + m * nwarps < n_items; m += 32) {
-    const int64_t gi = warp + (m + lane) * nwarps;
+  int64_t m = 0, seen = 0, dbase = 0;
+  for (;;) {
+    // this round's items: static = every nwarps-th item from warp + m*nwarps; dynamic (sched, a
+    // per-launch counter slot) = a guided grab of up to 32 consecutive items by lane 0
+    int64_t gi;
+    int cnt;
+    if (sched) {
+      unsigned long long b = 0, grab = 0;
+      if (lane == 0) {
+        grab = (unsigned long long)max((int64_t)1, min((int64_t)32, (n_items - seen) / (4 * nwarps)));
+        b = atomicAdd(sched, grab);
+      }
+      b = __shfl_sync(0xffffffffu, b, 0);
+      grab = __shfl_sync(0xffffffffu, grab, 0);
+      seen = (int64_t)(b + grab);
+      if ((int64_t)b >= n_items) break;
+      dbase = (int64_t)b;
+      cnt = (int)min((int64_t)grab, n_items - dbase);
+      gi = lane < cnt ? dbase + lane : n_items;
+    } else {
+      if (warp + m * nwarps >= n_items) break;
+      cnt = (int)min((int64_t)32, (n_items - 1 - warp) / nwarps - m + 1);
+      gi = warp + (m + lane) * nwarps;
+      m += 32;
+    }
     Item mine{nullptr, nullptr, 0u, 0u, 0, 0};
     const Plan* mp = nullptr;
     if (gi < n_items) {
@@ -429,7 +452,7 @@ __global__ void __launch_bounds__(256, DYNA_LANES_MINB) k_copy_lanes(const Src s
       if (kBatch) mp = &ip;
       mine = decode_item(ip, item);
     }
-    for (int j = 0; j < 32 && warp + (m + j) * nwarps < n_items; ++j) {
+    for (int j = 0; j < cnt; ++j) {
       const char* isrc = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, (unsigned long long)mine.src, j));
       char* idst = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, (unsigned long long)mine.dst, j));
       const uint32_t n = __shfl_sync(0xffffffffu, mine.n, j);
@@ -457,6 +480,11 @@ __global__ void __launch_bounds__(256, DYNA_LANES_MINB) k_copy_lanes(const Src s
     fence_for(cp);
     __syncwarp();
     if (lane == 0) account_chunk(cp, cur_k, cur_acc);
+  }
+  // dynamic: the last warp past the end resets the launch's counter slot
+  if (sched && lane == 0 && atomicAdd(sched + 1, 1ull) == (unsigned long long)nwarps - 1) {
+    sched[0] = 0ull;
+    sched[1] = 0ull;
   }
 }
 

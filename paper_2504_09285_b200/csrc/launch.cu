@@ -217,10 +217,14 @@ bool lanes_enabled() {
   return on;
 }
 
+// sched: a dynamic-scheduling counter slot (DYNA_SCHED_DYNAMIC) or nullptr.  k_copy_lanes grabs up to 32
+// consecutive items per warp and atomic (guided, like the ring's decoder: one 4-GiB call 0.93 -> 1.01 of
+// the copy peak; it loses on short and on overlapped calls, so it is an option, not a default:
+// profiles/r02_lanes_dynamic.jsonl); k_copy_vec (DYNA_KV_LANES=0) grabs one item at a time.
 template <int U, bool SIG, class Src>
 void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cudaStream_t st,
                 unsigned long long* sched) {
-  const bool lanes = !sched && lanes_enabled();
+  const bool lanes = lanes_enabled();
   const int occ = vec_occupancy(lanes ? (const void*)k_copy_lanes<U, SIG, Src>
                                       : (const void*)k_copy_vec<U, SIG, Src, false>);
   constexpr int wpc = kVecThreads / 32;  // warps per CTA
@@ -229,7 +233,7 @@ void launch_vec(const Src& src, int64_t n_items, int64_t max_grid, int sms, cuda
   const int64_t warps = balanced_workers(n_items, max_ctas * wpc);
   const int64_t grid = (warps + wpc - 1) / wpc;
   if (lanes)
-    launch_kernel(k_copy_lanes<U, SIG, Src>, (unsigned)grid, kVecThreads, 0, st, src);
+    launch_kernel(k_copy_lanes<U, SIG, Src>, (unsigned)grid, kVecThreads, 0, st, src, sched);
   else
     launch_kernel(k_copy_vec<U, SIG, Src, false>, (unsigned)grid, kVecThreads, 0, st, src, sched);
 }
