@@ -154,7 +154,25 @@ def main():
     ms = run_set(stream, calls, reps=5)
     report("target 4' shape: 4096-token Llama-3-8B chunk (1-GPU form), OVERLAP_PREV", payload, ms, 32768, 8,
            "NVLink form needs 2 GPUs")
-    del src, dst
+    # the push's halves and the staged variant on the 4' shape (SURVEY 8a a2 / a3 / a4, 1-GPU form):
+    # K1 pack (paged -> contiguous buffer), K3 unpack (buffer -> paged), and STAGED K1 -> K2 -> K3
+    chunk_bytes = 4096 * 2 * 32 * g.row_bytes
+    buf = torch.empty(chunk_bytes, dtype=torch.uint8, device="cuda")
+    calls = [lambda k=k: dk.dyna_kv_pack(st, (k * 4096, (k + 1) * 4096), (0, 32), buf.data_ptr(), chunk_bytes, cs)
+             for k in range(8)]
+    ms = run_set(stream, calls, reps=5)
+    report("4' shape: K1 pack (paged -> packed chunk), 8 chunks", payload, ms, 32768, 8, "a2 gather")
+    calls = [lambda k=k: dk.dyna_kv_unpack(buf.data_ptr(), chunk_bytes, dt, (k * 4096, (k + 1) * 4096), (0, 32), cs)
+             for k in range(8)]
+    ms = run_set(stream, calls, reps=5)
+    report("4' shape: K3 unpack (packed chunk -> paged), 8 chunks", payload, ms, 32768, 8, "a4 scatter")
+    calls = [lambda k=k: dk.dyna_kv_migrate_ex(st, dt, (k * 4096, (k + 1) * 4096), (0, 32), 4096, cs,
+                                               dk.opts(variant=dk.DYNA_VARIANT_STAGED))
+             for k in range(8)]
+    ms = run_set(stream, calls, reps=5)
+    report("4' shape: STAGED variant (K1 -> K2 copy engine -> K3), 8 chunks", payload, ms, 32768, 8,
+           "3x the fused variant's HBM traffic on one GPU")
+    del src, dst, buf
 
     # configs[4] Qwen2-72B-shaped shard (80 layers): one ordered pair's 4 requests, chunk 1024
     g = kvgen.QWEN2_72B
