@@ -302,11 +302,16 @@ dyna_status ensure_peer(int dev, int peer) {
 // Flag rows: per (sender instance, destination inbox uid), the next epoch and the next free
 // slot.  Slots are handed out in consecutive ranges and recycle after DYNA_MAX_CHUNKS chunks;
 // flags are raised with an atomic max, so a late writer never moves a flag backwards.
-constexpr size_t kRecentReservations = 128;
+// DYNA_MIGRATE_OVERLAP_PREV: a launch that may still be running holds its slots' counters.  At most 128
+// kernels run at once on a device, so only reservations made during the library's last
+// kWindowLaunches launches can belong to a running kernel; if those reservations (with the ring's
+// wrap waste) fit in DYNA_MAX_CHUNKS slots, none of them reuses another's slots.
+constexpr uint64_t kWindowLaunches = 128;
 struct FlagRow {
   uint64_t epoch = 0;
   int64_t cursor = 0;
-  std::deque<std::pair<int64_t, int64_t>> recent;  // (first slot, slots) of the latest reservations
+  std::deque<std::pair<uint64_t, int64_t>> recent;  // (library launch count at reservation, slots consumed)
+  int64_t window_slots = 0;                          // sum of `recent`'s slots
 };
 static std::map<std::pair<int, uint64_t>, FlagRow> g_flag_rows;
 
@@ -332,28 +337,31 @@ dyna_status flag_reserve(int sender, const dyna_kv_pool* dst, int64_t nchunks, u
     it = g_flag_rows.emplace(key, fr).first;
   }
   FlagRow& fr = it->second;
-  if (fr.cursor + nchunks > DYNA_MAX_CHUNKS) fr.cursor = 0;
+  int64_t consumed = nchunks;
+  if (fr.cursor + nchunks > DYNA_MAX_CHUNKS) {
+    consumed += DYNA_MAX_CHUNKS - fr.cursor;  // the skipped tail of the ring counts as used this lap
+    fr.cursor = 0;
+  }
   *first_slot = (int32_t)fr.cursor;
-  fr.recent.emplace_back(fr.cursor, nchunks);
-  if (fr.recent.size() > kRecentReservations + 1) fr.recent.pop_front();
+  const uint64_t now = g_launches.load();
+  while (!fr.recent.empty() && fr.recent.front().first + kWindowLaunches < now) {
+    fr.window_slots -= fr.recent.front().second;
+    fr.recent.pop_front();
+  }
+  fr.recent.emplace_back(now, consumed);
+  fr.window_slots += consumed;
   fr.cursor += nchunks;
   *epoch = ++fr.epoch;
   return DYNA_OK;
 }
 
 bool flag_slots_shared_recently(int sender, const dyna_kv_pool* dst, int32_t first, int64_t n) {
+  (void)first;
+  (void)n;
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_flag_rows.find(std::make_pair(sender, dst->uid));
   if (it == g_flag_rows.end()) return true;
-  bool self_skipped = false;
-  for (const auto& rv : it->second.recent) {
-    if (!self_skipped && rv.first == first && rv.second == n) {  // the caller's own reservation
-      self_skipped = true;
-      continue;
-    }
-    if (rv.first < first + n && first < rv.first + rv.second) return true;
-  }
-  return false;
+  return it->second.window_slots > DYNA_MAX_CHUNKS;  // the recent reservations wrapped onto each other
 }
 
 // Zeroed device memory allocated during a call: zeroed on a non-blocking library stream, waited

@@ -114,9 +114,10 @@ dyna_status ensure_peer(int dev, int peer);
 uint64_t new_uid();
 dyna_status flag_reserve(int sender, const dyna_kv_pool* dst, int64_t nchunks, uint64_t* epoch, int32_t* first_slot);
 // DYNA_MIGRATE_OVERLAP_PREV with flags: whether the slots [first, first + n) (a reservation just
-// made) intersect one of the row's last kRecentReservations other reservations — a launch that may
-// still be running (at most 128 kernels run concurrently on a device) — so the overlapped launch
-// must wait for its predecessor before it touches those slots' counters.
+// made) may be shared with a launch that is still running — conservatively, whether the row's
+// reservations of the library's last 128 launches (at most 128 kernels run at once on a device;
+// one batch launch may hold many reservations) wrapped the ring onto each other — so the overlapped
+// launch must wait for its predecessor before it touches those slots' counters.
 bool flag_slots_shared_recently(int sender, const dyna_kv_pool* dst, int32_t first, int64_t n);
 struct Span {  // the rows [lo, hi) of block `id` of the pool with this uid, heads [h0, h1) of them
   uint64_t uid;
