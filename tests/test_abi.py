@@ -119,6 +119,16 @@ def test_host_validation_without_gpu():
     with pytest.raises(dk.DynaKVError) as e:
         dk.dyna_kv_wait(0)
     assert e.value.status == dk.DYNA_EINVAL
+    # option validation comes first: an unknown flag bit is refused as such, the overlap flag is a valid
+    # option (the call then fails on its NULL tables)
+    empty = dk.dyna_block_table()
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_migrate_ex(empty, empty, (0, 1), (0, 1), 1, 0, dk.opts(flags=16))
+    assert e.value.status == dk.DYNA_EINVAL and "dyna_kv_opts" in str(e.value)
+    with pytest.raises(dk.DynaKVError) as e:
+        dk.dyna_kv_migrate_ex(empty, empty, (0, 1), (0, 1), 1, 0,
+                              dk.opts(flags=dk.DYNA_MIGRATE_OVERLAP_PREV | dk.DYNA_MIGRATE_SIGNAL))
+    assert e.value.status == dk.DYNA_EINVAL and "dyna_kv_opts" not in str(e.value)
 
 
 def test_calibration_table_roundtrip_without_gpu():
