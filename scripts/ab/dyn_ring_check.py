@@ -1,3 +1,6 @@
+#!/usr/bin/env python
+"""Spot check of the ring's guided dynamic grabs (explicit DYNA_SCHED_DYNAMIC) against the oracle on a few
+shapes, plain and signalled.  Prints one line per case and BAD <count>."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch, kvgen, oracle, paper_2504_09285_b200 as dk
